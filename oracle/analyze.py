@@ -1,0 +1,185 @@
+"""O2 Analyze — partition, cluster tree and symbolic per-level schedule (oracle; test infrastructure only).
+
+Integer-only; the library's `hs_analyze` must reproduce every output bit-exactly.
+
+Paper passages:
+  * clustering = a partition of the graph G_A, computed "algebraically ... with
+    existing software packages" (§3 "Matrix Partitioning"); Zoltan
+    geometric partition with clusters of about 100.  Reading Q11: RCB.
+  * extruded partitioning: partition one layer, extrude so that every vertical
+    line lies in one cluster (§4.2).  Reading Q19: a column's
+    coordinate is the (x, y) of its lowest-index DOF.
+  * neighbours: "pi_p and pi_q are neighbors if the matrix block A(pi_p,pi_q) != 0"
+    (P:494), re-applied to A_c at every level (Alg. 1).  Reading
+    Q6: n(s) is the structural block pattern of the level's input, fixed for
+    the level; Q7: w(s) = current fill adjacency minus n(s).
+  * Alg. 1 loops "for i <- 0 to m-1" over the clusters; reading Q8:
+    greedy independent-set batches, interior clusters of 8 fixed subdomains
+    first, then boundary clusters, ascending id.  Q9: binary cluster tree fixed
+    here, parent = union of the children's coarse DOFs.  Q10: the top
+    ("if the size of A is small enough") is the first level with
+    <= top_clusters clusters.
+"""
+from __future__ import annotations
+
+import dataclasses
+import numpy as np
+
+
+@dataclasses.dataclass
+class Level:
+    nclus: int
+    H: list            # H_l adjacency, sorted lists (structural block pattern of A_l)
+    nlist: list        # n(s) = H_l-adj(s), ascending
+    wlist: list        # w(s) = F-adj(s) \ n(s) at the moment s is eliminated, ascending
+    batches: list      # list of lists of cluster ids (ascending inside a batch)
+    nphase1: int       # number of phase-I (interior) batches
+    interior: np.ndarray   # bool per cluster
+    Ffinal: list       # fill graph after the level, sorted lists
+
+
+@dataclasses.dataclass
+class Analysis:
+    n: int
+    D: int
+    L_top: int
+    nsub_log2: int
+    perm: np.ndarray       # perm[new] = old  (int64)
+    leaf_off: np.ndarray   # DOF offsets of the 2^D leaves in the permuted order (int64, 2^D + 1)
+    levels: list           # Level for l = 0 .. L_top-1
+    H_top: list            # block pattern of the top level (l = L_top)
+
+    def subdomain(self, level: int, c: int) -> int:
+        d = self.D - level
+        sd = min(self.nsub_log2, self.D)
+        return c >> (d - sd)
+
+
+def _units(n, coords, column_id):
+    """Units (O2.1): extruded columns (ascending column id) or single DOFs."""
+    if column_id is None:
+        dofs_of = None
+        ucoord = np.asarray(coords, dtype=np.float64).reshape(n, -1)
+        return ucoord, None
+    column_id = np.asarray(column_id, dtype=np.int64)
+    cids, first = np.unique(column_id, return_index=True)   # first = lowest DOF index per column
+    c = np.asarray(coords, dtype=np.float64).reshape(n, -1)
+    ucoord = c[first, : min(2, c.shape[1])]
+    unit_of_dof = np.searchsorted(cids, column_id)
+    return ucoord, unit_of_dof
+
+
+def rcb(ucoord: np.ndarray, D: int):
+    """O2.3: perfect binary RCB tree to depth D.  Returns the leaf of every unit.
+    At a node: split on the axis of largest extent (lowest axis on ties), sort
+    by (coordinate, unit id), left child = first ceil(|I|/2) units."""
+    U = ucoord.shape[0]
+    leaf = np.zeros(U, dtype=np.int64)
+    nodes = [np.arange(U, dtype=np.int64)]
+    for depth in range(D):
+        nxt = []
+        for I in nodes:
+            if I.size == 0:
+                nxt.append(I)
+                nxt.append(I)
+                continue
+            cc = ucoord[I]
+            ext = cc.max(axis=0) - cc.min(axis=0)
+            ax = int(np.argmax(ext))                       # first maximum = lowest axis
+            order = np.lexsort((I, cc[:, ax]))             # key: (coord_ax, unit id)
+            S = I[order]
+            h = (S.size + 1) // 2
+            nxt.append(S[:h])
+            nxt.append(S[h:])
+        nodes = nxt
+    for x, I in enumerate(nodes):
+        leaf[I] = x
+    return leaf
+
+
+def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_columns=0,
+            top_log2=3, nsub_log2=3) -> Analysis:
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    colind = np.asarray(colind, dtype=np.int64)
+    ucoord, unit_of_dof = _units(n, coords, column_id)
+    U = ucoord.shape[0]
+    leaf_units = leaf_columns if column_id is not None else leaf_size
+    if leaf_units <= 0:
+        raise ValueError("leaf size must be positive")
+    # O2.2 depth: smallest D with ceil(U / 2^D) <= leaf_units
+    D = 0
+    while -(-U // (1 << D)) > leaf_units:
+        D += 1
+    uleaf = rcb(ucoord, D)
+    dof_leaf = uleaf if unit_of_dof is None else uleaf[unit_of_dof]
+    # O2.4 permutation: leaves left to right, DOFs ascending inside a leaf
+    perm = np.lexsort((np.arange(n), dof_leaf)).astype(np.int64)
+    nleaf = 1 << D
+    counts = np.bincount(dof_leaf, minlength=nleaf)
+    leaf_off = np.zeros(nleaf + 1, dtype=np.int64)
+    np.cumsum(counts, out=leaf_off[1:])
+    L_top = max(0, D - top_log2)
+    sd = min(nsub_log2, D)
+    # O2.7 H_0: leaves p != q adjacent iff the CSR stores an entry between them
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rowptr))
+    lp = dof_leaf[rows]
+    lq = dof_leaf[colind]
+    off = lp != lq
+    pairs = np.unique(lp[off] * nleaf + lq[off])
+    H = [[] for _ in range(nleaf)]
+    for pq in pairs.tolist():
+        H[pq // nleaf].append(pq % nleaf)
+    H = [sorted(set(h)) for h in H]
+    levels = []
+    for l in range(L_top):
+        nclus = 1 << (D - l)
+        d = D - l
+        sub = [c >> (d - sd) for c in range(nclus)]
+        F = [set(h) for h in H]
+        nlist = [list(h) for h in H]
+        interior = np.array([all(sub[q] == sub[s] for q in H[s]) for s in range(nclus)], dtype=bool)
+        wlist = [None] * nclus
+        processed = np.zeros(nclus, dtype=bool)
+        batches = []
+        nphase1 = 0
+        for phase in (1, 2):
+            while True:
+                cand = [s for s in range(nclus) if not processed[s] and (phase == 2 or interior[s])]
+                if not cand:
+                    break
+                B = []
+                Bset = set()
+                for s in cand:                                   # greedy, ascending id
+                    if not (F[s] & Bset):
+                        B.append(s)
+                        Bset.add(s)
+                for s in B:                                      # record w(s) before the fill
+                    wlist[s] = sorted(F[s] - set(nlist[s]))
+                for s in B:                                      # fill: clique on n(s)
+                    ns = nlist[s]
+                    for p in ns:
+                        F[p].update(q for q in ns if q != p)
+                for s in B:
+                    processed[s] = True
+                batches.append(B)
+                if phase == 1:
+                    nphase1 += 1
+        Ffinal = [sorted(f) for f in F]
+        levels.append(Level(nclus, H, nlist, wlist, batches, nphase1, interior, Ffinal))
+        # O2.9 H_{l+1}: parents adjacent iff some children are F_final-adjacent
+        Hn = [set() for _ in range(nclus // 2)]
+        for c in range(nclus):
+            P = c >> 1
+            for q in F[c]:
+                Q = q >> 1
+                if Q != P:
+                    Hn[P].add(Q)
+        H = [sorted(h) for h in Hn]
+    return Analysis(n=n, D=D, L_top=L_top, nsub_log2=sd, perm=perm, leaf_off=leaf_off,
+                    levels=levels, H_top=H)
+
+
+def analyze_problem(p, top_log2=3, nsub_log2=3) -> Analysis:
+    return analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id,
+                   leaf_size=p.leaf_size, leaf_columns=p.leaf_columns,
+                   top_log2=top_log2, nsub_log2=nsub_log2)

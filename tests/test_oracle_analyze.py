@@ -1,0 +1,127 @@
+"""Pin P7: the oracle's analyze against closed forms and brute force.
+
+* RCB on grid coordinates gives exact boxes: C1 -> 64 boxes of 4x4, C2 -> 4096
+  cubes of 4^3, C3 -> 8192 leaves of 2x4 (or 4x2) whole columns, Q1 -> 1x2 columns
+  (extruded partitioning keeps every vertical line in one cluster).
+* every batch is an independent set of the fill graph at its time and is maximal
+  (brute-force re-simulation of Alg. 1's loop), interior clusters first.
+"""
+import numpy as np
+import pytest
+
+from problems import gen_poisson2d, gen_laplace3d, gen_slab, gen_stokes_q1
+from oracle.analyze import analyze_problem, analyze
+
+
+def _boxes(p, an, dims):
+    """For each leaf, return the set of per-axis extents of its unit coordinates."""
+    out = set()
+    inv = np.empty(p.n, dtype=np.int64)
+    inv[an.perm] = np.arange(p.n)
+    for c in range(an.leaf_off.shape[0] - 1):
+        d = an.perm[an.leaf_off[c]:an.leaf_off[c + 1]]
+        cc = p.coords[d][:, :dims]
+        lo, hi = cc.min(0), cc.max(0)
+        out.add(tuple((hi - lo).tolist()))
+    return out
+
+
+def test_C1_boxes():
+    p = gen_poisson2d(32)
+    an = analyze_problem(p)
+    assert an.D == 6 and an.L_top == 3 and len(an.levels) == 3
+    assert np.all(np.diff(an.leaf_off) == 16)
+    assert _boxes(p, an, 2) == {(3.0, 3.0)}
+    # leaves are aligned 4x4 boxes
+    for c in range(64):
+        d = an.perm[an.leaf_off[c]:an.leaf_off[c + 1]]
+        cc = p.coords[d]
+        assert np.all(cc.min(0) % 4 == 0)
+    assert sorted(an.perm.tolist()) == list(range(p.n))
+
+
+def test_C2_cubes():
+    p = gen_laplace3d(64)
+    an = analyze_problem(p)
+    assert an.D == 12 and an.L_top == 9
+    assert np.all(np.diff(an.leaf_off) == 64)
+    assert _boxes(p, an, 3) == {(3.0, 3.0, 3.0)}
+
+
+def test_C3_columns():
+    p = gen_slab(256, 10)
+    an = analyze_problem(p)
+    assert an.D == 13
+    assert np.all(np.diff(an.leaf_off) == 80)
+    # column integrity: every column lies in exactly one leaf
+    leaf_of = np.empty(p.n, dtype=np.int64)
+    for c in range(1 << an.D):
+        leaf_of[an.perm[an.leaf_off[c]:an.leaf_off[c + 1]]] = c
+    for col in range(0, 256 * 256, 97):
+        assert np.unique(leaf_of[p.column_id == col]).size == 1
+    assert _boxes(p, an, 2) <= {(1000.0, 3000.0), (3000.0, 1000.0)}
+
+
+def test_Q1_columns():
+    p = gen_stokes_q1(16, 16, 4, leaf_columns=2)
+    an = analyze_problem(p)
+    assert an.D == 7
+    assert np.all(np.diff(an.leaf_off) == 2 * 4 * 2)
+    assert _boxes(p, an, 2) <= {(1.0, 0.0), (0.0, 1.0)}
+
+
+def _resimulate(an):
+    """Brute force: walk the batches with a fresh fill graph and check
+    independence, maximality, phase order and the recorded w(s)."""
+    for l, lev in enumerate(an.levels):
+        nclus = lev.nclus
+        F = [set(h) for h in lev.H]
+        done = np.zeros(nclus, dtype=bool)
+        for bi, B in enumerate(lev.batches):
+            phase1 = bi < lev.nphase1
+            Bs = set(B)
+            for s in B:
+                assert not done[s]
+                assert not (F[s] & Bs), "batch not independent"
+                if phase1:
+                    assert lev.interior[s]
+                assert lev.wlist[s] == sorted(F[s] - set(lev.H[s]))
+                assert lev.nlist[s] == lev.H[s]
+            # maximality: every skipped eligible cluster is adjacent to a member
+            for t in range(nclus):
+                if done[t] or t in Bs or (phase1 and not lev.interior[t]):
+                    continue
+                # greedy scan: t was skipped only because an earlier member is adjacent
+                assert {b for b in F[t] & Bs if b < t}, "batch not maximal"
+            for s in B:
+                for p_ in lev.H[s]:
+                    for q in lev.H[s]:
+                        if p_ != q:
+                            F[p_].add(q)
+                done[s] = True
+        assert done.all()
+        assert [sorted(f) for f in F] == lev.Ffinal
+        # subdomain locality of phase-I fill
+        for s in range(nclus):
+            if lev.interior[s]:
+                assert all(an.subdomain(l, q) == an.subdomain(l, s) for q in lev.H[s])
+
+
+@pytest.mark.parametrize("gen", [lambda: gen_poisson2d(32), lambda: gen_laplace3d(16, leaf_size=16),
+                                 lambda: gen_slab(32, 4, leaf_columns=4),
+                                 lambda: gen_stokes_q1(12, 12, 3, leaf_columns=2)])
+def test_batches_independent_maximal(gen):
+    p = gen()
+    an = analyze_problem(p)
+    assert len(an.levels) >= 1
+    _resimulate(an)
+
+
+def test_depth_rule_and_empty_children():
+    # U = 10 units, leaf 3 -> D = 2 (ceil(10/4) = 3); children may be empty for tiny U
+    p = gen_poisson2d(5, 2, leaf_size=3)
+    an = analyze(p.n, p.rowptr, p.colind, p.coords, None, leaf_size=3)
+    assert an.D == 2 and an.L_top == 0
+    assert an.leaf_off[-1] == 10 and np.all(np.diff(an.leaf_off) <= 3)
+    an1 = analyze(p.n, p.rowptr, p.colind, p.coords, None, leaf_size=1)
+    assert an1.D == 4 and (np.diff(an1.leaf_off) == 0).sum() == 6
