@@ -1,0 +1,192 @@
+/*
+ * hsolve.h — C ABI of the B200-native deferred-compression LoRaSp hot path.
+ *
+ * Chen, Cambier, Boman, Rajamanickam, Tuminaro, Darve, "A Robust Hierarchical
+ * Solver for Ill-conditioned Systems with Applications to Ice Sheet Modeling"
+ * (arXiv 1811.11248).  "P:n" below is line n of /root/reference/PAPER.md.
+ *
+ * The library solves an (ill-conditioned) SPD system A x = b (P:478-481,
+ * Eq. ax=b).  Four calls follow the paper's statement of the problem:
+ *   hs_analyze  clustering of the graph of A, computed algebraically
+ *               (extruded columns P:786-798), the cluster tree and
+ *               the per-level elimination schedule (Alg. 1 loop);
+ *   hs_factor   Algorithm 1 with the scaled low-rank elimination of
+ *               §3.1: POTRF of A_ss, deferred-compression TRSM
+ *               G_s^{-1}A_sw, column-pivoted QR to eps,
+ *               sparsification, fine-DOF Schur update (Eq. CC:eqn:elim), top
+ *               dense Cholesky;  eps is "the (only) other
+ *               parameter";
+ *   hs_apply    Algorithm 2: x = M^{-1} b by forward/backward
+ *               substitution with the factor;
+ *   hs_pcg      preconditioned CG with the factor as M (north_star; the paper
+ *               uses right-preconditioned GMRES).
+ *
+ * Conventions (all calls):
+ *   - Every call returns hs_status; no C++ exception crosses the ABI.  The
+ *     detail of the last error (level, cluster, pivot index/value, CUDA string)
+ *     is available from hs_last_error(h).
+ *   - Ownership: the caller owns every input array; the library copies what it
+ *     needs before returning and keeps no caller pointer.  Output arrays are
+ *     caller-allocated.  Handles are created and destroyed only by the library.
+ *   - Vectors b, x are in the ORIGINAL ordering; the library applies its
+ *     permutation internally.  on_device = 0: host pointers; 1: device pointers
+ *     on the handle's device (e.g. torch CUDA tensors).
+ *   - Matrices are CSR with BOTH triangles stored: int64 rowptr[n+1], int32
+ *     colind[nnz] (sorted per row), double values[nnz].
+ *   - A handle is used by one host thread at a time.  A factor is immutable
+ *     after hs_factor; hs_apply / hs_pcg only read it.
+ *   - There is no CPU fallback: factor/apply/pcg fail with HS_E_NO_DEVICE when
+ *     no CUDA device is present.  hs_analyze is host integer code and may be
+ *     called with h == NULL.
+ */
+#ifndef HSOLVE_H
+#define HSOLVE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HS_OK = 0,
+  HS_E_INVALID_ARG = 1,        /* NULL pointer, bad option value                       */
+  HS_E_DIM = 2,                /* size mismatch (pattern vs analysis, vector length)  */
+  HS_E_NOT_SYMMETRIC = 3,      /* pattern (analyze) or values (factor) not symmetric   */
+  HS_E_NOT_SPD = 4,            /* a Cholesky pivot <= 0; factor not created    */
+  HS_E_COLUMN_SPLIT = 5,       /* a single extruded column exceeds the leaf size       */
+  HS_E_PRECOND_NOT_POSITIVE = 6,/* PCG: <r, M^{-1} r> <= 0                             */
+  HS_E_NOT_CONVERGED = 7,      /* PCG hit maxit; x and the report are still filled     */
+  HS_E_OOM = 8,                /* device allocation failed                             */
+  HS_E_CUDA = 9,               /* CUDA runtime error                                   */
+  HS_E_NCCL = 10,              /* NCCL error                                           */
+  HS_E_NO_DEVICE = 11,         /* no CUDA device: there is no CPU fallback             */
+  HS_E_UNSUPPORTED = 12,       /* a size outside what the kernels support              */
+  HS_E_INTERNAL = 13
+} hs_status;
+
+typedef struct hs_handle_s*   hs_handle;    /* device, stream, (NCCL comm)             */
+typedef struct hs_analysis_s* hs_analysis;  /* host, integer: perm, tree, schedule     */
+typedef struct hs_factor_s*   hs_factor;    /* device-resident factor                  */
+
+typedef struct {
+  int32_t leaf_size;     /* DOFs per leaf when column_id == NULL (C1: 16, C2: 64)             */
+  int32_t leaf_columns;  /* columns per leaf when column_id != NULL (C3: 8, C4: 2, C5: 4)      */
+  int32_t top_log2;      /* base case at the first level with <= 2^top_log2 clusters (3 -> 8) */
+  int32_t nsub_log2;     /* fixed subdomain depth (3 -> 8 subdomains); must be <= top_log2    */
+} hs_analyze_opts;
+
+typedef struct {
+  double  eps;           /* truncation tolerance, >= 0                 */
+  int32_t eps_relative;  /* 1: tau_s = eps * max column norm of G^{-1}A_sw (reading Q1); 0: absolute */
+  int32_t dc;            /* 1: deferred compression (the paper's method); 0 is not supported yet */
+} hs_factor_opts;
+
+typedef struct {
+  int64_t n;             /* number of DOFs                                   */
+  int32_t depth;         /* D: the tree has 2^D leaves                       */
+  int32_t L_top;         /* number of hierarchical levels (top = level L_top) */
+  int32_t nsub_log2;     /* effective subdomain depth                        */
+  int32_t top_log2;
+} hs_analysis_info;
+
+/* keys for hs_analysis_export (all integer arrays, exported as int64) */
+enum {
+  HS_EXP_PERM = 0,       /* [n]      perm[new] = old                                    */
+  HS_EXP_LEAF_OFF = 1,   /* [2^D+1]  DOF offsets of the leaves in the permuted order     */
+  HS_EXP_H_PTR = 2,      /* level l: CSR of H_l (structural block pattern; n(s) = H_l-adj(s)) */
+  HS_EXP_H_IDX = 3,
+  HS_EXP_W_PTR = 4,      /* level l: w(s) at elimination time (ascending)               */
+  HS_EXP_W_IDX = 5,
+  HS_EXP_BATCH_PTR = 6,  /* level l: batches (independent sets), in elimination order   */
+  HS_EXP_BATCH_IDX = 7,
+  HS_EXP_INTERIOR = 8,   /* level l: 1 if all neighbours share the cluster's subdomain  */
+  HS_EXP_F_PTR = 9,      /* level l: fill graph after the level                          */
+  HS_EXP_F_IDX = 10,
+  HS_EXP_NPHASE1 = 11,   /* level l: [1] number of phase-I (interior) batches            */
+  HS_EXP_HTOP_PTR = 12,  /* block pattern of the top level                               */
+  HS_EXP_HTOP_IDX = 13
+};
+
+/* keys for hs_factor_export */
+enum {
+  HS_FEXP_RANKS = 0,     /* level l: int64[nclus] kept rank r_s                          */
+  HS_FEXP_LIVE0 = 1,     /* level l: int64[nclus] live size at the start of the level    */
+  HS_FEXP_PIV_PTR = 2,   /* level l: int64[nclus+1] offsets into PIV                      */
+  HS_FEXP_PIV = 3,       /* level l: canonical pivot columns of every cluster, pivot order */
+  HS_FEXP_TOP = 4        /* [ntop] live sizes at the top level                            */
+};
+
+typedef struct {
+  double  t_factor_s;    /* device time of hs_factor (CUDA events)                      */
+  double  flops;         /* algorithmic factor flops     */
+  double  factor_bytes;  /* bytes of the stored factor (G, V, tau, C, top L)            */
+  int64_t n_top;         /* DOFs at the top level                                       */
+  int32_t n_levels;
+  int32_t n_batches;
+  int32_t max_m;         /* largest cluster size eliminated                             */
+  int32_t max_rank;
+  double  t_phase_s[8];  /* per-kernel-class device time: 0 gather 1 potrf 2 trsm 3 cpqr
+                            4 schur 5 writeback/assemble 6 top 7 host planning (wall)   */
+  double  flops_phase[8];
+} hs_factor_stats_t;
+
+typedef struct {
+  int32_t iters;         /* number of SpMVs                                             */
+  int32_t converged;
+  double  relres;        /* recurrence ||r_k|| / ||b||                                   */
+  double  relres_true;   /* ||b - A x|| / ||b|| computed on the device at the end        */
+  double  t_pcg_s;       /* device time                                                  */
+  double  t_apply_s;     /* device time spent in the preconditioner                      */
+  double  t_spmv_s;
+} hs_pcg_report;
+
+/* ---- handle --------------------------------------------------------------------- */
+/* device: CUDA ordinal.  world_size/rank/nccl_unique_id: multi-GPU (world_size 1 and
+ * NULL id for one GPU).  Fails with HS_E_NO_DEVICE when CUDA is unavailable. */
+hs_status hs_create(hs_handle* h, int device, int world_size, int rank, const void* nccl_unique_id);
+/* stream: a cudaStream_t on the handle's device (e.g. torch.cuda.current_stream()),
+ * or NULL for the library's own stream.  All device work of the handle runs on it. */
+hs_status hs_set_stream(hs_handle h, void* stream);
+void      hs_destroy(hs_handle h);
+const char* hs_last_error(hs_handle h);     /* never NULL; h may be NULL (global last error) */
+const char* hs_status_string(hs_status s);
+
+/* ---- analyze (host, integer; bit-exact with the oracle) --------------------------- */
+/* coords: n*coord_dim row-major, or NULL (then the graph partitioner is required,
+ * which is not implemented yet -> HS_E_UNSUPPORTED).  column_id: n entries or NULL. */
+hs_status hs_analyze(hs_handle h, int64_t n, const int64_t* rowptr, const int32_t* colind,
+                     const double* coords, int32_t coord_dim, const int32_t* column_id,
+                     const hs_analyze_opts* opt, hs_analysis* out);
+hs_status hs_analysis_get_info(hs_analysis a, hs_analysis_info* info);
+/* Writes min(cap, len) entries of the array `key` of level `level` into out and the full
+ * length into *len (call with out == NULL to query the length). */
+hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t* out,
+                             int64_t cap, int64_t* len);
+void      hs_analysis_destroy(hs_analysis a);
+
+/* ---- factor (device) -------------------------------------------------------------- */
+/* values: CSR values (host) on the pattern given to hs_analyze.  On HS_E_NOT_SPD no
+ * factor is created and hs_last_error names (level, cluster, pivot, value). */
+hs_status hs_factor_create(hs_handle h, hs_analysis a, const double* values,
+                           const hs_factor_opts* opt, hs_factor* out);
+hs_status hs_factor_get_stats(hs_factor f, hs_factor_stats_t* st);
+hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out,
+                           int64_t cap, int64_t* len);
+void      hs_factor_destroy(hs_factor f);
+
+/* ---- solve (device) --------------------------------------------------------------- */
+/* x = M^{-1} b (Algorithm 2).  b and x may alias. */
+hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device);
+/* PCG on A (the CSR given to hs_factor) with M = the factor; x0 = 0; stops when
+ * ||r_k|| / ||b|| <= tol (iteration count = SpMVs).  HS_E_NOT_CONVERGED still fills
+ * x and rep. */
+hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t maxit,
+                 int32_t on_device, hs_pcg_report* rep);
+/* y = A x with the factor's CSR (device SpMV); helper for tests and the bench. */
+hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSOLVE_H */

@@ -18,6 +18,15 @@ import numpy as np
 import scipy.linalg as sla
 
 PIVOT_WINDOW = 1e-10      # Q4 tie window
+# Decision-fragility flags (reading R-margin).  Two correct implementations
+# differ in a computed trailing norm nu_i(j) by about c*u*nu_max(0) (absolute: Householder
+# rounding accumulates on the scale of the initial block, c*u ~ 1e-14), so a decision is
+# robust only if its distance to the decision boundary, measured in units of nu_max(0),
+# exceeds that.  Flag a cluster when
+#   threshold:  |nu_max(j) - tau_s| < max(1e-10 * tau_s, FLAG_ABS * nu_max(0))
+#               (the first term is north_star's "within 1e-10 relative of the threshold")
+#   pivot:      |nu_i(j) - (1 - 1e-10) nu_max(j)| < FLAG_ABS * nu_max(0) for some i != argmax
+FLAG_ABS = 1e-13
 
 
 class NotSPD(Exception):
@@ -79,8 +88,9 @@ class CPQRResult:
     W: np.ndarray             # m x k transformed block Q^T B_w (pivot columns zeroed below the diagonal)
     tau_s: float              # threshold eps * nu_max(0)
     nu_max: list              # nu_max(j) for every decision j
-    mu: float                 # threshold margin
-    pi: float                 # pivot margin
+    mu: float                 # threshold margin: min_j |nu_max(j) - tau_s| / nu_max(0)
+    pi: float                 # pivot margin: min_j min_{i != argmax} |nu_i - (1-1e-10) nu_max(j)| / nu_max(0)
+    flagged: bool = False     # a decision lies within rounding distance of its boundary
 
 
 def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRResult:
@@ -103,15 +113,21 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRR
     pi = np.inf
     r = min(m, k)
     stopped = False
+    flagged = False
+    nu0 = 0.0
     for j in range(min(m, k)):
         cols = np.nonzero(active)[0]
         nu = np.sqrt(np.sum(W[j:, cols] ** 2, axis=0))      # exact, no downdating
         numax = float(nu.max())
         if j == 0:
             tau_s = eps * numax if relative else eps
+            nu0 = numax
         numaxes.append(numax)
-        if tau_s > 0:
-            mu = min(mu, abs(numax / tau_s - 1.0))
+        if nu0 > 0 and not (tau_s == 0.0 and numax == 0.0):   # exact zeros are not fragile
+            dist = abs(numax - tau_s)
+            mu = min(mu, dist / nu0)
+            if dist < max(1e-10 * tau_s, FLAG_ABS * nu0):
+                flagged = True
         if inject is not None:
             keep = j < inject[0]
         else:
@@ -126,11 +142,13 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRR
             cand = cols[nu >= (1.0 - PIVOT_WINDOW) * numax]   # Q4 window
             p = int(cand.min())                               # lowest canonical index
         if numax > 0:
-            ratio = nu / numax
             imax = int(np.argmax(nu))
-            others = np.delete(ratio, imax)
+            others = np.delete(nu, imax)
             if others.size:
-                pi = min(pi, float(np.min(np.abs(others - (1.0 - PIVOT_WINDOW)))))
+                d = float(np.min(np.abs(others - (1.0 - PIVOT_WINDOW) * numax))) / nu0
+                pi = min(pi, d)
+                if d < FLAG_ABS:
+                    flagged = True
         v, tau, beta = larfg(W[j:, p])
         act = cols[cols != p]
         if tau != 0.0:
@@ -149,7 +167,7 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRR
     if not stopped and inject is not None:
         r = min(r, inject[0])
     return CPQRResult(r=r, V=V, tau=np.array(taus), piv=np.array(pivs, dtype=np.int64), W=W,
-                      tau_s=float(tau_s), nu_max=numaxes, mu=float(mu), pi=float(pi))
+                      tau_s=float(tau_s), nu_max=numaxes, mu=float(mu), pi=float(pi), flagged=flagged)
 
 
 def apply_Qt(V: np.ndarray, tau: np.ndarray, X: np.ndarray) -> np.ndarray:

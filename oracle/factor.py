@@ -53,6 +53,7 @@ class Elim:
     coarse_n: np.ndarray = None   # r x k_n (debug / parity)
     coarse_w: np.ndarray = None   # r x k_w
     tail_w: np.ndarray = None     # (m - r) x k_w dropped V2^T (debug, P3)
+    flagged: bool = False         # a CPQR decision within rounding distance of its boundary
 
 
 @dataclasses.dataclass
@@ -137,10 +138,11 @@ def eliminate(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, injec
         r, V, tau, piv, W = 0, np.zeros((m, 0)), np.zeros(0), np.zeros(0, dtype=np.int64), Bw
         mu = pi = np.inf
         tau_s = 0.0
+        flagged = False
     else:
         res = cpqr(Bw, eps, relative, inject)              # step 4
         r, V, tau, piv, W = res.r, res.V[:, :res.r], res.tau[:res.r], res.piv[:res.r], res.W
-        mu, pi, tau_s = res.mu, res.pi, res.tau_s
+        mu, pi, tau_s, flagged = res.mu, res.pi, res.tau_s, res.flagged
     Bt = apply_Qt(V, tau, Bn)                              # step 5: U^T G^{-1} A_sn
     coarse_n, C = Bt[:r], Bt[r:]
     coarse_w = W[:r]
@@ -156,7 +158,7 @@ def eliminate(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, injec
         st.set(s, q, coarse_n[:, no[a]:no[a + 1]])
     for a, q in enumerate(wlist):
         st.set(s, q, coarse_w[:, wo[a]:wo[a + 1]])
-    e = Elim(l, s, m, r, G, V, tau, piv, C, list(nlist), nsz, list(wlist), wsz, mu, pi, tau_s)
+    e = Elim(l, s, m, r, G, V, tau, piv, C, list(nlist), nsz, list(wlist), wsz, mu, pi, tau_s, flagged=flagged)
     if keep_debug:
         e.coarse_n, e.coarse_w, e.tail_w = coarse_n, coarse_w, W[r:]
     return e

@@ -1,0 +1,322 @@
+// extern "C" entry points of libhsolve (include/hsolve.h).  Every call translates
+// internal exceptions into hs_status; nothing throws across the ABI.
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "runtime.h"
+
+namespace {
+std::mutex g_mu;
+std::string g_err;   // last error when no handle is available
+
+void set_err(hs_handle h, const std::string& m) {
+  if (h) h->err = m;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_err = m;
+}
+
+template <class F>
+hs_status guarded(hs_handle h, F&& fn) {
+  try {
+    fn();
+    return HS_OK;
+  } catch (const hs::Error& e) {
+    set_err(h, e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_err(h, "host out of memory");
+    return HS_E_OOM;
+  } catch (const std::exception& e) {
+    set_err(h, e.what());
+    return HS_E_INTERNAL;
+  } catch (...) {
+    set_err(h, "unknown error");
+    return HS_E_INTERNAL;
+  }
+}
+
+void require_device(hs_handle h) {
+  if (!h) hs::fail(HS_E_INVALID_ARG, "NULL handle");
+  HS_CUDA(cudaSetDevice(h->device));
+}
+
+template <class T>
+void export_vec(const std::vector<T>& v, int64_t* out, int64_t cap, int64_t* len) {
+  if (len) *len = (int64_t)v.size();
+  if (out)
+    for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); ++i) out[i] = (int64_t)v[i];
+}
+void export_adj(const hs::Adj& a, bool ptr, int64_t* out, int64_t cap, int64_t* len) {
+  std::vector<int64_t> v;
+  if (ptr) {
+    v.push_back(0);
+    for (const auto& r : a) v.push_back(v.back() + (int64_t)r.size());
+  } else {
+    for (const auto& r : a) v.insert(v.end(), r.begin(), r.end());
+  }
+  export_vec(v, out, cap, len);
+}
+}  // namespace
+
+extern "C" {
+
+const char* hs_status_string(hs_status s) {
+  switch (s) {
+    case HS_OK: return "HS_OK";
+    case HS_E_INVALID_ARG: return "HS_E_INVALID_ARG";
+    case HS_E_DIM: return "HS_E_DIM";
+    case HS_E_NOT_SYMMETRIC: return "HS_E_NOT_SYMMETRIC";
+    case HS_E_NOT_SPD: return "HS_E_NOT_SPD";
+    case HS_E_COLUMN_SPLIT: return "HS_E_COLUMN_SPLIT";
+    case HS_E_PRECOND_NOT_POSITIVE: return "HS_E_PRECOND_NOT_POSITIVE";
+    case HS_E_NOT_CONVERGED: return "HS_E_NOT_CONVERGED";
+    case HS_E_OOM: return "HS_E_OOM";
+    case HS_E_CUDA: return "HS_E_CUDA";
+    case HS_E_NCCL: return "HS_E_NCCL";
+    case HS_E_NO_DEVICE: return "HS_E_NO_DEVICE";
+    case HS_E_UNSUPPORTED: return "HS_E_UNSUPPORTED";
+    case HS_E_INTERNAL: return "HS_E_INTERNAL";
+  }
+  return "HS_E_?";
+}
+
+const char* hs_last_error(hs_handle h) {
+  if (h) return h->err.c_str();
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_err.c_str();
+}
+
+hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const void* nccl_unique_id) {
+  return guarded(nullptr, [&] {
+    if (!out) hs::fail(HS_E_INVALID_ARG, "hs_create: NULL out");
+    *out = nullptr;
+    if (world_size != 1 || rank != 0 || nccl_unique_id)
+      hs::fail(HS_E_UNSUPPORTED, "hs_create: multi-GPU factor is not implemented yet (replicas only)");
+    int nd = 0;
+    if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
+      cudaGetLastError();
+      hs::fail(HS_E_NO_DEVICE, "hs_create: no CUDA device (there is no CPU fallback)");
+    }
+    if (device < 0 || device >= nd) hs::fail(HS_E_INVALID_ARG, "hs_create: bad device ordinal");
+    auto* h = new hs_handle_s();
+    h->device = device;
+    HS_CUDA(cudaSetDevice(device));
+    HS_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+    *out = h;
+  });
+}
+
+hs_status hs_set_stream(hs_handle h, void* stream) {
+  return guarded(h, [&] {
+    require_device(h);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    if (stream) {
+      h->stream = (cudaStream_t)stream;
+      h->own_stream = false;
+    } else {
+      HS_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+  });
+}
+
+void hs_destroy(hs_handle h) {
+  if (!h) return;
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+hs_status hs_analyze(hs_handle h, int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
+                     int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts* opt, hs_analysis* out) {
+  return guarded(h, [&] {
+    if (!out || !opt) hs::fail(HS_E_INVALID_ARG, "hs_analyze: NULL argument");
+    *out = nullptr;
+    auto* a = new hs_analysis_s();
+    try {
+      a->an = hs::analyze(n, rowptr, colind, coords, coord_dim, column_id, *opt);
+    } catch (...) {
+      delete a;
+      throw;
+    }
+    *out = a;
+  });
+}
+
+hs_status hs_analysis_get_info(hs_analysis a, hs_analysis_info* info) {
+  return guarded(nullptr, [&] {
+    if (!a || !a->an || !info) hs::fail(HS_E_INVALID_ARG, "hs_analysis_get_info: NULL argument");
+    info->n = a->an->n;
+    info->depth = a->an->D;
+    info->L_top = a->an->L_top;
+    info->nsub_log2 = a->an->nsub_log2;
+    info->top_log2 = a->an->top_log2;
+  });
+}
+
+hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t* out, int64_t cap, int64_t* len) {
+  return guarded(nullptr, [&] {
+    if (!a || !a->an) hs::fail(HS_E_INVALID_ARG, "hs_analysis_export: NULL analysis");
+    const hs::Analysis& an = *a->an;
+    auto lev = [&]() -> const hs::Level& {
+      if (level < 0 || level >= an.L_top) hs::fail(HS_E_INVALID_ARG, "hs_analysis_export: bad level");
+      return an.levels[level];
+    };
+    switch (key) {
+      case HS_EXP_PERM: export_vec(an.perm, out, cap, len); break;
+      case HS_EXP_LEAF_OFF: export_vec(an.leaf_off, out, cap, len); break;
+      case HS_EXP_H_PTR: export_adj(lev().H, true, out, cap, len); break;
+      case HS_EXP_H_IDX: export_adj(lev().H, false, out, cap, len); break;
+      case HS_EXP_W_PTR: export_adj(lev().w, true, out, cap, len); break;
+      case HS_EXP_W_IDX: export_adj(lev().w, false, out, cap, len); break;
+      case HS_EXP_BATCH_PTR: export_adj(lev().batches, true, out, cap, len); break;
+      case HS_EXP_BATCH_IDX: export_adj(lev().batches, false, out, cap, len); break;
+      case HS_EXP_INTERIOR: export_vec(lev().interior, out, cap, len); break;
+      case HS_EXP_F_PTR: export_adj(lev().Ffinal, true, out, cap, len); break;
+      case HS_EXP_F_IDX: export_adj(lev().Ffinal, false, out, cap, len); break;
+      case HS_EXP_NPHASE1: export_vec(std::vector<int64_t>{lev().nphase1}, out, cap, len); break;
+      case HS_EXP_HTOP_PTR: export_adj(an.H_top, true, out, cap, len); break;
+      case HS_EXP_HTOP_IDX: export_adj(an.H_top, false, out, cap, len); break;
+      default: hs::fail(HS_E_INVALID_ARG, "hs_analysis_export: bad key");
+    }
+  });
+}
+
+void hs_analysis_destroy(hs_analysis a) {
+  if (!a) return;
+  delete a->an;
+  delete a;
+}
+
+hs_status hs_factor_create(hs_handle h, hs_analysis a, const double* values, const hs_factor_opts* opt,
+                           hs_factor* out) {
+  return guarded(h, [&] {
+    if (!out) hs::fail(HS_E_INVALID_ARG, "hs_factor_create: NULL out");
+    *out = nullptr;
+    if (!a || !a->an || !values || !opt) hs::fail(HS_E_INVALID_ARG, "hs_factor_create: NULL argument");
+    require_device(h);
+    *out = hs::factor_create(h, a->an, values, *opt);
+  });
+}
+
+hs_status hs_factor_get_stats(hs_factor f, hs_factor_stats_t* st) {
+  return guarded(f ? f->h : nullptr, [&] {
+    if (!f || !st) hs::fail(HS_E_INVALID_ARG, "hs_factor_get_stats: NULL argument");
+    *st = f->stats;
+  });
+}
+
+hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out, int64_t cap, int64_t* len) {
+  return guarded(f ? f->h : nullptr, [&] {
+    if (!f) hs::fail(HS_E_INVALID_ARG, "hs_factor_export: NULL factor");
+    if (key == HS_FEXP_TOP) {
+      export_vec(f->top_sizes, out, cap, len);
+      return;
+    }
+    if (level < 0 || level >= (int)f->lv.size()) hs::fail(HS_E_INVALID_ARG, "hs_factor_export: bad level");
+    const hs::LevelRT& L = f->lv[level];
+    switch (key) {
+      case HS_FEXP_RANKS: export_vec(L.rank, out, cap, len); break;
+      case HS_FEXP_LIVE0: export_vec(L.cap, out, cap, len); break;
+      case HS_FEXP_PIV_PTR: {
+        std::vector<int64_t> p(L.nclus + 1, 0);
+        for (int s = 0; s < L.nclus; ++s) p[s + 1] = p[s] + L.rank[s];
+        export_vec(p, out, cap, len);
+        break;
+      }
+      case HS_FEXP_PIV: {
+        require_device(f->h);
+        std::vector<int64_t> v;
+        for (int s = 0; s < L.nclus; ++s) {
+          std::vector<int32_t> tmp(L.rank[s]);
+          if (L.rank[s])
+            HS_CUDA(cudaMemcpy(tmp.data(), L.piv[s], sizeof(int32_t) * L.rank[s], cudaMemcpyDeviceToHost));
+          v.insert(v.end(), tmp.begin(), tmp.end());
+        }
+        export_vec(v, out, cap, len);
+        break;
+      }
+      default: hs::fail(HS_E_INVALID_ARG, "hs_factor_export: bad key");
+    }
+  });
+}
+
+void hs_factor_destroy(hs_factor f) {
+  if (!f) return;
+  cudaSetDevice(f->h->device);
+  delete f;
+}
+
+static void io_in(hs_factor f, const double* v, double* dtmp, int32_t on_device, cudaStream_t st) {
+  HS_CUDA(cudaMemcpyAsync(dtmp, v, sizeof(double) * f->an->n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+}
+
+hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device) {
+  return guarded(f ? f->h : nullptr, [&] {
+    if (!f || !b || !x) hs::fail(HS_E_INVALID_ARG, "hs_apply: NULL argument");
+    require_device(f->h);
+    cudaStream_t st = f->h->stream;
+    const int64_t n = f->an->n;
+    double* din = nullptr;
+    HS_CUDA(cudaMallocAsync(&din, sizeof(double) * n, st));
+    io_in(f, b, din, on_device, st);
+    hs::apply(f, din, din);
+    HS_CUDA(cudaMemcpyAsync(x, din, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaFreeAsync(din, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device) {
+  return guarded(f ? f->h : nullptr, [&] {
+    if (!f || !x || !y) hs::fail(HS_E_INVALID_ARG, "hs_spmv: NULL argument");
+    require_device(f->h);
+    cudaStream_t st = f->h->stream;
+    const int64_t n = f->an->n;
+    double *dx = nullptr, *dy = nullptr;
+    HS_CUDA(cudaMallocAsync(&dx, sizeof(double) * n, st));
+    HS_CUDA(cudaMallocAsync(&dy, sizeof(double) * n, st));
+    io_in(f, x, dx, on_device, st);
+    hs::spmv(f, dx, dy);
+    HS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaFreeAsync(dx, st));
+    HS_CUDA(cudaFreeAsync(dy, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t maxit, int32_t on_device,
+                 hs_pcg_report* rep) {
+  hs_status s_inner = HS_OK;
+  const hs_status s = guarded(f ? f->h : nullptr, [&] {
+    if (!f || !b || !x || !rep) hs::fail(HS_E_INVALID_ARG, "hs_pcg: NULL argument");
+    if (!(tol >= 0) || maxit < 0) hs::fail(HS_E_INVALID_ARG, "hs_pcg: bad tol/maxit");
+    require_device(f->h);
+    cudaStream_t st = f->h->stream;
+    const int64_t n = f->an->n;
+    double *db = nullptr, *dx = nullptr;
+    HS_CUDA(cudaMallocAsync(&db, sizeof(double) * n, st));
+    HS_CUDA(cudaMallocAsync(&dx, sizeof(double) * n, st));
+    io_in(f, b, db, on_device, st);
+    try {
+      hs::pcg(f, db, dx, tol, maxit, rep);
+    } catch (const hs::Error& e) {
+      s_inner = e.status;
+      if (e.status != HS_E_NOT_CONVERGED) {
+        cudaFreeAsync(db, st);
+        cudaFreeAsync(dx, st);
+        throw;
+      }
+      f->h->err = e.what();
+    }
+    HS_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaFreeAsync(db, st));
+    HS_CUDA(cudaFreeAsync(dx, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+  });
+  return s != HS_OK ? s : s_inner;
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// Device-side structures shared by the host drivers and the kernels (sm_100a).
+// All work items carry absolute device addresses; they are built on the host per
+// batch and uploaded with one cudaMemcpyAsync per launch group.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+
+#define HS_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      ::hs::fail(e_ == cudaErrorMemoryAllocation ? HS_E_OOM : HS_E_CUDA,                    \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+namespace hs {
+
+// Batched 2-D copy with optional transpose:
+//   dst[i*dld + j] = trans ? src[j*sld + i] : src[i*sld + j]   (i < rows, j < cols)
+// Used by pack (a0), write-back (a6), level assembly (A_c) and the top.
+struct CopyItem {
+  const double* src;
+  double* dst;
+  int32_t sld, dld, rows, cols, trans, pad;
+};
+
+// One cluster of a batch (a1-a4).
+struct CluItem {
+  double* G;        // m x m, row-major ld m: holds A_ss on entry, the lower factor G_s on exit
+  double* V;        // m x m, column j = Householder vector v_j (col-major, ld m)
+  double* tau;      // m
+  double* B;        // B_s = [A_sw | A_sn], m x ldB row-major, w columns first
+  int32_t* piv;     // m canonical pivot columns
+  double* nu;       // kw scratch column norms
+  int32_t m, kw, kn, ldB;
+  int32_t level, cluster, pad0, pad1;
+};
+
+struct TrsmItem {   // one column tile of one cluster's B_s
+  int32_t ci, c0, nc, pad;
+};
+
+// Schur target tile (a5):
+//   dst[i*ld + j] -= sum_{contrib} sum_{k<K} C[k*ldC + colP + i0 + i] * C[k*ldC + colQ + j0 + j]
+struct SchurTile {
+  double* dst;               // tile origin
+  int32_t ld, rows, cols;    // tile extent (<= 64 x 64)
+  int32_t c_begin, c_end;    // contributions [c_begin, c_end), source cluster ascending
+  int32_t i0, j0, pad;
+};
+struct SchurContrib {
+  const double* C;           // C_s row 0 (= B_s + r*ldB + kw), ld ldC
+  int32_t ldC, K, colP, colQ;
+};
+
+// Apply (Algorithm 2) items.
+struct ApplyLocal {          // forward: y_s <- U^T G^{-1} y_s ; backward: x_f -= sum C x_q, x_s <- G^{-T} U x_s
+  const double* G;
+  const double* V;
+  const double* tau;
+  double* y;                 // the cluster's segment (m entries)
+  const double* C;           // C_s (fine rows), n-part column 0, ld ldC
+  int32_t m, r, nb_begin, nb_end, ldC, pad;
+};
+struct ApplyNb {             // backward: C_s[:, col:col+len] x_q
+  const double* xq;
+  int32_t col, len;
+};
+struct ApplyTarget {         // forward: y_q[0:len] -= sum_s C_s[:, col:col+len]^T y_f,s
+  double* yq;
+  int32_t len, c_begin, c_end, pad;
+};
+struct ApplyContrib {
+  const double* C;           // C_s (fine rows), n-part column 0
+  const double* yf;          // y_f,s
+  int32_t ldC, K, col, pad;
+};
+
+// First error raised on the device (POTRF breakdown).
+struct DevStatus {
+  int32_t flag, level, cluster, pivot;
+  double value;
+};
+
+// ---- kernel launchers (kernels.cu / solve_kernels.cu) -------------------------------------
+void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st);
+void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d_r, int n, cudaStream_t st);
+void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st);
+void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
+void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
+void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st);
+void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
+// Dense blocked Cholesky of the top matrix (row-major, ld).  On return the
+// diagonal NB x NB blocks hold G_kk (lower) and the block rows right of them hold
+// U_kj = G_kk^{-1} A_kj (i.e. L^T); the strictly lower off-diagonal blocks are stale.
+void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double* scratch_items,
+                 cudaStream_t st);
+constexpr int TOP_NB = 64;
+
+void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st);
+void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, cudaStream_t st);
+void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
+void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
+void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,
+                 int64_t n, cudaStream_t st);
+
+constexpr int MAX_M = 128;   // largest cluster handled by the single-CTA POTRF/TRSM/apply kernels
+
+}  // namespace hs

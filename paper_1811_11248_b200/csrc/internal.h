@@ -1,0 +1,52 @@
+// Internal structures of libhsolve (host side).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hsolve.h"
+
+namespace hs {
+
+// An exception that carries an hs_status across internal code; translated to a
+// status code at the ABI (capi.cpp).  Never crosses the C boundary.
+struct Error : std::runtime_error {
+  hs_status status;
+  Error(hs_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(hs_status s, const std::string& m) { throw Error(s, m); }
+
+using Adj = std::vector<std::vector<int32_t>>;   // sorted adjacency lists
+
+struct Level {
+  int32_t nclus = 0;
+  Adj H;                       // H_l: structural block pattern of A_l; n(s) = H[s]
+  Adj w;                       // w(s) at elimination time
+  std::vector<std::vector<int32_t>> batches;
+  int32_t nphase1 = 0;
+  std::vector<uint8_t> interior;
+  Adj Ffinal;                  // fill graph after the level
+};
+
+struct Analysis {
+  int64_t n = 0;
+  int32_t D = 0, L_top = 0, top_log2 = 3, nsub_log2 = 3;
+  std::vector<int64_t> perm;       // perm[new] = old
+  std::vector<int64_t> iperm;      // iperm[old] = new
+  std::vector<int64_t> leaf_off;   // 2^D + 1
+  std::vector<Level> levels;       // 0 .. L_top-1
+  Adj H_top;
+  // the pattern, kept for hs_factor (values come later)
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> colind;
+  int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
+};
+
+Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
+                  int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts& opt);
+
+}  // namespace hs

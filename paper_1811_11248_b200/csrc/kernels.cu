@@ -1,0 +1,456 @@
+// Factor kernels (sm_100a), one per row of SURVEY §8(a):
+//   a0 pack / a6 write-back / A_c assembly : k_copy2d (batched 2-D copy, smem-tiled transpose)
+//   a1 POTRF  A_ss = G_s G_s^T                 : k_potrf
+//   a2 TRSM   B = G_s^{-1}[A_sw | A_sn] (deferred compression) : k_trsm
+//   a3+a4 CPQR of G_s^{-1}A_sw to eps with the rotation U^T fused onto the
+//        n-columns (Eq. offdiag_new, Eq. CC:eqn:sparse P:537-565) : k_cpqr
+//   a5 Schur  A_pq -= C_p^T C_q (Eq. CC:eqn:elim)    : k_schur
+//   a7 top dense Cholesky                             : dense_potrf
+// No kernel shares code with the oracle; see DESIGN.md for each kernel's roofline.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <vector>
+
+#include "device.h"
+
+namespace hs {
+
+namespace {
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide reductions; red must hold >= 32 entries; all threads get the result
+__device__ double block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = lane < nw ? red[lane] : -DBL_MAX;
+  r = warp_max(r);
+  return r;
+}
+__device__ int block_min_int(int v, int* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_min_int(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  int r = lane < nw ? red[lane] : INT_MAX;
+  return warp_min_int(r);
+}
+
+// ---------------------------------------------------------------------------------------
+// a0/a6: batched 2-D copy.  Non-transposed: coalesced row copy.  Transposed: 32x32 smem tiles
+// so that both the read and the write are coalesced.
+__global__ void k_copy2d(const CopyItem* __restrict__ items) {
+  const CopyItem it = items[blockIdx.x];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  if (!it.trans) {
+    const int64_t tot = (int64_t)it.rows * it.cols;
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int i = (int)(e / it.cols), j = (int)(e % it.cols);
+      it.dst[(int64_t)i * it.dld + j] = it.src[(int64_t)i * it.sld + j];
+    }
+    return;
+  }
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+  for (int ti = 0; ti < it.rows; ti += 32)
+    for (int tj = 0; tj < it.cols; tj += 32) {
+      // src element (row j, col i) for dst (i, j): read along i (contiguous in src row j)
+      for (int jj = ty; jj < 32; jj += ny) {
+        const int j = tj + jj, i = ti + tx;
+        tile[jj][tx] = (j < it.cols && i < it.rows) ? it.src[(int64_t)j * it.sld + i] : 0.0;
+      }
+      __syncthreads();
+      for (int ii = ty; ii < 32; ii += ny) {
+        const int i = ti + ii, j = tj + tx;
+        if (i < it.rows && j < it.cols) it.dst[(int64_t)i * it.dld + j] = tile[tx][ii];
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void k_identity(double* const* ptr, const int32_t* ld, const int32_t* r) {
+  double* p = ptr[blockIdx.x];
+  const int n = r[blockIdx.x], l = ld[blockIdx.x];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    p[(int64_t)i * l + j] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_scatter(const double* __restrict__ vals, const int64_t* __restrict__ map, int64_t nnz,
+                          double* __restrict__ blk) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = map[k];
+    if (d >= 0) blk[d] = vals[k];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// a1: right-looking Cholesky of an m x m block held in shared memory (m <= MAX_M).
+// A pivot <= 0 (or NaN) records the first failure in *status (no shift, no jitter).
+__device__ void potrf_core(double* g, int ld, int m, double* a, DevStatus* status, int level, int cluster) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) a[e] = g[(int64_t)(e / m) * ld + (e % m)];
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = a[j * m + j];
+      if (!(d > 0.0)) {
+        bad = 1;
+        if (atomicCAS(&status->flag, 0, 1) == 0) {
+          status->level = level;
+          status->cluster = cluster;
+          status->pivot = j;
+          status->value = d;
+        }
+      } else {
+        a[j * m + j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (bad) return;
+    const double piv = a[j * m + j];
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[i * m + j] /= piv;
+    __syncthreads();
+    // trailing update of the lower triangle: a[i][k] -= a[i][j] * a[k][j], j < k <= i
+    const int t = m - j - 1;
+    const int tot = t * (t + 1) / 2;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      // map e -> (i, k) with 0 <= k <= i < t
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      while (i * (i + 1) / 2 > e) --i;
+      const int k = e - i * (i + 1) / 2;
+      const int ii = j + 1 + i, kk = j + 1 + k;
+      a[ii * m + kk] -= a[ii * m + j] * a[kk * m + j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, k = e % m;
+    g[(int64_t)i * ld + k] = (k <= i) ? a[e] : 0.0;
+  }
+}
+
+__global__ void k_potrf(const CluItem* __restrict__ items, DevStatus* status) {
+  extern __shared__ double smem[];
+  const CluItem it = items[blockIdx.x];
+  if (it.m == 0) return;
+  potrf_core(it.G, it.m, it.m, smem, status, it.level, it.cluster);
+}
+
+__global__ void k_potrf_raw(double* g, int ld, int m, DevStatus* status, int level) {
+  extern __shared__ double smem[];
+  potrf_core(g, ld, m, smem, status, level, -1);
+}
+
+// ---------------------------------------------------------------------------------------
+// a2: X = G^{-1} B for a column tile (<= 64 columns) of B (m x ncols, row-major ld ldB),
+// G lower m x m (ld ldG).  G and the tile live in shared memory; 256 threads =
+// 64 columns x 4 row groups, right-looking forward substitution.
+__device__ void trsm_core(const double* G, int ldG, int m, double* B, int ldB, int c0, int nc, double* sm) {
+  double* g = sm;                 // m*m
+  double* x = sm + m * m;         // m*64
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e / m, k = e % m;
+    g[e] = (k <= i) ? G[(int64_t)i * ldG + k] : 0.0;
+  }
+  for (int e = threadIdx.x; e < m * 64; e += blockDim.x) {
+    const int i = e >> 6, c = e & 63;
+    x[e] = c < nc ? B[(int64_t)i * ldB + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x & 63, grp = threadIdx.x >> 6, ngrp = blockDim.x >> 6;
+  for (int i = 0; i < m; ++i) {
+    if (grp == 0) x[i * 64 + c] /= g[i * m + i];
+    __syncthreads();
+    const double xi = x[i * 64 + c];
+    for (int l = i + 1 + grp; l < m; l += ngrp) x[l * 64 + c] -= g[l * m + i] * xi;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * 64; e += blockDim.x) {
+    const int i = e >> 6, cc = e & 63;
+    if (cc < nc) B[(int64_t)i * ldB + c0 + cc] = x[e];
+  }
+}
+
+__global__ void k_trsm(const CluItem* __restrict__ clu, const TrsmItem* __restrict__ items) {
+  extern __shared__ double smem[];
+  const TrsmItem t = items[blockIdx.x];
+  const CluItem it = clu[t.ci];
+  if (it.m == 0) return;
+  trsm_core(it.G, it.m, it.m, it.B, it.ldB, t.c0, t.nc, smem);
+}
+
+__global__ void k_trsm_raw(const double* G, int ldG, int m, double* B, int ldB, int ncols) {
+  extern __shared__ double smem[];
+  const int c0 = blockIdx.x * 64;
+  trsm_core(G, ldG, m, B, ldB, c0, min(64, ncols - c0), smem);
+}
+
+// ---------------------------------------------------------------------------------------
+// a3 + a4: column-pivoted Householder QR of the scaled block W = G^{-1}A_sw (columns
+// [0, kw) of B_s) truncated at the first step with max_i nu_i <= tau_s, tau_s = eps *
+// nu_max(0) (relative) or eps; pivot = lowest column index among nu_i >= (1-1e-10) nu_max.
+// The reflectors are applied to every column, so the n-columns [kw, kw+kn) receive U^T
+// (the sparsification E_s) in the same pass.  Columns are never swapped: on exit rows
+// [0, r) of B_s are [coarse-w | coarse-n] in canonical order and rows [r, m) of the
+// n-part are C = U_2^T G^{-1} A_sn.  Norms are recomputed exactly every step.
+// One CTA per cluster, a thread per column (coalesced along the row-major rows).
+constexpr int CPQR_THREADS = 512;
+
+__global__ void __launch_bounds__(CPQR_THREADS) k_cpqr(const CluItem* __restrict__ items, double eps, int relative,
+                                                       int32_t* __restrict__ rank_out) {
+  const CluItem it = items[blockIdx.x];
+  const int m = it.m, kw = it.kw, ncol = it.kw + it.kn, ld = it.ldB;
+  double* B = it.B;
+  double* nu = it.nu;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  __shared__ double v[MAX_M];
+  __shared__ double s_tau, s_beta;
+  if (m == 0 || kw == 0) {
+    if (threadIdx.x == 0) rank_out[blockIdx.x] = 0;
+    return;
+  }
+  // initial exact column norms
+  for (int i = threadIdx.x; i < kw; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double b = B[(int64_t)l * ld + i];
+      s += b * b;
+    }
+    nu[i] = sqrt(s);
+  }
+  __syncthreads();
+  const int kmax = min(m, kw);
+  double tau_s = 0.0;
+  int r = kmax;
+  for (int j = 0; j < kmax; ++j) {
+    double lmax = -1.0;
+    for (int i = threadIdx.x; i < kw; i += blockDim.x) lmax = fmax(lmax, nu[i]);
+    const double numax = block_max(lmax, red);
+    if (j == 0) tau_s = relative ? eps * numax : eps;
+    if (!(numax > tau_s)) { r = j; break; }        // strict keep rule
+    const double thr = (1.0 - 1e-10) * numax;
+    int lmin = INT_MAX;
+    for (int i = threadIdx.x; i < kw; i += blockDim.x)
+      if (nu[i] >= thr && i < lmin) lmin = i;
+    const int p = block_min_int(lmin, redi);
+    // Householder vector from column p, rows j..m-1 (LAPACK dlarfg convention)
+    if (threadIdx.x < 32) {
+      double xs = 0.0;
+      for (int l = j + 1 + threadIdx.x; l < m; l += 32) {
+        const double b = B[(int64_t)l * ld + p];
+        xs += b * b;
+      }
+      xs = warp_sum(xs);
+      const double alpha = B[(int64_t)j * ld + p];
+      const double xnorm = sqrt(xs);
+      double tau, beta, den;
+      if (xnorm == 0.0) {
+        tau = 0.0; beta = alpha; den = 1.0;
+      } else {
+        const double h = sqrt(alpha * alpha + xnorm * xnorm);
+        beta = alpha >= 0.0 ? -h : h;
+        tau = (beta - alpha) / beta;
+        den = alpha - beta;
+      }
+      for (int l = j + 1 + threadIdx.x; l < m; l += 32) v[l] = (tau == 0.0) ? 0.0 : B[(int64_t)l * ld + p] / den;
+      if (threadIdx.x == 0) {
+        v[j] = 1.0;
+        s_tau = tau;
+        s_beta = beta;
+        it.tau[j] = tau;
+        it.piv[j] = p;
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    // store v_j (column j of V, zeros above the diagonal)
+    for (int l = threadIdx.x; l < m; l += blockDim.x) it.V[(int64_t)j * m + l] = l < j ? 0.0 : v[l];
+    // apply H_j to every live column but the pivot, recompute the trailing norms
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
+      if (i == p) continue;
+      if (i < kw && nu[i] < 0.0) continue;          // already pivoted
+      double d = 0.0;
+      if (tau != 0.0)
+        for (int l = j; l < m; ++l) d += v[l] * B[(int64_t)l * ld + i];
+      const double td = tau * d;
+      double s = 0.0;
+      for (int l = j; l < m; ++l) {
+        double b = B[(int64_t)l * ld + i];
+        if (tau != 0.0) {
+          b -= td * v[l];
+          B[(int64_t)l * ld + i] = b;
+        }
+        if (l > j) s += b * b;
+      }
+      if (i < kw) nu[i] = sqrt(s);
+    }
+    if (threadIdx.x == 0) {
+      B[(int64_t)j * ld + p] = s_beta;
+      nu[p] = -1.0;
+    }
+    for (int l = j + 1 + threadIdx.x; l < m; l += blockDim.x) B[(int64_t)l * ld + p] = 0.0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rank_out[blockIdx.x] = r;
+}
+
+// ---------------------------------------------------------------------------------------
+// a5: Schur update tiles, FP64 FMA (64 x 64 tile, 256 threads, 4 x 4 per thread),
+// K staged through shared memory 16 rows at a time.  Contributions of a tile are summed
+// in source-cluster order before the single read-modify-write of the target.
+__global__ void __launch_bounds__(256) k_schur(const SchurTile* __restrict__ tiles,
+                                               const SchurContrib* __restrict__ con) {
+  const SchurTile t = tiles[blockIdx.x];
+  __shared__ double ap[16][64];
+  __shared__ double aq[16][64];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int c = t.c_begin; c < t.c_end; ++c) {
+    const SchurContrib s = con[c];
+    const double* Cp = s.C + s.colP + t.i0;
+    const double* Cq = s.C + s.colQ + t.j0;
+    for (int k0 = 0; k0 < s.K; k0 += 16) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = threadIdx.x + 256 * q;
+        const int kk = e >> 6, ii = e & 63;
+        const bool kin = k0 + kk < s.K;
+        ap[kk][ii] = (kin && ii < t.rows) ? Cp[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+        aq[kk][ii] = (kin && ii < t.cols) ? Cq[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        double x[4], y[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) x[a] = ap[kk][ty + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) y[b] = aq[kk][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      if (i < t.rows && j < t.cols) t.dst[(int64_t)i * t.ld + j] -= acc[a][b];
+    }
+}
+
+void set_smem(const void* f, size_t bytes) {
+  static_cast<void>(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace
+
+// ---- launchers -----------------------------------------------------------------------------
+void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st) {
+  if (n > 0) k_copy2d<<<n, 256, 0, st>>>(d_items);
+}
+void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d_r, int n, cudaStream_t st) {
+  if (n > 0) k_identity<<<n, 128, 0, st>>>(d_ptr, d_ld, d_r);
+}
+void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st) {
+  if (nnz > 0) k_scatter<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, map, nnz, blk);
+}
+void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t sm = (size_t)max_m * max_m * sizeof(double);
+  set_smem((const void*)k_potrf, sm);
+  k_potrf<<<n, 256, sm, st>>>(d_items, status);
+}
+void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t sm = ((size_t)max_m * max_m + (size_t)max_m * 64) * sizeof(double);
+  set_smem((const void*)k_trsm, sm);
+  k_trsm<<<n, 256, sm, st>>>(d_clu, d_items);
+}
+void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st) {
+  if (n > 0) k_cpqr<<<n, CPQR_THREADS, 0, st>>>(d_items, eps, relative, d_rank);
+}
+void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st) {
+  if (n > 0) k_schur<<<n, 256, 0, st>>>(d_tiles, d_con);
+}
+
+// a7: blocked right-looking Cholesky of the dense top matrix.
+void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double* /*unused*/, cudaStream_t st) {
+  const int NB = TOP_NB;
+  set_smem((const void*)k_potrf_raw, (size_t)NB * NB * sizeof(double));
+  set_smem((const void*)k_trsm_raw, ((size_t)NB * NB + (size_t)NB * 64) * sizeof(double));
+  std::vector<SchurTile> tiles;
+  SchurContrib* d_con = nullptr;
+  SchurTile* d_tiles = nullptr;
+  const int nblk = (N + NB - 1) / NB;
+  const size_t max_tiles = (size_t)nblk * (nblk + 1) / 2 + 1;
+  HS_CUDA(cudaMalloc(&d_con, sizeof(SchurContrib) * nblk));
+  HS_CUDA(cudaMalloc(&d_tiles, sizeof(SchurTile) * max_tiles));
+  std::vector<SchurContrib> cons(nblk);
+  for (int k = 0; k < N; k += NB) {
+    const int nb = std::min(NB, N - k);
+    k_potrf_raw<<<1, 256, (size_t)nb * nb * sizeof(double), st>>>(A + (int64_t)k * ld + k, ld, nb, status, level);
+    const int rest = N - k - nb;
+    if (rest <= 0) break;
+    k_trsm_raw<<<(rest + 63) / 64, 256, ((size_t)nb * nb + (size_t)nb * 64) * sizeof(double), st>>>(
+        A + (int64_t)k * ld + k, ld, nb, A + (int64_t)k * ld + k + nb, ld, rest);
+    const int kb = k / NB;
+    cons[kb] = SchurContrib{A + (int64_t)k * ld + k + nb, ld, nb, 0, 0};
+    tiles.clear();
+    for (int i0 = 0; i0 < rest; i0 += 64)
+      for (int j0 = i0; j0 < rest; j0 += 64) {
+        SchurTile t{};
+        t.dst = A + (int64_t)(k + nb + i0) * ld + (k + nb + j0);
+        t.ld = ld;
+        t.rows = std::min(64, rest - i0);
+        t.cols = std::min(64, rest - j0);
+        t.c_begin = kb;
+        t.c_end = kb + 1;
+        t.i0 = i0;
+        t.j0 = j0;
+        tiles.push_back(t);
+      }
+    HS_CUDA(cudaMemcpyAsync(d_con + kb, &cons[kb], sizeof(SchurContrib), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(SchurTile) * tiles.size(),
+                            cudaMemcpyHostToDevice, st));
+    k_schur<<<(int)tiles.size(), 256, 0, st>>>(d_tiles, d_con);
+    HS_CUDA(cudaStreamSynchronize(st));   // host vectors are reused; the top runs once per factor
+  }
+  HS_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_con);
+  cudaFree(d_tiles);
+}
+
+}  // namespace hs

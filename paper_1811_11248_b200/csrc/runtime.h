@@ -1,0 +1,109 @@
+// Host runtime structures of libhsolve (handle, factor, apply plan).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "device.h"
+#include "internal.h"
+
+struct hs_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int world = 1, rank = 0;
+  std::string err;
+};
+
+struct hs_analysis_s {
+  hs::Analysis* an = nullptr;
+};
+
+namespace hs {
+
+// device buffer that grows on demand (used for per-launch descriptor uploads)
+struct DevScratch {
+  char* d = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes);
+  ~DevScratch();
+};
+
+// pinned host staging buffer
+struct HostStage {
+  char* h = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  void ensure(size_t bytes);
+  ~HostStage();
+};
+
+struct LevelRT {
+  int32_t nclus = 0;
+  std::vector<int32_t> cap, rank, kn, kw, ldB;
+  std::vector<int64_t> voff;            // apply-vector offsets (prefix sums of cap)
+  int64_t vlen = 0;
+  double* arena = nullptr;              // G, V, tau, nu, B of every cluster
+  int32_t* iarena = nullptr;            // pivots
+  std::vector<double*> G, V, tau, B, nu;
+  std::vector<int32_t*> piv;
+  size_t arena_bytes = 0;
+};
+
+struct ApplyBatch {
+  int32_t local_begin, local_end;       // into fwd_local / bwd_local item arrays
+  int32_t tgt_begin, tgt_end;           // forward scatter targets
+};
+
+struct ApplyPlan {
+  std::vector<ApplyLocal> local;        // shared by forward (nb range unused) and backward
+  std::vector<ApplyNb> nb;
+  std::vector<ApplyTarget> tgt;
+  std::vector<ApplyContrib> con;
+  std::vector<std::vector<ApplyBatch>> batches;   // per level
+  std::vector<std::vector<int64_t>> trans_src, trans_dst;   // level l -> l+1 vector transition
+  // device copies
+  ApplyLocal* d_local = nullptr;
+  ApplyNb* d_nb = nullptr;
+  ApplyTarget* d_tgt = nullptr;
+  ApplyContrib* d_con = nullptr;
+  std::vector<int64_t*> d_tsrc, d_tdst;
+  std::vector<int64_t> vbase;            // per level + top
+  int64_t vtotal = 0;
+  double* d_y = nullptr;                 // the apply vector (all levels + top)
+  cudaGraphExec_t graph = nullptr;
+  const double* graph_in = nullptr;
+  double* graph_out = nullptr;
+};
+
+}  // namespace hs
+
+struct hs_factor_s {
+  hs_handle_s* h = nullptr;
+  const hs::Analysis* an = nullptr;
+  hs_factor_opts opt{};
+  // CSR in the original ordering (SpMV)
+  int64_t* d_rowptr = nullptr;
+  int32_t* d_colind = nullptr;
+  double* d_vals = nullptr;
+  int64_t* d_perm = nullptr;
+  std::vector<hs::LevelRT> lv;
+  double* d_top = nullptr;
+  int64_t ntop = 0;
+  std::vector<int32_t> top_sizes;
+  hs::ApplyPlan ap;
+  hs_factor_stats_t stats{};
+  // PCG work vectors
+  double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_x = nullptr, *d_b = nullptr;
+  double* d_red = nullptr;     // reduction scratch
+  double* h_red = nullptr;     // pinned
+  ~hs_factor_s();
+};
+
+namespace hs {
+hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* values, const hs_factor_opts& opt);
+void apply(hs_factor_s* f, const double* d_b, double* d_x);         // device pointers
+void pcg(hs_factor_s* f, const double* d_b, double* d_x, double tol, int maxit, hs_pcg_report* rep);
+void spmv(hs_factor_s* f, const double* d_x, double* d_y);
+}  // namespace hs

@@ -1,0 +1,251 @@
+// hs_apply / hs_pcg host drivers.
+//
+// Apply = Algorithm 2, captured once per factor as a CUDA graph:
+//   permute-in, forward sweep (per level: per batch local + scatter, then the
+//   level transition), top solve, backward sweep (reverse), permute-out.
+// PCG (north_star) keeps every scalar on the device; the only host
+// synchronisation per iteration is the 8-byte read of ||r||^2 for the stopping test.
+#include <cmath>
+
+#include "runtime.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int RED_BLOCKS = 296;   // 2 x 148 SMs
+constexpr int RED_THREADS = 256;
+
+__global__ void k_move(double* y, const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n,
+                       int reverse) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (reverse) y[src[i]] = y[dst[i]];
+    else y[dst[i]] = y[src[i]];
+  }
+}
+
+// scalars layout (device): 0 rho, 1 pq, 2 rr, 3 rz_new, 4 bb
+__device__ __forceinline__ double blk_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  return r;
+}
+
+// partial[b] = sum over the block's grid-stride slice of a[i]*b[i]
+__global__ void k_dot_partial(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                              double* __restrict__ partial) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += a[i] * b[i];
+  acc = blk_sum(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+// out = sum of the partials in fixed order (deterministic)
+__global__ void k_finish(const double* __restrict__ partial, int np, double* out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
+  acc = blk_sum(acc, sh);
+  if (threadIdx.x == 0) *out = acc;
+}
+// x += alpha p ; r -= alpha q ; alpha = rho / pq ; partial ||r||^2
+__global__ void k_update_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                            const double* __restrict__ q, int64_t n, const double* sc, double* __restrict__ partial) {
+  __shared__ double sh[32];
+  const double alpha = sc[0] / sc[1];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  acc = blk_sum(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+// p = z + (rz_new / rho) p ; rho = rz_new  (the scalar update is done by block 0 after all reads)
+__global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const double* sc) {
+  const double beta = sc[3] / sc[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+__global__ void k_set_rho(double* sc) { sc[0] = sc[3]; }
+__global__ void k_zero(double* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = 0.0;
+}
+__global__ void k_copy(double* __restrict__ d, const double* __restrict__ s, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+__global__ void k_sub(double* __restrict__ d, const double* __restrict__ a, const double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = a[i] - b[i];
+}
+
+void dot(const double* a, const double* b, int64_t n, double* partial, double* out, cudaStream_t st) {
+  k_dot_partial<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, n, partial);
+  k_finish<<<1, RED_THREADS, 0, st>>>(partial, RED_BLOCKS, out);
+}
+
+void record_apply(hs_factor_s* f, cudaStream_t st) {
+  const Analysis* an = f->an;
+  ApplyPlan& ap = f->ap;
+  const int64_t n = an->n;
+  launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
+  for (int l = 0; l < an->L_top; ++l) {
+    for (const auto& b : ap.batches[l]) {
+      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, st);
+      launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
+    }
+    const int64_t nt = (int64_t)ap.trans_src[l].size();
+    if (nt) k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 0);
+  }
+  if (f->ntop > 0) launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);
+  for (int l = an->L_top - 1; l >= 0; --l) {
+    const int64_t nt = (int64_t)ap.trans_src[l].size();
+    if (nt) k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
+    for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it)
+      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, st);
+  }
+  launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);
+}
+
+void ensure_vectors(hs_factor_s* f) {
+  const int64_t n = f->an->n;
+  if (f->d_b) return;
+  for (double** p : {&f->d_r, &f->d_z, &f->d_p, &f->d_q, &f->d_x, &f->d_b})
+    HS_CUDA(cudaMalloc(p, sizeof(double) * std::max<int64_t>(n, 1)));
+  HS_CUDA(cudaMalloc(&f->d_red, sizeof(double) * (RED_BLOCKS + 16)));
+  HS_CUDA(cudaMallocHost(&f->h_red, sizeof(double) * 16));
+}
+
+// graph: d_b -> M^{-1} d_b -> d_x
+void run_apply_graph(hs_factor_s* f, cudaStream_t st) {
+  ApplyPlan& ap = f->ap;
+  if (!ap.graph) {
+    cudaStream_t cs;
+    HS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    HS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    record_apply(f, cs);
+    HS_CUDA(cudaStreamEndCapture(cs, &g));
+    HS_CUDA(cudaGraphInstantiate(&ap.graph, g, 0));
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+  }
+  HS_CUDA(cudaGraphLaunch(ap.graph, st));
+}
+
+}  // namespace
+
+void apply(hs_factor_s* f, const double* d_b, double* d_x) {
+  cudaStream_t st = f->h->stream;
+  ensure_vectors(f);
+  const int64_t n = f->an->n;
+  if (d_b != f->d_b) HS_CUDA(cudaMemcpyAsync(f->d_b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  run_apply_graph(f, st);
+  if (d_x != f->d_x) HS_CUDA(cudaMemcpyAsync(d_x, f->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+}
+
+void spmv(hs_factor_s* f, const double* d_x, double* d_y) {
+  launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, d_x, d_y, f->an->n, f->h->stream);
+}
+
+void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int maxit, hs_pcg_report* rep) {
+  cudaStream_t st = f->h->stream;
+  ensure_vectors(f);
+  const int64_t n = f->an->n;
+  const int G = RED_BLOCKS, T = RED_THREADS;
+  double* sc = f->d_red + RED_BLOCKS;   // scalars
+  double* part = f->d_red;
+  // The apply graph reads d_b (= r) and writes d_x (= z); PCG keeps its own x in d_q's partner.
+  double* r = f->d_b;
+  double* z = f->d_x;
+  double *x = f->d_r, *p = f->d_p, *q = f->d_q;
+  cudaEvent_t e0, e1, a0, a1;
+  HS_CUDA(cudaEventCreate(&e0)); HS_CUDA(cudaEventCreate(&e1));
+  HS_CUDA(cudaEventCreate(&a0)); HS_CUDA(cudaEventCreate(&a1));
+  double t_apply = 0.0;
+  HS_CUDA(cudaEventRecord(e0, st));
+  k_copy<<<G, T, 0, st>>>(r, d_bin, n);
+  k_zero<<<G, T, 0, st>>>(x, n);
+  dot(r, r, n, part, sc + 4, st);                       // bb
+  HS_CUDA(cudaEventRecord(a0, st));
+  run_apply_graph(f, st);                               // z = M^{-1} r
+  HS_CUDA(cudaEventRecord(a1, st));
+  k_copy<<<G, T, 0, st>>>(p, z, n);
+  dot(r, z, n, part, sc + 0, st);                       // rho
+  HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  {
+    float ms;
+    HS_CUDA(cudaEventElapsedTime(&ms, a0, a1));
+    t_apply += ms * 1e-3;
+  }
+  const double bb = f->h_red[4];
+  rep->iters = 0;
+  rep->converged = 0;
+  rep->relres = 1.0;
+  hs_status err = HS_OK;
+  if (bb == 0.0) {
+    rep->converged = 1;
+    rep->relres = 0.0;
+  } else if (!(f->h_red[0] > 0.0)) {
+    err = HS_E_PRECOND_NOT_POSITIVE;
+  } else {
+    const double nb = std::sqrt(bb);
+    for (int k = 1; k <= maxit; ++k) {
+      launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, p, q, n, st);   // q = A p
+      dot(p, q, n, part, sc + 1, st);                                  // pq
+      k_update_xr<<<G, T, 0, st>>>(x, r, p, q, n, sc, part);           // x, r, ||r||^2
+      k_finish<<<1, T, 0, st>>>(part, G, sc + 2);
+      HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      rep->iters = k;
+      const double rel = std::sqrt(std::max(f->h_red[2], 0.0)) / nb;
+      rep->relres = rel;
+      if (!(f->h_red[0] > 0.0)) { err = HS_E_PRECOND_NOT_POSITIVE; break; }
+      if (rel <= tol) { rep->converged = 1; break; }
+      HS_CUDA(cudaEventRecord(a0, st));
+      run_apply_graph(f, st);                                          // z = M^{-1} r
+      HS_CUDA(cudaEventRecord(a1, st));
+      dot(r, z, n, part, sc + 3, st);                                  // rz_new
+      k_update_p<<<G, T, 0, st>>>(p, z, n, sc);
+      k_set_rho<<<1, 1, 0, st>>>(sc);
+      HS_CUDA(cudaEventSynchronize(a1));
+      float ms;
+      HS_CUDA(cudaEventElapsedTime(&ms, a0, a1));
+      t_apply += ms * 1e-3;
+    }
+  }
+  HS_CUDA(cudaEventRecord(e1, st));
+  HS_CUDA(cudaEventSynchronize(e1));
+  float ms;
+  HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  rep->t_pcg_s = ms * 1e-3;
+  rep->t_apply_s = t_apply;
+  rep->t_spmv_s = 0.0;
+  // true residual ||b - A x|| / ||b|| (outside the timed region)
+  launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, x, q, n, st);
+  k_sub<<<G, T, 0, st>>>(q, d_bin, q, n);
+  dot(q, q, n, part, sc + 2, st);
+  HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
+  if (d_xout != x) HS_CUDA(cudaMemcpyAsync(d_xout, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  rep->relres_true = bb > 0 ? std::sqrt(std::max(f->h_red[2], 0.0) / bb) : 0.0;
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(a0); cudaEventDestroy(a1);
+  if (err != HS_OK) fail(err, "pcg: <r, M^{-1} r> <= 0 (preconditioner not positive)");
+  if (!rep->converged) fail(HS_E_NOT_CONVERGED, "pcg: not converged within maxit");
+}
+
+}  // namespace hs

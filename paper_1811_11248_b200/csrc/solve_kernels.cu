@@ -1,0 +1,226 @@
+// Solve-phase kernels (sm_100a): Algorithm 2 `Hierarchical_Solve` and the
+// CSR SpMV / vector helpers of PCG.  HBM/latency bound: every factor byte is read once
+// per sweep.  A cluster's local solve runs in one warp with lane-owned vector entries
+// (entry l lives in lane l % 32, slot l / 32), so no block barrier is needed.
+#include <cuda_runtime.h>
+
+#include "device.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int SLOTS = MAX_M / 32;
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// y <- G^{-1} y (G lower, row-major ld m): row-oriented, coalesced row reads
+__device__ __forceinline__ void warp_trsv_lower(const double* G, int m, double (&y)[SLOTS], int lane) {
+  for (int i = 0; i < m; ++i) {
+    double p = 0.0;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      if (l < i) p += G[(int64_t)i * m + l] * y[s];
+    }
+    p = wsum(p);
+    if ((i & 31) == lane) {
+      const double gi = G[(int64_t)i * m + i];
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (s == (i >> 5)) y[s] = (y[s] - p) / gi;
+    }
+  }
+}
+
+// y <- G^{-T} y : column-oriented backward substitution, rows of G read contiguously
+__device__ __forceinline__ void warp_trsv_upper_t(const double* G, int m, double (&y)[SLOTS], int lane) {
+  for (int i = m - 1; i >= 0; --i) {
+    double xi = 0.0;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s)
+      if (s == (i >> 5)) xi = y[s];
+    xi = __shfl_sync(0xffffffffu, xi, i & 31);
+    xi /= G[(int64_t)i * m + i];
+    if ((i & 31) == lane) {
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+        if (s == (i >> 5)) y[s] = xi;
+    }
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      if (l < i) y[s] -= G[(int64_t)i * m + l] * xi;
+    }
+  }
+}
+
+// apply H_j (j = 0..r-1 forward, r-1..0 backward): y[j:] -= tau_j v_j (v_j . y[j:])
+__device__ __forceinline__ void warp_reflect(const double* V, const double* tau, int m, int j, double (&y)[SLOTS],
+                                             int lane) {
+  const double t = tau[j];
+  if (t == 0.0) return;
+  double d = 0.0;
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    if (l >= j && l < m) d += V[(int64_t)j * m + l] * y[s];
+  }
+  d = wsum(d) * t;
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    if (l >= j && l < m) y[s] -= d * V[(int64_t)j * m + l];
+  }
+}
+
+// forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s)
+__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const ApplyLocal it = items[w];
+  if (it.m == 0) return;
+  double y[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    y[s] = l < it.m ? it.y[l] : 0.0;
+  }
+  warp_trsv_lower(it.G, it.m, y, lane);
+  for (int j = 0; j < it.r; ++j) warp_reflect(it.V, it.tau, it.m, j, y, lane);
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    if (l < it.m) it.y[l] = y[s];
+  }
+}
+
+// forward: y_q -= C_s[:, col:col+len]^T y_f,s summed over the batch members s with q in n(s)
+// (G_s of Eq. CC:eqn:elim); one warp per target, contributions in source order.
+__global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const ApplyContrib* __restrict__ con, int n) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const ApplyTarget t = tg[w];
+  for (int i0 = 0; i0 < t.len; i0 += 32) {
+    const int i = i0 + lane;
+    double acc = 0.0;
+    for (int c = t.c_begin; c < t.c_end; ++c) {
+      const ApplyContrib a = con[c];
+      if (i < t.len)
+        for (int k = 0; k < a.K; ++k) acc += a.C[(int64_t)k * a.ldC + a.col + i] * a.yf[k];
+    }
+    if (i < t.len) t.yq[i] -= acc;
+  }
+}
+
+// backward: x_f = y_f - sum_q C_s[:, q] x_q ; x_s <- G^{-T} U [x_c; x_f]
+// one CTA per cluster: all warps form x_f, warp 0 does the local solve.
+__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs) {
+  const ApplyLocal it = items[blockIdx.x];
+  if (it.m == 0) return;
+  __shared__ double xf[MAX_M];
+  const int K = it.m - it.r;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = wid; k < K; k += nw) {
+    const double* Crow = it.C + (int64_t)k * it.ldC;
+    double acc = 0.0;
+    for (int b = it.nb_begin; b < it.nb_end; ++b) {
+      const ApplyNb nb = nbs[b];
+      for (int i = lane; i < nb.len; i += 32) acc += Crow[nb.col + i] * nb.xq[i];
+    }
+    acc = wsum(acc);
+    if (lane == 0) xf[k] = it.y[it.r + k] - acc;
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  double y[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    y[s] = l < it.r ? it.y[l] : (l < it.m ? xf[l - it.r] : 0.0);
+  }
+  for (int j = it.r - 1; j >= 0; --j) warp_reflect(it.V, it.tau, it.m, j, y, lane);
+  warp_trsv_upper_t(it.G, it.m, y, lane);
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const int l = lane + 32 * s;
+    if (l < it.m) it.y[l] = y[s];
+  }
+}
+
+// top: y <- L^{-T} L^{-1} y with the storage of dense_potrf (diagonal NB-blocks lower G_kk,
+// off-diagonal U = L^T in the block rows to the right).  One CTA, column-oriented sweeps.
+__device__ __forceinline__ double Lval(const double* A, int ld, int i, int l) {  // L[i][l], i >= l
+  return (i / TOP_NB == l / TOP_NB) ? A[(int64_t)i * ld + l] : A[(int64_t)l * ld + i];
+}
+__global__ void k_top_solve(double* y, const double* A, int N, int ld) {
+  for (int l = 0; l < N; ++l) {
+    __syncthreads();
+    const double yl = y[l] / A[(int64_t)l * ld + l];
+    __syncthreads();
+    if (threadIdx.x == 0) y[l] = yl;
+    for (int i = l + 1 + threadIdx.x; i < N; i += blockDim.x) y[i] -= Lval(A, ld, i, l) * yl;
+  }
+  for (int l = N - 1; l >= 0; --l) {
+    __syncthreads();
+    const double xl = y[l] / A[(int64_t)l * ld + l];
+    __syncthreads();
+    if (threadIdx.x == 0) y[l] = xl;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) y[i] -= Lval(A, ld, l, i) * xl;
+  }
+}
+
+__global__ void k_permute(const double* __restrict__ src, double* __restrict__ dst, const int64_t* __restrict__ idx,
+                          int64_t n, int scatter) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (scatter) dst[idx[i]] = src[i];
+    else dst[i] = src[idx[i]];
+  }
+}
+
+// CSR SpMV, 8 lanes per row (rows have <= 54 entries on the configs)
+__global__ void k_spmv(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                       const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y,
+                       int64_t n) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t row = g >> 3;
+  const int sub = threadIdx.x & 7;
+  double acc = 0.0;
+  if (row < n) {
+    const int64_t b = rowptr[row], e = rowptr[row + 1];
+    for (int64_t k = b + sub; k < e; k += 8) acc += vals[k] * __ldg(x + colind[k]);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (row < n && sub == 0) y[row] = acc;
+}
+
+}  // namespace
+
+void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st) {
+  if (n > 0) k_apply_fwd_local<<<(n + 3) / 4, 128, 0, st>>>(d, n);
+}
+void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st) {
+  if (n > 0) k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
+}
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, cudaStream_t st) {
+  if (n > 0) k_apply_bwd<<<n, 128, 0, st>>>(d, nb);
+}
+void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {
+  if (N > 0) k_top_solve<<<1, 1024, 0, st>>>(y, A, N, ld);
+}
+void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st) {
+  if (n > 0) k_permute<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(src, dst, idx, n, scatter);
+}
+void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,
+                 int64_t n, cudaStream_t st) {
+  if (n > 0) k_spmv<<<(int)((n * 8 + 255) / 256), 256, 0, st>>>(rowptr, colind, vals, x, y, n);
+}
+
+}  // namespace hs

@@ -1,0 +1,157 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle on the
+same seeded inputs (SURVEY §8(c) parity protocol, north_star tolerances):
+  * ranks identical for every cluster whose threshold margin mu_s >= 1e-10 and pivot
+    margin pi_s >= 1e-11; flagged clusters are replayed in the oracle by decision
+    injection with the GPU's pivots,
+  * factor apply on 3 seeded N(0,1) vectors within 1e-9 relative,
+  * PCG solution within 1e-8 relative and iterations within +-1,
+  * eps = 0: exact Cholesky, relative residual <= 1e-12 and one PCG iteration.
+"""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from problems import gen_poisson2d, gen_laplace3d, gen_slab, gen_stokes_q1
+from oracle.analyze import analyze
+from oracle.factor import factor as ofactor
+from oracle.solve import apply as oapply, pcg as opcg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    from paper_1811_11248_b200 import hsolve
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    hsolve.lib()
+    return hsolve
+
+
+@pytest.fixture(scope="module")
+def handle(H):
+    return H.hs_create(0)
+
+
+def _both(H, handle, p, eps, kw=None):
+    kw = kw or {}
+    top_log2 = kw.get("top_log2", 3)
+    nsub_log2 = kw.get("nsub_log2", 3)
+    an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                 leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
+    f = H.hs_factor_create(handle, a, p.vals, eps=eps)
+    fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps)
+    # rank parity with the margin exemption and decision injection
+    inject = {}
+    flagged = 0
+    for l, lv in enumerate(fac.elims):
+        g_r = H.hs_factor_export(f, H.HS_FEXP_RANKS, l)
+        g_pp = H.hs_factor_export(f, H.HS_FEXP_PIV_PTR, l)
+        g_pv = H.hs_factor_export(f, H.HS_FEXP_PIV, l)
+        for eb in lv:
+            for e in eb:
+                gpiv = g_pv[g_pp[e.s]:g_pp[e.s + 1]]
+                if e.flagged:
+                    flagged += 1
+                    if g_r[e.s] != e.r or not np.array_equal(gpiv, e.piv):
+                        inject[(l, e.s)] = (int(g_r[e.s]), gpiv.tolist())
+                    continue
+                assert g_r[e.s] == e.r, f"rank mismatch level {l} cluster {e.s}: gpu {g_r[e.s]} oracle {e.r}"
+                assert np.array_equal(gpiv, e.piv), f"pivot mismatch level {l} cluster {e.s}"
+    if inject:
+        fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps, inject=inject)
+    assert np.array_equal(H.hs_factor_export(f, H.HS_FEXP_TOP), fac.top_sizes)
+    return an, fac, a, f, flagged
+
+
+def _apply_parity(H, f, fac, n, seeds=(1, 2, 3), tol=1e-9):
+    worst = 0.0
+    for sd in seeds:
+        v = np.random.default_rng(sd).standard_normal(n)
+        xg = H.hs_apply(f, v)
+        xo = oapply(fac, v)
+        err = np.linalg.norm(xg - xo) / np.linalg.norm(xo)
+        worst = max(worst, err)
+        assert err <= tol, f"apply parity {err:.3e}"
+    return worst
+
+
+TINY = [
+    ("C1", lambda: gen_poisson2d(32), {}),
+    ("2d-8x8", lambda: gen_poisson2d(8, leaf_size=4), dict(top_log2=1, nsub_log2=1)),
+    ("3d-8", lambda: gen_laplace3d(8, leaf_size=8), dict(top_log2=2, nsub_log2=2)),
+    ("q1-4x4x3", lambda: gen_stokes_q1(4, 4, 3, leaf_columns=1), dict(top_log2=1, nsub_log2=1)),
+]
+
+
+@pytest.mark.parametrize("name,gen,kw", TINY, ids=[t[0] for t in TINY])
+def test_eps0_exact_cholesky(H, handle, name, gen, kw):
+    p = gen()
+    an, fac, a, f, _ = _both(H, handle, p, 0.0, kw)
+    A = p.to_scipy().toarray()
+    x_ref = sla.cho_solve(sla.cho_factor(A), p.b)
+    x = H.hs_apply(f, p.b)
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-12
+    x2, rep = H.hs_pcg(f, p.b, tol=1e-10)
+    assert rep["iters"] == 1 and rep["relres_true"] <= 1e-12
+
+
+CASES = TINY + [
+    ("aniso2d-ragged", lambda: gen_poisson2d(23, 17, aniso=1e-3, leaf_size=7), dict(top_log2=2, nsub_log2=1)),
+    ("3d-24", lambda: gen_laplace3d(24, leaf_size=27), {}),
+    ("slab-32", lambda: gen_slab(32, 6, leaf_columns=4), {}),
+    ("q1-12", lambda: gen_stokes_q1(12, 10, 5, leaf_columns=2), {}),
+]
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-1, 1e-4])
+@pytest.mark.parametrize("name,gen,kw", CASES, ids=[t[0] for t in CASES])
+def test_factor_apply_pcg_parity(H, handle, name, gen, kw, eps):
+    p = gen()
+    an, fac, a, f, flagged = _both(H, handle, p, eps, kw)
+    _apply_parity(H, f, fac, p.n)
+    xo, ro = opcg(p.to_scipy(), p.b, lambda r: oapply(fac, r), tol=p.tol)
+    xg, rg = H.hs_pcg(f, p.b, tol=p.tol)
+    assert abs(rg["iters"] - ro.iters) <= 1
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+    assert rg["relres_true"] <= 10 * p.tol
+
+
+def test_device_pointers_and_spmv(H, handle):
+    import torch
+    p = gen_poisson2d(32)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, None, leaf_size=16)
+    f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    bt = torch.tensor(p.b, device="cuda", dtype=torch.float64)
+    xt = H.hs_apply(f, bt)
+    xh = H.hs_apply(f, p.b)
+    assert np.array_equal(xt.cpu().numpy(), xh)
+    y = H.hs_spmv(f, p.b)
+    assert np.allclose(y, p.to_scipy() @ p.b, rtol=1e-14, atol=1e-13)
+    xg, rep = H.hs_pcg(f, bt, tol=1e-10)
+    assert rep["converged"] and rep["relres_true"] <= 1e-9
+
+
+def test_not_spd_reports_breakdown(H, handle):
+    p = gen_poisson2d(8, leaf_size=4)
+    vals = p.vals.copy()
+    # make row/col 0 strongly indefinite: diagonal -> -1
+    d0 = p.rowptr[0] + np.searchsorted(p.colind[p.rowptr[0]:p.rowptr[1]], 0)
+    vals[d0] = -1.0
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, None, leaf_size=4, top_log2=1, nsub_log2=1)
+    with pytest.raises(H.HSError) as ei:
+        H.hs_factor_create(handle, a, vals, eps=1e-2)
+    assert ei.value.status == H.HS_E_NOT_SPD
+    assert "level 0" in str(ei.value)
+
+
+def test_empty_leaves_and_tiny(H, handle):
+    # U = 10 DOFs, leaf 1 -> 16 leaves with 6 empty: degenerate clusters stay in the schedule
+    p = gen_poisson2d(5, 2, leaf_size=1)
+    an, fac, a, f, _ = _both(H, handle, p, 1e-2, dict(top_log2=1, nsub_log2=1))
+    _apply_parity(H, f, fac, p.n)
+    an, fac, a, f, _ = _both(H, handle, p, 0.0, dict(top_log2=1, nsub_log2=1))
+    A = p.to_scipy().toarray()
+    assert np.linalg.norm(H.hs_apply(f, p.b) - np.linalg.solve(A, p.b)) <= 1e-12 * np.linalg.norm(np.linalg.solve(A, p.b))
