@@ -19,13 +19,14 @@ import scipy.linalg as sla
 
 PIVOT_WINDOW = 1e-10      # Q4 tie window
 # Decision-fragility flags (reading R-margin).  Two correct implementations
-# differ in a computed trailing norm nu_i(j) by about c*u*nu_max(0) (absolute: Householder
-# rounding accumulates on the scale of the initial block, c*u ~ 1e-14), so a decision is
-# robust only if its distance to the decision boundary, measured in units of nu_max(0),
-# exceeds that.  Flag a cluster when
-#   threshold:  |nu_max(j) - tau_s| < max(1e-10 * tau_s, FLAG_ABS * nu_max(0))
+# differ in a computed trailing norm nu_i(j) by about m*u*kappa(G_s)*nu_max(0): the
+# triangular solve G_s^{-1}A_sw has forward error <= m*u*kappa(G_s) (Higham, Thm 8.5) and the
+# Householder rounding accumulates on the scale of the initial block.  A decision is
+# robust only if its distance to the decision boundary, in units of nu_max(0), exceeds
+# that.  With noise = FLAG_ABS * max(1, kappa(G_s)) (passed by the caller), flag when
+#   threshold:  |nu_max(j) - tau_s| < max(1e-10 * tau_s, noise * nu_max(0))
 #               (the first term is north_star's "within 1e-10 relative of the threshold")
-#   pivot:      |nu_i(j) - (1 - 1e-10) nu_max(j)| < FLAG_ABS * nu_max(0) for some i != argmax
+#   pivot:      |nu_i(j) - (1 - 1e-10) nu_max(j)| < noise * nu_max(0) for some i != argmax
 FLAG_ABS = 1e-13
 
 
@@ -93,7 +94,7 @@ class CPQRResult:
     flagged: bool = False     # a decision lies within rounding distance of its boundary
 
 
-def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRResult:
+def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None, noise: float = FLAG_ABS) -> CPQRResult:
     """Businger-Golub column-pivoted Householder QR directly on B (m x k),
     truncated at the first step whose largest trailing column norm is <= tau_s.
 
@@ -126,7 +127,7 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRR
         if nu0 > 0 and not (tau_s == 0.0 and numax == 0.0):   # exact zeros are not fragile
             dist = abs(numax - tau_s)
             mu = min(mu, dist / nu0)
-            if dist < max(1e-10 * tau_s, FLAG_ABS * nu0):
+            if dist < max(1e-10 * tau_s, noise * nu0):
                 flagged = True
         if inject is not None:
             keep = j < inject[0]
@@ -147,7 +148,7 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None) -> CPQRR
             if others.size:
                 d = float(np.min(np.abs(others - (1.0 - PIVOT_WINDOW) * numax))) / nu0
                 pi = min(pi, d)
-                if d < FLAG_ABS:
+                if d < noise:
                     flagged = True
         v, tau, beta = larfg(W[j:, p])
         act = cols[cols != p]

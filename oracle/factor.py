@@ -29,7 +29,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .analyze import Analysis
-from .dense import chol, tri_solve, cpqr, apply_Qt, NotSPD  # noqa: F401
+from .dense import chol, tri_solve, cpqr, apply_Qt, NotSPD, FLAG_ABS  # noqa: F401
 
 
 @dataclasses.dataclass
@@ -140,7 +140,8 @@ def eliminate(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, injec
         tau_s = 0.0
         flagged = False
     else:
-        res = cpqr(Bw, eps, relative, inject)              # step 4
+        kappa = float(np.linalg.cond(G)) if m > 0 else 1.0
+        res = cpqr(Bw, eps, relative, inject, noise=FLAG_ABS * max(1.0, kappa))   # step 4
         r, V, tau, piv, W = res.r, res.V[:, :res.r], res.tau[:res.r], res.piv[:res.r], res.W
         mu, pi, tau_s, flagged = res.mu, res.pi, res.tau_s, res.flagged
     Bt = apply_Qt(V, tau, Bn)                              # step 5: U^T G^{-1} A_sn
