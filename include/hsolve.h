@@ -173,6 +173,17 @@ hs_status hs_factor_create(hs_handle h, hs_analysis a, const double* values,
 hs_status hs_factor_get_stats(hs_factor f, hs_factor_stats_t* st);
 hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out,
                            int64_t cap, int64_t* len);
+/* Debug/parity aid: the elimination record of one cluster (doubles, row-major):
+ *   HS_CEXP_SHAPE [5]        m, r, kw, kn, ldB
+ *   HS_CEXP_G     [m*m]      G_s (lower)
+ *   HS_CEXP_V     [r*m]      Householder vectors v_0..v_{r-1} (each m long, zeros above j)
+ *   HS_CEXP_TAU   [r]
+ *   HS_CEXP_B     [m*ldB]    B_s after the elimination: columns [0,kw) = w part, [kw,kw+kn) =
+ *                            n part; rows [0,r) = coarse rows, rows [r,m) of the n part = C.
+ * Copies from the device; same length-query convention as hs_analysis_export. */
+enum { HS_CEXP_SHAPE = 0, HS_CEXP_G = 1, HS_CEXP_V = 2, HS_CEXP_TAU = 3, HS_CEXP_B = 4 };
+hs_status hs_factor_export_cluster(hs_factor f, int32_t key, int32_t level, int32_t cluster,
+                                   double* out, int64_t cap, int64_t* len);
 void      hs_factor_destroy(hs_factor f);
 
 /* ---- solve (device) --------------------------------------------------------------- */

@@ -28,6 +28,12 @@ PIVOT_WINDOW = 1e-10      # Q4 tie window
 #               (the first term is north_star's "within 1e-10 relative of the threshold")
 #   pivot:      |nu_i(j) - (1 - 1e-10) nu_max(j)| < noise * nu_max(0) for some i != argmax
 FLAG_ABS = 1e-13
+# Noise floor (reading R-floor): for eps > 0 in relative mode,
+#   tau_s = max(eps * nu_max(B_w), NOISE_FLOOR * max(nu_max(B_w), nu_max(B_n))).
+# A w-block that is zero in exact arithmetic (cancelling fill) holds rounding noise of
+# ~1e-15 of the row's scale; a purely relative eps would "compress" that noise and take
+# decisions on it.  Columns below 1e-12 of the cluster's scaled row are numerically zero.
+NOISE_FLOOR = 1e-12
 
 
 class NotSPD(Exception):
@@ -94,7 +100,8 @@ class CPQRResult:
     flagged: bool = False     # a decision lies within rounding distance of its boundary
 
 
-def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None, noise: float = FLAG_ABS) -> CPQRResult:
+def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None, noise: float = FLAG_ABS,
+         row_scale: float = 0.0) -> CPQRResult:
     """Businger-Golub column-pivoted Householder QR directly on B (m x k),
     truncated at the first step whose largest trailing column norm is <= tau_s.
 
@@ -122,6 +129,8 @@ def cpqr(B: np.ndarray, eps: float, relative: bool = True, inject=None, noise: f
         numax = float(nu.max())
         if j == 0:
             tau_s = eps * numax if relative else eps
+            if relative and eps > 0:
+                tau_s = max(tau_s, NOISE_FLOOR * max(numax, row_scale))
             nu0 = numax
         numaxes.append(numax)
         if nu0 > 0 and not (tau_s == 0.0 and numax == 0.0):   # exact zeros are not fragile

@@ -141,7 +141,8 @@ def eliminate(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, injec
         flagged = False
     else:
         kappa = float(np.linalg.cond(G)) if m > 0 else 1.0
-        res = cpqr(Bw, eps, relative, inject, noise=FLAG_ABS * max(1.0, kappa))   # step 4
+        row_scale = float(np.sqrt(np.sum(Bn ** 2, axis=0)).max()) if Bn.shape[1] else 0.0
+        res = cpqr(Bw, eps, relative, inject, noise=FLAG_ABS * max(1.0, kappa), row_scale=row_scale)   # step 4
         r, V, tau, piv, W = res.r, res.V[:, :res.r], res.tau[:res.r], res.piv[:res.r], res.W
         mu, pi, tau_s, flagged = res.mu, res.pi, res.tau_s, res.flagged
     Bt = apply_Qt(V, tau, Bn)                              # step 5: U^T G^{-1} A_sn

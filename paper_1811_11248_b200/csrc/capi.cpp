@@ -243,6 +243,37 @@ hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out
   });
 }
 
+hs_status hs_factor_export_cluster(hs_factor f, int32_t key, int32_t level, int32_t cluster, double* out,
+                                   int64_t cap, int64_t* len) {
+  return guarded(f ? f->h : nullptr, [&] {
+    if (!f) hs::fail(HS_E_INVALID_ARG, "hs_factor_export_cluster: NULL factor");
+    if (level < 0 || level >= (int)f->lv.size()) hs::fail(HS_E_INVALID_ARG, "hs_factor_export_cluster: bad level");
+    const hs::LevelRT& L = f->lv[level];
+    if (cluster < 0 || cluster >= L.nclus) hs::fail(HS_E_INVALID_ARG, "hs_factor_export_cluster: bad cluster");
+    const int64_t m = L.cap[cluster], r = L.rank[cluster];
+    std::vector<double> v;
+    auto dev = [&](const double* p, int64_t cnt) {
+      v.resize(cnt);
+      if (cnt) HS_CUDA(cudaMemcpy(v.data(), p, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    };
+    require_device(f->h);
+    HS_CUDA(cudaStreamSynchronize(f->h->stream));
+    switch (key) {
+      case HS_CEXP_SHAPE:
+        v = {(double)m, (double)r, (double)L.kw[cluster], (double)L.kn[cluster], (double)L.ldB[cluster]};
+        break;
+      case HS_CEXP_G: dev(L.G[cluster], m * m); break;
+      case HS_CEXP_V: dev(L.V[cluster], r * m); break;
+      case HS_CEXP_TAU: dev(L.tau[cluster], r); break;
+      case HS_CEXP_B: dev(L.B[cluster], m * L.ldB[cluster]); break;
+      default: hs::fail(HS_E_INVALID_ARG, "hs_factor_export_cluster: bad key");
+    }
+    if (len) *len = (int64_t)v.size();
+    if (out)
+      for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); ++i) out[i] = v[i];
+  });
+}
+
 void hs_factor_destroy(hs_factor f) {
   if (!f) return;
   cudaSetDevice(f->h->device);

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <unordered_map>
@@ -484,6 +486,25 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
       launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
       launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
       S.n_batches++;
+      if (const char* dd = std::getenv("HS_DEBUG_DUMP")) {   // debug aid: block store after every batch
+        HS_CUDA(cudaStreamSynchronize(st));
+        char path[512];
+        std::snprintf(path, sizeof path, "%s/l%d_b%d.bin", dd, l, (int)ap.batches[l].size() - 1);
+        FILE* fp = std::fopen(path, "wb");
+        if (fp) {
+          std::vector<double> host(bs.total);
+          if (bs.total) HS_CUDA(cudaMemcpy(host.data(), bs.d, bs.total * sizeof(double), cudaMemcpyDeviceToHost));
+          for (int p = 0; p < lev.nclus; ++p)
+            for (const auto& qo : bs.rows[p]) {
+              const int32_t q = qo.first;
+              int32_t hdr[4] = {p, q, live[p], live[q]};
+              std::fwrite(hdr, sizeof hdr, 1, fp);
+              for (int i = 0; i < live[p]; ++i)
+                std::fwrite(host.data() + qo.second + (int64_t)i * cap[q], sizeof(double), live[q], fp);
+            }
+          std::fclose(fp);
+        }
+      }
     }
     // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] -----------------
     const double tp2 = now_s();

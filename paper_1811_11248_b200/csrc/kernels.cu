@@ -242,6 +242,17 @@ __global__ void __launch_bounds__(CPQR_THREADS) k_cpqr(const CluItem* __restrict
     }
     nu[i] = sqrt(s);
   }
+  // scale of the n part (noise floor of tau_s, reading R-floor)
+  double lmax_n = 0.0;
+  for (int i = kw + threadIdx.x; i < ncol; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double b = B[(int64_t)l * ld + i];
+      s += b * b;
+    }
+    lmax_n = fmax(lmax_n, sqrt(s));
+  }
+  const double row_n = block_max(lmax_n, red);
   __syncthreads();
   const int kmax = min(m, kw);
   double tau_s = 0.0;
@@ -250,7 +261,10 @@ __global__ void __launch_bounds__(CPQR_THREADS) k_cpqr(const CluItem* __restrict
     double lmax = -1.0;
     for (int i = threadIdx.x; i < kw; i += blockDim.x) lmax = fmax(lmax, nu[i]);
     const double numax = block_max(lmax, red);
-    if (j == 0) tau_s = relative ? eps * numax : eps;
+    if (j == 0) {
+      tau_s = relative ? eps * numax : eps;
+      if (relative && eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(numax, row_n));   // noise floor
+    }
     if (!(numax > tau_s)) { r = j; break; }        // strict keep rule
     const double thr = (1.0 - 1e-10) * numax;
     int lmin = INT_MAX;

@@ -32,7 +32,9 @@ HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(
 # every symbol include/hsolve.h declares
 SYMBOLS = ["hs_create", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
            "hs_analysis_get_info", "hs_analysis_export", "hs_analysis_destroy", "hs_factor_create",
-           "hs_factor_get_stats", "hs_factor_export", "hs_factor_destroy", "hs_apply", "hs_pcg", "hs_spmv"]
+           "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
+           "hs_pcg", "hs_spmv"]
+HS_CEXP_SHAPE, HS_CEXP_G, HS_CEXP_V, HS_CEXP_TAU, HS_CEXP_B = range(5)
 
 
 class HSError(RuntimeError):
@@ -103,6 +105,7 @@ def lib():
         L.hs_factor_create.argtypes = [vp, vp, vp, C.POINTER(hs_factor_opts), C.POINTER(vp)]
         L.hs_factor_get_stats.argtypes = [vp, C.POINTER(hs_factor_stats_t)]
         L.hs_factor_export.argtypes = [vp, i32, i32, vp, i64, C.POINTER(i64)]
+        L.hs_factor_export_cluster.argtypes = [vp, i32, i32, i32, vp, i64, C.POINTER(i64)]
         L.hs_factor_destroy.argtypes = [vp]
         L.hs_factor_destroy.restype = None
         L.hs_apply.argtypes = [vp, vp, vp, i32]
@@ -229,6 +232,25 @@ def hs_factor_export(f: Factor, key: int, level: int = 0) -> np.ndarray:
     out = np.zeros(max(n.value, 1), dtype=np.int64)
     _check(lib().hs_factor_export(f.ptr, key, level, out.ctypes.data, n.value, C.byref(n)), f.handle.ptr)
     return out[:n.value]
+
+
+def hs_factor_export_cluster(f: Factor, key: int, level: int, cluster: int) -> np.ndarray:
+    n = C.c_int64()
+    _check(lib().hs_factor_export_cluster(f.ptr, key, level, cluster, None, 0, C.byref(n)), f.handle.ptr)
+    out = np.zeros(max(n.value, 1), dtype=np.float64)
+    _check(lib().hs_factor_export_cluster(f.ptr, key, level, cluster, out.ctypes.data, n.value, C.byref(n)),
+           f.handle.ptr)
+    return out[:n.value]
+
+
+def cluster_record(f: Factor, level: int, cluster: int) -> dict:
+    """G, V, tau, B of one eliminated cluster (debug / per-cluster parity aid)."""
+    m, r, kw, kn, ldB = (int(x) for x in hs_factor_export_cluster(f, HS_CEXP_SHAPE, level, cluster))
+    return {"m": m, "r": r, "kw": kw, "kn": kn,
+            "G": hs_factor_export_cluster(f, HS_CEXP_G, level, cluster).reshape(m, m),
+            "V": hs_factor_export_cluster(f, HS_CEXP_V, level, cluster).reshape(r, m).T,
+            "tau": hs_factor_export_cluster(f, HS_CEXP_TAU, level, cluster),
+            "B": hs_factor_export_cluster(f, HS_CEXP_B, level, cluster).reshape(m, ldB)}
 
 
 def hs_apply(f: Factor, b, x=None):
