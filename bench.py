@@ -1,0 +1,296 @@
+"""Benchmark of the deferred-compression LoRaSp hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+A step = one pass of the whole hot path on one synthetic system: hs_factor (Algorithm 1:
+POTRF, deferred-compression TRSM, CPQR to eps, Schur updates, top Cholesky) followed by
+hs_pcg (CSR SpMV + the Algorithm-2 apply) to the config's tolerance.  The default workload
+is BASELINE.json configs[1] (C2: 3-D 64^3 Laplacian, k = exp(GRF), leaf 64, eps 1e-2,
+PCG to 1e-8), the config the metric is quoted on; inputs (CSR values, b) are resident in
+HBM when the timed region starts and the analysis (pattern only) is done once before it.
+value = DOF/s = N * K / (device time of the K steps); e2e repeats the step through the
+same C API with HOST buffers (values and b uploaded, x downloaded inside the timed region).
+N > 1: one process per GPU, each running its own full replica (weak scaling, no
+data-path collective: the subdomain-sharded factor is not built yet).
+--impl reference times the CPU oracle (oracle/) on the host cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factor+PCG DOF/s at 1/2/4/8 B200; FP64 TFLOP/s frac of peak; PCG iters"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    fp = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+    f64 = json.load(open(fp)) if os.path.exists(fp) else {}
+    return mp, f64
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.path = f"/tmp/hs_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        load = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample_run(nc: int):
+    """The oracle as it stands, one thread, on a bounded sample of the C2 family."""
+    from threadpoolctl import threadpool_limits
+    from problems import gen_laplace3d
+    from oracle.analyze import analyze_problem
+    from oracle.factor import factor
+    from oracle.solve import apply, pcg
+    with threadpool_limits(1):
+        p = gen_laplace3d(nc)
+        an = analyze_problem(p)
+        t0 = time.perf_counter()
+        f = factor(an, p.rowptr, p.colind, p.vals, eps=p.eps)
+        x, rep = pcg(p.to_scipy(), p.b, lambda r: apply(f, r), tol=p.tol)
+        t = time.perf_counter() - t0
+    return p.n, t, rep.iters
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    nc = 24 if args.steps + args.warmup > 4 else 32
+    for _ in range(args.warmup):
+        cpu_sample_run(nc)
+    tot, n, its = 0.0, 0, 0
+    for _ in range(args.steps):
+        n, t, its = cpu_sample_run(nc)
+        tot += t
+    value = n * args.steps / tot
+    sample = (f"C2 family (3-D Laplacian, k=exp(GRF sigma 1, ell 8), leaf 64, eps 1e-2, PCG 1e-8) at {nc}^3 = "
+              f"{n} DOFs per step (C2 is 64^3 = 262144; the full C2 oracle factor takes ~300 s)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 sample: " + sample, "pcg_iters": its},
+            "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1811_11248_b200 import hsolve as H
+    from problems import gen_config
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = gen_config(args.config)
+    if args.eps is not None:
+        p.eps = args.eps
+    h = H.hs_create(local)
+    stream = torch.cuda.current_stream()
+    H.hs_set_stream(h, stream.cuda_stream)
+    t0 = time.perf_counter()
+    a = H.hs_analyze(h, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+    t_analyze = time.perf_counter() - t0
+    vals = torch.tensor(p.vals, dtype=torch.float64, device="cuda")
+    b = torch.tensor(p.b, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(b)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        f = H.hs_factor_create(h, a, vals, eps=p.eps)
+        xx, rep = H.hs_pcg(f, b, tol=p.tol, x=x)
+        return f, rep
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    l0 = H.hs_launch_count()
+    tot_ms = 0.0
+    stats, reps = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f, rep = step()
+        e1.record(stream)
+        e1.synchronize()
+        tot_ms += e0.elapsed_time(e1)
+        stats.append(H.hs_factor_get_stats(f))
+        reps.append(rep)
+        del f
+    barrier()
+    launches = H.hs_launch_count() - l0
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * p.n * args.steps / (tot_ms * 1e-3)
+    # ---- e2e through the C API with host buffers -------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        hv = np.ascontiguousarray(p.vals)
+        hb = np.ascontiguousarray(p.b)
+        hx = np.empty_like(hb)
+        H.hs_pcg(H.hs_factor_create(h, a, hv, eps=p.eps), hb, tol=p.tol, x=hx)
+        e2e_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            f = H.hs_factor_create(h, a, hv, eps=p.eps)
+            H.hs_pcg(f, hb, tol=p.tol, x=hx)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+            del f
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": world * p.n * args.steps / (e2e_ms * 1e-3), "unit": "DOF/s",
+               "h2d_bytes_per_step": int(p.vals.nbytes + p.b.nbytes), "d2h_bytes_per_step": int(hx.nbytes)}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    # ---- roofline of the dominant kernel class -----------------------------------------------
+    mp, f64 = peaks()
+    names = ["gather", "potrf", "trsm", "cpqr", "schur", "writeback", "top"]
+    t_ph = np.sum([s["t_phase_s"][:7] for s in stats], axis=0)
+    fl_ph = np.sum([s["flops_phase"][:7] for s in stats], axis=0)
+    t_pcg = sum(r["t_pcg_s"] for r in reps)
+    t_apply = sum(r["t_apply_s"] for r in reps)
+    dom = int(np.argmax(t_ph))
+    alu_peak = f64.get("dfma_tflops")
+    dmma_peak = f64.get("dmma_tflops") or f64.get("dgemm_tflops")
+    if names[dom] in ("potrf", "trsm", "cpqr", "schur", "top"):
+        achieved = fl_ph[dom] / t_ph[dom] / 1e12
+        peak = alu_peak if alu_peak else None
+        roof = {"bound": "alu", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if peak else None, "traffic": None,
+                "peak_source": "profiles/fp64_peaks.json dfma_tflops (FFMA.F64 chain, measured on this pool's B200)"
+                if peak else "FP64 peak not measured yet"}
+    else:
+        # byte-bound copy kernels: algorithmic bytes are not accounted per phase yet
+        roof = {"bound": "hbm", "kernel": names[dom], "achieved": None, "peak": mp.get("hbm_gbs"), "unit": "GB/s",
+                "frac": None, "traffic": None}
+    S = stats[-1]
+    factor_flops = float(np.mean([s["flops"] for s in stats]))
+    t_fac = float(np.mean([s["t_factor_s"] for s in stats]))
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        n_s, t_s, it_s = cpu_sample_run(32)
+        cpu = {"value": n_s / t_s, "unit": "DOF/s", "cores": 1, "kind": "oracle",
+               "sample": f"C2 family at 32^3 = {n_s} DOFs (1/8 of C2), same generator/leaf/eps/tol, factor+PCG "
+                         f"({it_s} iterations) in {t_s:.1f} s on 1 host thread"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {p.name}, N={p.n}, nnz={p.nnz}, eps={p.eps}, pcg_tol={p.tol}, "
+                               f"leaf={p.leaf_size or p.leaf_columns}",
+                   "l2": "256 MB buffer written between timed steps (and the factor working set > L2)",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "pcg_iters": [r["iters"] for r in reps], "relres_true": reps[-1]["relres_true"],
+                   "t_analyze_s": t_analyze, "t_factor_s": t_fac, "t_pcg_s": t_pcg / args.steps,
+                   "t_apply_s_per_step": t_apply / args.steps,
+                   "factor_tflops": factor_flops / t_fac / 1e12,
+                   "factor_gflop": factor_flops / 1e9, "factor_gb": S["factor_bytes"] / 1e9,
+                   "phase_s_per_step": {nm: float(t_ph[i] / args.steps) for i, nm in enumerate(names)},
+                   "host_planning_s_per_step": float(np.mean([s["t_phase_s"][7] for s in stats])),
+                   "batches": S["n_batches"], "levels": S["n_levels"], "n_top": S["n_top"],
+                   "max_m": S["max_m"], "max_rank": S["max_rank"]},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -80,6 +80,8 @@ typedef struct {
   double  eps;           /* truncation tolerance, >= 0                 */
   int32_t eps_relative;  /* 1: tau_s = eps * max column norm of G^{-1}A_sw (reading Q1); 0: absolute */
   int32_t dc;            /* 1: deferred compression (the paper's method); 0 is not supported yet */
+  int32_t values_on_device; /* 1: `values` is a device pointer on the handle's device          */
+  int32_t reserved;
 } hs_factor_opts;
 
 typedef struct {
@@ -166,8 +168,12 @@ hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t*
 void      hs_analysis_destroy(hs_analysis a);
 
 /* ---- factor (device) -------------------------------------------------------------- */
-/* values: CSR values (host) on the pattern given to hs_analyze.  On HS_E_NOT_SPD no
- * factor is created and hs_last_error names (level, cluster, pivot, value). */
+/* values: CSR values on the pattern given to hs_analyze (host pointer, or device pointer
+ * when opt->values_on_device).  The analysis must outlive every factor made from it: the
+ * first factor caches the pattern and its level-0 scatter map on the device inside the
+ * analysis, so re-factoring new values on the same pattern (Newton / continuation
+ * sequences) uploads only the values.  On HS_E_NOT_SPD no factor is created and
+ * hs_last_error names (level, cluster, pivot, value). */
 hs_status hs_factor_create(hs_handle h, hs_analysis a, const double* values,
                            const hs_factor_opts* opt, hs_factor* out);
 hs_status hs_factor_get_stats(hs_factor f, hs_factor_stats_t* st);
@@ -196,6 +202,10 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
                  int32_t on_device, hs_pcg_report* rep);
 /* y = A x with the factor's CSR (device SpMV); helper for tests and the bench. */
 hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device);
+
+/* Number of kernels this process has launched through the library so far (every node
+ * of a replayed CUDA graph counts).  Evidence for the bench's gpu_launches. */
+int64_t hs_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -186,6 +186,12 @@ hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t*
 
 void hs_analysis_destroy(hs_analysis a) {
   if (!a) return;
+  if (a->an && a->an->dev >= 0) {
+    cudaSetDevice(a->an->dev);
+    for (void* p : {(void*)a->an->d_rowptr, (void*)a->an->d_colind, (void*)a->an->d_perm, (void*)a->an->d_map,
+                    (void*)a->an->d_tmap})
+      if (p) cudaFree(p);
+  }
   delete a->an;
   delete a;
 }
@@ -317,6 +323,8 @@ hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device) {
     HS_CUDA(cudaStreamSynchronize(st));
   });
 }
+
+int64_t hs_launch_count(void) { return hs::launch_count(); }
 
 hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t maxit, int32_t on_device,
                  hs_pcg_report* rep) {

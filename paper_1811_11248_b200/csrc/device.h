@@ -56,6 +56,30 @@ struct SchurContrib {
   int32_t ldC, K, colP, colQ;
 };
 
+// Schur update v2 (a5), one source cluster per tile, device-side target lookup:
+// the tile (i0, j0) of X = C^T C (C = K x kn, the n-part of the fine rows) is computed
+// densely and each element subtracted from its target block A(q_a, q_b) (q_a >= q_b).
+// Diagonal blocks keep LOWER-triangle semantics (only li >= lj is maintained).
+// Sources of one launch ("wave") never share a neighbour, so no two tiles of a launch
+// touch the same target element (deterministic, no atomics).
+struct SchurSrc {
+  const double* C;           // fine rows of the n-part, ld ldC
+  int32_t ldC, K, kn, nb_off, nnb, pad;
+};
+struct SchurTile2 {
+  int32_t src, i0, j0, pad;
+};
+struct NbCol {               // neighbour q occupies columns [col, col+len) of the n-part
+  int32_t q, col, len, pad;
+};
+struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
+  double* blk;
+  const int64_t* ptr;
+  const int32_t* q;
+  const int64_t* off;
+  const int32_t* cap;
+};
+
 // Apply (Algorithm 2) items.
 struct ApplyLocal {          // forward: y_s <- U^T G^{-1} y_s ; backward: x_f -= sum C x_q, x_s <- G^{-T} U x_s
   const double* G;
@@ -85,7 +109,13 @@ struct DevStatus {
   double value;
 };
 
+// ---- launch accounting (every launcher counts its kernels; graphs count their nodes) -----
+void count_launch(int64_t n);
+int64_t launch_count();
+
 // ---- kernel launchers (kernels.cu / solve_kernels.cu) -------------------------------------
+// values symmetry: *flag = 1 if |v[k] - v[tmap[k]]| > 1e-12 max(|v[k]|, |v[tmap[k]]|) for some k
+void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32_t* flag, cudaStream_t st);
 void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st);
 void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d_r, int n, cudaStream_t st);
 void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st);
@@ -93,6 +123,8 @@ void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, c
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st);
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
+void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
+                   cudaStream_t st);
 // Dense blocked Cholesky of the top matrix (row-major, ld).  On return the
 // diagonal NB x NB blocks hold G_kk (lower) and the block rows right of them hold
 // U_kj = G_kk^{-1} A_kj (i.e. L^T); the strictly lower off-diagonal blocks are stale.
@@ -102,7 +134,7 @@ constexpr int TOP_NB = 64;
 
 void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st);
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, cudaStream_t st);
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

@@ -81,6 +81,10 @@ struct BlockStore {
   size_t total = 0;
 
   void build(const std::vector<int32_t>& caps, const Adj& edges) {
+    layout(caps, edges);
+    if (total) HS_CUDA(cudaMalloc(&d, total * sizeof(double)));
+  }
+  void layout(const std::vector<int32_t>& caps, const Adj& edges) {
     cap = caps;
     const int n = (int)caps.size();
     rows.assign(n, {});
@@ -95,7 +99,6 @@ struct BlockStore {
       off += (int64_t)caps[p] * caps[p];
     }
     total = (size_t)off;
-    if (total) HS_CUDA(cudaMalloc(&d, total * sizeof(double)));
   }
   int64_t off(int32_t p, int32_t q) const {   // p >= q
     const auto& r = rows[p];
@@ -120,9 +123,76 @@ struct BlockStore {
       trans = 1;
     }
   }
+  // device copy of the directory for the Schur kernel's target lookup
+  int64_t* d_ptr = nullptr;
+  int32_t* d_q = nullptr;
+  int64_t* d_off = nullptr;
+  int32_t* d_cap = nullptr;
+  void upload_dir(cudaStream_t st) {
+    const int n = (int)cap.size();
+    std::vector<int64_t> ptr(n + 1, 0), off;
+    std::vector<int32_t> qq;
+    for (int p = 0; p < n; ++p) {
+      for (const auto& e : rows[p]) {
+        qq.push_back(e.first);
+        off.push_back(e.second);
+      }
+      ptr[p + 1] = (int64_t)qq.size();
+    }
+    HS_CUDA(cudaMalloc(&d_ptr, sizeof(int64_t) * (n + 1)));
+    HS_CUDA(cudaMalloc(&d_q, sizeof(int32_t) * std::max<size_t>(qq.size(), 1)));
+    HS_CUDA(cudaMalloc(&d_off, sizeof(int64_t) * std::max<size_t>(off.size(), 1)));
+    HS_CUDA(cudaMalloc(&d_cap, sizeof(int32_t) * std::max(n, 1)));
+    HS_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d_q, qq.data(), sizeof(int32_t) * qq.size(), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d_cap, cap.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaStreamSynchronize(st));   // host vectors go out of scope
+  }
+  BlockDir dir() const { return BlockDir{d, d_ptr, d_q, d_off, d_cap}; }
   void release() {
-    if (d) cudaFree(d);
+    for (void* p : {(void*)d, (void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
+      if (p) cudaFree(p);
+    forget();
+  }
+  void forget() {
     d = nullptr;
+    d_ptr = nullptr;
+    d_q = nullptr;
+    d_off = nullptr;
+    d_cap = nullptr;
+  }
+};
+
+// Per-kernel-class device time (CUDA events on the library stream), collected at the
+// batch's rank read-back, which already synchronises: a = [gather|potrf|trsm|cpqr],
+// b = [schur|write-back] of the previous batch.
+struct PhaseTimer {
+  cudaEvent_t a[5], b[3];
+  bool b_pending = false;
+  PhaseTimer() {
+    for (auto& e : a) HS_CUDA(cudaEventCreate(&e));
+    for (auto& e : b) HS_CUDA(cudaEventCreate(&e));
+  }
+  ~PhaseTimer() {
+    for (auto& e : a) cudaEventDestroy(e);
+    for (auto& e : b) cudaEventDestroy(e);
+  }
+  static double el(cudaEvent_t x, cudaEvent_t y) {
+    float ms = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&ms, x, y));
+    return ms * 1e-3;
+  }
+  void collect_b(hs_factor_stats_t& S) {
+    if (!b_pending) return;
+    HS_CUDA(cudaEventSynchronize(b[2]));
+    S.t_phase_s[4] += el(b[0], b[1]);
+    S.t_phase_s[5] += el(b[1], b[2]);
+    b_pending = false;
+  }
+  void collect(hs_factor_stats_t& S) {   // after a synchronising point
+    for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
+    collect_b(S);
   }
 };
 
@@ -149,7 +219,7 @@ hs_factor_s::~hs_factor_s() {
   auto fr = [](void* p) {
     if (p) cudaFree(p);
   };
-  fr(d_rowptr); fr(d_colind); fr(d_vals); fr(d_perm); fr(d_top);
+  fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
   fr(ap.d_local); fr(ap.d_nb); fr(ap.d_tgt); fr(ap.d_con); fr(ap.d_y);
   for (auto* p : ap.d_tsrc) fr(p);
@@ -161,48 +231,86 @@ hs_factor_s::~hs_factor_s() {
 
 namespace hs {
 
-hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* values, const hs_factor_opts& opt) {
-  if (opt.eps < 0 || !std::isfinite(opt.eps)) fail(HS_E_INVALID_ARG, "factor: eps must be finite and >= 0");
-  if (opt.dc != 1) fail(HS_E_UNSUPPORTED, "factor: only dc = 1 (deferred compression) is implemented");
+// Pattern-only device data, computed once per analysis and cached in it: the CSR pattern,
+// the permutation, the map of every CSR entry into the level-0 block store and the
+// transpose map used by the on-device symmetry check.
+static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st) {
+  if (an->dev == device && an->d_map) return;
+  if (an->dev >= 0 && an->dev != device) fail(HS_E_INVALID_ARG, "factor: analysis already bound to another device");
   const int64_t n = an->n, nnz = an->rowptr[n];
-  // numerical symmetry of the values (A SPD, A_ns = A_sn^T)
-  for (int64_t i = 0; i < n; ++i)
+  const int nleaf0 = (int)(an->leaf_off.size() - 1);
+  std::vector<int32_t> cap(nleaf0);
+  for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
+  BlockStore layout;
+  layout.layout(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top);
+  std::vector<int32_t> leaf_of(n);
+  for (int c = 0; c < nleaf0; ++c)
+    for (int64_t k = an->leaf_off[c]; k < an->leaf_off[c + 1]; ++k) leaf_of[k] = c;
+  std::vector<int64_t> map(nnz, -1), tmap(nnz);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t pi = an->iperm[i];
+    const int32_t p = leaf_of[pi];
     for (int64_t k = an->rowptr[i]; k < an->rowptr[i + 1]; ++k) {
       const int64_t j = an->colind[k];
-      if (j <= i) continue;
       const int32_t* b = an->colind.data() + an->rowptr[j];
       const int32_t* e = an->colind.data() + an->rowptr[j + 1];
-      const int64_t kk = an->rowptr[j] + (std::lower_bound(b, e, (int32_t)i) - b);
-      const double a = values[k], t = values[kk];
-      if (std::fabs(a - t) > 1e-12 * std::max(std::fabs(a), std::fabs(t)))
-        fail(HS_E_NOT_SYMMETRIC, "factor: values are not symmetric");
+      tmap[k] = an->rowptr[j] + (std::lower_bound(b, e, (int32_t)i) - b);
+      const int64_t pj = an->iperm[j];
+      const int32_t q = leaf_of[pj];
+      if (p < q) continue;
+      const int64_t o = layout.off(p, q);
+      if (o < 0) fail(HS_E_INTERNAL, "factor: level-0 block missing");
+      map[k] = o + (pi - an->leaf_off[p]) * cap[q] + (pj - an->leaf_off[q]);
     }
+  }
+  HS_CUDA(cudaMalloc(&an->d_rowptr, sizeof(int64_t) * (n + 1)));
+  HS_CUDA(cudaMalloc(&an->d_colind, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  HS_CUDA(cudaMalloc(&an->d_perm, sizeof(int64_t) * n));
+  HS_CUDA(cudaMalloc(&an->d_map, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+  HS_CUDA(cudaMalloc(&an->d_tmap, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+  HS_CUDA(cudaMemcpyAsync(an->d_rowptr, an->rowptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaMemcpyAsync(an->d_colind, an->colind.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaMemcpyAsync(an->d_perm, an->perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaMemcpyAsync(an->d_map, map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaMemcpyAsync(an->d_tmap, tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  an->dev = device;
+}
+
+hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* values, const hs_factor_opts& opt) {
+  if (opt.eps < 0 || !std::isfinite(opt.eps)) fail(HS_E_INVALID_ARG, "factor: eps must be finite and >= 0");
+  if (opt.dc != 1) fail(HS_E_UNSUPPORTED, "factor: only dc = 1 (deferred compression) is implemented");
+  Analysis* an = const_cast<Analysis*>(an_c);   // the device pattern cache lives in the analysis
+  const int64_t n = an->n, nnz = an->rowptr[n];
   cudaStream_t st = h->stream;
+  ensure_device_pattern(an, h->device, st);
   auto* f = new hs_factor_s();
   std::unique_ptr<hs_factor_s> guard(f);
   f->h = h;
   f->an = an;
   f->opt = opt;
-  const double t_wall0 = now_s();
   double t_plan = 0.0;
   cudaEvent_t ev0, ev1;
   HS_CUDA(cudaEventCreate(&ev0));
   HS_CUDA(cudaEventCreate(&ev1));
   HS_CUDA(cudaEventRecord(ev0, st));
-
-  HS_CUDA(cudaMalloc(&f->d_rowptr, sizeof(int64_t) * (n + 1)));
-  HS_CUDA(cudaMalloc(&f->d_colind, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  f->d_rowptr = an->d_rowptr;      // borrowed from the analysis
+  f->d_colind = an->d_colind;
+  f->d_perm = an->d_perm;
   HS_CUDA(cudaMalloc(&f->d_vals, sizeof(double) * std::max<int64_t>(nnz, 1)));
-  HS_CUDA(cudaMalloc(&f->d_perm, sizeof(int64_t) * n));
-  HS_CUDA(cudaMemcpyAsync(f->d_rowptr, an->rowptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-  HS_CUDA(cudaMemcpyAsync(f->d_colind, an->colind.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
-  HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
-  HS_CUDA(cudaMemcpyAsync(f->d_perm, an->perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz,
+                          opt.values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
 
   DevStatus* d_status = nullptr;
   DevStatus h_status{};
   HS_CUDA(cudaMalloc(&d_status, sizeof(DevStatus)));
   std::unique_ptr<void, void (*)(void*)> status_guard(d_status, [](void* p) { cudaFree(p); });
+  HS_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), st));
+  // numerical symmetry of the values (A SPD, A_ns = A_sn^T), checked on the device
+  launch_symcheck(f->d_vals, an->d_tmap, nnz, &d_status->pivot, st);
+  HS_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  if (h_status.pivot) fail(HS_E_NOT_SYMMETRIC, "factor: values are not symmetric");
   HS_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), st));
 
   // ---- level-0 blocks from the permuted CSR ------------------------------------------------
@@ -212,30 +320,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
   BlockStore bs;
   bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top);
   if (bs.total) HS_CUDA(cudaMemsetAsync(bs.d, 0, bs.total * sizeof(double), st));
-  {
-    std::vector<int32_t> leaf_of(n);
-    for (int c = 0; c < nleaf0; ++c)
-      for (int64_t k = an->leaf_off[c]; k < an->leaf_off[c + 1]; ++k) leaf_of[k] = c;
-    std::vector<int64_t> map(nnz, -1);
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t pi = an->iperm[i];
-      const int32_t p = leaf_of[pi];
-      for (int64_t k = an->rowptr[i]; k < an->rowptr[i + 1]; ++k) {
-        const int64_t pj = an->iperm[an->colind[k]];
-        const int32_t q = leaf_of[pj];
-        if (p < q) continue;
-        const int64_t o = bs.off(p, q);
-        if (o < 0) fail(HS_E_INTERNAL, "factor: level-0 block missing");
-        map[k] = o + (pi - an->leaf_off[p]) * cap[q] + (pj - an->leaf_off[q]);
-      }
-    }
-    int64_t* d_map = nullptr;
-    HS_CUDA(cudaMalloc(&d_map, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
-    HS_CUDA(cudaMemcpyAsync(d_map, map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-    launch_scatter(f->d_vals, d_map, nnz, bs.d, st);
-    HS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_map);
-  }
+  launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
+  if (an->L_top > 0) bs.upload_dir(st);
 
   Upload upA, upB;
   int32_t* d_rank = nullptr;
@@ -249,6 +335,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
   std::unique_ptr<void, void (*)(void*)> hrank_guard(h_rank, [](void* p) { cudaFreeHost(p); });
 
   hs_factor_stats_t& S = f->stats;
+  PhaseTimer pt;
   ApplyPlan& ap = f->ap;
   int64_t vbase = 0;
   f->lv.resize(an->L_top);
@@ -256,9 +343,13 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
   ap.trans_src.resize(an->L_top);
   ap.trans_dst.resize(an->L_top);
 
+  const bool prof = std::getenv("HS_PROFILE") != nullptr;
   for (int l = 0; l < an->L_top; ++l) {
     const Level& lev = an->levels[l];
     LevelRT& L = f->lv[l];
+    const double lv_t0 = now_s(), lv_plan0 = t_plan;
+    double lv_ph0[8];
+    std::memcpy(lv_ph0, S.t_phase_s, sizeof lv_ph0);
     L.nclus = lev.nclus;
     L.cap = cap;
     L.rank.assign(lev.nclus, 0);
@@ -302,6 +393,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
       L.nu[s] = L.arena + oN[s]; L.B[s] = L.arena + oB[s]; L.piv[s] = L.iarena + oP[s];
     }
     std::vector<int32_t> live = cap;
+    std::vector<uint64_t> wave_mask(lev.nclus, 0);
 
     for (const auto& Bt : lev.batches) {
       const double tp0 = now_s();
@@ -347,16 +439,24 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
       upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm);
       t_plan += now_s() - tp0;
       upA.send(st);
+      HS_CUDA(cudaEventRecord(pt.a[0], st));
       launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
+      HS_CUDA(cudaEventRecord(pt.a[1], st));
       launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
+      HS_CUDA(cudaEventRecord(pt.a[2], st));
       launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
+      HS_CUDA(cudaEventRecord(pt.a[3], st));
       launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
+      HS_CUDA(cudaEventRecord(pt.a[4], st));
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream
+      pt.collect(S);
       const double tp1 = now_s();
       // ---- Schur update, write-back, apply plan ----------------------------------------------
-      std::unordered_map<uint64_t, std::vector<SchurContrib>> tgt;   // (p<<32|q) -> contributions
-      std::vector<uint64_t> tgt_order;
+      std::vector<SchurSrc> srcs;
+      std::vector<NbCol> nbc;
+      std::vector<std::vector<SchurTile2>> waves;
+      std::vector<int32_t> touched;
       std::vector<CopyItem> wb;
       std::vector<double*> id_ptr;
       std::vector<int32_t> id_ld, id_r;
@@ -384,20 +484,30 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
         const auto& ns = lev.H[s];
         std::vector<int32_t> noff(ns.size() + 1, 0);
         for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + live[ns[a]];
-        if (K > 0)
-          for (size_t a = 0; a < ns.size(); ++a) {
-            if (live[ns[a]] == 0) continue;
-            for (size_t b = 0; b <= a; ++b) {
-              if (live[ns[b]] == 0) continue;
-              const uint64_t key = ((uint64_t)(uint32_t)ns[a] << 32) | (uint32_t)ns[b];
-              auto itn = tgt.find(key);
-              if (itn == tgt.end()) {
-                tgt_order.push_back(key);
-                itn = tgt.emplace(key, std::vector<SchurContrib>{}).first;
-              }
-              itn->second.push_back(SchurContrib{C, ldB, K, noff[a], noff[b]});
+        if (K > 0 && kn > 0) {
+          // wave = lowest wave in which no earlier source shares a neighbour with s
+          uint64_t used = 0;
+          for (int32_t q : ns)
+            if (live[q] > 0) used |= wave_mask[q];
+          int w = 0;
+          while (w < 63 && ((used >> w) & 1ull)) ++w;
+          if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
+          const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
+          SchurSrc sc{C, ldB, K, kn, (int32_t)nbc.size(), 0, 0};
+          for (size_t a = 0; a < ns.size(); ++a)
+            if (live[ns[a]] > 0) {
+              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], 0});
+              if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
+              wave_mask[ns[a]] |= bit;
             }
-          }
+          sc.nnb = (int32_t)nbc.size() - sc.nb_off;
+          const int32_t si = (int32_t)srcs.size();
+          srcs.push_back(sc);
+          if ((int)waves.size() <= w) waves.resize(w + 1);
+          const int T = (kn + 63) / 64;
+          for (int ti = 0; ti < T; ++ti)
+            for (int tj = 0; tj <= ti; ++tj) waves[w].push_back(SchurTile2{si, ti * 64, tj * 64, 0});
+        }
         // write-back of row s: [I_r | coarse-w | coarse-n]
         if (r > 0) {
           double* p; int32_t ld, tr;
@@ -433,31 +543,16 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
                                              K, noff[a], 0});
         }
         al.nb_end = (int32_t)ap.nb.size();
+        if (K > 0) ap.max_kn = std::max(ap.max_kn, kn);
         al.y = reinterpret_cast<double*>((uintptr_t)L.voff[s]);
         ap.local.push_back(al);
       }
-      // Schur tiles (targets in first-touch order, contributions in source order)
-      std::vector<SchurTile> tiles;
-      std::vector<SchurContrib> cons;
-      for (uint64_t key : tgt_order) {
-        const int32_t p = (int32_t)(key >> 32), q = (int32_t)(key & 0xffffffffu);
-        const auto& cl = tgt[key];
-        const int32_t cb = (int32_t)cons.size();
-        cons.insert(cons.end(), cl.begin(), cl.end());
-        const int32_t ce = (int32_t)cons.size();
-        double* base; int32_t ld, tr;
-        bs.get(p, q, base, ld, tr);
-        if (tr) fail(HS_E_INTERNAL, "schur: transposed target");
-        for (int32_t i0 = 0; i0 < live[p]; i0 += 64)
-          for (int32_t j0 = 0; j0 < live[q]; j0 += 64) {
-            SchurTile t{};
-            t.dst = base + (int64_t)i0 * ld + j0;
-            t.ld = ld;
-            t.rows = std::min(64, live[p] - i0);
-            t.cols = std::min(64, live[q] - j0);
-            t.c_begin = cb; t.c_end = ce; t.i0 = i0; t.j0 = j0;
-            tiles.push_back(t);
-          }
+      for (int32_t q : touched) wave_mask[q] = 0;
+      std::vector<SchurTile2> tiles;
+      std::vector<int32_t> wave_off(1, 0);
+      for (const auto& wv : waves) {
+        tiles.insert(tiles.end(), wv.begin(), wv.end());
+        wave_off.push_back((int32_t)tiles.size());
       }
       for (int32_t q : atgt_order) {
         const auto& cl = atgt[q];
@@ -474,17 +569,23 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
       ap.batches[l].push_back(abt);
       for (int bi = 0; bi < nb; ++bi) live[Bt[bi]] = L.rank[Bt[bi]];
       upB.reset();
-      const size_t jT = upB.add(tiles), jC = upB.add(cons), jW = upB.add(wb), jP = upB.add(id_ptr),
-                   jL = upB.add(id_ld), jR = upB.add(id_r);
+      const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
+                   jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r);
       upB.stage.ensure(upB.total);
       upB.dev.ensure(upB.total);
-      upB.copy_in(jT, tiles); upB.copy_in(jC, cons); upB.copy_in(jW, wb);
+      upB.copy_in(jT, tiles); upB.copy_in(jS, srcs); upB.copy_in(jN, nbc); upB.copy_in(jW, wb);
       upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r);
       t_plan += now_s() - tp1;
       upB.send(st);
-      launch_schur(upB.dptr<SchurTile>(jT), upB.dptr<SchurContrib>(jC), (int)tiles.size(), st);
+      HS_CUDA(cudaEventRecord(pt.b[0], st));
+      for (size_t w = 0; w + 1 < wave_off.size(); ++w)
+        launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w], upB.dptr<SchurSrc>(jS),
+                      upB.dptr<NbCol>(jN), bs.dir(), st);
+      HS_CUDA(cudaEventRecord(pt.b[1], st));
       launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
       launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
+      HS_CUDA(cudaEventRecord(pt.b[2], st));
+      pt.b_pending = true;
       S.n_batches++;
       if (const char* dd = std::getenv("HS_DEBUG_DUMP")) {   // debug aid: block store after every batch
         HS_CUDA(cudaStreamSynchronize(st));
@@ -524,6 +625,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
         for (int a = 0; a < 2; ++a)
           for (int b = 0; b < 2; ++b) {
             const int32_t c = 2 * P + a, d = 2 * Q + b;
+            if (P == Q && a < b) continue;   // upper part of a diagonal block (lower semantics)
             if (L.rank[c] == 0 || L.rank[d] == 0 || !bs.has(c, d)) continue;
             double* p; int32_t ld, tr;
             bs.get(c, d, p, ld, tr);
@@ -548,12 +650,32 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
     upA.copy_in(iA, asmb);
     t_plan += now_s() - tp2;
     upA.send(st);
+    HS_CUDA(cudaEventRecord(pt.a[0], st));
     launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
+    HS_CUDA(cudaEventRecord(pt.a[1], st));
     HS_CUDA(cudaStreamSynchronize(st));
+    pt.collect_b(S);
+    S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
     bs.release();
     bs = std::move(nbs);
-    nbs.d = nullptr;
+    nbs.forget();
+    if (l + 1 < an->L_top) bs.upload_dir(st);
     cap = capn;
+    if (prof) {
+      int64_t sm = 0, sr = 0, skn = 0, skw = 0, mx = 0;
+      for (int s = 0; s < lev.nclus; ++s) {
+        sm += L.cap[s]; sr += L.rank[s]; skn += L.kn[s]; skw += L.kw[s];
+        mx = std::max<int64_t>(mx, L.kn[s] + L.kw[s]);
+      }
+      std::fprintf(stderr,
+                   "[hs profile] level %d: %d clusters %zu batches wall %.1f ms plan %.1f ms | gather %.1f potrf %.1f "
+                   "trsm %.1f cpqr %.1f schur %.1f wb %.1f ms | sum m %lld r %lld kn %lld kw %lld max ldB %lld\n",
+                   l, lev.nclus, lev.batches.size(), 1e3 * (now_s() - lv_t0), 1e3 * (t_plan - lv_plan0),
+                   1e3 * (S.t_phase_s[0] - lv_ph0[0]), 1e3 * (S.t_phase_s[1] - lv_ph0[1]),
+                   1e3 * (S.t_phase_s[2] - lv_ph0[2]), 1e3 * (S.t_phase_s[3] - lv_ph0[3]),
+                   1e3 * (S.t_phase_s[4] - lv_ph0[4]), 1e3 * (S.t_phase_s[5] - lv_ph0[5]), (long long)sm,
+                   (long long)sr, (long long)skn, (long long)skw, (long long)mx);
+    }
   }
   // ---- top: dense Cholesky of all live DOFs ----------------------------------
   {
@@ -575,7 +697,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
           const int32_t Q = qo.first;
           if (cap[P] == 0 || cap[Q] == 0) continue;
           double* src = bs.d + qo.second;
-          items.push_back(CopyItem{src, f->d_top + toff[P] * N + toff[Q], cap[Q], (int32_t)N, cap[P], cap[Q], 0, 0});
+          // diagonal blocks hold the lower triangle only: symmetrise them into A_top
+          items.push_back(CopyItem{src, f->d_top + toff[P] * N + toff[Q], cap[Q], (int32_t)N, cap[P], cap[Q],
+                                   P == Q ? 2 : 0, 0});
           if (P != Q)
             items.push_back(CopyItem{src, f->d_top + toff[Q] * N + toff[P], cap[Q], (int32_t)N, cap[Q], cap[P], 1, 0});
         }
@@ -586,8 +710,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
       upA.copy_in(iA, items);
       upA.send(st);
       launch_copy2d(upA.dptr<CopyItem>(iA), (int)items.size(), st);
+      HS_CUDA(cudaEventRecord(pt.a[0], st));
       dense_potrf(f->d_top, (int)N, (int)N, d_status, an->L_top, nullptr, st);
+      HS_CUDA(cudaEventRecord(pt.a[1], st));
       check_status(d_status, &h_status, st);
+      S.t_phase_s[6] += PhaseTimer::el(pt.a[0], pt.a[1]);
       S.flops += (double)N * N * N / 3.0;
       S.flops_phase[6] += (double)N * N * N / 3.0;
     }
@@ -612,7 +739,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* val
     }
   fb += 8.0 * (double)f->ntop * (f->ntop + 1) / 2;
   S.factor_bytes = fb;
-  (void)t_wall0;
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
   HS_CUDA(cudaMalloc(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1)));

@@ -43,6 +43,13 @@ struct Analysis {
   // the pattern, kept for hs_factor (values come later)
   std::vector<int64_t> rowptr;
   std::vector<int32_t> colind;
+  // device cache of the pattern (filled by the first factor; freed by hs_analysis_destroy)
+  int dev = -1;
+  int64_t* d_rowptr = nullptr;
+  int32_t* d_colind = nullptr;
+  int64_t* d_perm = nullptr;
+  int64_t* d_map = nullptr;     // CSR entry -> offset in the level-0 block store (-1: upper)
+  int64_t* d_tmap = nullptr;    // CSR entry (i,j) -> index of (j,i) (value symmetry check)
   int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
 };
 

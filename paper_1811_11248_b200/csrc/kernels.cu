@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <atomic>
 #include <vector>
 
 #include "device.h"
@@ -61,6 +62,14 @@ __device__ int block_min_int(int v, int* red) {
 __global__ void k_copy2d(const CopyItem* __restrict__ items) {
   const CopyItem it = items[blockIdx.x];
   if (it.rows <= 0 || it.cols <= 0) return;
+  if (it.trans == 2) {   // square block with lower-triangle semantics -> full symmetric copy
+    const int64_t tot = (int64_t)it.rows * it.cols;
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int i = (int)(e / it.cols), j = (int)(e % it.cols);
+      it.dst[(int64_t)i * it.dld + j] = i >= j ? it.src[(int64_t)i * it.sld + j] : it.src[(int64_t)j * it.sld + i];
+    }
+    return;
+  }
   if (!it.trans) {
     const int64_t tot = (int64_t)it.rows * it.cols;
     for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
@@ -385,39 +394,230 @@ __global__ void __launch_bounds__(256) k_schur(const SchurTile* __restrict__ til
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// a5 v2: Schur update X_nn -= C^T C (Eq. CC:eqn:elim) for one source cluster per tile.
+// The 64 x 64 tile of C^T C is formed with FP64 FMA (K staged through smem 16 rows at a
+// time), then every element is subtracted in place from its target block, found on the
+// device: row/column owners by binary search in the source's neighbour-column table,
+// block pointers by binary search in the level's block directory (one lookup per distinct
+// owner pair of the tile).  HBM-bound: 16 bytes of read-modify-write per target element.
+constexpr int SCH_MAXO = 32;   // distinct owners per tile side held in the pointer table
+
+__device__ __forceinline__ int64_t dir_find(const BlockDir& d, int p, int q) {   // p >= q; -1 if absent
+  int64_t lo = d.ptr[p], hi = d.ptr[p + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (d.q[mid] < q) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < d.ptr[p + 1] && d.q[lo] == q) ? d.off[lo] : -1;
+}
+
+__device__ __forceinline__ int nb_owner(const NbCol* nb, int nnb, int c) {   // last a with nb[a].col <= c
+  int lo = 0, hi = nnb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (nb[mid].col <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
+                                                const NbCol* __restrict__ nbc, BlockDir dir) {
+  const SchurTile2 t = tiles[blockIdx.x];
+  const SchurSrc s = srcs[t.src];
+  const NbCol* nb = nbc + s.nb_off;
+  __shared__ double ap[16][64];
+  __shared__ double aq[16][64];
+  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
+  __shared__ int r_slot[64], c_slot[64];
+  __shared__ int r_list[SCH_MAXO], c_list[SCH_MAXO];
+  __shared__ int nr, nc;
+  __shared__ double* ptab[SCH_MAXO][SCH_MAXO];
+  __shared__ int ldtab[SCH_MAXO];
+  const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
+  const int tid = threadIdx.x;
+  if (tid < 64) {
+    if (tid < rows) {
+      const int a = nb_owner(nb, s.nnb, t.i0 + tid);
+      r_own[tid] = a;
+      r_loc[tid] = t.i0 + tid - nb[a].col;
+    }
+  } else if (tid < 128) {
+    const int u = tid - 64;
+    if (u < cols) {
+      const int b = nb_owner(nb, s.nnb, t.j0 + u);
+      c_own[u] = b;
+      c_loc[u] = t.j0 + u - nb[b].col;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {   // distinct owners (rows/cols are sorted by owner)
+    int k = -1;
+    for (int i = 0; i < rows; ++i) {
+      if (i == 0 || r_own[i] != r_own[i - 1]) {
+        ++k;
+        if (k < SCH_MAXO) r_list[k] = r_own[i];
+      }
+      r_slot[i] = k;
+    }
+    nr = k + 1;
+  } else if (tid == 32) {
+    int k = -1;
+    for (int j = 0; j < cols; ++j) {
+      if (j == 0 || c_own[j] != c_own[j - 1]) {
+        ++k;
+        if (k < SCH_MAXO) c_list[k] = c_own[j];
+      }
+      c_slot[j] = k;
+    }
+    nc = k + 1;
+  }
+  __syncthreads();
+  const bool table = nr <= SCH_MAXO && nc <= SCH_MAXO;
+  if (table) {
+    for (int e = tid; e < nr * nc; e += blockDim.x) {
+      const int ra = e / nc, cb = e % nc;
+      const int qa = nb[r_list[ra]].q, qb = nb[c_list[cb]].q;
+      double* p = nullptr;
+      if (qa >= qb) {
+        const int64_t o = dir_find(dir, qa, qb);
+        if (o >= 0) p = dir.blk + o;
+      }
+      ptab[ra][cb] = p;
+    }
+    for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
+  }
+  __syncthreads();
+  // dense 64 x 64 tile of C^T C
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const double* Cp = s.C + t.i0;
+  const double* Cq = s.C + t.j0;
+  for (int k0 = 0; k0 < s.K; k0 += 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      const int kk = e >> 6, ii = e & 63;
+      const bool kin = k0 + kk < s.K;
+      ap[kk][ii] = (kin && ii < rows) ? Cp[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+      aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) x[a] = ap[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) y[b] = aq[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  // scatter-subtract into the target blocks
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      if (i >= rows || j >= cols) continue;
+      const int oa = r_own[i], ob = c_own[j];
+      if (oa < ob) continue;                               // upper: the transposed block
+      const int li = r_loc[i], lj = c_loc[j];
+      if (oa == ob && li < lj) continue;                   // diagonal block: lower triangle only
+      double* p;
+      int ld;
+      if (table) {
+        p = ptab[r_slot[i]][c_slot[j]];
+        ld = ldtab[c_slot[j]];
+      } else {
+        const int qa = nb[oa].q, qb = nb[ob].q;
+        const int64_t o = dir_find(dir, qa, qb);
+        p = o >= 0 ? dir.blk + o : nullptr;
+        ld = dir.cap[qb];
+      }
+      if (p) p[(int64_t)li * ld + lj] -= acc[a][b];
+    }
+}
+
+__global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,
+                           int32_t* flag) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const double a = v[k], t = v[tmap[k]];
+    if (!(fabs(a - t) <= 1e-12 * fmax(fabs(a), fabs(t)))) *flag = 1;
+  }
+}
+
 void set_smem(const void* f, size_t bytes) {
   static_cast<void>(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+std::atomic<int64_t> g_launches{0};
+
 }  // namespace
 
+void count_launch(int64_t n) { g_launches += n; }
+int64_t launch_count() { return g_launches.load(); }
+
 // ---- launchers -----------------------------------------------------------------------------
+void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32_t* flag, cudaStream_t st) {
+  if (nnz <= 0) return;
+  k_symcheck<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, tmap, nnz, flag);
+  count_launch(1);
+}
 void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st) {
-  if (n > 0) k_copy2d<<<n, 256, 0, st>>>(d_items);
+  if (n <= 0) return;
+  k_copy2d<<<n, 256, 0, st>>>(d_items);
+  count_launch(1);
 }
 void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d_r, int n, cudaStream_t st) {
-  if (n > 0) k_identity<<<n, 128, 0, st>>>(d_ptr, d_ld, d_r);
+  if (n <= 0) return;
+  k_identity<<<n, 128, 0, st>>>(d_ptr, d_ld, d_r);
+  count_launch(1);
 }
 void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st) {
-  if (nnz > 0) k_scatter<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, map, nnz, blk);
+  if (nnz <= 0) return;
+  k_scatter<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, map, nnz, blk);
+  count_launch(1);
 }
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st) {
   if (n <= 0) return;
   const size_t sm = (size_t)max_m * max_m * sizeof(double);
   set_smem((const void*)k_potrf, sm);
   k_potrf<<<n, 256, sm, st>>>(d_items, status);
+  count_launch(1);
 }
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st) {
   if (n <= 0) return;
   const size_t sm = ((size_t)max_m * max_m + (size_t)max_m * 64) * sizeof(double);
   set_smem((const void*)k_trsm, sm);
   k_trsm<<<n, 256, sm, st>>>(d_clu, d_items);
+  count_launch(1);
 }
 void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st) {
-  if (n > 0) k_cpqr<<<n, CPQR_THREADS, 0, st>>>(d_items, eps, relative, d_rank);
+  if (n <= 0) return;
+  k_cpqr<<<n, CPQR_THREADS, 0, st>>>(d_items, eps, relative, d_rank);
+  count_launch(1);
 }
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st) {
-  if (n > 0) k_schur<<<n, 256, 0, st>>>(d_tiles, d_con);
+  if (n <= 0) return;
+  k_schur<<<n, 256, 0, st>>>(d_tiles, d_con);
+  count_launch(1);
+}
+void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
+                   cudaStream_t st) {
+  if (n <= 0) return;
+  k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
+  count_launch(1);
 }
 
 // a7: blocked right-looking Cholesky of the dense top matrix.
@@ -437,7 +637,10 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
     const int nb = std::min(NB, N - k);
     k_potrf_raw<<<1, 256, (size_t)nb * nb * sizeof(double), st>>>(A + (int64_t)k * ld + k, ld, nb, status, level);
     const int rest = N - k - nb;
-    if (rest <= 0) break;
+    if (rest <= 0) {
+      count_launch(1);
+      break;
+    }
     k_trsm_raw<<<(rest + 63) / 64, 256, ((size_t)nb * nb + (size_t)nb * 64) * sizeof(double), st>>>(
         A + (int64_t)k * ld + k, ld, nb, A + (int64_t)k * ld + k + nb, ld, rest);
     const int kb = k / NB;
@@ -460,6 +663,7 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
     HS_CUDA(cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(SchurTile) * tiles.size(),
                             cudaMemcpyHostToDevice, st));
     k_schur<<<(int)tiles.size(), 256, 0, st>>>(d_tiles, d_con);
+    count_launch(3);
     HS_CUDA(cudaStreamSynchronize(st));   // host vectors are reused; the top runs once per factor
   }
   HS_CUDA(cudaStreamSynchronize(st));

@@ -73,6 +73,8 @@ struct ApplyPlan {
   int64_t vtotal = 0;
   double* d_y = nullptr;                 // the apply vector (all levels + top)
   cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
+  int32_t max_kn = 0;                    // largest n-part of a cluster with fine DOFs (apply smem)
   const double* graph_in = nullptr;
   double* graph_out = nullptr;
 };

@@ -6,6 +6,9 @@
 // PCG (north_star) keeps every scalar on the device; the only host
 // synchronisation per iteration is the 8-byte read of ||r||^2 for the stopping test.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "runtime.h"
 
@@ -95,29 +98,70 @@ __global__ void k_sub(double* __restrict__ d, const double* __restrict__ a, cons
 void dot(const double* a, const double* b, int64_t n, double* partial, double* out, cudaStream_t st) {
   k_dot_partial<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, n, partial);
   k_finish<<<1, RED_THREADS, 0, st>>>(partial, RED_BLOCKS, out);
+  count_launch(2);
 }
 
-void record_apply(hs_factor_s* f, cudaStream_t st) {
+void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev = nullptr) {
   const Analysis* an = f->an;
   ApplyPlan& ap = f->ap;
   const int64_t n = an->n;
+  auto mark = [&]() {
+    if (!ev) return;
+    cudaEvent_t e;
+    HS_CUDA(cudaEventCreate(&e));
+    HS_CUDA(cudaEventRecord(e, st));
+    ev->push_back(e);
+  };
+  mark();
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
+    mark();
     for (const auto& b : ap.batches[l]) {
       launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, st);
       launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
     }
     const int64_t nt = (int64_t)ap.trans_src[l].size();
-    if (nt) k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 0);
+    if (nt) {
+      k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 0);
+      count_launch(1);
+    }
   }
+  mark();
   if (f->ntop > 0) launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);
   for (int l = an->L_top - 1; l >= 0; --l) {
+    mark();
     const int64_t nt = (int64_t)ap.trans_src[l].size();
-    if (nt) k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
+    if (nt) {
+      k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
+      count_launch(1);
+    }
     for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it)
-      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, st);
+      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, ap.max_kn, st);
   }
+  mark();
   launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);
+  mark();
+}
+
+// HS_PROFILE=1: one eager (non-graph) apply with events at every level boundary
+void profile_apply(hs_factor_s* f, cudaStream_t st) {
+  std::vector<cudaEvent_t> ev;
+  record_apply(f, st, &ev);
+  HS_CUDA(cudaStreamSynchronize(st));
+  const int L = f->an->L_top;
+  auto el = [&](int i) {
+    float ms;
+    HS_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+    return ms;
+  };
+  std::fprintf(stderr, "[hs profile] apply (eager): permute-in %.3f ms\n", el(0));
+  for (int l = 0; l < L; ++l)
+    std::fprintf(stderr, "[hs profile]   fwd level %d: %.3f ms (%zu batches)\n", l, el(1 + l), f->ap.batches[l].size());
+  std::fprintf(stderr, "[hs profile]   top: %.3f ms (N_top %lld)\n", el(1 + L), (long long)f->ntop);
+  for (int k = 0; k < L; ++k)
+    std::fprintf(stderr, "[hs profile]   bwd level %d: %.3f ms\n", L - 1 - k, el(2 + L + k));
+  std::fprintf(stderr, "[hs profile]   permute-out %.3f ms\n", el(2 + 2 * L));
+  for (auto e : ev) cudaEventDestroy(e);
 }
 
 void ensure_vectors(hs_factor_s* f) {
@@ -136,14 +180,18 @@ void run_apply_graph(hs_factor_s* f, cudaStream_t st) {
     cudaStream_t cs;
     HS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t g;
+    const int64_t c0 = launch_count();
     HS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     record_apply(f, cs);
     HS_CUDA(cudaStreamEndCapture(cs, &g));
+    ap.graph_kernels = launch_count() - c0;   // captured, not launched
+    count_launch(-ap.graph_kernels);
     HS_CUDA(cudaGraphInstantiate(&ap.graph, g, 0));
     cudaGraphDestroy(g);
     cudaStreamDestroy(cs);
   }
   HS_CUDA(cudaGraphLaunch(ap.graph, st));
+  count_launch(ap.graph_kernels);
 }
 
 }  // namespace
@@ -153,6 +201,7 @@ void apply(hs_factor_s* f, const double* d_b, double* d_x) {
   ensure_vectors(f);
   const int64_t n = f->an->n;
   if (d_b != f->d_b) HS_CUDA(cudaMemcpyAsync(f->d_b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (std::getenv("HS_PROFILE")) profile_apply(f, st);
   run_apply_graph(f, st);
   if (d_x != f->d_x) HS_CUDA(cudaMemcpyAsync(d_x, f->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
 }
@@ -184,6 +233,7 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   run_apply_graph(f, st);                               // z = M^{-1} r
   HS_CUDA(cudaEventRecord(a1, st));
   k_copy<<<G, T, 0, st>>>(p, z, n);
+  count_launch(3);   // the two copies and the zero
   dot(r, z, n, part, sc + 0, st);                       // rho
   HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
   HS_CUDA(cudaStreamSynchronize(st));
@@ -209,6 +259,7 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
       dot(p, q, n, part, sc + 1, st);                                  // pq
       k_update_xr<<<G, T, 0, st>>>(x, r, p, q, n, sc, part);           // x, r, ||r||^2
       k_finish<<<1, T, 0, st>>>(part, G, sc + 2);
+      count_launch(2);
       HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
       HS_CUDA(cudaStreamSynchronize(st));
       rep->iters = k;
@@ -222,6 +273,7 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
       dot(r, z, n, part, sc + 3, st);                                  // rz_new
       k_update_p<<<G, T, 0, st>>>(p, z, n, sc);
       k_set_rho<<<1, 1, 0, st>>>(sc);
+      count_launch(2);
       HS_CUDA(cudaEventSynchronize(a1));
       float ms;
       HS_CUDA(cudaEventElapsedTime(&ms, a0, a1));
@@ -238,6 +290,7 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   // true residual ||b - A x|| / ||b|| (outside the timed region)
   launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, x, q, n, st);
   k_sub<<<G, T, 0, st>>>(q, d_bin, q, n);
+  count_launch(1);
   dot(q, q, n, part, sc + 2, st);
   HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
   if (d_xout != x) HS_CUDA(cudaMemcpyAsync(d_xout, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));

@@ -124,16 +124,27 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
 __global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs) {
   const ApplyLocal it = items[blockIdx.x];
   if (it.m == 0) return;
+  extern __shared__ double xs[];            // x_n gathered in the column order of C (kn entries)
   __shared__ double xf[MAX_M];
   const int K = it.m - it.r;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int kn = 0;
+  if (K > 0) {
+    // warps take neighbours, lanes their entries: the independent loads overlap
+    for (int b = it.nb_begin + wid; b < it.nb_end; b += nw) {
+      const ApplyNb nb = nbs[b];
+      for (int i = lane; i < nb.len; i += 32) xs[nb.col + i] = nb.xq[i];
+    }
+    if (it.nb_end > it.nb_begin) {
+      const ApplyNb last = nbs[it.nb_end - 1];
+      kn = last.col + last.len;
+    }
+    __syncthreads();
+  }
   for (int k = wid; k < K; k += nw) {
     const double* Crow = it.C + (int64_t)k * it.ldC;
     double acc = 0.0;
-    for (int b = it.nb_begin; b < it.nb_end; ++b) {
-      const ApplyNb nb = nbs[b];
-      for (int i = lane; i < nb.len; i += 32) acc += Crow[nb.col + i] * nb.xq[i];
-    }
+    for (int c = lane; c < kn; c += 32) acc += Crow[c] * xs[c];
     acc = wsum(acc);
     if (lane == 0) xf[k] = it.y[it.r + k] - acc;
   }
@@ -204,23 +215,41 @@ __global__ void k_spmv(const int64_t* __restrict__ rowptr, const int32_t* __rest
 }  // namespace
 
 void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st) {
-  if (n > 0) k_apply_fwd_local<<<(n + 3) / 4, 128, 0, st>>>(d, n);
+  if (n <= 0) return;
+  k_apply_fwd_local<<<(n + 3) / 4, 128, 0, st>>>(d, n);
+  count_launch(1);
 }
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st) {
-  if (n > 0) k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
+  if (n <= 0) return;
+  k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
+  count_launch(1);
 }
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, cudaStream_t st) {
-  if (n > 0) k_apply_bwd<<<n, 128, 0, st>>>(d, nb);
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t sm = sizeof(double) * (size_t)std::max(max_kn, 1);
+  static size_t configured = 0;
+  if (sm > configured) {
+    HS_CUDA(cudaFuncSetAttribute((const void*)k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    configured = sm;
+  }
+  k_apply_bwd<<<n, 256, sm, st>>>(d, nb);
+  count_launch(1);
 }
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {
-  if (N > 0) k_top_solve<<<1, 1024, 0, st>>>(y, A, N, ld);
+  if (N <= 0) return;
+  k_top_solve<<<1, 1024, 0, st>>>(y, A, N, ld);
+  count_launch(1);
 }
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st) {
-  if (n > 0) k_permute<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(src, dst, idx, n, scatter);
+  if (n <= 0) return;
+  k_permute<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(src, dst, idx, n, scatter);
+  count_launch(1);
 }
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,
                  int64_t n, cudaStream_t st) {
-  if (n > 0) k_spmv<<<(int)((n * 8 + 255) / 256), 256, 0, st>>>(rowptr, colind, vals, x, y, n);
+  if (n <= 0) return;
+  k_spmv<<<(int)((n * 8 + 255) / 256), 256, 0, st>>>(rowptr, colind, vals, x, y, n);
+  count_launch(1);
 }
 
 }  // namespace hs

@@ -33,7 +33,7 @@ HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(
 SYMBOLS = ["hs_create", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
            "hs_analysis_get_info", "hs_analysis_export", "hs_analysis_destroy", "hs_factor_create",
            "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
-           "hs_pcg", "hs_spmv"]
+           "hs_pcg", "hs_spmv", "hs_launch_count"]
 HS_CEXP_SHAPE, HS_CEXP_G, HS_CEXP_V, HS_CEXP_TAU, HS_CEXP_B = range(5)
 
 
@@ -49,7 +49,8 @@ class hs_analyze_opts(C.Structure):
 
 
 class hs_factor_opts(C.Structure):
-    _fields_ = [("eps", C.c_double), ("eps_relative", C.c_int32), ("dc", C.c_int32)]
+    _fields_ = [("eps", C.c_double), ("eps_relative", C.c_int32), ("dc", C.c_int32),
+                ("values_on_device", C.c_int32), ("reserved", C.c_int32)]
 
 
 class hs_analysis_info(C.Structure):
@@ -111,9 +112,11 @@ def lib():
         L.hs_apply.argtypes = [vp, vp, vp, i32]
         L.hs_pcg.argtypes = [vp, vp, vp, dp, i32, i32, C.POINTER(hs_pcg_report)]
         L.hs_spmv.argtypes = [vp, vp, vp, i32]
+        L.hs_launch_count.argtypes = []
+        L.hs_launch_count.restype = i64
         for s in SYMBOLS:
             if s not in ("hs_destroy", "hs_analysis_destroy", "hs_factor_destroy", "hs_last_error",
-                         "hs_status_string"):
+                         "hs_status_string", "hs_launch_count"):
                 getattr(L, s).restype = C.c_int
         _lib = L
     return _lib
@@ -212,12 +215,21 @@ def hs_analysis_export(a: Analysis, key: int, level: int = 0) -> np.ndarray:
 
 
 def hs_factor_create(h: Handle, a: Analysis, values, eps=1e-2, eps_relative=1, dc=1) -> Factor:
-    values = np.ascontiguousarray(values, dtype=np.float64)
-    opt = hs_factor_opts(eps, eps_relative, dc)
+    """values: numpy (host) or a torch CUDA float64 tensor (device-resident CSR values)."""
+    if hasattr(values, "is_cuda") and values.is_cuda:
+        vp, on_dev = _ptr(values)
+    else:
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        vp, on_dev = C.c_void_p(values.ctypes.data), 0
+    opt = hs_factor_opts(eps, eps_relative, dc, on_dev, 0)
     f = C.c_void_p()
-    _check(lib().hs_factor_create(h.ptr, a.ptr, values.ctypes.data, C.byref(opt), C.byref(f)), h.ptr)
+    _check(lib().hs_factor_create(h.ptr, a.ptr, vp, C.byref(opt), C.byref(f)), h.ptr)
     info = hs_analysis_get_info(a)
     return Factor(f, h, a, info["n"])
+
+
+def hs_launch_count() -> int:
+    return int(lib().hs_launch_count())
 
 
 def hs_factor_get_stats(f: Factor) -> dict:

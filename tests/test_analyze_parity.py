@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_header_symbols_exported():
     hdr = open(os.path.join(ROOT, "include", "hsolve.h")).read()
-    decl = set(re.findall(r"^\s*(?:hs_status|void|const char\*)\s+(hs_\w+)\s*\(", hdr, re.M))
+    decl = set(re.findall(r"^\s*(?:hs_status|void|const char\*|int64_t)\s+(hs_\w+)\s*\(", hdr, re.M))
     assert decl == set(H.SYMBOLS)
     L = H.lib()
     for s in decl:

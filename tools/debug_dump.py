@@ -40,6 +40,8 @@ else:
         scale = max(np.abs(st.get(a, b_)).max() if st.get(a, b_).size else 0.0 for (a, b_) in g)
         for (pp, qq), M in g.items():
             O = st.get(pp, qq)
+            if pp == qq:          # diagonal blocks keep lower-triangle semantics on the GPU
+                O, M = np.tril(O), np.tril(M)
             if O.shape != M.shape:
                 print("shape", l, b, pp, qq, O.shape, M.shape); worst = np.inf; continue
             if M.size:
