@@ -122,6 +122,9 @@ void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double*
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st);
+// thread-block-cluster CPQR; picks the cluster size from the batch shape, returns it
+int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
+                 int32_t* d_rank, cudaStream_t st);
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st);
@@ -132,9 +135,9 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
                  cudaStream_t st);
 constexpr int TOP_NB = 64;
 
-void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st);
+void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st);
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, cudaStream_t st);
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, int64_t cap, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

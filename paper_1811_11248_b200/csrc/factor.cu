@@ -344,6 +344,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ap.trans_dst.resize(an->L_top);
 
   const bool prof = std::getenv("HS_PROFILE") != nullptr;
+  const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;   // A/B switch for the old kernel
   for (int l = 0; l < an->L_top; ++l) {
     const Level& lev = an->levels[l];
     LevelRT& L = f->lv[l];
@@ -395,7 +396,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::vector<int32_t> live = cap;
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
 
+    int64_t level_dofs = 0;
+    for (int32_t c : cap) level_dofs += c;
     for (const auto& Bt : lev.batches) {
+      if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
       const double tp0 = now_s();
       const int nb = (int)Bt.size();
       std::vector<CopyItem> gather;
@@ -446,7 +450,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       HS_CUDA(cudaEventRecord(pt.a[2], st));
       launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
       HS_CUDA(cudaEventRecord(pt.a[3], st));
-      launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
+      if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
+      else launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
       HS_CUDA(cudaEventRecord(pt.a[4], st));
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream
@@ -566,6 +571,24 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       abt.local_end = (int32_t)ap.local.size();
       abt.tgt_end = (int32_t)ap.tgt.size();
+      {   // shared-memory staging sizes of the apply kernels (doubles; <= ~208 KB)
+        const int64_t LIM = 26000;
+        for (int32_t i = abt.local_begin; i < abt.local_end; ++i) {
+          const ApplyLocal& a = ap.local[i];
+          if (a.nb_end > a.nb_begin) {
+            const ApplyNb& lastnb = ap.nb[a.nb_end - 1];
+            abt.kn_bwd = std::max(abt.kn_bwd, lastnb.col + lastnb.len);
+          }
+        }
+        if (abt.kn_bwd > LIM) fail(HS_E_UNSUPPORTED, "apply: neighbour block row too wide for shared memory");
+        abt.cap_bwd = abt.kn_bwd;
+        for (int32_t i = abt.local_begin; i < abt.local_end; ++i) {
+          const ApplyLocal& a = ap.local[i];
+          const int64_t need = (int64_t)a.m * a.m + (int64_t)a.m * a.r + a.r;
+          if (need <= LIM) abt.cap_fwd = std::max(abt.cap_fwd, need);
+          if (abt.kn_bwd + need <= LIM) abt.cap_bwd = std::max(abt.cap_bwd, abt.kn_bwd + need);
+        }
+      }
       ap.batches[l].push_back(abt);
       for (int bi = 0; bi < nb; ++bi) live[Bt[bi]] = L.rank[Bt[bi]];
       upB.reset();

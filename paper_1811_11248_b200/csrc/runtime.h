@@ -54,6 +54,9 @@ struct LevelRT {
 struct ApplyBatch {
   int32_t local_begin, local_end;       // into fwd_local / bwd_local item arrays
   int32_t tgt_begin, tgt_end;           // forward scatter targets
+  int64_t cap_fwd = 0;                  // dynamic smem (doubles) of the forward local kernel
+  int32_t kn_bwd = 0;                   // x_n staging size of the backward kernel
+  int64_t cap_bwd = 0;                  // total dynamic smem (doubles) of the backward kernel
 };
 
 struct ApplyPlan {

@@ -117,7 +117,7 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   for (int l = 0; l < an->L_top; ++l) {
     mark();
     for (const auto& b : ap.batches[l]) {
-      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, st);
+      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, st);
       launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
     }
     const int64_t nt = (int64_t)ap.trans_src[l].size();
@@ -136,7 +136,8 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
       count_launch(1);
     }
     for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it)
-      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, ap.max_kn, st);
+      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, it->kn_bwd,
+                       it->cap_bwd, st);
   }
   mark();
   launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);

@@ -78,21 +78,43 @@ __device__ __forceinline__ void warp_reflect(const double* V, const double* tau,
   }
 }
 
+// Stage G (m x m), V (m x r) and tau (r) of a cluster in shared memory at `sm` when they
+// fit in `cap` doubles (one coalesced pass by the whole CTA instead of a latency-bound
+// chain of dependent global loads in the warp solve); returns the pointers to use.
+__device__ __forceinline__ void stage_local(const ApplyLocal& it, double* sm, int64_t cap, const double*& G,
+                                            const double*& V, const double*& tau) {
+  const int64_t mm = (int64_t)it.m * it.m, mr = (int64_t)it.m * it.r;
+  G = it.G;
+  V = it.V;
+  tau = it.tau;
+  if (mm + mr + it.r > cap) return;
+  for (int64_t e = threadIdx.x; e < mm; e += blockDim.x) sm[e] = it.G[e];
+  for (int64_t e = threadIdx.x; e < mr; e += blockDim.x) sm[mm + e] = it.V[e];
+  for (int e = threadIdx.x; e < it.r; e += blockDim.x) sm[mm + mr + e] = it.tau[e];
+  G = sm;
+  V = sm + mm;
+  tau = sm + mm + mr;
+}
+
 // forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s)
-__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// one CTA per cluster: the CTA stages the factors, warp 0 solves.
+__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, int64_t cap) {
+  extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
-  if (w >= n) return;
-  const ApplyLocal it = items[w];
+  const ApplyLocal it = items[blockIdx.x];
   if (it.m == 0) return;
+  const double *G, *V, *tau;
+  stage_local(it, sm, cap, G, V, tau);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
   double y[SLOTS];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const int l = lane + 32 * s;
     y[s] = l < it.m ? it.y[l] : 0.0;
   }
-  warp_trsv_lower(it.G, it.m, y, lane);
-  for (int j = 0; j < it.r; ++j) warp_reflect(it.V, it.tau, it.m, j, y, lane);
+  warp_trsv_lower(G, it.m, y, lane);
+  for (int j = 0; j < it.r; ++j) warp_reflect(V, tau, it.m, j, y, lane);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const int l = lane + 32 * s;
@@ -112,8 +134,11 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
     double acc = 0.0;
     for (int c = t.c_begin; c < t.c_end; ++c) {
       const ApplyContrib a = con[c];
-      if (i < t.len)
-        for (int k = 0; k < a.K; ++k) acc += a.C[(int64_t)k * a.ldC + a.col + i] * a.yf[k];
+      if (i < t.len) {
+        const double* Ci = a.C + a.col + i;
+#pragma unroll 4
+        for (int k = 0; k < a.K; ++k) acc += Ci[(int64_t)k * a.ldC] * __ldg(a.yf + k);
+      }
     }
     if (i < t.len) t.yq[i] -= acc;
   }
@@ -121,19 +146,22 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
 
 // backward: x_f = y_f - sum_q C_s[:, q] x_q ; x_s <- G^{-T} U [x_c; x_f]
 // one CTA per cluster: all warps form x_f, warp 0 does the local solve.
-__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs) {
+__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs, int max_kn,
+                            int64_t cap) {
   const ApplyLocal it = items[blockIdx.x];
   if (it.m == 0) return;
   extern __shared__ double xs[];            // x_n gathered in the column order of C (kn entries)
   __shared__ double xf[MAX_M];
+  const double *G, *V, *tau;
+  stage_local(it, xs + max_kn, cap - max_kn, G, V, tau);
   const int K = it.m - it.r;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int kn = 0;
   if (K > 0) {
-    // warps take neighbours, lanes their entries: the independent loads overlap
-    for (int b = it.nb_begin + wid; b < it.nb_end; b += nw) {
+    // a thread per neighbour descriptor, then its entries: every load is independent
+    for (int b = it.nb_begin + threadIdx.x; b < it.nb_end; b += blockDim.x) {
       const ApplyNb nb = nbs[b];
-      for (int i = lane; i < nb.len; i += 32) xs[nb.col + i] = nb.xq[i];
+      for (int i = 0; i < nb.len; ++i) xs[nb.col + i] = nb.xq[i];
     }
     if (it.nb_end > it.nb_begin) {
       const ApplyNb last = nbs[it.nb_end - 1];
@@ -156,8 +184,8 @@ __global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb*
     const int l = lane + 32 * s;
     y[s] = l < it.r ? it.y[l] : (l < it.m ? xf[l - it.r] : 0.0);
   }
-  for (int j = it.r - 1; j >= 0; --j) warp_reflect(it.V, it.tau, it.m, j, y, lane);
-  warp_trsv_upper_t(it.G, it.m, y, lane);
+  for (int j = it.r - 1; j >= 0; --j) warp_reflect(V, tau, it.m, j, y, lane);
+  warp_trsv_upper_t(G, it.m, y, lane);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const int l = lane + 32 * s;
@@ -214,9 +242,19 @@ __global__ void k_spmv(const int64_t* __restrict__ rowptr, const int32_t* __rest
 
 }  // namespace
 
-void launch_apply_fwd_local(const ApplyLocal* d, int n, cudaStream_t st) {
+static void set_dyn_smem(const void* f, size_t bytes, size_t& configured) {
+  if (bytes > configured) {
+    HS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    configured = bytes;
+  }
+}
+
+void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st) {
   if (n <= 0) return;
-  k_apply_fwd_local<<<(n + 3) / 4, 128, 0, st>>>(d, n);
+  static size_t configured = 48 * 1024;
+  const size_t sm = sizeof(double) * (size_t)cap;
+  set_dyn_smem((const void*)k_apply_fwd_local, sm, configured);
+  k_apply_fwd_local<<<n, 128, sm, st>>>(d, n, cap);
   count_launch(1);
 }
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st) {
@@ -224,15 +262,12 @@ void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n
   k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
   count_launch(1);
 }
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, cudaStream_t st) {
+void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, int64_t cap, cudaStream_t st) {
   if (n <= 0) return;
-  const size_t sm = sizeof(double) * (size_t)std::max(max_kn, 1);
-  static size_t configured = 0;
-  if (sm > configured) {
-    HS_CUDA(cudaFuncSetAttribute((const void*)k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    configured = sm;
-  }
-  k_apply_bwd<<<n, 256, sm, st>>>(d, nb);
+  static size_t configured = 48 * 1024;
+  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
+  set_dyn_smem((const void*)k_apply_bwd, sm, configured);
+  k_apply_bwd<<<n, 256, sm, st>>>(d, nb, max_kn, cap);
   count_launch(1);
 }
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {
