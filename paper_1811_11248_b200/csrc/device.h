@@ -81,13 +81,18 @@ struct BlockDir {            // the level's block store: row p has blocks (p, q<
 };
 
 // Apply (Algorithm 2) items.
-struct ApplyLocal {          // forward: y_s <- U^T G^{-1} y_s ; backward: x_f -= sum C x_q, x_s <- G^{-T} U x_s
+struct ApplyLocal {          // forward: y_s <- U^T G^{-1} y_s
+                             // backward: x_f = y_f - sum C x_q, x_s <- G^{-T} U x_s
   const double* G;
   const double* V;
   const double* tau;
   double* y;                 // the cluster's segment (m entries)
   const double* C;           // C_s (fine rows), n-part column 0, ld ldC
-  int32_t m, r, nb_begin, nb_end, ldC, pad;
+  int32_t m, r, nb_begin, nb_end, ldC, part_off, kn, pad;
+};
+constexpr int BWD_CHUNK = 256;   // columns of C per backward matvec CTA
+struct ApplyChunk {          // backward matvec: columns [c0, c0+BWD_CHUNK) of cluster `li` of the batch
+  int32_t li, c0, part, pad;    // partial sums of the K rows go to parts[part .. part+K)
 };
 struct ApplyNb {             // backward: C_s[:, col:col+len] x_q
   const double* xq;
@@ -137,7 +142,11 @@ constexpr int TOP_NB = 64;
 
 void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st);
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, int64_t cap, cudaStream_t st);
+// backward, stage 1: partial sums of C x_n over column chunks (many CTAs per cluster)
+void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb, const ApplyChunk* ch, int n,
+                              double* parts, cudaStream_t st);
+// backward, stage 2: x_f = y_f - sum of the partials (fixed order), x_s <- G^{-T} U [x_c; x_f]
+void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

@@ -221,7 +221,7 @@ hs_factor_s::~hs_factor_s() {
   };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
-  fr(ap.d_local); fr(ap.d_nb); fr(ap.d_tgt); fr(ap.d_con); fr(ap.d_y);
+  fr(ap.d_local); fr(ap.d_nb); fr(ap.d_tgt); fr(ap.d_con); fr(ap.d_y); fr(ap.d_chunks); fr(ap.d_parts);
   for (auto* p : ap.d_tsrc) fr(p);
   for (auto* p : ap.d_tdst) fr(p);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
@@ -395,6 +395,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     }
     std::vector<int32_t> live = cap;
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
+    std::vector<int32_t> atgt_slot(lev.nclus, -1);
+    ap.lvl_local.push_back((int32_t)ap.local.size());
+    ap.lvl_nb.push_back((int32_t)ap.nb.size());
+    ap.lvl_con.push_back((int32_t)ap.con.size());
+    ap.lvl_tgt.push_back((int32_t)ap.tgt.size());
 
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
@@ -468,8 +473,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       ApplyBatch abt{};
       abt.local_begin = (int32_t)ap.local.size();
       abt.tgt_begin = (int32_t)ap.tgt.size();
-      std::unordered_map<int32_t, std::vector<ApplyContrib>> atgt;
-      std::vector<int32_t> atgt_order;
+      std::vector<std::pair<int32_t, std::vector<ApplyContrib>>> atgt;   // forward scatter, first-touch order
+      std::vector<ApplyChunk> bwd_chunks;
+      int64_t bwd_parts = 0;
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bt[bi];
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
@@ -533,21 +539,28 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         ApplyLocal al{};
         al.G = L.G[s]; al.V = L.V[s]; al.tau = L.tau[s];
         al.y = nullptr;   // patched with the device base after the factor
-        al.C = C; al.ldC = ldB; al.m = m; al.r = r;
+        al.C = C; al.ldC = ldB; al.m = m; al.r = r; al.kn = kn;
         al.nb_begin = (int32_t)ap.nb.size();
         for (size_t a = 0; a < ns.size(); ++a) {
           const int32_t q = ns[a];
           if (live[q] == 0 || K == 0) continue;
           ap.nb.push_back(ApplyNb{reinterpret_cast<const double*>((uintptr_t)(L.voff[q])), noff[a], live[q]});
-          auto ita = atgt.find(q);
-          if (ita == atgt.end()) {
-            atgt_order.push_back(q);
-            ita = atgt.emplace(q, std::vector<ApplyContrib>{}).first;
+          if (atgt_slot[q] < 0) {
+            atgt_slot[q] = (int32_t)atgt.size();
+            atgt.push_back({q, {}});
           }
-          ita->second.push_back(ApplyContrib{C, reinterpret_cast<const double*>((uintptr_t)(L.voff[s] + r)), ldB,
-                                             K, noff[a], 0});
+          atgt[atgt_slot[q]].second.push_back(
+              ApplyContrib{C, reinterpret_cast<const double*>((uintptr_t)(L.voff[s] + r)), ldB, K, noff[a], 0});
         }
         al.nb_end = (int32_t)ap.nb.size();
+        al.part_off = 0;
+        if (K > 0 && al.nb_end > al.nb_begin) {   // backward matvec column chunks
+          al.part_off = (int32_t)bwd_parts;
+          for (int32_t c0 = 0; c0 < kn; c0 += BWD_CHUNK) {
+            bwd_chunks.push_back(ApplyChunk{(int32_t)(ap.local.size() - abt.local_begin), c0, (int32_t)bwd_parts, 0});
+            bwd_parts += K;
+          }
+        }
         if (K > 0) ap.max_kn = std::max(ap.max_kn, kn);
         al.y = reinterpret_cast<double*>((uintptr_t)L.voff[s]);
         ap.local.push_back(al);
@@ -559,35 +572,30 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         tiles.insert(tiles.end(), wv.begin(), wv.end());
         wave_off.push_back((int32_t)tiles.size());
       }
-      for (int32_t q : atgt_order) {
-        const auto& cl = atgt[q];
+      for (auto& tq : atgt) {
         ApplyTarget t{};
-        t.yq = reinterpret_cast<double*>((uintptr_t)L.voff[q]);
-        t.len = live[q];
+        t.yq = reinterpret_cast<double*>((uintptr_t)L.voff[tq.first]);
+        t.len = live[tq.first];
         t.c_begin = (int32_t)ap.con.size();
-        ap.con.insert(ap.con.end(), cl.begin(), cl.end());
+        ap.con.insert(ap.con.end(), tq.second.begin(), tq.second.end());
         t.c_end = (int32_t)ap.con.size();
         ap.tgt.push_back(t);
+        atgt_slot[tq.first] = -1;
       }
+      abt.chunk_begin = (int32_t)ap.chunks.size();
+      ap.chunks.insert(ap.chunks.end(), bwd_chunks.begin(), bwd_chunks.end());
+      abt.chunk_end = (int32_t)ap.chunks.size();
+      ap.max_parts = std::max(ap.max_parts, bwd_parts);
       abt.local_end = (int32_t)ap.local.size();
       abt.tgt_end = (int32_t)ap.tgt.size();
-      {   // shared-memory staging sizes of the apply kernels (doubles; <= ~208 KB)
-        const int64_t LIM = 26000;
-        for (int32_t i = abt.local_begin; i < abt.local_end; ++i) {
-          const ApplyLocal& a = ap.local[i];
-          if (a.nb_end > a.nb_begin) {
-            const ApplyNb& lastnb = ap.nb[a.nb_end - 1];
-            abt.kn_bwd = std::max(abt.kn_bwd, lastnb.col + lastnb.len);
-          }
-        }
-        if (abt.kn_bwd > LIM) fail(HS_E_UNSUPPORTED, "apply: neighbour block row too wide for shared memory");
-        abt.cap_bwd = abt.kn_bwd;
+      {   // shared-memory staging of G/V/tau in the apply's local kernels (doubles; <= ~200 KB)
+        const int64_t LIM = 25000;
         for (int32_t i = abt.local_begin; i < abt.local_end; ++i) {
           const ApplyLocal& a = ap.local[i];
           const int64_t need = (int64_t)a.m * a.m + (int64_t)a.m * a.r + a.r;
           if (need <= LIM) abt.cap_fwd = std::max(abt.cap_fwd, need);
-          if (abt.kn_bwd + need <= LIM) abt.cap_bwd = std::max(abt.cap_bwd, abt.kn_bwd + need);
         }
+        abt.cap_bwd = abt.cap_fwd;
       }
       ap.batches[l].push_back(abt);
       for (int bi = 0; bi < nb; ++bi) live[Bt[bi]] = L.rank[Bt[bi]];
@@ -766,22 +774,20 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ap.vtotal = vbase;
   HS_CUDA(cudaMalloc(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1)));
   // patch vector offsets (stored as integers) into absolute addresses
-  std::vector<int64_t> lvl_of_local;
   {
+    auto end_of = [&](const std::vector<int32_t>& starts, int l, size_t total) {
+      return l + 1 < (int)starts.size() ? (size_t)starts[l + 1] : total;
+    };
     for (int l = 0; l < an->L_top; ++l) {
       double* base = ap.d_y + ap.vbase[l];
-      for (const auto& b : ap.batches[l]) {
-        for (int32_t i = b.local_begin; i < b.local_end; ++i) {
-          ApplyLocal& a = ap.local[i];
-          a.y = base + (uintptr_t)a.y;
-          for (int32_t k = a.nb_begin; k < a.nb_end; ++k) ap.nb[k].xq = base + (uintptr_t)ap.nb[k].xq;
-        }
-        for (int32_t t = b.tgt_begin; t < b.tgt_end; ++t) {
-          ApplyTarget& tg = ap.tgt[t];
-          tg.yq = base + (uintptr_t)tg.yq;
-          for (int32_t c = tg.c_begin; c < tg.c_end; ++c) ap.con[c].yf = base + (uintptr_t)ap.con[c].yf;
-        }
-      }
+      for (size_t i = ap.lvl_local[l]; i < end_of(ap.lvl_local, l, ap.local.size()); ++i)
+        ap.local[i].y = base + (uintptr_t)ap.local[i].y;
+      for (size_t i = ap.lvl_nb[l]; i < end_of(ap.lvl_nb, l, ap.nb.size()); ++i)
+        ap.nb[i].xq = base + (uintptr_t)ap.nb[i].xq;
+      for (size_t i = ap.lvl_con[l]; i < end_of(ap.lvl_con, l, ap.con.size()); ++i)
+        ap.con[i].yf = base + (uintptr_t)ap.con[i].yf;
+      for (size_t i = ap.lvl_tgt[l]; i < end_of(ap.lvl_tgt, l, ap.tgt.size()); ++i)
+        ap.tgt[i].yq = base + (uintptr_t)ap.tgt[i].yq;
     }
   }
   auto up = [&](auto& vec, auto*& dptr) {
@@ -794,6 +800,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   up(ap.nb, ap.d_nb);
   up(ap.tgt, ap.d_tgt);
   up(ap.con, ap.d_con);
+  up(ap.chunks, ap.d_chunks);
+  HS_CUDA(cudaMalloc(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1)));
   ap.d_tsrc.assign(an->L_top, nullptr);
   ap.d_tdst.assign(an->L_top, nullptr);
   for (int l = 0; l < an->L_top; ++l) {

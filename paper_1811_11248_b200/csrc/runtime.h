@@ -57,6 +57,7 @@ struct ApplyBatch {
   int64_t cap_fwd = 0;                  // dynamic smem (doubles) of the forward local kernel
   int32_t kn_bwd = 0;                   // x_n staging size of the backward kernel
   int64_t cap_bwd = 0;                  // total dynamic smem (doubles) of the backward kernel
+  int32_t chunk_begin = 0, chunk_end = 0;   // backward matvec chunks
 };
 
 struct ApplyPlan {
@@ -65,6 +66,11 @@ struct ApplyPlan {
   std::vector<ApplyTarget> tgt;
   std::vector<ApplyContrib> con;
   std::vector<std::vector<ApplyBatch>> batches;   // per level
+  std::vector<int32_t> lvl_local, lvl_nb, lvl_con, lvl_tgt;   // per-level start indices (address patching)
+  std::vector<ApplyChunk> chunks;        // backward matvec column chunks
+  ApplyChunk* d_chunks = nullptr;
+  int64_t max_parts = 0;                 // partial sums of the largest batch
+  double* d_parts = nullptr;
   std::vector<std::vector<int64_t>> trans_src, trans_dst;   // level l -> l+1 vector transition
   // device copies
   ApplyLocal* d_local = nullptr;

@@ -135,9 +135,11 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
       k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
       count_launch(1);
     }
-    for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it)
-      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_nb, it->local_end - it->local_begin, it->kn_bwd,
-                       it->cap_bwd, st);
+    for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it) {
+      launch_apply_bwd_partial(ap.d_local + it->local_begin, ap.d_nb, ap.d_chunks + it->chunk_begin,
+                               it->chunk_end - it->chunk_begin, ap.d_parts, st);
+      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd, st);
+    }
   }
   mark();
   launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);

@@ -123,7 +123,8 @@ __global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, i
 }
 
 // forward: y_q -= C_s[:, col:col+len]^T y_f,s summed over the batch members s with q in n(s)
-// (G_s of Eq. CC:eqn:elim); one warp per target, contributions in source order.
+// (G_s of Eq. CC:eqn:elim); one warp per target, contributions in source order, the K
+// loads of an entry issued back to back.
 __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const ApplyContrib* __restrict__ con, int n) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -136,7 +137,7 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
       const ApplyContrib a = con[c];
       if (i < t.len) {
         const double* Ci = a.C + a.col + i;
-#pragma unroll 4
+#pragma unroll 8
         for (int k = 0; k < a.K; ++k) acc += Ci[(int64_t)k * a.ldC] * __ldg(a.yf + k);
       }
     }
@@ -144,39 +145,76 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
   }
 }
 
-// backward: x_f = y_f - sum_q C_s[:, q] x_q ; x_s <- G^{-T} U [x_c; x_f]
-// one CTA per cluster: all warps form x_f, warp 0 does the local solve.
-__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs, int max_kn,
-                            int64_t cap) {
-  const ApplyLocal it = items[blockIdx.x];
-  if (it.m == 0) return;
-  extern __shared__ double xs[];            // x_n gathered in the column order of C (kn entries)
-  __shared__ double xf[MAX_M];
-  const double *G, *V, *tau;
-  stage_local(it, xs + max_kn, cap - max_kn, G, V, tau);
+// backward stage 1: for BWD_CHUNK columns c of C_s, parts[k] = sum_c C_s[k][c] x_n[c]
+// (x_n[c] read straight from the neighbour's segment); a thread per column, the K rows in
+// groups of 8 independent loads, fixed-order block reduction.
+constexpr int NB_SMEM = 512;
+__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLocal* __restrict__ items,
+                                                                 const ApplyNb* __restrict__ nbs,
+                                                                 const ApplyChunk* __restrict__ chunks,
+                                                                 double* __restrict__ parts) {
+  const ApplyChunk ch = chunks[blockIdx.x];
+  const ApplyLocal it = items[ch.li];
+  __shared__ ApplyNb snb[NB_SMEM];
+  __shared__ double wred[BWD_CHUNK / 32][8];
+  const int nnb = it.nb_end - it.nb_begin;
+  const ApplyNb* nbl = nbs + it.nb_begin;
+  if (nnb <= NB_SMEM) {
+    for (int b = threadIdx.x; b < nnb; b += blockDim.x) snb[b] = nbl[b];
+    __syncthreads();
+    nbl = snb;
+  }
   const int K = it.m - it.r;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int kn = 0;
-  if (K > 0) {
-    // a thread per neighbour descriptor, then its entries: every load is independent
-    for (int b = it.nb_begin + threadIdx.x; b < it.nb_end; b += blockDim.x) {
-      const ApplyNb nb = nbs[b];
-      for (int i = 0; i < nb.len; ++i) xs[nb.col + i] = nb.xq[i];
+  const int c = ch.c0 + threadIdx.x;
+  double x = 0.0;
+  if (c < it.kn) {
+    int lo = 0, hi = nnb - 1;   // last neighbour with col <= c
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (nbl[mid].col <= c) lo = mid;
+      else hi = mid - 1;
     }
-    if (it.nb_end > it.nb_begin) {
-      const ApplyNb last = nbs[it.nb_end - 1];
-      kn = last.col + last.len;
+    x = nbl[lo].xq[c - nbl[lo].col];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Cc = it.C + c;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    double p[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) p[q] = (c < it.kn && k0 + q < K) ? Cc[(int64_t)(k0 + q) * it.ldC] * x : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) p[q] = wsum(p[q]);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) wred[wid][q] = p[q];
+    __syncthreads();
+    if (threadIdx.x < 8 && k0 + threadIdx.x < K) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += wred[w][threadIdx.x];
+      parts[ch.part + k0 + threadIdx.x] = s;
     }
     __syncthreads();
   }
-  for (int k = wid; k < K; k += nw) {
-    const double* Crow = it.C + (int64_t)k * it.ldC;
-    double acc = 0.0;
-    for (int c = lane; c < kn; c += 32) acc += Crow[c] * xs[c];
-    acc = wsum(acc);
-    if (lane == 0) xf[k] = it.y[it.r + k] - acc;
+}
+
+// backward stage 2: x_f = y_f - sum_chunks parts (fixed order) ; x_s <- G^{-T} U [x_c; x_f]
+// (S_s^T E_s^T G_s^T of W_s^T, Alg. 2 backward substitution); one CTA per cluster.
+__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const double* __restrict__ parts, int64_t cap) {
+  const ApplyLocal it = items[blockIdx.x];
+  if (it.m == 0) return;
+  extern __shared__ double sm[];
+  __shared__ double xf[MAX_M];
+  const double *G, *V, *tau;
+  stage_local(it, sm, cap, G, V, tau);
+  const int K = it.m - it.r;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nch = (it.nb_end > it.nb_begin && K > 0) ? (it.kn + BWD_CHUNK - 1) / BWD_CHUNK : 0;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nch; ++q) s += parts[it.part_off + (int64_t)q * K + k];
+    xf[k] = it.y[it.r + k] - s;
   }
-  __syncthreads();
+  __syncthreads();   // staged G/V and x_f visible
   if (wid != 0) return;
   double y[SLOTS];
 #pragma unroll
@@ -251,8 +289,8 @@ static void set_dyn_smem(const void* f, size_t bytes, size_t& configured) {
 
 void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st) {
   if (n <= 0) return;
-  static size_t configured = 48 * 1024;
-  const size_t sm = sizeof(double) * (size_t)cap;
+  static size_t configured = 0;
+  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
   set_dyn_smem((const void*)k_apply_fwd_local, sm, configured);
   k_apply_fwd_local<<<n, 128, sm, st>>>(d, n, cap);
   count_launch(1);
@@ -262,12 +300,18 @@ void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n
   k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
   count_launch(1);
 }
-void launch_apply_bwd(const ApplyLocal* d, const ApplyNb* nb, int n, int max_kn, int64_t cap, cudaStream_t st) {
+void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb, const ApplyChunk* ch, int n,
+                              double* parts, cudaStream_t st) {
   if (n <= 0) return;
-  static size_t configured = 48 * 1024;
+  k_apply_bwd_partial<<<n, BWD_CHUNK, 0, st>>>(d_local_batch, nb, ch, parts);
+  count_launch(1);
+}
+void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st) {
+  if (n <= 0) return;
+  static size_t configured = 0;
   const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
   set_dyn_smem((const void*)k_apply_bwd, sm, configured);
-  k_apply_bwd<<<n, 256, sm, st>>>(d, nb, max_kn, cap);
+  k_apply_bwd<<<n, 128, sm, st>>>(d, parts, cap);
   count_launch(1);
 }
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {
