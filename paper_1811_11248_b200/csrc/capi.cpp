@@ -105,6 +105,12 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
     HS_CUDA(cudaSetDevice(device));
     HS_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
+    // keep freed factor memory in the stream-ordered pool: re-factoring reuses it without
+    // going back to the driver (cudaFree of GB-sized arenas synchronises and is slow)
+    cudaMemPool_t pool;
+    HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     *out = h;
   });
 }

@@ -23,13 +23,13 @@ namespace hs {
 
 void DevScratch::ensure(size_t bytes) {
   if (bytes <= cap) return;
-  if (d) cudaFree(d);
+  if (d) cudaFreeAsync(d, st);
   d = nullptr;
   cap = std::max(bytes, cap * 2);
-  HS_CUDA(cudaMalloc(&d, cap));
+  HS_CUDA(cudaMallocAsync(&d, cap, st));
 }
 DevScratch::~DevScratch() {
-  if (d) cudaFree(d);
+  if (d) cudaFreeAsync(d, st);
 }
 void HostStage::ensure(size_t bytes) {
   if (bytes <= cap) return;
@@ -44,45 +44,17 @@ HostStage::~HostStage() {
 
 namespace {
 
-// Uploads a set of host vectors into one device scratch region with one memcpy.
-struct Upload {
-  HostStage stage;
-  DevScratch dev;
-  std::vector<std::pair<size_t, size_t>> parts;   // (offset, bytes)
-  size_t total = 0;
-  void reset() {
-    parts.clear();
-    total = 0;
-  }
-  template <class T>
-  size_t add(const std::vector<T>& v) {
-    const size_t off = (total + 255) & ~size_t(255);
-    parts.push_back({off, v.size() * sizeof(T)});
-    total = off + v.size() * sizeof(T);
-    return parts.size() - 1;
-  }
-  template <class T>
-  void copy_in(size_t idx, const std::vector<T>& v) {
-    if (!v.empty()) std::memcpy(stage.h + parts[idx].first, v.data(), v.size() * sizeof(T));
-  }
-  template <class T>
-  T* dptr(size_t idx) {
-    return reinterpret_cast<T*>(dev.d + parts[idx].first);
-  }
-  void send(cudaStream_t st) {
-    if (total) HS_CUDA(cudaMemcpyAsync(dev.d, stage.h, total, cudaMemcpyHostToDevice, st));
-  }
-};
-
 struct BlockStore {
   double* d = nullptr;
   std::vector<int32_t> cap;
   std::vector<std::vector<std::pair<int32_t, int64_t>>> rows;   // p -> sorted (q <= p, offset)
   size_t total = 0;
+  cudaStream_t st = nullptr;       // stream-ordered pool allocations
 
-  void build(const std::vector<int32_t>& caps, const Adj& edges) {
+  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream) {
+    st = stream;
     layout(caps, edges);
-    if (total) HS_CUDA(cudaMalloc(&d, total * sizeof(double)));
+    if (total) HS_CUDA(cudaMallocAsync(&d, total * sizeof(double), st));
   }
   void layout(const std::vector<int32_t>& caps, const Adj& edges) {
     cap = caps;
@@ -128,7 +100,7 @@ struct BlockStore {
   int32_t* d_q = nullptr;
   int64_t* d_off = nullptr;
   int32_t* d_cap = nullptr;
-  void upload_dir(cudaStream_t st) {
+  void upload_dir() {
     const int n = (int)cap.size();
     std::vector<int64_t> ptr(n + 1, 0), off;
     std::vector<int32_t> qq;
@@ -139,10 +111,10 @@ struct BlockStore {
       }
       ptr[p + 1] = (int64_t)qq.size();
     }
-    HS_CUDA(cudaMalloc(&d_ptr, sizeof(int64_t) * (n + 1)));
-    HS_CUDA(cudaMalloc(&d_q, sizeof(int32_t) * std::max<size_t>(qq.size(), 1)));
-    HS_CUDA(cudaMalloc(&d_off, sizeof(int64_t) * std::max<size_t>(off.size(), 1)));
-    HS_CUDA(cudaMalloc(&d_cap, sizeof(int32_t) * std::max(n, 1)));
+    HS_CUDA(cudaMallocAsync(&d_ptr, sizeof(int64_t) * (n + 1), st));
+    HS_CUDA(cudaMallocAsync(&d_q, sizeof(int32_t) * std::max<size_t>(qq.size(), 1), st));
+    HS_CUDA(cudaMallocAsync(&d_off, sizeof(int64_t) * std::max<size_t>(off.size(), 1), st));
+    HS_CUDA(cudaMallocAsync(&d_cap, sizeof(int32_t) * std::max(n, 1), st));
     HS_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(d_q, qq.data(), sizeof(int32_t) * qq.size(), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
@@ -152,7 +124,7 @@ struct BlockStore {
   BlockDir dir() const { return BlockDir{d, d_ptr, d_q, d_off, d_cap}; }
   void release() {
     for (void* p : {(void*)d, (void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, st);
     forget();
   }
   void forget() {
@@ -216,8 +188,9 @@ void check_status(DevStatus* d_status, DevStatus* h_status, cudaStream_t st) {
 
 hs_factor_s::~hs_factor_s() {
   using namespace hs;
-  auto fr = [](void* p) {
-    if (p) cudaFree(p);
+  cudaStream_t st = h ? h->stream : nullptr;
+  auto fr = [st](void* p) {
+    if (p) cudaFreeAsync(p, st);
   };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
@@ -290,6 +263,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->an = an;
   f->opt = opt;
   double t_plan = 0.0;
+  double t_sub[4] = {0, 0, 0, 0};
+  double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
   cudaEvent_t ev0, ev1;
   HS_CUDA(cudaEventCreate(&ev0));
   HS_CUDA(cudaEventCreate(&ev1));
@@ -297,7 +272,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->d_rowptr = an->d_rowptr;      // borrowed from the analysis
   f->d_colind = an->d_colind;
   f->d_perm = an->d_perm;
-  HS_CUDA(cudaMalloc(&f->d_vals, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  HS_CUDA(cudaMallocAsync(&f->d_vals, sizeof(double) * std::max<int64_t>(nnz, 1), st));
   HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz,
                           opt.values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
 
@@ -318,12 +293,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   std::vector<int32_t> cap(nleaf0);
   for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
   BlockStore bs;
-  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top);
+  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st);
   if (bs.total) HS_CUDA(cudaMemsetAsync(bs.d, 0, bs.total * sizeof(double), st));
   launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
-  if (an->L_top > 0) bs.upload_dir(st);
+  if (an->L_top > 0) bs.upload_dir();
 
-  Upload upA, upB;
+  Upload& upA = h->upA;   // persistent per handle: pinned staging is allocated once
+  Upload& upB = h->upB;
+  upA.dev.st = st;
+  upB.dev.st = st;
   int32_t* d_rank = nullptr;
   int32_t* h_rank = nullptr;
   int max_batch = 1;
@@ -385,8 +363,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       oP[s] = ioff; ioff += m;
     }
     L.arena_bytes = (size_t)off * sizeof(double);
-    HS_CUDA(cudaMalloc(&L.arena, std::max<size_t>(L.arena_bytes, 8)));
-    HS_CUDA(cudaMalloc(&L.iarena, std::max<size_t>(sizeof(int32_t) * ioff, 4)));
+    HS_CUDA(cudaMallocAsync(&L.arena, std::max<size_t>(L.arena_bytes, 8), st));
+    HS_CUDA(cudaMallocAsync(&L.iarena, std::max<size_t>(sizeof(int32_t) * ioff, 4), st));
     L.G.resize(lev.nclus); L.V.resize(lev.nclus); L.tau.resize(lev.nclus); L.B.resize(lev.nclus);
     L.nu.resize(lev.nclus); L.piv.resize(lev.nclus);
     for (int s = 0; s < lev.nclus; ++s) {
@@ -471,6 +449,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<double*> id_ptr;
       std::vector<int32_t> id_ld, id_r;
       ApplyBatch abt{};
+      double tq_prev = now_s();
       abt.local_begin = (int32_t)ap.local.size();
       abt.tgt_begin = (int32_t)ap.tgt.size();
       std::vector<std::pair<int32_t, std::vector<ApplyContrib>>> atgt;   // forward scatter, first-touch order
@@ -519,6 +498,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           for (int ti = 0; ti < T; ++ti)
             for (int tj = 0; tj <= ti; ++tj) waves[w].push_back(SchurTile2{si, ti * 64, tj * 64, 0});
         }
+        const double tq0 = now_s();
+        t_sub[0] += tq0 - tq_prev;
         // write-back of row s: [I_r | coarse-w | coarse-n]
         if (r > 0) {
           double* p; int32_t ld, tr;
@@ -535,6 +516,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               col += live[q];
             }
         }
+        const double tq1 = now_s();
+        t_sub[1] += tq1 - tq0;
         // apply plan: local item (+ backward neighbour list) and forward scatter contributions
         ApplyLocal al{};
         al.G = L.G[s]; al.V = L.V[s]; al.tau = L.tau[s];
@@ -564,7 +547,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         if (K > 0) ap.max_kn = std::max(ap.max_kn, kn);
         al.y = reinterpret_cast<double*>((uintptr_t)L.voff[s]);
         ap.local.push_back(al);
+        tq_prev = now_s();
+        t_sub[2] += tq_prev - tq1;
       }
+      const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
       std::vector<SchurTile2> tiles;
       std::vector<int32_t> wave_off(1, 0);
@@ -599,6 +585,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       ap.batches[l].push_back(abt);
       for (int bi = 0; bi < nb; ++bi) live[Bt[bi]] = L.rank[Bt[bi]];
+      t_sub[3] += now_s() - tq3;
       upB.reset();
       const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
                    jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r);
@@ -645,25 +632,29 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (int P = 0; P < nP; ++P) capn[P] = L.rank[2 * P] + L.rank[2 * P + 1];
     const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
     BlockStore nbs;
-    nbs.build(capn, En);
+    nbs.build(capn, En, st);
     if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
+    // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
+    // (c odd ? r(2P) : 0, d odd ? r(2Q) : 0); the upper child pair of a parent diagonal
+    // block never occurs (c >= d), matching its lower-triangle semantics
     std::vector<CopyItem> asmb;
-    for (int P = 0; P < nP; ++P)
-      for (const auto& qo : nbs.rows[P]) {
-        const int32_t Q = qo.first;
-        double* dst = nbs.d + qo.second;
+    for (int32_t c = 0; c < lev.nclus; ++c) {
+      if (L.rank[c] == 0) continue;
+      const int32_t P = c >> 1;
+      const auto& prow = nbs.rows[P];
+      size_t pi = 0;
+      for (const auto& dof : bs.rows[c]) {
+        const int32_t d = dof.first;
+        if (L.rank[d] == 0) continue;
+        const int32_t Q = d >> 1;
+        while (pi < prow.size() && prow[pi].first < Q) ++pi;   // d ascending -> Q ascending
+        if (pi == prow.size() || prow[pi].first != Q) fail(HS_E_INTERNAL, "assembly: parent block missing");
         const int32_t dld = capn[Q];
-        for (int a = 0; a < 2; ++a)
-          for (int b = 0; b < 2; ++b) {
-            const int32_t c = 2 * P + a, d = 2 * Q + b;
-            if (P == Q && a < b) continue;   // upper part of a diagonal block (lower semantics)
-            if (L.rank[c] == 0 || L.rank[d] == 0 || !bs.has(c, d)) continue;
-            double* p; int32_t ld, tr;
-            bs.get(c, d, p, ld, tr);
-            const int32_t ro = a ? L.rank[2 * P] : 0, co = b ? L.rank[2 * Q] : 0;
-            asmb.push_back(CopyItem{p, dst + (int64_t)ro * dld + co, ld, dld, L.rank[c], L.rank[d], tr, 0});
-          }
+        const int32_t ro = (c & 1) ? L.rank[2 * P] : 0, co = (d & 1) ? L.rank[2 * Q] : 0;
+        asmb.push_back(CopyItem{bs.d + dof.second, nbs.d + prow[pi].second + (int64_t)ro * dld + co, cap[d], dld,
+                                L.rank[c], L.rank[d], 0, 0});
       }
+    }
     // forward vector transition (children's coarse entries -> parent segment)
     int64_t pofs = 0;
     for (int P = 0; P < nP; ++P)
@@ -680,6 +671,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     upA.dev.ensure(upA.total);
     upA.copy_in(iA, asmb);
     t_plan += now_s() - tp2;
+    t_trans += now_s() - tp2;
     upA.send(st);
     HS_CUDA(cudaEventRecord(pt.a[0], st));
     launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
@@ -690,7 +682,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     bs.release();
     bs = std::move(nbs);
     nbs.forget();
-    if (l + 1 < an->L_top) bs.upload_dir(st);
+    if (l + 1 < an->L_top) bs.upload_dir();
     cap = capn;
     if (prof) {
       int64_t sm = 0, sr = 0, skn = 0, skw = 0, mx = 0;
@@ -720,7 +712,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     ap.vbase.push_back(vbase);
     vbase += N;
     if (N > 0) {
-      HS_CUDA(cudaMalloc(&f->d_top, sizeof(double) * N * N));
+      HS_CUDA(cudaMallocAsync(&f->d_top, sizeof(double) * N * N, st));
       HS_CUDA(cudaMemsetAsync(f->d_top, 0, sizeof(double) * N * N, st));
       std::vector<CopyItem> items;
       for (int P = 0; P < ntc; ++P)
@@ -760,6 +752,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   cudaEventDestroy(ev1);
   S.t_factor_s = ms * 1e-3;
   S.t_phase_s[7] = t_plan;
+  if (std::getenv("HS_PROFILE"))
+    std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
+                 1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
   S.n_levels = an->L_top;
   // factor bytes: G (m^2/2), V (m r), tau, C ((m - r) kn) per cluster + top (N^2/2)
   double fb = 0.0;
@@ -772,7 +767,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   S.factor_bytes = fb;
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
-  HS_CUDA(cudaMalloc(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1)));
+  HS_CUDA(cudaMallocAsync(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1), st));
   // patch vector offsets (stored as integers) into absolute addresses
   {
     auto end_of = [&](const std::vector<int32_t>& starts, int l, size_t total) {
@@ -793,7 +788,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   auto up = [&](auto& vec, auto*& dptr) {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
     if (vec.empty()) return;
-    HS_CUDA(cudaMalloc(&dptr, sizeof(T) * vec.size()));
+    HS_CUDA(cudaMallocAsync(&dptr, sizeof(T) * vec.size(), st));
     HS_CUDA(cudaMemcpyAsync(dptr, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice, st));
   };
   up(ap.local, ap.d_local);
@@ -801,7 +796,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   up(ap.tgt, ap.d_tgt);
   up(ap.con, ap.d_con);
   up(ap.chunks, ap.d_chunks);
-  HS_CUDA(cudaMalloc(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1)));
+  HS_CUDA(cudaMallocAsync(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1), st));
   ap.d_tsrc.assign(an->L_top, nullptr);
   ap.d_tdst.assign(an->L_top, nullptr);
   for (int l = 0; l < an->L_top; ++l) {

@@ -389,10 +389,8 @@ __global__ void __launch_bounds__(CPQR2_THREADS) k_cpqr2(const CluItem* __restri
   const int ldw = sm ? chunk : ld;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (sm)
-    for (int e = tid; e < m * nloc; e += blockDim.x) {
-      const int l = e / nloc, c = e % nloc;
-      W[l * ldw + c] = it.B[(int64_t)l * ld + c_lo + c];
-    }
+    for (int l = 0; l < m; ++l)
+      for (int c = tid; c < nloc; c += blockDim.x) W[l * ldw + c] = it.B[(int64_t)l * ld + c_lo + c];
   __syncthreads();
   double lrow = 0.0;
   for (int c = tid; c < nloc; c += blockDim.x) {
@@ -522,9 +520,11 @@ __global__ void __launch_bounds__(CPQR2_THREADS) k_cpqr2(const CluItem* __restri
       double* Wc = W + c;
       double d = 0.0;
       if (tau != 0.0)
+#pragma unroll 8
         for (int l = j; l < m; ++l) d += vloc[l] * Wc[(int64_t)l * ldw];
       const double td = tau * d;
       double s = 0.0;
+#pragma unroll 8
       for (int l = j; l < m; ++l) {
         double b = Wc[(int64_t)l * ldw];
         if (tau != 0.0) {
@@ -542,10 +542,8 @@ __global__ void __launch_bounds__(CPQR2_THREADS) k_cpqr2(const CluItem* __restri
     for (int l = fix_j + tid; l < m; l += blockDim.x) W[(int64_t)l * ldw + fix_p] = (l == fix_j) ? fix_beta : 0.0;
   __syncthreads();
   if (sm)
-    for (int e = tid; e < m * nloc; e += blockDim.x) {
-      const int l = e / nloc, c = e % nloc;
-      it.B[(int64_t)l * ld + c_lo + c] = W[l * ldw + c];
-    }
+    for (int l = 0; l < m; ++l)
+      for (int c = tid; c < nloc; c += blockDim.x) it.B[(int64_t)l * ld + c_lo + c] = W[l * ldw + c];
   if (crank == 0 && tid == 0) rank_out[item] = r;
 }
 
@@ -834,16 +832,22 @@ int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, do
                                  (int)CPQR2_SMEM_BUDGET + 8192));
     attr = true;
   }
-  int CS = 1;
-  while (CS < 16 && (int64_t)n * CS < 296 && maxcol / (2 * CS) >= 32) CS *= 2;
-  for (;;) {
+  auto smem_for = [&](int cs) {
     size_t smem = 8;
     for (const auto& it : h_items) {
       if (it.m == 0 || it.kw == 0) continue;
-      const int chunk = (it.kw + it.kn + CS - 1) / CS;
+      const int chunk = (it.kw + it.kn + cs - 1) / cs;
       const size_t need = (cpqr2_smem_mode(it.m, chunk) ? ((size_t)it.m * chunk + chunk) : (size_t)chunk) * sizeof(double);
       smem = std::max(smem, need);
     }
+    return smem;
+  };
+  // The per-step critical path is each CTA's column loop, so split the columns as far
+  // as the barrier/DSMEM overhead allows (>= 64 columns per CTA), up to 16 CTAs.
+  int CS = 1;
+  while (CS < 16 && maxcol / (2 * CS) >= 64) CS *= 2;
+  for (;;) {
+    const size_t smem = smem_for(CS);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

@@ -8,13 +8,6 @@
 #include "device.h"
 #include "internal.h"
 
-struct hs_handle_s {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  int world = 1, rank = 0;
-  std::string err;
-};
 
 struct hs_analysis_s {
   hs::Analysis* an = nullptr;
@@ -26,6 +19,7 @@ namespace hs {
 struct DevScratch {
   char* d = nullptr;
   size_t cap = 0;
+  cudaStream_t st = nullptr;   // stream-ordered pool allocation
   void ensure(size_t bytes);
   ~DevScratch();
 };
@@ -37,6 +31,36 @@ struct HostStage {
   size_t used = 0;
   void ensure(size_t bytes);
   ~HostStage();
+};
+
+// Uploads a set of host vectors into one device scratch region with one memcpy.
+struct Upload {
+  HostStage stage;
+  DevScratch dev;
+  std::vector<std::pair<size_t, size_t>> parts;   // (offset, bytes)
+  size_t total = 0;
+  void reset() {
+    parts.clear();
+    total = 0;
+  }
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = (total + 255) & ~size_t(255);
+    parts.push_back({off, v.size() * sizeof(T)});
+    total = off + v.size() * sizeof(T);
+    return parts.size() - 1;
+  }
+  template <class T>
+  void copy_in(size_t idx, const std::vector<T>& v) {
+    if (!v.empty()) std::memcpy(stage.h + parts[idx].first, v.data(), v.size() * sizeof(T));
+  }
+  template <class T>
+  T* dptr(size_t idx) {
+    return reinterpret_cast<T*>(dev.d + parts[idx].first);
+  }
+  void send(cudaStream_t st) {
+    if (total) HS_CUDA(cudaMemcpyAsync(dev.d, stage.h, total, cudaMemcpyHostToDevice, st));
+  }
 };
 
 struct LevelRT {
@@ -89,6 +113,15 @@ struct ApplyPlan {
 };
 
 }  // namespace hs
+
+struct hs_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int world = 1, rank = 0;
+  std::string err;
+  hs::Upload upA, upB;          // descriptor staging, reused across factors
+};
 
 struct hs_factor_s {
   hs_handle_s* h = nullptr;

@@ -79,6 +79,18 @@ class hs_pcg_report(C.Structure):
 
 
 _lib = None
+_exiting = False
+
+
+def _at_exit():
+    # Handles, analyses and factors are not released during interpreter shutdown: the
+    # CUDA runtime may already be torn down and object finalisation order is arbitrary.
+    global _exiting
+    _exiting = True
+
+
+import atexit  # noqa: E402
+atexit.register(_at_exit)
 
 
 def lib():
@@ -142,7 +154,7 @@ class Handle:
         self.ptr = ptr
 
     def __del__(self):
-        if self.ptr and _lib is not None:
+        if self.ptr and _lib is not None and not _exiting:
             _lib.hs_destroy(self.ptr)
             self.ptr = None
 
@@ -153,7 +165,7 @@ class Analysis:
         self._keep = keep
 
     def __del__(self):
-        if self.ptr and _lib is not None:
+        if self.ptr and _lib is not None and not _exiting:
             _lib.hs_analysis_destroy(self.ptr)
             self.ptr = None
 
@@ -166,7 +178,7 @@ class Factor:
         self.n = n
 
     def __del__(self):
-        if self.ptr and _lib is not None:
+        if self.ptr and _lib is not None and not _exiting:
             _lib.hs_factor_destroy(self.ptr)
             self.ptr = None
 
