@@ -131,6 +131,15 @@ hs_status hs_set_stream(hs_handle h, void* stream) {
 
 void hs_destroy(hs_handle h) {
   if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  // release the staging buffers while their stream is still alive (stream-ordered frees)
+  for (hs::Upload* u : {&h->upA, &h->upB}) {
+    if (u->dev.d) cudaFreeAsync(u->dev.d, u->dev.st);
+    u->dev.d = nullptr;
+    u->dev.cap = 0;
+  }
+  if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

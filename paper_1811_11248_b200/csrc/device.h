@@ -140,18 +140,19 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
                  cudaStream_t st);
 constexpr int TOP_NB = 64;
 
-void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st);
+void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, int max_m, cudaStream_t st);
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
 // backward, stage 1: partial sums of C x_n over column chunks (many CTAs per cluster)
 void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb, const ApplyChunk* ch, int n,
                               double* parts, cudaStream_t st);
 // backward, stage 2: x_f = y_f - sum of the partials (fixed order), x_s <- G^{-T} U [x_c; x_f]
-void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st);
+void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, int max_m, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,
                  int64_t n, cudaStream_t st);
 
-constexpr int MAX_M = 128;   // largest cluster handled by the single-CTA POTRF/TRSM/apply kernels
+constexpr int MAX_M = 512;   // largest cluster the kernels handle (HS_E_UNSUPPORTED beyond)
+constexpr int SMEM_M = 128;  // POTRF/TRSM stage the whole G in shared memory up to this size
 
 }  // namespace hs

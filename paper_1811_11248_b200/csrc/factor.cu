@@ -414,7 +414,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             }
             col += live[q];
           }
-        for (int32_t c0 = 0; c0 < ldB; c0 += 64) trsm.push_back(TrsmItem{bi, c0, std::min(64, ldB - c0), 0});
+        const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
+        for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
         S.flops += (double)m * m * m / 3.0 + (double)m * m * ldB;
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
@@ -580,6 +581,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           const ApplyLocal& a = ap.local[i];
           const int64_t need = (int64_t)a.m * a.m + (int64_t)a.m * a.r + a.r;
           if (need <= LIM) abt.cap_fwd = std::max(abt.cap_fwd, need);
+          abt.max_m = std::max(abt.max_m, a.m);
         }
         abt.cap_bwd = abt.cap_fwd;
       }

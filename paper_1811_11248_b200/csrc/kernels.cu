@@ -165,8 +165,55 @@ __device__ void potrf_core(double* g, int ld, int m, double* a, DevStatus* statu
 __global__ void k_potrf(const CluItem* __restrict__ items, DevStatus* status) {
   extern __shared__ double smem[];
   const CluItem it = items[blockIdx.x];
-  if (it.m == 0) return;
+  if (it.m == 0 || it.m > SMEM_M) return;
   potrf_core(it.G, it.m, it.m, smem, status, it.level, it.cluster);
+}
+
+// a1 for m > SMEM_M: the same right-looking Cholesky in place in global memory (L1/L2
+// resident: <= 2 MB per cluster), 1024 threads.  Coarse clusters only.
+__global__ void __launch_bounds__(1024) k_potrf_gl(const CluItem* __restrict__ items, DevStatus* status) {
+  const CluItem it = items[blockIdx.x];
+  const int m = it.m;
+  if (m <= SMEM_M) return;
+  double* a = it.G;
+  __shared__ int bad;
+  __shared__ double piv;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = a[(int64_t)j * m + j];
+      if (!(d > 0.0)) {
+        bad = 1;
+        if (atomicCAS(&status->flag, 0, 1) == 0) {
+          status->level = it.level;
+          status->cluster = it.cluster;
+          status->pivot = j;
+          status->value = d;
+        }
+      } else {
+        piv = sqrt(d);
+        a[(int64_t)j * m + j] = piv;
+      }
+    }
+    __syncthreads();
+    if (bad) return;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[(int64_t)i * m + j] /= piv;
+    __syncthreads();
+    const int t = m - j - 1;
+    // rows i of the trailing lower triangle: a warp per row, lanes over k <= i
+    for (int i = (threadIdx.x >> 5); i < t; i += (blockDim.x >> 5)) {
+      const int ii = j + 1 + i;
+      const double aij = a[(int64_t)ii * m + j];
+      for (int k = (threadIdx.x & 31); k <= i; k += 32) {
+        const int kk = j + 1 + k;
+        a[(int64_t)ii * m + kk] -= aij * a[(int64_t)kk * m + j];
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)m * m; e += blockDim.x)
+    if ((e % m) > (e / m)) a[e] = 0.0;
 }
 
 __global__ void k_potrf_raw(double* g, int ld, int m, DevStatus* status, int level) {
@@ -178,28 +225,43 @@ __global__ void k_potrf_raw(double* g, int ld, int m, DevStatus* status, int lev
 // a2: X = G^{-1} B for a column tile (<= 64 columns) of B (m x ncols, row-major ld ldB),
 // G lower m x m (ld ldG).  G and the tile live in shared memory; 256 threads =
 // 64 columns x 4 row groups, right-looking forward substitution.
+// Tile width TW = 64 with G staged in smem for m <= SMEM_M; TW = 32 with G read through
+// L1/L2 for larger m (the tile alone then fits: 32 x 512 doubles = 128 KB).
 __device__ void trsm_core(const double* G, int ldG, int m, double* B, int ldB, int c0, int nc, double* sm) {
-  double* g = sm;                 // m*m
-  double* x = sm + m * m;         // m*64
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int i = e / m, k = e % m;
-    g[e] = (k <= i) ? G[(int64_t)i * ldG + k] : 0.0;
+  const bool gs = m <= SMEM_M;
+  const int TW = gs ? 64 : 32;
+  const double* g;
+  int ldg;
+  double* x;
+  if (gs) {
+    double* gg = sm;              // m*m
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = e / m, k = e % m;
+      gg[e] = (k <= i) ? G[(int64_t)i * ldG + k] : 0.0;
+    }
+    g = gg;
+    ldg = m;
+    x = sm + m * m;               // m*TW
+  } else {
+    g = G;
+    ldg = ldG;
+    x = sm;
   }
-  for (int e = threadIdx.x; e < m * 64; e += blockDim.x) {
-    const int i = e >> 6, c = e & 63;
+  for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+    const int i = e / TW, c = e % TW;
     x[e] = c < nc ? B[(int64_t)i * ldB + c0 + c] : 0.0;
   }
   __syncthreads();
-  const int c = threadIdx.x & 63, grp = threadIdx.x >> 6, ngrp = blockDim.x >> 6;
+  const int c = threadIdx.x % TW, grp = threadIdx.x / TW, ngrp = blockDim.x / TW;
   for (int i = 0; i < m; ++i) {
-    if (grp == 0) x[i * 64 + c] /= g[i * m + i];
+    if (grp == 0) x[i * TW + c] /= g[(int64_t)i * ldg + i];
     __syncthreads();
-    const double xi = x[i * 64 + c];
-    for (int l = i + 1 + grp; l < m; l += ngrp) x[l * 64 + c] -= g[l * m + i] * xi;
+    const double xi = x[i * TW + c];
+    for (int l = i + 1 + grp; l < m; l += ngrp) x[l * TW + c] -= g[(int64_t)l * ldg + i] * xi;
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < m * 64; e += blockDim.x) {
-    const int i = e >> 6, cc = e & 63;
+  for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+    const int i = e / TW, cc = e % TW;
     if (cc < nc) B[(int64_t)i * ldB + c0 + cc] = x[e];
   }
 }
@@ -797,14 +859,22 @@ void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double*
 }
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st) {
   if (n <= 0) return;
-  const size_t sm = (size_t)max_m * max_m * sizeof(double);
+  const int ms = std::min(max_m, SMEM_M);
+  const size_t sm = (size_t)ms * ms * sizeof(double);
   set_smem((const void*)k_potrf, sm);
   k_potrf<<<n, 256, sm, st>>>(d_items, status);
   count_launch(1);
+  if (max_m > SMEM_M) {
+    k_potrf_gl<<<n, 1024, 0, st>>>(d_items, status);
+    count_launch(1);
+  }
 }
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st) {
   if (n <= 0) return;
-  const size_t sm = ((size_t)max_m * max_m + (size_t)max_m * 64) * sizeof(double);
+  const int ms = std::min(max_m, SMEM_M);
+  size_t words = (size_t)ms * ms + (size_t)ms * 64;
+  if (max_m > SMEM_M) words = std::max(words, (size_t)max_m * 32);
+  const size_t sm = words * sizeof(double);
   set_smem((const void*)k_trsm, sm);
   k_trsm<<<n, 256, sm, st>>>(d_clu, d_items);
   count_launch(1);

@@ -82,6 +82,7 @@ struct ApplyBatch {
   int32_t kn_bwd = 0;                   // x_n staging size of the backward kernel
   int64_t cap_bwd = 0;                  // total dynamic smem (doubles) of the backward kernel
   int32_t chunk_begin = 0, chunk_end = 0;   // backward matvec chunks
+  int32_t max_m = 0;                        // largest cluster of the batch (kernel variant)
 };
 
 struct ApplyPlan {

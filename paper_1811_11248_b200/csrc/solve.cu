@@ -117,7 +117,7 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   for (int l = 0; l < an->L_top; ++l) {
     mark();
     for (const auto& b : ap.batches[l]) {
-      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, st);
+      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, b.max_m, st);
       launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
     }
     const int64_t nt = (int64_t)ap.trans_src[l].size();
@@ -138,7 +138,8 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
     for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it) {
       launch_apply_bwd_partial(ap.d_local + it->local_begin, ap.d_nb, ap.d_chunks + it->chunk_begin,
                                it->chunk_end - it->chunk_begin, ap.d_parts, st);
-      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd, st);
+      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd,
+                       it->max_m, st);
     }
   }
   mark();

@@ -10,7 +10,6 @@ namespace hs {
 
 namespace {
 
-constexpr int SLOTS = MAX_M / 32;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -19,6 +18,7 @@ __device__ __forceinline__ double wsum(double v) {
 }
 
 // y <- G^{-1} y (G lower, row-major ld m): row-oriented, coalesced row reads
+template <int SLOTS>
 __device__ __forceinline__ void warp_trsv_lower(const double* G, int m, double (&y)[SLOTS], int lane) {
   for (int i = 0; i < m; ++i) {
     double p = 0.0;
@@ -38,6 +38,7 @@ __device__ __forceinline__ void warp_trsv_lower(const double* G, int m, double (
 }
 
 // y <- G^{-T} y : column-oriented backward substitution, rows of G read contiguously
+template <int SLOTS>
 __device__ __forceinline__ void warp_trsv_upper_t(const double* G, int m, double (&y)[SLOTS], int lane) {
   for (int i = m - 1; i >= 0; --i) {
     double xi = 0.0;
@@ -60,6 +61,7 @@ __device__ __forceinline__ void warp_trsv_upper_t(const double* G, int m, double
 }
 
 // apply H_j (j = 0..r-1 forward, r-1..0 backward): y[j:] -= tau_j v_j (v_j . y[j:])
+template <int SLOTS>
 __device__ __forceinline__ void warp_reflect(const double* V, const double* tau, int m, int j, double (&y)[SLOTS],
                                              int lane) {
   const double t = tau[j];
@@ -98,6 +100,7 @@ __device__ __forceinline__ void stage_local(const ApplyLocal& it, double* sm, in
 
 // forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s)
 // one CTA per cluster: the CTA stages the factors, warp 0 solves.
+template <int SLOTS>
 __global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, int64_t cap) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31;
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLoca
 
 // backward stage 2: x_f = y_f - sum_chunks parts (fixed order) ; x_s <- G^{-T} U [x_c; x_f]
 // (S_s^T E_s^T G_s^T of W_s^T, Alg. 2 backward substitution); one CTA per cluster.
+template <int SLOTS>
 __global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const double* __restrict__ parts, int64_t cap) {
   const ApplyLocal it = items[blockIdx.x];
   if (it.m == 0) return;
@@ -287,12 +291,18 @@ static void set_dyn_smem(const void* f, size_t bytes, size_t& configured) {
   }
 }
 
-void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st) {
-  if (n <= 0) return;
+template <int S>
+void fwd_local_s(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st) {
   static size_t configured = 0;
   const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
-  set_dyn_smem((const void*)k_apply_fwd_local, sm, configured);
-  k_apply_fwd_local<<<n, 128, sm, st>>>(d, n, cap);
+  set_dyn_smem((const void*)k_apply_fwd_local<S>, sm, configured);
+  k_apply_fwd_local<S><<<n, 128, sm, st>>>(d, n, cap);
+}
+void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, int max_m, cudaStream_t st) {
+  if (n <= 0) return;
+  if (max_m <= 128) fwd_local_s<4>(d, n, cap, st);
+  else if (max_m <= 256) fwd_local_s<8>(d, n, cap, st);
+  else fwd_local_s<16>(d, n, cap, st);
   count_launch(1);
 }
 void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st) {
@@ -306,12 +316,18 @@ void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb
   k_apply_bwd_partial<<<n, BWD_CHUNK, 0, st>>>(d_local_batch, nb, ch, parts);
   count_launch(1);
 }
-void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st) {
-  if (n <= 0) return;
+template <int S>
+void bwd_s(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st) {
   static size_t configured = 0;
   const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
-  set_dyn_smem((const void*)k_apply_bwd, sm, configured);
-  k_apply_bwd<<<n, 128, sm, st>>>(d, parts, cap);
+  set_dyn_smem((const void*)k_apply_bwd<S>, sm, configured);
+  k_apply_bwd<S><<<n, 128, sm, st>>>(d, parts, cap);
+}
+void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, int max_m, cudaStream_t st) {
+  if (n <= 0) return;
+  if (max_m <= 128) bwd_s<4>(d, parts, n, cap, st);
+  else if (max_m <= 256) bwd_s<8>(d, parts, n, cap, st);
+  else bwd_s<16>(d, parts, n, cap, st);
   count_launch(1);
 }
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {

@@ -125,7 +125,19 @@ CASES = TINY + [
     ("3d-24", lambda: gen_laplace3d(24, leaf_size=27), {}),
     ("slab-32", lambda: gen_slab(32, 6, leaf_columns=4), {}),
     ("q1-12", lambda: gen_stokes_q1(12, 10, 5, leaf_columns=2), {}),
+    # clusters larger than the shared-memory POTRF/TRSM limit (m = 216 at level 0, up to 432 above)
+    ("3d-12-bigleaf", lambda: gen_laplace3d(12, leaf_size=216), dict(top_log2=1, nsub_log2=1)),
 ]
+
+
+def test_eps0_big_clusters(H, handle):
+    p = gen_laplace3d(12, leaf_size=216)
+    an, _, a, f, _ = _both(H, handle, p, 0.0, dict(top_log2=1, nsub_log2=1))
+    A = p.to_scipy().toarray()
+    x_ref = sla.cho_solve(sla.cho_factor(A), p.b)
+    x = H.hs_apply(f, p.b)
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-12
+    assert H.hs_factor_get_stats(f)["max_m"] > 128
 
 
 @pytest.mark.parametrize("eps", [1e-2, 1e-1, 1e-4])
