@@ -107,6 +107,20 @@ struct ApplyContrib {
   const double* yf;          // y_f,s
   int32_t ldC, K, col, pad;
 };
+struct ApplyBatchDev {       // a batch's item ranges in the apply arrays
+  int32_t local_begin, local_end, tgt_begin, tgt_end, chunk_begin, chunk_end;
+};
+struct ApplyLevelArgs {      // one level of the apply, swept by one cooperative kernel
+  const ApplyBatchDev* batches;
+  int32_t nbatch, pad;
+  const ApplyLocal* local;
+  const ApplyTarget* tgt;
+  const ApplyContrib* con;
+  const ApplyNb* nb;
+  const ApplyChunk* chunks;
+  double* parts;
+  int64_t cap;               // dynamic shared memory (doubles) for factor staging
+};
 
 // First error raised on the device (POTRF breakdown).
 struct DevStatus {
@@ -147,6 +161,8 @@ void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb
                               double* parts, cudaStream_t st);
 // backward, stage 2: x_f = y_f - sum of the partials (fixed order), x_s <- G^{-T} U [x_c; x_f]
 void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, int max_m, cudaStream_t st);
+// one cooperative launch per level and direction (grid-wide barriers between batches)
+void launch_apply_level(const ApplyLevelArgs& a, int max_m, int backward, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

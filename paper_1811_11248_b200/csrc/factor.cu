@@ -196,6 +196,7 @@ hs_factor_s::~hs_factor_s() {
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
   fr(ap.d_local); fr(ap.d_nb); fr(ap.d_tgt); fr(ap.d_con); fr(ap.d_y); fr(ap.d_chunks); fr(ap.d_parts);
   for (auto* p : ap.d_tsrc) fr(p);
+  for (auto* p : ap.d_lvl_batches) fr(p);
   for (auto* p : ap.d_tdst) fr(p);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
   fr(d_r); fr(d_z); fr(d_p); fr(d_q); fr(d_x); fr(d_b); fr(d_red);
@@ -798,6 +799,20 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   up(ap.tgt, ap.d_tgt);
   up(ap.con, ap.d_con);
   up(ap.chunks, ap.d_chunks);
+  // per-level batch tables for the cooperative level kernels of the apply
+  ap.d_lvl_batches.assign(an->L_top, nullptr);
+  ap.lvl_max_m.assign(an->L_top, 0);
+  ap.lvl_cap.assign(an->L_top, 0);
+  for (int l = 0; l < an->L_top; ++l) {
+    std::vector<ApplyBatchDev> tb;
+    for (const auto& b : ap.batches[l]) {
+      tb.push_back(ApplyBatchDev{b.local_begin, b.local_end, b.tgt_begin, b.tgt_end, b.chunk_begin, b.chunk_end});
+      ap.lvl_max_m[l] = std::max(ap.lvl_max_m[l], b.max_m);
+      ap.lvl_cap[l] = std::max(ap.lvl_cap[l], std::max(b.cap_fwd, b.cap_bwd));
+    }
+    up(tb, ap.d_lvl_batches[l]);
+    HS_CUDA(cudaStreamSynchronize(st));   // tb is a temporary
+  }
   HS_CUDA(cudaMallocAsync(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1), st));
   ap.d_tsrc.assign(an->L_top, nullptr);
   ap.d_tdst.assign(an->L_top, nullptr);

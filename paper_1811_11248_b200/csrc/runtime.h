@@ -92,6 +92,9 @@ struct ApplyPlan {
   std::vector<ApplyContrib> con;
   std::vector<std::vector<ApplyBatch>> batches;   // per level
   std::vector<int32_t> lvl_local, lvl_nb, lvl_con, lvl_tgt;   // per-level start indices (address patching)
+  std::vector<ApplyBatchDev*> d_lvl_batches;   // per level: the batches' item ranges (device)
+  std::vector<int32_t> lvl_max_m;
+  std::vector<int64_t> lvl_cap;
   std::vector<ApplyChunk> chunks;        // backward matvec column chunks
   ApplyChunk* d_chunks = nullptr;
   int64_t max_parts = 0;                 // partial sums of the largest batch

@@ -101,10 +101,27 @@ void dot(const double* a, const double* b, int64_t n, double* partial, double* o
   count_launch(2);
 }
 
+ApplyLevelArgs level_args(hs_factor_s* f, int l) {
+  ApplyPlan& ap = f->ap;
+  ApplyLevelArgs a{};
+  a.batches = ap.d_lvl_batches[l];
+  a.nbatch = (int32_t)ap.batches[l].size();
+  a.local = ap.d_local;
+  a.tgt = ap.d_tgt;
+  a.con = ap.d_con;
+  a.nb = ap.d_nb;
+  a.chunks = ap.d_chunks;
+  a.parts = ap.d_parts;
+  a.cap = ap.lvl_cap[l];
+  return a;
+}
+
 void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev = nullptr) {
   const Analysis* an = f->an;
   ApplyPlan& ap = f->ap;
   const int64_t n = an->n;
+  // HS_APPLY_PER_BATCH=1: one launch per batch phase instead of one cooperative kernel per level
+  const bool per_batch = std::getenv("HS_APPLY_PER_BATCH") != nullptr;
   auto mark = [&]() {
     if (!ev) return;
     cudaEvent_t e;
@@ -116,9 +133,13 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
     mark();
-    for (const auto& b : ap.batches[l]) {
-      launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, b.max_m, st);
-      launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
+    if (per_batch) {
+      for (const auto& b : ap.batches[l]) {
+        launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, b.max_m, st);
+        launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
+      }
+    } else {
+      launch_apply_level(level_args(f, l), ap.lvl_max_m[l], 0, st);
     }
     const int64_t nt = (int64_t)ap.trans_src[l].size();
     if (nt) {
@@ -135,11 +156,15 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
       k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
       count_launch(1);
     }
-    for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it) {
-      launch_apply_bwd_partial(ap.d_local + it->local_begin, ap.d_nb, ap.d_chunks + it->chunk_begin,
-                               it->chunk_end - it->chunk_begin, ap.d_parts, st);
-      launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd,
-                       it->max_m, st);
+    if (per_batch) {
+      for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it) {
+        launch_apply_bwd_partial(ap.d_local + it->local_begin, ap.d_nb, ap.d_chunks + it->chunk_begin,
+                                 it->chunk_end - it->chunk_begin, ap.d_parts, st);
+        launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd,
+                         it->max_m, st);
+      }
+    } else {
+      launch_apply_level(level_args(f, l), ap.lvl_max_m[l], 1, st);
     }
   }
   mark();

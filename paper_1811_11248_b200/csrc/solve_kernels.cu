@@ -2,6 +2,7 @@
 // CSR SpMV / vector helpers of PCG.  HBM/latency bound: every factor byte is read once
 // per sweep.  A cluster's local solve runs in one warp with lane-owned vector entries
 // (entry l lives in lane l % 32, slot l / 32), so no block barrier is needed.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "device.h"
@@ -98,41 +99,40 @@ __device__ __forceinline__ void stage_local(const ApplyLocal& it, double* sm, in
   tau = sm + mm + mr;
 }
 
-// forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s)
-// one CTA per cluster: the CTA stages the factors, warp 0 solves.
+// The vector y (and the backward partial sums) change inside a level kernel, so they are
+// read with __ldcg (L2, bypassing the non-coherent L1); factor data are read normally.
+// forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s).
+// CTA-level device function (every thread of the CTA calls it): the CTA stages the
+// factors, warp 0 solves.  `sm` is the CTA's dynamic shared memory (cap doubles).
 template <int SLOTS>
-__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, int64_t cap) {
-  extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31;
-  const ApplyLocal it = items[blockIdx.x];
+__device__ void dev_fwd_local(const ApplyLocal& it, double* sm, int64_t cap) {
   if (it.m == 0) return;
+  const int lane = threadIdx.x & 31;
   const double *G, *V, *tau;
   stage_local(it, sm, cap, G, V, tau);
   __syncthreads();
-  if (threadIdx.x >= 32) return;
-  double y[SLOTS];
+  if (threadIdx.x < 32) {
+    double y[SLOTS];
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    y[s] = l < it.m ? it.y[l] : 0.0;
-  }
-  warp_trsv_lower(G, it.m, y, lane);
-  for (int j = 0; j < it.r; ++j) warp_reflect(V, tau, it.m, j, y, lane);
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      y[s] = l < it.m ? __ldcg(it.y + l) : 0.0;
+    }
+    warp_trsv_lower(G, it.m, y, lane);
+    for (int j = 0; j < it.r; ++j) warp_reflect(V, tau, it.m, j, y, lane);
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    if (l < it.m) it.y[l] = y[s];
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      if (l < it.m) it.y[l] = y[s];
+    }
   }
+  __syncthreads();   // smem reusable by the CTA's next item
 }
 
 // forward: y_q -= C_s[:, col:col+len]^T y_f,s summed over the batch members s with q in n(s)
-// (G_s of Eq. CC:eqn:elim); one warp per target, contributions in source order, the K
-// loads of an entry issued back to back.
-__global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const ApplyContrib* __restrict__ con, int n) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (w >= n) return;
-  const ApplyTarget t = tg[w];
+// (G_s of Eq. CC:eqn:elim); warp-level, contributions in source order, the K loads of an
+// entry issued back to back.
+__device__ __forceinline__ void dev_fwd_scatter(const ApplyTarget& t, const ApplyContrib* __restrict__ con, int lane) {
   for (int i0 = 0; i0 < t.len; i0 += 32) {
     const int i = i0 + lane;
     double acc = 0.0;
@@ -141,22 +141,19 @@ __global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const Ap
       if (i < t.len) {
         const double* Ci = a.C + a.col + i;
 #pragma unroll 8
-        for (int k = 0; k < a.K; ++k) acc += Ci[(int64_t)k * a.ldC] * __ldg(a.yf + k);
+        for (int k = 0; k < a.K; ++k) acc += Ci[(int64_t)k * a.ldC] * __ldcg(a.yf + k);
       }
     }
-    if (i < t.len) t.yq[i] -= acc;
+    if (i < t.len) t.yq[i] = __ldcg(t.yq + i) - acc;
   }
 }
 
-// backward stage 1: for BWD_CHUNK columns c of C_s, parts[k] = sum_c C_s[k][c] x_n[c]
-// (x_n[c] read straight from the neighbour's segment); a thread per column, the K rows in
-// groups of 8 independent loads, fixed-order block reduction.
+// backward stage 1 (CTA-level, blockDim == BWD_CHUNK): for BWD_CHUNK columns c of C_s,
+// parts[k] = sum_c C_s[k][c] x_n[c] (x_n[c] read straight from the neighbour's segment); a
+// thread per column, the K rows in groups of 8 independent loads, fixed-order reduction.
 constexpr int NB_SMEM = 512;
-__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLocal* __restrict__ items,
-                                                                 const ApplyNb* __restrict__ nbs,
-                                                                 const ApplyChunk* __restrict__ chunks,
-                                                                 double* __restrict__ parts) {
-  const ApplyChunk ch = chunks[blockIdx.x];
+__device__ void dev_bwd_partial(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs,
+                                const ApplyChunk& ch, double* __restrict__ parts) {
   const ApplyLocal it = items[ch.li];
   __shared__ ApplyNb snb[NB_SMEM];
   __shared__ double wred[BWD_CHUNK / 32][8];
@@ -177,7 +174,7 @@ __global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLoca
       if (nbl[mid].col <= c) lo = mid;
       else hi = mid - 1;
     }
-    x = nbl[lo].xq[c - nbl[lo].col];
+    x = __ldcg(nbl[lo].xq + (c - nbl[lo].col));
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* Cc = it.C + c;
@@ -198,40 +195,95 @@ __global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLoca
     }
     __syncthreads();
   }
+  __syncthreads();   // snb reusable
 }
 
-// backward stage 2: x_f = y_f - sum_chunks parts (fixed order) ; x_s <- G^{-T} U [x_c; x_f]
-// (S_s^T E_s^T G_s^T of W_s^T, Alg. 2 backward substitution); one CTA per cluster.
+// backward stage 2 (CTA-level): x_f = y_f - sum_chunks parts (fixed order) ;
+// x_s <- G^{-T} U [x_c; x_f] (S_s^T E_s^T G_s^T of W_s^T, Alg. 2 backward substitution).
 template <int SLOTS>
-__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const double* __restrict__ parts, int64_t cap) {
-  const ApplyLocal it = items[blockIdx.x];
+__device__ void dev_bwd_local(const ApplyLocal& it, const double* __restrict__ parts, double* sm, int64_t cap) {
   if (it.m == 0) return;
-  extern __shared__ double sm[];
   __shared__ double xf[MAX_M];
   const double *G, *V, *tau;
   stage_local(it, sm, cap, G, V, tau);
   const int K = it.m - it.r;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int nch = (it.nb_end > it.nb_begin && K > 0) ? (it.kn + BWD_CHUNK - 1) / BWD_CHUNK : 0;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double s = 0.0;
-    for (int q = 0; q < nch; ++q) s += parts[it.part_off + (int64_t)q * K + k];
-    xf[k] = it.y[it.r + k] - s;
+    for (int q = 0; q < nch; ++q) s += __ldcg(parts + it.part_off + (int64_t)q * K + k);
+    xf[k] = __ldcg(it.y + it.r + k) - s;
   }
   __syncthreads();   // staged G/V and x_f visible
-  if (wid != 0) return;
-  double y[SLOTS];
+  if (threadIdx.x < 32) {
+    double y[SLOTS];
 #pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    y[s] = l < it.r ? it.y[l] : (l < it.m ? xf[l - it.r] : 0.0);
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      y[s] = l < it.r ? __ldcg(it.y + l) : (l < it.m ? xf[l - it.r] : 0.0);
+    }
+    for (int j = it.r - 1; j >= 0; --j) warp_reflect(V, tau, it.m, j, y, lane);
+    warp_trsv_upper_t(G, it.m, y, lane);
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int l = lane + 32 * s;
+      if (l < it.m) it.y[l] = y[s];
+    }
   }
-  for (int j = it.r - 1; j >= 0; --j) warp_reflect(V, tau, it.m, j, y, lane);
-  warp_trsv_upper_t(G, it.m, y, lane);
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    if (l < it.m) it.y[l] = y[s];
+  __syncthreads();
+}
+
+// ---- per-batch kernels (eager path, HS_APPLY_PER_BATCH=1) ---------------------------------
+template <int SLOTS>
+__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, int64_t cap) {
+  extern __shared__ double sm[];
+  dev_fwd_local<SLOTS>(items[blockIdx.x], sm, cap);
+}
+__global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const ApplyContrib* __restrict__ con, int n) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w < n) dev_fwd_scatter(tg[w], con, threadIdx.x & 31);
+}
+__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLocal* __restrict__ items,
+                                                                 const ApplyNb* __restrict__ nbs,
+                                                                 const ApplyChunk* __restrict__ chunks,
+                                                                 double* __restrict__ parts) {
+  dev_bwd_partial(items, nbs, chunks[blockIdx.x], parts);
+}
+template <int SLOTS>
+__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const double* __restrict__ parts, int64_t cap) {
+  extern __shared__ double sm[];
+  dev_bwd_local<SLOTS>(items[blockIdx.x], parts, sm, cap);
+}
+
+// ---- one cooperative kernel per level and direction: the level's batches in order, a
+// grid-wide barrier between dependent phases (local -> scatter -> next batch) ---------------
+template <int SLOTS>
+__global__ void __launch_bounds__(BWD_CHUNK) k_apply_fwd_level(ApplyLevelArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  extern __shared__ double sm[];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int b = 0; b < a.nbatch; ++b) {
+    const ApplyBatchDev B = a.batches[b];
+    for (int i = B.local_begin + blockIdx.x; i < B.local_end; i += gridDim.x) dev_fwd_local<SLOTS>(a.local[i], sm, a.cap);
+    g.sync();
+    for (int t = B.tgt_begin + gw; t < B.tgt_end; t += nwarps) dev_fwd_scatter(a.tgt[t], a.con, threadIdx.x & 31);
+    g.sync();
+  }
+}
+template <int SLOTS>
+__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_level(ApplyLevelArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  extern __shared__ double sm[];
+  for (int b = a.nbatch - 1; b >= 0; --b) {
+    const ApplyBatchDev B = a.batches[b];
+    for (int c = B.chunk_begin + blockIdx.x; c < B.chunk_end; c += gridDim.x)
+      dev_bwd_partial(a.local + B.local_begin, a.nb, a.chunks[c], a.parts);
+    g.sync();
+    for (int i = B.local_begin + blockIdx.x; i < B.local_end; i += gridDim.x)
+      dev_bwd_local<SLOTS>(a.local[i], a.parts, sm, a.cap);
+    g.sync();
   }
 }
 
@@ -330,6 +382,31 @@ void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t c
   else bwd_s<16>(d, parts, n, cap, st);
   count_launch(1);
 }
+template <int S>
+void level_s(const ApplyLevelArgs& a, int backward, cudaStream_t st) {
+  const void* fn = backward ? (const void*)k_apply_bwd_level<S> : (const void*)k_apply_fwd_level<S>;
+  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(a.cap, 1);
+  static size_t configured[2] = {0, 0};
+  set_dyn_smem(fn, sm, configured[backward ? 1 : 0]);
+  int per_sm = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BWD_CHUNK, sm));
+  if (per_sm <= 0) fail(HS_E_INTERNAL, "apply level kernel: no co-resident CTA fits");
+  int dev = 0, nsm = 0;
+  HS_CUDA(cudaGetDevice(&dev));
+  HS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = nsm * std::min(per_sm, 4);
+  ApplyLevelArgs args = a;
+  void* params[] = {&args};
+  HS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BWD_CHUNK), params, sm, st));
+}
+void launch_apply_level(const ApplyLevelArgs& a, int max_m, int backward, cudaStream_t st) {
+  if (a.nbatch <= 0) return;
+  if (max_m <= 128) level_s<4>(a, backward, st);
+  else if (max_m <= 256) level_s<8>(a, backward, st);
+  else level_s<16>(a, backward, st);
+  count_launch(1);
+}
+
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st) {
   if (N <= 0) return;
   k_top_solve<<<1, 1024, 0, st>>>(y, A, N, ld);

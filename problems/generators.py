@@ -366,3 +366,17 @@ CONFIGS = {
 
 def gen_config(name: str, **kw) -> Problem:
     return CONFIGS[name](**kw)
+
+
+def gen_config_scaled(name: str, scale: int) -> Problem:
+    """The config's operator on a horizontally reduced grid (1/scale per horizontal axis);
+    used for proxies of C4/C5 that fit quick runs (same layers, leaf, eps, tol, fields)."""
+    if name == "C4":
+        return gen_stokes_q1(512 // scale, 512 // scale, 20, aspect=1e3, leaf_columns=2)
+    if name == "C5":
+        return gen_stokes_q1(1024 // scale, 1024 // scale, 16, aspect=1e4, leaf_columns=4)
+    if name == "C3":
+        return gen_slab(256 // scale, 10)
+    if name == "C2":
+        return gen_laplace3d(64 // scale)
+    raise KeyError(name)

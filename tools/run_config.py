@@ -1,0 +1,27 @@
+"""Run factor + PCG on a full-size config on the GPU and print shape/time statistics."""
+import json, sys, time
+sys.path.insert(0, ".")
+import numpy as np
+from paper_1811_11248_b200 import hsolve as H
+from problems import gen_config
+name = sys.argv[1]
+eps = float(sys.argv[2]) if len(sys.argv) > 2 else None
+t = time.time(); p = gen_config(name); tg = time.time() - t
+if eps is not None:
+    p.eps = eps
+print(f"{name}: N={p.n} nnz={p.nnz} gen {tg:.1f}s", flush=True)
+h = H.hs_create(0)
+t = time.time()
+a = H.hs_analyze(h, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size, leaf_columns=p.leaf_columns)
+print("analyze", round(time.time() - t, 2), H.hs_analysis_get_info(a), flush=True)
+for rep in range(2):
+    t = time.time()
+    f = H.hs_factor_create(h, a, p.vals, eps=p.eps)
+    st = H.hs_factor_get_stats(f)
+    print(f"factor wall {time.time()-t:.2f}s dev {st['t_factor_s']:.3f}s batches {st['n_batches']} levels {st['n_levels']} "
+          f"max_m {st['max_m']} max_r {st['max_rank']} n_top {st['n_top']} GF {st['flops']/1e9:.1f} GB {st['factor_bytes']/1e9:.2f}",
+          flush=True)
+    x, rep_ = H.hs_pcg(f, p.b, tol=p.tol, raise_not_converged=False)
+    print("pcg", {k: rep_[k] for k in ("iters", "converged", "relres_true", "t_pcg_s")}, flush=True)
+    if rep == 0:
+        del f
