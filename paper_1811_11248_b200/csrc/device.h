@@ -37,6 +37,7 @@ struct CluItem {
   double* nu;       // kw scratch column norms
   int32_t m, kw, kn, ldB;
   int32_t level, cluster, pad0, pad1;
+  double* T;        // m x m row-major: T_s = U^T G^{-1} (formed after CPQR for the apply)
 };
 
 struct TrsmItem {   // one column tile of one cluster's B_s
@@ -80,46 +81,55 @@ struct BlockDir {            // the level's block store: row p has blocks (p, q<
   const int32_t* cap;
 };
 
-// Apply (Algorithm 2) items.
-struct ApplyLocal {          // forward: y_s <- U^T G^{-1} y_s
-                             // backward: x_f = y_f - sum C x_q, x_s <- G^{-T} U x_s
-  const double* G;
-  const double* V;
-  const double* tau;
-  double* y;                 // the cluster's segment (m entries)
+// Apply (Algorithm 2) as a dependency-driven task list per level.
+// The local transform of cluster s is the explicit m x m matrix T_s = U_s^T G_s^{-1}
+// (E_s S_s of W_s), formed once by the factor (k_form_T), so the forward step
+// [y_c; y_f] = T_s y_s and the backward step x_s = T_s^T [x_c; x_f] are parallel matvecs.
+// Coarse outputs are written straight to the parent level's vector (the level
+// transition of P:636), the fine part y_f to a per-level buffer for the backward sweep.
+struct ApplySrc {
+  const double* T;           // m x m row-major
   const double* C;           // C_s (fine rows), n-part column 0, ld ldC
-  int32_t m, r, nb_begin, nb_end, ldC, part_off, kn, pad;
+  const double* y;           // live segment at elimination (level vector), m entries
+  double* yc;                // coarse destination (parent level vector), r entries
+  double* yf;                // fine buffer, K = m - r entries
+  double* x;                 // backward output (level vector segment, = y)
+  int32_t m, r, ldC, kn;
+  int32_t pre;               // forward events on s before its elimination
+  int32_t nchunk;            // backward tasks of s (>= 1)
+  int32_t nb_begin, nb_end;  // neighbour list (backward gather)
+  int64_t part;              // partial sums of the backward chunks: nchunk x K
 };
-constexpr int BWD_CHUNK = 256;   // columns of C per backward matvec CTA
-struct ApplyChunk {          // backward matvec: columns [c0, c0+BWD_CHUNK) of cluster `li` of the batch
-  int32_t li, c0, part, pad;    // partial sums of the K rows go to parts[part .. part+K)
+struct FwdTgt {              // y_q[0:len] -= C_s[:, col:col+len]^T y_f,s
+  double* y;                 // q's live segment (level or parent vector)
+  int32_t q, col, len, seq;  // seq: forward event number of this update on q
+  int32_t proc, pad;         // proc: q already eliminated (its live segment is coarse)
 };
-struct ApplyNb {             // backward: C_s[:, col:col+len] x_q
-  const double* xq;
-  int32_t col, len;
+struct FwdTask {             // a group of targets of source s; `first` also emits s's outputs
+  int32_t s, t_begin, t_end, first;
 };
-struct ApplyTarget {         // forward: y_q[0:len] -= sum_s C_s[:, col:col+len]^T y_f,s
-  double* yq;
-  int32_t len, c_begin, c_end, pad;
+struct BwdNb {               // neighbour q: columns [col, col+len) of C_s read x from `x`
+  const double* x;
+  int32_t q, col, len, later;   // later: q eliminated after s at this level (wait for it)
 };
-struct ApplyContrib {
-  const double* C;           // C_s (fine rows), n-part column 0
-  const double* yf;          // y_f,s
-  int32_t ldC, K, col, pad;
+struct BwdTask {             // columns [c0, c0+nc) of C_s x_n -> partial sums
+  int32_t s, c0, nc, chunk;
 };
-struct ApplyBatchDev {       // a batch's item ranges in the apply arrays
-  int32_t local_begin, local_end, tgt_begin, tgt_end, chunk_begin, chunk_end;
-};
-struct ApplyLevelArgs {      // one level of the apply, swept by one cooperative kernel
-  const ApplyBatchDev* batches;
-  int32_t nbatch, pad;
-  const ApplyLocal* local;
-  const ApplyTarget* tgt;
-  const ApplyContrib* con;
-  const ApplyNb* nb;
-  const ApplyChunk* chunks;
+constexpr int APPLY_THREADS = 256;
+constexpr int BWD_COLS = 512;        // columns of C per backward task
+constexpr int FWD_COLS = 256;        // target columns per forward task
+struct ApplyLevelArgs {
+  const ApplySrc* src;
+  const FwdTask* ftask;
+  const FwdTgt* ftgt;
+  const BwdTask* btask;
+  const BwdNb* bnb;
   double* parts;
-  int64_t cap;               // dynamic shared memory (doubles) for factor staging
+  int32_t* cnt;              // forward event counters (nclus)
+  int32_t* bcnt;             // backward chunk arrivals (nclus)
+  int32_t* done;             // backward completion flags (nclus)
+  int32_t* ticket;           // [0] forward, [1] backward
+  int32_t nftask, nbtask;
 };
 
 // First error raised on the device (POTRF breakdown).
@@ -154,15 +164,10 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
                  cudaStream_t st);
 constexpr int TOP_NB = 64;
 
-void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, int max_m, cudaStream_t st);
-void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st);
-// backward, stage 1: partial sums of C x_n over column chunks (many CTAs per cluster)
-void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb, const ApplyChunk* ch, int n,
-                              double* parts, cudaStream_t st);
-// backward, stage 2: x_f = y_f - sum of the partials (fixed order), x_s <- G^{-T} U [x_c; x_f]
-void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, int max_m, cudaStream_t st);
-// one cooperative launch per level and direction (grid-wide barriers between batches)
-void launch_apply_level(const ApplyLevelArgs& a, int max_m, int backward, cudaStream_t st);
+// T_s = U^T G^{-1} for the clusters of a batch (after CPQR; the rank comes from d_rank)
+void launch_form_T(const CluItem* d_items, const int32_t* d_rank, int n, int max_m, cudaStream_t st);
+void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st);
+void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

@@ -140,7 +140,7 @@ struct BlockStore {
 // batch's rank read-back, which already synchronises: a = [gather|potrf|trsm|cpqr],
 // b = [schur|write-back] of the previous batch.
 struct PhaseTimer {
-  cudaEvent_t a[5], b[3];
+  cudaEvent_t a[6], b[3];
   bool b_pending = false;
   PhaseTimer() {
     for (auto& e : a) HS_CUDA(cudaEventCreate(&e));
@@ -164,6 +164,7 @@ struct PhaseTimer {
   }
   void collect(hs_factor_stats_t& S) {   // after a synchronising point
     for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
+    S.t_phase_s[5] += el(a[4], a[5]);   // T_s formation (apply operator) with write-back/assembly
     collect_b(S);
   }
 };
@@ -194,10 +195,8 @@ hs_factor_s::~hs_factor_s() {
   };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
-  fr(ap.d_local); fr(ap.d_nb); fr(ap.d_tgt); fr(ap.d_con); fr(ap.d_y); fr(ap.d_chunks); fr(ap.d_parts);
-  for (auto* p : ap.d_tsrc) fr(p);
-  for (auto* p : ap.d_lvl_batches) fr(p);
-  for (auto* p : ap.d_tdst) fr(p);
+  for (auto& p : ap.lv) { fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); }
+  fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
   fr(d_r); fr(d_z); fr(d_p); fr(d_q); fr(d_x); fr(d_b); fr(d_red);
   if (h_red) cudaFreeHost(h_red);
@@ -318,9 +317,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ApplyPlan& ap = f->ap;
   int64_t vbase = 0;
   f->lv.resize(an->L_top);
-  ap.batches.resize(an->L_top);
-  ap.trans_src.resize(an->L_top);
-  ap.trans_dst.resize(an->L_top);
+  ap.lv.resize(an->L_top);
 
   const bool prof = std::getenv("HS_PROFILE") != nullptr;
   const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;   // A/B switch for the old kernel
@@ -342,7 +339,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     ap.vbase.push_back(vbase);
     vbase += L.vlen;
     // ---- level arena: G, V (cap^2), tau (cap), nu (bound kw), B (cap x bound(kn + kw)) ----
-    std::vector<int64_t> oG(lev.nclus), oV(lev.nclus), oT(lev.nclus), oN(lev.nclus), oB(lev.nclus), oP(lev.nclus);
+    std::vector<int64_t> oG(lev.nclus), oV(lev.nclus), oT(lev.nclus), oN(lev.nclus), oB(lev.nclus), oP(lev.nclus),
+        oX(lev.nclus);
     int64_t off = 0, ioff = 0;
     for (int s = 0; s < lev.nclus; ++s) {
       const int64_t m = cap[s];
@@ -361,24 +359,27 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       oN[s] = off; off += bw;
       oB[s] = off; off += m * (bn + bw);
       off = (off + 3) & ~int64_t(3);                 // 32-byte alignment
+      oX[s] = off; off += m * m;                     // T_s (apply operator)
       oP[s] = ioff; ioff += m;
     }
     L.arena_bytes = (size_t)off * sizeof(double);
     HS_CUDA(cudaMallocAsync(&L.arena, std::max<size_t>(L.arena_bytes, 8), st));
     HS_CUDA(cudaMallocAsync(&L.iarena, std::max<size_t>(sizeof(int32_t) * ioff, 4), st));
     L.G.resize(lev.nclus); L.V.resize(lev.nclus); L.tau.resize(lev.nclus); L.B.resize(lev.nclus);
-    L.nu.resize(lev.nclus); L.piv.resize(lev.nclus);
+    L.nu.resize(lev.nclus); L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
     for (int s = 0; s < lev.nclus; ++s) {
       L.G[s] = L.arena + oG[s]; L.V[s] = L.arena + oV[s]; L.tau[s] = L.arena + oT[s];
-      L.nu[s] = L.arena + oN[s]; L.B[s] = L.arena + oB[s]; L.piv[s] = L.iarena + oP[s];
+      L.nu[s] = L.arena + oN[s]; L.B[s] = L.arena + oB[s]; L.piv[s] = L.iarena + oP[s]; L.T[s] = L.arena + oX[s];
     }
     std::vector<int32_t> live = cap;
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
-    std::vector<int32_t> atgt_slot(lev.nclus, -1);
-    ap.lvl_local.push_back((int32_t)ap.local.size());
-    ap.lvl_nb.push_back((int32_t)ap.nb.size());
-    ap.lvl_con.push_back((int32_t)ap.con.size());
-    ap.lvl_tgt.push_back((int32_t)ap.tgt.size());
+    // apply plan of the level: forward event counts, processed flags, backward tasks per batch
+    ApplyLevelPlan& AP = ap.lv[l];
+    AP.src.assign(lev.nclus, ApplySrc{});
+    std::vector<int32_t> fev(lev.nclus, 0);
+    std::vector<uint8_t> proc(lev.nclus, 0);
+    std::vector<std::vector<BwdTask>> bwd_batches;
+    std::vector<int64_t> foff(lev.nclus, 0);
 
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
@@ -400,7 +401,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = ldB;
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
-        it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
+        it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s; it.T = L.T[s];
         max_m = std::max(max_m, m);
         if (m == 0) continue;
         double* p; int32_t ld, tr;
@@ -438,6 +439,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
       else launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
       HS_CUDA(cudaEventRecord(pt.a[4], st));
+      launch_form_T(upA.dptr<CluItem>(iC), d_rank, nb, max_m, st);
+      HS_CUDA(cudaEventRecord(pt.a[5], st));
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream
       pt.collect(S);
@@ -450,13 +453,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<CopyItem> wb;
       std::vector<double*> id_ptr;
       std::vector<int32_t> id_ld, id_r;
-      ApplyBatch abt{};
       double tq_prev = now_s();
-      abt.local_begin = (int32_t)ap.local.size();
-      abt.tgt_begin = (int32_t)ap.tgt.size();
-      std::vector<std::pair<int32_t, std::vector<ApplyContrib>>> atgt;   // forward scatter, first-touch order
-      std::vector<ApplyChunk> bwd_chunks;
-      int64_t bwd_parts = 0;
+      bwd_batches.emplace_back();
+      std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bt[bi];
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
@@ -520,35 +519,42 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         const double tq1 = now_s();
         t_sub[1] += tq1 - tq0;
-        // apply plan: local item (+ backward neighbour list) and forward scatter contributions
-        ApplyLocal al{};
-        al.G = L.G[s]; al.V = L.V[s]; al.tau = L.tau[s];
-        al.y = nullptr;   // patched with the device base after the factor
-        al.C = C; al.ldC = ldB; al.m = m; al.r = r; al.kn = kn;
-        al.nb_begin = (int32_t)ap.nb.size();
-        for (size_t a = 0; a < ns.size(); ++a) {
-          const int32_t q = ns[a];
-          if (live[q] == 0 || K == 0) continue;
-          ap.nb.push_back(ApplyNb{reinterpret_cast<const double*>((uintptr_t)(L.voff[q])), noff[a], live[q]});
-          if (atgt_slot[q] < 0) {
-            atgt_slot[q] = (int32_t)atgt.size();
-            atgt.push_back({q, {}});
+        // apply plan (Algorithm 2): the cluster's record, its forward target tasks (targets
+        // grouped up to FWD_COLS columns) and its backward column chunks
+        if (m > 0) {
+          ApplySrc& as = AP.src[s];
+          as.T = L.T[s]; as.C = C; as.ldC = ldB; as.m = m; as.r = r; as.kn = kn;
+          as.pre = fev[s]++;
+          as.nb_begin = (int32_t)AP.bnb.size();
+          const int32_t tb = (int32_t)AP.ftgt.size();
+          for (size_t a = 0; a < ns.size(); ++a) {
+            const int32_t q = ns[a];
+            if (live[q] == 0 || K == 0) continue;
+            AP.ftgt.push_back(FwdTgt{nullptr, q, noff[a], live[q], fev[q]++, proc[q], 0});
+            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], live[q], proc[q] ? 0 : 1});
           }
-          atgt[atgt_slot[q]].second.push_back(
-              ApplyContrib{C, reinterpret_cast<const double*>((uintptr_t)(L.voff[s] + r)), ldB, K, noff[a], 0});
-        }
-        al.nb_end = (int32_t)ap.nb.size();
-        al.part_off = 0;
-        if (K > 0 && al.nb_end > al.nb_begin) {   // backward matvec column chunks
-          al.part_off = (int32_t)bwd_parts;
-          for (int32_t c0 = 0; c0 < kn; c0 += BWD_CHUNK) {
-            bwd_chunks.push_back(ApplyChunk{(int32_t)(ap.local.size() - abt.local_begin), c0, (int32_t)bwd_parts, 0});
-            bwd_parts += K;
+          as.nb_end = (int32_t)AP.bnb.size();
+          const int32_t te = (int32_t)AP.ftgt.size();
+          if (tb == te) AP.ftask.push_back(FwdTask{s, tb, tb, 1});
+          for (int32_t g0 = tb, first = 1; g0 < te; first = 0) {
+            int32_t g1 = g0, cols = 0;
+            while (g1 < te && (g1 == g0 || (cols + AP.ftgt[g1].len <= FWD_COLS && g1 - g0 < 16))) cols += AP.ftgt[g1++].len;
+            AP.ftask.push_back(FwdTask{s, g0, g1, first});
+            g0 = g1;
           }
+          as.part = AP.parts;
+          if (K > 0 && kn > 0) {
+            as.nchunk = (kn + BWD_COLS - 1) / BWD_COLS;
+            for (int32_t c = 0; c < as.nchunk; ++c)
+              bwd_tasks.push_back(BwdTask{s, c * BWD_COLS, std::min(BWD_COLS, kn - c * BWD_COLS), c});
+            AP.parts += (int64_t)as.nchunk * K;
+          } else {
+            as.nchunk = 1;
+            bwd_tasks.push_back(BwdTask{s, 0, 0, 0});
+          }
+          foff[s] = ap.ftotal;
+          ap.ftotal += K;
         }
-        if (K > 0) ap.max_kn = std::max(ap.max_kn, kn);
-        al.y = reinterpret_cast<double*>((uintptr_t)L.voff[s]);
-        ap.local.push_back(al);
         tq_prev = now_s();
         t_sub[2] += tq_prev - tq1;
       }
@@ -560,34 +566,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         tiles.insert(tiles.end(), wv.begin(), wv.end());
         wave_off.push_back((int32_t)tiles.size());
       }
-      for (auto& tq : atgt) {
-        ApplyTarget t{};
-        t.yq = reinterpret_cast<double*>((uintptr_t)L.voff[tq.first]);
-        t.len = live[tq.first];
-        t.c_begin = (int32_t)ap.con.size();
-        ap.con.insert(ap.con.end(), tq.second.begin(), tq.second.end());
-        t.c_end = (int32_t)ap.con.size();
-        ap.tgt.push_back(t);
-        atgt_slot[tq.first] = -1;
+      for (int bi = 0; bi < nb; ++bi) {
+        live[Bt[bi]] = L.rank[Bt[bi]];
+        proc[Bt[bi]] = 1;
       }
-      abt.chunk_begin = (int32_t)ap.chunks.size();
-      ap.chunks.insert(ap.chunks.end(), bwd_chunks.begin(), bwd_chunks.end());
-      abt.chunk_end = (int32_t)ap.chunks.size();
-      ap.max_parts = std::max(ap.max_parts, bwd_parts);
-      abt.local_end = (int32_t)ap.local.size();
-      abt.tgt_end = (int32_t)ap.tgt.size();
-      {   // shared-memory staging of G/V/tau in the apply's local kernels (doubles; <= ~200 KB)
-        const int64_t LIM = 25000;
-        for (int32_t i = abt.local_begin; i < abt.local_end; ++i) {
-          const ApplyLocal& a = ap.local[i];
-          const int64_t need = (int64_t)a.m * a.m + (int64_t)a.m * a.r + a.r;
-          if (need <= LIM) abt.cap_fwd = std::max(abt.cap_fwd, need);
-          abt.max_m = std::max(abt.max_m, a.m);
-        }
-        abt.cap_bwd = abt.cap_fwd;
-      }
-      ap.batches[l].push_back(abt);
-      for (int bi = 0; bi < nb; ++bi) live[Bt[bi]] = L.rank[Bt[bi]];
       t_sub[3] += now_s() - tq3;
       upB.reset();
       const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
@@ -611,7 +593,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (const char* dd = std::getenv("HS_DEBUG_DUMP")) {   // debug aid: block store after every batch
         HS_CUDA(cudaStreamSynchronize(st));
         char path[512];
-        std::snprintf(path, sizeof path, "%s/l%d_b%d.bin", dd, l, (int)ap.batches[l].size() - 1);
+        std::snprintf(path, sizeof path, "%s/l%d_b%d.bin", dd, l, (int)bwd_batches.size() - 1);
         FILE* fp = std::fopen(path, "wb");
         if (fp) {
           std::vector<double> host(bs.total);
@@ -658,16 +640,33 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                                 L.rank[c], L.rank[d], 0, 0});
       }
     }
-    // forward vector transition (children's coarse entries -> parent segment)
-    int64_t pofs = 0;
-    for (int P = 0; P < nP; ++P)
-      for (int a = 0; a < 2; ++a) {
-        const int32_t c = 2 * P + a;
-        for (int32_t i = 0; i < L.rank[c]; ++i) {
-          ap.trans_src[l].push_back(L.voff[c] + i);
-          ap.trans_dst[l].push_back(pofs++);
-        }
+    // apply plan: resolve vector positions (offsets into d_y / d_yf, made absolute at the
+    // end).  A cluster's live segment is its level segment until it is eliminated, then its
+    // coarse rows inside the parent's segment [coarse(2P); coarse(2P+1)].
+    {
+      std::vector<int64_t> voffn(nP + 1, 0);
+      for (int P = 0; P < nP; ++P) voffn[P + 1] = voffn[P] + capn[P];
+      const int64_t vb = ap.vbase[l], vbn = vbase;   // vbase already advanced past this level
+      auto lpos = [&](int32_t c) { return (double*)(uintptr_t)(vb + L.voff[c]); };
+      auto ppos = [&](int32_t c) {
+        return (double*)(uintptr_t)(vbn + voffn[c >> 1] + ((c & 1) ? L.rank[c - 1] : 0));
+      };
+      for (int32_t c = 0; c < lev.nclus; ++c) {
+        ApplySrc& as = AP.src[c];
+        if (as.m == 0) continue;
+        as.y = lpos(c);
+        as.x = lpos(c);
+        as.yc = ppos(c);
+        as.yf = (double*)(uintptr_t)foff[c];
       }
+      for (auto& t : AP.ftgt) t.y = t.proc ? ppos(t.q) : lpos(t.q);
+      for (auto& nbr : AP.bnb) nbr.x = (double*)(nbr.later ? lpos(nbr.q) : ppos(nbr.q));
+      for (auto it = bwd_batches.rbegin(); it != bwd_batches.rend(); ++it)
+        AP.btask.insert(AP.btask.end(), it->begin(), it->end());
+      AP.ctr_off = ap.ctr_total;
+      ap.ctr_total += 3 * (int64_t)lev.nclus + 2;
+      ap.max_parts = std::max(ap.max_parts, AP.parts);
+    }
     upA.reset();
     const size_t iA = upA.add(asmb);
     upA.stage.ensure(upA.total);
@@ -759,69 +758,43 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
   S.n_levels = an->L_top;
-  // factor bytes: G (m^2/2), V (m r), tau, C ((m - r) kn) per cluster + top (N^2/2)
+  // factor bytes read by the apply: T_s (m^2) and C_s ((m - r) kn) per cluster + top (N^2/2)
   double fb = 0.0;
   for (const auto& L : f->lv)
     for (int s = 0; s < L.nclus; ++s) {
       const double m = L.cap[s], r = L.rank[s];
-      fb += 8.0 * (m * (m + 1) / 2 + m * r + r + (m - r) * L.kn[s]);
+      fb += 8.0 * (m * m + (m - r) * L.kn[s]);
     }
   fb += 8.0 * (double)f->ntop * (f->ntop + 1) / 2;
   S.factor_bytes = fb;
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
   HS_CUDA(cudaMallocAsync(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1), st));
-  // patch vector offsets (stored as integers) into absolute addresses
-  {
-    auto end_of = [&](const std::vector<int32_t>& starts, int l, size_t total) {
-      return l + 1 < (int)starts.size() ? (size_t)starts[l + 1] : total;
-    };
-    for (int l = 0; l < an->L_top; ++l) {
-      double* base = ap.d_y + ap.vbase[l];
-      for (size_t i = ap.lvl_local[l]; i < end_of(ap.lvl_local, l, ap.local.size()); ++i)
-        ap.local[i].y = base + (uintptr_t)ap.local[i].y;
-      for (size_t i = ap.lvl_nb[l]; i < end_of(ap.lvl_nb, l, ap.nb.size()); ++i)
-        ap.nb[i].xq = base + (uintptr_t)ap.nb[i].xq;
-      for (size_t i = ap.lvl_con[l]; i < end_of(ap.lvl_con, l, ap.con.size()); ++i)
-        ap.con[i].yf = base + (uintptr_t)ap.con[i].yf;
-      for (size_t i = ap.lvl_tgt[l]; i < end_of(ap.lvl_tgt, l, ap.tgt.size()); ++i)
-        ap.tgt[i].yq = base + (uintptr_t)ap.tgt[i].yq;
-    }
-  }
+  HS_CUDA(cudaMallocAsync(&ap.d_yf, sizeof(double) * std::max<int64_t>(ap.ftotal, 1), st));
+  HS_CUDA(cudaMallocAsync(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1), st));
+  HS_CUDA(cudaMallocAsync(&ap.d_ctr, sizeof(int32_t) * std::max<int64_t>(ap.ctr_total, 1), st));
   auto up = [&](auto& vec, auto*& dptr) {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
     if (vec.empty()) return;
     HS_CUDA(cudaMallocAsync(&dptr, sizeof(T) * vec.size(), st));
     HS_CUDA(cudaMemcpyAsync(dptr, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice, st));
   };
-  up(ap.local, ap.d_local);
-  up(ap.nb, ap.d_nb);
-  up(ap.tgt, ap.d_tgt);
-  up(ap.con, ap.d_con);
-  up(ap.chunks, ap.d_chunks);
-  // per-level batch tables for the cooperative level kernels of the apply
-  ap.d_lvl_batches.assign(an->L_top, nullptr);
-  ap.lvl_max_m.assign(an->L_top, 0);
-  ap.lvl_cap.assign(an->L_top, 0);
-  for (int l = 0; l < an->L_top; ++l) {
-    std::vector<ApplyBatchDev> tb;
-    for (const auto& b : ap.batches[l]) {
-      tb.push_back(ApplyBatchDev{b.local_begin, b.local_end, b.tgt_begin, b.tgt_end, b.chunk_begin, b.chunk_end});
-      ap.lvl_max_m[l] = std::max(ap.lvl_max_m[l], b.max_m);
-      ap.lvl_cap[l] = std::max(ap.lvl_cap[l], std::max(b.cap_fwd, b.cap_bwd));
+  for (int l = 0; l < an->L_top; ++l) {   // offsets (stored as integers) -> absolute addresses
+    ApplyLevelPlan& AP = ap.lv[l];
+    for (auto& as : AP.src) {
+      if (as.m == 0) continue;
+      as.y = ap.d_y + (uintptr_t)as.y;
+      as.x = ap.d_y + (uintptr_t)as.x;
+      as.yc = ap.d_y + (uintptr_t)as.yc;
+      as.yf = ap.d_yf + (uintptr_t)as.yf;
     }
-    up(tb, ap.d_lvl_batches[l]);
-    HS_CUDA(cudaStreamSynchronize(st));   // tb is a temporary
-  }
-  HS_CUDA(cudaMallocAsync(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1), st));
-  ap.d_tsrc.assign(an->L_top, nullptr);
-  ap.d_tdst.assign(an->L_top, nullptr);
-  for (int l = 0; l < an->L_top; ++l) {
-    // absolute indices into d_y: src at level l, dst at level l+1
-    for (auto& v : ap.trans_src[l]) v += ap.vbase[l];
-    for (auto& v : ap.trans_dst[l]) v += ap.vbase[l + 1];
-    up(ap.trans_src[l], ap.d_tsrc[l]);
-    up(ap.trans_dst[l], ap.d_tdst[l]);
+    for (auto& t : AP.ftgt) t.y = ap.d_y + (uintptr_t)t.y;
+    for (auto& nbr : AP.bnb) nbr.x = ap.d_y + (uintptr_t)nbr.x;
+    up(AP.src, AP.d_src);
+    up(AP.ftask, AP.d_ftask);
+    up(AP.ftgt, AP.d_ftgt);
+    up(AP.btask, AP.d_btask);
+    up(AP.bnb, AP.d_bnb);
   }
   HS_CUDA(cudaStreamSynchronize(st));
   return guard.release();

@@ -281,6 +281,77 @@ __global__ void k_trsm_raw(const double* G, int ldG, int m, double* B, int ldB, 
 }
 
 // ---------------------------------------------------------------------------------------
+// Apply operator of a cluster: T_s = U_s^T G_s^{-1} = H_{r-1} ... H_0 G_s^{-1} (the E_s S_s
+// of W_s = P_s G_s E_s S_s), m x m row-major, formed once after CPQR so that the
+// apply's local steps (Algorithm 2) are parallel matvecs instead of a serial
+// triangular solve.  One CTA per (cluster, column tile): the tile of the identity is
+// forward-substituted with G (smem-staged for m <= SMEM_M, else read through L1/L2),
+// then the r reflectors are applied, H_0 first; the rank comes from the CPQR's output.
+__global__ void __launch_bounds__(256) k_form_T(const CluItem* __restrict__ items, const int32_t* __restrict__ rank,
+                                                int tiles_per) {
+  extern __shared__ double sm[];
+  const int ci = blockIdx.x / tiles_per, tile = blockIdx.x % tiles_per;
+  const CluItem it = items[ci];
+  const int m = it.m;
+  const bool gs = m <= SMEM_M;
+  const int TW = gs ? 64 : 32;
+  const int c0 = tile * TW;
+  if (m == 0 || c0 >= m) return;
+  const int nc = min(TW, m - c0);
+  const int r = rank[ci];
+  const double* g;
+  int ldg;
+  double* x;
+  if (gs) {
+    double* gg = sm;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = e / m, k = e % m;
+      gg[e] = (k <= i) ? it.G[(int64_t)i * m + k] : 0.0;
+    }
+    g = gg;
+    ldg = m;
+    x = sm + m * m;
+  } else {
+    g = it.G;
+    ldg = m;
+    x = sm;
+  }
+  __shared__ double red[8][64];
+  for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+    const int i = e / TW, c = e % TW;
+    x[e] = (c < nc && i == c0 + c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x % TW, grp = threadIdx.x / TW, ngrp = blockDim.x / TW;
+  // X <- G^{-1} X  (rows above c0 stay zero: start the substitution at row c0)
+  for (int i = c0; i < m; ++i) {
+    if (grp == 0) x[i * TW + c] /= g[(int64_t)i * ldg + i];
+    __syncthreads();
+    const double xi = x[i * TW + c];
+    for (int l = i + 1 + grp; l < m; l += ngrp) x[l * TW + c] -= g[(int64_t)l * ldg + i] * xi;
+    __syncthreads();
+  }
+  // X <- H_j X for j = 0 .. r-1, H_j = I - tau_j v_j v_j^T (v_j = column j of V, zeros above j)
+  for (int j = 0; j < r; ++j) {
+    const double t = it.tau[j];
+    const double* v = it.V + (int64_t)j * m;
+    double d = 0.0;
+    for (int l = j + grp; l < m; l += ngrp) d += v[l] * x[l * TW + c];
+    red[grp][c] = d;
+    __syncthreads();
+    double s = 0.0;
+    for (int q = 0; q < ngrp; ++q) s += red[q][c];
+    const double td = t * s;
+    for (int l = j + grp; l < m; l += ngrp) x[l * TW + c] -= td * v[l];
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+    const int i = e / TW, cc = e % TW;
+    if (cc < nc) it.T[(int64_t)i * m + c0 + cc] = x[e];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // a3 + a4: column-pivoted Householder QR of the scaled block W = G^{-1}A_sw (columns
 // [0, kw) of B_s) truncated at the first step with max_i nu_i <= tau_s, tau_s = eps *
 // nu_max(0) (relative) or eps; pivot = lowest column index among nu_i >= (1-1e-10) nu_max.
@@ -877,6 +948,19 @@ void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m
   const size_t sm = words * sizeof(double);
   set_smem((const void*)k_trsm, sm);
   k_trsm<<<n, 256, sm, st>>>(d_clu, d_items);
+  count_launch(1);
+}
+void launch_form_T(const CluItem* d_items, const int32_t* d_rank, int n, int max_m, cudaStream_t st) {
+  if (n <= 0 || max_m <= 0) return;
+  const bool gs = max_m <= SMEM_M;
+  const int TW = gs ? 64 : 32;
+  const int ms = std::min(max_m, SMEM_M);
+  size_t words = (size_t)ms * ms + (size_t)ms * 64;
+  if (!gs) words = std::max(words, (size_t)max_m * 32);
+  const size_t sm = words * sizeof(double);
+  set_smem((const void*)k_form_T, sm);
+  const int tiles = (max_m + TW - 1) / TW;
+  k_form_T<<<n * tiles, 256, sm, st>>>(d_items, d_rank, tiles);
   count_launch(1);
 }
 void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st) {

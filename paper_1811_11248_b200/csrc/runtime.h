@@ -70,50 +70,38 @@ struct LevelRT {
   int64_t vlen = 0;
   double* arena = nullptr;              // G, V, tau, nu, B of every cluster
   int32_t* iarena = nullptr;            // pivots
-  std::vector<double*> G, V, tau, B, nu;
+  std::vector<double*> G, V, tau, B, nu, T;
   std::vector<int32_t*> piv;
   size_t arena_bytes = 0;
 };
 
-struct ApplyBatch {
-  int32_t local_begin, local_end;       // into fwd_local / bwd_local item arrays
-  int32_t tgt_begin, tgt_end;           // forward scatter targets
-  int64_t cap_fwd = 0;                  // dynamic smem (doubles) of the forward local kernel
-  int32_t kn_bwd = 0;                   // x_n staging size of the backward kernel
-  int64_t cap_bwd = 0;                  // total dynamic smem (doubles) of the backward kernel
-  int32_t chunk_begin = 0, chunk_end = 0;   // backward matvec chunks
-  int32_t max_m = 0;                        // largest cluster of the batch (kernel variant)
+// Apply plan of one level (Algorithm 2): per-cluster records, the forward task list in
+// batch order and the backward task list in reverse batch order (solve_kernels.cu).
+struct ApplyLevelPlan {
+  std::vector<ApplySrc> src;            // by cluster id (m = 0: unused)
+  std::vector<FwdTask> ftask;
+  std::vector<FwdTgt> ftgt;
+  std::vector<BwdTask> btask;
+  std::vector<BwdNb> bnb;
+  int64_t ctr_off = 0;                  // counters: cnt[nclus] bcnt[nclus] done[nclus] ticket[2]
+  int64_t parts = 0;                    // partial-sum doubles of the backward sweep
+  ApplySrc* d_src = nullptr;
+  FwdTask* d_ftask = nullptr;
+  FwdTgt* d_ftgt = nullptr;
+  BwdTask* d_btask = nullptr;
+  BwdNb* d_bnb = nullptr;
 };
 
 struct ApplyPlan {
-  std::vector<ApplyLocal> local;        // shared by forward (nb range unused) and backward
-  std::vector<ApplyNb> nb;
-  std::vector<ApplyTarget> tgt;
-  std::vector<ApplyContrib> con;
-  std::vector<std::vector<ApplyBatch>> batches;   // per level
-  std::vector<int32_t> lvl_local, lvl_nb, lvl_con, lvl_tgt;   // per-level start indices (address patching)
-  std::vector<ApplyBatchDev*> d_lvl_batches;   // per level: the batches' item ranges (device)
-  std::vector<int32_t> lvl_max_m;
-  std::vector<int64_t> lvl_cap;
-  std::vector<ApplyChunk> chunks;        // backward matvec column chunks
-  ApplyChunk* d_chunks = nullptr;
-  int64_t max_parts = 0;                 // partial sums of the largest batch
-  double* d_parts = nullptr;
-  std::vector<std::vector<int64_t>> trans_src, trans_dst;   // level l -> l+1 vector transition
-  // device copies
-  ApplyLocal* d_local = nullptr;
-  ApplyNb* d_nb = nullptr;
-  ApplyTarget* d_tgt = nullptr;
-  ApplyContrib* d_con = nullptr;
-  std::vector<int64_t*> d_tsrc, d_tdst;
-  std::vector<int64_t> vbase;            // per level + top
-  int64_t vtotal = 0;
+  std::vector<ApplyLevelPlan> lv;
+  std::vector<int64_t> vbase;            // per level + top: offset of the level vector in d_y
+  int64_t vtotal = 0, ftotal = 0, ctr_total = 0, max_parts = 0;
   double* d_y = nullptr;                 // the apply vector (all levels + top)
+  double* d_yf = nullptr;                // fine parts y_f of every cluster (forward -> backward)
+  double* d_parts = nullptr;
+  int32_t* d_ctr = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
-  int32_t max_kn = 0;                    // largest n-part of a cluster with fine DOFs (apply smem)
-  const double* graph_in = nullptr;
-  double* graph_out = nullptr;
 };
 
 }  // namespace hs

@@ -1,8 +1,9 @@
 // hs_apply / hs_pcg host drivers.
 //
 // Apply = Algorithm 2, captured once per factor as a CUDA graph:
-//   permute-in, forward sweep (per level: per batch local + scatter, then the
-//   level transition), top solve, backward sweep (reverse), permute-out.
+//   permute-in, forward sweep (one dependency-driven task kernel per level; coarse parts go
+//   straight into the parent level's segments), top solve, backward sweep (reverse),
+//   permute-out.
 // PCG (north_star) keeps every scalar on the device; the only host
 // synchronisation per iteration is the 8-byte read of ||r||^2 for the stopping test.
 #include <cmath>
@@ -18,14 +19,6 @@ namespace {
 
 constexpr int RED_BLOCKS = 296;   // 2 x 148 SMs
 constexpr int RED_THREADS = 256;
-
-__global__ void k_move(double* y, const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n,
-                       int reverse) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    if (reverse) y[src[i]] = y[dst[i]];
-    else y[dst[i]] = y[src[i]];
-  }
-}
 
 // scalars layout (device): 0 rho, 1 pq, 2 rr, 3 rz_new, 4 bb
 __device__ __forceinline__ double blk_sum(double v, double* sh) {
@@ -103,25 +96,30 @@ void dot(const double* a, const double* b, int64_t n, double* partial, double* o
 
 ApplyLevelArgs level_args(hs_factor_s* f, int l) {
   ApplyPlan& ap = f->ap;
+  const ApplyLevelPlan& P = ap.lv[l];
+  const int64_t n = (int64_t)P.src.size();
   ApplyLevelArgs a{};
-  a.batches = ap.d_lvl_batches[l];
-  a.nbatch = (int32_t)ap.batches[l].size();
-  a.local = ap.d_local;
-  a.tgt = ap.d_tgt;
-  a.con = ap.d_con;
-  a.nb = ap.d_nb;
-  a.chunks = ap.d_chunks;
+  a.src = P.d_src;
+  a.ftask = P.d_ftask;
+  a.ftgt = P.d_ftgt;
+  a.btask = P.d_btask;
+  a.bnb = P.d_bnb;
   a.parts = ap.d_parts;
-  a.cap = ap.lvl_cap[l];
+  a.cnt = ap.d_ctr + P.ctr_off;
+  a.bcnt = a.cnt + n;
+  a.done = a.cnt + 2 * n;
+  a.ticket = a.cnt + 3 * n;
+  a.nftask = (int32_t)P.ftask.size();
+  a.nbtask = (int32_t)P.btask.size();
   return a;
 }
 
+// Algorithm 2: permute-in, forward sweep (one dependency-driven kernel per level), top
+// solve, backward sweep (reverse), permute-out.  The event counters start from zero.
 void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev = nullptr) {
   const Analysis* an = f->an;
   ApplyPlan& ap = f->ap;
   const int64_t n = an->n;
-  // HS_APPLY_PER_BATCH=1: one launch per batch phase instead of one cooperative kernel per level
-  const bool per_batch = std::getenv("HS_APPLY_PER_BATCH") != nullptr;
   auto mark = [&]() {
     if (!ev) return;
     cudaEvent_t e;
@@ -130,42 +128,17 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
     ev->push_back(e);
   };
   mark();
+  if (ap.ctr_total) HS_CUDA(cudaMemsetAsync(ap.d_ctr, 0, sizeof(int32_t) * ap.ctr_total, st));
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
     mark();
-    if (per_batch) {
-      for (const auto& b : ap.batches[l]) {
-        launch_apply_fwd_local(ap.d_local + b.local_begin, b.local_end - b.local_begin, b.cap_fwd, b.max_m, st);
-        launch_apply_fwd_scatter(ap.d_tgt + b.tgt_begin, ap.d_con, b.tgt_end - b.tgt_begin, st);
-      }
-    } else {
-      launch_apply_level(level_args(f, l), ap.lvl_max_m[l], 0, st);
-    }
-    const int64_t nt = (int64_t)ap.trans_src[l].size();
-    if (nt) {
-      k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 0);
-      count_launch(1);
-    }
+    launch_apply_fwd_level(level_args(f, l), st);
   }
   mark();
   if (f->ntop > 0) launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);
   for (int l = an->L_top - 1; l >= 0; --l) {
     mark();
-    const int64_t nt = (int64_t)ap.trans_src[l].size();
-    if (nt) {
-      k_move<<<(int)std::min<int64_t>((nt + 255) / 256, 1184), 256, 0, st>>>(ap.d_y, ap.d_tsrc[l], ap.d_tdst[l], nt, 1);
-      count_launch(1);
-    }
-    if (per_batch) {
-      for (auto it = ap.batches[l].rbegin(); it != ap.batches[l].rend(); ++it) {
-        launch_apply_bwd_partial(ap.d_local + it->local_begin, ap.d_nb, ap.d_chunks + it->chunk_begin,
-                                 it->chunk_end - it->chunk_begin, ap.d_parts, st);
-        launch_apply_bwd(ap.d_local + it->local_begin, ap.d_parts, it->local_end - it->local_begin, it->cap_bwd,
-                         it->max_m, st);
-      }
-    } else {
-      launch_apply_level(level_args(f, l), ap.lvl_max_m[l], 1, st);
-    }
+    launch_apply_bwd_level(level_args(f, l), st);
   }
   mark();
   launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);
@@ -185,10 +158,11 @@ void profile_apply(hs_factor_s* f, cudaStream_t st) {
   };
   std::fprintf(stderr, "[hs profile] apply (eager): permute-in %.3f ms\n", el(0));
   for (int l = 0; l < L; ++l)
-    std::fprintf(stderr, "[hs profile]   fwd level %d: %.3f ms (%zu batches)\n", l, el(1 + l), f->ap.batches[l].size());
+    std::fprintf(stderr, "[hs profile]   fwd level %d: %.3f ms (%zu tasks)\n", l, el(1 + l), f->ap.lv[l].ftask.size());
   std::fprintf(stderr, "[hs profile]   top: %.3f ms (N_top %lld)\n", el(1 + L), (long long)f->ntop);
   for (int k = 0; k < L; ++k)
-    std::fprintf(stderr, "[hs profile]   bwd level %d: %.3f ms\n", L - 1 - k, el(2 + L + k));
+    std::fprintf(stderr, "[hs profile]   bwd level %d: %.3f ms (%zu tasks)\n", L - 1 - k, el(2 + L + k),
+                 f->ap.lv[L - 1 - k].btask.size());
   std::fprintf(stderr, "[hs profile]   permute-out %.3f ms\n", el(2 + 2 * L));
   for (auto e : ev) cudaEventDestroy(e);
 }

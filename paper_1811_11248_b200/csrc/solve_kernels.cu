@@ -2,7 +2,6 @@
 // CSR SpMV / vector helpers of PCG.  HBM/latency bound: every factor byte is read once
 // per sweep.  A cluster's local solve runs in one warp with lane-owned vector entries
 // (entry l lives in lane l % 32, slot l / 32), so no block barrier is needed.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "device.h"
@@ -18,272 +17,143 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// y <- G^{-1} y (G lower, row-major ld m): row-oriented, coalesced row reads
-template <int SLOTS>
-__device__ __forceinline__ void warp_trsv_lower(const double* G, int m, double (&y)[SLOTS], int lane) {
-  for (int i = 0; i < m; ++i) {
-    double p = 0.0;
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      if (l < i) p += G[(int64_t)i * m + l] * y[s];
-    }
-    p = wsum(p);
-    if ((i & 31) == lane) {
-      const double gi = G[(int64_t)i * m + i];
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-        if (s == (i >> 5)) y[s] = (y[s] - p) / gi;
-    }
-  }
+// ---- dependency-driven level sweeps -------------------------------------------------------
+// Tasks are claimed in list order through an atomic ticket, so a claimed task only ever
+// waits on tasks with smaller tickets, which are held by running CTAs (no co-residency
+// assumption, no deadlock).  Producers: write, __threadfence, barrier, one atomic.
+// Consumers: acquire-load spin, barrier, then L2 (__ldcg) reads of the vector data.
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_ge(const int32_t* p, int32_t v) {
+  while (ld_acquire(p) < v) __nanosleep(32);
 }
 
-// y <- G^{-T} y : column-oriented backward substitution, rows of G read contiguously
-template <int SLOTS>
-__device__ __forceinline__ void warp_trsv_upper_t(const double* G, int m, double (&y)[SLOTS], int lane) {
-  for (int i = m - 1; i >= 0; --i) {
-    double xi = 0.0;
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s)
-      if (s == (i >> 5)) xi = y[s];
-    xi = __shfl_sync(0xffffffffu, xi, i & 31);
-    xi /= G[(int64_t)i * m + i];
-    if ((i & 31) == lane) {
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-        if (s == (i >> 5)) y[s] = xi;
+// Forward sweep of one level (Algorithm 2 lines 3-6 for every cluster of the level, in the
+// batch order of the factor).  Task (s, targets [t_begin, t_end)):
+//   wait until y_s is final (its `pre` forward events applied);
+//   z = T_s y_s (rows r..m-1 only unless `first`): the first task of s writes the coarse
+//   part z[0:r] to the parent vector and y_f = z[r:m] to the fine buffer (event `pre` on s);
+//   for every target q (one warp each): wait for q's earlier events, y_q -= C_s[:, q]^T y_f.
+// Every vector entry is updated in a fixed order (the event sequence), so the sweep is
+// deterministic.
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
+  __shared__ double ys[MAX_M];
+  __shared__ double z[MAX_M];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int t = s_task;
+    if (t >= a.nftask) return;
+    const FwdTask tk = a.ftask[t];
+    const ApplySrc S = a.src[tk.s];
+    const int m = S.m, r = S.r, K = m - r;
+    if (tid == 0) wait_ge(a.cnt + tk.s, S.pre);
+    __syncthreads();
+    for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
+    __syncthreads();
+    const int row0 = tk.first ? 0 : r;
+    for (int i = row0 + warp; i < m; i += nw) {
+      const double* Ti = S.T + (int64_t)i * m;
+      double acc = 0.0;
+      for (int j = lane; j < m; j += 32) acc += Ti[j] * ys[j];
+      acc = wsum(acc);
+      if (lane == 0) z[i] = acc;
     }
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      if (l < i) y[s] -= G[(int64_t)i * m + l] * xi;
+    __syncthreads();
+    if (tk.first) {
+      for (int i = tid; i < r; i += APPLY_THREADS) S.yc[i] = z[i];
+      for (int k = tid; k < K; k += APPLY_THREADS) S.yf[k] = z[r + k];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(a.cnt + tk.s, 1);
     }
-  }
-}
-
-// apply H_j (j = 0..r-1 forward, r-1..0 backward): y[j:] -= tau_j v_j (v_j . y[j:])
-template <int SLOTS>
-__device__ __forceinline__ void warp_reflect(const double* V, const double* tau, int m, int j, double (&y)[SLOTS],
-                                             int lane) {
-  const double t = tau[j];
-  if (t == 0.0) return;
-  double d = 0.0;
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    if (l >= j && l < m) d += V[(int64_t)j * m + l] * y[s];
-  }
-  d = wsum(d) * t;
-#pragma unroll
-  for (int s = 0; s < SLOTS; ++s) {
-    const int l = lane + 32 * s;
-    if (l >= j && l < m) y[s] -= d * V[(int64_t)j * m + l];
-  }
-}
-
-// Stage G (m x m), V (m x r) and tau (r) of a cluster in shared memory at `sm` when they
-// fit in `cap` doubles (one coalesced pass by the whole CTA instead of a latency-bound
-// chain of dependent global loads in the warp solve); returns the pointers to use.
-__device__ __forceinline__ void stage_local(const ApplyLocal& it, double* sm, int64_t cap, const double*& G,
-                                            const double*& V, const double*& tau) {
-  const int64_t mm = (int64_t)it.m * it.m, mr = (int64_t)it.m * it.r;
-  G = it.G;
-  V = it.V;
-  tau = it.tau;
-  if (mm + mr + it.r > cap) return;
-  for (int64_t e = threadIdx.x; e < mm; e += blockDim.x) sm[e] = it.G[e];
-  for (int64_t e = threadIdx.x; e < mr; e += blockDim.x) sm[mm + e] = it.V[e];
-  for (int e = threadIdx.x; e < it.r; e += blockDim.x) sm[mm + mr + e] = it.tau[e];
-  G = sm;
-  V = sm + mm;
-  tau = sm + mm + mr;
-}
-
-// The vector y (and the backward partial sums) change inside a level kernel, so they are
-// read with __ldcg (L2, bypassing the non-coherent L1); factor data are read normally.
-// forward: y_s <- U^T G^{-1} y_s (S_s then E_s of W_s = P_s G_s E_s S_s).
-// CTA-level device function (every thread of the CTA calls it): the CTA stages the
-// factors, warp 0 solves.  `sm` is the CTA's dynamic shared memory (cap doubles).
-template <int SLOTS>
-__device__ void dev_fwd_local(const ApplyLocal& it, double* sm, int64_t cap) {
-  if (it.m == 0) return;
-  const int lane = threadIdx.x & 31;
-  const double *G, *V, *tau;
-  stage_local(it, sm, cap, G, V, tau);
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double y[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      y[s] = l < it.m ? __ldcg(it.y + l) : 0.0;
-    }
-    warp_trsv_lower(G, it.m, y, lane);
-    for (int j = 0; j < it.r; ++j) warp_reflect(V, tau, it.m, j, y, lane);
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      if (l < it.m) it.y[l] = y[s];
-    }
-  }
-  __syncthreads();   // smem reusable by the CTA's next item
-}
-
-// forward: y_q -= C_s[:, col:col+len]^T y_f,s summed over the batch members s with q in n(s)
-// (G_s of Eq. CC:eqn:elim); warp-level, contributions in source order, the K loads of an
-// entry issued back to back.
-__device__ __forceinline__ void dev_fwd_scatter(const ApplyTarget& t, const ApplyContrib* __restrict__ con, int lane) {
-  for (int i0 = 0; i0 < t.len; i0 += 32) {
-    const int i = i0 + lane;
-    double acc = 0.0;
-    for (int c = t.c_begin; c < t.c_end; ++c) {
-      const ApplyContrib a = con[c];
-      if (i < t.len) {
-        const double* Ci = a.C + a.col + i;
-#pragma unroll 8
-        for (int k = 0; k < a.K; ++k) acc += Ci[(int64_t)k * a.ldC] * __ldcg(a.yf + k);
+    for (int g = tk.t_begin + warp; g < tk.t_end; g += nw) {
+      const FwdTgt q = a.ftgt[g];
+      if (lane == 0) wait_ge(a.cnt + q.q, q.seq);
+      __syncwarp();
+      for (int i = lane; i < q.len; i += 32) {
+        const double* Ci = S.C + q.col + i;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * z[r + k];
+        q.y[i] = __ldcg(q.y + i) - acc;
       }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(a.cnt + q.q, 1);
     }
-    if (i < t.len) t.yq[i] = __ldcg(t.yq + i) - acc;
+    __syncthreads();   // s_task, ys, z reusable
   }
 }
 
-// backward stage 1 (CTA-level, blockDim == BWD_CHUNK): for BWD_CHUNK columns c of C_s,
-// parts[k] = sum_c C_s[k][c] x_n[c] (x_n[c] read straight from the neighbour's segment); a
-// thread per column, the K rows in groups of 8 independent loads, fixed-order reduction.
-constexpr int NB_SMEM = 512;
-__device__ void dev_bwd_partial(const ApplyLocal* __restrict__ items, const ApplyNb* __restrict__ nbs,
-                                const ApplyChunk& ch, double* __restrict__ parts) {
-  const ApplyLocal it = items[ch.li];
-  __shared__ ApplyNb snb[NB_SMEM];
-  __shared__ double wred[BWD_CHUNK / 32][8];
-  const int nnb = it.nb_end - it.nb_begin;
-  const ApplyNb* nbl = nbs + it.nb_begin;
-  if (nnb <= NB_SMEM) {
-    for (int b = threadIdx.x; b < nnb; b += blockDim.x) snb[b] = nbl[b];
+// Backward sweep of one level (Algorithm 2 backward substitution, reverse batch order).
+// Task (s, columns [c0, c0+nc) of C_s): wait for the neighbours eliminated after s whose
+// columns overlap the chunk, then partial sums p[k] = sum_c C_s[k][c] x_n[c].  The last
+// chunk of s to arrive finishes s: x_f = y_f - sum of the partials (chunk order),
+// x_s = T_s^T [x_c; x_f], and publishes done[s].
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
+  __shared__ double xn[BWD_COLS];
+  __shared__ double u[MAX_M];
+  __shared__ int s_task, s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(a.ticket + 1, 1);
     __syncthreads();
-    nbl = snb;
-  }
-  const int K = it.m - it.r;
-  const int c = ch.c0 + threadIdx.x;
-  double x = 0.0;
-  if (c < it.kn) {
-    int lo = 0, hi = nnb - 1;   // last neighbour with col <= c
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (nbl[mid].col <= c) lo = mid;
-      else hi = mid - 1;
+    const int t = s_task;
+    if (t >= a.nbtask) return;
+    const BwdTask tk = a.btask[t];
+    const ApplySrc S = a.src[tk.s];
+    const int m = S.m, r = S.r, K = m - r;
+    if (tk.nc > 0) {
+      const int c1 = tk.c0 + tk.nc;
+      for (int b = S.nb_begin + tid; b < S.nb_end; b += APPLY_THREADS) {
+        const BwdNb nb = a.bnb[b];
+        if (nb.later && nb.col < c1 && nb.col + nb.len > tk.c0) wait_ge(a.done + nb.q, 1);
+      }
+      __syncthreads();
+      for (int b = S.nb_begin; b < S.nb_end; ++b) {   // gather x_n for the chunk
+        const BwdNb nb = a.bnb[b];
+        const int lo = max(nb.col, tk.c0), hi = min(nb.col + nb.len, c1);
+        for (int c = lo + tid; c < hi; c += APPLY_THREADS) xn[c - tk.c0] = __ldcg(nb.x + (c - nb.col));
+      }
+      __syncthreads();
+      double* part = a.parts + S.part + (int64_t)tk.chunk * K;
+      for (int k = warp; k < K; k += nw) {
+        const double* Ck = S.C + (int64_t)k * S.ldC + tk.c0;
+        double acc = 0.0;
+        for (int c = lane; c < tk.nc; c += 32) acc += Ck[c] * xn[c];
+        acc = wsum(acc);
+        if (lane == 0) part[k] = acc;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = (atomicAdd(a.bcnt + tk.s, 1) == S.nchunk - 1);
+      __syncthreads();
+      if (!s_last) continue;
+      __threadfence();
     }
-    x = __ldcg(nbl[lo].xq + (c - nbl[lo].col));
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* Cc = it.C + c;
-  for (int k0 = 0; k0 < K; k0 += 8) {
-    double p[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) p[q] = (c < it.kn && k0 + q < K) ? Cc[(int64_t)(k0 + q) * it.ldC] * x : 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) p[q] = wsum(p[q]);
-    if (lane == 0)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) wred[wid][q] = p[q];
-    __syncthreads();
-    if (threadIdx.x < 8 && k0 + threadIdx.x < K) {
+    const bool has_parts = tk.nc > 0;
+    for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.yc + i);
+    for (int k = tid; k < K; k += APPLY_THREADS) {
       double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += wred[w][threadIdx.x];
-      parts[ch.part + k0 + threadIdx.x] = s;
+      if (has_parts)
+        for (int q = 0; q < S.nchunk; ++q) s += __ldcg(a.parts + S.part + (int64_t)q * K + k);
+      u[r + k] = __ldcg(S.yf + k) - s;
     }
     __syncthreads();
-  }
-  __syncthreads();   // snb reusable
-}
-
-// backward stage 2 (CTA-level): x_f = y_f - sum_chunks parts (fixed order) ;
-// x_s <- G^{-T} U [x_c; x_f] (S_s^T E_s^T G_s^T of W_s^T, Alg. 2 backward substitution).
-template <int SLOTS>
-__device__ void dev_bwd_local(const ApplyLocal& it, const double* __restrict__ parts, double* sm, int64_t cap) {
-  if (it.m == 0) return;
-  __shared__ double xf[MAX_M];
-  const double *G, *V, *tau;
-  stage_local(it, sm, cap, G, V, tau);
-  const int K = it.m - it.r;
-  const int lane = threadIdx.x & 31;
-  const int nch = (it.nb_end > it.nb_begin && K > 0) ? (it.kn + BWD_CHUNK - 1) / BWD_CHUNK : 0;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < nch; ++q) s += __ldcg(parts + it.part_off + (int64_t)q * K + k);
-    xf[k] = __ldcg(it.y + it.r + k) - s;
-  }
-  __syncthreads();   // staged G/V and x_f visible
-  if (threadIdx.x < 32) {
-    double y[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      y[s] = l < it.r ? __ldcg(it.y + l) : (l < it.m ? xf[l - it.r] : 0.0);
+    for (int i = tid; i < m; i += APPLY_THREADS) {
+      double acc = 0.0;
+      for (int j = 0; j < m; ++j) acc += S.T[(int64_t)j * m + i] * u[j];
+      S.x[i] = acc;
     }
-    for (int j = it.r - 1; j >= 0; --j) warp_reflect(V, tau, it.m, j, y, lane);
-    warp_trsv_upper_t(G, it.m, y, lane);
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int l = lane + 32 * s;
-      if (l < it.m) it.y[l] = y[s];
-    }
-  }
-  __syncthreads();
-}
-
-// ---- per-batch kernels (eager path, HS_APPLY_PER_BATCH=1) ---------------------------------
-template <int SLOTS>
-__global__ void k_apply_fwd_local(const ApplyLocal* __restrict__ items, int n, int64_t cap) {
-  extern __shared__ double sm[];
-  dev_fwd_local<SLOTS>(items[blockIdx.x], sm, cap);
-}
-__global__ void k_apply_fwd_scatter(const ApplyTarget* __restrict__ tg, const ApplyContrib* __restrict__ con, int n) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w < n) dev_fwd_scatter(tg[w], con, threadIdx.x & 31);
-}
-__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_partial(const ApplyLocal* __restrict__ items,
-                                                                 const ApplyNb* __restrict__ nbs,
-                                                                 const ApplyChunk* __restrict__ chunks,
-                                                                 double* __restrict__ parts) {
-  dev_bwd_partial(items, nbs, chunks[blockIdx.x], parts);
-}
-template <int SLOTS>
-__global__ void k_apply_bwd(const ApplyLocal* __restrict__ items, const double* __restrict__ parts, int64_t cap) {
-  extern __shared__ double sm[];
-  dev_bwd_local<SLOTS>(items[blockIdx.x], parts, sm, cap);
-}
-
-// ---- one cooperative kernel per level and direction: the level's batches in order, a
-// grid-wide barrier between dependent phases (local -> scatter -> next batch) ---------------
-template <int SLOTS>
-__global__ void __launch_bounds__(BWD_CHUNK) k_apply_fwd_level(ApplyLevelArgs a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group g = cg::this_grid();
-  extern __shared__ double sm[];
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int b = 0; b < a.nbatch; ++b) {
-    const ApplyBatchDev B = a.batches[b];
-    for (int i = B.local_begin + blockIdx.x; i < B.local_end; i += gridDim.x) dev_fwd_local<SLOTS>(a.local[i], sm, a.cap);
-    g.sync();
-    for (int t = B.tgt_begin + gw; t < B.tgt_end; t += nwarps) dev_fwd_scatter(a.tgt[t], a.con, threadIdx.x & 31);
-    g.sync();
-  }
-}
-template <int SLOTS>
-__global__ void __launch_bounds__(BWD_CHUNK) k_apply_bwd_level(ApplyLevelArgs a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group g = cg::this_grid();
-  extern __shared__ double sm[];
-  for (int b = a.nbatch - 1; b >= 0; --b) {
-    const ApplyBatchDev B = a.batches[b];
-    for (int c = B.chunk_begin + blockIdx.x; c < B.chunk_end; c += gridDim.x)
-      dev_bwd_partial(a.local + B.local_begin, a.nb, a.chunks[c], a.parts);
-    g.sync();
-    for (int i = B.local_begin + blockIdx.x; i < B.local_end; i += gridDim.x)
-      dev_bwd_local<SLOTS>(a.local[i], a.parts, sm, a.cap);
-    g.sync();
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(a.done + tk.s, 1);
   }
 }
 
@@ -336,74 +206,26 @@ __global__ void k_spmv(const int64_t* __restrict__ rowptr, const int32_t* __rest
 
 }  // namespace
 
-static void set_dyn_smem(const void* f, size_t bytes, size_t& configured) {
-  if (bytes > configured) {
-    HS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    configured = bytes;
+static int apply_grid(const void* fn, int ntask) {
+  static int per_sm[2] = {0, 0}, nsm = 0;
+  const int k = fn == (const void*)k_apply_fwd ? 0 : 1;
+  if (!per_sm[k]) {
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], fn, APPLY_THREADS, 0));
+    int dev = 0;
+    HS_CUDA(cudaGetDevice(&dev));
+    HS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (per_sm[k] <= 0) fail(HS_E_INTERNAL, "apply level kernel does not fit on an SM");
   }
+  return std::max(1, std::min(ntask, nsm * per_sm[k]));
 }
-
-template <int S>
-void fwd_local_s(const ApplyLocal* d, int n, int64_t cap, cudaStream_t st) {
-  static size_t configured = 0;
-  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
-  set_dyn_smem((const void*)k_apply_fwd_local<S>, sm, configured);
-  k_apply_fwd_local<S><<<n, 128, sm, st>>>(d, n, cap);
-}
-void launch_apply_fwd_local(const ApplyLocal* d, int n, int64_t cap, int max_m, cudaStream_t st) {
-  if (n <= 0) return;
-  if (max_m <= 128) fwd_local_s<4>(d, n, cap, st);
-  else if (max_m <= 256) fwd_local_s<8>(d, n, cap, st);
-  else fwd_local_s<16>(d, n, cap, st);
+void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
+  if (a.nftask <= 0) return;
+  k_apply_fwd<<<apply_grid((const void*)k_apply_fwd, a.nftask), APPLY_THREADS, 0, st>>>(a);
   count_launch(1);
 }
-void launch_apply_fwd_scatter(const ApplyTarget* d, const ApplyContrib* c, int n, cudaStream_t st) {
-  if (n <= 0) return;
-  k_apply_fwd_scatter<<<(n + 3) / 4, 128, 0, st>>>(d, c, n);
-  count_launch(1);
-}
-void launch_apply_bwd_partial(const ApplyLocal* d_local_batch, const ApplyNb* nb, const ApplyChunk* ch, int n,
-                              double* parts, cudaStream_t st) {
-  if (n <= 0) return;
-  k_apply_bwd_partial<<<n, BWD_CHUNK, 0, st>>>(d_local_batch, nb, ch, parts);
-  count_launch(1);
-}
-template <int S>
-void bwd_s(const ApplyLocal* d, const double* parts, int n, int64_t cap, cudaStream_t st) {
-  static size_t configured = 0;
-  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(cap, 1);
-  set_dyn_smem((const void*)k_apply_bwd<S>, sm, configured);
-  k_apply_bwd<S><<<n, 128, sm, st>>>(d, parts, cap);
-}
-void launch_apply_bwd(const ApplyLocal* d, const double* parts, int n, int64_t cap, int max_m, cudaStream_t st) {
-  if (n <= 0) return;
-  if (max_m <= 128) bwd_s<4>(d, parts, n, cap, st);
-  else if (max_m <= 256) bwd_s<8>(d, parts, n, cap, st);
-  else bwd_s<16>(d, parts, n, cap, st);
-  count_launch(1);
-}
-template <int S>
-void level_s(const ApplyLevelArgs& a, int backward, cudaStream_t st) {
-  const void* fn = backward ? (const void*)k_apply_bwd_level<S> : (const void*)k_apply_fwd_level<S>;
-  const size_t sm = sizeof(double) * (size_t)std::max<int64_t>(a.cap, 1);
-  static size_t configured[2] = {0, 0};
-  set_dyn_smem(fn, sm, configured[backward ? 1 : 0]);
-  int per_sm = 0;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BWD_CHUNK, sm));
-  if (per_sm <= 0) fail(HS_E_INTERNAL, "apply level kernel: no co-resident CTA fits");
-  int dev = 0, nsm = 0;
-  HS_CUDA(cudaGetDevice(&dev));
-  HS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = nsm * std::min(per_sm, 4);
-  ApplyLevelArgs args = a;
-  void* params[] = {&args};
-  HS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BWD_CHUNK), params, sm, st));
-}
-void launch_apply_level(const ApplyLevelArgs& a, int max_m, int backward, cudaStream_t st) {
-  if (a.nbatch <= 0) return;
-  if (max_m <= 128) level_s<4>(a, backward, st);
-  else if (max_m <= 256) level_s<8>(a, backward, st);
-  else level_s<16>(a, backward, st);
+void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
+  if (a.nbtask <= 0) return;
+  k_apply_bwd<<<apply_grid((const void*)k_apply_bwd, a.nbtask), APPLY_THREADS, 0, st>>>(a);
   count_launch(1);
 }
 
