@@ -105,6 +105,9 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
     HS_CUDA(cudaSetDevice(device));
     HS_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
+    HS_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    HS_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     // keep freed factor memory in the stream-ordered pool: re-factoring reuses it without
     // going back to the driver (cudaFree of GB-sized arenas synchronises and is slow)
     cudaMemPool_t pool;
@@ -140,7 +143,11 @@ void hs_destroy(hs_handle h) {
     u->dev.cap = 0;
   }
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->side) cudaStreamSynchronize(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 

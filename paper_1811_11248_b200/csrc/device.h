@@ -37,7 +37,14 @@ struct CluItem {
   double* nu;       // kw scratch column norms
   int32_t m, kw, kn, ldB;
   int32_t level, cluster, pad0, pad1;
-  double* T;        // m x m row-major: T_s = U^T G^{-1} (formed after CPQR for the apply)
+};
+
+struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
+  const double* G;
+  const double* V;
+  const double* tau;
+  double* T;
+  int32_t m, r;
 };
 
 struct TrsmItem {   // one column tile of one cluster's B_s
@@ -165,7 +172,7 @@ void dense_potrf(double* A, int N, int ld, DevStatus* status, int level, double*
 constexpr int TOP_NB = 64;
 
 // T_s = U^T G^{-1} for the clusters of a batch (after CPQR; the rank comes from d_rank)
-void launch_form_T(const CluItem* d_items, const int32_t* d_rank, int n, int max_m, cudaStream_t st);
+void launch_form_T(const FormTItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);

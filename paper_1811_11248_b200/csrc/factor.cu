@@ -140,7 +140,7 @@ struct BlockStore {
 // batch's rank read-back, which already synchronises: a = [gather|potrf|trsm|cpqr],
 // b = [schur|write-back] of the previous batch.
 struct PhaseTimer {
-  cudaEvent_t a[6], b[3];
+  cudaEvent_t a[5], b[3];
   bool b_pending = false;
   PhaseTimer() {
     for (auto& e : a) HS_CUDA(cudaEventCreate(&e));
@@ -164,7 +164,6 @@ struct PhaseTimer {
   }
   void collect(hs_factor_stats_t& S) {   // after a synchronising point
     for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
-    S.t_phase_s[5] += el(a[4], a[5]);   // T_s formation (apply operator) with write-back/assembly
     collect_b(S);
   }
 };
@@ -194,6 +193,7 @@ hs_factor_s::~hs_factor_s() {
     if (p) cudaFreeAsync(p, st);
   };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
+  for (auto* p : d_formT) fr(p);
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
   for (auto& p : ap.lv) { fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); }
   fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr);
@@ -265,6 +265,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   double t_plan = 0.0;
   double t_sub[4] = {0, 0, 0, 0};
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
+  double t_tr[4] = {0, 0, 0, 0};   // level transition: block store build, upload_dir, arena alloc, release
   cudaEvent_t ev0, ev1;
   HS_CUDA(cudaEventCreate(&ev0));
   HS_CUDA(cudaEventCreate(&ev1));
@@ -363,8 +364,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       oP[s] = ioff; ioff += m;
     }
     L.arena_bytes = (size_t)off * sizeof(double);
+    const double ta0 = now_s();
     HS_CUDA(cudaMallocAsync(&L.arena, std::max<size_t>(L.arena_bytes, 8), st));
     HS_CUDA(cudaMallocAsync(&L.iarena, std::max<size_t>(sizeof(int32_t) * ioff, 4), st));
+    t_tr[2] += now_s() - ta0;
     L.G.resize(lev.nclus); L.V.resize(lev.nclus); L.tau.resize(lev.nclus); L.B.resize(lev.nclus);
     L.nu.resize(lev.nclus); L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
     for (int s = 0; s < lev.nclus; ++s) {
@@ -401,7 +404,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = ldB;
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
-        it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s; it.T = L.T[s];
+        it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
         max_m = std::max(max_m, m);
         if (m == 0) continue;
         double* p; int32_t ld, tr;
@@ -439,8 +442,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
       else launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
       HS_CUDA(cudaEventRecord(pt.a[4], st));
-      launch_form_T(upA.dptr<CluItem>(iC), d_rank, nb, max_m, st);
-      HS_CUDA(cudaEventRecord(pt.a[5], st));
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream
       pt.collect(S);
@@ -610,6 +611,26 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
       }
     }
+    // ---- apply operators T_s of the level, on the side stream (overlaps the next level) -------
+    {
+      std::vector<FormTItem> ft;
+      int max_m = 0;
+      for (int s = 0; s < lev.nclus; ++s)
+        if (L.cap[s] > 0) {
+          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], L.cap[s], L.rank[s]});
+          max_m = std::max(max_m, L.cap[s]);
+        }
+      FormTItem* d_ft = nullptr;
+      if (!ft.empty()) {
+        HS_CUDA(cudaEventRecord(h->ev_fork, st));
+        HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        HS_CUDA(cudaMallocAsync(&d_ft, sizeof(FormTItem) * ft.size(), h->side));
+        HS_CUDA(cudaMemcpyAsync(d_ft, ft.data(), sizeof(FormTItem) * ft.size(), cudaMemcpyHostToDevice, h->side));
+        launch_form_T(d_ft, (int)ft.size(), max_m, h->side);
+        HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // ft (pageable) is consumed by the copy
+      }
+      f->d_formT.push_back(d_ft);
+    }
     // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] -----------------
     const double tp2 = now_s();
     const int nP = lev.nclus / 2;
@@ -619,6 +640,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     BlockStore nbs;
     nbs.build(capn, En, st);
     if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
+    t_tr[0] += now_s() - tp2;
     // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
     // (c odd ? r(2P) : 0, d odd ? r(2Q) : 0); the upper child pair of a parent diagonal
     // block never occurs (c >= d), matching its lower-triangle semantics
@@ -681,10 +703,13 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     HS_CUDA(cudaStreamSynchronize(st));
     pt.collect_b(S);
     S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
+    const double tr1 = now_s();
     bs.release();
     bs = std::move(nbs);
     nbs.forget();
+    t_tr[3] += now_s() - tr1;
     if (l + 1 < an->L_top) bs.upload_dir();
+    t_tr[1] += now_s() - tr1;
     cap = capn;
     if (prof) {
       int64_t sm = 0, sr = 0, skn = 0, skw = 0, mx = 0;
@@ -746,6 +771,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     HS_CUDA(cudaStreamSynchronize(st));
     bs.release();
   }
+  HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // join the side stream (apply operators)
+  HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
   HS_CUDA(cudaEventRecord(ev1, st));
   HS_CUDA(cudaEventSynchronize(ev1));
   float ms = 0.f;
@@ -757,6 +784,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
+  if (std::getenv("HS_PROFILE"))
+    std::fprintf(stderr, "[hs profile] level transitions: block store build %.1f ms, release+upload_dir (sync) %.1f ms "
+                 "(release %.1f), arena alloc %.1f ms\n", 1e3 * t_tr[0], 1e3 * t_tr[1], 1e3 * t_tr[3], 1e3 * t_tr[2]);
   S.n_levels = an->L_top;
   // factor bytes read by the apply: T_s (m^2) and C_s ((m - r) kn) per cluster + top (N^2/2)
   double fb = 0.0;

@@ -286,19 +286,19 @@ __global__ void k_trsm_raw(const double* G, int ldG, int m, double* B, int ldB, 
 // apply's local steps (Algorithm 2) are parallel matvecs instead of a serial
 // triangular solve.  One CTA per (cluster, column tile): the tile of the identity is
 // forward-substituted with G (smem-staged for m <= SMEM_M, else read through L1/L2),
-// then the r reflectors are applied, H_0 first; the rank comes from the CPQR's output.
-__global__ void __launch_bounds__(256) k_form_T(const CluItem* __restrict__ items, const int32_t* __restrict__ rank,
-                                                int tiles_per) {
+// then the r reflectors are applied, H_0 first.  Launched once per level, after its last
+// batch, on a side stream: T_s is only read by the apply, so it overlaps the next level.
+__global__ void __launch_bounds__(256) k_form_T(const FormTItem* __restrict__ items, int tiles_per) {
   extern __shared__ double sm[];
   const int ci = blockIdx.x / tiles_per, tile = blockIdx.x % tiles_per;
-  const CluItem it = items[ci];
+  const FormTItem it = items[ci];
   const int m = it.m;
   const bool gs = m <= SMEM_M;
   const int TW = gs ? 64 : 32;
   const int c0 = tile * TW;
   if (m == 0 || c0 >= m) return;
   const int nc = min(TW, m - c0);
-  const int r = rank[ci];
+  const int r = it.r;
   const double* g;
   int ldg;
   double* x;
@@ -950,7 +950,7 @@ void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m
   k_trsm<<<n, 256, sm, st>>>(d_clu, d_items);
   count_launch(1);
 }
-void launch_form_T(const CluItem* d_items, const int32_t* d_rank, int n, int max_m, cudaStream_t st) {
+void launch_form_T(const FormTItem* d_items, int n, int max_m, cudaStream_t st) {
   if (n <= 0 || max_m <= 0) return;
   const bool gs = max_m <= SMEM_M;
   const int TW = gs ? 64 : 32;
@@ -960,7 +960,7 @@ void launch_form_T(const CluItem* d_items, const int32_t* d_rank, int n, int max
   const size_t sm = words * sizeof(double);
   set_smem((const void*)k_form_T, sm);
   const int tiles = (max_m + TW - 1) / TW;
-  k_form_T<<<n * tiles, 256, sm, st>>>(d_items, d_rank, tiles);
+  k_form_T<<<n * tiles, 256, sm, st>>>(d_items, tiles);
   count_launch(1);
 }
 void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st) {

@@ -109,6 +109,8 @@ struct ApplyPlan {
 struct hs_handle_s {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // factor work off the critical path (apply operators T_s)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool own_stream = false;
   int world = 1, rank = 0;
   std::string err;
@@ -128,6 +130,7 @@ struct hs_factor_s {
   double* d_top = nullptr;
   int64_t ntop = 0;
   std::vector<int32_t> top_sizes;
+  std::vector<hs::FormTItem*> d_formT;   // per level, on the side stream
   hs::ApplyPlan ap;
   hs_factor_stats_t stats{};
   // PCG work vectors

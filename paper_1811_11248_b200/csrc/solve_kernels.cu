@@ -30,6 +30,10 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
 __device__ __forceinline__ void wait_ge(const int32_t* p, int32_t v) {
   while (ld_acquire(p) < v) __nanosleep(32);
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+constexpr int NB_SMEM = 512;   // neighbour tables up to this size are staged in shared memory
 
 // Forward sweep of one level (Algorithm 2 lines 3-6 for every cluster of the level, in the
 // batch order of the factor).  Task (s, targets [t_begin, t_end)):
@@ -52,11 +56,19 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
     const FwdTask tk = a.ftask[t];
     const ApplySrc S = a.src[tk.s];
     const int m = S.m, r = S.r, K = m - r;
+    const int row0 = tk.first ? 0 : r;
+    // prefetch this task's rows of T_s and the targets' columns of C_s while y_s completes
+    for (int e = tid * 16; e < (m - row0) * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + (int64_t)row0 * m + e);
+    if (tk.t_end > tk.t_begin) {
+      const FwdTgt t0 = a.ftgt[tk.t_begin], t1 = a.ftgt[tk.t_end - 1];
+      const int cb = t0.col, ce = t1.col + t1.len;
+      for (int k = warp; k < K; k += nw)
+        for (int c = cb + lane * 16; c < ce; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
+    }
     if (tid == 0) wait_ge(a.cnt + tk.s, S.pre);
     __syncthreads();
     for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
     __syncthreads();
-    const int row0 = tk.first ? 0 : r;
     for (int i = row0 + warp; i < m; i += nw) {
       const double* Ti = S.T + (int64_t)i * m;
       double acc = 0.0;
@@ -99,6 +111,8 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
 __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
   __shared__ double xn[BWD_COLS];
   __shared__ double u[MAX_M];
+  __shared__ int ncol[NB_SMEM];
+  __shared__ const double* nx[NB_SMEM];
   __shared__ int s_task, s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
   for (;;) {
@@ -111,15 +125,32 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
     const int m = S.m, r = S.r, K = m - r;
     if (tk.nc > 0) {
       const int c1 = tk.c0 + tk.nc;
-      for (int b = S.nb_begin + tid; b < S.nb_end; b += APPLY_THREADS) {
-        const BwdNb nb = a.bnb[b];
+      const int nnb = S.nb_end - S.nb_begin;
+      const bool staged = nnb <= NB_SMEM;
+      for (int b = tid; b < nnb; b += APPLY_THREADS) {   // neighbour table -> smem; wait for later ones
+        const BwdNb nb = a.bnb[S.nb_begin + b];
+        if (staged) {
+          ncol[b] = nb.col;
+          nx[b] = nb.x;
+        }
         if (nb.later && nb.col < c1 && nb.col + nb.len > tk.c0) wait_ge(a.done + nb.q, 1);
       }
+      // prefetch the chunk's rows of C while the neighbours finish
+      for (int k = warp; k < K; k += nw)
+        for (int c = lane * 16; c < tk.nc; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + tk.c0 + c);
       __syncthreads();
-      for (int b = S.nb_begin; b < S.nb_end; ++b) {   // gather x_n for the chunk
-        const BwdNb nb = a.bnb[b];
-        const int lo = max(nb.col, tk.c0), hi = min(nb.col + nb.len, c1);
-        for (int c = lo + tid; c < hi; c += APPLY_THREADS) xn[c - tk.c0] = __ldcg(nb.x + (c - nb.col));
+      for (int c = tid; c < tk.nc; c += APPLY_THREADS) {   // gather x_n: owner by binary search
+        const int cc = tk.c0 + c;
+        int lo = 0, hi = nnb - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          const int col = staged ? ncol[mid] : a.bnb[S.nb_begin + mid].col;
+          if (col <= cc) lo = mid;
+          else hi = mid - 1;
+        }
+        const int col = staged ? ncol[lo] : a.bnb[S.nb_begin + lo].col;
+        const double* x = staged ? nx[lo] : a.bnb[S.nb_begin + lo].x;
+        xn[c] = __ldcg(x + (cc - col));
       }
       __syncthreads();
       double* part = a.parts + S.part + (int64_t)tk.chunk * K;
