@@ -108,12 +108,8 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
     HS_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     HS_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     HS_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-    // keep freed factor memory in the stream-ordered pool: re-factoring reuses it without
-    // going back to the driver (cudaFree of GB-sized arenas synchronises and is slow)
-    cudaMemPool_t pool;
-    HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    h->upA.dev.dc = &h->cache;
+    h->upB.dev.dc = &h->cache;
     *out = h;
   });
 }
@@ -121,6 +117,9 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
 hs_status hs_set_stream(hs_handle h, void* stream) {
   return guarded(h, [&] {
     require_device(h);
+    // cached memory is reused in host order, which is only stream-ordered on one stream:
+    // drain the old stream before switching
+    if (h->stream) HS_CUDA(cudaStreamSynchronize(h->stream));
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     if (stream) {
       h->stream = (cudaStream_t)stream;
@@ -138,7 +137,7 @@ void hs_destroy(hs_handle h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   // release the staging buffers while their stream is still alive (stream-ordered frees)
   for (hs::Upload* u : {&h->upA, &h->upB}) {
-    if (u->dev.d) cudaFreeAsync(u->dev.d, u->dev.st);
+    if (u->dev.d) h->cache.free(u->dev.d);
     u->dev.d = nullptr;
     u->dev.cap = 0;
   }
@@ -148,6 +147,7 @@ void hs_destroy(hs_handle h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  h->cache.trim();
   delete h;
 }
 
@@ -319,11 +319,11 @@ hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device) {
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
     double* din = nullptr;
-    HS_CUDA(cudaMallocAsync(&din, sizeof(double) * n, st));
+    din = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, b, din, on_device, st);
     hs::apply(f, din, din);
     HS_CUDA(cudaMemcpyAsync(x, din, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    HS_CUDA(cudaFreeAsync(din, st));
+    f->h->cache.free(din);
     HS_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -335,13 +335,13 @@ hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device) {
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
     double *dx = nullptr, *dy = nullptr;
-    HS_CUDA(cudaMallocAsync(&dx, sizeof(double) * n, st));
-    HS_CUDA(cudaMallocAsync(&dy, sizeof(double) * n, st));
+    dx = (double*)f->h->cache.alloc(sizeof(double) * n);
+    dy = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, x, dx, on_device, st);
     hs::spmv(f, dx, dy);
     HS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    HS_CUDA(cudaFreeAsync(dx, st));
-    HS_CUDA(cudaFreeAsync(dy, st));
+    f->h->cache.free(dx);
+    f->h->cache.free(dy);
     HS_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -358,23 +358,23 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
     double *db = nullptr, *dx = nullptr;
-    HS_CUDA(cudaMallocAsync(&db, sizeof(double) * n, st));
-    HS_CUDA(cudaMallocAsync(&dx, sizeof(double) * n, st));
+    db = (double*)f->h->cache.alloc(sizeof(double) * n);
+    dx = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, b, db, on_device, st);
     try {
       hs::pcg(f, db, dx, tol, maxit, rep);
     } catch (const hs::Error& e) {
       s_inner = e.status;
       if (e.status != HS_E_NOT_CONVERGED) {
-        cudaFreeAsync(db, st);
-        cudaFreeAsync(dx, st);
+        f->h->cache.free(db);
+        f->h->cache.free(dx);
         throw;
       }
       f->h->err = e.what();
     }
     HS_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    HS_CUDA(cudaFreeAsync(db, st));
-    HS_CUDA(cudaFreeAsync(dx, st));
+    f->h->cache.free(db);
+    f->h->cache.free(dx);
     HS_CUDA(cudaStreamSynchronize(st));
   });
   return s != HS_OK ? s : s_inner;

@@ -21,15 +21,59 @@
 
 namespace hs {
 
+void* DevCache::alloc(size_t bytes) {
+  const size_t c = size_class(std::max<size_t>(bytes, 1));
+  void* p = nullptr;
+  auto it = bins.find(c);
+  if (it != bins.end() && !it->second.empty()) {
+    p = it->second.back();
+    it->second.pop_back();
+    cached -= c;
+  } else {
+    cudaError_t e = cudaMalloc(&p, c);
+    if (e == cudaErrorMemoryAllocation) {   // give the cache back to the driver and retry once
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(&p, c);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(e == cudaErrorMemoryAllocation ? HS_E_OOM : HS_E_CUDA,
+           std::string("device allocation of ") + std::to_string(c) + " bytes: " + cudaGetErrorString(e));
+    }
+  }
+  live[p] = c;
+  in_use += c;
+  peak = std::max(peak, in_use);
+  return p;
+}
+void DevCache::free(void* p) {
+  if (!p) return;
+  auto it = live.find(p);
+  if (it == live.end()) return;
+  bins[it->second].push_back(p);
+  cached += it->second;
+  in_use -= it->second;
+  live.erase(it);
+}
+void DevCache::trim() {
+  if (!cached) return;
+  cudaDeviceSynchronize();
+  for (auto& b : bins)
+    for (void* p : b.second) cudaFree(p);
+  bins.clear();
+  cached = 0;
+}
+
 void DevScratch::ensure(size_t bytes) {
   if (bytes <= cap) return;
-  if (d) cudaFreeAsync(d, st);
+  dc->free(d);
   d = nullptr;
-  cap = std::max(bytes, cap * 2);
-  HS_CUDA(cudaMallocAsync(&d, cap, st));
+  cap = DevCache::size_class(std::max(bytes, cap * 2));
+  d = (char*)dc->alloc(cap);
 }
 DevScratch::~DevScratch() {
-  if (d) cudaFreeAsync(d, st);
+  if (d && dc) dc->free(d);
 }
 void HostStage::ensure(size_t bytes) {
   if (bytes <= cap) return;
@@ -49,12 +93,14 @@ struct BlockStore {
   std::vector<int32_t> cap;
   std::vector<std::vector<std::pair<int32_t, int64_t>>> rows;   // p -> sorted (q <= p, offset)
   size_t total = 0;
-  cudaStream_t st = nullptr;       // stream-ordered pool allocations
+  cudaStream_t st = nullptr;
+  DevCache* dc = nullptr;
 
-  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream) {
+  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache) {
     st = stream;
+    dc = cache;
     layout(caps, edges);
-    if (total) HS_CUDA(cudaMallocAsync(&d, total * sizeof(double), st));
+    if (total) d = (double*)dc->alloc(total * sizeof(double));
   }
   void layout(const std::vector<int32_t>& caps, const Adj& edges) {
     cap = caps;
@@ -111,10 +157,10 @@ struct BlockStore {
       }
       ptr[p + 1] = (int64_t)qq.size();
     }
-    HS_CUDA(cudaMallocAsync(&d_ptr, sizeof(int64_t) * (n + 1), st));
-    HS_CUDA(cudaMallocAsync(&d_q, sizeof(int32_t) * std::max<size_t>(qq.size(), 1), st));
-    HS_CUDA(cudaMallocAsync(&d_off, sizeof(int64_t) * std::max<size_t>(off.size(), 1), st));
-    HS_CUDA(cudaMallocAsync(&d_cap, sizeof(int32_t) * std::max(n, 1), st));
+    d_ptr = (int64_t*)dc->alloc(sizeof(int64_t) * (n + 1));
+    d_q = (int32_t*)dc->alloc(sizeof(int32_t) * std::max<size_t>(qq.size(), 1));
+    d_off = (int64_t*)dc->alloc(sizeof(int64_t) * std::max<size_t>(off.size(), 1));
+    d_cap = (int32_t*)dc->alloc(sizeof(int32_t) * std::max(n, 1));
     HS_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(d_q, qq.data(), sizeof(int32_t) * qq.size(), cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
@@ -124,7 +170,7 @@ struct BlockStore {
   BlockDir dir() const { return BlockDir{d, d_ptr, d_q, d_off, d_cap}; }
   void release() {
     for (void* p : {(void*)d, (void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
-      if (p) cudaFreeAsync(p, st);
+      if (p) dc->free(p);
     forget();
   }
   void forget() {
@@ -188,10 +234,12 @@ void check_status(DevStatus* d_status, DevStatus* h_status, cudaStream_t st) {
 
 hs_factor_s::~hs_factor_s() {
   using namespace hs;
-  cudaStream_t st = h ? h->stream : nullptr;
-  auto fr = [st](void* p) {
-    if (p) cudaFreeAsync(p, st);
-  };
+  if (!h) return;
+  // the apply operators are formed on the side stream: make sure that work is done before
+  // the arenas go back to the cache (the factor joined it, but a failed factor may not have)
+  if (h->side) cudaStreamSynchronize(h->side);
+  DevCache* dc = &h->cache;
+  auto fr = [dc](void* p) { dc->free(p); };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
   for (auto* p : d_formT) fr(p);
   for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
@@ -273,7 +321,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->d_rowptr = an->d_rowptr;      // borrowed from the analysis
   f->d_colind = an->d_colind;
   f->d_perm = an->d_perm;
-  HS_CUDA(cudaMallocAsync(&f->d_vals, sizeof(double) * std::max<int64_t>(nnz, 1), st));
+  DevCache& dc = h->cache;
+  f->d_vals = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(nnz, 1));
   HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz,
                           opt.values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
 
@@ -294,15 +343,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   std::vector<int32_t> cap(nleaf0);
   for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
   BlockStore bs;
-  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st);
+  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc);
   if (bs.total) HS_CUDA(cudaMemsetAsync(bs.d, 0, bs.total * sizeof(double), st));
   launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
   if (an->L_top > 0) bs.upload_dir();
 
   Upload& upA = h->upA;   // persistent per handle: pinned staging is allocated once
   Upload& upB = h->upB;
-  upA.dev.st = st;
-  upB.dev.st = st;
+  upA.dev.dc = &dc;
+  upB.dev.dc = &dc;
   int32_t* d_rank = nullptr;
   int32_t* h_rank = nullptr;
   int max_batch = 1;
@@ -365,8 +414,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     }
     L.arena_bytes = (size_t)off * sizeof(double);
     const double ta0 = now_s();
-    HS_CUDA(cudaMallocAsync(&L.arena, std::max<size_t>(L.arena_bytes, 8), st));
-    HS_CUDA(cudaMallocAsync(&L.iarena, std::max<size_t>(sizeof(int32_t) * ioff, 4), st));
+    L.arena = (double*)dc.alloc(std::max<size_t>(L.arena_bytes, 8));
+    L.iarena = (int32_t*)dc.alloc(std::max<size_t>(sizeof(int32_t) * ioff, 4));
     t_tr[2] += now_s() - ta0;
     L.G.resize(lev.nclus); L.V.resize(lev.nclus); L.tau.resize(lev.nclus); L.B.resize(lev.nclus);
     L.nu.resize(lev.nclus); L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
@@ -624,7 +673,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (!ft.empty()) {
         HS_CUDA(cudaEventRecord(h->ev_fork, st));
         HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        HS_CUDA(cudaMallocAsync(&d_ft, sizeof(FormTItem) * ft.size(), h->side));
+        d_ft = (FormTItem*)dc.alloc(sizeof(FormTItem) * ft.size());
         HS_CUDA(cudaMemcpyAsync(d_ft, ft.data(), sizeof(FormTItem) * ft.size(), cudaMemcpyHostToDevice, h->side));
         launch_form_T(d_ft, (int)ft.size(), max_m, h->side);
         HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // ft (pageable) is consumed by the copy
@@ -638,7 +687,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (int P = 0; P < nP; ++P) capn[P] = L.rank[2 * P] + L.rank[2 * P + 1];
     const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
     BlockStore nbs;
-    nbs.build(capn, En, st);
+    nbs.build(capn, En, st, &dc);
     if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
     t_tr[0] += now_s() - tp2;
     // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
@@ -739,7 +788,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     ap.vbase.push_back(vbase);
     vbase += N;
     if (N > 0) {
-      HS_CUDA(cudaMallocAsync(&f->d_top, sizeof(double) * N * N, st));
+      f->d_top = (double*)dc.alloc(sizeof(double) * N * N);
       HS_CUDA(cudaMemsetAsync(f->d_top, 0, sizeof(double) * N * N, st));
       std::vector<CopyItem> items;
       for (int P = 0; P < ntc; ++P)
@@ -799,14 +848,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   S.factor_bytes = fb;
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
-  HS_CUDA(cudaMallocAsync(&ap.d_y, sizeof(double) * std::max<int64_t>(vbase, 1), st));
-  HS_CUDA(cudaMallocAsync(&ap.d_yf, sizeof(double) * std::max<int64_t>(ap.ftotal, 1), st));
-  HS_CUDA(cudaMallocAsync(&ap.d_parts, sizeof(double) * std::max<int64_t>(ap.max_parts, 1), st));
-  HS_CUDA(cudaMallocAsync(&ap.d_ctr, sizeof(int32_t) * std::max<int64_t>(ap.ctr_total, 1), st));
+  ap.d_y = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));
+  ap.d_yf = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.ftotal, 1));
+  ap.d_parts = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.max_parts, 1));
+  ap.d_ctr = (int32_t*)dc.alloc(sizeof(int32_t) * std::max<int64_t>(ap.ctr_total, 1));
   auto up = [&](auto& vec, auto*& dptr) {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
     if (vec.empty()) return;
-    HS_CUDA(cudaMallocAsync(&dptr, sizeof(T) * vec.size(), st));
+    dptr = (T*)dc.alloc(sizeof(T) * vec.size());
     HS_CUDA(cudaMemcpyAsync(dptr, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice, st));
   };
   for (int l = 0; l < an->L_top; ++l) {   // offsets (stored as integers) -> absolute addresses

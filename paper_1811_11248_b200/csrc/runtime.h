@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "device.h"
@@ -15,11 +17,33 @@ struct hs_analysis_s {
 
 namespace hs {
 
+// Per-handle caching device allocator.  Every factor / apply / PCG buffer comes from here and
+// goes back here: blocks are binned by size class (<= 25% rounding) and reused in host
+// order.  All users of a handle's memory run on the handle's stream (the side stream is
+// joined before a factor is returned), so reuse in host order is stream-ordered reuse.
+// Memory goes back to the driver only on OOM (retry after a trim) and at hs_destroy;
+// steady-state re-factoring therefore makes no driver allocation calls at all.
+struct DevCache {
+  std::map<size_t, std::vector<void*>> bins;
+  std::unordered_map<void*, size_t> live;
+  size_t cached = 0, in_use = 0, peak = 0;
+  static size_t size_class(size_t b) {
+    if (b <= 4096) return 4096;
+    int k = 63 - __builtin_clzll((unsigned long long)b);   // 2^k <= b < 2^(k+1)
+    const size_t q = size_t(1) << (k - 2);                  // quarter steps
+    return (b + q - 1) / q * q;
+  }
+  void* alloc(size_t bytes);
+  void free(void* p);
+  void trim();        // return every cached block to the driver (synchronises the device)
+  ~DevCache() { trim(); }
+};
+
 // device buffer that grows on demand (used for per-launch descriptor uploads)
 struct DevScratch {
   char* d = nullptr;
   size_t cap = 0;
-  cudaStream_t st = nullptr;   // stream-ordered pool allocation
+  DevCache* dc = nullptr;
   void ensure(size_t bytes);
   ~DevScratch();
 };
@@ -114,6 +138,7 @@ struct hs_handle_s {
   bool own_stream = false;
   int world = 1, rank = 0;
   std::string err;
+  hs::DevCache cache;           // declared before the staging buffers (destroyed after them)
   hs::Upload upA, upB;          // descriptor staging, reused across factors
 };
 

@@ -171,8 +171,8 @@ void ensure_vectors(hs_factor_s* f) {
   const int64_t n = f->an->n;
   if (f->d_b) return;
   for (double** p : {&f->d_r, &f->d_z, &f->d_p, &f->d_q, &f->d_x, &f->d_b})
-    HS_CUDA(cudaMallocAsync(p, sizeof(double) * std::max<int64_t>(n, 1), f->h->stream));
-  HS_CUDA(cudaMallocAsync(&f->d_red, sizeof(double) * (RED_BLOCKS + 16), f->h->stream));
+    *p = (double*)f->h->cache.alloc(sizeof(double) * std::max<int64_t>(n, 1));
+  f->d_red = (double*)f->h->cache.alloc(sizeof(double) * (RED_BLOCKS + 16));
   HS_CUDA(cudaMallocHost(&f->h_red, sizeof(double) * 16));
 }
 
