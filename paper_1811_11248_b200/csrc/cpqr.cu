@@ -1,0 +1,679 @@
+// a3 + a4: rank-revealing compression of the deferred-compression block B_w = G_s^{-1} A_sw
+// (Eq. offdiag_new) by Businger-Golub column-pivoted QR, and the
+// sparsification rotation U^T of the neighbour columns B_n = G_s^{-1} A_sn
+// (Eq. CC:eqn:sparse).  Decisions follow SURVEY §8(c) O3.4 / DESIGN.md §2:
+//   * exact column norms nu_i = ||W[j:m, i]|| recomputed from the current entries each step;
+//   * tau_s = eps * nu_max(0) (relative, with the R-floor 1e-12 * max(nu_max(B_w), nu_max(B_n)));
+//   * stop with r = j as soon as nu_max <= tau_s (keep iff nu_max > tau_s);
+//   * pivot = lowest canonical column among nu_i >= (1 - 1e-10) nu_max;
+//   * LAPACK dlarfg Householder convention.
+//
+// Design (sm_100a).  One thread-block cluster of CS CTAs per graph cluster s.  The w-columns
+// are split in contiguous slices over the CTAs and live in shared memory for all r steps
+// (global-memory mode when they do not fit even at CS = 16).  Inside a CTA a column is
+// owned by a group of G lanes (G = rows / MR, rows interleaved), so the dot product and the
+// norm of a column are G-lane shuffle reductions instead of one thread's serial chain.
+// Per step the cluster exchanges one triple per CTA through distributed shared memory:
+// (local max norm M_c, its lowest local candidate i_c, nu(i_c)).  That resolves the pivot
+// with ONE cluster barrier whenever the lowest-ranked CTA holding a global candidate has
+// nu(i_c) >= (1 - 1e-10) max_c M_c (always, unless near-ties straddle the local and global
+// windows); otherwise a second exchange of the exact lowest candidates decides.
+// The neighbour columns are not touched during the pivoting loop: k_rotate_n applies
+// Q^T = H_{r-1}...H_0 to B_n afterwards, a column per lane group held in registers and the
+// reflectors staged in shared memory (rows [0, r) -> coarse-n, rows [r, m) -> C = U_2^T G^{-1} A_sn).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "device.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int CQ_THREADS = 512;
+constexpr int CQ_WARPS = CQ_THREADS / 32;
+constexpr double CQ_WINDOW = 1.0 - 1e-10;   // pivot tie window
+
+// lanes per column: the smallest power of two G with G * MR >= m (G <= 32)
+__host__ __device__ __forceinline__ int cq_group(int m, int MR) {
+  int G = 1;
+  while (G < 32 && G * MR < m) G <<= 1;
+  return G;
+}
+// Shared-memory layout of the w-slice: COLUMN-major, column stride ldm >= m with
+// ldm == G (mod 16) for G < 16, so that a half-warp (16/G columns x G consecutive rows)
+// touches 16 distinct 8-byte bank pairs, and a lane's rows l = t + i G sit at compile-time
+// offsets i G from its column base.
+__host__ __device__ __forceinline__ int cq_ldm(int m, int G) {
+  int l = m < 1 ? 1 : m;
+  if (G >= 16) return (l + 1) & ~1;
+  const int rem = ((l - G) % 16 + 16) % 16;
+  return l + (rem ? 16 - rem : 0);
+}
+__host__ __device__ __forceinline__ int cq_msg_words(int m);
+// dynamic shared memory words: W slice (SM mode) + norms + message staging and slots
+__host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, int MR, bool sm) {
+  const int wchunk = (kw + CS - 1) / CS;
+  const size_t w = sm ? (((size_t)wchunk * cq_ldm(m, cq_group(m, MR)) + 1) & ~(size_t)1) : 0;
+  return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * cq_msg_words(m);
+}
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int wmin_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- cluster messaging primitives (mbarrier + st.shared::cluster) ----------------------
+__device__ __forceinline__ uint32_t sm_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t remote(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void bar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)   // suspend (not spin) up to 1 ms per try
+        : "memory");
+}
+
+__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// bulk copy (async proxy) of `bytes` from this CTA's shared memory into another CTA's,
+// signalling complete_tx on the destination's mbarrier
+__device__ __forceinline__ void bulk_push(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src_cta), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct __align__(16) CqFb {     // fallback message: exact lowest candidate w.r.t. the global window
+  int F, pad[3];
+};
+struct CqShared {
+  unsigned long long bar1[2], bar2, bar3[2];   // step messages / fallback vector / fallback candidates
+  CqFb mine3[2], slot3[2][16];
+  double wred[CQ_WARPS];
+  __align__(16) double vstage[MAX_M + 8];      // fallback: owner's (tau, beta, v) staging
+  __align__(16) double vbuf[MAX_M + 8];        // fallback: received (tau, beta, v)
+};
+// Step message of one CTA (doubles): [0] M_c, [1] nu(i_c), [2] i_c (canonical, -1: none),
+// [3] tau, [4] beta of the Householder reflector of column i_c, [5..8) pad, [8, 8+m) v
+__host__ __device__ __forceinline__ int cq_msg_words(int m) { return (8 + m + 1) & ~1; }
+
+// The pivoting loop for a fixed group size G (lanes per column).
+//
+// Step j, every CTA c of the cluster (messages double-buffered by j & 1):
+//   (1) local max M_c of its column norms, its lowest local candidate i_c w.r.t. the local
+//       window, and -- speculatively -- the Householder reflector of column i_c; warp 0
+//       bulk-copies the message (M_c, nu(i_c), i_c, tau, beta, v) into slot c of every CTA
+//       (cp.async.bulk shared::cta -> shared::cluster, complete_tx on the receiver's bar1);
+//   (2) wait on the local bar1 and decide (stop, p) from the CS messages -- the same
+//       arithmetic in every CTA, so the decision is uniform.  The pivot is i_c of the
+//       lowest CTA c holding a global candidate, whose reflector arrived with it; only a
+//       near-tie straddling the local and global windows takes a second exchange (bar3)
+//       and an owner push of the reflector (bar2);
+//   (3) apply H_j to the local active columns and recompute their norms; the owner writes
+//       the pivot column as (beta, 0, ..., 0) and the reflector to V / tau / piv.
+// One mbarrier wait per step, no cluster-wide barrier inside the loop.
+template <int MR, int G, bool SM>
+__device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int relative, int32_t* rank_slot,
+                                          double* dsm, CqShared& sh, long long* trace) {
+  // HS_CQ_TRACE debug aid: clock64 timeline of cluster 0 / CTA 0 / thread 0
+#define CQ_TR(k)                                                            \
+  do {                                                                      \
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[k] = clock64(); \
+  } while (0)
+  CQ_TR(0);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int m = it.m, kw = it.kw, ld = it.ldB;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int t = tid % G, grp = tid / G;
+  constexpr int NGRP = CQ_THREADS / G;
+  const int wchunk = (kw + CS - 1) / CS;
+  const int w_lo = crank * wchunk;
+  const int nw = max(0, min(kw - w_lo, wchunk));
+  const int ldm = cq_ldm(m, G);
+  const int msgw = cq_msg_words(m);
+  const uint32_t msgb = (uint32_t)(msgw * 8);
+  // element (l, c) of the slice: shared memory column-major (SM) or B_s in place (row-major)
+  const int sr = SM ? 1 : ld, sc = SM ? ldm : 1;
+  // dynamic shared memory (16-byte aligned regions, the bulk copies require it):
+  // [W (SM mode): wchunk x ldm] [nu: wchunk] [mine: 2 x msgw] [slots: 2 x CS x msgw]
+  double* W = SM ? dsm : it.B + w_lo;
+  double* nu = SM ? dsm + (((size_t)wchunk * ldm + 1) & ~(size_t)1) : dsm;
+  double* mine = nu + ((wchunk + 1) & ~1);
+  double* slots = mine + 2 * msgw;
+  const int kiters = (nw + NGRP - 1) / NGRP;
+  const int nr = (m - t + G - 1) / G;   // rows l = t + i G < m of this lane: i < nr
+
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      bar_init(sm_addr(&sh.bar1[b]), 1);   // the local expect_tx arrival; data by complete_tx
+      bar_init(sm_addr(&sh.bar3[b]), 1);
+    }
+    bar_init(sm_addr(&sh.bar2), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // ---- stage the w-slice (transpose to column-major; coalesced global reads) ----------
+  if (SM) {
+    const int tot = m * nw;
+    const double* __restrict__ src = it.B + w_lo;
+    for (int e0 = tid; e0 < tot; e0 += 4 * CQ_THREADS) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * CQ_THREADS;
+        v[u] = e < tot ? src[(size_t)(e / nw) * ld + (e % nw)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * CQ_THREADS;
+        if (e < tot) W[(e % nw) * ldm + e / nw] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  CQ_TR(1);
+  // ---- initial column norms of the slice ------------------------------------------------
+  double lm = -1.0;
+  for (int k = 0; k < kiters; ++k) {
+    const int c = grp + k * NGRP;
+    const double* colp = W + (size_t)(c < nw ? c : 0) * sc + (size_t)t * sr;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < MR; ++i)
+      if (c < nw && i < nr) {
+        const double x = colp[(size_t)i * G * sr];
+        s += x * x;
+      }
+    s = group_sum<G>(s);
+    if (c < nw) {
+      const double v = sqrt(s);
+      if (t == 0) nu[c] = v;
+      lm = fmax(lm, v);
+    }
+  }
+  // max n-column norm of B_n from the TRSM: the same value in every CTA (R-floor)
+  const double Rn = __longlong_as_double((long long)*it.nmax);
+  cl.sync();   // barriers initialised cluster-wide before any remote complete_tx
+  CQ_TR(2);
+
+  const int kmax = min(m, kw);
+  double tau_s = 0.0;
+  int r = kmax;
+  int use3[2] = {0, 0}, use2 = 0;
+  for (int j = 0; j < kmax; ++j) {
+    const int buf = j & 1;
+    const uint32_t par = (uint32_t)((j >> 1) & 1);
+    double* mymsg = mine + buf * msgw;
+    double* slot = slots + (size_t)buf * CS * msgw;
+    // (1) local max, local candidate and its reflector -> every CTA
+    lm = wmax(lm);
+    if (lane == 0) sh.wred[wid] = lm;
+    if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
+    __syncthreads();
+    if (j < 60) CQ_TR(3 + 4 * j);
+    if (wid == 0) {
+      double Mc = lane < CQ_WARPS ? sh.wred[lane] : -1.0;
+      Mc = wmax(Mc);
+      const double thr_c = CQ_WINDOW * Mc;
+      int li = INT_MAX;
+      if (Mc >= 0.0)
+        for (int c = lane; c < nw; c += 32)
+          if (nu[c] >= thr_c) {
+            li = c;
+            break;
+          }
+      li = wmin_i(li);
+      if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
+        const double* col = W + (size_t)li * sc;
+        double xs = 0.0;
+        for (int l = j + 1 + lane; l < m; l += 32) {
+          const double b = col[(size_t)l * sr];
+          xs += b * b;
+        }
+        xs = wsum(xs);
+        const double alpha = col[(size_t)j * sr];
+        const double xnorm = sqrt(xs);
+        double tau, beta, rden;
+        if (xnorm == 0.0) {
+          tau = 0.0;
+          beta = alpha;
+          rden = 0.0;
+        } else {
+          const double h = sqrt(alpha * alpha + xnorm * xnorm);
+          beta = alpha >= 0.0 ? -h : h;
+          tau = (beta - alpha) / beta;
+          rden = 1.0 / (alpha - beta);   // dlarfg scales x by 1/(alpha - beta)
+        }
+        for (int l = lane; l < m; l += 32)
+          mymsg[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : col[(size_t)l * sr] * rden;
+        if (lane == 0) {
+          mymsg[1] = nu[li];
+          mymsg[2] = (double)(w_lo + li);
+          mymsg[3] = tau;
+          mymsg[4] = beta;
+        }
+      } else if (lane == 0) {
+        mymsg[1] = -1.0;
+        mymsg[2] = -1.0;
+      }
+      if (lane == 0) mymsg[0] = Mc;
+      fence_proxy_async();
+      __syncwarp();
+      if (lane < CS)
+        bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
+                  remote(sm_addr(&sh.bar1[buf]), lane));
+    }
+    // (2) decision from the CS messages (identical in every thread of every CTA)
+    bar_wait(sm_addr(&sh.bar1[buf]), par);
+    if (j < 60) CQ_TR(4 + 4 * j);
+    double M = -1.0;
+    for (int k = 0; k < CS; ++k) M = fmax(M, slot[(size_t)k * msgw]);
+    if (j == 0) {
+      tau_s = relative ? eps * M : eps;
+      if (relative && eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(M, Rn));
+    }
+    if (!(M > tau_s)) {
+      r = j;
+      break;
+    }
+    const double thr = CQ_WINDOW * M;
+    int k0 = 0;
+    while (!(slot[(size_t)k0 * msgw] >= thr)) ++k0;   // lowest CTA holding a global candidate
+    const double* vmsg = slot + (size_t)k0 * msgw;     // its reflector
+    int p = (int)vmsg[2];
+    if (!(vmsg[1] >= thr)) {
+      // near-tie straddling the local and global windows: exchange the exact candidates,
+      // then the owner forms and pushes the reflector of the true pivot
+      const uint32_t par3 = (uint32_t)(use3[buf]++ & 1);
+      if (tid == 0) bar_expect(sm_addr(&sh.bar3[buf]), (uint32_t)(CS * sizeof(CqFb)));
+      if (wid == 0) {
+        int li = INT_MAX;
+        for (int c = lane; c < nw; c += 32)
+          if (nu[c] >= thr) {
+            li = c;
+            break;
+          }
+        li = wmin_i(li);
+        if (lane == 0) {
+          sh.mine3[buf].F = li == INT_MAX ? INT_MAX : w_lo + li;
+          fence_proxy_async();
+        }
+        __syncwarp();
+        if (lane < CS)
+          bulk_push(remote(sm_addr(&sh.slot3[buf][crank]), lane), sm_addr(&sh.mine3[buf]), (uint32_t)sizeof(CqFb),
+                    remote(sm_addr(&sh.bar3[buf]), lane));
+      }
+      bar_wait(sm_addr(&sh.bar3[buf]), par3);
+      p = INT_MAX;
+      for (int k = 0; k < CS; ++k) p = min(p, sh.slot3[buf][k].F);
+      const int ow = p / wchunk;
+      const uint32_t vbytes = (uint32_t)(((8 + m) * 8 + 15) & ~15);
+      const uint32_t par2 = (uint32_t)(use2++ & 1);
+      if (tid == 0) bar_expect(sm_addr(&sh.bar2), vbytes);
+      if (crank == ow && wid == 0) {
+        const double* col = W + (size_t)(p - ow * wchunk) * sc;
+        double xs = 0.0;
+        for (int l = j + 1 + lane; l < m; l += 32) {
+          const double b = col[(size_t)l * sr];
+          xs += b * b;
+        }
+        xs = wsum(xs);
+        const double alpha = col[(size_t)j * sr];
+        const double xnorm = sqrt(xs);
+        double tau, beta, rden;
+        if (xnorm == 0.0) {
+          tau = 0.0;
+          beta = alpha;
+          rden = 0.0;
+        } else {
+          const double h = sqrt(alpha * alpha + xnorm * xnorm);
+          beta = alpha >= 0.0 ? -h : h;
+          tau = (beta - alpha) / beta;
+          rden = 1.0 / (alpha - beta);
+        }
+        for (int l = lane; l < m; l += 32)
+          sh.vstage[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : col[(size_t)l * sr] * rden;
+        if (lane == 0) {
+          sh.vstage[2] = (double)p;
+          sh.vstage[3] = tau;
+          sh.vstage[4] = beta;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane < CS)
+          bulk_push(remote(sm_addr(sh.vbuf), lane), sm_addr(sh.vstage), vbytes, remote(sm_addr(&sh.bar2), lane));
+      }
+      bar_wait(sm_addr(&sh.bar2), par2);
+      vmsg = sh.vbuf;
+    }
+    const int owner = p / wchunk, ploc = p - owner * wchunk;
+    const double tau = vmsg[3], beta = vmsg[4];
+    if (crank == owner && wid == 0) {   // the reflector for the apply operators / rotation
+      for (int l = lane; l < m; l += 32) it.V[(size_t)j * m + l] = vmsg[8 + l];
+      if (lane == 0) {
+        it.tau[j] = tau;
+        it.piv[j] = p;
+        nu[ploc] = -1.0;   // visible to the other warps after the next step's barrier
+      }
+    }
+    if (j < 60) CQ_TR(5 + 4 * j);
+    // (3) apply H_j to the active columns (two per group in flight), norms over rows > j.
+    // v is zero above row j, so rows < j pass through unchanged: every row of the lane is
+    // loaded, updated and stored without a row predicate; only the norm is masked (l > j).
+    double vr[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) vr[i] = (i < nr) ? vmsg[8 + t + i * G] : 0.0;
+    const int gi = (j >= t) ? (j - t) / G + 1 : 0;   // rows l > j of this lane: i >= gi
+    lm = -1.0;
+    for (int k = 0; k < kiters; k += 2) {
+      double* cp[2];
+      int cxs[2];
+      bool act[2], piv[2];
+      double x[2][MR], d[2], ss[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = grp + (k + u) * NGRP;
+        const bool in = (k + u) < kiters && c < nw;
+        const int cx = in ? c : 0;
+        cxs[u] = cx;
+        cp[u] = W + (size_t)cx * sc + (size_t)t * sr;
+        piv[u] = in && crank == owner && c == ploc;
+        act[u] = in && !piv[u] && nu[cx] >= 0.0;
+        d[u] = 0.0;
+#pragma unroll
+        for (int i = 0; i < MR; ++i) {
+          x[u][i] = (i < nr) ? cp[u][(size_t)i * G * sr] : 0.0;
+          d[u] += vr[i] * x[u][i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) d[u] = group_sum<G>(d[u]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double td = tau * d[u];
+        ss[u] = 0.0;
+        if (act[u]) {
+#pragma unroll
+          for (int i = 0; i < MR; ++i) {
+            const double y = x[u][i] - td * vr[i];
+            if (i < nr) cp[u][(size_t)i * G * sr] = y;
+            if (i >= gi) ss[u] += y * y;
+          }
+        } else if (piv[u]) {   // the pivot column: (beta, 0, ..., 0) from row j
+#pragma unroll
+          for (int i = 0; i < MR; ++i)
+            if (i < nr && t + i * G >= j) cp[u][(size_t)i * G * sr] = (t + i * G == j) ? beta : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) ss[u] = group_sum<G>(ss[u]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (act[u]) {
+          const double v = sqrt(ss[u]);
+          if (t == 0) nu[cxs[u]] = v;
+          lm = fmax(lm, v);
+        }
+    }
+    if (j < 60) CQ_TR(6 + 4 * j);
+  }
+  CQ_TR(250);
+  __syncthreads();
+  // ---- coarse-w rows back to global memory (rows [0, r) of the slice) -----------------
+  if (SM)
+    for (int e = tid; e < r * nw; e += CQ_THREADS) {
+      const int l = e / nw, c = e % nw;
+      it.B[(size_t)l * ld + w_lo + c] = W[(size_t)c * ldm + l];
+    }
+  cl.sync();   // no CTA leaves while another may still copy into its shared memory
+  CQ_TR(251);
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[252] = r;
+#undef CQ_TR
+  if (crank == 0 && tid == 0) *rank_slot = r;
+}
+
+template <int MR, bool SM>
+__global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
+                                                          int32_t* __restrict__ rank_out, long long* trace) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int item = blockIdx.x / (int)cl.num_blocks();
+  const CluItem it = items[item];
+  if (it.m == 0 || it.kw == 0) {   // uniform over the cluster: nobody reaches a cluster barrier
+    if (cl.block_rank() == 0 && threadIdx.x == 0) rank_out[item] = 0;
+    return;
+  }
+  extern __shared__ double dsm[];
+  __shared__ CqShared sh;
+  switch (cq_group(it.m, MR)) {
+    case 1: cpqr_body<MR, 1, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 2: cpqr_body<MR, 2, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 4: cpqr_body<MR, 4, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 8: cpqr_body<MR, 8, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 16: cpqr_body<MR, 16, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    default: cpqr_body<MR, 32, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+  }
+}
+
+// a4 on the n-columns: one CTA per tile of NGRP = CQ_THREADS / G columns of one cluster.
+template <int MR, int G>
+__device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, int r, const double* Vs,
+                                            const double* ts) {
+  const int m = it.m, ld = it.ldB;
+  const int tid = threadIdx.x, t = tid % G, grp = tid / G;
+  const bool act = grp < nc;
+  double* col = it.B + it.kw + c0 + grp;
+  double x[MR];
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    const int l = t + i * G;
+    x[i] = (act && l < m) ? col[(size_t)l * ld] : 0.0;
+  }
+  for (int j = 0; j < r; ++j) {
+    const double* v = Vs + (size_t)j * m;
+    double vv[MR];
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int l = t + i * G;
+      vv[i] = (l < m) ? v[l] : 0.0;
+      d += vv[i] * x[i];
+    }
+    d = group_sum<G>(d);
+    const double td = ts[j] * d;
+#pragma unroll
+    for (int i = 0; i < MR; ++i) x[i] -= td * vv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    const int l = t + i * G;
+    if (act && l < m) col[(size_t)l * ld] = x[i];
+  }
+}
+
+template <int MR>
+__global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restrict__ clu,
+                                                         const TrsmItem* __restrict__ items,
+                                                         const int32_t* __restrict__ rank, int cap_words) {
+  extern __shared__ double rsm[];
+  const TrsmItem ti = items[blockIdx.x];
+  const CluItem it = clu[ti.ci];
+  const int r = rank[ti.ci];
+  if (it.m == 0 || r == 0) return;
+  // reflectors staged in shared memory when they fit, else read through L1
+  const bool staged = (size_t)it.m * r + r <= (size_t)cap_words;
+  const double* Vs = it.V;
+  const double* ts = it.tau;
+  if (staged) {
+    for (int e = threadIdx.x; e < it.m * r; e += CQ_THREADS) rsm[e] = it.V[e];
+    for (int e = threadIdx.x; e < r; e += CQ_THREADS) rsm[(size_t)it.m * r + e] = it.tau[e];
+    __syncthreads();
+    Vs = rsm;
+    ts = rsm + (size_t)it.m * r;
+  }
+  switch (cq_group(it.m, MR)) {
+    case 1: rotate_body<MR, 1>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    case 2: rotate_body<MR, 2>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    case 4: rotate_body<MR, 4>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    case 8: rotate_body<MR, 8>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    case 16: rotate_body<MR, 16>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    default: rotate_body<MR, 32>(it, ti.c0, ti.nc, r, Vs, ts); break;
+  }
+}
+
+template <int MR, bool SM>
+void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
+                cudaStream_t st, long long* trace) {
+  static bool attr = false;
+  auto kern = k_cpqr3<MR, SM>;
+  if (!attr) {
+    HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(n * CS);
+  cfg.blockDim = dim3(CQ_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, relative, d_rank, trace));
+  count_launch(1);
+}
+
+}  // namespace
+
+// Host side: pick the cluster size CS (smallest power of two whose per-CTA w-slice fits the
+// shared-memory target; HS_CPQR_SMEM_KB overrides the 192 KB default), the rows-per-lane
+// template (MR = 8 up to m = 256, else 16) and shared vs global mode.
+int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
+                 int32_t* d_rank, cudaStream_t st) {
+  const int n = (int)h_items.size();
+  if (n <= 0) return 0;
+  static const size_t target = [] {
+    const char* e = std::getenv("HS_CPQR_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 192) * 1024;
+  }();
+  int max_m = 0;
+  for (const auto& it : h_items) max_m = std::max(max_m, it.m);
+  const int MR = max_m <= 256 ? 8 : 16;
+  auto need = [&](int cs, bool sm) {
+    size_t w = 2;
+    for (const auto& it : h_items)
+      if (it.m > 0 && it.kw > 0) w = std::max(w, cq_smem_words(it.m, it.kw, cs, MR, sm));
+    return w * sizeof(double);
+  };
+  const size_t cap = 200 * 1024 - sizeof(CqShared);
+  int CS = 1;
+  while (CS < 16 && need(CS, true) > std::min(target, cap)) CS *= 2;
+  const bool sm = need(CS, true) <= cap;
+  const size_t smem = need(CS, sm);
+  if (smem > cap) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
+  // HS_CQ_TRACE=k: clock64 timeline of the k-th launch (cluster 0, CTA 0) on stderr
+  static const int trace_at = [] {
+    const char* e = std::getenv("HS_CQ_TRACE");
+    return e ? std::atoi(e) : -1;
+  }();
+  static int launches = 0;
+  long long* trace = nullptr;
+  if (launches++ == trace_at) {
+    HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
+    HS_CUDA(cudaMemsetAsync(trace, 0, 256 * sizeof(long long), st));
+  }
+  if (MR == 8) {
+    if (sm) launch_one<8, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+    else launch_one<8, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+  } else {
+    if (sm) launch_one<16, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+    else launch_one<16, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+  }
+  if (trace) {
+    long long h[256];
+    HS_CUDA(cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(trace);
+    const long long t0 = h[0];
+    std::fprintf(stderr, "[cq trace] launch %d: n=%d CS=%d smem=%zu m0=%d kw0=%d r=%lld | stage %lld norms %lld cyc\n",
+                 trace_at, n, CS, smem, h_items[0].m, h_items[0].kw, h[252], h[1] - t0, h[2] - h[1]);
+    for (int j = 0; j < 60 && h[3 + 4 * j]; ++j)
+      std::fprintf(stderr, "[cq trace]  step %2d: B1 %6lld  C1 %6lld  B3 %6lld  upd %6lld\n", j,
+                   h[3 + 4 * j] - (j ? h[6 + 4 * (j - 1)] : h[2]), h[4 + 4 * j] - h[3 + 4 * j],
+                   h[5 + 4 * j] - h[4 + 4 * j], h[6 + 4 * j] - h[5 + 4 * j]);
+    std::fprintf(stderr, "[cq trace]  loop end %lld, exit %lld, total %lld cyc\n", h[250] - t0, h[251] - h[250], h[251] - t0);
+  }
+  return CS;
+}
+
+// rows per lane: 8 up to m = 256 (the kernels' group size G <= 32), else 16
+static int rot_mr(int max_m) { return max_m <= 256 ? 8 : 16; }
+int rot_tile_cols(int m, int max_m) { return CQ_THREADS / cq_group(std::max(m, 1), rot_mr(max_m)); }
+
+void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, const int32_t* d_rank,
+                     cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t words = std::min<size_t>((size_t)max_m * max_m + max_m, 24 * 1024);
+  const size_t smem = sizeof(double) * words;
+  if (max_m <= 256) {
+    static bool attr = false;
+    if (!attr) {
+      HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_rotate_n<8><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_rotate_n<16><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
+  }
+  count_launch(1);
+}
+
+}  // namespace hs

@@ -35,6 +35,7 @@ struct CluItem {
   double* B;        // B_s = [A_sw | A_sn], m x ldB row-major, w columns first
   int32_t* piv;     // m canonical pivot columns
   double* nu;       // kw scratch column norms
+  unsigned long long* nmax;   // max n-column norm of B_n (double bits; zeroed by the upload, set by TRSM)
   int32_t m, kw, kn, ldB;
   int32_t level, cluster, pad0, pad1;
 };
@@ -161,6 +162,15 @@ void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_
 // thread-block-cluster CPQR; picks the cluster size from the batch shape, returns it
 int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
                  int32_t* d_rank, cudaStream_t st);
+// a3+a4 v3 (cpqr.cu): thread-block cluster per graph cluster, column groups of G lanes,
+// one DSMEM exchange per step, n-columns rotated after the pivoting loop; returns CS
+int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
+                 int32_t* d_rank, cudaStream_t st);
+// a4 for the n-columns: B_n <- Q^T B_n with Q = H_0...H_{r-1} from the CPQR (rank from d_rank).
+// items: (cluster, first column within the n-part, count) tiles of rot_tile_cols(m) columns.
+int rot_tile_cols(int m, int max_m);   // columns per rotation tile (max_m: of the launch)
+void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, const int32_t* d_rank,
+                     cudaStream_t st);
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st);

@@ -370,7 +370,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ap.lv.resize(an->L_top);
 
   const bool prof = std::getenv("HS_PROFILE") != nullptr;
-  const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;   // A/B switch for the old kernel
+  // A/B switches for the previous CPQR kernels (single CTA / cluster with per-thread columns)
+  const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;
+  const bool cpqr_v2 = std::getenv("HS_CPQR_V2") != nullptr;
   for (int l = 0; l < an->L_top; ++l) {
     const Level& lev = an->levels[l];
     LevelRT& L = f->lv[l];
@@ -441,8 +443,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       const int nb = (int)Bt.size();
       std::vector<CopyItem> gather;
       std::vector<CluItem> clu(nb);
-      std::vector<TrsmItem> trsm;
+      std::vector<TrsmItem> trsm, rot;
       int max_m = 1;
+      for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bt[bi]]);
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bt[bi];
         const int32_t m = live[s];
@@ -470,15 +473,23 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           }
         const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
         for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
+        if (!cpqr_single_cta && !cpqr_v2 && kw > 0) {   // v3 rotates the n-columns in k_rotate_n
+          const int32_t rw = rot_tile_cols(m, max_m);
+          for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
+        }
         S.flops += (double)m * m * m / 3.0 + (double)m * m * ldB;
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
       }
       upA.reset();
-      const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm);
+      std::vector<unsigned long long> nmax(nb, 0ull);
+      const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
+                   iM = upA.add(nmax);
       upA.stage.ensure(upA.total);
       upA.dev.ensure(upA.total);
-      upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm);
+      for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
+      upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
+      upA.copy_in(iM, nmax);
       t_plan += now_s() - tp0;
       upA.send(st);
       HS_CUDA(cudaEventRecord(pt.a[0], st));
@@ -489,7 +500,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
       HS_CUDA(cudaEventRecord(pt.a[3], st));
       if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
-      else launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+      else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+      else {
+        launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+        launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
+      }
       HS_CUDA(cudaEventRecord(pt.a[4], st));
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream

@@ -266,12 +266,31 @@ __device__ void trsm_core(const double* G, int ldG, int m, double* B, int ldB, i
   }
 }
 
+// largest column norm of the n-columns [n0, nc) of the solved tile (R-floor of tau_s)
+__device__ void trsm_nmax(const double* x, int m, int TW, int n0, int nc, unsigned long long* nmax) {
+  const int c = threadIdx.x;
+  double s = -1.0;
+  if (c < TW && c >= n0 && c < nc) {
+    s = 0.0;
+    for (int i = 0; i < m; ++i) s += x[i * TW + c] * x[i * TW + c];
+    s = sqrt(s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0 && s >= 0.0) atomicMax(nmax, (unsigned long long)__double_as_longlong(s));
+}
+
 __global__ void k_trsm(const CluItem* __restrict__ clu, const TrsmItem* __restrict__ items) {
   extern __shared__ double smem[];
   const TrsmItem t = items[blockIdx.x];
   const CluItem it = clu[t.ci];
   if (it.m == 0) return;
   trsm_core(it.G, it.m, it.m, it.B, it.ldB, t.c0, t.nc, smem);
+  if (it.nmax && t.c0 + t.nc > it.kw) {
+    __syncthreads();
+    const int TW = it.m <= SMEM_M ? 64 : 32;
+    const double* x = it.m <= SMEM_M ? smem + it.m * it.m : smem;
+    trsm_nmax(x, it.m, TW, max(0, it.kw - t.c0), t.nc, it.nmax);
+  }
 }
 
 __global__ void k_trsm_raw(const double* G, int ldG, int m, double* B, int ldB, int ncols) {
