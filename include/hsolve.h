@@ -186,7 +186,9 @@ hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out
  *   HS_CEXP_TAU   [r]
  *   HS_CEXP_B     [m*ldB]    B_s after the elimination: columns [0,kw) = w part, [kw,kw+kn) =
  *                            n part; rows [0,r) = coarse rows, rows [r,m) of the n part = C.
- * Copies from the device; same length-query convention as hs_analysis_export. */
+ * Copies from the device; same length-query convention as hs_analysis_export.  G, V,
+ * TAU and B live in per-batch workspace that is recycled unless the factor was created
+ * with HS_KEEP_RECORDS=1 in the environment (HS_E_UNSUPPORTED otherwise). */
 enum { HS_CEXP_SHAPE = 0, HS_CEXP_G = 1, HS_CEXP_V = 2, HS_CEXP_TAU = 3, HS_CEXP_B = 4 };
 hs_status hs_factor_export_cluster(hs_factor f, int32_t key, int32_t level, int32_t cluster,
                                    double* out, int64_t cap, int64_t* len);

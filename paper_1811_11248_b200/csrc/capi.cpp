@@ -286,6 +286,9 @@ hs_status hs_factor_export_cluster(hs_factor f, int32_t key, int32_t level, int3
     };
     require_device(f->h);
     HS_CUDA(cudaStreamSynchronize(f->h->stream));
+    if (key != HS_CEXP_SHAPE && m > 0 && !L.G[cluster])
+      hs::fail(HS_E_UNSUPPORTED, "hs_factor_export_cluster: per-cluster records are freed after each batch; "
+                                 "factor with HS_KEEP_RECORDS=1 in the environment to keep them");
     switch (key) {
       case HS_CEXP_SHAPE:
         v = {(double)m, (double)r, (double)L.kw[cluster], (double)L.kn[cluster], (double)L.ldB[cluster]};

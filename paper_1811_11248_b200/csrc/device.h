@@ -154,6 +154,8 @@ int64_t launch_count();
 // values symmetry: *flag = 1 if |v[k] - v[tmap[k]]| > 1e-12 max(|v[k]|, |v[tmap[k]]|) for some k
 void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32_t* flag, cudaStream_t st);
 void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st);
+// splits items larger than ~16K elements into row ranges (one CTA each) in place
+void split_copies(std::vector<CopyItem>& items);
 void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d_r, int n, cudaStream_t st);
 void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st);
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);

@@ -218,6 +218,64 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Per-batch workspace whose last reader runs on the side stream (k_form_T): returned to the
+// cache only once the side-stream event recorded after that reader has completed.
+struct DeferredFree {
+  DevCache* dc = nullptr;
+  std::vector<std::pair<cudaEvent_t, std::vector<void*>>> q;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+  void push(cudaEvent_t e, std::vector<void*> ptrs) { q.push_back({e, std::move(ptrs)}); }
+  void drain(bool wait) {
+    size_t k = 0;
+    for (; k < q.size(); ++k) {
+      if (wait) HS_CUDA(cudaEventSynchronize(q[k].first));
+      else if (cudaEventQuery(q[k].first) != cudaSuccess) break;
+      for (void* p : q[k].second) dc->free(p);
+      pool.push_back(q[k].first);
+    }
+    cudaGetLastError();   // a not-ready query is not an error
+    q.erase(q.begin(), q.begin() + k);
+  }
+  ~DeferredFree() {
+    for (auto& e : q) cudaEventSynchronize(e.first);
+    for (auto& e : q)
+      for (void* p : e.second) dc->free(p);
+    for (auto& e : q) pool.push_back(e.first);
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
+// Bump allocator for the persistent C_s records of a factor: slabs from the cache.
+struct Slab {
+  DevCache* dc = nullptr;
+  std::vector<double*>* owned = nullptr;
+  double* cur = nullptr;
+  int64_t left = 0;
+  double* get(int64_t words) {
+    words = (words + 3) & ~int64_t(3);
+    if (words > left) {
+      const int64_t sz = std::max<int64_t>(words, (int64_t)8 << 20);   // >= 64 MB
+      cur = (double*)dc->alloc(sizeof(double) * sz);
+      owned->push_back(cur);
+      left = sz;
+    }
+    double* p = cur;
+    cur += words;
+    left -= words;
+    return p;
+  }
+};
+
 void check_status(DevStatus* d_status, DevStatus* h_status, cudaStream_t st) {
   HS_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   HS_CUDA(cudaStreamSynchronize(st));
@@ -241,8 +299,12 @@ hs_factor_s::~hs_factor_s() {
   DevCache* dc = &h->cache;
   auto fr = [dc](void* p) { dc->free(p); };
   fr(d_vals); fr(d_top);   // d_rowptr, d_colind, d_perm are borrowed from the analysis
-  for (auto* p : d_formT) fr(p);
-  for (auto& l : lv) { fr(l.arena); fr(l.iarena); }
+  for (auto& l : lv) {
+    fr(l.arena);
+    fr(l.iarena);
+    for (double* p : l.wchunks) fr(p);
+    for (double* p : l.cchunks) fr(p);
+  }
   for (auto& p : ap.lv) { fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); }
   fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
@@ -310,6 +372,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->h = h;
   f->an = an;
   f->opt = opt;
+  f->keep_records = std::getenv("HS_KEEP_RECORDS") != nullptr;
   double t_plan = 0.0;
   double t_sub[4] = {0, 0, 0, 0};
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
@@ -364,6 +427,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
 
   hs_factor_stats_t& S = f->stats;
   PhaseTimer pt;
+  DeferredFree deferred;
+  deferred.dc = &dc;
   ApplyPlan& ap = f->ap;
   int64_t vbase = 0;
   f->lv.resize(an->L_top);
@@ -390,9 +455,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     L.vlen = L.voff[lev.nclus];
     ap.vbase.push_back(vbase);
     vbase += L.vlen;
-    // ---- level arena: G, V (cap^2), tau (cap), nu (bound kw), B (cap x bound(kn + kw)) ----
-    std::vector<int64_t> oG(lev.nclus), oV(lev.nclus), oT(lev.nclus), oN(lev.nclus), oB(lev.nclus), oP(lev.nclus),
-        oX(lev.nclus);
+    // ---- level arena (persistent): T_s (cap^2) and the pivots; the rest is per batch ----
+    std::vector<int64_t> oX(lev.nclus), oP(lev.nclus);
     int64_t off = 0, ioff = 0;
     for (int s = 0; s < lev.nclus; ++s) {
       const int64_t m = cap[s];
@@ -402,16 +466,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                       l, (long long)m, MAX_M);
         fail(HS_E_UNSUPPORTED, buf);
       }
-      int64_t bn = 0, bw = 0;
-      for (int32_t q : lev.H[s]) bn += cap[q];
-      for (int32_t q : lev.w[s]) bw += cap[q];
-      oG[s] = off; off += m * m;
-      oV[s] = off; off += m * m;
-      oT[s] = off; off += m;
-      oN[s] = off; off += bw;
-      oB[s] = off; off += m * (bn + bw);
-      off = (off + 3) & ~int64_t(3);                 // 32-byte alignment
-      oX[s] = off; off += m * m;                     // T_s (apply operator)
+      oX[s] = off; off += (m * m + 3) & ~int64_t(3);   // T_s (apply operator), 32-byte aligned
       oP[s] = ioff; ioff += m;
     }
     L.arena_bytes = (size_t)off * sizeof(double);
@@ -419,11 +474,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     L.arena = (double*)dc.alloc(std::max<size_t>(L.arena_bytes, 8));
     L.iarena = (int32_t*)dc.alloc(std::max<size_t>(sizeof(int32_t) * ioff, 4));
     t_tr[2] += now_s() - ta0;
-    L.G.resize(lev.nclus); L.V.resize(lev.nclus); L.tau.resize(lev.nclus); L.B.resize(lev.nclus);
-    L.nu.resize(lev.nclus); L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
+    L.G.assign(lev.nclus, nullptr); L.V.assign(lev.nclus, nullptr); L.tau.assign(lev.nclus, nullptr);
+    L.B.assign(lev.nclus, nullptr); L.nu.assign(lev.nclus, nullptr); L.C.assign(lev.nclus, nullptr);
+    L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
+    Slab cslab;
+    cslab.dc = &dc;
+    cslab.owned = &L.cchunks;
     for (int s = 0; s < lev.nclus; ++s) {
-      L.G[s] = L.arena + oG[s]; L.V[s] = L.arena + oV[s]; L.tau[s] = L.arena + oT[s];
-      L.nu[s] = L.arena + oN[s]; L.B[s] = L.arena + oB[s]; L.piv[s] = L.iarena + oP[s]; L.T[s] = L.arena + oX[s];
+      L.piv[s] = L.iarena + oP[s];
+      L.T[s] = L.arena + oX[s];
     }
     std::vector<int32_t> live = cap;
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
@@ -446,6 +505,19 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<TrsmItem> trsm, rot;
       int max_m = 1;
       for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bt[bi]]);
+      // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
+      int64_t wsz = 0;
+      std::vector<int64_t> wo(nb);
+      for (int bi = 0; bi < nb; ++bi) {
+        const int32_t s = Bt[bi];
+        const int64_t m = live[s];
+        int64_t kn = 0, kw = 0;
+        for (int32_t q : lev.H[s]) kn += live[q];
+        for (int32_t q : lev.w[s]) kw += live[q];
+        wo[bi] = wsz;
+        wsz += 2 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
+      }
+      double* ws = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4));
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bt[bi];
         const int32_t m = live[s];
@@ -454,6 +526,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         for (int32_t q : lev.w[s]) kw += live[q];
         const int32_t ldB = kn + kw;
         L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = ldB;
+        double* w0 = ws + wo[bi];
+        L.G[s] = w0;
+        L.V[s] = w0 + (int64_t)m * m;
+        L.tau[s] = w0 + 2 * (int64_t)m * m;
+        L.nu[s] = L.tau[s] + ((m + 3) & ~3);
+        L.B[s] = L.nu[s] + ((kw + 3) & ~3);   // 32-byte aligned
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
         it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
@@ -481,6 +559,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
       }
+      split_copies(gather);
       upA.reset();
       std::vector<unsigned long long> nmax(nb, 0ull);
       const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
@@ -509,6 +588,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       check_status(d_status, &h_status, st);       // synchronises the stream
       pt.collect(S);
+      deferred.drain(false);
       const double tp1 = now_s();
       // ---- Schur update, write-back, apply plan ----------------------------------------------
       std::vector<SchurSrc> srcs;
@@ -521,6 +601,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       double tq_prev = now_s();
       bwd_batches.emplace_back();
       std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
+      // persistent C_s = rows [r, m) of the n-part, compacted to ld kn (the factor record
+      // the apply reads); the Schur update still reads C in place from the batch workspace
+      std::vector<FormTItem> ft;
+      int ft_max_m = 0;
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bt[bi];
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
@@ -530,6 +614,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.max_rank = std::max(S.max_rank, r);
         const int32_t K = m - r;
         const double* C = L.B[s] + (int64_t)r * ldB + kw;
+        if (m > 0) {
+          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, r});
+          ft_max_m = std::max(ft_max_m, m);
+        }
+        if (K > 0 && kn > 0) L.C[s] = cslab.get((int64_t)K * kn);
         // algorithmic flops of CPQR (+ rotation of the n-columns) and Schur
         double fq = 0.0;
         for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
@@ -582,13 +671,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               col += live[q];
             }
         }
+        if (L.C[s]) wb.push_back(CopyItem{C, L.C[s], ldB, kn, K, kn, 0, 0});
         const double tq1 = now_s();
         t_sub[1] += tq1 - tq0;
         // apply plan (Algorithm 2): the cluster's record, its forward target tasks (targets
         // grouped up to FWD_COLS columns) and its backward column chunks
         if (m > 0) {
           ApplySrc& as = AP.src[s];
-          as.T = L.T[s]; as.C = C; as.ldC = ldB; as.m = m; as.r = r; as.kn = kn;
+          as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
           as.pre = fev[s]++;
           as.nb_begin = (int32_t)AP.bnb.size();
           const int32_t tb = (int32_t)AP.ftgt.size();
@@ -636,13 +726,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         proc[Bt[bi]] = 1;
       }
       t_sub[3] += now_s() - tq3;
+      split_copies(wb);
       upB.reset();
       const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
-                   jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r);
+                   jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft);
       upB.stage.ensure(upB.total);
       upB.dev.ensure(upB.total);
       upB.copy_in(jT, tiles); upB.copy_in(jS, srcs); upB.copy_in(jN, nbc); upB.copy_in(jW, wb);
-      upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r);
+      upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
       t_plan += now_s() - tp1;
       upB.send(st);
       HS_CUDA(cudaEventRecord(pt.b[0], st));
@@ -655,6 +746,33 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       HS_CUDA(cudaEventRecord(pt.b[2], st));
       pt.b_pending = true;
       S.n_batches++;
+      // apply operators T_s = U^T G^{-1} of the batch on the side stream (they are only read
+      // by the apply): reads the workspace's G, V, tau, so the workspace (and the items'
+      // own buffer) go back to the cache once the side stream has passed this point
+      FormTItem* d_ft = nullptr;
+      cudaEvent_t ev_ft = nullptr;
+      if (!ft.empty()) {
+        d_ft = (FormTItem*)dc.alloc(sizeof(FormTItem) * ft.size());
+        // own copy of the items: upB's device buffer is rewritten by the next batch
+        HS_CUDA(cudaMemcpyAsync(d_ft, upB.dptr<FormTItem>(jF), sizeof(FormTItem) * ft.size(),
+                                cudaMemcpyDeviceToDevice, st));
+        HS_CUDA(cudaEventRecord(h->ev_fork, st));
+        HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        launch_form_T(d_ft, (int)ft.size(), ft_max_m, h->side);
+        ev_ft = deferred.take();
+        HS_CUDA(cudaEventRecord(ev_ft, h->side));
+      }
+      if (f->keep_records) {
+        L.wchunks.push_back(ws);
+        if (d_ft) deferred.push(ev_ft, {d_ft});
+      } else {
+        if (ev_ft) deferred.push(ev_ft, {ws, d_ft});
+        else dc.free(ws);
+        for (int bi = 0; bi < nb; ++bi) {
+          const int32_t s = Bt[bi];
+          L.G[s] = L.V[s] = L.tau[s] = L.nu[s] = L.B[s] = nullptr;
+        }
+      }
       if (const char* dd = std::getenv("HS_DEBUG_DUMP")) {   // debug aid: block store after every batch
         HS_CUDA(cudaStreamSynchronize(st));
         char path[512];
@@ -674,26 +792,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           std::fclose(fp);
         }
       }
-    }
-    // ---- apply operators T_s of the level, on the side stream (overlaps the next level) -------
-    {
-      std::vector<FormTItem> ft;
-      int max_m = 0;
-      for (int s = 0; s < lev.nclus; ++s)
-        if (L.cap[s] > 0) {
-          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], L.cap[s], L.rank[s]});
-          max_m = std::max(max_m, L.cap[s]);
-        }
-      FormTItem* d_ft = nullptr;
-      if (!ft.empty()) {
-        HS_CUDA(cudaEventRecord(h->ev_fork, st));
-        HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        d_ft = (FormTItem*)dc.alloc(sizeof(FormTItem) * ft.size());
-        HS_CUDA(cudaMemcpyAsync(d_ft, ft.data(), sizeof(FormTItem) * ft.size(), cudaMemcpyHostToDevice, h->side));
-        launch_form_T(d_ft, (int)ft.size(), max_m, h->side);
-        HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // ft (pageable) is consumed by the copy
-      }
-      f->d_formT.push_back(d_ft);
     }
     // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] -----------------
     const double tp2 = now_s();
@@ -753,6 +851,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       ap.ctr_total += 3 * (int64_t)lev.nclus + 2;
       ap.max_parts = std::max(ap.max_parts, AP.parts);
     }
+    split_copies(asmb);
     upA.reset();
     const size_t iA = upA.add(asmb);
     upA.stage.ensure(upA.total);
@@ -817,6 +916,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           if (P != Q)
             items.push_back(CopyItem{src, f->d_top + toff[Q] * N + toff[P], cap[Q], (int32_t)N, cap[Q], cap[P], 1, 0});
         }
+      split_copies(items);
       upA.reset();
       const size_t iA = upA.add(items);
       upA.stage.ensure(upA.total);
@@ -837,6 +937,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   }
   HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // join the side stream (apply operators)
   HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
+  deferred.drain(true);
   HS_CUDA(cudaEventRecord(ev1, st));
   HS_CUDA(cudaEventSynchronize(ev1));
   float ms = 0.f;
@@ -848,6 +949,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
+  if (std::getenv("HS_PROFILE"))
+    std::fprintf(stderr, "[hs profile] device cache: in use %.2f GB, peak %.2f GB, cached %.2f GB\n", dc.in_use / 1e9,
+                 dc.peak / 1e9, dc.cached / 1e9);
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] level transitions: block store build %.1f ms, release+upload_dir (sync) %.1f ms "
                  "(release %.1f), arena alloc %.1f ms\n", 1e3 * t_tr[0], 1e3 * t_tr[1], 1e3 * t_tr[3], 1e3 * t_tr[2]);

@@ -71,11 +71,12 @@ __global__ void k_copy2d(const CopyItem* __restrict__ items) {
     }
     return;
   }
-  if (!it.trans) {
-    const int64_t tot = (int64_t)it.rows * it.cols;
-    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int i = (int)(e / it.cols), j = (int)(e % it.cols);
-      it.dst[(int64_t)i * it.dld + j] = it.src[(int64_t)i * it.sld + j];
+  if (!it.trans) {   // a warp per row (no integer division), rows strided over the warps
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = w; i < it.rows; i += nw) {
+      const double* __restrict__ s = it.src + (int64_t)i * it.sld;
+      double* __restrict__ d = it.dst + (int64_t)i * it.dld;
+      for (int j = lane; j < it.cols; j += 32) d[j] = s[j];
     }
     return;
   }
@@ -931,6 +932,30 @@ void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32
   if (nnz <= 0) return;
   k_symcheck<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, tmap, nnz, flag);
   count_launch(1);
+}
+void split_copies(std::vector<CopyItem>& items) {
+  constexpr int64_t PIECE = 16384;
+  bool big = false;
+  for (const auto& it : items) big |= (int64_t)it.rows * it.cols > PIECE && it.trans != 2;
+  if (!big) return;
+  std::vector<CopyItem> out;
+  out.reserve(items.size() * 2);
+  for (const auto& it : items) {
+    if ((int64_t)it.rows * it.cols <= PIECE || it.trans == 2) {
+      out.push_back(it);
+      continue;
+    }
+    const int step = std::max(1, (int)(PIECE / std::max(it.cols, 1)));
+    for (int i0 = 0; i0 < it.rows; i0 += step) {
+      CopyItem p = it;
+      p.rows = std::min(step, it.rows - i0);
+      // dst rows [i0, i0+rows); source rows (trans 0) or source columns (trans 1)
+      p.dst = it.dst + (int64_t)i0 * it.dld;
+      p.src = it.trans ? it.src + i0 : it.src + (int64_t)i0 * it.sld;
+      out.push_back(p);
+    }
+  }
+  items.swap(out);
 }
 void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st) {
   if (n <= 0) return;

@@ -36,7 +36,11 @@ struct DevCache {
   void* alloc(size_t bytes);
   void free(void* p);
   void trim();        // return every cached block to the driver (synchronises the device)
-  ~DevCache() { trim(); }
+  ~DevCache() {       // the handle is going away: also blocks leaked by a failed call
+    trim();
+    for (auto& kv : live) cudaFree(kv.first);
+    live.clear();
+  }
 };
 
 // device buffer that grows on demand (used for per-launch descriptor uploads)
@@ -92,10 +96,13 @@ struct LevelRT {
   std::vector<int32_t> cap, rank, kn, kw, ldB;
   std::vector<int64_t> voff;            // apply-vector offsets (prefix sums of cap)
   int64_t vlen = 0;
-  double* arena = nullptr;              // G, V, tau, nu, B of every cluster
-  int32_t* iarena = nullptr;            // pivots
-  std::vector<double*> G, V, tau, B, nu, T;
+  double* arena = nullptr;              // T_s of every cluster (persistent: the apply operators)
+  int32_t* iarena = nullptr;            // pivots (persistent)
+  // per-batch workspace G, V, tau, nu, B (freed after the batch unless HS_KEEP_RECORDS);
+  // C_s compacted into per-batch chunks of the persistent factor
+  std::vector<double*> G, V, tau, B, nu, T, C;
   std::vector<int32_t*> piv;
+  std::vector<double*> wchunks, cchunks;
   size_t arena_bytes = 0;
 };
 
@@ -155,8 +162,8 @@ struct hs_factor_s {
   double* d_top = nullptr;
   int64_t ntop = 0;
   std::vector<int32_t> top_sizes;
-  std::vector<hs::FormTItem*> d_formT;   // per level, on the side stream
   hs::ApplyPlan ap;
+  bool keep_records = false;             // HS_KEEP_RECORDS: per-cluster G, V, tau, B stay exportable
   hs_factor_stats_t stats{};
   // PCG work vectors
   double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_x = nullptr, *d_b = nullptr;
