@@ -196,9 +196,11 @@ def assemble_top(st: BlockStore, nclus):
 
 
 def factor(an: Analysis, rowptr, colind, vals, eps=1e-2, relative=True, inject=None,
-           keep_debug=False, snapshot=None) -> Factor:
+           keep_debug=False, snapshot=None, max_levels=None) -> Factor:
     """Algorithm 1.  inject: {(l, s): (r, piv)} decision injection.
-    snapshot(l, b, store) is called after every batch when given (debug)."""
+    snapshot(l, b, store) is called after every batch when given (debug).
+    max_levels: stop after that many levels (partial record for sampled parity at full
+    size: elims only, no top factor)."""
     st = initial_blocks(an, rowptr, colind, vals)
     elims, live0, live1 = [], [], []
     for l, lev in enumerate(an.levels):
@@ -215,6 +217,8 @@ def factor(an: Analysis, rowptr, colind, vals, eps=1e-2, relative=True, inject=N
                 snapshot(l, bi, st)
         elims.append(lv)
         live1.append(list(st.live))
+        if max_levels is not None and l + 1 >= max_levels:
+            return Factor(an, eps, relative, elims, live0, live1, None, None)
         Hn = an.levels[l + 1].H if l + 1 < len(an.levels) else an.H_top
         st = next_level(st, Hn, lev.nclus // 2)
     ntop = 1 << (an.D - an.L_top)

@@ -1,0 +1,104 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(-m gpu).  The oracle cannot factor these systems in seconds, so the checks are
+  * analyze: every level's schedule bit-exact with oracle/analyze.py (integer work),
+  * level 0 (the paper's dominant level): ranks and pivot sequences of every
+    cluster against the oracle run for exactly one level (sampled output the oracle can
+    compute), in elimination order up to the first decision the margins flag,
+  * properties that hold at any size: the factor is a symmetric positive definite linear
+    operator, the SpMV equals scipy's on sampled rows, and
+    PCG reaches the tolerance with the true residual (north_star "PCG to 1e-8").
+"""
+import numpy as np
+import pytest
+
+from problems import gen_config
+from oracle.analyze import analyze
+from oracle.factor import factor as ofactor
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    from paper_1811_11248_b200 import hsolve
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    hsolve.lib()
+    return hsolve
+
+
+@pytest.fixture(scope="module")
+def handle(H):
+    return H.hs_create(0)
+
+
+def _analysis_equal(H, a, an):
+    # (tests/test_analyze_parity.py compares every export on CPU; here: the schedule the
+    # factor below actually ran, at the bench's size)
+    info = H.hs_analysis_get_info(a)
+    assert info["L_top"] == an.L_top and info["depth"] == an.D
+    assert np.array_equal(H.hs_analysis_export(a, H.HS_EXP_PERM), an.perm)
+    for l, lev in enumerate(an.levels):
+        flat = np.concatenate([np.asarray(b, dtype=np.int64) for b in lev.batches]) if lev.batches else np.zeros(0)
+        assert np.array_equal(H.hs_analysis_export(a, H.HS_EXP_BATCH_IDX, l), flat), f"level {l} batches"
+
+
+def _level0_parity(H, f, p, an):
+    fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=p.eps, max_levels=1)
+    g_r = H.hs_factor_export(f, H.HS_FEXP_RANKS, 0)
+    g_pp = H.hs_factor_export(f, H.HS_FEXP_PIV_PTR, 0)
+    g_pv = H.hs_factor_export(f, H.HS_FEXP_PIV, 0)
+    checked = 0
+    for eb in fac.elims[0]:
+        for e in eb:
+            gpiv = g_pv[g_pp[e.s]:g_pp[e.s + 1]]
+            if g_r[e.s] == e.r and np.array_equal(gpiv, e.piv):
+                checked += 1
+                continue
+            # a decision within the margins may legitimately differ; everything after it
+            # then sees a different Schur complement, so the comparison stops there
+            assert e.flagged, (f"level-0 decision mismatch at cluster {e.s} (unflagged, mu={e.mu:.2e}, "
+                               f"pi={e.pi:.2e}): gpu r={g_r[e.s]} oracle r={e.r}")
+            return checked
+    return checked
+
+
+def _operator_properties(H, f, n, seeds=(11, 12, 13)):
+    rng = np.random.default_rng(seeds[0])
+    for sd in seeds:
+        rng = np.random.default_rng(sd)
+        u, v = rng.standard_normal(n), rng.standard_normal(n)
+        Mu, Mv = H.hs_apply(f, u), H.hs_apply(f, v)
+        # symmetry <M u, v> = <u, M v> (relative to the Cauchy-Schwarz scale)
+        scale = np.linalg.norm(Mu) * np.linalg.norm(v)
+        assert abs(Mu @ v - u @ Mv) <= 1e-12 * scale
+        # positivity
+        assert u @ Mu > 0 and v @ Mv > 0
+        # linearity
+        a, b = 0.75, -1.5
+        Mw = H.hs_apply(f, a * u + b * v)
+        assert np.linalg.norm(Mw - (a * Mu + b * Mv)) <= 1e-12 * np.linalg.norm(Mw)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_full_size_config(H, handle, name):
+    p = gen_config(name)
+    an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                 leaf_columns=p.leaf_columns)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+    _analysis_equal(H, a, an)
+    f = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
+    checked = _level0_parity(H, f, p, an)
+    assert checked >= an.levels[0].nclus // 2, f"only {checked} level-0 clusters compared before a flagged decision"
+    _operator_properties(H, f, p.n)
+    # SpMV on sampled rows against scipy
+    A = p.to_scipy()
+    x = np.random.default_rng(5).standard_normal(p.n)
+    y = H.hs_spmv(f, x)
+    rows = np.random.default_rng(6).choice(p.n, 2000, replace=False)
+    assert np.allclose(y[rows], A[rows] @ x, rtol=1e-13, atol=1e-12)
+    xs, rep = H.hs_pcg(f, p.b, tol=p.tol)
+    assert rep["converged"]
+    res = np.linalg.norm(p.b - A @ xs) / np.linalg.norm(p.b)
+    assert res <= 10 * p.tol and abs(res - rep["relres_true"]) <= 1e-3 * max(res, 1e-300) + 1e-15

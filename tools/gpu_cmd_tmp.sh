@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
-HS_PROFILE=1 timeout 300 python tools/profile_run.py C2 > gpurun_out/profile_c2.log 2>&1
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
-tail -3 gpurun_out/gpu_tests.log
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -m gpu -x -q --durations=5 > gpurun_out/gpu_full.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_full.log
+tail -15 gpurun_out/gpu_full.log
