@@ -358,9 +358,9 @@ CONFIGS = {
     # configs[2]: 256x256x10 slab, ratio 1e4, lognormal sigma 2, column leaves (8 columns)
     "C3": lambda **kw: gen_slab(256, 10, **kw),
     # configs[3]: Q1 first-order-Stokes 512x512x20 nodes x 2 DOF
-    "C4": lambda **kw: gen_stokes_q1(512, 512, 20, aspect=1e3, leaf_columns=2, **kw),
+    "C4": lambda **kw: gen_stokes_q1(512, 512, 20, aspect=1e3, **{"leaf_columns": 2, **kw}),
     # configs[4]: 1024x1024x16 nodes x 2 DOF, aspect 1e4
-    "C5": lambda **kw: gen_stokes_q1(1024, 1024, 16, aspect=1e4, leaf_columns=4, **kw),
+    "C5": lambda **kw: gen_stokes_q1(1024, 1024, 16, aspect=1e4, **{"leaf_columns": 4, **kw}),
 }
 
 

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -m gpu -x -q --durations=5 > gpurun_out/gpu_full.log 2>&1; echo "EXIT $?" >> gpurun_out/gpu_full.log
-tail -15 gpurun_out/gpu_full.log
+LEAF_COLUMNS=1 HS_PROFILE=1 timeout 1500 python tools/run_config.py C4 > gpurun_out/c4.log 2>&1

@@ -6,7 +6,11 @@ from paper_1811_11248_b200 import hsolve as H
 from problems import gen_config
 name = sys.argv[1]
 eps = float(sys.argv[2]) if len(sys.argv) > 2 else None
-t = time.time(); p = gen_config(name); tg = time.time() - t
+import os
+kw = {}
+if os.environ.get("LEAF_COLUMNS"):
+    kw["leaf_columns"] = int(os.environ["LEAF_COLUMNS"])
+t = time.time(); p = gen_config(name, **kw); tg = time.time() - t
 if eps is not None:
     p.eps = eps
 print(f"{name}: N={p.n} nnz={p.nnz} gen {tg:.1f}s", flush=True)
