@@ -250,6 +250,14 @@ def run_ours(args, rank, world, local):
         # byte-bound copy kernels: algorithmic bytes are not accounted per phase yet
         roof = {"bound": "hbm", "kernel": names[dom], "achieved": None, "peak": mp.get("hbm_gbs"), "unit": "GB/s",
                 "frac": None, "traffic": None}
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # (tools/profile_round.sh -> profiles/*_traffic.json; one representative launch)
+    tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
+    if tp:
+        tr = json.load(open(os.path.join(ROOT, "profiles", tp[-1])))
+        if tr.get("class") == roof["kernel"]:
+            roof["traffic"] = tr["dram_bytes_per_launch"]
+            roof["traffic_source"] = f"profiles/{tp[-1]}: {tr['note']}"
     S = stats[-1]
     factor_flops = float(np.mean([s["flops"] for s in stats]))
     t_fac = float(np.mean([s["t_factor_s"] for s in stats]))
