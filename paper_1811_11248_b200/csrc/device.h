@@ -74,12 +74,14 @@ struct SchurContrib {
 struct SchurSrc {
   const double* C;           // fine rows of the n-part, ld ldC
   int32_t ldC, K, kn, nb_off, nnb, pad;
+  int32_t* own;              // [kn] neighbour index owning each n-column (k_schur_prep)
+  double** pairs;            // [nnb (nnb+1) / 2] target block of neighbour pair (a >= b), or null
 };
 struct SchurTile2 {
   int32_t src, i0, j0, pad;
 };
 struct NbCol {               // neighbour q occupies columns [col, col+len) of the n-part
-  int32_t q, col, len, pad;
+  int32_t q, col, len, idx;  // idx: position of q in the full n(s) list (pair table index)
 };
 struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
   double* blk;
@@ -176,6 +178,12 @@ void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int m
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st);
+// per-source column owners (nb index per n-column), once per batch before the waves
+void launch_schur_prep(const SchurSrc* d_src, int nsrc, int max_kn, const NbCol* d_nb, cudaStream_t st);
+// per level: target block of every neighbour pair (a >= b) of every cluster's n(s) list
+// (hptr/hq: n(s) as CSR; poff: offsets of each cluster's triangular table in pairs)
+void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* poff, int nclus, int64_t nrows,
+                        const int64_t* row_cl, double** pairs, const BlockDir& dir, cudaStream_t st);
 // Dense blocked Cholesky of the top matrix (row-major, ld).  On return the
 // diagonal NB x NB blocks hold G_kk (lower) and the block rows right of them hold
 // U_kj = G_kk^{-1} A_kj (i.e. L^T); the strictly lower off-diagonal blocks are stale.

@@ -276,6 +276,44 @@ struct Slab {
   }
 };
 
+// n(s) neighbour-pair -> target block pointer tables of one level, built on the device once
+// per level (the Schur tiles index them instead of searching the directory per tile).
+struct LevelPairs {
+  DevCache* dc = nullptr;
+  double** pairs = nullptr;
+  char* meta = nullptr;
+  std::vector<int64_t> poff;
+  template <class BS>
+  void build(const Level& lev, const BS& bs, DevCache& cache, Upload& up, cudaStream_t st) {
+    dc = &cache;
+    const int n = lev.nclus;
+    std::vector<int64_t> hptr(n + 1, 0), row_cl;
+    std::vector<int32_t> hq;
+    poff.assign(n + 1, 0);
+    for (int s = 0; s < n; ++s) {
+      const int64_t nn = (int64_t)lev.H[s].size();
+      hptr[s + 1] = hptr[s] + nn;
+      poff[s + 1] = poff[s] + nn * (nn + 1) / 2;
+      hq.insert(hq.end(), lev.H[s].begin(), lev.H[s].end());
+      for (int64_t a = 0; a < nn; ++a) row_cl.push_back(s);
+    }
+    if (poff[n] == 0) return;
+    pairs = (double**)dc->alloc(sizeof(double*) * poff[n]);
+    up.reset();
+    const size_t iP = up.add(hptr), iQ = up.add(hq), iO = up.add(poff), iR = up.add(row_cl);
+    up.stage.ensure(up.total);
+    up.dev.ensure(up.total);
+    up.copy_in(iP, hptr); up.copy_in(iQ, hq); up.copy_in(iO, poff); up.copy_in(iR, row_cl);
+    up.send(st);
+    launch_level_pairs(up.dptr<int64_t>(iP), up.dptr<int32_t>(iQ), up.dptr<int64_t>(iO), n, (int64_t)row_cl.size(),
+                       up.dptr<int64_t>(iR), pairs, bs.dir(), st);
+    HS_CUDA(cudaStreamSynchronize(st));   // the staging buffers are reused by the first batch
+  }
+  ~LevelPairs() {
+    if (pairs) dc->free(pairs);
+  }
+};
+
 void check_status(DevStatus* d_status, DevStatus* h_status, cudaStream_t st) {
   HS_CUDA(cudaMemcpyAsync(h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   HS_CUDA(cudaStreamSynchronize(st));
@@ -484,6 +522,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       L.piv[s] = L.iarena + oP[s];
       L.T[s] = L.arena + oX[s];
     }
+    // neighbour-pair target tables of the level (pattern-only; k_level_pairs)
+    LevelPairs lp;
+    lp.build(lev, bs, dc, upA, st);
     std::vector<int32_t> live = cap;
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
     // apply plan of the level: forward event counts, processed flags, backward tasks per batch
@@ -592,6 +633,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       const double tp1 = now_s();
       // ---- Schur update, write-back, apply plan ----------------------------------------------
       std::vector<SchurSrc> srcs;
+      std::vector<int32_t> src_cl;
       std::vector<NbCol> nbc;
       std::vector<std::vector<SchurTile2>> waves;
       std::vector<int32_t> touched;
@@ -641,13 +683,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           SchurSrc sc{C, ldB, K, kn, (int32_t)nbc.size(), 0, 0};
           for (size_t a = 0; a < ns.size(); ++a)
             if (live[ns[a]] > 0) {
-              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], 0});
+              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], (int32_t)a});
               if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
               wave_mask[ns[a]] |= bit;
             }
           sc.nnb = (int32_t)nbc.size() - sc.nb_off;
           const int32_t si = (int32_t)srcs.size();
           srcs.push_back(sc);
+          src_cl.push_back(s);
           if ((int)waves.size() <= w) waves.resize(w + 1);
           const int T = (kn + 63) / 64;
           for (int ti = 0; ti < T; ++ti)
@@ -715,6 +758,22 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
+      // scratch of k_schur_prep (column owners); the pair tables are the level's
+      int64_t prep_words = 0;
+      int max_kn_src = 0;
+      for (const auto& sc : srcs) {
+        prep_words += ((int64_t)sc.kn + 1) / 2;
+        max_kn_src = std::max(max_kn_src, sc.kn);
+      }
+      char* prep = prep_words ? (char*)dc.alloc(8 * prep_words) : nullptr;
+      {
+        char* cur = prep;
+        for (size_t k = 0; k < srcs.size(); ++k) {
+          srcs[k].own = (int32_t*)cur;
+          cur += 8 * (((int64_t)srcs[k].kn + 1) / 2);
+          srcs[k].pairs = lp.pairs + lp.poff[src_cl[k]];
+        }
+      }
       std::vector<SchurTile2> tiles;
       std::vector<int32_t> wave_off(1, 0);
       for (const auto& wv : waves) {
@@ -737,6 +796,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       t_plan += now_s() - tp1;
       upB.send(st);
       HS_CUDA(cudaEventRecord(pt.b[0], st));
+      launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
+      if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)
       for (size_t w = 0; w + 1 < wave_off.size(); ++w)
         launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w], upB.dptr<SchurSrc>(jS),
                       upB.dptr<NbCol>(jN), bs.dir(), st);

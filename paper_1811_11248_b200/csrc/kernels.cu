@@ -799,14 +799,14 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
   const int tid = threadIdx.x;
   if (tid < 64) {
     if (tid < rows) {
-      const int a = nb_owner(nb, s.nnb, t.i0 + tid);
+      const int a = s.own[t.i0 + tid];
       r_own[tid] = a;
       r_loc[tid] = t.i0 + tid - nb[a].col;
     }
   } else if (tid < 128) {
     const int u = tid - 64;
     if (u < cols) {
-      const int b = nb_owner(nb, s.nnb, t.j0 + u);
+      const int b = s.own[t.j0 + u];
       c_own[u] = b;
       c_loc[u] = t.j0 + u - nb[b].col;
     }
@@ -838,13 +838,8 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
   if (table) {
     for (int e = tid; e < nr * nc; e += blockDim.x) {
       const int ra = e / nc, cb = e % nc;
-      const int qa = nb[r_list[ra]].q, qb = nb[c_list[cb]].q;
-      double* p = nullptr;
-      if (qa >= qb) {
-        const int64_t o = dir_find(dir, qa, qb);
-        if (o >= 0) p = dir.blk + o;
-      }
-      ptab[ra][cb] = p;
+      const int a = nb[r_list[ra]].idx, b = nb[c_list[cb]].idx;
+      ptab[ra][cb] = a >= b ? s.pairs[(int64_t)a * (a + 1) / 2 + b] : nullptr;
     }
     for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
   }
@@ -882,11 +877,14 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
     }
     __syncthreads();
   }
-  // scatter-subtract into the target blocks
+  // scatter-subtract into the target blocks: all 16 target addresses first, then all 16
+  // loads in flight, then the stores (no load waits behind a possibly aliasing store)
+  double* tp[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
+      tp[a][b] = nullptr;
       const int i = ty + 16 * a, j = tx + 16 * b;
       if (i >= rows || j >= cols) continue;
       const int oa = r_own[i], ob = c_own[j];
@@ -899,13 +897,22 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
         p = ptab[r_slot[i]][c_slot[j]];
         ld = ldtab[c_slot[j]];
       } else {
-        const int qa = nb[oa].q, qb = nb[ob].q;
-        const int64_t o = dir_find(dir, qa, qb);
-        p = o >= 0 ? dir.blk + o : nullptr;
-        ld = dir.cap[qb];
+        const int fa = nb[oa].idx, fb = nb[ob].idx;
+        p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
+        ld = dir.cap[nb[ob].q];
       }
-      if (p) p[(int64_t)li * ld + lj] -= acc[a][b];
+      if (p) tp[a][b] = p + (int64_t)li * ld + lj;
     }
+  double old[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) old[a][b] = tp[a][b] ? *tp[a][b] : 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (tp[a][b]) *tp[a][b] = old[a][b] - acc[a][b];
 }
 
 __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,
@@ -1070,6 +1077,40 @@ int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, do
   }
 }
 
+// Column owners of the batch's sources: grid (source, 256-column chunk).
+__global__ void __launch_bounds__(256) k_schur_prep(const SchurSrc* __restrict__ srcs, const NbCol* __restrict__ nbc) {
+  const SchurSrc s = srcs[blockIdx.y];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < s.kn) s.own[c] = nb_owner(nbc + s.nb_off, s.nnb, c);
+}
+void launch_schur_prep(const SchurSrc* d_src, int nsrc, int max_kn, const NbCol* d_nb, cudaStream_t st) {
+  if (nsrc <= 0 || max_kn <= 0) return;
+  k_schur_prep<<<dim3((max_kn + 255) / 256, nsrc), 256, 0, st>>>(d_src, d_nb);
+  count_launch(1);
+}
+// Level pair tables: a warp per (cluster s, neighbour a); lanes over b <= a look the block
+// (q_a, q_b) up in the level's directory.  Pattern-only, once per level.
+__global__ void __launch_bounds__(256) k_level_pairs(const int64_t* __restrict__ hptr, const int32_t* __restrict__ hq,
+                                                     const int64_t* __restrict__ poff, const int64_t* __restrict__ row_cl,
+                                                     int64_t nrows, double** __restrict__ pairs, BlockDir dir) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;
+  const int64_t s = row_cl[w];
+  const int a = (int)(w - hptr[s]);
+  const int32_t* q = hq + hptr[s];
+  double** out = pairs + poff[s] + (int64_t)a * (a + 1) / 2;
+  for (int b = lane; b <= a; b += 32) {
+    const int64_t o = dir_find(dir, q[a], q[b]);
+    out[b] = o >= 0 ? dir.blk + o : nullptr;
+  }
+}
+void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* poff, int nclus, int64_t nrows,
+                        const int64_t* row_cl, double** pairs, const BlockDir& dir, cudaStream_t st) {
+  if (nrows <= 0) return;
+  k_level_pairs<<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(hptr, hq, poff, row_cl, nrows, pairs, dir);
+  count_launch(1);
+}
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st) {
   if (n <= 0) return;
