@@ -110,6 +110,17 @@ enum {
   HS_EXP_HTOP_IDX = 13
 };
 
+/* keys for hs_dist_plan_export (multi-GPU decomposition plan) */
+enum {
+  HS_DEXP_OWNER = 0,     /* level l (0..L_top): int64[nclus] owning rank of each cluster       */
+  HS_DEXP_RECV_PTR = 1,  /* level l < L_top: int64[nclus+1] offsets into RECV                  */
+  HS_DEXP_RECV = 2,      /* ranks (other than the owner) receiving cluster s's elimination     */
+                         /* record (r, C_s, coarse rows) -- phase-II clusters only             */
+  HS_DEXP_HELD_PTR = 3,  /* level l < L_top: int64[nclus+1] offsets into HELD                  */
+  HS_DEXP_HELD = 4       /* for each p: the q <= p of the level's final fill graph whose block */
+                         /* (p, q) rank `rank` stores (it owns p or q)                        */
+};
+
 /* keys for hs_factor_export */
 enum {
   HS_FEXP_RANKS = 0,     /* level l: int64[nclus] kept rank r_s                          */
@@ -166,6 +177,11 @@ hs_status hs_analysis_get_info(hs_analysis a, hs_analysis_info* info);
 hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t* out,
                              int64_t cap, int64_t* len);
 void      hs_analysis_destroy(hs_analysis a);
+/* The decomposition plan of rank `rank` of `world` GPUs (host, integer; no device needed).
+ * world must divide the number of fixed subdomains (8 by default).  Same length-query
+ * convention as hs_analysis_export.  HS_E_INVALID_ARG on a bad key/level/world/rank. */
+hs_status hs_dist_plan_export(hs_analysis a, int32_t world, int32_t rank, int32_t key, int32_t level,
+                              int64_t* out, int64_t cap, int64_t* len);
 
 /* ---- factor (device) -------------------------------------------------------------- */
 /* values: CSR values on the pattern given to hs_analyze (host pointer, or device pointer

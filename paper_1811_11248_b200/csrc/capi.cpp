@@ -206,6 +206,53 @@ hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t*
   });
 }
 
+hs_status hs_dist_plan_export(hs_analysis a, int32_t world, int32_t rank, int32_t key, int32_t level, int64_t* out,
+                              int64_t cap, int64_t* len) {
+  return guarded(nullptr, [&] {
+    if (!a || !a->an) hs::fail(HS_E_INVALID_ARG, "hs_dist_plan_export: NULL analysis");
+    const hs::Analysis& an = *a->an;
+    const hs::DistPlan P = hs::make_plan(an, world, rank);
+    if (level < 0 || level > an.L_top || (key != HS_DEXP_OWNER && level >= an.L_top))
+      hs::fail(HS_E_INVALID_ARG, "hs_dist_plan_export: bad level");
+    std::vector<int64_t> v;
+    switch (key) {
+      case HS_DEXP_OWNER: v.assign(P.owner[level].begin(), P.owner[level].end()); break;
+      case HS_DEXP_RECV_PTR:
+      case HS_DEXP_RECV: {
+        const hs::Level& lev = an.levels[level];
+        std::vector<int64_t> ptr(1, 0), idx;
+        std::vector<uint8_t> phase2(lev.nclus, 0);
+        for (size_t b = lev.nphase1; b < lev.batches.size(); ++b)
+          for (int32_t s : lev.batches[b]) phase2[s] = 1;
+        for (int s = 0; s < lev.nclus; ++s) {
+          if (phase2[s])
+            for (int32_t h : hs::receivers(an, P, level, s)) idx.push_back(h);
+          ptr.push_back((int64_t)idx.size());
+        }
+        v = key == HS_DEXP_RECV_PTR ? ptr : idx;
+        break;
+      }
+      case HS_DEXP_HELD_PTR:
+      case HS_DEXP_HELD: {
+        const hs::Level& lev = an.levels[level];
+        std::vector<int64_t> ptr(1, 0), idx;
+        for (int p = 0; p < lev.nclus; ++p) {
+          for (int32_t q : lev.Ffinal[p])
+            if (q < p && P.holds(level, p, q)) idx.push_back(q);
+          if (P.holds(level, p, p)) idx.push_back(p);
+          ptr.push_back((int64_t)idx.size());
+        }
+        v = key == HS_DEXP_HELD_PTR ? ptr : idx;
+        break;
+      }
+      default: hs::fail(HS_E_INVALID_ARG, "hs_dist_plan_export: bad key");
+    }
+    if (len) *len = (int64_t)v.size();
+    if (out)
+      for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); ++i) out[i] = v[i];
+  });
+}
+
 void hs_analysis_destroy(hs_analysis a) {
   if (!a) return;
   if (a->an && a->an->dev >= 0) {

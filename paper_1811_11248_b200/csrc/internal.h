@@ -53,6 +53,17 @@ struct Analysis {
   int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
 };
 
+// Multi-GPU decomposition plan (dist.cpp).
+struct DistPlan {
+  int world = 1, rank = 0;
+  std::vector<std::vector<int32_t>> owner;   // [level 0..L_top][cluster] -> owning rank
+  bool own(int l, int c) const { return owner[l][c] == rank; }
+  bool holds(int l, int p, int q) const { return owner[l][p] == rank || owner[l][q] == rank; }
+};
+DistPlan make_plan(const Analysis& an, int world, int rank);
+// ranks other than the owner that receive the elimination record of cluster s of level l
+std::vector<int32_t> receivers(const Analysis& an, const DistPlan& P, int l, int s);
+
 Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
                   int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts& opt);
 

@@ -26,12 +26,14 @@ for _i, _s in enumerate(STATUS):
 (HS_EXP_PERM, HS_EXP_LEAF_OFF, HS_EXP_H_PTR, HS_EXP_H_IDX, HS_EXP_W_PTR, HS_EXP_W_IDX, HS_EXP_BATCH_PTR,
  HS_EXP_BATCH_IDX, HS_EXP_INTERIOR, HS_EXP_F_PTR, HS_EXP_F_IDX, HS_EXP_NPHASE1, HS_EXP_HTOP_PTR,
  HS_EXP_HTOP_IDX) = range(14)
+# hs_dist_plan_export keys
+HS_DEXP_OWNER, HS_DEXP_RECV_PTR, HS_DEXP_RECV, HS_DEXP_HELD_PTR, HS_DEXP_HELD = range(5)
 # hs_factor_export keys
 HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(5)
 
 # every symbol include/hsolve.h declares
 SYMBOLS = ["hs_create", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
-           "hs_analysis_get_info", "hs_analysis_export", "hs_analysis_destroy", "hs_factor_create",
+           "hs_analysis_get_info", "hs_analysis_export", "hs_dist_plan_export", "hs_analysis_destroy", "hs_factor_create",
            "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
            "hs_pcg", "hs_spmv", "hs_launch_count"]
 HS_CEXP_SHAPE, HS_CEXP_G, HS_CEXP_V, HS_CEXP_TAU, HS_CEXP_B = range(5)
@@ -113,6 +115,7 @@ def lib():
         L.hs_analyze.argtypes = [vp, i64, vp, vp, vp, i32, vp, C.POINTER(hs_analyze_opts), C.POINTER(vp)]
         L.hs_analysis_get_info.argtypes = [vp, C.POINTER(hs_analysis_info)]
         L.hs_analysis_export.argtypes = [vp, i32, i32, vp, i64, C.POINTER(i64)]
+        L.hs_dist_plan_export.argtypes = [vp, i32, i32, i32, i32, vp, i64, C.POINTER(i64)]
         L.hs_analysis_destroy.argtypes = [vp]
         L.hs_analysis_destroy.restype = None
         L.hs_factor_create.argtypes = [vp, vp, vp, C.POINTER(hs_factor_opts), C.POINTER(vp)]
@@ -216,6 +219,14 @@ def hs_analysis_get_info(a: Analysis) -> dict:
     info = hs_analysis_info()
     _check(lib().hs_analysis_get_info(a.ptr, C.byref(info)))
     return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def hs_dist_plan_export(a: Analysis, world: int, rank: int, key: int, level: int = 0) -> np.ndarray:
+    n = C.c_int64()
+    _check(lib().hs_dist_plan_export(a.ptr, world, rank, key, level, None, 0, C.byref(n)))
+    out = np.empty(n.value, dtype=np.int64)
+    _check(lib().hs_dist_plan_export(a.ptr, world, rank, key, level, out.ctypes.data, n.value, C.byref(n)))
+    return out
 
 
 def hs_analysis_export(a: Analysis, key: int, level: int = 0) -> np.ndarray:

@@ -88,3 +88,67 @@ def test_distributed_oracle_equals_sequential(name, world):
     # the same arithmetic in the same order; BLAS kernels may still round differently on
     # arrays that travelled through pickling (alignment-dependent SIMD paths)
     assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def _plan_worker(rank, world, port, name, path):
+    """Each rank asks the library for ITS plan and checks it against the oracle's
+    decomposition (oracle/dist.py owner rule, the blocks an elimination writes); the
+    ranks then cross-check what they hold over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_11248_b200 import hsolve as H
+        p = CASES[name]()
+        an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+        a = H.hs_analyze(None, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                         leaf_columns=p.leaf_columns)
+        comm = _Gloo(world)
+        held_all = []
+        for l, lev in enumerate(an.levels):
+            own = H.hs_dist_plan_export(a, world, rank, H.HS_DEXP_OWNER, l)
+            assert own.tolist() == [owner(an, l, c, world) for c in range(lev.nclus)]
+            rp = H.hs_dist_plan_export(a, world, rank, H.HS_DEXP_RECV_PTR, l)
+            rv = H.hs_dist_plan_export(a, world, rank, H.HS_DEXP_RECV, l)
+            hp = H.hs_dist_plan_export(a, world, rank, H.HS_DEXP_HELD_PTR, l)
+            hv = H.hs_dist_plan_export(a, world, rank, H.HS_DEXP_HELD, l)
+            held = {(pp, int(q)) for pp in range(lev.nclus) for q in hv[hp[pp]:hp[pp + 1]]}
+            # held = the final-fill blocks with an owned endpoint (+ owned diagonals)
+            ref = {(pp, q) for pp in range(lev.nclus) for q in list(lev.Ffinal[pp]) + [pp]
+                   if q <= pp and (own[pp] == rank or own[q] == rank)}
+            assert held == ref
+            phase2 = {s for B in lev.batches[lev.nphase1:] for s in B}
+            for s in range(lev.nclus):
+                recv = set(rv[rp[s]:rp[s + 1]].tolist())
+                if s not in phase2:
+                    assert not recv
+                    continue
+                nw = list(lev.nlist[s]) + list(lev.wlist[s])
+                written = {(max(x, y), min(x, y)) for x in lev.nlist[s] for y in lev.nlist[s]}
+                written |= {(max(s, q), min(s, q)) for q in nw} | {(s, s)}
+                holders = {h for h in range(world) for (x, y) in written
+                           if owner(an, l, x, world) == h or owner(an, l, y, world) == h}
+                # exactly the ranks (other than the owner) holding a block the elimination writes
+                assert recv == holders - {owner(an, l, s, world)}, (l, s)
+            held_all.append(sorted(held))
+        gathered = comm.all_gather(held_all)
+        if rank == 0:
+            for l, lev in enumerate(an.levels):
+                union = set()
+                for g in range(world):
+                    union |= set(map(tuple, gathered[g][l]))
+                allb = {(pp, q) for pp in range(lev.nclus) for q in list(lev.Ffinal[pp]) + [pp] if q <= pp}
+                assert union == allb, l
+            np.save(path, np.array([1]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["C1", "q1-12"])
+def test_library_plan_matches_decomposition(name, world):
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ok.npy")
+        mp.spawn(_plan_worker, args=(world, _free_port(), name, path), nprocs=world, join=True)
+        assert os.path.exists(path)
