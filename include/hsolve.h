@@ -158,6 +158,10 @@ typedef struct {
 /* device: CUDA ordinal.  world_size/rank/nccl_unique_id: multi-GPU (world_size 1 and
  * NULL id for one GPU).  Fails with HS_E_NO_DEVICE when CUDA is unavailable. */
 hs_status hs_create(hs_handle* h, int device, int world_size, int rank, const void* nccl_unique_id);
+/* Rank 0 of a multi-GPU job creates the 128-byte NCCL id, broadcasts it over the job's own
+ * process group (e.g. torch.distributed) and every rank passes it to hs_create.  NCCL is
+ * loaded on first use (dlopen of libnccl.so.2, HS_NCCL_LIB overrides); HS_E_NCCL if absent. */
+hs_status hs_nccl_unique_id(void* out128);
 /* stream: a cudaStream_t on the handle's device (e.g. torch.cuda.current_stream()),
  * or NULL for the library's own stream.  All device work of the handle runs on it. */
 hs_status hs_set_stream(hs_handle h, void* stream);

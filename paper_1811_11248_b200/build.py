@@ -61,7 +61,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             sys.stderr.write(out)
     if failed:
         raise RuntimeError("libhsolve build failed")
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("libhsolve link failed:\n" + r.stdout)

@@ -92,8 +92,8 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
   return guarded(nullptr, [&] {
     if (!out) hs::fail(HS_E_INVALID_ARG, "hs_create: NULL out");
     *out = nullptr;
-    if (world_size != 1 || rank != 0 || nccl_unique_id)
-      hs::fail(HS_E_UNSUPPORTED, "hs_create: multi-GPU factor is not implemented yet (replicas only)");
+    if (world_size < 1 || rank < 0 || rank >= world_size) hs::fail(HS_E_INVALID_ARG, "hs_create: bad world/rank");
+    if (world_size > 1 && !nccl_unique_id) hs::fail(HS_E_INVALID_ARG, "hs_create: world_size > 1 needs an NCCL id");
     int nd = 0;
     if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
       cudaGetLastError();
@@ -110,7 +110,26 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
     HS_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     h->upA.dev.dc = &h->cache;
     h->upB.dev.dc = &h->cache;
+    h->world = world_size;
+    h->rank = rank;
+    if (world_size > 1) {
+      try {
+        h->comm = hs::comm_init(world_size, rank, nccl_unique_id);
+      } catch (...) {
+        cudaStreamDestroy(h->stream);
+        cudaStreamDestroy(h->side);
+        delete h;
+        throw;
+      }
+    }
     *out = h;
+  });
+}
+
+hs_status hs_nccl_unique_id(void* out128) {
+  return guarded(nullptr, [&] {
+    if (!out128) hs::fail(HS_E_INVALID_ARG, "hs_nccl_unique_id: NULL out");
+    hs::nccl_unique_id(out128);
   });
 }
 
@@ -148,6 +167,7 @@ void hs_destroy(hs_handle h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   h->cache.trim();
+  if (h->comm) hs::comm_destroy(h->comm);
   delete h;
 }
 
@@ -365,6 +385,8 @@ static void io_in(hs_factor f, const double* v, double* dtmp, int32_t on_device,
 hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device) {
   return guarded(f ? f->h : nullptr, [&] {
     if (!f || !b || !x) hs::fail(HS_E_INVALID_ARG, "hs_apply: NULL argument");
+    if (f->h->world > 1 && f->h->rank != 0)
+      hs::fail(HS_E_UNSUPPORTED, "hs_apply: the multi-GPU factor is applied on rank 0 (records gathered there)");
     require_device(f->h);
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
@@ -404,6 +426,8 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
   const hs_status s = guarded(f ? f->h : nullptr, [&] {
     if (!f || !b || !x || !rep) hs::fail(HS_E_INVALID_ARG, "hs_pcg: NULL argument");
     if (!(tol >= 0) || maxit < 0) hs::fail(HS_E_INVALID_ARG, "hs_pcg: bad tol/maxit");
+    if (f->h->world > 1 && f->h->rank != 0)
+      hs::fail(HS_E_UNSUPPORTED, "hs_pcg: the multi-GPU factor is solved on rank 0 (records gathered there)");
     require_device(f->h);
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;

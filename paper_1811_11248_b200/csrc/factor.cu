@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <unordered_map>
 
@@ -96,25 +97,29 @@ struct BlockStore {
   cudaStream_t st = nullptr;
   DevCache* dc = nullptr;
 
-  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache) {
+  // dp/level (multi-GPU): keep only the blocks this rank holds (it owns p or q)
+  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache,
+             const DistPlan* dp = nullptr, int level = 0) {
     st = stream;
     dc = cache;
-    layout(caps, edges);
+    layout(caps, edges, dp, level);
     if (total) d = (double*)dc->alloc(total * sizeof(double));
   }
-  void layout(const std::vector<int32_t>& caps, const Adj& edges) {
+  void layout(const std::vector<int32_t>& caps, const Adj& edges, const DistPlan* dp = nullptr, int level = 0) {
     cap = caps;
     const int n = (int)caps.size();
     rows.assign(n, {});
     int64_t off = 0;
     for (int p = 0; p < n; ++p) {
       for (int32_t q : edges[p])
-        if (q < p) {
+        if (q < p && (!dp || dp->holds(level, p, q))) {
           rows[p].push_back({q, off});
           off += (int64_t)caps[p] * caps[q];
         }
-      rows[p].push_back({p, off});
-      off += (int64_t)caps[p] * caps[p];
+      if (!dp || dp->own(level, p)) {
+        rows[p].push_back({p, off});
+        off += (int64_t)caps[p] * caps[p];
+      }
     }
     total = (size_t)off;
   }
@@ -355,15 +360,22 @@ namespace hs {
 // Pattern-only device data, computed once per analysis and cached in it: the CSR pattern,
 // the permutation, the map of every CSR entry into the level-0 block store and the
 // transpose map used by the on-device symmetry check.
-static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st) {
-  if (an->dev == device && an->d_map) return;
+static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, const DistPlan& dp) {
+  if (an->dev == device && an->d_map && an->map_world == dp.world && an->map_rank == dp.rank) return;
   if (an->dev >= 0 && an->dev != device) fail(HS_E_INVALID_ARG, "factor: analysis already bound to another device");
+  if (an->d_map) {   // cached for another (world, rank): rebuild
+    HS_CUDA(cudaStreamSynchronize(st));
+    for (void* p : {(void*)an->d_rowptr, (void*)an->d_colind, (void*)an->d_perm, (void*)an->d_map, (void*)an->d_tmap})
+      if (p) cudaFree(p);
+    an->d_rowptr = nullptr; an->d_colind = nullptr; an->d_perm = nullptr; an->d_map = nullptr; an->d_tmap = nullptr;
+  }
+  const bool dist = dp.world > 1;
   const int64_t n = an->n, nnz = an->rowptr[n];
   const int nleaf0 = (int)(an->leaf_off.size() - 1);
   std::vector<int32_t> cap(nleaf0);
   for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
   BlockStore layout;
-  layout.layout(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top);
+  layout.layout(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, dist && an->L_top > 0 ? &dp : nullptr, 0);
   std::vector<int32_t> leaf_of(n);
   for (int c = 0; c < nleaf0; ++c)
     for (int64_t k = an->leaf_off[c]; k < an->leaf_off[c + 1]; ++k) leaf_of[k] = c;
@@ -380,7 +392,10 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st) {
       const int32_t q = leaf_of[pj];
       if (p < q) continue;
       const int64_t o = layout.off(p, q);
-      if (o < 0) fail(HS_E_INTERNAL, "factor: level-0 block missing");
+      if (o < 0) {
+        if (dist) continue;   // a block this rank does not hold
+        fail(HS_E_INTERNAL, "factor: level-0 block missing");
+      }
       map[k] = o + (pi - an->leaf_off[p]) * cap[q] + (pj - an->leaf_off[q]);
     }
   }
@@ -396,6 +411,8 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st) {
   HS_CUDA(cudaMemcpyAsync(an->d_tmap, tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
   HS_CUDA(cudaStreamSynchronize(st));
   an->dev = device;
+  an->map_world = dp.world;
+  an->map_rank = dp.rank;
 }
 
 hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* values, const hs_factor_opts& opt) {
@@ -404,7 +421,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   Analysis* an = const_cast<Analysis*>(an_c);   // the device pattern cache lives in the analysis
   const int64_t n = an->n, nnz = an->rowptr[n];
   cudaStream_t st = h->stream;
-  ensure_device_pattern(an, h->device, st);
+  const DistPlan DP = make_plan(*an, h->world, h->rank);
+  ensure_device_pattern(an, h->device, st, DP);
   auto* f = new hs_factor_s();
   std::unique_ptr<hs_factor_s> guard(f);
   f->h = h;
@@ -444,7 +462,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   std::vector<int32_t> cap(nleaf0);
   for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
   BlockStore bs;
-  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc);
+  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc,
+           h->world > 1 && an->L_top > 0 ? &DP : nullptr, 0);
   if (bs.total) HS_CUDA(cudaMemsetAsync(bs.d, 0, bs.total * sizeof(double), st));
   launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
   if (an->L_top > 0) bs.upload_dir();
@@ -476,6 +495,41 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   // A/B switches for the previous CPQR kernels (single CTA / cluster with per-thread columns)
   const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;
   const bool cpqr_v2 = std::getenv("HS_CPQR_V2") != nullptr;
+  // ---- multi-GPU (dist.cpp; protocol of oracle/dist.py) ---------------------
+  // Rank g eliminates the clusters of its subdomains and stores only the blocks it holds
+  // (it owns an endpoint).  Phase-I batches are local; before phase II and at the level end
+  // the kept ranks are all-reduced; after each phase-II batch the owner of s sends B_s (rows
+  // [0, r) = coarse rows, the fine n-rows = C_s) to the owners of n(s) u w(s), which apply
+  // the Schur update and the write-back to the blocks they hold.  The factor records (T_s,
+  // C_s) and the top blocks are gathered to rank 0, which builds the apply (v1: the apply and
+  // PCG run on rank 0).
+  const bool dist = h->world > 1;
+  const bool plan_apply = !dist || h->rank == 0;
+  auto own = [&](int lv, int c) { return !dist || DP.own(lv, c); };
+  int32_t* d_ired = nullptr;   // int32 all-reduce scratch
+  int32_t* h_ired = nullptr;
+  size_t ired_cap = 0;
+  auto allreduce_i32 = [&](std::vector<int32_t>& v) {   // in place, sum over ranks (blocking)
+    if (v.empty()) return;
+    if (v.size() > ired_cap) {
+      if (d_ired) dc.free(d_ired);
+      if (h_ired) cudaFreeHost(h_ired);
+      ired_cap = std::max(v.size(), 2 * ired_cap);
+      d_ired = (int32_t*)dc.alloc(sizeof(int32_t) * ired_cap);
+      HS_CUDA(cudaMallocHost(&h_ired, sizeof(int32_t) * ired_cap));
+    }
+    std::memcpy(h_ired, v.data(), sizeof(int32_t) * v.size());
+    HS_CUDA(cudaMemcpyAsync(d_ired, h_ired, sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice, st));
+    comm_allreduce_sum_i32(h->comm, d_ired, v.size(), st);
+    HS_CUDA(cudaMemcpyAsync(h_ired, d_ired, sizeof(int32_t) * v.size(), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(v.data(), h_ired, sizeof(int32_t) * v.size());
+  };
+  std::unique_ptr<void, std::function<void(void*)>> ired_guard((void*)1, [&](void*) {
+    if (d_ired) dc.free(d_ired);
+    if (h_ired) cudaFreeHost(h_ired);
+  });
+
   for (int l = 0; l < an->L_top; ++l) {
     const Level& lev = an->levels[l];
     LevelRT& L = f->lv[l];
@@ -493,8 +547,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     L.vlen = L.voff[lev.nclus];
     ap.vbase.push_back(vbase);
     vbase += L.vlen;
-    // ---- level arena (persistent): T_s (cap^2) and the pivots; the rest is per batch ----
-    std::vector<int64_t> oX(lev.nclus), oP(lev.nclus);
+    // ---- level arena (persistent): T_s (cap^2) and the pivots of the owned clusters -------
+    std::vector<int64_t> oX(lev.nclus, -1), oP(lev.nclus, 0);
     int64_t off = 0, ioff = 0;
     for (int s = 0; s < lev.nclus; ++s) {
       const int64_t m = cap[s];
@@ -504,6 +558,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                       l, (long long)m, MAX_M);
         fail(HS_E_UNSUPPORTED, buf);
       }
+      if (!own(l, s)) continue;
       oX[s] = off; off += (m * m + 3) & ~int64_t(3);   // T_s (apply operator), 32-byte aligned
       oP[s] = ioff; ioff += m;
     }
@@ -514,59 +569,73 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     t_tr[2] += now_s() - ta0;
     L.G.assign(lev.nclus, nullptr); L.V.assign(lev.nclus, nullptr); L.tau.assign(lev.nclus, nullptr);
     L.B.assign(lev.nclus, nullptr); L.nu.assign(lev.nclus, nullptr); L.C.assign(lev.nclus, nullptr);
-    L.piv.resize(lev.nclus); L.T.resize(lev.nclus);
+    L.piv.assign(lev.nclus, nullptr); L.T.assign(lev.nclus, nullptr);
     Slab cslab;
     cslab.dc = &dc;
     cslab.owned = &L.cchunks;
-    for (int s = 0; s < lev.nclus; ++s) {
-      L.piv[s] = L.iarena + oP[s];
-      L.T[s] = L.arena + oX[s];
-    }
+    for (int s = 0; s < lev.nclus; ++s)
+      if (oX[s] >= 0) {
+        L.piv[s] = L.iarena + oP[s];
+        L.T[s] = L.arena + oX[s];
+      }
     // neighbour-pair target tables of the level (pattern-only; k_level_pairs)
     LevelPairs lp;
     lp.build(lev, bs, dc, upA, st);
     std::vector<int32_t> live = cap;
+    std::vector<uint8_t> done(lev.nclus, 0);   // eliminated (rank known here)
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
-    // apply plan of the level: forward event counts, processed flags, backward tasks per batch
-    ApplyLevelPlan& AP = ap.lv[l];
-    AP.src.assign(lev.nclus, ApplySrc{});
-    std::vector<int32_t> fev(lev.nclus, 0);
-    std::vector<uint8_t> proc(lev.nclus, 0);
-    std::vector<std::vector<BwdTask>> bwd_batches;
-    std::vector<int64_t> foff(lev.nclus, 0);
+    // all-reduce of the kept ranks of the eliminated clusters (dist): owners contribute
+    auto sync_ranks = [&](const std::vector<uint8_t>& elim) {
+      std::vector<int32_t> v(lev.nclus, 0);
+      for (int s = 0; s < lev.nclus; ++s)
+        if (own(l, s) && elim[s]) v[s] = L.rank[s];
+      allreduce_i32(v);
+      for (int s = 0; s < lev.nclus; ++s)
+        if (elim[s] && !own(l, s)) {
+          L.rank[s] = v[s];
+          live[s] = v[s];
+          done[s] = 1;
+        }
+    };
+    std::vector<uint8_t> elim_so_far(lev.nclus, 0);
 
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
-    for (const auto& Bt : lev.batches) {
+    for (size_t bidx = 0; bidx < lev.batches.size(); ++bidx) {
+      const auto& Bt = lev.batches[bidx];
       if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
+      const bool phase2 = (int)bidx >= lev.nphase1;
+      if (dist && phase2 && (int)bidx == lev.nphase1) sync_ranks(elim_so_far);   // phase-I ranks
       const double tp0 = now_s();
-      const int nb = (int)Bt.size();
+      // shapes of every cluster of the batch from the current live sizes
+      for (int32_t s : Bt) {
+        int32_t kn = 0, kw = 0;
+        for (int32_t q : lev.H[s]) kn += live[q];
+        for (int32_t q : lev.w[s]) kw += live[q];
+        L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw;
+      }
+      std::vector<int32_t> Bo;   // the batch's clusters eliminated here
+      for (int32_t s : Bt)
+        if (own(l, s)) Bo.push_back(s);
+      const int nb = (int)Bo.size();
       std::vector<CopyItem> gather;
       std::vector<CluItem> clu(nb);
       std::vector<TrsmItem> trsm, rot;
       int max_m = 1;
-      for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bt[bi]]);
+      for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bo[bi]]);
       // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
       int64_t wsz = 0;
       std::vector<int64_t> wo(nb);
       for (int bi = 0; bi < nb; ++bi) {
-        const int32_t s = Bt[bi];
-        const int64_t m = live[s];
-        int64_t kn = 0, kw = 0;
-        for (int32_t q : lev.H[s]) kn += live[q];
-        for (int32_t q : lev.w[s]) kw += live[q];
+        const int32_t s = Bo[bi];
+        const int64_t m = live[s], kn = L.kn[s], kw = L.kw[s];
         wo[bi] = wsz;
         wsz += 2 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
       }
-      double* ws = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4));
+      double* ws = nb ? (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4)) : nullptr;
       for (int bi = 0; bi < nb; ++bi) {
-        const int32_t s = Bt[bi];
-        const int32_t m = live[s];
-        int32_t kn = 0, kw = 0;
-        for (int32_t q : lev.H[s]) kn += live[q];
-        for (int32_t q : lev.w[s]) kw += live[q];
-        const int32_t ldB = kn + kw;
-        L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = ldB;
+        const int32_t s = Bo[bi];
+        const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
         double* w0 = ws + wo[bi];
         L.G[s] = w0;
         L.V[s] = w0 + (int64_t)m * m;
@@ -576,7 +645,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
         it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
-        max_m = std::max(max_m, m);
         if (m == 0) continue;
         double* p; int32_t ld, tr;
         bs.get(s, s, p, ld, tr);
@@ -600,38 +668,70 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
       }
-      split_copies(gather);
-      upA.reset();
-      std::vector<unsigned long long> nmax(nb, 0ull);
-      const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
-                   iM = upA.add(nmax);
-      upA.stage.ensure(upA.total);
-      upA.dev.ensure(upA.total);
-      for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
-      upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
-      upA.copy_in(iM, nmax);
-      t_plan += now_s() - tp0;
-      upA.send(st);
-      HS_CUDA(cudaEventRecord(pt.a[0], st));
-      launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
-      HS_CUDA(cudaEventRecord(pt.a[1], st));
-      launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
-      HS_CUDA(cudaEventRecord(pt.a[2], st));
-      launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
-      HS_CUDA(cudaEventRecord(pt.a[3], st));
-      if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
-      else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-      else {
-        launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-        launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
+      if (nb > 0) {
+        split_copies(gather);
+        upA.reset();
+        std::vector<unsigned long long> nmax(nb, 0ull);
+        const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
+                     iM = upA.add(nmax);
+        upA.stage.ensure(upA.total);
+        upA.dev.ensure(upA.total);
+        for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
+        upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
+        upA.copy_in(iM, nmax);
+        t_plan += now_s() - tp0;
+        upA.send(st);
+        HS_CUDA(cudaEventRecord(pt.a[0], st));
+        launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
+        HS_CUDA(cudaEventRecord(pt.a[1], st));
+        launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
+        HS_CUDA(cudaEventRecord(pt.a[2], st));
+        launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
+        HS_CUDA(cudaEventRecord(pt.a[3], st));
+        if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
+        else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+        else {
+          launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+          launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
+        }
+        HS_CUDA(cudaEventRecord(pt.a[4], st));
+        HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+        check_status(d_status, &h_status, st);       // synchronises the stream
+        pt.collect(S);
+      } else {
+        t_plan += now_s() - tp0;
       }
-      HS_CUDA(cudaEventRecord(pt.a[4], st));
-      HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
-      check_status(d_status, &h_status, st);       // synchronises the stream
-      pt.collect(S);
       deferred.drain(false);
       const double tp1 = now_s();
-      // ---- Schur update, write-back, apply plan ----------------------------------------------
+      for (int bi = 0; bi < nb; ++bi) {
+        const int32_t s = Bo[bi];
+        L.rank[s] = live[s] == 0 ? 0 : h_rank[bi];
+        elim_so_far[s] = 1;
+      }
+      // ---- phase II across GPUs: the batch's ranks, then the elimination records ---------
+      std::vector<double*> rbuf(Bt.size(), nullptr);   // received B_s of remote clusters
+      if (dist && phase2) {
+        std::vector<int32_t> v(Bt.size(), 0);
+        for (size_t k = 0; k < Bt.size(); ++k)
+          if (own(l, Bt[k])) v[k] = L.rank[Bt[k]];
+        allreduce_i32(v);
+        for (size_t k = 0; k < Bt.size(); ++k) L.rank[Bt[k]] = v[k];
+        comm_group_start();
+        for (size_t k = 0; k < Bt.size(); ++k) {
+          const int32_t s = Bt[k];
+          const size_t words = (size_t)live[s] * L.ldB[s];
+          if (!words) continue;
+          const std::vector<int32_t> rc = receivers(*an, DP, l, s);
+          if (own(l, s)) {
+            for (int32_t hdst : rc) comm_send_f64(h->comm, L.B[s], words, hdst, st);
+          } else if (std::binary_search(rc.begin(), rc.end(), (int32_t)h->rank)) {
+            rbuf[k] = (double*)dc.alloc(sizeof(double) * words);
+            comm_recv_f64(h->comm, rbuf[k], words, DP.owner[l][s], st);
+          }
+        }
+        comm_group_end();
+      }
+      // ---- Schur update, write-back (local and received records) --------------------------
       std::vector<SchurSrc> srcs;
       std::vector<int32_t> src_cl;
       std::vector<NbCol> nbc;
@@ -641,32 +741,35 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<double*> id_ptr;
       std::vector<int32_t> id_ld, id_r;
       double tq_prev = now_s();
-      bwd_batches.emplace_back();
-      std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
       // persistent C_s = rows [r, m) of the n-part, compacted to ld kn (the factor record
       // the apply reads); the Schur update still reads C in place from the batch workspace
       std::vector<FormTItem> ft;
       int ft_max_m = 0;
-      for (int bi = 0; bi < nb; ++bi) {
-        const int32_t s = Bt[bi];
+      for (size_t k = 0; k < Bt.size(); ++k) {
+        const int32_t s = Bt[k];
+        const bool mine = own(l, s);
+        const double* Bs = mine ? L.B[s] : rbuf[k];
+        if (!mine && !Bs) continue;   // a remote cluster whose record this rank does not need
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
-        const int32_t r = m == 0 ? 0 : h_rank[bi];
-        L.rank[s] = r;
-        S.max_m = std::max(S.max_m, m);
-        S.max_rank = std::max(S.max_rank, r);
+        const int32_t r = L.rank[s];
         const int32_t K = m - r;
-        const double* C = L.B[s] + (int64_t)r * ldB + kw;
-        if (m > 0) {
-          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, r});
-          ft_max_m = std::max(ft_max_m, m);
+        const double* C = Bs + (int64_t)r * ldB + kw;
+        if (mine) {
+          S.max_m = std::max(S.max_m, m);
+          S.max_rank = std::max(S.max_rank, r);
+          if (m > 0) {
+            ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, r});
+            ft_max_m = std::max(ft_max_m, m);
+          }
+          if (K > 0 && kn > 0) L.C[s] = cslab.get((int64_t)K * kn);
+          // algorithmic flops of CPQR (+ rotation of the n-columns) and Schur
+          double fq = 0.0;
+          for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
+          S.flops += fq + (double)K * kn * (kn + 1);
+          S.flops_phase[3] += fq;
+          S.flops_phase[4] += (double)K * kn * (kn + 1);
         }
-        if (K > 0 && kn > 0) L.C[s] = cslab.get((int64_t)K * kn);
-        // algorithmic flops of CPQR (+ rotation of the n-columns) and Schur
-        double fq = 0.0;
-        for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
-        S.flops += fq + (double)K * kn * (kn + 1);
-        S.flops_phase[3] += fq;
-        S.flops_phase[4] += (double)K * kn * (kn + 1);
+        if (m == 0) continue;
         // neighbour column offsets inside the n-part
         const auto& ns = lev.H[s];
         std::vector<int32_t> noff(ns.size() + 1, 0);
@@ -698,63 +801,28 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         const double tq0 = now_s();
         t_sub[0] += tq0 - tq_prev;
-        // write-back of row s: [I_r | coarse-w | coarse-n]
+        // write-back of row s: [I_r | coarse-w | coarse-n] into the blocks held here
         if (r > 0) {
           double* p; int32_t ld, tr;
-          bs.get(s, s, p, ld, tr);
-          id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
+          if (mine) {
+            bs.get(s, s, p, ld, tr);
+            id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
+          }
           int32_t col = 0;
           for (int pass = 0; pass < 2; ++pass)
             for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
-              if (live[q] > 0) {
+              if (live[q] > 0 && bs.has(s, q)) {
                 bs.get(s, q, p, ld, tr);
-                if (!tr) wb.push_back(CopyItem{L.B[s] + col, p, ldB, ld, r, live[q], 0, 0});
-                else wb.push_back(CopyItem{L.B[s] + col, p, ldB, ld, live[q], r, 1, 0});
+                if (!tr) wb.push_back(CopyItem{Bs + col, p, ldB, ld, r, live[q], 0, 0});
+                else wb.push_back(CopyItem{Bs + col, p, ldB, ld, live[q], r, 1, 0});
               }
               col += live[q];
             }
         }
-        if (L.C[s]) wb.push_back(CopyItem{C, L.C[s], ldB, kn, K, kn, 0, 0});
+        if (mine && L.C[s]) wb.push_back(CopyItem{C, L.C[s], ldB, kn, K, kn, 0, 0});
         const double tq1 = now_s();
         t_sub[1] += tq1 - tq0;
-        // apply plan (Algorithm 2): the cluster's record, its forward target tasks (targets
-        // grouped up to FWD_COLS columns) and its backward column chunks
-        if (m > 0) {
-          ApplySrc& as = AP.src[s];
-          as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
-          as.pre = fev[s]++;
-          as.nb_begin = (int32_t)AP.bnb.size();
-          const int32_t tb = (int32_t)AP.ftgt.size();
-          for (size_t a = 0; a < ns.size(); ++a) {
-            const int32_t q = ns[a];
-            if (live[q] == 0 || K == 0) continue;
-            AP.ftgt.push_back(FwdTgt{nullptr, q, noff[a], live[q], fev[q]++, proc[q], 0});
-            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], live[q], proc[q] ? 0 : 1});
-          }
-          as.nb_end = (int32_t)AP.bnb.size();
-          const int32_t te = (int32_t)AP.ftgt.size();
-          if (tb == te) AP.ftask.push_back(FwdTask{s, tb, tb, 1});
-          for (int32_t g0 = tb, first = 1; g0 < te; first = 0) {
-            int32_t g1 = g0, cols = 0;
-            while (g1 < te && (g1 == g0 || (cols + AP.ftgt[g1].len <= FWD_COLS && g1 - g0 < 16))) cols += AP.ftgt[g1++].len;
-            AP.ftask.push_back(FwdTask{s, g0, g1, first});
-            g0 = g1;
-          }
-          as.part = AP.parts;
-          if (K > 0 && kn > 0) {
-            as.nchunk = (kn + BWD_COLS - 1) / BWD_COLS;
-            for (int32_t c = 0; c < as.nchunk; ++c)
-              bwd_tasks.push_back(BwdTask{s, c * BWD_COLS, std::min(BWD_COLS, kn - c * BWD_COLS), c});
-            AP.parts += (int64_t)as.nchunk * K;
-          } else {
-            as.nchunk = 1;
-            bwd_tasks.push_back(BwdTask{s, 0, 0, 0});
-          }
-          foff[s] = ap.ftotal;
-          ap.ftotal += K;
-        }
         tq_prev = now_s();
-        t_sub[2] += tq_prev - tq1;
       }
       const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
@@ -780,64 +848,75 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         tiles.insert(tiles.end(), wv.begin(), wv.end());
         wave_off.push_back((int32_t)tiles.size());
       }
-      for (int bi = 0; bi < nb; ++bi) {
-        live[Bt[bi]] = L.rank[Bt[bi]];
-        proc[Bt[bi]] = 1;
-      }
-      t_sub[3] += now_s() - tq3;
-      split_copies(wb);
-      upB.reset();
-      const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
-                   jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft);
-      upB.stage.ensure(upB.total);
-      upB.dev.ensure(upB.total);
-      upB.copy_in(jT, tiles); upB.copy_in(jS, srcs); upB.copy_in(jN, nbc); upB.copy_in(jW, wb);
-      upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
-      t_plan += now_s() - tp1;
-      upB.send(st);
-      HS_CUDA(cudaEventRecord(pt.b[0], st));
-      launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
-      if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)
-      for (size_t w = 0; w + 1 < wave_off.size(); ++w)
-        launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w], upB.dptr<SchurSrc>(jS),
-                      upB.dptr<NbCol>(jN), bs.dir(), st);
-      HS_CUDA(cudaEventRecord(pt.b[1], st));
-      launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
-      launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
-      HS_CUDA(cudaEventRecord(pt.b[2], st));
-      pt.b_pending = true;
-      S.n_batches++;
-      // apply operators T_s = U^T G^{-1} of the batch on the side stream (they are only read
-      // by the apply): reads the workspace's G, V, tau, so the workspace (and the items'
-      // own buffer) go back to the cache once the side stream has passed this point
-      FormTItem* d_ft = nullptr;
-      cudaEvent_t ev_ft = nullptr;
-      if (!ft.empty()) {
-        d_ft = (FormTItem*)dc.alloc(sizeof(FormTItem) * ft.size());
-        // own copy of the items: upB's device buffer is rewritten by the next batch
-        HS_CUDA(cudaMemcpyAsync(d_ft, upB.dptr<FormTItem>(jF), sizeof(FormTItem) * ft.size(),
-                                cudaMemcpyDeviceToDevice, st));
-        HS_CUDA(cudaEventRecord(h->ev_fork, st));
-        HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        launch_form_T(d_ft, (int)ft.size(), ft_max_m, h->side);
-        ev_ft = deferred.take();
-        HS_CUDA(cudaEventRecord(ev_ft, h->side));
-      }
-      if (f->keep_records) {
-        L.wchunks.push_back(ws);
-        if (d_ft) deferred.push(ev_ft, {d_ft});
-      } else {
-        if (ev_ft) deferred.push(ev_ft, {ws, d_ft});
-        else dc.free(ws);
-        for (int bi = 0; bi < nb; ++bi) {
-          const int32_t s = Bt[bi];
-          L.G[s] = L.V[s] = L.tau[s] = L.nu[s] = L.B[s] = nullptr;
+      for (int32_t s : Bt)
+        if (own(l, s) || (dist && phase2)) {   // the rank of s is known here
+          live[s] = L.rank[s];
+          done[s] = 1;
         }
+      t_sub[3] += now_s() - tq3;
+      const bool second = !srcs.empty() || !wb.empty() || !id_ptr.empty() || !ft.empty();
+      if (second) {
+        split_copies(wb);
+        upB.reset();
+        const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
+                     jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft);
+        upB.stage.ensure(upB.total);
+        upB.dev.ensure(upB.total);
+        upB.copy_in(jT, tiles); upB.copy_in(jS, srcs); upB.copy_in(jN, nbc); upB.copy_in(jW, wb);
+        upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
+        t_plan += now_s() - tp1;
+        upB.send(st);
+        HS_CUDA(cudaEventRecord(pt.b[0], st));
+        launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
+        for (size_t w = 0; w + 1 < wave_off.size(); ++w)
+          launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
+                        upB.dptr<SchurSrc>(jS), upB.dptr<NbCol>(jN), bs.dir(), st);
+        HS_CUDA(cudaEventRecord(pt.b[1], st));
+        launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
+        launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
+        HS_CUDA(cudaEventRecord(pt.b[2], st));
+        pt.b_pending = true;
+        // apply operators T_s = U^T G^{-1} of the batch on the side stream (they are only
+        // read by the apply): reads the workspace's G, V, tau, so the workspace (and the
+        // items' own buffer) go back to the cache once the side stream has passed this point
+        FormTItem* d_ft = nullptr;
+        cudaEvent_t ev_ft = nullptr;
+        if (!ft.empty()) {
+          d_ft = (FormTItem*)dc.alloc(sizeof(FormTItem) * ft.size());
+          // own copy of the items: upB's device buffer is rewritten by the next batch
+          HS_CUDA(cudaMemcpyAsync(d_ft, upB.dptr<FormTItem>(jF), sizeof(FormTItem) * ft.size(),
+                                  cudaMemcpyDeviceToDevice, st));
+          HS_CUDA(cudaEventRecord(h->ev_fork, st));
+          HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+          launch_form_T(d_ft, (int)ft.size(), ft_max_m, h->side);
+          ev_ft = deferred.take();
+          HS_CUDA(cudaEventRecord(ev_ft, h->side));
+        }
+        if (f->keep_records) {
+          if (ws) L.wchunks.push_back(ws);
+          if (d_ft) deferred.push(ev_ft, {d_ft});
+          ws = nullptr;
+        } else if (ev_ft) {
+          deferred.push(ev_ft, {ws, d_ft});
+          ws = nullptr;
+        }
+      } else {
+        t_plan += now_s() - tp1;
       }
+      if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)
+      for (double* b : rbuf)
+        if (b) dc.free(b);
+      if (ws) {
+        if (f->keep_records) L.wchunks.push_back(ws);
+        else dc.free(ws);
+      }
+      if (!f->keep_records)
+        for (int32_t s : Bo) L.G[s] = L.V[s] = L.tau[s] = L.nu[s] = L.B[s] = nullptr;
+      S.n_batches++;
       if (const char* dd = std::getenv("HS_DEBUG_DUMP")) {   // debug aid: block store after every batch
         HS_CUDA(cudaStreamSynchronize(st));
         char path[512];
-        std::snprintf(path, sizeof path, "%s/l%d_b%d.bin", dd, l, (int)bwd_batches.size() - 1);
+        std::snprintf(path, sizeof path, "%s/l%d_b%d.bin", dd, l, (int)bidx);
         FILE* fp = std::fopen(path, "wb");
         if (fp) {
           std::vector<double> host(bs.total);
@@ -854,41 +933,155 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
       }
     }
-    // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] (P:636) -----------------
+    // ---- every rank learns every kept rank; the records go to rank 0 (dist) -----------------
     const double tp2 = now_s();
+    if (dist) {
+      std::vector<uint8_t> all(lev.nclus, 1);
+      sync_ranks(all);
+      // shapes at elimination of every cluster, now that every rank is known: during phase I
+      // a remote interior cluster's neighbours' ranks were not known here
+      std::vector<int32_t> lv2 = cap;
+      for (const auto& Bt : lev.batches) {
+        for (int32_t s : Bt) {
+          int32_t kn = 0, kw = 0;
+          for (int32_t q : lev.H[s]) kn += lv2[q];
+          for (int32_t q : lev.w[s]) kw += lv2[q];
+          L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw;
+        }
+        for (int32_t s : Bt) lv2[s] = L.rank[s];
+      }
+      // T_s is formed on the side stream: join it before the records travel
+      HS_CUDA(cudaEventRecord(h->ev_join, h->side));
+      HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
+      // record sizes of rank g's clusters (ascending id): T (m^2, 4-aligned), C (K kn)
+      auto sizes = [&](int g, int64_t& tw, int64_t& cw) {
+        tw = cw = 0;
+        for (int s = 0; s < lev.nclus; ++s)
+          if (DP.owner[l][s] == g) {
+            tw += ((int64_t)cap[s] * cap[s] + 3) & ~int64_t(3);
+            const int64_t K = cap[s] - L.rank[s];
+            if (K > 0 && L.kn[s] > 0) cw += K * L.kn[s];
+          }
+      };
+      if (h->rank != 0) {
+        int64_t tw, cw;
+        sizes(h->rank, tw, cw);
+        double* cpack = cw ? (double*)dc.alloc(sizeof(double) * cw) : nullptr;
+        std::vector<CopyItem> pk;
+        int64_t co = 0;
+        for (int s = 0; s < lev.nclus; ++s)
+          if (own(l, s) && L.C[s]) {
+            const int32_t K = cap[s] - L.rank[s];
+            pk.push_back(CopyItem{L.C[s], cpack + co, L.kn[s], L.kn[s], K, L.kn[s], 0, 0});
+            co += (int64_t)K * L.kn[s];
+          }
+        split_copies(pk);
+        upA.reset();
+        const size_t iK = upA.add(pk);
+        upA.stage.ensure(upA.total);
+        upA.dev.ensure(upA.total);
+        upA.copy_in(iK, pk);
+        upA.send(st);
+        launch_copy2d(upA.dptr<CopyItem>(iK), (int)pk.size(), st);
+        comm_group_start();
+        comm_send_f64(h->comm, L.arena, (size_t)tw, 0, st);
+        comm_send_f64(h->comm, cpack, (size_t)cw, 0, st);
+        comm_group_end();
+        HS_CUDA(cudaStreamSynchronize(st));
+        if (cpack) dc.free(cpack);
+      } else {
+        std::vector<double*> tb(h->world, nullptr), cb(h->world, nullptr);
+        comm_group_start();
+        for (int g = 1; g < h->world; ++g) {
+          int64_t tw, cw;
+          sizes(g, tw, cw);
+          if (tw) tb[g] = (double*)dc.alloc(sizeof(double) * tw);
+          if (cw) cb[g] = (double*)dc.alloc(sizeof(double) * cw);
+          if (tb[g]) L.cchunks.push_back(tb[g]);
+          if (cb[g]) L.cchunks.push_back(cb[g]);
+          comm_recv_f64(h->comm, tb[g], (size_t)tw, g, st);
+          comm_recv_f64(h->comm, cb[g], (size_t)cw, g, st);
+        }
+        comm_group_end();
+        std::vector<int64_t> to(h->world, 0), co(h->world, 0);
+        for (int s = 0; s < lev.nclus; ++s) {
+          const int g = DP.owner[l][s];
+          if (g == 0) continue;
+          L.T[s] = tb[g] + to[g];
+          to[g] += ((int64_t)cap[s] * cap[s] + 3) & ~int64_t(3);
+          const int64_t K = cap[s] - L.rank[s];
+          if (K > 0 && L.kn[s] > 0) {
+            L.C[s] = cb[g] + co[g];
+            co[g] += K * L.kn[s];
+          }
+        }
+      }
+    }
+    // ---- apply plan of the level (Algorithm 2), replayed in elimination order ---------------
     const int nP = lev.nclus / 2;
     std::vector<int32_t> capn(nP);
     for (int P = 0; P < nP; ++P) capn[P] = L.rank[2 * P] + L.rank[2 * P + 1];
-    const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
-    BlockStore nbs;
-    nbs.build(capn, En, st, &dc);
-    if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
-    t_tr[0] += now_s() - tp2;
-    // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
-    // (c odd ? r(2P) : 0, d odd ? r(2Q) : 0); the upper child pair of a parent diagonal
-    // block never occurs (c >= d), matching its lower-triangle semantics
-    std::vector<CopyItem> asmb;
-    for (int32_t c = 0; c < lev.nclus; ++c) {
-      if (L.rank[c] == 0) continue;
-      const int32_t P = c >> 1;
-      const auto& prow = nbs.rows[P];
-      size_t pi = 0;
-      for (const auto& dof : bs.rows[c]) {
-        const int32_t d = dof.first;
-        if (L.rank[d] == 0) continue;
-        const int32_t Q = d >> 1;
-        while (pi < prow.size() && prow[pi].first < Q) ++pi;   // d ascending -> Q ascending
-        if (pi == prow.size() || prow[pi].first != Q) fail(HS_E_INTERNAL, "assembly: parent block missing");
-        const int32_t dld = capn[Q];
-        const int32_t ro = (c & 1) ? L.rank[2 * P] : 0, co = (d & 1) ? L.rank[2 * Q] : 0;
-        asmb.push_back(CopyItem{bs.d + dof.second, nbs.d + prow[pi].second + (int64_t)ro * dld + co, cap[d], dld,
-                                L.rank[c], L.rank[d], 0, 0});
+    if (plan_apply) {
+      ApplyLevelPlan& AP = ap.lv[l];
+      AP.src.assign(lev.nclus, ApplySrc{});
+      std::vector<int32_t> fev(lev.nclus, 0), lv2 = cap;
+      std::vector<uint8_t> proc(lev.nclus, 0);
+      std::vector<std::vector<BwdTask>> bwd_batches;
+      std::vector<int64_t> foff(lev.nclus, 0);
+      const double ta = now_s();
+      for (const auto& Bt : lev.batches) {
+        if (level_dofs == 0) break;
+        bwd_batches.emplace_back();
+        std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
+        for (int32_t s : Bt) {
+          const int32_t m = lv2[s], r = L.rank[s], K = m - r, kn = L.kn[s];
+          if (m == 0) continue;
+          const auto& ns = lev.H[s];
+          std::vector<int32_t> noff(ns.size() + 1, 0);
+          for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + lv2[ns[a]];
+          // the cluster's record, its forward target tasks (targets grouped up to FWD_COLS
+          // columns) and its backward column chunks
+          ApplySrc& as = AP.src[s];
+          as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
+          as.pre = fev[s]++;
+          as.nb_begin = (int32_t)AP.bnb.size();
+          const int32_t tb = (int32_t)AP.ftgt.size();
+          for (size_t a = 0; a < ns.size(); ++a) {
+            const int32_t q = ns[a];
+            if (lv2[q] == 0 || K == 0) continue;
+            AP.ftgt.push_back(FwdTgt{nullptr, q, noff[a], lv2[q], fev[q]++, proc[q], 0});
+            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1});
+          }
+          as.nb_end = (int32_t)AP.bnb.size();
+          const int32_t te = (int32_t)AP.ftgt.size();
+          if (tb == te) AP.ftask.push_back(FwdTask{s, tb, tb, 1});
+          for (int32_t g0 = tb, first = 1; g0 < te; first = 0) {
+            int32_t g1 = g0, cols = 0;
+            while (g1 < te && (g1 == g0 || (cols + AP.ftgt[g1].len <= FWD_COLS && g1 - g0 < 16))) cols += AP.ftgt[g1++].len;
+            AP.ftask.push_back(FwdTask{s, g0, g1, first});
+            g0 = g1;
+          }
+          as.part = AP.parts;
+          if (K > 0 && kn > 0) {
+            as.nchunk = (kn + BWD_COLS - 1) / BWD_COLS;
+            for (int32_t c = 0; c < as.nchunk; ++c)
+              bwd_tasks.push_back(BwdTask{s, c * BWD_COLS, std::min(BWD_COLS, kn - c * BWD_COLS), c});
+            AP.parts += (int64_t)as.nchunk * K;
+          } else {
+            as.nchunk = 1;
+            bwd_tasks.push_back(BwdTask{s, 0, 0, 0});
+          }
+          foff[s] = ap.ftotal;
+          ap.ftotal += K;
+        }
+        for (int32_t s : Bt) {
+          lv2[s] = L.rank[s];
+          proc[s] = 1;
+        }
       }
-    }
-    // apply plan: resolve vector positions (offsets into d_y / d_yf, made absolute at the
-    // end).  A cluster's live segment is its level segment until it is eliminated, then its
-    // coarse rows inside the parent's segment [coarse(2P); coarse(2P+1)].
-    {
+      // vector positions (offsets into d_y / d_yf, made absolute at the end).  A cluster's
+      // live segment is its level segment until it is eliminated, then its coarse rows
+      // inside the parent's segment [coarse(2P); coarse(2P+1)].
       std::vector<int64_t> voffn(nP + 1, 0);
       for (int P = 0; P < nP; ++P) voffn[P + 1] = voffn[P] + capn[P];
       const int64_t vb = ap.vbase[l], vbn = vbase;   // vbase already advanced past this level
@@ -911,6 +1104,38 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       AP.ctr_off = ap.ctr_total;
       ap.ctr_total += 3 * (int64_t)lev.nclus + 2;
       ap.max_parts = std::max(ap.max_parts, AP.parts);
+      t_sub[2] += now_s() - ta;
+    }
+    // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] (P:636) -----------------
+    const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
+    BlockStore nbs;
+    nbs.build(capn, En, st, &dc, dist ? &DP : nullptr, l + 1);
+    if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
+    t_tr[0] += now_s() - tp2;
+    // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
+    // (c odd ? r(2P) : 0, d odd ? r(2Q) : 0); the upper child pair of a parent diagonal
+    // block never occurs (c >= d), matching its lower-triangle semantics.  A rank holds
+    // every child block of the parent blocks it holds (same owners).
+    std::vector<CopyItem> asmb;
+    for (int32_t c = 0; c < lev.nclus; ++c) {
+      if (L.rank[c] == 0) continue;
+      const int32_t P = c >> 1;
+      const auto& prow = nbs.rows[P];
+      size_t pi = 0;
+      for (const auto& dof : bs.rows[c]) {
+        const int32_t d = dof.first;
+        if (L.rank[d] == 0) continue;
+        const int32_t Q = d >> 1;
+        while (pi < prow.size() && prow[pi].first < Q) ++pi;   // d ascending -> Q ascending
+        if (pi == prow.size() || prow[pi].first != Q) {
+          if (dist) continue;   // a parent block this rank does not hold
+          fail(HS_E_INTERNAL, "assembly: parent block missing");
+        }
+        const int32_t dld = capn[Q];
+        const int32_t ro = (c & 1) ? L.rank[2 * P] : 0, co = (d & 1) ? L.rank[2 * Q] : 0;
+        asmb.push_back(CopyItem{bs.d + dof.second, nbs.d + prow[pi].second + (int64_t)ro * dld + co, cap[d], dld,
+                                L.rank[c], L.rank[d], 0, 0});
+      }
     }
     split_copies(asmb);
     upA.reset();
@@ -951,7 +1176,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                    (long long)sr, (long long)skn, (long long)skw, (long long)mx);
     }
   }
-  // ---- top: dense Cholesky of all live DOFs ----------------------------------
+  // ---- top: dense Cholesky of all live DOFs, on rank 0 -------------------------
   {
     const int ntc = (int)cap.size();
     std::vector<int64_t> toff(ntc + 1, 0);
@@ -962,21 +1187,61 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     S.n_top = N;
     ap.vbase.push_back(vbase);
     vbase += N;
-    if (N > 0) {
+    const int Ltop = an->L_top;
+    // the top blocks (P, Q) held by rank g with g owning P, in store order
+    auto top_blocks = [&](int g) {
+      std::vector<std::pair<int32_t, int32_t>> v;
+      for (int P = 0; P < ntc; ++P) {
+        if (dist && Ltop > 0 && DP.owner[Ltop][P] != g) continue;
+        for (int32_t Q : an->H_top[P])
+          if (Q < P) v.push_back({P, Q});
+        v.push_back({P, P});
+      }
+      return v;
+    };
+    std::vector<std::pair<const double*, std::pair<int32_t, int32_t>>> src;   // rank 0: block data
+    std::vector<double*> tbufs;
+    if (N > 0 && dist && Ltop > 0) {
+      if (h->rank != 0) {
+        comm_group_start();
+        for (auto pq : top_blocks(h->rank)) {
+          double* p; int32_t ld, tr;
+          if (!bs.has(pq.first, pq.second)) continue;
+          bs.get(pq.first, pq.second, p, ld, tr);
+          comm_send_f64(h->comm, p, (size_t)cap[pq.first] * cap[pq.second], 0, st);
+        }
+        comm_group_end();
+        HS_CUDA(cudaStreamSynchronize(st));
+      } else {
+        comm_group_start();
+        for (int g = 1; g < h->world; ++g)
+          for (auto pq : top_blocks(g)) {
+            // rank g stores (P, Q) iff it holds it: it owns P here, and the block exists in H_top
+            const size_t words = (size_t)cap[pq.first] * cap[pq.second];
+            double* b = words ? (double*)dc.alloc(sizeof(double) * words) : nullptr;
+            tbufs.push_back(b);
+            comm_recv_f64(h->comm, b, words, g, st);
+            src.push_back({b, pq});
+          }
+        comm_group_end();
+      }
+    }
+    if (N > 0 && plan_apply) {
       f->d_top = (double*)dc.alloc(sizeof(double) * N * N);
       HS_CUDA(cudaMemsetAsync(f->d_top, 0, sizeof(double) * N * N, st));
-      std::vector<CopyItem> items;
       for (int P = 0; P < ntc; ++P)
-        for (const auto& qo : bs.rows[P]) {
-          const int32_t Q = qo.first;
-          if (cap[P] == 0 || cap[Q] == 0) continue;
-          double* src = bs.d + qo.second;
-          // diagonal blocks hold the lower triangle only: symmetrise them into A_top
-          items.push_back(CopyItem{src, f->d_top + toff[P] * N + toff[Q], cap[Q], (int32_t)N, cap[P], cap[Q],
-                                   P == Q ? 2 : 0, 0});
-          if (P != Q)
-            items.push_back(CopyItem{src, f->d_top + toff[Q] * N + toff[P], cap[Q], (int32_t)N, cap[Q], cap[P], 1, 0});
-        }
+        for (const auto& qo : bs.rows[P])
+          if (!dist || Ltop == 0 || DP.owner[Ltop][P] == 0) src.push_back({bs.d + qo.second, {P, qo.first}});
+      std::vector<CopyItem> items;
+      for (const auto& e : src) {
+        const int32_t P = e.second.first, Q = e.second.second;
+        if (cap[P] == 0 || cap[Q] == 0 || !e.first) continue;
+        // diagonal blocks hold the lower triangle only: symmetrise them into A_top
+        items.push_back(CopyItem{e.first, f->d_top + toff[P] * N + toff[Q], cap[Q], (int32_t)N, cap[P], cap[Q],
+                                 P == Q ? 2 : 0, 0});
+        if (P != Q)
+          items.push_back(CopyItem{e.first, f->d_top + toff[Q] * N + toff[P], cap[Q], (int32_t)N, cap[Q], cap[P], 1, 0});
+      }
       split_copies(items);
       upA.reset();
       const size_t iA = upA.add(items);
@@ -994,6 +1259,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       S.flops_phase[6] += (double)N * N * N / 3.0;
     }
     HS_CUDA(cudaStreamSynchronize(st));
+    for (double* b : tbufs)
+      if (b) dc.free(b);
     bs.release();
   }
   HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // join the side stream (apply operators)

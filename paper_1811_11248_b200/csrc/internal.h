@@ -45,6 +45,7 @@ struct Analysis {
   std::vector<int32_t> colind;
   // device cache of the pattern (filled by the first factor; freed by hs_analysis_destroy)
   int dev = -1;
+  int map_world = 1, map_rank = 0;   // the (world, rank) the cached level-0 scatter map is for
   int64_t* d_rowptr = nullptr;
   int32_t* d_colind = nullptr;
   int64_t* d_perm = nullptr;

@@ -32,7 +32,7 @@ HS_DEXP_OWNER, HS_DEXP_RECV_PTR, HS_DEXP_RECV, HS_DEXP_HELD_PTR, HS_DEXP_HELD = 
 HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(5)
 
 # every symbol include/hsolve.h declares
-SYMBOLS = ["hs_create", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
+SYMBOLS = ["hs_create", "hs_nccl_unique_id", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
            "hs_analysis_get_info", "hs_analysis_export", "hs_dist_plan_export", "hs_analysis_destroy", "hs_factor_create",
            "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
            "hs_pcg", "hs_spmv", "hs_launch_count"]
@@ -106,6 +106,7 @@ def lib():
         vp, i32, i64, dp = C.c_void_p, C.c_int32, C.c_int64, C.c_double
         L.hs_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, vp]
         L.hs_set_stream.argtypes = [vp, vp]
+        L.hs_nccl_unique_id.argtypes = [vp]
         L.hs_destroy.argtypes = [vp]
         L.hs_destroy.restype = None
         L.hs_last_error.argtypes = [vp]
@@ -186,9 +187,16 @@ class Factor:
             self.ptr = None
 
 
-def hs_create(device: int = 0, world_size: int = 1, rank: int = 0, nccl_unique_id=None) -> Handle:
+def hs_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().hs_nccl_unique_id(buf))
+    return buf.raw
+
+
+def hs_create(device: int = 0, world_size: int = 1, rank: int = 0, nccl_unique_id: bytes | None = None) -> Handle:
     h = C.c_void_p()
-    _check(lib().hs_create(C.byref(h), device, world_size, rank, nccl_unique_id))
+    uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
+    _check(lib().hs_create(C.byref(h), device, world_size, rank, uid))
     return Handle(h)
 
 
