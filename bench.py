@@ -10,8 +10,10 @@ PCG to 1e-8), the config the metric is quoted on; inputs (CSR values, b) are res
 HBM when the timed region starts and the analysis (pattern only) is done once before it.
 value = DOF/s = N * K / (device time of the K steps); e2e repeats the step through the
 same C API with HOST buffers (values and b uploaded, x downloaded inside the timed region).
-N > 1: one process per GPU, each running its own full replica (weak scaling, no
-data-path collective: the subdomain-sharded factor is not built yet).
+N > 1 (torchrun, one process per GPU): the factor is partitioned by the 8 fixed subdomains
+over the GPUs with NCCL exchanges (strong scaling: one system
+per step), the solve runs on rank 0; --replicas runs N independent systems instead (weak).
+A watchdog aborts a run whose exchanges never complete (exit 3, an error JSON line).
 --impl reference times the CPU oracle (oracle/) on the host cores on a bounded sample.
 """
 from __future__ import annotations
@@ -41,6 +43,10 @@ def parse():
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent single-GPU factorizations instead of the subdomain-distributed one")
+    ap.add_argument("--watchdog", type=float, default=900.0,
+                    help="N>1: abort (exit 3) if the run has not finished after this many seconds")
     return ap.parse_args()
 
 
@@ -143,13 +149,30 @@ def run_ours(args, rank, world, local):
     from paper_1811_11248_b200 import hsolve as H
     from problems import gen_config
     torch.cuda.set_device(local)
+    dist_factor = world > 1 and not args.replicas
     if world > 1:
+        import threading
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+        def _watchdog():   # an NCCL exchange that never completes must not hang the job
+            time.sleep(args.watchdog)
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": "DOF/s", "n_gpus": world,
+                                  "error": f"watchdog: no result after {args.watchdog:.0f} s"}), flush=True)
+            os._exit(3)
+        threading.Thread(target=_watchdog, daemon=True).start()
     p = gen_config(args.config)
     if args.eps is not None:
         p.eps = args.eps
-    h = H.hs_create(local)
+    if dist_factor:
+        # the factor is partitioned by the 8 fixed subdomains over the ranks
+        # (NCCL exchanges inside hs_factor_create); the solve runs on rank 0 (v1)
+        uid = [H.hs_nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        h = H.hs_create(local, world, rank, uid[0])
+    else:
+        h = H.hs_create(local)
     stream = torch.cuda.current_stream()
     H.hs_set_stream(h, stream.cuda_stream)
     t0 = time.perf_counter()
@@ -166,9 +189,13 @@ def run_ours(args, rank, world, local):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    solver = not dist_factor or rank == 0
+
     def step():
         f = H.hs_factor_create(h, a, vals, eps=p.eps)
-        xx, rep = H.hs_pcg(f, b, tol=p.tol, x=x)
+        rep = None
+        if solver:
+            xx, rep = H.hs_pcg(f, b, tol=p.tol, x=x)
         return f, rep
 
     for _ in range(args.warmup):
@@ -198,14 +225,18 @@ def run_ours(args, rank, world, local):
         t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         tot_ms = float(t.item())
-    value = world * p.n * args.steps / (tot_ms * 1e-3)
+    units = p.n if dist_factor else world * p.n   # distributed: one system split over the GPUs
+    value = units * args.steps / (tot_ms * 1e-3)
     # ---- e2e through the C API with host buffers -------------------------------------------
     e2e = None
     if not args.no_e2e:
         hv = np.ascontiguousarray(p.vals)
         hb = np.ascontiguousarray(p.b)
         hx = np.empty_like(hb)
-        H.hs_pcg(H.hs_factor_create(h, a, hv, eps=p.eps), hb, tol=p.tol, x=hx)
+        f = H.hs_factor_create(h, a, hv, eps=p.eps)
+        if solver:
+            H.hs_pcg(f, hb, tol=p.tol, x=hx)
+        del f
         e2e_ms = 0.0
         for _ in range(args.steps):
             flush.zero_()
@@ -214,7 +245,8 @@ def run_ours(args, rank, world, local):
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             f = H.hs_factor_create(h, a, hv, eps=p.eps)
-            H.hs_pcg(f, hb, tol=p.tol, x=hx)
+            if solver:
+                H.hs_pcg(f, hb, tol=p.tol, x=hx)
             e1.record(stream)
             e1.synchronize()
             e2e_ms += e0.elapsed_time(e1)
@@ -223,7 +255,7 @@ def run_ours(args, rank, world, local):
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": world * p.n * args.steps / (e2e_ms * 1e-3), "unit": "DOF/s",
+        e2e = {"value": units * args.steps / (e2e_ms * 1e-3), "unit": "DOF/s",
                "h2d_bytes_per_step": int(p.vals.nbytes + p.b.nbytes), "d2h_bytes_per_step": int(hx.nbytes)}
     if rank != 0:
         if world > 1:
@@ -269,12 +301,14 @@ def run_ours(args, rank, world, local):
                          f"({it_s} iterations) in {t_s:.1f} s on 1 host thread"}
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if dist_factor else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {p.name}, N={p.n}, nnz={p.nnz}, eps={p.eps}, pcg_tol={p.tol}, "
                                f"leaf={p.leaf_size or p.leaf_columns}",
                    "l2": "256 MB buffer written between timed steps (and the factor working set > L2)",
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": (f"subdomains over {world} GPUs (factor), solve on rank 0" if dist_factor
+                                   else "replicas" if world > 1 else "single"),
                    "pcg_iters": [r["iters"] for r in reps], "relres_true": reps[-1]["relres_true"],
                    "t_analyze_s": t_analyze, "t_factor_s": t_fac, "t_pcg_s": t_pcg / args.steps,
                    "t_apply_s_per_step": t_apply / args.steps,
