@@ -162,6 +162,13 @@ hs_status hs_create(hs_handle* h, int device, int world_size, int rank, const vo
  * process group (e.g. torch.distributed) and every rank passes it to hs_create.  NCCL is
  * loaded on first use (dlopen of libnccl.so.2, HS_NCCL_LIB overrides); HS_E_NCCL if absent. */
 hs_status hs_nccl_unique_id(void* out128);
+/* Test harness for the multi-GPU factor on ONE device: world_size ranks run as host threads
+ * of one process, each with its own handle (hs_create_loopback); their exchanges become
+ * device-to-device copies ordered by CUDA events between the ranks' streams and host
+ * barriers (no kernel waits on another rank).  The world object outlives its handles. */
+hs_status hs_loopback_world_create(int32_t world_size, void** world);
+void      hs_loopback_world_destroy(void* world);
+hs_status hs_create_loopback(hs_handle* h, int device, void* world, int32_t rank);
 /* stream: a cudaStream_t on the handle's device (e.g. torch.cuda.current_stream()),
  * or NULL for the library's own stream.  All device work of the handle runs on it. */
 hs_status hs_set_stream(hs_handle h, void* stream);

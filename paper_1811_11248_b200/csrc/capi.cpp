@@ -88,12 +88,37 @@ const char* hs_last_error(hs_handle h) {
   return g_err.c_str();
 }
 
+static hs_status create_impl(hs_handle* out, int device, int world_size, int rank, const void* nccl_unique_id,
+                             void* loopback);
+
 hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const void* nccl_unique_id) {
+  return create_impl(out, device, world_size, rank, nccl_unique_id, nullptr);
+}
+
+hs_status hs_loopback_world_create(int32_t world, void** out) {
+  return guarded(nullptr, [&] {
+    if (!out || world < 2) hs::fail(HS_E_INVALID_ARG, "hs_loopback_world_create: need world >= 2");
+    *out = hs::loop_world_create(world);
+  });
+}
+
+void hs_loopback_world_destroy(void* w) {
+  if (w) hs::loop_world_destroy((hs::LoopWorld*)w);
+}
+
+hs_status hs_create_loopback(hs_handle* out, int device, void* world, int32_t rank) {
+  if (!world) return HS_E_INVALID_ARG;
+  return create_impl(out, device, hs::loop_world_size((hs::LoopWorld*)world), rank, nullptr, world);
+}
+
+static hs_status create_impl(hs_handle* out, int device, int world_size, int rank, const void* nccl_unique_id,
+                             void* loopback) {
   return guarded(nullptr, [&] {
     if (!out) hs::fail(HS_E_INVALID_ARG, "hs_create: NULL out");
     *out = nullptr;
     if (world_size < 1 || rank < 0 || rank >= world_size) hs::fail(HS_E_INVALID_ARG, "hs_create: bad world/rank");
-    if (world_size > 1 && !nccl_unique_id) hs::fail(HS_E_INVALID_ARG, "hs_create: world_size > 1 needs an NCCL id");
+    if (world_size > 1 && !nccl_unique_id && !loopback)
+      hs::fail(HS_E_INVALID_ARG, "hs_create: world_size > 1 needs an NCCL id");
     int nd = 0;
     if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
       cudaGetLastError();
@@ -112,7 +137,9 @@ hs_status hs_create(hs_handle* out, int device, int world_size, int rank, const 
     h->upB.dev.dc = &h->cache;
     h->world = world_size;
     h->rank = rank;
-    if (world_size > 1) {
+    if (world_size > 1 && loopback) {
+      h->comm = hs::comm_loopback((hs::LoopWorld*)loopback, rank);
+    } else if (world_size > 1) {
       try {
         h->comm = hs::comm_init(world_size, rank, nccl_unique_id);
       } catch (...) {
@@ -326,6 +353,8 @@ hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out
         std::vector<int64_t> v;
         for (int s = 0; s < L.nclus; ++s) {
           std::vector<int32_t> tmp(L.rank[s]);
+          if (L.rank[s] && !L.piv[s])
+            hs::fail(HS_E_UNSUPPORTED, "hs_factor_export: pivots of clusters eliminated on another rank stay there");
           if (L.rank[s])
             HS_CUDA(cudaMemcpy(tmp.data(), L.piv[s], sizeof(int32_t) * L.rank[s], cudaMemcpyDeviceToHost));
           v.insert(v.end(), tmp.begin(), tmp.end());

@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -563,13 +565,12 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
 template <int MR, bool SM>
 void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
                 cudaStream_t st, long long* trace) {
-  static bool attr = false;
   auto kern = k_cpqr3<MR, SM>;
-  if (!attr) {
+  static std::once_flag once;
+  std::call_once(once, [&] {
     HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -619,7 +620,7 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
     const char* e = std::getenv("HS_CQ_TRACE");
     return e ? std::atoi(e) : -1;
   }();
-  static int launches = 0;
+  static std::atomic<int> launches{0};
   long long* trace = nullptr;
   if (launches++ == trace_at) {
     HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
@@ -659,18 +660,16 @@ void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int m
   const size_t words = std::min<size_t>((size_t)max_m * max_m + max_m, 24 * 1024);
   const size_t smem = sizeof(double) * words;
   if (max_m <= 256) {
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag once;
+    std::call_once(once, [] {
       HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    });
     k_rotate_n<8><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
   } else {
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag once;
+    std::call_once(once, [] {
       HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    });
     k_rotate_n<16><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
   }
   count_launch(1);

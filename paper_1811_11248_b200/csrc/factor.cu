@@ -597,7 +597,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           done[s] = 1;
         }
     };
-    std::vector<uint8_t> elim_so_far(lev.nclus, 0);
 
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
@@ -605,7 +604,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       const auto& Bt = lev.batches[bidx];
       if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
       const bool phase2 = (int)bidx >= lev.nphase1;
-      if (dist && phase2 && (int)bidx == lev.nphase1) sync_ranks(elim_so_far);   // phase-I ranks
+      if (dist && phase2 && (int)bidx == lev.nphase1) {   // the phase-I ranks of every owner
+        std::vector<uint8_t> ph1(lev.nclus, 0);
+        for (int b = 0; b < lev.nphase1; ++b)
+          for (int32_t s : lev.batches[b]) ph1[s] = 1;
+        sync_ranks(ph1);
+      }
       const double tp0 = now_s();
       // shapes of every cluster of the batch from the current live sizes
       for (int32_t s : Bt) {
@@ -706,7 +710,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
         L.rank[s] = live[s] == 0 ? 0 : h_rank[bi];
-        elim_so_far[s] = 1;
       }
       // ---- phase II across GPUs: the batch's ranks, then the elimination records ---------
       std::vector<double*> rbuf(Bt.size(), nullptr);   // received B_s of remote clusters
@@ -716,7 +719,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           if (own(l, Bt[k])) v[k] = L.rank[Bt[k]];
         allreduce_i32(v);
         for (size_t k = 0; k < Bt.size(); ++k) L.rank[Bt[k]] = v[k];
-        comm_group_start();
+        comm_group_start(h->comm);
         for (size_t k = 0; k < Bt.size(); ++k) {
           const int32_t s = Bt[k];
           const size_t words = (size_t)live[s] * L.ldB[s];
@@ -729,7 +732,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             comm_recv_f64(h->comm, rbuf[k], words, DP.owner[l][s], st);
           }
         }
-        comm_group_end();
+        comm_group_end(h->comm, st);
       }
       // ---- Schur update, write-back (local and received records) --------------------------
       std::vector<SchurSrc> srcs;
@@ -983,15 +986,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upA.copy_in(iK, pk);
         upA.send(st);
         launch_copy2d(upA.dptr<CopyItem>(iK), (int)pk.size(), st);
-        comm_group_start();
+        comm_group_start(h->comm);
         comm_send_f64(h->comm, L.arena, (size_t)tw, 0, st);
         comm_send_f64(h->comm, cpack, (size_t)cw, 0, st);
-        comm_group_end();
+        comm_group_end(h->comm, st);
         HS_CUDA(cudaStreamSynchronize(st));
         if (cpack) dc.free(cpack);
       } else {
         std::vector<double*> tb(h->world, nullptr), cb(h->world, nullptr);
-        comm_group_start();
+        comm_group_start(h->comm);
         for (int g = 1; g < h->world; ++g) {
           int64_t tw, cw;
           sizes(g, tw, cw);
@@ -1002,7 +1005,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           comm_recv_f64(h->comm, tb[g], (size_t)tw, g, st);
           comm_recv_f64(h->comm, cb[g], (size_t)cw, g, st);
         }
-        comm_group_end();
+        comm_group_end(h->comm, st);
         std::vector<int64_t> to(h->world, 0), co(h->world, 0);
         for (int s = 0; s < lev.nclus; ++s) {
           const int g = DP.owner[l][s];
@@ -1203,17 +1206,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::vector<double*> tbufs;
     if (N > 0 && dist && Ltop > 0) {
       if (h->rank != 0) {
-        comm_group_start();
+        comm_group_start(h->comm);
         for (auto pq : top_blocks(h->rank)) {
           double* p; int32_t ld, tr;
           if (!bs.has(pq.first, pq.second)) continue;
           bs.get(pq.first, pq.second, p, ld, tr);
           comm_send_f64(h->comm, p, (size_t)cap[pq.first] * cap[pq.second], 0, st);
         }
-        comm_group_end();
+        comm_group_end(h->comm, st);
         HS_CUDA(cudaStreamSynchronize(st));
       } else {
-        comm_group_start();
+        comm_group_start(h->comm);
         for (int g = 1; g < h->world; ++g)
           for (auto pq : top_blocks(g)) {
             // rank g stores (P, Q) iff it holds it: it owns P here, and the block exists in H_top
@@ -1223,7 +1226,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             comm_recv_f64(h->comm, b, words, g, st);
             src.push_back({b, pq});
           }
-        comm_group_end();
+        comm_group_end(h->comm, st);
       }
     }
     if (N > 0 && plan_apply) {

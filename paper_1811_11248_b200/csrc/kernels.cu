@@ -12,6 +12,9 @@
 
 #include <cfloat>
 #include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "device.h"
@@ -923,15 +926,32 @@ __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restri
   }
 }
 
+// The opt-in dynamic shared memory of a kernel only ever grows: handles on other host
+// threads (multi-rank loopback, several solvers in one process) launch the same kernels, so
+// lowering it could make a concurrent launch fail.
 void set_smem(const void* f, size_t bytes) {
-  static_cast<void>(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[f];
+  if (bytes <= c) return;
+  HS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
 }
 
 std::atomic<int64_t> g_launches{0};
 
 }  // namespace
 
-void count_launch(int64_t n) { g_launches += n; }
+void count_launch(int64_t n) {
+  g_launches += n;
+  // a launch that could not start (configuration error) must not pass silently
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(HS_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+}
 int64_t launch_count() { return g_launches.load(); }
 
 // ---- launchers -----------------------------------------------------------------------------
@@ -1030,13 +1050,12 @@ int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, do
   if (n <= 0) return 0;
   int maxcol = 0;
   for (const auto& it : h_items) maxcol = std::max(maxcol, it.kw + it.kn);
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag once;
+  std::call_once(once, [] {
     HS_CUDA(cudaFuncSetAttribute((const void*)k_cpqr2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     HS_CUDA(cudaFuncSetAttribute((const void*)k_cpqr2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)CPQR2_SMEM_BUDGET + 8192));
-    attr = true;
-  }
+  });
   auto smem_for = [&](int cs) {
     size_t smem = 8;
     for (const auto& it : h_items) {

@@ -138,15 +138,22 @@ struct ApplyPlan {
 }  // namespace hs
 
 namespace hs {
-// NCCL (comm.cpp), loaded only for world_size > 1
+// Multi-GPU transport (comm.cpp): NCCL (loaded only for world_size > 1), or the loopback
+// test harness (P ranks as host threads on one device, copies ordered by events)
+struct Comm;
+struct LoopWorld;
 void nccl_unique_id(void* out128);
-void* comm_init(int world, int rank, const void* id128);
-void comm_destroy(void* c);
-void comm_allreduce_sum_i32(void* c, int32_t* d_buf, size_t n, cudaStream_t st);
-void comm_group_start();
-void comm_group_end();
-void comm_send_f64(void* c, const double* d, size_t n, int peer, cudaStream_t st);
-void comm_recv_f64(void* c, double* d, size_t n, int peer, cudaStream_t st);
+Comm* comm_init(int world, int rank, const void* id128);
+Comm* comm_loopback(LoopWorld* w, int rank);
+LoopWorld* loop_world_create(int world);
+void loop_world_destroy(LoopWorld* w);
+int loop_world_size(LoopWorld* w);
+void comm_destroy(Comm* c);
+void comm_allreduce_sum_i32(Comm* c, int32_t* d_buf, size_t n, cudaStream_t st);
+void comm_group_start(Comm* c);
+void comm_group_end(Comm* c, cudaStream_t st);
+void comm_send_f64(Comm* c, const double* d, size_t n, int peer, cudaStream_t st);
+void comm_recv_f64(Comm* c, double* d, size_t n, int peer, cudaStream_t st);
 }  // namespace hs
 
 struct hs_handle_s {
@@ -156,7 +163,7 @@ struct hs_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool own_stream = false;
   int world = 1, rank = 0;
-  void* comm = nullptr;         // ncclComm_t when world > 1
+  hs::Comm* comm = nullptr;     // world > 1: NCCL or loopback transport
   std::string err;
   hs::DevCache cache;           // declared before the staging buffers (destroyed after them)
   hs::Upload upA, upB;          // descriptor staging, reused across factors

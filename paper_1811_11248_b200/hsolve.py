@@ -32,7 +32,8 @@ HS_DEXP_OWNER, HS_DEXP_RECV_PTR, HS_DEXP_RECV, HS_DEXP_HELD_PTR, HS_DEXP_HELD = 
 HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(5)
 
 # every symbol include/hsolve.h declares
-SYMBOLS = ["hs_create", "hs_nccl_unique_id", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
+SYMBOLS = ["hs_create", "hs_nccl_unique_id", "hs_loopback_world_create", "hs_loopback_world_destroy",
+           "hs_create_loopback", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
            "hs_analysis_get_info", "hs_analysis_export", "hs_dist_plan_export", "hs_analysis_destroy", "hs_factor_create",
            "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
            "hs_pcg", "hs_spmv", "hs_launch_count"]
@@ -107,6 +108,10 @@ def lib():
         L.hs_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, vp]
         L.hs_set_stream.argtypes = [vp, vp]
         L.hs_nccl_unique_id.argtypes = [vp]
+        L.hs_loopback_world_create.argtypes = [i32, C.POINTER(vp)]
+        L.hs_loopback_world_destroy.argtypes = [vp]
+        L.hs_loopback_world_destroy.restype = None
+        L.hs_create_loopback.argtypes = [C.POINTER(vp), C.c_int, vp, i32]
         L.hs_destroy.argtypes = [vp]
         L.hs_destroy.restype = None
         L.hs_last_error.argtypes = [vp]
@@ -132,6 +137,7 @@ def lib():
         L.hs_launch_count.restype = i64
         for s in SYMBOLS:
             if s not in ("hs_destroy", "hs_analysis_destroy", "hs_factor_destroy", "hs_last_error",
+                         "hs_loopback_world_destroy",
                          "hs_status_string", "hs_launch_count"):
                 getattr(L, s).restype = C.c_int
         _lib = L
@@ -191,6 +197,26 @@ def hs_nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().hs_nccl_unique_id(buf))
     return buf.raw
+
+
+class LoopbackWorld:
+    """Test harness: `world` ranks as host threads on one device (hs_create_loopback)."""
+
+    def __init__(self, world: int):
+        self.ptr = C.c_void_p()
+        _check(lib().hs_loopback_world_create(world, C.byref(self.ptr)))
+        self.world = world
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value and _lib is not None:
+            _lib.hs_loopback_world_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def hs_create_loopback(device: int, world: LoopbackWorld, rank: int) -> Handle:
+    h = C.c_void_p()
+    _check(lib().hs_create_loopback(C.byref(h), device, world.ptr, rank))
+    return Handle(h)
 
 
 def hs_create(device: int = 0, world_size: int = 1, rank: int = 0, nccl_unique_id: bytes | None = None) -> Handle:
