@@ -105,15 +105,18 @@ struct BlockStore {
     layout(caps, edges, dp, level);
     if (total) d = (double*)dc->alloc(total * sizeof(double));
   }
+  std::vector<std::vector<std::pair<int32_t, int64_t>>> cols;   // q -> sorted (p > q, offset)
   void layout(const std::vector<int32_t>& caps, const Adj& edges, const DistPlan* dp = nullptr, int level = 0) {
     cap = caps;
     const int n = (int)caps.size();
     rows.assign(n, {});
+    cols.assign(n, {});
     int64_t off = 0;
     for (int p = 0; p < n; ++p) {
       for (int32_t q : edges[p])
         if (q < p && (!dp || dp->holds(level, p, q))) {
           rows[p].push_back({q, off});
+          cols[q].push_back({p, off});
           off += (int64_t)caps[p] * caps[q];
         }
       if (!dp || dp->own(level, p)) {
@@ -130,6 +133,28 @@ struct BlockStore {
     return it->second;
   }
   bool has(int32_t p, int32_t q) const { return p >= q ? off(p, q) >= 0 : off(q, p) >= 0; }
+  // offsets of the blocks (s, q), q in `list` (ascending, q != s), -1 where absent: one
+  // merge over row s (q < s) and column s (q > s) instead of a search per block
+  void row_offsets(int32_t s, const std::vector<int32_t>& list, std::vector<int64_t>& out) const {
+    const auto& R = rows[s];
+    const auto& K = cols[s];
+    size_t i = 0, j = 0;
+    for (int32_t q : list) {
+      if (q < s) {
+        while (i < R.size() && R[i].first < q) ++i;
+        out.push_back(i < R.size() && R[i].first == q ? R[i].second : -1);
+      } else {
+        while (j < K.size() && K[j].first < q) ++j;
+        out.push_back(j < K.size() && K[j].first == q ? K[j].second : -1);
+      }
+    }
+  }
+  // block (s, q) from a row_offsets() entry, as get() returns it
+  void at(int32_t s, int32_t q, int64_t o, double*& ptr, int32_t& ld, int32_t& trans) const {
+    ptr = d + o;
+    ld = q < s ? cap[q] : cap[s];
+    trans = q < s ? 0 : 1;
+  }
   // A(p, q) as (pointer, ld, trans): A(p,q)[i][j] = trans ? ptr[j*ld + i] : ptr[i*ld + j]
   void get(int32_t p, int32_t q, double*& ptr, int32_t& ld, int32_t& trans) const {
     if (p >= q) {
@@ -583,6 +608,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     lp.build(lev, bs, dc, upA, st);
     std::vector<int32_t> live = cap;
     std::vector<uint8_t> done(lev.nclus, 0);   // eliminated (rank known here)
+    // store offsets of row s's blocks, [w(s) ..., n(s) ...] (computed once per cluster)
+    std::vector<std::vector<int64_t>> roff(lev.nclus);
+    auto row_offs = [&](int32_t s) -> const std::vector<int64_t>& {
+      auto& v = roff[s];
+      if (v.empty() && !(lev.w[s].empty() && lev.H[s].empty())) {
+        v.reserve(lev.w[s].size() + lev.H[s].size());
+        bs.row_offsets(s, lev.w[s], v);
+        bs.row_offsets(s, lev.H[s], v);
+      }
+      return v;
+    };
     std::vector<uint64_t> wave_mask(lev.nclus, 0);
     // all-reduce of the kept ranks of the eliminated clusters (dist): owners contribute
     auto sync_ranks = [&](const std::vector<uint8_t>& elim) {
@@ -654,10 +690,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         bs.get(s, s, p, ld, tr);
         gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, tr, 0});
         int32_t col = 0;
+        const auto& ro = row_offs(s);
+        size_t kq = 0;
         for (int pass = 0; pass < 2; ++pass)
           for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+            const int64_t o = ro[kq++];
             if (live[q] > 0) {
-              bs.get(s, q, p, ld, tr);
+              if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
+              bs.at(s, q, o, p, ld, tr);
               gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
             }
             col += live[q];
@@ -812,10 +852,13 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
           }
           int32_t col = 0;
+          const auto& ro = row_offs(s);
+          size_t kq = 0;
           for (int pass = 0; pass < 2; ++pass)
             for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
-              if (live[q] > 0 && bs.has(s, q)) {
-                bs.get(s, q, p, ld, tr);
+              const int64_t o = ro[kq++];
+              if (live[q] > 0 && o >= 0) {
+                bs.at(s, q, o, p, ld, tr);
                 if (!tr) wb.push_back(CopyItem{Bs + col, p, ldB, ld, r, live[q], 0, 0});
                 else wb.push_back(CopyItem{Bs + col, p, ldB, ld, live[q], r, 1, 0});
               }
