@@ -109,6 +109,18 @@ struct ApplySrc {
   int32_t nchunk;            // backward tasks of s (>= 1)
   int32_t nb_begin, nb_end;  // neighbour list (backward gather)
   int64_t part;              // partial sums of the backward chunks: nchunk x K
+  int32_t pre_begin, pre_end;    // forward contributions to y_s from sources eliminated before s
+  int32_t post_begin, post_end;  // contributions to s's coarse part from sources eliminated after s
+  int32_t tg_begin, tg_end;      // the contributions s produces (Contrib list)
+};
+struct PullSrc {             // y[0:len] -= contrib[slot : slot+len], produced by source t
+  int64_t slot;
+  int32_t t, pad;
+};
+struct Contrib {             // contrib[slot : slot+len] = C_s[:, col:col+len]^T y_f,s (source s)
+  int64_t slot;
+  int32_t col, len;
+  int32_t q, pre;            // target; pre: q is eliminated later (counts toward arr[q])
 };
 struct FwdTgt {              // y_q[0:len] -= C_s[:, col:col+len]^T y_f,s
   double* y;                 // q's live segment (level or parent vector)
@@ -130,6 +142,11 @@ constexpr int BWD_COLS = 512;        // columns of C per backward task
 constexpr int FWD_COLS = 256;        // target columns per forward task
 struct ApplyLevelArgs {
   const ApplySrc* src;
+  const PullSrc* pull;       // pre / post contribution lists (pull-mode forward sweep)
+  const Contrib* ctb;        // contributions produced per source
+  double* contrib;           // their values
+  const int32_t* post_cl;    // clusters with post contributions
+  int32_t npost, pad0;
   const FwdTask* ftask;
   const FwdTgt* ftgt;
   const BwdTask* btask;
@@ -138,6 +155,7 @@ struct ApplyLevelArgs {
   int32_t* cnt;              // forward event counters (nclus)
   int32_t* bcnt;             // backward chunk arrivals (nclus)
   int32_t* done;             // backward completion flags (nclus)
+  int32_t* arr;              // forward: contributions arrived per target (nclus)
   int32_t* ticket;           // [0] forward, [1] backward
   int32_t nftask, nbtask;
 };
@@ -194,6 +212,7 @@ constexpr int TOP_NB = 64;
 // T_s = U^T G^{-1} for the clusters of a batch (after CPQR; the rank comes from d_rank)
 void launch_form_T(const FormTItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st);
+void launch_apply_post_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);

@@ -373,8 +373,10 @@ hs_factor_s::~hs_factor_s() {
     for (double* p : l.wchunks) fr(p);
     for (double* p : l.cchunks) fr(p);
   }
-  for (auto& p : ap.lv) { fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); }
-  fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr);
+  for (auto& p : ap.lv) {
+    fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb);
+  }
+  fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr); fr(ap.d_contrib);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
   fr(d_r); fr(d_z); fr(d_p); fr(d_q); fr(d_x); fr(d_b); fr(d_red);
   if (h_red) cudaFreeHost(h_red);
@@ -1072,6 +1074,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       AP.src.assign(lev.nclus, ApplySrc{});
       std::vector<int32_t> fev(lev.nclus, 0), lv2 = cap;
       std::vector<uint8_t> proc(lev.nclus, 0);
+      std::vector<std::vector<PullSrc>> pre(lev.nclus), post(lev.nclus);
+      int64_t slots = 0;   // contribution slots of the level
       std::vector<std::vector<BwdTask>> bwd_batches;
       std::vector<int64_t> foff(lev.nclus, 0);
       const double ta = now_s();
@@ -1091,19 +1095,27 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
           as.pre = fev[s]++;
           as.nb_begin = (int32_t)AP.bnb.size();
-          const int32_t tb = (int32_t)AP.ftgt.size();
+          // forward (pull form): s contributes to the unprocessed neighbours before their own
+          // elimination (their pre lists) and to the coarse parts of the processed ones
+          // afterwards (post lists); lists grow in elimination order
+          as.tg_begin = (int32_t)AP.ctb.size();
           for (size_t a = 0; a < ns.size(); ++a) {
             const int32_t q = ns[a];
             if (lv2[q] == 0 || K == 0) continue;
-            AP.ftgt.push_back(FwdTgt{nullptr, q, noff[a], lv2[q], fev[q]++, proc[q], 0});
+            (proc[q] ? post[q] : pre[q]).push_back(PullSrc{slots, s, 0});
+            AP.ctb.push_back(Contrib{slots, noff[a], lv2[q], q, proc[q] ? 0 : 1});
+            slots += lv2[q];
             AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1});
           }
+          as.tg_end = (int32_t)AP.ctb.size();
           as.nb_end = (int32_t)AP.bnb.size();
-          const int32_t te = (int32_t)AP.ftgt.size();
-          if (tb == te) AP.ftask.push_back(FwdTask{s, tb, tb, 1});
-          for (int32_t g0 = tb, first = 1; g0 < te; first = 0) {
+          // T(s) with s's first contribution group, then the other groups (<= FWD_COLS
+          // columns / 16 targets each) as tasks of their own
+          if (as.tg_begin == as.tg_end) AP.ftask.push_back(FwdTask{s, as.tg_begin, as.tg_end, 1});
+          for (int32_t g0 = as.tg_begin, first = 1; g0 < as.tg_end; first = 0) {
             int32_t g1 = g0, cols = 0;
-            while (g1 < te && (g1 == g0 || (cols + AP.ftgt[g1].len <= FWD_COLS && g1 - g0 < 16))) cols += AP.ftgt[g1++].len;
+            while (g1 < as.tg_end && (g1 == g0 || (cols + AP.ctb[g1].len <= FWD_COLS && g1 - g0 < 16)))
+              cols += AP.ctb[g1++].len;
             AP.ftask.push_back(FwdTask{s, g0, g1, first});
             g0 = g1;
           }
@@ -1147,8 +1159,20 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       for (auto& nbr : AP.bnb) nbr.x = (double*)(nbr.later ? lpos(nbr.q) : ppos(nbr.q));
       for (auto it = bwd_batches.rbegin(); it != bwd_batches.rend(); ++it)
         AP.btask.insert(AP.btask.end(), it->begin(), it->end());
+      AP.contrib_off = ap.contrib_total;
+      ap.contrib_total += slots;
+      for (int32_t c = 0; c < lev.nclus; ++c) {
+        ApplySrc& as = AP.src[c];
+        as.pre_begin = (int32_t)AP.pull.size();
+        AP.pull.insert(AP.pull.end(), pre[c].begin(), pre[c].end());
+        as.pre_end = (int32_t)AP.pull.size();
+        as.post_begin = (int32_t)AP.pull.size();
+        AP.pull.insert(AP.pull.end(), post[c].begin(), post[c].end());
+        as.post_end = (int32_t)AP.pull.size();
+        if (!post[c].empty() && as.m > 0) AP.post_cl.push_back(c);
+      }
       AP.ctr_off = ap.ctr_total;
-      ap.ctr_total += 3 * (int64_t)lev.nclus + 2;
+      ap.ctr_total += 4 * (int64_t)lev.nclus + 2;
       ap.max_parts = std::max(ap.max_parts, AP.parts);
       t_sub[2] += now_s() - ta;
     }
@@ -1344,6 +1368,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ap.d_y = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));
   ap.d_yf = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.ftotal, 1));
   ap.d_parts = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.max_parts, 1));
+  ap.d_contrib = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.contrib_total, 1));
   ap.d_ctr = (int32_t*)dc.alloc(sizeof(int32_t) * std::max<int64_t>(ap.ctr_total, 1));
   auto up = [&](auto& vec, auto*& dptr) {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
@@ -1367,6 +1392,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     up(AP.ftgt, AP.d_ftgt);
     up(AP.btask, AP.d_btask);
     up(AP.bnb, AP.d_bnb);
+    up(AP.pull, AP.d_pull);
+    up(AP.ctb, AP.d_ctb);
+    up(AP.post_cl, AP.d_post_cl);
   }
   HS_CUDA(cudaStreamSynchronize(st));
   return guard.release();

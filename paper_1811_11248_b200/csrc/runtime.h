@@ -114,6 +114,10 @@ struct ApplyLevelPlan {
   std::vector<FwdTgt> ftgt;
   std::vector<BwdTask> btask;
   std::vector<BwdNb> bnb;
+  std::vector<PullSrc> pull;            // pre / post lists of every cluster
+  std::vector<Contrib> ctb;             // contributions each source produces
+  std::vector<int32_t> post_cl;
+  int64_t contrib_off = 0;              // this level's slots in ApplyPlan::d_contrib
   int64_t ctr_off = 0;                  // counters: cnt[nclus] bcnt[nclus] done[nclus] ticket[2]
   int64_t parts = 0;                    // partial-sum doubles of the backward sweep
   ApplySrc* d_src = nullptr;
@@ -121,6 +125,9 @@ struct ApplyLevelPlan {
   FwdTgt* d_ftgt = nullptr;
   BwdTask* d_btask = nullptr;
   BwdNb* d_bnb = nullptr;
+  PullSrc* d_pull = nullptr;
+  Contrib* d_ctb = nullptr;
+  int32_t* d_post_cl = nullptr;
 };
 
 struct ApplyPlan {
@@ -130,6 +137,8 @@ struct ApplyPlan {
   double* d_y = nullptr;                 // the apply vector (all levels + top)
   double* d_yf = nullptr;                // fine parts y_f of every cluster (forward -> backward)
   double* d_parts = nullptr;
+  double* d_contrib = nullptr;           // forward contributions (pull sweep), all levels
+  int64_t contrib_total = 0;
   int32_t* d_ctr = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;

@@ -102,13 +102,19 @@ ApplyLevelArgs level_args(hs_factor_s* f, int l) {
   a.src = P.d_src;
   a.ftask = P.d_ftask;
   a.ftgt = P.d_ftgt;
+  a.pull = P.d_pull;
+  a.ctb = P.d_ctb;
+  a.contrib = ap.d_contrib + P.contrib_off;
+  a.post_cl = P.d_post_cl;
+  a.npost = (int32_t)P.post_cl.size();
   a.btask = P.d_btask;
   a.bnb = P.d_bnb;
   a.parts = ap.d_parts;
   a.cnt = ap.d_ctr + P.ctr_off;
   a.bcnt = a.cnt + n;
   a.done = a.cnt + 2 * n;
-  a.ticket = a.cnt + 3 * n;
+  a.arr = a.cnt + 3 * n;
+  a.ticket = a.cnt + 4 * n;
   a.nftask = (int32_t)P.ftask.size();
   a.nbtask = (int32_t)P.btask.size();
   return a;
@@ -133,6 +139,7 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   for (int l = 0; l < an->L_top; ++l) {
     mark();
     launch_apply_fwd_level(level_args(f, l), st);
+    launch_apply_post_level(level_args(f, l), st);
   }
   mark();
   if (f->ntop > 0) launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);

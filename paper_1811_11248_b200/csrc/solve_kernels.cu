@@ -36,16 +36,41 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 constexpr int NB_SMEM = 512;   // neighbour tables up to this size are staged in shared memory
 
 // Forward sweep of one level (Algorithm 2 lines 3-6 for every cluster of the level, in the
-// batch order of the factor).  Task (s, targets [t_begin, t_end)):
-//   wait until y_s is final (its `pre` forward events applied);
-//   z = T_s y_s (rows r..m-1 only unless `first`): the first task of s writes the coarse
-//   part z[0:r] to the parent vector and y_f = z[r:m] to the fine buffer (event `pre` on s);
-//   for every target q (one warp each): wait for q's earlier events, y_q -= C_s[:, q]^T y_f.
-// Every vector entry is updated in a fixed order (the event sequence), so the sweep is
-// deterministic.
+// batch order of the factor), produce-then-pull.  Two task kinds, ticketed in elimination
+// order (a task only waits on tasks with smaller tickets, held by running CTAs):
+//   T(s): wait until every contribution to y_s from sources eliminated before s has
+//         arrived (arr[s]), y_s -= those contributions in elimination order, z = T_s y_s,
+//         coarse part z[0:r] -> parent vector, y_f = z[r:m] -> fine buffer, publish cnt[s];
+//   P(s, group): wait for cnt[s], then contrib(s -> q) = C_s[:, cols(q)]^T y_f for the
+//         group's targets (a warp per target), count them into arr[q].
+// The contributions to clusters eliminated before their source (their coarse parts) are
+// subtracted by k_apply_post after the level.  Every entry is accumulated in the factor's
+// event order, so the sweep is deterministic and equal to the sequential Algorithm 2 loop;
+// no target waits on another target's update.
+constexpr int PRE_SMEM = 1024;   // pre-contribution slots staged in shared memory
+
+__device__ __forceinline__ void produce(const ApplyLevelArgs& a, const ApplySrc& S, int K, const double* zf, int g0,
+                                        int g1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = APPLY_THREADS / 32;
+  for (int g = g0 + warp; g < g1; g += nw) {
+    const Contrib c = a.ctb[g];
+    for (int i = lane; i < c.len; i += 32) {
+      const double* Ci = S.C + c.col + i;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * zf[k];
+      a.contrib[c.slot + i] = acc;
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && c.pre) atomicAdd(a.arr + c.q, 1);
+  }
+}
+
 __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
   __shared__ double ys[MAX_M];
   __shared__ double z[MAX_M];
+  __shared__ int64_t pslot[PRE_SMEM];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
   for (;;) {
@@ -54,52 +79,74 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
     const int t = s_task;
     if (t >= a.nftask) return;
     const FwdTask tk = a.ftask[t];
-    const ApplySrc S = a.src[tk.s];
+    const int s = tk.s;
+    const ApplySrc S = a.src[s];
     const int m = S.m, r = S.r, K = m - r;
-    const int row0 = tk.first ? 0 : r;
-    // prefetch this task's rows of T_s and the targets' columns of C_s while y_s completes
-    for (int e = tid * 16; e < (m - row0) * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + (int64_t)row0 * m + e);
-    if (tk.t_end > tk.t_begin) {
-      const FwdTgt t0 = a.ftgt[tk.t_begin], t1 = a.ftgt[tk.t_end - 1];
-      const int cb = t0.col, ce = t1.col + t1.len;
-      for (int k = warp; k < K; k += nw)
-        for (int c = cb + lane * 16; c < ce; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
-    }
-    if (tid == 0) wait_ge(a.cnt + tk.s, S.pre);
-    __syncthreads();
-    for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
-    __syncthreads();
-    for (int i = row0 + warp; i < m; i += nw) {
-      const double* Ti = S.T + (int64_t)i * m;
-      double acc = 0.0;
-      for (int j = lane; j < m; j += 32) acc += Ti[j] * ys[j];
-      acc = wsum(acc);
-      if (lane == 0) z[i] = acc;
-    }
-    __syncthreads();
-    if (tk.first) {
+    if (tk.first) {   // ---- T(s) and s's first contribution group
+      for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
+      if (tk.t_end > tk.t_begin) {
+        const Contrib c0 = a.ctb[tk.t_begin], c1 = a.ctb[tk.t_end - 1];
+        for (int k = warp; k < K; k += nw)
+          for (int c = c0.col + lane * 16; c < c1.col + c1.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
+      }
+      const int npre = S.pre_end - S.pre_begin;
+      const bool staged = npre <= PRE_SMEM;
+      if (staged)
+        for (int e = tid; e < npre; e += APPLY_THREADS) pslot[e] = a.pull[S.pre_begin + e].slot;
+      if (tid == 0) wait_ge(a.arr + s, npre);
+      __syncthreads();
+      for (int i = tid; i < m; i += APPLY_THREADS) {
+        double v = __ldcg(S.y + i);
+        int e = 0;
+        for (; e + 8 <= npre; e += 8) {   // 8 loads in flight, subtracted in order
+          double c[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            c[u] = __ldcg(a.contrib + (staged ? pslot[e + u] : a.pull[S.pre_begin + e + u].slot) + i);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v -= c[u];
+        }
+        for (; e < npre; ++e) v -= __ldcg(a.contrib + (staged ? pslot[e] : a.pull[S.pre_begin + e].slot) + i);
+        ys[i] = v;
+      }
+      __syncthreads();
+      for (int i = warp; i < m; i += nw) {
+        const double* Ti = S.T + (int64_t)i * m;
+        double acc = 0.0;
+        for (int j = lane; j < m; j += 32) acc += Ti[j] * ys[j];
+        acc = wsum(acc);
+        if (lane == 0) z[i] = acc;
+      }
+      __syncthreads();
       for (int i = tid; i < r; i += APPLY_THREADS) S.yc[i] = z[i];
       for (int k = tid; k < K; k += APPLY_THREADS) S.yf[k] = z[r + k];
       __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(a.cnt + tk.s, 1);
-    }
-    for (int g = tk.t_begin + warp; g < tk.t_end; g += nw) {
-      const FwdTgt q = a.ftgt[g];
-      if (lane == 0) wait_ge(a.cnt + q.q, q.seq);
-      __syncwarp();
-      for (int i = lane; i < q.len; i += 32) {
-        const double* Ci = S.C + q.col + i;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int k = 0; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * z[r + k];
-        q.y[i] = __ldcg(q.y + i) - acc;
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(a.cnt + q.q, 1);
+      if (tid == 0) atomicExch(a.cnt + s, 1);
+      produce(a, S, K, z + r, tk.t_begin, tk.t_end);
+    } else {          // ---- P(s, group)
+      const Contrib c0 = a.ctb[tk.t_begin], c1 = a.ctb[tk.t_end - 1];
+      for (int k = warp; k < K; k += nw)
+        for (int c = c0.col + lane * 16; c < c1.col + c1.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
+      if (tid == 0) wait_ge(a.cnt + s, 1);
+      __syncthreads();
+      for (int k = tid; k < K; k += APPLY_THREADS) z[k] = __ldcg(S.yf + k);
+      __syncthreads();
+      produce(a, S, K, z, tk.t_begin, tk.t_end);
     }
     __syncthreads();   // s_task, ys, z reusable
+  }
+}
+
+// Contributions to the coarse parts of clusters eliminated before their sources
+// (Algorithm 2: y_q -= C^T y_f for processed q), every one of the level being final.
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_post(ApplyLevelArgs a) {
+  const int q = a.post_cl[blockIdx.x];
+  const ApplySrc Q = a.src[q];
+  for (int i = threadIdx.x; i < Q.r; i += APPLY_THREADS) {
+    double v = Q.yc[i];
+    for (int e = Q.post_begin; e < Q.post_end; ++e) v -= a.contrib[a.pull[e].slot + i];
+    Q.yc[i] = v;
   }
 }
 
@@ -252,6 +299,11 @@ static int apply_grid(const void* fn, int ntask) {
 void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
   if (a.nftask <= 0) return;
   k_apply_fwd<<<apply_grid((const void*)k_apply_fwd, a.nftask), APPLY_THREADS, 0, st>>>(a);
+  count_launch(1);
+}
+void launch_apply_post_level(const ApplyLevelArgs& a, cudaStream_t st) {
+  if (a.npost <= 0) return;
+  k_apply_post<<<a.npost, APPLY_THREADS, 0, st>>>(a);
   count_launch(1);
 }
 void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
