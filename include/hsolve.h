@@ -177,8 +177,12 @@ const char* hs_last_error(hs_handle h);     /* never NULL; h may be NULL (global
 const char* hs_status_string(hs_status s);
 
 /* ---- analyze (host, integer; bit-exact with the oracle) --------------------------- */
-/* coords: n*coord_dim row-major, or NULL (then the graph partitioner is required,
- * which is not implemented yet -> HS_E_UNSUPPORTED).  column_id: n entries or NULL. */
+/* coords: n*coord_dim row-major (recursive coordinate bisection), or NULL:
+ * coordinate-free recursive BFS bisection of the matrix graph (NEXT f4; the
+ * paper's "algebraic" clustering): at every tree node a BFS of the induced
+ * subgraph from its smallest unit finds a pseudo-peripheral unit g, the BFS order from g
+ * is split into its first ceil(|I|/2) units (left) and the rest.  column_id: n entries or
+ * NULL (with column_id, coordinates are required: HS_E_UNSUPPORTED otherwise). */
 hs_status hs_analyze(hs_handle h, int64_t n, const int64_t* rowptr, const int32_t* colind,
                      const double* coords, int32_t coord_dim, const int32_t* column_id,
                      const hs_analyze_opts* opt, hs_analysis* out);

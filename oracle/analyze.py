@@ -97,10 +97,80 @@ def rcb(ucoord: np.ndarray, D: int):
     return leaf
 
 
+def _bfs_order(I_sorted, inset, rowptr, colind, start):
+    """BFS over the subgraph induced by the unit set I (membership mask `inset`),
+    neighbours in ascending id, restarting from the smallest unvisited unit of I when a
+    component is exhausted."""
+    from collections import deque
+    seen = {start}
+    order = [start]
+    q = deque([start])
+    nxt_start = 0
+    while len(order) < len(I_sorted):
+        if not q:
+            while I_sorted[nxt_start] in seen:
+                nxt_start += 1
+            v = int(I_sorted[nxt_start])
+            seen.add(v)
+            order.append(v)
+            q.append(v)
+        u = q.popleft()
+        for w in colind[rowptr[u]:rowptr[u + 1]]:      # CSR rows are sorted: ascending id
+            w = int(w)
+            if inset[w] and w not in seen:
+                seen.add(w)
+                order.append(w)
+                q.append(w)
+    return order
+
+
+def gbisect(n, rowptr, colind, D):
+    """O2.3 without coordinates (NEXT f4; SPEC S:202 "recursive BFS level-set bisection";
+    the paper's clustering is "algebraic").  Perfect binary tree to depth D.
+    At a node with unit set I (ascending):
+      1. BFS on the subgraph induced by I from min(I) (restarting as in _bfs_order); its
+         last unit g is a pseudo-peripheral start;
+      2. order = the same BFS from g;
+      3. left child = the first ceil(|I|/2) units of the order, right child = the rest.
+    Returns the leaf of every unit (units are DOFs)."""
+    leaf = np.zeros(n, dtype=np.int64)
+    inset = np.zeros(n, dtype=bool)
+    nodes = [np.arange(n, dtype=np.int64)]
+    for depth in range(D):
+        nxt = []
+        for I in nodes:
+            if I.size == 0:
+                nxt += [I, I]
+                continue
+            inset[I] = True
+            first = _bfs_order(I, inset, rowptr, colind, int(I[0]))
+            order = _bfs_order(I, inset, rowptr, colind, first[-1])
+            inset[I] = False
+            order = np.asarray(order, dtype=np.int64)
+            h = (order.size + 1) // 2
+            nxt.append(np.sort(order[:h]))
+            nxt.append(np.sort(order[h:]))
+        nodes = nxt
+    for x, I in enumerate(nodes):
+        leaf[I] = x
+    return leaf
+
+
 def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_columns=0,
             top_log2=3, nsub_log2=3) -> Analysis:
     rowptr = np.asarray(rowptr, dtype=np.int64)
     colind = np.asarray(colind, dtype=np.int64)
+    if coords is None:
+        if column_id is not None:
+            raise ValueError("graph bisection works on DOF units (no column_id)")
+        U = n
+        leaf_units = leaf_size
+        if leaf_units <= 0:
+            raise ValueError("leaf size must be positive")
+        D = 0
+        while -(-U // (1 << D)) > leaf_units:
+            D += 1
+        return _schedule(n, rowptr, colind, gbisect(n, rowptr, colind, D), D, top_log2, nsub_log2)
     ucoord, unit_of_dof = _units(n, coords, column_id)
     U = ucoord.shape[0]
     leaf_units = leaf_columns if column_id is not None else leaf_size
@@ -112,6 +182,10 @@ def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_column
         D += 1
     uleaf = rcb(ucoord, D)
     dof_leaf = uleaf if unit_of_dof is None else uleaf[unit_of_dof]
+    return _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2)
+
+
+def _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2) -> Analysis:
     # O2.4 permutation: leaves left to right, DOFs ascending inside a leaf
     perm = np.lexsort((np.arange(n), dof_leaf)).astype(np.int64)
     nleaf = 1 << D

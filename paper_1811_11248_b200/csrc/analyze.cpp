@@ -43,8 +43,8 @@ void merge_into(std::vector<int32_t>& dst, const std::vector<int32_t>& src, int3
 Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
                   int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts& opt) {
   if (n <= 0 || !rowptr || !colind) fail(HS_E_INVALID_ARG, "analyze: empty matrix or NULL pattern");
-  if (!coords || coord_dim <= 0)
-    fail(HS_E_UNSUPPORTED, "analyze: coordinate-free (graph) partitioning is not implemented (NEXT f4)");
+  const bool graph = !coords || coord_dim <= 0;   // coordinate-free: graph bisection (NEXT f4)
+  if (graph && column_id) fail(HS_E_UNSUPPORTED, "analyze: graph bisection works on DOF units (no column_id)");
   if (opt.top_log2 < 0 || opt.nsub_log2 < 0 || opt.nsub_log2 > opt.top_log2)
     fail(HS_E_INVALID_ARG, "analyze: need 0 <= nsub_log2 <= top_log2");
   const int64_t nnz = rowptr[n];
@@ -73,7 +73,10 @@ Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const
   std::vector<double> uc;              // unit coordinates, row-major [U][dims]
   std::vector<int64_t> unit_of_dof;    // empty when units are DOFs
   int64_t U;
-  if (!column_id) {
+  if (graph) {
+    U = n;
+    dims = 0;
+  } else if (!column_id) {
     U = n;
     dims = coord_dim;
     uc.assign(coords, coords + n * coord_dim);
@@ -106,11 +109,65 @@ Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const
   while (((U + (int64_t(1) << D) - 1) >> D) > leaf_units) ++D;
   if (D > 30) fail(HS_E_UNSUPPORTED, "analyze: tree too deep");
   an->D = D;
-  // ---- RCB (O2.3) ---------------------------------------------------------------------
+  // ---- RCB (O2.3), or recursive BFS bisection without coordinates ----------------------
   std::vector<std::vector<int64_t>> nodes(1);
   nodes[0].resize(U);
   std::iota(nodes[0].begin(), nodes[0].end(), 0);
-  for (int d = 0; d < D; ++d) {
+  if (graph) {
+    // At a node with unit set I (ascending): BFS on the induced subgraph from min(I)
+    // (neighbours in ascending id, restarting from the smallest unvisited unit when a
+    // component is exhausted); from its last unit g the same BFS gives the order; the left
+    // child takes the first ceil(|I|/2) units (the paper's "algebraic"
+    // clustering P:483-485).
+    std::vector<uint8_t> inset(n, 0), seen(n, 0);
+    std::vector<int64_t> order, queue;
+    auto bfs = [&](const std::vector<int64_t>& I, int64_t start) {
+      order.clear();
+      queue.clear();
+      size_t qh = 0, nxt_start = 0;
+      seen[start] = 1;
+      order.push_back(start);
+      queue.push_back(start);
+      while (order.size() < I.size()) {
+        if (qh == queue.size()) {
+          while (seen[I[nxt_start]]) ++nxt_start;
+          const int64_t v = I[nxt_start];
+          seen[v] = 1;
+          order.push_back(v);
+          queue.push_back(v);
+        }
+        const int64_t u = queue[qh++];
+        for (int64_t k = rowptr[u]; k < rowptr[u + 1]; ++k) {
+          const int64_t w = colind[k];
+          if (inset[w] && !seen[w]) {
+            seen[w] = 1;
+            order.push_back(w);
+            queue.push_back(w);
+          }
+        }
+      }
+      for (int64_t v : order) seen[v] = 0;
+    };
+    for (int d = 0; d < D; ++d) {
+      std::vector<std::vector<int64_t>> nxt(nodes.size() * 2);
+      for (size_t x = 0; x < nodes.size(); ++x) {
+        const auto& I = nodes[x];
+        if (I.empty()) continue;
+        for (int64_t u : I) inset[u] = 1;
+        bfs(I, I[0]);
+        const int64_t g = order.back();
+        bfs(I, g);
+        for (int64_t u : I) inset[u] = 0;
+        const size_t h = (I.size() + 1) / 2;
+        nxt[2 * x].assign(order.begin(), order.begin() + h);
+        nxt[2 * x + 1].assign(order.begin() + h, order.end());
+        std::sort(nxt[2 * x].begin(), nxt[2 * x].end());
+        std::sort(nxt[2 * x + 1].begin(), nxt[2 * x + 1].end());
+      }
+      nodes.swap(nxt);
+    }
+  }
+  for (int d = 0; d < (graph ? 0 : D); ++d) {
     std::vector<std::vector<int64_t>> nxt(nodes.size() * 2);
     for (size_t x = 0; x < nodes.size(); ++x) {
       auto& I = nodes[x];

@@ -52,6 +52,24 @@ CASES = [
 ]
 
 
+def _NoCoords(p):
+    """The problem with its coordinates removed: analyze falls back to graph bisection."""
+    import copy
+    q = copy.copy(p)
+    q.coords, q.column_id, q.leaf_columns = None, None, 0
+    if not q.leaf_size:
+        q.leaf_size = 40
+    return q
+
+
+CASES += [
+    ("graph-C1", lambda: _NoCoords(gen_poisson2d(32)), {}),
+    ("graph-3d-16", lambda: _NoCoords(gen_laplace3d(16, leaf_size=16)), {}),
+    ("graph-aniso-ragged", lambda: _NoCoords(gen_poisson2d(23, 17, leaf_size=7)), dict(top_log2=2, nsub_log2=1)),
+    ("graph-q1", lambda: _NoCoords(gen_stokes_q1(9, 7, 3, leaf_columns=2)), {}),
+]
+
+
 @pytest.mark.parametrize("name,gen,kw", CASES, ids=[c[0] for c in CASES])
 def test_analyze_bit_exact(name, gen, kw):
     p = gen()
@@ -81,8 +99,9 @@ def test_analyze_bit_exact(name, gen, kw):
 
 def test_analyze_errors():
     p = gen_poisson2d(8)
-    with pytest.raises(H.HSError) as ei:
-        H.hs_analyze(None, p.n, p.rowptr, p.colind, None, None, leaf_size=4)
+    with pytest.raises(H.HSError) as ei:   # graph bisection needs DOF units
+        H.hs_analyze(None, p.n, p.rowptr, p.colind, None, np.zeros(p.n, dtype=np.int32), leaf_size=4,
+                     leaf_columns=2)
     assert ei.value.status == H.HS_E_UNSUPPORTED
     with pytest.raises(H.HSError) as ei:
         H.hs_analyze(None, p.n, p.rowptr, p.colind, p.coords, None, leaf_size=0)

@@ -120,7 +120,17 @@ def test_eps0_exact_cholesky(H, handle, name, gen, kw):
     assert rep["iters"] == 1 and rep["relres_true"] <= 1e-12
 
 
+def _NoCoords(p):
+    """The problem without coordinates: analyze uses graph bisection (NEXT f4)."""
+    import copy
+    q = copy.copy(p)
+    q.coords, q.column_id, q.leaf_columns = None, None, 0
+    return q
+
+
 CASES = TINY + [
+    ("graph-3d-16", lambda: _NoCoords(gen_laplace3d(16, leaf_size=16)), {}),
+    ("graph-C1", lambda: _NoCoords(gen_poisson2d(32)), {}),
     ("aniso2d-ragged", lambda: gen_poisson2d(23, 17, aniso=1e-3, leaf_size=7), dict(top_log2=2, nsub_log2=1)),
     ("3d-24", lambda: gen_laplace3d(24, leaf_size=27), {}),
     ("slab-32", lambda: gen_slab(32, 6, leaf_columns=4), {}),

@@ -125,3 +125,45 @@ def test_depth_rule_and_empty_children():
     assert an.leaf_off[-1] == 10 and np.all(np.diff(an.leaf_off) <= 3)
     an1 = analyze(p.n, p.rowptr, p.colind, p.coords, None, leaf_size=1)
     assert an1.D == 4 and (np.diff(an1.leaf_off) == 0).sum() == 6
+
+
+def test_graph_bisection_path_closed_form():
+    """Pin of the coordinate-free tree (NEXT f4): on a path graph the BFS from min(I)
+    ends at max(I), the BFS from there lists I in descending order, so every node splits
+    into its upper and lower halves and every leaf is a contiguous index range."""
+    import scipy.sparse as sp
+    from oracle.analyze import gbisect
+    n, D = 96, 4
+    A = sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1]).tocsr()
+    leaf = gbisect(n, A.indptr.astype(np.int64), A.indices.astype(np.int64), D)
+    # leaf 0 = the top of the index range (left child = first half of the descending BFS)
+    expect = np.zeros(n, dtype=np.int64)
+    lo, hi = [0], [n]
+    nodes = [np.arange(n)]
+    for _ in range(D):
+        nxt = []
+        for I in nodes:
+            h = (I.size + 1) // 2
+            desc = I[::-1]
+            nxt += [np.sort(desc[:h]), np.sort(desc[h:])]
+        nodes = nxt
+    for x, I in enumerate(nodes):
+        expect[I] = x
+    assert np.array_equal(leaf, expect)
+    for x in range(1 << D):   # contiguous leaves of 6 DOFs
+        idx = np.nonzero(leaf == x)[0]
+        assert idx.size == 6 and np.all(np.diff(idx) == 1)
+
+
+def test_graph_bisection_disconnected_and_balanced():
+    """Two disjoint grids: the BFS restarts on the unvisited component; every tree node
+    splits into ceil/floor halves (perfect binary tree, O2.2)."""
+    import scipy.sparse as sp
+    from oracle.analyze import gbisect
+    p = gen_poisson2d(6)
+    A = p.to_scipy()
+    B = sp.block_diag([A, A]).tocsr()
+    n = B.shape[0]
+    leaf = gbisect(n, B.indptr.astype(np.int64), B.indices.astype(np.int64), 3)
+    counts = np.bincount(leaf, minlength=8)
+    assert counts.sum() == n and counts.max() - counts.min() <= 1
