@@ -233,6 +233,12 @@ hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device);
  * x and rep. */
 hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t maxit,
                  int32_t on_device, hs_pcg_report* rep);
+/* Right-preconditioned restarted GMRES(restart) with M = the factor -- the paper's Krylov
+ * protocol (GMRES(200), tol 1e-12, maxit 1000; NEXT f3).  x0 = 0; stops when the
+ * recurrence residual |g_{j+1}| / ||b|| <= tol; rep->iters = Arnoldi steps, t_pcg_s = the
+ * solve's device time.  HS_E_NOT_CONVERGED still fills x and rep. */
+hs_status hs_gmres(hs_factor f, const double* b, double* x, double tol, int32_t restart, int32_t maxit,
+                   int32_t on_device, hs_pcg_report* rep);
 /* y = A x with the factor's CSR (device SpMV); helper for tests and the bench. */
 hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device);
 

@@ -130,3 +130,69 @@ def pcg(A, b, precond, tol=1e-8, maxit=1000):
         rho = rho2
     true = float(np.linalg.norm(b - A @ x)) / nb
     return x, PCGReport(k, conv, hist[-1], true, hist)
+
+
+@dataclasses.dataclass
+class GMRESReport:
+    iters: int              # Arnoldi steps (one A M^{-1} product each)
+    converged: bool
+    relres: float           # recurrence |g_{j+1}| / ||b||
+    relres_true: float      # ||b - A x|| / ||b||
+    restarts: int
+
+
+def gmres(A, b, precond, tol=1e-12, restart=200, maxit=1000):
+    """Right-preconditioned restarted GMRES — the paper's Krylov protocol: GMRES(200),
+    tolerance 1e-12, at most 1000 iterations (NEXT f3).  Textbook form (Saad,
+    "Iterative Methods for Sparse Linear Systems", Alg. 9.5 with the modified Gram-Schmidt
+    Arnoldi of Alg. 6.2 and Givens rotations, Sec. 6.5.3): x0 = 0; solve A M^{-1} u = b,
+    x = M^{-1} u; stop when |g_{j+1}| / ||b|| <= tol or after maxit Arnoldi steps."""
+    b = np.asarray(b, dtype=np.float64)
+    n = b.shape[0]
+    x = np.zeros(n)
+    nb = float(np.linalg.norm(b))
+    if nb == 0.0:
+        return x, GMRESReport(0, True, 0.0, 0.0, 0)
+    its, restarts, rel = 0, 0, 1.0
+    while True:
+        r = b - A @ x
+        beta = float(np.linalg.norm(r))
+        rel = beta / nb
+        if rel <= tol or its >= maxit:
+            break
+        V = [r / beta]
+        H = np.zeros((restart + 1, restart))
+        g = np.zeros(restart + 1)
+        g[0] = beta
+        cs, sn = np.zeros(restart), np.zeros(restart)
+        k = 0
+        for j in range(restart):
+            its += 1
+            w = A @ precond(V[j])
+            for i in range(j + 1):                  # modified Gram-Schmidt
+                H[i, j] = w @ V[i]
+                w = w - H[i, j] * V[i]
+            hn = float(np.linalg.norm(w))
+            H[j + 1, j] = hn
+            for i in range(j):                      # previous rotations
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = np.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = (1.0, 0.0) if den == 0.0 else (H[j, j] / den, H[j + 1, j] / den)
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            k = j + 1
+            rel = abs(g[j + 1]) / nb
+            if rel <= tol or its >= maxit or hn == 0.0:
+                break
+            V.append(w / hn)
+        y = sla.solve_triangular(H[:k, :k], g[:k], lower=False)
+        x = x + precond(np.column_stack(V[:k]) @ y)
+        restarts += 1
+        if rel <= tol or its >= maxit:
+            break
+    rt = float(np.linalg.norm(b - A @ x)) / nb
+    return x, GMRESReport(its, rel <= tol, rel, rt, restarts)

@@ -483,4 +483,37 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
   return s != HS_OK ? s : s_inner;
 }
 
+hs_status hs_gmres(hs_factor f, const double* b, double* x, double tol, int32_t restart, int32_t maxit,
+                   int32_t on_device, hs_pcg_report* rep) {
+  hs_status s_inner = HS_OK;
+  const hs_status s = guarded(f ? f->h : nullptr, [&] {
+    if (!f || !b || !x || !rep) hs::fail(HS_E_INVALID_ARG, "hs_gmres: NULL argument");
+    if (!(tol >= 0) || maxit < 0 || restart < 1) hs::fail(HS_E_INVALID_ARG, "hs_gmres: bad tol/restart/maxit");
+    if (f->h->world > 1 && f->h->rank != 0)
+      hs::fail(HS_E_UNSUPPORTED, "hs_gmres: the multi-GPU factor is solved on rank 0 (records gathered there)");
+    require_device(f->h);
+    cudaStream_t st = f->h->stream;
+    const int64_t n = f->an->n;
+    double* db = (double*)f->h->cache.alloc(sizeof(double) * n);
+    double* dx = (double*)f->h->cache.alloc(sizeof(double) * n);
+    io_in(f, b, db, on_device, st);
+    try {
+      hs::gmres(f, db, dx, tol, restart, maxit, rep);
+    } catch (const hs::Error& e) {
+      s_inner = e.status;
+      if (e.status != HS_E_NOT_CONVERGED) {
+        f->h->cache.free(db);
+        f->h->cache.free(dx);
+        throw;
+      }
+      f->h->err = e.what();
+    }
+    HS_CUDA(cudaMemcpyAsync(x, dx, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    f->h->cache.free(db);
+    f->h->cache.free(dx);
+  });
+  return s != HS_OK ? s : s_inner;
+}
+
 }  // extern "C"

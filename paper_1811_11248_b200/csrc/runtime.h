@@ -205,5 +205,6 @@ namespace hs {
 hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an, const double* values, const hs_factor_opts& opt);
 void apply(hs_factor_s* f, const double* d_b, double* d_x);         // device pointers
 void pcg(hs_factor_s* f, const double* d_b, double* d_x, double tol, int maxit, hs_pcg_report* rep);
+void gmres(hs_factor_s* f, const double* d_b, double* d_x, double tol, int restart, int maxit, hs_pcg_report* rep);
 void spmv(hs_factor_s* f, const double* d_x, double* d_y);
 }  // namespace hs

@@ -88,6 +88,38 @@ __global__ void k_sub(double* __restrict__ d, const double* __restrict__ a, cons
     d[i] = a[i] - b[i];
 }
 
+// ---- GMRES helpers (NEXT f3): V is column-major, column i at V + i*ldv -----------------
+// h[i] = <V_i, w> for i < ncol (a block per column, fixed-order reduction)
+__global__ void k_gemv_t(const double* __restrict__ V, int64_t ldv, const double* __restrict__ w, int64_t n,
+                         double* __restrict__ h) {
+  __shared__ double sh[32];
+  const double* v = V + (int64_t)blockIdx.x * ldv;
+  double acc = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) acc += v[k] * w[k];
+  acc = blk_sum(acc, sh);
+  if (threadIdx.x == 0) h[blockIdx.x] = acc;
+}
+// w += sign * V[:, :ncol] h
+__global__ void k_gemv_n(const double* __restrict__ V, int64_t ldv, int ncol, const double* __restrict__ h,
+                         double sign, double* __restrict__ w, int64_t n) {
+  extern __shared__ double hs_[];
+  for (int i = threadIdx.x; i < ncol; i += blockDim.x) hs_[i] = h[i];
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < ncol; ++i) acc += V[(int64_t)i * ldv + k] * hs_[i];
+    w[k] += sign * acc;
+  }
+}
+__global__ void k_scale(double* __restrict__ d, const double* __restrict__ s, double a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = a * s[i];
+}
+__global__ void k_axpy(double* __restrict__ x, const double* __restrict__ z, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += z[i];
+}
+
 void dot(const double* a, const double* b, int64_t n, double* partial, double* out, cudaStream_t st) {
   k_dot_partial<<<RED_BLOCKS, RED_THREADS, 0, st>>>(a, b, n, partial);
   k_finish<<<1, RED_THREADS, 0, st>>>(partial, RED_BLOCKS, out);
@@ -309,6 +341,139 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(a0); cudaEventDestroy(a1);
   if (err != HS_OK) fail(err, "pcg: <r, M^{-1} r> <= 0 (preconditioner not positive)");
   if (!rep->converged) fail(HS_E_NOT_CONVERGED, "pcg: not converged within maxit");
+}
+
+// Right-preconditioned restarted GMRES (NEXT f3; the paper's protocol: GMRES(200),
+// tol 1e-12, maxit 1000): x0 = 0, A M^{-1} u = b, x = M^{-1} u.  Arnoldi with classical
+// Gram-Schmidt applied twice (CGS2: two block projections per step instead of j dependent
+// dot products); the Hessenberg column, the Givens rotations and the small triangular
+// solve live on the host (one read of j+2 scalars per step).  Iterations = Arnoldi steps.
+void gmres(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int restart, int maxit,
+           hs_pcg_report* rep) {
+  cudaStream_t st = f->h->stream;
+  ensure_vectors(f);
+  const int64_t n = f->an->n;
+  const int G = RED_BLOCKS, T = RED_THREADS;
+  if (restart < 1) fail(HS_E_INVALID_ARG, "gmres: restart must be >= 1");
+  DevCache& dc = f->h->cache;
+  const int64_t ldv = (n + 31) & ~int64_t(31);
+  double* V = (double*)dc.alloc(sizeof(double) * ldv * (restart + 1));
+  double* x = (double*)dc.alloc(sizeof(double) * n);
+  double* w = (double*)dc.alloc(sizeof(double) * n);
+  double* dh = (double*)dc.alloc(sizeof(double) * (2 * (restart + 1) + 8));
+  std::vector<double> hh(2 * (restart + 1) + 8);
+  double* part = f->d_red;
+  double* sc = f->d_red + RED_BLOCKS;
+  cudaEvent_t e0, e1;
+  HS_CUDA(cudaEventCreate(&e0));
+  HS_CUDA(cudaEventCreate(&e1));
+  HS_CUDA(cudaEventRecord(e0, st));
+  auto norm2 = [&](const double* a) {   // blocking ||a||
+    dot(a, a, n, part, sc, st);
+    HS_CUDA(cudaMemcpyAsync(f->h_red, sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(std::max(f->h_red[0], 0.0));
+  };
+  auto apply_to = [&](const double* v, double* out) {   // out = M^{-1} v
+    HS_CUDA(cudaMemcpyAsync(f->d_b, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    run_apply_graph(f, st);
+    if (out != f->d_x) HS_CUDA(cudaMemcpyAsync(out, f->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  };
+  const size_t hsm = sizeof(double) * (restart + 1);
+  k_zero<<<G, T, 0, st>>>(x, n);
+  count_launch(1);
+  const double nb = norm2(d_bin);
+  int its = 0;
+  double rel = 1.0;
+  rep->iters = 0;
+  rep->converged = 0;
+  if (nb == 0.0) rel = 0.0;
+  while (nb > 0.0) {
+    // r = b - A x into V_0
+    launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, x, w, n, st);
+    k_sub<<<G, T, 0, st>>>(w, d_bin, w, n);
+    count_launch(1);
+    const double beta = norm2(w);
+    rel = beta / nb;
+    if (rel <= tol || its >= maxit || beta == 0.0) break;
+    k_scale<<<G, T, 0, st>>>(V, w, 1.0 / beta, n);
+    count_launch(1);
+    std::vector<double> H((size_t)(restart + 1) * restart, 0.0), g(restart + 1, 0.0), cs(restart), sn(restart);
+    auto Hij = [&](int i, int j) -> double& { return H[(size_t)i * restart + j]; };
+    g[0] = beta;
+    int k = 0;
+    for (int j = 0; j < restart; ++j) {
+      ++its;
+      apply_to(V + (int64_t)j * ldv, f->d_x);                              // z = M^{-1} v_j
+      launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, f->d_x, w, n, st);   // w = A z
+      for (int pass = 0; pass < 2; ++pass) {                                // CGS2
+        k_gemv_t<<<j + 1, T, 0, st>>>(V, ldv, w, n, dh + pass * (restart + 1));
+        k_gemv_n<<<G, T, hsm, st>>>(V, ldv, j + 1, dh + pass * (restart + 1), -1.0, w, n);
+        count_launch(2);
+      }
+      dot(w, w, n, part, dh + 2 * (restart + 1), st);
+      HS_CUDA(cudaMemcpyAsync(hh.data(), dh, sizeof(double) * (2 * (restart + 1) + 1), cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      for (int i = 0; i <= j; ++i) Hij(i, j) = hh[i] + hh[restart + 1 + i];
+      const double hn = std::sqrt(std::max(hh[2 * (restart + 1)], 0.0));
+      Hij(j + 1, j) = hn;
+      for (int i = 0; i < j; ++i) {   // previous rotations
+        const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
+        Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
+        Hij(i, j) = t;
+      }
+      const double den = std::hypot(Hij(j, j), Hij(j + 1, j));
+      cs[j] = den == 0.0 ? 1.0 : Hij(j, j) / den;
+      sn[j] = den == 0.0 ? 0.0 : Hij(j + 1, j) / den;
+      Hij(j, j) = den;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      k = j + 1;
+      rel = std::fabs(g[j + 1]) / nb;
+      if (rel <= tol || its >= maxit || hn == 0.0) break;
+      k_scale<<<G, T, 0, st>>>(V + (int64_t)(j + 1) * ldv, w, 1.0 / hn, n);
+      count_launch(1);
+    }
+    // y = H(0:k, 0:k)^{-1} g(0:k); x += M^{-1} V y
+    std::vector<double> y(k);
+    for (int i = k - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int c = i + 1; c < k; ++c) t -= Hij(i, c) * y[c];
+      y[i] = t / Hij(i, i);
+    }
+    HS_CUDA(cudaMemcpyAsync(dh, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    k_zero<<<G, T, 0, st>>>(w, n);
+    k_gemv_n<<<G, T, hsm, st>>>(V, ldv, k, dh, 1.0, w, n);
+    count_launch(2);
+    apply_to(w, f->d_x);
+    k_axpy<<<G, T, 0, st>>>(x, f->d_x, n);
+    count_launch(1);
+    HS_CUDA(cudaStreamSynchronize(st));   // y (pageable) consumed; dh reusable
+    if (rel <= tol || its >= maxit) break;
+  }
+  HS_CUDA(cudaEventRecord(e1, st));
+  HS_CUDA(cudaEventSynchronize(e1));
+  float ms;
+  HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  rep->t_pcg_s = ms * 1e-3;
+  rep->t_apply_s = 0.0;
+  rep->t_spmv_s = 0.0;
+  rep->iters = its;
+  rep->relres = rel;
+  rep->converged = rel <= tol ? 1 : 0;
+  // true residual
+  launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, x, w, n, st);
+  k_sub<<<G, T, 0, st>>>(w, d_bin, w, n);
+  count_launch(1);
+  const double rn = norm2(w);
+  rep->relres_true = nb > 0 ? rn / nb : 0.0;
+  HS_CUDA(cudaMemcpyAsync(d_xout, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (void* p : {(void*)V, (void*)x, (void*)w, (void*)dh}) dc.free(p);
+  if (!rep->converged) fail(HS_E_NOT_CONVERGED, "gmres: not converged within maxit");
 }
 
 }  // namespace hs

@@ -35,7 +35,7 @@ HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(
 SYMBOLS = ["hs_create", "hs_nccl_unique_id", "hs_loopback_world_create", "hs_loopback_world_destroy",
            "hs_create_loopback", "hs_set_stream", "hs_destroy", "hs_last_error", "hs_status_string", "hs_analyze",
            "hs_analysis_get_info", "hs_analysis_export", "hs_dist_plan_export", "hs_analysis_destroy", "hs_factor_create",
-           "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply",
+           "hs_factor_get_stats", "hs_factor_export", "hs_factor_export_cluster", "hs_factor_destroy", "hs_apply", "hs_gmres",
            "hs_pcg", "hs_spmv", "hs_launch_count"]
 HS_CEXP_SHAPE, HS_CEXP_G, HS_CEXP_V, HS_CEXP_TAU, HS_CEXP_B = range(5)
 
@@ -132,6 +132,7 @@ def lib():
         L.hs_factor_destroy.restype = None
         L.hs_apply.argtypes = [vp, vp, vp, i32]
         L.hs_pcg.argtypes = [vp, vp, vp, dp, i32, i32, C.POINTER(hs_pcg_report)]
+        L.hs_gmres.argtypes = [vp, vp, vp, dp, i32, i32, i32, C.POINTER(hs_pcg_report)]
         L.hs_spmv.argtypes = [vp, vp, vp, i32]
         L.hs_launch_count.argtypes = []
         L.hs_launch_count.restype = i64
@@ -358,6 +359,22 @@ def hs_pcg(f: Factor, b, tol=1e-8, maxit=1000, x=None, raise_not_converged=True)
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.empty_like(b) if x is None else x
         st = lib().hs_pcg(f.ptr, b.ctypes.data, x.ctypes.data, tol, maxit, 0, C.byref(rep))
+    if st == HS_E_NOT_CONVERGED and not raise_not_converged:
+        return x, rep.as_dict()
+    _check(st, f.handle.ptr)
+    return x, rep.as_dict()
+
+
+def hs_gmres(f: Factor, b, tol=1e-12, restart=200, maxit=1000, x=None, raise_not_converged=True):
+    """Right-preconditioned GMRES(restart) with M = the factor.  Returns (x, report)."""
+    rep = hs_pcg_report()
+    if hasattr(b, "is_cuda") and b.is_cuda:
+        x = b.new_empty(b.shape) if x is None else x
+        st = lib().hs_gmres(f.ptr, _ptr(b)[0], _ptr(x)[0], tol, restart, maxit, 1, C.byref(rep))
+    else:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b) if x is None else x
+        st = lib().hs_gmres(f.ptr, b.ctypes.data, x.ctypes.data, tol, restart, maxit, 0, C.byref(rep))
     if st == HS_E_NOT_CONVERGED and not raise_not_converged:
         return x, rep.as_dict()
     _check(st, f.handle.ptr)

@@ -199,3 +199,21 @@ def test_empty_leaves_and_tiny(H, handle):
     an, _, a, f, _ = _both(H, handle, p, 0.0, dict(top_log2=1, nsub_log2=1))
     A = p.to_scipy().toarray()
     assert np.linalg.norm(H.hs_apply(f, p.b) - np.linalg.solve(A, p.b)) <= 1e-12 * np.linalg.norm(np.linalg.solve(A, p.b))
+
+
+@pytest.mark.parametrize("name,gen,kw", [CASES[0], CASES[7], CASES[9]], ids=[CASES[0][0], CASES[7][0], CASES[9][0]])
+def test_gmres_parity(H, handle, name, gen, kw):
+    """NEXT f3: the paper's Krylov protocol (right-preconditioned GMRES(200), tol 1e-12,
+    P:810) on the GPU against the oracle's textbook GMRES with the oracle's factor."""
+    from oracle.solve import gmres as ogmres
+    p = gen()
+    an, fac, a, f, flagged = _both(H, handle, p, 1e-2, kw)
+    xo, ro = ogmres(p.to_scipy(), p.b, lambda r: oapply(fac, r), tol=1e-12, restart=200, maxit=1000)
+    xg, rg = H.hs_gmres(f, p.b, tol=1e-12, restart=200, maxit=1000)
+    assert ro.converged and rg["converged"]
+    assert abs(rg["iters"] - ro.iters) <= 1
+    assert np.linalg.norm(xg - xo) <= 1e-8 * np.linalg.norm(xo)
+    assert rg["relres_true"] <= 1e-10
+    # a short restart still converges (restarted path)
+    xr, rr = H.hs_gmres(f, p.b, tol=1e-10, restart=2, maxit=1000)
+    assert rr["converged"] and rr["relres_true"] <= 1e-8

@@ -165,3 +165,43 @@ def test_eps_error_decreases():
         errs.append(np.linalg.norm(np.eye(p.n) - MA, 2))
     assert errs[0] > errs[1] > errs[2]
     assert errs[2] < 1e-2
+
+
+def test_gmres_minimal_residual_pin():
+    """Pin of the oracle GMRES (NEXT f3): after k Arnoldi steps from x0 = 0 the iterate
+    minimises ||b - A M^{-1} u|| over the Krylov space K_k(A M^{-1}, b) -- checked against
+    a brute-force least-squares solve over an explicitly built, QR-orthonormalised Krylov
+    basis (no Arnoldi, no Givens); with the exact inverse as preconditioner it stops after
+    one step."""
+    import scipy.sparse.linalg as spla
+    from oracle.solve import gmres
+    p = gen_poisson2d(8, leaf_size=4)
+    A = p.to_scipy()
+    b = p.b
+    D = A.diagonal()
+    M = lambda v: v / D                               # Jacobi
+    AM = lambda v: A @ M(v)
+    for k in range(1, 7):
+        x, rep = gmres(A, b, M, tol=1e-300, restart=50, maxit=k)
+        K = np.zeros((b.size, k))
+        v = b.copy()
+        for i in range(k):
+            K[:, i] = v
+            v = AM(v)
+        Q, _ = np.linalg.qr(K)
+        AQ = np.column_stack([AM(Q[:, i]) for i in range(k)])
+        c, *_ = np.linalg.lstsq(AQ, b, rcond=None)
+        best = np.linalg.norm(b - AQ @ c)
+        assert rep.iters == k
+        assert abs(np.linalg.norm(b - A @ x) - best) <= 1e-10 * np.linalg.norm(b)
+    lu = spla.splu(A.tocsc())
+    x, rep = gmres(A, b, lu.solve, tol=1e-12)
+    assert rep.iters == 1 and rep.converged and rep.relres_true <= 1e-12
+
+
+def test_gmres_restart_converges():
+    from oracle.solve import gmres
+    p = gen_poisson2d(12, leaf_size=4)
+    A = p.to_scipy()
+    x, rep = gmres(A, p.b, lambda v: v, tol=1e-10, restart=5, maxit=2000)
+    assert rep.converged and rep.restarts > 1 and rep.relres_true <= 1e-9
