@@ -6,7 +6,7 @@ sparse SPD operators, coordinates, extruded column ids and right-hand sides
 that both the oracle and the CUDA path consume.  See DESIGN.md "Input recipe".
 """
 from .generators import (Problem, gen_poisson2d, gen_laplace3d, gen_slab,
-                         gen_stokes_q1, gen_config, grf, rhs, CONFIGS)
+                         gen_stokes_q1, gen_config, gen_family, grf, rhs, CONFIGS)
 
 __all__ = ["Problem", "gen_poisson2d", "gen_laplace3d", "gen_slab",
-           "gen_stokes_q1", "gen_config", "grf", "rhs", "CONFIGS"]
+           "gen_stokes_q1", "gen_config", "gen_family", "grf", "rhs", "CONFIGS"]

@@ -380,3 +380,14 @@ def gen_config_scaled(name: str, scale: int) -> Problem:
     if name == "C2":
         return gen_laplace3d(64 // scale)
     raise KeyError(name)
+
+
+def gen_family(layers: int, level: int, base: int = 32) -> Problem:
+    """NEXT f2: weak-scaling family of the config-4 operator at a fixed number of element
+    layers (the paper's 6- and 11-layer Antarctica families, Tables `ilu` / `10layers`,
+    P:920-1007): (base 2^level)^2 horizontal nodes x (layers + 1) node layers x 2 DOF;
+    each level has 4x the DOFs of the previous one.  Same fields, leaf (2 columns), eps,
+    tol and domain aspect ratio as C4."""
+    n = base << level
+    return gen_stokes_q1(n, n, layers + 1, aspect=1e3, leaf_columns=2)
+

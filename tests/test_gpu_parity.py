@@ -217,3 +217,26 @@ def test_gmres_parity(H, handle, name, gen, kw):
     # a short restart still converges (restarted path)
     xr, rr = H.hs_gmres(f, p.b, tol=1e-10, restart=2, maxit=1000)
     assert rr["converged"] and rr["relres_true"] <= 1e-8
+
+
+def test_analyze_once_factor_many(H, handle):
+    """NEXT f2 / P:763 (Newton and continuation produce a sequence of systems with one
+    pattern): re-factoring new values on the same analysis (cached pattern and scatter map)
+    equals a fresh analysis bit for bit, and re-factoring the same values is deterministic.
+    (Scaling A by alpha is NOT a symmetry of the method: the coarse DOFs live in the
+    G-scaled space with diagonal I_r, so their couplings scale by sqrt(alpha) while
+    unprocessed blocks scale by alpha; the oracle shows the same.)"""
+    p = gen_stokes_q1(12, 10, 5, leaf_columns=2)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=2)
+    f1 = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    # a symmetric perturbation: scale row i and column i by d_i (D A D stays SPD)
+    d = 1.0 + 0.2 * np.sin(np.arange(p.n))
+    rows = np.repeat(np.arange(p.n), np.diff(p.rowptr))
+    vals2 = p.vals * d[rows] * d[p.colind]
+    f2 = H.hs_factor_create(handle, a, vals2, eps=1e-2)
+    a_new = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=2)
+    f3 = H.hs_factor_create(handle, a_new, vals2, eps=1e-2)
+    v = np.random.default_rng(4).standard_normal(p.n)
+    assert np.array_equal(H.hs_apply(f2, v), H.hs_apply(f3, v))
+    f4 = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    assert np.array_equal(H.hs_apply(f4, v), H.hs_apply(f1, v))
