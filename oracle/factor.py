@@ -54,6 +54,8 @@ class Elim:
     coarse_w: np.ndarray = None   # r x k_w
     tail_w: np.ndarray = None     # (m - r) x k_w dropped V2^T (debug, P3)
     flagged: bool = False         # a CPQR decision within rounding distance of its boundary
+    dc: bool = True               # False: original LoRaSp step (eliminate_nodc); G = L_f
+    Cc: np.ndarray = None         # dc = False: (m - r) x r, L_f^{-1} U2^T A_ss U1
 
 
 @dataclasses.dataclass
@@ -166,6 +168,67 @@ def eliminate(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, injec
     return e
 
 
+def eliminate_nodc(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, inject=None,
+                   keep_debug=False) -> Elim:
+    """NEXT f1: one step of the ORIGINAL LoRaSp sparsified elimination, WITHOUT deferred
+    compression (Eq. offdiag):
+      1. compress the UNSCALED block A_sw = U V^T = U1 V1^T + U2 V2^T with the same CPQR as
+         the DC path (readings Q1-Q5: tau_s relative to A_sw's largest column norm, R-floor
+         with the largest column norm of A_sn);
+      2. rotate row s by U^T and drop U2^T A_sw = V2^T: the fine DOFs f (the U2 part) no
+         longer couple to w;
+      3. eliminate f: A_ff = U2^T A_ss U2 = L_f L_f^T (not I: Table 1),
+         C_c = L_f^{-1} U2^T A_ss U1, C_n = L_f^{-1} U2^T A_sn;
+      4. Schur updates A_pq -= C_p^T C_q on n x n and on the coarse block of s:
+         diag(s) = U1^T A_ss U1 - C_c^T C_c, coarse-n = U1^T A_sn - C_c^T C_n,
+         coarse-w = V1^T (the kept CPQR rows).
+    Eliminating f and then the coarse DOFs equals one Cholesky step on s in the compressed
+    matrix A~ (Eq. sc_old), whose error against the exact Schur complement is Eq. err_old."""
+    m = st.live[s]
+    nsz = [st.live[q] for q in nlist]
+    wsz = [st.live[q] for q in wlist]
+    no, wo = _cols(nsz), _cols(wsz)
+    A_ss = st.get(s, s)
+    A_ss = np.tril(A_ss) + np.tril(A_ss, -1).T            # the store keeps the lower triangle
+    A_sn = np.hstack([st.get(s, q) for q in nlist]) if nlist else np.zeros((m, 0))
+    A_sw = np.hstack([st.get(s, q) for q in wlist]) if wlist else np.zeros((m, 0))
+    if A_sw.shape[1] == 0 or m == 0:
+        r, V, tau, piv, W = 0, np.zeros((m, 0)), np.zeros(0), np.zeros(0, dtype=np.int64), A_sw
+        mu = pi = np.inf
+        tau_s = 0.0
+        flagged = False
+    else:
+        kappa = float(np.linalg.cond(A_ss)) if m > 0 else 1.0
+        row_scale = float(np.sqrt(np.sum(A_sn ** 2, axis=0)).max()) if A_sn.shape[1] else 0.0
+        res = cpqr(A_sw, eps, relative, inject, noise=FLAG_ABS * max(1.0, kappa), row_scale=row_scale)   # step 1
+        r, V, tau, piv, W = res.r, res.V[:, :res.r], res.tau[:res.r], res.piv[:res.r], res.W
+        mu, pi, tau_s, flagged = res.mu, res.pi, res.tau_s, res.flagged
+    Ah = apply_Qt(V, tau, apply_Qt(V, tau, A_ss).T).T      # step 2: U^T A_ss U
+    Bn = apply_Qt(V, tau, A_sn)                            #          U^T A_sn
+    Lf = chol(Ah[r:, r:], l, s)                            # step 3
+    Cc = tri_solve(Lf, Ah[r:, :r])
+    C = tri_solve(Lf, Bn[r:])
+    for a, p in enumerate(nlist):                          # step 4: n x n
+        Cp = C[:, no[a]:no[a + 1]]
+        for b in range(a + 1):
+            q = nlist[b]
+            Cq = C[:, no[b]:no[b + 1]]
+            st.set(p, q, st.get(p, q) - Cp.T @ Cq)
+    st.live[s] = r                                         # coarse block of s
+    st.set(s, s, Ah[:r, :r] - Cc.T @ Cc)
+    coarse_n = Bn[:r] - Cc.T @ C
+    for a, q in enumerate(nlist):
+        st.set(s, q, coarse_n[:, no[a]:no[a + 1]])
+    coarse_w = W[:r]
+    for a, q in enumerate(wlist):
+        st.set(s, q, coarse_w[:, wo[a]:wo[a + 1]])
+    e = Elim(l, s, m, r, Lf, V, tau, piv, C, list(nlist), nsz, list(wlist), wsz, mu, pi, tau_s, flagged=flagged,
+             dc=False, Cc=Cc)
+    if keep_debug:
+        e.coarse_n, e.coarse_w, e.tail_w = coarse_n, coarse_w, W[r:]
+    return e
+
+
 def next_level(st: BlockStore, H_next, nclus_next) -> BlockStore:
     """Extract A_c: parent P = [coarse(2P); coarse(2P+1)], blocks are the
     2x2 assemblies of the child blocks (missing child blocks are zero)."""
@@ -196,7 +259,7 @@ def assemble_top(st: BlockStore, nclus):
 
 
 def factor(an: Analysis, rowptr, colind, vals, eps=1e-2, relative=True, inject=None,
-           keep_debug=False, snapshot=None, max_levels=None) -> Factor:
+           keep_debug=False, snapshot=None, max_levels=None, dc=True) -> Factor:
     """Algorithm 1.  inject: {(l, s): (r, piv)} decision injection.
     snapshot(l, b, store) is called after every batch when given (debug).
     max_levels: stop after that many levels (partial record for sampled parity at full
@@ -210,8 +273,8 @@ def factor(an: Analysis, rowptr, colind, vals, eps=1e-2, relative=True, inject=N
             eb = []
             for s in B:
                 inj = None if inject is None else inject.get((l, s))
-                eb.append(eliminate(st, l, s, lev.nlist[s], lev.wlist[s], eps, relative, inj,
-                                    keep_debug))
+                elim = eliminate if dc else eliminate_nodc
+                eb.append(elim(st, l, s, lev.nlist[s], lev.wlist[s], eps, relative, inj, keep_debug))
             lv.append(eb)
             if snapshot is not None:
                 snapshot(l, bi, st)

@@ -30,9 +30,14 @@ def apply(fac: Factor, b: np.ndarray) -> np.ndarray:
     for l, lv in enumerate(fac.elims):
         for eb in lv:
             for e in eb:
-                t = sla.solve_triangular(e.G, y[e.s], lower=True) if e.m else y[e.s].copy()
-                t = apply_Qt(e.V, e.tau, t)
-                yf = t[e.r:]
+                if e.dc:
+                    t = sla.solve_triangular(e.G, y[e.s], lower=True) if e.m else y[e.s].copy()
+                    t = apply_Qt(e.V, e.tau, t)
+                    yf = t[e.r:]
+                else:   # original LoRaSp step: [y_c; y_f] = U^T y_s, y_f <- L_f^{-1} y_f, y_c -= C_c^T y_f
+                    t = apply_Qt(e.V, e.tau, y[e.s])
+                    yf = sla.solve_triangular(e.G, t[e.r:], lower=True) if e.m > e.r else t[e.r:]
+                    t = np.concatenate([t[:e.r] - e.Cc.T @ yf, yf])
                 fine[(l, e.s)] = yf
                 o = 0
                 for q, k in zip(e.nlist, e.nsz):
@@ -72,9 +77,14 @@ def apply(fac: Factor, b: np.ndarray) -> np.ndarray:
                     assert x[q].shape[0] == k
                     xf = xf - e.C[:, o:o + k] @ x[q]
                     o += k
-                t = np.concatenate([x[e.s], xf])
-                t = apply_Q(e.V, e.tau, t)
-                x[e.s] = sla.solve_triangular(e.G, t, lower=True, trans="T") if e.m else t
+                if e.dc:
+                    t = np.concatenate([x[e.s], xf])
+                    t = apply_Q(e.V, e.tau, t)
+                    x[e.s] = sla.solve_triangular(e.G, t, lower=True, trans="T") if e.m else t
+                else:
+                    xf = xf - e.Cc @ x[e.s]
+                    xf = sla.solve_triangular(e.G, xf, lower=True, trans="T") if e.m > e.r else xf
+                    x[e.s] = apply_Q(e.V, e.tau, np.concatenate([x[e.s], xf]))
     xp = np.concatenate(x)
     out = np.empty_like(xp)
     out[an.perm] = xp

@@ -205,3 +205,78 @@ def test_gmres_restart_converges():
     A = p.to_scipy()
     x, rep = gmres(A, p.b, lambda v: v, tol=1e-10, restart=5, maxit=2000)
     assert rep.converged and rep.restarts > 1 and rep.relres_true <= 1e-9
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+@pytest.mark.parametrize("eps", [1e-1, 1e-2])
+def test_prop1_no_deferred_compression(idx, eps):
+    """NEXT f1 pin: the original LoRaSp step (eliminate_nodc) followed by the exact
+    elimination of s's coarse DOFs is one Cholesky step on s in the compressed matrix A~
+    (P:168-185), so its error against the exact Schur complement S_A (Eq. exact_sc) is
+    Eq. err_old: E_nn = 0, E_nw = A_ns A_ss^{-1} U2 V2^T, E_ww = A_ws A_ss^{-1} A_sw -
+    V1 U1^T A_ss^{-1} U1 V1^T, with Proposition 1's bound ||E_nw|| <= ||V2|| ||A_ns|| / s_min."""
+    from oracle.factor import eliminate_nodc
+    from oracle.dense import apply_Q
+    p, kw = tiny_problems()[idx]
+    an = _an(p, kw)
+    st = initial_blocks(an, p.rowptr, p.colind, p.vals)
+    checked = 0
+    for l, lev in enumerate(an.levels):
+        for B in lev.batches:
+            for s in B:
+                ns, ws = lev.nlist[s], lev.wlist[s]
+                before = copy.deepcopy(st)
+                e = eliminate_nodc(st, l, s, ns, ws, eps, True, keep_debug=True)
+                if sum(e.wsz) == 0 or e.m == 0:
+                    continue
+                M0, o0 = _dense_local(before, [s] + ns + ws)
+                m, r = e.m, e.r
+                Ass, Asr, Arr = M0[:m, :m], M0[:m, m:], M0[m:, m:]
+                SA = Arr - Asr.T @ np.linalg.solve(Ass, Asr)
+                M1, o1 = _dense_local(st, [s] + ns + ws)
+                Salg = M1[r:, r:] - M1[r:, :r] @ np.linalg.solve(M1[:r, :r], M1[:r, r:]) if r else M1[r:, r:]
+                E = Salg - SA
+                kn = sum(e.nsz)
+                Ans, Asw = Asr[:, :kn].T, Asr[:, kn:]
+                Q = apply_Q(e.V, e.tau, np.eye(m))
+                U1V1t = Q[:, :r] @ e.coarse_w                                           # U1 V1^T
+                U2V2t = Q[:, r:] @ e.tail_w                                             # U2 V2^T
+                assert np.allclose(U1V1t + U2V2t, Asw, atol=1e-11 * max(1.0, np.abs(Asw).max()))
+                scale = max(1.0, np.abs(SA).max())
+                amax = lambda X: float(np.abs(X).max()) if X.size else 0.0
+                assert amax(E[:kn, :kn]) <= 1e-10 * scale                              # E_nn = 0
+                Enw = Ans @ np.linalg.solve(Ass, U2V2t)
+                assert amax(E[:kn, kn:] - Enw) <= 1e-10 * scale                        # E_nw
+                Eww = Asw.T @ np.linalg.solve(Ass, Asw) - U1V1t.T @ np.linalg.solve(Ass, U1V1t)
+                assert amax(E[kn:, kn:] - Eww) <= 1e-10 * scale                        # E_ww
+                if kn:
+                    smin = np.linalg.eigvalsh(Ass).min()
+                    bound = np.linalg.norm(e.tail_w, 2) * np.linalg.norm(Ans, 2) / smin
+                    assert np.linalg.norm(E[:kn, kn:], 2) <= bound * (1 + 1e-9) + 1e-12 * scale
+                checked += 1
+        Hn = an.levels[l + 1].H if l + 1 < len(an.levels) else an.H_top
+        st = next_level(st, Hn, lev.nclus // 2)
+    assert checked > 0
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 3])
+def test_P1_no_dc_eps0_exact(idx):
+    """NEXT f1: with eps = 0 the original LoRaSp factorization is also an exact Cholesky."""
+    p, kw = tiny_problems()[idx]
+    an = _an(p, kw)
+    fac = factor(an, p.rowptr, p.colind, p.vals, eps=0.0, dc=False)
+    A = p.to_scipy().toarray()
+    x = apply(fac, p.b)
+    assert np.linalg.norm(x - np.linalg.solve(A, p.b)) <= 1e-12 * np.linalg.norm(np.linalg.solve(A, p.b))
+
+
+def test_no_dc_apply_symmetric_positive():
+    p = gen_poisson2d(32)
+    an = analyze_problem(p)
+    fac = factor(an, p.rowptr, p.colind, p.vals, eps=1e-2, dc=False)
+    rng = np.random.default_rng(7)
+    U = rng.standard_normal((p.n, 20))
+    MU = np.stack([apply(fac, U[:, i]) for i in range(20)], axis=1)
+    G = U.T @ MU
+    assert np.abs(G - G.T).max() <= 1e-12 * np.abs(G).max()
+    assert np.all(np.linalg.eigvalsh(0.5 * (G + G.T)) > 0)
