@@ -172,6 +172,13 @@ int64_t launch_count();
 
 // ---- kernel launchers (kernels.cu / solve_kernels.cu) -------------------------------------
 // values symmetry: *flag = 1 if |v[k] - v[tmap[k]]| > 1e-12 max(|v[k]|, |v[tmap[k]]|) for some k
+// NEXT f1 (nodc.cu): the original LoRaSp step without deferred compression
+void set_smem_attr(const void* f, size_t bytes);   // opt-in dynamic smem (only ever grows)
+void launch_nmax(const CluItem* d_clu, const TrsmItem* d_items, int n, cudaStream_t st);
+void launch_rot2(const CluItem* d_clu, int n, int max_m, const int32_t* d_rank, cudaStream_t st);
+void launch_coarse_update(const CluItem* d_clu, const TrsmItem* d_items, int n, const int32_t* d_rank,
+                          cudaStream_t st);
+void launch_form_T_nodc(const FormTItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32_t* flag, cudaStream_t st);
 void launch_copy2d(const CopyItem* d_items, int n, cudaStream_t st);
 // splits items larger than ~16K elements into row ranges (one CTA each) in place

@@ -444,7 +444,10 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, con
 
 hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* values, const hs_factor_opts& opt) {
   if (opt.eps < 0 || !std::isfinite(opt.eps)) fail(HS_E_INVALID_ARG, "factor: eps must be finite and >= 0");
-  if (opt.dc != 1) fail(HS_E_UNSUPPORTED, "factor: only dc = 1 (deferred compression) is implemented");
+  if (opt.dc != 0 && opt.dc != 1) fail(HS_E_INVALID_ARG, "factor: dc must be 0 or 1");
+  const bool nodc = opt.dc == 0;   // NEXT f1: the original LoRaSp step (nodc.cu)
+  if (nodc && (std::getenv("HS_CPQR_SINGLE_CTA") || std::getenv("HS_CPQR_V2")))
+    fail(HS_E_UNSUPPORTED, "factor: dc = 0 runs with the v3 CPQR only");
   Analysis* an = const_cast<Analysis*>(an_c);   // the device pattern cache lives in the analysis
   const int64_t n = an->n, nnz = an->rowptr[n];
   cudaStream_t st = h->stream;
@@ -656,6 +659,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         for (int32_t q : lev.w[s]) kw += live[q];
         L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw;
       }
+      CluItem* d_clu_batch = nullptr;   // this batch's cluster items on the device (upA)
       std::vector<int32_t> Bo;   // the batch's clusters eliminated here
       for (int32_t s : Bt)
         if (own(l, s)) Bo.push_back(s);
@@ -690,7 +694,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         if (m == 0) continue;
         double* p; int32_t ld, tr;
         bs.get(s, s, p, ld, tr);
-        gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, tr, 0});
+        // the store keeps the lower triangle of a diagonal block; dc = 0 rotates both sides
+        // of A_ss, so it is gathered as the full symmetric block (copy mode 2)
+        gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
         int32_t col = 0;
         const auto& ro = row_offs(s);
         size_t kq = 0;
@@ -730,10 +736,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         HS_CUDA(cudaEventRecord(pt.a[0], st));
         launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
         HS_CUDA(cudaEventRecord(pt.a[1], st));
-        launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
+        if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
         HS_CUDA(cudaEventRecord(pt.a[2], st));
-        launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
+        if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
+        else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), st);   // R-floor
         HS_CUDA(cudaEventRecord(pt.a[3], st));
+        d_clu_batch = upA.dptr<CluItem>(iC);
         if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
         else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
         else {
@@ -752,6 +760,56 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
         L.rank[s] = live[s] == 0 ? 0 : h_rank[bi];
+      }
+      if (nodc && nb > 0) {
+        // (U^T A_ss U) in G; L_f L_f^T = its fine block; C_c = L_f^{-1} G[r:, :r] in place,
+        // C_n = L_f^{-1} (U^T A_sn)_f in B; [A_cc | A_cn] -= C_c^T [C_c | C_n]
+        std::vector<CluItem> fine, fs;
+        std::vector<TrsmItem> fst, cu;
+        int fmax = 1;
+        for (int bi = 0; bi < nb; ++bi) {
+          const int32_t s = Bo[bi];
+          const int32_t m = live[s], r = L.rank[s], K = m - r;
+          if (K <= 0) continue;
+          CluItem f0 = clu[bi];
+          f0.G = L.G[s] + (int64_t)r * m + r;
+          f0.m = K;
+          f0.pad0 = m;            // ld of the fine block inside G
+          f0.nmax = nullptr;
+          fine.push_back(f0);
+          fmax = std::max(fmax, K);
+          const int32_t tw = K <= SMEM_M ? 64 : 32;
+          CluItem a0 = f0;        // right-hand sides: G[r:, :r] (ld m) and B[r:, kw:] (ld ldB)
+          a0.B = L.G[s] + (int64_t)r * m;
+          a0.ldB = m;
+          a0.kw = 0;
+          CluItem b0 = f0;
+          b0.B = L.B[s] + (int64_t)r * L.ldB[s] + L.kw[s];
+          b0.ldB = L.ldB[s];
+          b0.kw = 0;
+          for (int rhs = 0; rhs < 2; ++rhs) {
+            const int32_t nc_all = rhs == 0 ? r : L.kn[s];
+            if (nc_all <= 0) continue;
+            fs.push_back(rhs == 0 ? a0 : b0);
+            for (int32_t c0 = 0; c0 < nc_all; c0 += tw)
+              fst.push_back(TrsmItem{(int32_t)fs.size() - 1, c0, std::min(tw, nc_all - c0), 0});
+          }
+          for (int32_t c0 = 0; c0 < r + L.kn[s]; c0 += 256)
+            cu.push_back(TrsmItem{bi, c0, std::min(256, r + L.kn[s] - c0), 0});
+          S.flops += 4.0 * m * m * r + (double)K * K * K / 3.0 + (double)K * K * (r + L.kn[s]) +
+                     2.0 * r * K * (r + L.kn[s]);
+        }
+        upB.reset();
+        const size_t kF = upB.add(fine), kS = upB.add(fs), kT = upB.add(fst), kU = upB.add(cu);
+        upB.stage.ensure(upB.total);
+        upB.dev.ensure(upB.total);
+        upB.copy_in(kF, fine); upB.copy_in(kS, fs); upB.copy_in(kT, fst); upB.copy_in(kU, cu);
+        upB.send(st);
+        launch_rot2(d_clu_batch, nb, max_m, d_rank, st);
+        launch_potrf(upB.dptr<CluItem>(kF), (int)fine.size(), fmax, d_status, st);
+        launch_trsm(upB.dptr<CluItem>(kS), upB.dptr<TrsmItem>(kT), (int)fst.size(), fmax, st);
+        launch_coarse_update(d_clu_batch, upB.dptr<TrsmItem>(kU), (int)cu.size(), d_rank, st);
+        check_status(d_status, &h_status, st);   // a fine block that is not SPD (Table 1: "may be indefinite")
       }
       // ---- phase II across GPUs: the batch's ranks, then the elimination records ---------
       std::vector<double*> rbuf(Bt.size(), nullptr);   // received B_s of remote clusters
@@ -851,7 +909,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           double* p; int32_t ld, tr;
           if (mine) {
             bs.get(s, s, p, ld, tr);
-            id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
+            if (nodc) wb.push_back(CopyItem{L.G[s], p, m, ld, r, r, 0, 0});   // A_cc - C_c^T C_c
+            else {
+              id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
+            }
           }
           int32_t col = 0;
           const auto& ro = row_offs(s);
@@ -936,7 +997,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                                   cudaMemcpyDeviceToDevice, st));
           HS_CUDA(cudaEventRecord(h->ev_fork, st));
           HS_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-          launch_form_T(d_ft, (int)ft.size(), ft_max_m, h->side);
+          if (nodc) launch_form_T_nodc(d_ft, (int)ft.size(), ft_max_m, h->side);
+          else launch_form_T(d_ft, (int)ft.size(), ft_max_m, h->side);
           ev_ft = deferred.take();
           HS_CUDA(cudaEventRecord(ev_ft, h->side));
         }

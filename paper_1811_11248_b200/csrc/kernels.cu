@@ -170,7 +170,7 @@ __global__ void k_potrf(const CluItem* __restrict__ items, DevStatus* status) {
   extern __shared__ double smem[];
   const CluItem it = items[blockIdx.x];
   if (it.m == 0 || it.m > SMEM_M) return;
-  potrf_core(it.G, it.m, it.m, smem, status, it.level, it.cluster);
+  potrf_core(it.G, it.pad0 ? it.pad0 : it.m, it.m, smem, status, it.level, it.cluster);   // pad0: ld of G
 }
 
 // a1 for m > SMEM_M: the same right-looking Cholesky in place in global memory (L1/L2
@@ -180,13 +180,14 @@ __global__ void __launch_bounds__(1024) k_potrf_gl(const CluItem* __restrict__ i
   const int m = it.m;
   if (m <= SMEM_M) return;
   double* a = it.G;
+  const int64_t ld = it.pad0 ? it.pad0 : m;   // pad0: ld of G (sub-block factorizations)
   __shared__ int bad;
   __shared__ double piv;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   for (int j = 0; j < m; ++j) {
     if (threadIdx.x == 0) {
-      const double d = a[(int64_t)j * m + j];
+      const double d = a[(int64_t)j * ld + j];
       if (!(d > 0.0)) {
         bad = 1;
         if (atomicCAS(&status->flag, 0, 1) == 0) {
@@ -197,27 +198,27 @@ __global__ void __launch_bounds__(1024) k_potrf_gl(const CluItem* __restrict__ i
         }
       } else {
         piv = sqrt(d);
-        a[(int64_t)j * m + j] = piv;
+        a[(int64_t)j * ld + j] = piv;
       }
     }
     __syncthreads();
     if (bad) return;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[(int64_t)i * m + j] /= piv;
+    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) a[(int64_t)i * ld + j] /= piv;
     __syncthreads();
     const int t = m - j - 1;
     // rows i of the trailing lower triangle: a warp per row, lanes over k <= i
     for (int i = (threadIdx.x >> 5); i < t; i += (blockDim.x >> 5)) {
       const int ii = j + 1 + i;
-      const double aij = a[(int64_t)ii * m + j];
+      const double aij = a[(int64_t)ii * ld + j];
       for (int k = (threadIdx.x & 31); k <= i; k += 32) {
         const int kk = j + 1 + k;
-        a[(int64_t)ii * m + kk] -= aij * a[(int64_t)kk * m + j];
+        a[(int64_t)ii * ld + kk] -= aij * a[(int64_t)kk * ld + j];
       }
     }
     __syncthreads();
   }
   for (int64_t e = threadIdx.x; e < (int64_t)m * m; e += blockDim.x)
-    if ((e % m) > (e / m)) a[e] = 0.0;
+    if ((e % m) > (e / m)) a[(e / m) * ld + (e % m)] = 0.0;
 }
 
 __global__ void k_potrf_raw(double* g, int ld, int m, DevStatus* status, int level) {
@@ -288,7 +289,7 @@ __global__ void k_trsm(const CluItem* __restrict__ clu, const TrsmItem* __restri
   const TrsmItem t = items[blockIdx.x];
   const CluItem it = clu[t.ci];
   if (it.m == 0) return;
-  trsm_core(it.G, it.m, it.m, it.B, it.ldB, t.c0, t.nc, smem);
+  trsm_core(it.G, it.pad0 ? it.pad0 : it.m, it.m, it.B, it.ldB, t.c0, t.nc, smem);   // pad0: ld of G
   if (it.nmax && t.c0 + t.nc > it.kw) {
     __syncthreads();
     const int TW = it.m <= SMEM_M ? 64 : 32;
@@ -940,6 +941,12 @@ void set_smem(const void* f, size_t bytes) {
 }
 
 std::atomic<int64_t> g_launches{0};
+
+}  // namespace
+
+void set_smem_attr(const void* f, size_t bytes) { set_smem(f, bytes); }
+
+namespace {
 
 }  // namespace
 

@@ -33,7 +33,7 @@ def handle(H):
     return H.hs_create(0)
 
 
-def _both(H, handle, p, eps, kw=None):
+def _both(H, handle, p, eps, kw=None, dc=1):
     kw = kw or {}
     top_log2 = kw.get("top_log2", 3)
     nsub_log2 = kw.get("nsub_log2", 3)
@@ -41,17 +41,17 @@ def _both(H, handle, p, eps, kw=None):
                  leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
     a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
                      leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
-    f = H.hs_factor_create(handle, a, p.vals, eps=eps)
+    f = H.hs_factor_create(handle, a, p.vals, eps=eps, dc=dc)
     if eps == 0.0:
         # eps = 0 keeps every nonzero: decisions on rounding noise are not comparable,
         # and both sides are exact Cholesky factorizations (checked by the caller)
         return an, None, a, f, 0
-    fac, flagged = oracle_with_injection(H, f, an, p, eps)
+    fac, flagged = oracle_with_injection(H, f, an, p, eps, dc=dc)
     assert np.array_equal(H.hs_factor_export(f, H.HS_FEXP_TOP), fac.top_sizes)
     return an, fac, a, f, flagged
 
 
-def oracle_with_injection(H, f, an, p, eps, max_rounds=200):
+def oracle_with_injection(H, f, an, p, eps, max_rounds=200, dc=1):
     """Rank/pivot parity with the margin exemption: walk the clusters in elimination
     order; at the first disagreement, a flagged cluster gets the GPU's decisions
     injected into the oracle (which is re-run), an unflagged one fails the test."""
@@ -61,7 +61,7 @@ def oracle_with_injection(H, f, an, p, eps, max_rounds=200):
                     H.hs_factor_export(f, H.HS_FEXP_PIV, l)))
     inject = {}
     for _ in range(max_rounds):
-        fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps, inject=inject or None)
+        fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps, inject=inject or None, dc=bool(dc))
         first = None
         nflag = 0
         for l, lv in enumerate(fac.elims):
@@ -240,3 +240,31 @@ def test_analyze_once_factor_many(H, handle):
     assert np.array_equal(H.hs_apply(f2, v), H.hs_apply(f3, v))
     f4 = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
     assert np.array_equal(H.hs_apply(f4, v), H.hs_apply(f1, v))
+
+
+NODC = [CASES[0], CASES[3], CASES[7], CASES[8], CASES[9], CASES[10]]
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-1])
+@pytest.mark.parametrize("name,gen,kw", NODC, ids=[t[0] for t in NODC])
+def test_no_deferred_compression_parity(H, handle, name, gen, kw, eps):
+    """NEXT f1: the original LoRaSp step (hs_factor_opts.dc = 0: CPQR of the unscaled A_sw,
+    rotation of A_ss from both sides, fine Cholesky, coarse-block update) against
+    oracle/factor.py eliminate_nodc: ranks and pivots (decision injection for flagged
+    clusters), apply within 1e-9, PCG within 1e-8 and +-1 iteration."""
+    p = gen()
+    an, fac, a, f, flagged = _both(H, handle, p, eps, kw, dc=0)
+    _apply_parity(H, f, fac, p.n)
+    xo, ro = opcg(p.to_scipy(), p.b, lambda r: oapply(fac, r), tol=p.tol)
+    xg, rg = H.hs_pcg(f, p.b, tol=p.tol)
+    assert abs(rg["iters"] - ro.iters) <= 1
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+
+
+@pytest.mark.parametrize("name,gen,kw", TINY, ids=[t[0] for t in TINY])
+def test_no_deferred_compression_eps0_exact(H, handle, name, gen, kw):
+    p = gen()
+    an, fac, a, f, _ = _both(H, handle, p, 0.0, kw, dc=0)
+    A = p.to_scipy().toarray()
+    x_ref = sla.cho_solve(sla.cho_factor(A), p.b)
+    assert np.linalg.norm(H.hs_apply(f, p.b) - x_ref) / np.linalg.norm(x_ref) <= 1e-12

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
-tail -3 gpurun_out/gpu_tests.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "no_deferred" > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
+tail -30 gpurun_out/gpu_tests.log
