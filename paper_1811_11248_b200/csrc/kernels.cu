@@ -791,8 +791,8 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
   const SchurTile2 t = tiles[blockIdx.x];
   const SchurSrc s = srcs[t.src];
   const NbCol* nb = nbc + s.nb_off;
-  __shared__ double ap[16][64];
-  __shared__ double aq[16][64];
+  __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
+  __shared__ double aq[16][68];
   __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
   __shared__ int r_slot[64], c_slot[64];
   __shared__ int r_list[SCH_MAXO], c_list[SCH_MAXO];
@@ -848,13 +848,13 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
     for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
   }
   __syncthreads();
-  // dense 64 x 64 tile of C^T C
-  const int tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
+  // dense 64 x 64 tile of C^T C on the FP64 tensor cores (DMMA, mma.sync m8n8k4): warp w
+  // owns output rows 8w..8w+7 and the eight 8 x 8 column tiles; lane l holds rows
+  // 8w + l/4, columns 8 tc + 2 (l % 4) + {0, 1} (the m8n8k4 accumulator layout).
+  const int lane = tid & 31, w = tid >> 5;
+  double acc[8][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int tc = 0; tc < 8; ++tc) acc[tc][0] = acc[tc][1] = 0.0;
   const double* Cp = s.C + t.i0;
   const double* Cq = s.C + t.j0;
   for (int k0 = 0; k0 < s.K; k0 += 16) {
@@ -868,28 +868,27 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double x[4], y[4];
+    for (int kk = 0; kk < 16; kk += 4) {
+      const double a = ap[kk + (lane & 3)][8 * w + (lane >> 2)];   // A = C_p^T, row-major 8 x 4
 #pragma unroll
-      for (int a = 0; a < 4; ++a) x[a] = ap[kk][ty + 16 * a];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) y[b] = aq[kk][tx + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+      for (int tc = 0; tc < 8; ++tc) {
+        const double b = aq[kk + (lane & 3)][8 * tc + (lane >> 2)];   // B = C_q, col-major 4 x 8
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[tc][0]), "+d"(acc[tc][1])
+                     : "d"(a), "d"(b));
+      }
     }
     __syncthreads();
   }
   // scatter-subtract into the target blocks: all 16 target addresses first, then all 16
   // loads in flight, then the stores (no load waits behind a possibly aliasing store)
-  double* tp[4][4];
+  double* tp[8][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      tp[a][b] = nullptr;
-      const int i = ty + 16 * a, j = tx + 16 * b;
+    for (int e = 0; e < 2; ++e) {
+      tp[tc][e] = nullptr;
+      const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
       if (i >= rows || j >= cols) continue;
       const int oa = r_own[i], ob = c_own[j];
       if (oa < ob) continue;                               // upper: the transposed block
@@ -905,18 +904,18 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
         p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
         ld = dir.cap[nb[ob].q];
       }
-      if (p) tp[a][b] = p + (int64_t)li * ld + lj;
+      if (p) tp[tc][e] = p + (int64_t)li * ld + lj;
     }
-  double old[4][4];
+  double old[8][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) old[a][b] = tp[a][b] ? *tp[a][b] : 0.0;
+    for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] ? *tp[tc][e] : 0.0;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (tp[a][b]) *tp[a][b] = old[a][b] - acc[a][b];
+    for (int e = 0; e < 2; ++e)
+      if (tp[tc][e]) *tp[tc][e] = old[tc][e] - acc[tc][e];
 }
 
 __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,

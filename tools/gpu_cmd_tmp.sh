@@ -1,8 +1,4 @@
 mkdir -p gpurun_out
-timeout 2400 python tools/dc_sweep.py 2 > gpurun_out/dc_sweep.jsonl 2> gpurun_out/dc_sweep.err
-python -c "
-import json
-for l in open('gpurun_out/dc_sweep.jsonl'):
-    d=json.loads(l); print(d['family'], d['level'], d['n'], d['eps'], 'dc' if d['dc'] else 'nodc', d.get('pcg_iters'), d.get('gmres_iters'), round(d.get('t_factor_s',0),3), d.get('error','')[:60])
-"
-tail -3 gpurun_out/dc_sweep.err
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+tail -2 gpurun_out/gpu_tests.log
