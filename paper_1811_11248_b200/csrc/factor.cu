@@ -750,10 +750,112 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         HS_CUDA(cudaEventRecord(pt.a[4], st));
         HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
-        check_status(d_status, &h_status, st);       // synchronises the stream
-        pt.collect(S);
       } else {
         t_plan += now_s() - tp0;
+      }
+      // ---- pre-plan of the batch's second half while its first half runs: everything but
+      // the kept ranks (patched after the read-back; a source whose rank turns out full is a
+      // phantom whose tiles exit at once).  Remote clusters of a phase-II batch are planned if
+      // this rank will receive their record.
+      const double tpp = now_s();
+      std::vector<SchurSrc> srcs;
+      std::vector<int32_t> src_cl;
+      std::vector<NbCol> nbc;
+      std::vector<std::vector<SchurTile2>> waves;
+      std::vector<int32_t> touched;
+      std::vector<CopyItem> wb;
+      std::vector<double*> id_ptr;
+      std::vector<int32_t> id_ld, id_r;
+      std::vector<FormTItem> ft;
+      int ft_max_m = 0;
+      struct Pend {
+        int32_t s, k;
+        bool mine;
+        int64_t src, id, diag, ft;
+        size_t wb_begin, wb_end;
+      };
+      std::vector<Pend> pend;
+      std::vector<int32_t> live_at(Bt.size());
+      for (size_t k = 0; k < Bt.size(); ++k) {
+        const int32_t s = Bt[k];
+        live_at[k] = live[s];
+        const bool mine = own(l, s);
+        if (!mine) {
+          if (!(dist && phase2)) continue;
+          const std::vector<int32_t> rc = receivers(*an, DP, l, s);
+          if (!std::binary_search(rc.begin(), rc.end(), (int32_t)h->rank)) continue;
+        }
+        const int32_t m = live[s], kn = L.kn[s], ldB = L.ldB[s];
+        if (m == 0) continue;
+        Pend pd{s, (int32_t)k, mine, -1, -1, -1, -1, wb.size(), wb.size()};
+        if (mine) {
+          pd.ft = (int64_t)ft.size();
+          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, 0});
+          ft_max_m = std::max(ft_max_m, m);
+        }
+        // neighbour column offsets inside the n-part
+        const auto& ns = lev.H[s];
+        std::vector<int32_t> noff(ns.size() + 1, 0);
+        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + live[ns[a]];
+        if (kn > 0) {
+          // wave = lowest wave in which no earlier source shares a neighbour with s
+          uint64_t used = 0;
+          for (int32_t q : ns)
+            if (live[q] > 0) used |= wave_mask[q];
+          int w = 0;
+          while (w < 63 && ((used >> w) & 1ull)) ++w;
+          if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
+          const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
+          SchurSrc sc{nullptr, ldB, 0, kn, (int32_t)nbc.size(), 0, 0};
+          for (size_t a = 0; a < ns.size(); ++a)
+            if (live[ns[a]] > 0) {
+              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], (int32_t)a});
+              if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
+              wave_mask[ns[a]] |= bit;
+            }
+          sc.nnb = (int32_t)nbc.size() - sc.nb_off;
+          pd.src = (int64_t)srcs.size();
+          srcs.push_back(sc);
+          src_cl.push_back(s);
+          if ((int)waves.size() <= w) waves.resize(w + 1);
+          const int T = (kn + 63) / 64;
+          for (int ti = 0; ti < T; ++ti)
+            for (int tj = 0; tj <= ti; ++tj) waves[w].push_back(SchurTile2{(int32_t)pd.src, ti * 64, tj * 64, 0});
+        }
+        // write-back of row s: [I_r | coarse-w | coarse-n] into the blocks held here (rows r)
+        double* p; int32_t ld, tr;
+        if (mine) {
+          bs.get(s, s, p, ld, tr);
+          if (nodc) {
+            pd.diag = (int64_t)wb.size();
+            wb.push_back(CopyItem{L.G[s], p, m, ld, 0, 0, 0, 0});   // A_cc - C_c^T C_c
+          } else {
+            pd.id = (int64_t)id_ptr.size();
+            id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(0);
+          }
+        }
+        pd.wb_begin = wb.size();
+        int32_t col = 0;
+        const auto& ro = row_offs(s);
+        size_t kq = 0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+            const int64_t o = ro[kq++];
+            if (live[q] > 0 && o >= 0) {
+              bs.at(s, q, o, p, ld, tr);
+              const double* off = (const double*)(uintptr_t)col;   // + B_s once known
+              if (!tr) wb.push_back(CopyItem{off, p, ldB, ld, 0, live[q], 0, 0});
+              else wb.push_back(CopyItem{off, p, ldB, ld, live[q], 0, 1, 0});
+            }
+            col += live[q];
+          }
+        pd.wb_end = wb.size();
+        pend.push_back(pd);
+      }
+      t_sub[0] += now_s() - tpp;
+      if (nb > 0) {
+        check_status(d_status, &h_status, st);       // synchronises the stream
+        pt.collect(S);
       }
       deferred.drain(false);
       const double tp1 = now_s();
@@ -834,37 +936,38 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         comm_group_end(h->comm, st);
       }
-      // ---- Schur update, write-back (local and received records) --------------------------
-      std::vector<SchurSrc> srcs;
-      std::vector<int32_t> src_cl;
-      std::vector<NbCol> nbc;
-      std::vector<std::vector<SchurTile2>> waves;
-      std::vector<int32_t> touched;
-      std::vector<CopyItem> wb;
-      std::vector<double*> id_ptr;
-      std::vector<int32_t> id_ld, id_r;
-      double tq_prev = now_s();
-      // persistent C_s = rows [r, m) of the n-part, compacted to ld kn (the factor record
-      // the apply reads); the Schur update still reads C in place from the batch workspace
-      std::vector<FormTItem> ft;
-      int ft_max_m = 0;
-      for (size_t k = 0; k < Bt.size(); ++k) {
-        const int32_t s = Bt[k];
-        const bool mine = own(l, s);
-        const double* Bs = mine ? L.B[s] : rbuf[k];
-        if (!mine && !Bs) continue;   // a remote cluster whose record this rank does not need
-        const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
+      // ---- Schur update, write-back: patch the pre-planned records with the ranks ----------
+      for (auto& pd : pend) {
+        const int32_t s = pd.s;
+        const double* Bs = pd.mine ? L.B[s] : rbuf[pd.k];
+        if (!pd.mine && !Bs) continue;
+        const int32_t m = live_at[pd.k], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
         const int32_t r = L.rank[s];
         const int32_t K = m - r;
         const double* C = Bs + (int64_t)r * ldB + kw;
-        if (mine) {
+        if (pd.src >= 0) {
+          srcs[pd.src].C = C;
+          srcs[pd.src].K = K;
+        }
+        for (size_t i = pd.wb_begin; i < pd.wb_end; ++i) {   // src holds the column offset
+          CopyItem& c = wb[i];
+          c.src = Bs + (uintptr_t)c.src;
+          if (c.trans) c.cols = r;
+          else c.rows = r;
+        }
+        if (pd.id >= 0) id_r[pd.id] = r;
+        if (pd.diag >= 0) {   // dc = 0: the coarse block A_cc - C_c^T C_c
+          wb[pd.diag].rows = r;
+          wb[pd.diag].cols = r;
+        }
+        if (pd.ft >= 0) ft[pd.ft].r = r;
+        if (pd.mine) {
           S.max_m = std::max(S.max_m, m);
           S.max_rank = std::max(S.max_rank, r);
-          if (m > 0) {
-            ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, r});
-            ft_max_m = std::max(ft_max_m, m);
+          if (K > 0 && kn > 0) {
+            L.C[s] = cslab.get((int64_t)K * kn);
+            wb.push_back(CopyItem{C, L.C[s], ldB, kn, K, kn, 0, 0});
           }
-          if (K > 0 && kn > 0) L.C[s] = cslab.get((int64_t)K * kn);
           // algorithmic flops of CPQR (+ rotation of the n-columns) and Schur
           double fq = 0.0;
           for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
@@ -872,67 +975,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           S.flops_phase[3] += fq;
           S.flops_phase[4] += (double)K * kn * (kn + 1);
         }
-        if (m == 0) continue;
-        // neighbour column offsets inside the n-part
-        const auto& ns = lev.H[s];
-        std::vector<int32_t> noff(ns.size() + 1, 0);
-        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + live[ns[a]];
-        if (K > 0 && kn > 0) {
-          // wave = lowest wave in which no earlier source shares a neighbour with s
-          uint64_t used = 0;
-          for (int32_t q : ns)
-            if (live[q] > 0) used |= wave_mask[q];
-          int w = 0;
-          while (w < 63 && ((used >> w) & 1ull)) ++w;
-          if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
-          const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
-          SchurSrc sc{C, ldB, K, kn, (int32_t)nbc.size(), 0, 0};
-          for (size_t a = 0; a < ns.size(); ++a)
-            if (live[ns[a]] > 0) {
-              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], (int32_t)a});
-              if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
-              wave_mask[ns[a]] |= bit;
-            }
-          sc.nnb = (int32_t)nbc.size() - sc.nb_off;
-          const int32_t si = (int32_t)srcs.size();
-          srcs.push_back(sc);
-          src_cl.push_back(s);
-          if ((int)waves.size() <= w) waves.resize(w + 1);
-          const int T = (kn + 63) / 64;
-          for (int ti = 0; ti < T; ++ti)
-            for (int tj = 0; tj <= ti; ++tj) waves[w].push_back(SchurTile2{si, ti * 64, tj * 64, 0});
-        }
-        const double tq0 = now_s();
-        t_sub[0] += tq0 - tq_prev;
-        // write-back of row s: [I_r | coarse-w | coarse-n] into the blocks held here
-        if (r > 0) {
-          double* p; int32_t ld, tr;
-          if (mine) {
-            bs.get(s, s, p, ld, tr);
-            if (nodc) wb.push_back(CopyItem{L.G[s], p, m, ld, r, r, 0, 0});   // A_cc - C_c^T C_c
-            else {
-              id_ptr.push_back(p); id_ld.push_back(ld); id_r.push_back(r);
-            }
-          }
-          int32_t col = 0;
-          const auto& ro = row_offs(s);
-          size_t kq = 0;
-          for (int pass = 0; pass < 2; ++pass)
-            for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
-              const int64_t o = ro[kq++];
-              if (live[q] > 0 && o >= 0) {
-                bs.at(s, q, o, p, ld, tr);
-                if (!tr) wb.push_back(CopyItem{Bs + col, p, ldB, ld, r, live[q], 0, 0});
-                else wb.push_back(CopyItem{Bs + col, p, ldB, ld, live[q], r, 1, 0});
-              }
-              col += live[q];
-            }
-        }
-        if (mine && L.C[s]) wb.push_back(CopyItem{C, L.C[s], ldB, kn, K, kn, 0, 0});
-        const double tq1 = now_s();
-        t_sub[1] += tq1 - tq0;
-        tq_prev = now_s();
       }
+      t_sub[1] += now_s() - tp1;
       const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
       // scratch of k_schur_prep (column owners); the pair tables are the level's

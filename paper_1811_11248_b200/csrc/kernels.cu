@@ -790,6 +790,7 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
   const SchurTile2 t = tiles[blockIdx.x];
   const SchurSrc s = srcs[t.src];
+  if (s.K <= 0) return;   // planned before its rank was known and kept everything (uniform)
   const NbCol* nb = nbc + s.nb_off;
   __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
   __shared__ double aq[16][68];
