@@ -48,6 +48,24 @@ struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operato
   int32_t m, r;
 };
 
+// a0 + a1 + a2 for the DC path (fused.cu): per cluster (k_chol_inv) or per 64-column tile
+// (k_scale_tile) of a cluster
+struct FusedItem {
+  const double* Ass;          // diagonal block in the store (lower, row-major, ld lda)
+  double* G;                  // workspace G_s
+  double* Ginv;               // unused
+  double* B;                  // workspace B_s (m x ldB)
+  unsigned long long* nmax;   // R-floor slot
+  int32_t m, lda, ldB, kw;
+  int32_t c0, nc, seg_begin, seg_end;
+  int32_t level, cluster, bi, pad;
+};
+struct FusedSeg {             // block (s, q) of the store: B_s columns [col, col + len)
+  const double* src;
+  int32_t sld, trans, col, len;
+};
+constexpr int CI_MAX_M = 112;   // k_scale_tile: G (ld m + 1) and a 64-column tile in shared memory, <= 28 rows per lane
+
 struct TrsmItem {   // one column tile of one cluster's B_s
   int32_t ci, c0, nc, pad;
 };
@@ -77,6 +95,17 @@ struct SchurSrc {
   int32_t* own;              // [kn] neighbour index owning each n-column (k_schur_prep)
   double** pairs;            // [nnb (nnb+1) / 2] target block of neighbour pair (a >= b), or null
 };
+// Device-side patch of a batch's pre-planned second half with the kept ranks r_s read from
+// d_rank (no host round trip between CPQR and the Schur update): one thread per item.
+enum PatchKind : int32_t { PK_SRC = 0, PK_ROWS, PK_COLS, PK_I32, PK_FT, PK_CCOPY };
+struct PatchItem {
+  void* target;          // SchurSrc* / CopyItem* / int32_t* / FormTItem*
+  const double* base;    // B_s
+  int32_t bi, kind, m, ldB;
+  int32_t kw, i0, step, pad;
+};
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st);
+
 struct SchurTile2 {
   int32_t src, i0, j0, pad;
 };
@@ -165,6 +194,8 @@ struct DevStatus {
   int32_t flag, level, cluster, pivot;
   double value;
 };
+void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
+void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st);
 
 // ---- launch accounting (every launcher counts its kernels; graphs count their nodes) -----
 void count_launch(int64_t n);

@@ -238,8 +238,11 @@ struct PhaseTimer {
     S.t_phase_s[5] += el(b[1], b[2]);
     b_pending = false;
   }
-  void collect(hs_factor_stats_t& S) {   // after a synchronising point
+  void collect_a(hs_factor_stats_t& S) {
     for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
+  }
+  void collect(hs_factor_stats_t& S) {   // after a synchronising point
+    collect_a(S);
     collect_b(S);
   }
 };
@@ -511,6 +514,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   HS_CUDA(cudaMallocHost(&h_rank, sizeof(int32_t) * max_batch));
   std::unique_ptr<void, void (*)(void*)> rank_guard(d_rank, [](void* p) { cudaFree(p); });
   std::unique_ptr<void, void (*)(void*)> hrank_guard(h_rank, [](void* p) { cudaFreeHost(p); });
+  DevStatus* h_stat = nullptr;   // pinned: read back asynchronously with the ranks
+  HS_CUDA(cudaMallocHost(&h_stat, sizeof(DevStatus)));
+  std::unique_ptr<void, void (*)(void*)> hstat_guard(h_stat, [](void* p) { cudaFreeHost(p); });
+  cudaEvent_t ev_rank = nullptr;
+  HS_CUDA(cudaEventCreateWithFlags(&ev_rank, cudaEventDisableTiming));
+  std::unique_ptr<void, void (*)(void*)> evr_guard((void*)ev_rank, [](void* e) { cudaEventDestroy((cudaEvent_t)e); });
 
   hs_factor_stats_t& S = f->stats;
   PhaseTimer pt;
@@ -525,6 +534,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   // A/B switches for the previous CPQR kernels (single CTA / cluster with per-thread columns)
   const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;
   const bool cpqr_v2 = std::getenv("HS_CPQR_V2") != nullptr;
+  const bool no_fused = std::getenv("HS_NO_FUSED_POTRF_TRSM") != nullptr;   // separate gather/POTRF/TRSM
   // ---- multi-GPU (dist.cpp; protocol of oracle/dist.py) ---------------------
   // Rank g eliminates the clusters of its subdomains and stores only the blocks it holds
   // (it owns an endpoint).  Phase-I batches are local; before phase II and at the level end
@@ -536,6 +546,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   const bool dist = h->world > 1;
   const bool plan_apply = !dist || h->rank == 0;
   auto own = [&](int lv, int c) { return !dist || DP.own(lv, c); };
+  // Single GPU, DC: the second half of a batch is patched with the kept ranks on the device
+  // (k_patch) and launched right behind the first half; the host reads the ranks back one
+  // batch later, while that second half runs (HS_HOST_PATCH=1: synchronous host patch).
+  const bool dpatch = !dist && !nodc && std::getenv("HS_HOST_PATCH") == nullptr;
   int32_t* d_ired = nullptr;   // int32 all-reduce scratch
   int32_t* h_ired = nullptr;
   size_t ired_cap = 0;
@@ -639,6 +653,39 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
     };
 
+    // the batch whose ranks are still on their way to the host (dpatch): (s, m) of its clusters
+    std::vector<std::pair<int32_t, int32_t>> pend_cl;
+    bool pend_active = false;
+    auto finish_pending = [&]() {
+      if (!pend_active) return;
+      pend_active = false;
+      HS_CUDA(cudaEventSynchronize(ev_rank));
+      if (h_stat->flag) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "NOT_SPD: Cholesky breakdown at level %d cluster %d pivot %d value %.17g (P:283)",
+                      h_stat->level, h_stat->cluster, h_stat->pivot, h_stat->value);
+        fail(HS_E_NOT_SPD, buf);
+      }
+      pt.collect_a(S);
+      for (size_t bi = 0; bi < pend_cl.size(); ++bi) {
+        const int32_t s = pend_cl[bi].first, m = pend_cl[bi].second;
+        const int32_t r = m == 0 ? 0 : h_rank[bi];
+        L.rank[s] = r;
+        live[s] = r;
+        done[s] = 1;
+        if (m == 0) continue;
+        const int32_t K = m - r, kn = L.kn[s], kw = L.kw[s];
+        if (K == 0) L.C[s] = nullptr;   // the slab piece (sized for m rows) stays unused
+        S.max_m = std::max(S.max_m, m);
+        S.max_rank = std::max(S.max_rank, r);
+        double fq = 0.0;
+        for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
+        S.flops += fq + (double)K * kn * (kn + 1);
+        S.flops_phase[3] += fq;
+        S.flops_phase[4] += (double)K * kn * (kn + 1);
+      }
+    };
+
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
     for (size_t bidx = 0; bidx < lev.batches.size(); ++bidx) {
@@ -651,6 +698,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           for (int32_t s : lev.batches[b]) ph1[s] = 1;
         sync_ranks(ph1);
       }
+      finish_pending();   // the previous batch's ranks (its second half may still be running)
       const double tp0 = now_s();
       // shapes of every cluster of the batch from the current live sizes
       for (int32_t s : Bt) {
@@ -667,8 +715,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<CopyItem> gather;
       std::vector<CluItem> clu(nb);
       std::vector<TrsmItem> trsm, rot;
+      std::vector<FusedItem> fci, fz;   // gather-free Cholesky+inverse per cluster, scaling per tile
+      std::vector<FusedSeg> fseg;
       int max_m = 1;
       for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bo[bi]]);
+      const bool fused = !nodc && max_m <= CI_MAX_M && !no_fused;
       // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
       int64_t wsz = 0;
       std::vector<int64_t> wo(nb);
@@ -696,7 +747,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         bs.get(s, s, p, ld, tr);
         // the store keeps the lower triangle of a diagonal block; dc = 0 rotates both sides
         // of A_ss, so it is gathered as the full symmetric block (copy mode 2)
-        gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
+        if (fused && tr) fail(HS_E_INTERNAL, "diagonal block stored transposed");
+        const double* pss = p;
+        const int32_t ldss = ld;
+        if (!fused) gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
+        const int32_t seg0 = (int32_t)fseg.size();
         int32_t col = 0;
         const auto& ro = row_offs(s);
         size_t kq = 0;
@@ -706,12 +761,27 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             if (live[q] > 0) {
               if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
               bs.at(s, q, o, p, ld, tr);
-              gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+              if (fused) fseg.push_back(FusedSeg{p, ld, tr, col, live[q]});
+              else gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
             }
             col += live[q];
           }
         const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
-        for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
+        if (fused) {
+          // segments are in column order: each tile takes the run of segments overlapping it
+          int32_t sb = seg0;
+          const int32_t se = (int32_t)fseg.size();
+          fci.push_back(FusedItem{pss, L.G[s], L.V[s], L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+          for (int32_t c0 = 0; c0 < ldB; c0 += 64) {
+            const int32_t nc = std::min(64, ldB - c0);
+            while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
+            int32_t sf = sb;
+            while (sf < se && fseg[sf].col < c0 + nc) ++sf;
+            fz.push_back(FusedItem{pss, L.G[s], L.V[s], L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
+          }
+        } else {
+          for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
+        }
         if (!cpqr_single_cta && !cpqr_v2 && kw > 0) {   // v3 rotates the n-columns in k_rotate_n
           const int32_t rw = rot_tile_cols(m, max_m);
           for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
@@ -725,21 +795,29 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upA.reset();
         std::vector<unsigned long long> nmax(nb, 0ull);
         const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
-                     iM = upA.add(nmax);
+                     iM = upA.add(nmax), iF = upA.add(fz), iS = upA.add(fseg), iI = upA.add(fci);
         upA.stage.ensure(upA.total);
         upA.dev.ensure(upA.total);
         for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
+        for (auto& f : fz) f.nmax = upA.dptr<unsigned long long>(iM) + f.bi;
         upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
-        upA.copy_in(iM, nmax);
+        upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
         t_plan += now_s() - tp0;
         upA.send(st);
         HS_CUDA(cudaEventRecord(pt.a[0], st));
-        launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
-        HS_CUDA(cudaEventRecord(pt.a[1], st));
-        if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
-        HS_CUDA(cudaEventRecord(pt.a[2], st));
-        if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
-        else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), st);   // R-floor
+        if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
+          HS_CUDA(cudaEventRecord(pt.a[1], st));
+          launch_chol(upA.dptr<FusedItem>(iI), (int)fci.size(), max_m, d_status, st);
+          HS_CUDA(cudaEventRecord(pt.a[2], st));
+          launch_scale_tiles(upA.dptr<FusedItem>(iF), (int)fz.size(), upA.dptr<FusedSeg>(iS), max_m, st);
+        } else {
+          launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
+          HS_CUDA(cudaEventRecord(pt.a[1], st));
+          if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
+          HS_CUDA(cudaEventRecord(pt.a[2], st));
+          if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
+          else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), st);   // R-floor
+        }
         HS_CUDA(cudaEventRecord(pt.a[3], st));
         d_clu_batch = upA.dptr<CluItem>(iC);
         if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
@@ -750,6 +828,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         HS_CUDA(cudaEventRecord(pt.a[4], st));
         HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+        if (dpatch) {
+          HS_CUDA(cudaMemcpyAsync(h_stat, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+          HS_CUDA(cudaEventRecord(ev_rank, st));
+        }
       } else {
         t_plan += now_s() - tp0;
       }
@@ -853,16 +935,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         pend.push_back(pd);
       }
       t_sub[0] += now_s() - tpp;
-      if (nb > 0) {
+      if (nb > 0 && !dpatch) {
         check_status(d_status, &h_status, st);       // synchronises the stream
         pt.collect(S);
       }
       deferred.drain(false);
       const double tp1 = now_s();
-      for (int bi = 0; bi < nb; ++bi) {
-        const int32_t s = Bo[bi];
-        L.rank[s] = live[s] == 0 ? 0 : h_rank[bi];
-      }
+      if (!dpatch)
+        for (int bi = 0; bi < nb; ++bi) {
+          const int32_t s = Bo[bi];
+          L.rank[s] = live[s] == 0 ? 0 : h_rank[bi];
+        }
       if (nodc && nb > 0) {
         // (U^T A_ss U) in G; L_f L_f^T = its fine block; C_c = L_f^{-1} G[r:, :r] in place,
         // C_n = L_f^{-1} (U^T A_sn)_f in B; [A_cc | A_cn] -= C_c^T [C_c | C_n]
@@ -937,7 +1020,61 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         comm_group_end(h->comm, st);
       }
       // ---- Schur update, write-back: patch the pre-planned records with the ranks ----------
+      // dpatch: the patch items (target = section + index, resolved after the upload layout)
+      struct PRef {
+        PatchItem it;
+        int sec;       // 0 srcs, 1 wb, 2 id_r, 3 ft
+        size_t idx;
+      };
+      std::vector<PRef> prefs;
+      if (dpatch) {
+        if (nb != (int)Bt.size()) fail(HS_E_INTERNAL, "device patch: batch not fully owned");
+        for (auto& pd : pend) {
+          const int32_t s = pd.s;
+          const double* Bs = L.B[s];
+          const int32_t m = live_at[pd.k], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
+          PatchItem base{nullptr, Bs, pd.k, PK_SRC, m, ldB, kw, 0, 0, 0};
+          if (pd.src >= 0) {
+            srcs[pd.src].C = Bs + kw;
+            srcs[pd.src].K = 0;
+            prefs.push_back({base, 0, (size_t)pd.src});
+          }
+          for (size_t i = pd.wb_begin; i < pd.wb_end; ++i) {
+            CopyItem& c = wb[i];
+            c.src = Bs + (uintptr_t)c.src;
+            PatchItem q = base;
+            q.kind = c.trans ? PK_COLS : PK_ROWS;
+            prefs.push_back({q, 1, i});
+          }
+          if (pd.id >= 0) {
+            PatchItem q = base;
+            q.kind = PK_I32;
+            prefs.push_back({q, 2, (size_t)pd.id});
+          }
+          if (pd.ft >= 0) {
+            PatchItem q = base;
+            q.kind = PK_FT;
+            prefs.push_back({q, 3, (size_t)pd.ft});
+          }
+          if (kn > 0) {   // C_s = B_s[r:, kw:] into a slab piece sized for K <= m rows
+            L.C[s] = cslab.get((int64_t)m * kn);
+            const int32_t step = std::max(1, 16384 / kn);
+            for (int32_t i0 = 0; i0 < m; i0 += step) {
+              PatchItem q = base;
+              q.kind = PK_CCOPY;
+              q.i0 = i0;
+              q.step = step;
+              prefs.push_back({q, 1, wb.size()});
+              wb.push_back(CopyItem{Bs + kw, L.C[s] + (int64_t)i0 * kn, ldB, kn, 0, kn, 0, 0});
+            }
+          }
+        }
+        pend_cl.clear();
+        for (size_t k = 0; k < Bt.size(); ++k) pend_cl.emplace_back(Bt[k], live_at[k]);
+        pend_active = nb > 0;
+      }
       for (auto& pd : pend) {
+        if (dpatch) break;
         const int32_t s = pd.s;
         const double* Bs = pd.mine ? L.B[s] : rbuf[pd.k];
         if (!pd.mine && !Bs) continue;
@@ -1001,25 +1138,42 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         tiles.insert(tiles.end(), wv.begin(), wv.end());
         wave_off.push_back((int32_t)tiles.size());
       }
-      for (int32_t s : Bt)
-        if (own(l, s) || (dist && phase2)) {   // the rank of s is known here
-          live[s] = L.rank[s];
-          done[s] = 1;
-        }
+      if (!dpatch)
+        for (int32_t s : Bt)
+          if (own(l, s) || (dist && phase2)) {   // the rank of s is known here
+            live[s] = L.rank[s];
+            done[s] = 1;
+          }
       t_sub[3] += now_s() - tq3;
       const bool second = !srcs.empty() || !wb.empty() || !id_ptr.empty() || !ft.empty();
       if (second) {
-        split_copies(wb);
+        if (!dpatch) split_copies(wb);   // dpatch: item indices are patch targets (C copies pre-split)
         upB.reset();
+        std::vector<PatchItem> patch(prefs.size());
         const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
-                     jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft);
+                     jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft),
+                     jX = upB.add(patch);
         upB.stage.ensure(upB.total);
         upB.dev.ensure(upB.total);
+        for (size_t i = 0; i < prefs.size(); ++i) {
+          PatchItem q = prefs[i].it;
+          const size_t x = prefs[i].idx;
+          switch (prefs[i].sec) {
+            case 0: q.target = upB.dptr<SchurSrc>(jS) + x; break;
+            case 1: q.target = upB.dptr<CopyItem>(jW) + x; break;
+            case 2: q.target = upB.dptr<int32_t>(jR) + x; break;
+            default: q.target = upB.dptr<FormTItem>(jF) + x; break;
+          }
+          patch[i] = q;
+        }
         upB.copy_in(jT, tiles); upB.copy_in(jS, srcs); upB.copy_in(jN, nbc); upB.copy_in(jW, wb);
         upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
+        upB.copy_in(jX, patch);
         t_plan += now_s() - tp1;
         upB.send(st);
+        pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         HS_CUDA(cudaEventRecord(pt.b[0], st));
+        launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
         launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
@@ -1087,6 +1241,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
       }
     }
+    finish_pending();
     // ---- every rank learns every kept rank; the records go to rank 0 (dist) -----------------
     const double tp2 = now_s();
     if (dist) {

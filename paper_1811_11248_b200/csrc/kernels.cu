@@ -967,6 +967,39 @@ void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32
   k_symcheck<<<(int)std::min<int64_t>((nnz + 255) / 256, 148 * 16), 256, 0, st>>>(vals, tmap, nnz, flag);
   count_launch(1);
 }
+namespace {
+__global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const PatchItem p = items[i];
+  const int r = p.m == 0 ? 0 : rank[p.bi], K = p.m - r;
+  switch (p.kind) {
+    case PK_SRC: {   // C_s = B_s[r:, kw:], K fine rows (a full rank leaves a phantom source)
+      SchurSrc* t = (SchurSrc*)p.target;
+      t->C = p.base + (int64_t)r * p.ldB + p.kw;
+      t->K = K;
+      break;
+    }
+    case PK_ROWS: ((CopyItem*)p.target)->rows = r; break;
+    case PK_COLS: ((CopyItem*)p.target)->cols = r; break;
+    case PK_I32: *(int32_t*)p.target = r; break;
+    case PK_FT: ((FormTItem*)p.target)->r = r; break;
+    case PK_CCOPY: {   // rows [i0, i0 + step) of C_s into its slab
+      CopyItem* t = (CopyItem*)p.target;
+      t->src = p.base + (int64_t)(r + p.i0) * p.ldB + p.kw;
+      t->rows = max(0, min(p.step, K - p.i0));
+      break;
+    }
+  }
+}
+}  // namespace
+
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st) {
+  if (n <= 0) return;
+  k_patch<<<(n + 127) / 128, 128, 0, st>>>(d_items, n, d_rank);
+  count_launch(1);
+}
+
 void split_copies(std::vector<CopyItem>& items) {
   constexpr int64_t PIECE = 16384;
   bool big = false;
