@@ -162,12 +162,14 @@ struct FwdTask {             // a group of targets of source s; `first` also emi
 struct BwdNb {               // neighbour q: columns [col, col+len) of C_s read x from `x`
   const double* x;
   int32_t q, col, len, later;   // later: q eliminated after s at this level (wait for it)
+  int32_t off, pad;             // position of q's columns inside its backward chunk
 };
-struct BwdTask {             // columns [c0, c0+nc) of C_s x_n -> partial sums
-  int32_t s, c0, nc, chunk;
+struct BwdTask {             // neighbours bnb[b0, b1) of s (nc columns in all) -> partial sums
+  int32_t s, b0, b1, nc, chunk, pad;
 };
 constexpr int APPLY_THREADS = 256;
 constexpr int BWD_COLS = 512;        // columns of C per backward task
+constexpr int BWD_CRIT = 2;          // later neighbours with a backward chunk of their own
 constexpr int FWD_COLS = 256;        // target columns per forward task
 struct ApplyLevelArgs {
   const ApplySrc* src;
@@ -187,6 +189,8 @@ struct ApplyLevelArgs {
   int32_t* arr;              // forward: contributions arrived per target (nclus)
   int32_t* ticket;           // [0] forward, [1] backward
   int32_t nftask, nbtask;
+  int32_t flags, pad;        // experiment switches (HS_APPLY_FLAGS)
+  long long* trace;          // HS_APPLY_TRACE: 8 globaltimer stamps per task (profiling only)
 };
 
 // First error raised on the device (POTRF breakdown).

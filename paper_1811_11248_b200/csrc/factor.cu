@@ -1340,6 +1340,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<std::vector<BwdTask>> bwd_batches;
       std::vector<int64_t> foff(lev.nclus, 0);
       const double ta = now_s();
+      std::vector<int32_t> bpos(lev.nclus, 0);   // batch index of each cluster
+      for (size_t b = 0; b < lev.batches.size(); ++b)
+        for (int32_t c : lev.batches[b]) bpos[c] = (int32_t)b;
       for (const auto& Bt : lev.batches) {
         if (level_dofs == 0) break;
         bwd_batches.emplace_back();
@@ -1366,10 +1369,18 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             (proc[q] ? post[q] : pre[q]).push_back(PullSrc{slots, s, 0});
             AP.ctb.push_back(Contrib{slots, noff[a], lv2[q], q, proc[q] ? 0 : 1});
             slots += lv2[q];
-            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1});
+            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1, 0, 0});
           }
           as.tg_end = (int32_t)AP.ctb.size();
           as.nb_end = (int32_t)AP.bnb.size();
+          // produce order: the targets eliminated soonest first (T(s) produces the first
+          // group itself, so the next cluster on the chain waits for one task, not two);
+          // the order in which a target subtracts its contributions is its pre list's
+          std::stable_sort(AP.ctb.begin() + as.tg_begin, AP.ctb.begin() + as.tg_end,
+                           [&](const Contrib& x, const Contrib& y) {
+                             const int32_t bx = x.pre ? bpos[x.q] : INT32_MAX, by = y.pre ? bpos[y.q] : INT32_MAX;
+                             return bx < by;
+                           });
           // T(s) with s's first contribution group, then the other groups (<= FWD_COLS
           // columns / 16 targets each) as tasks of their own
           if (as.tg_begin == as.tg_end) AP.ftask.push_back(FwdTask{s, as.tg_begin, as.tg_end, 1});
@@ -1381,14 +1392,34 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             g0 = g1;
           }
           as.part = AP.parts;
-          if (K > 0 && kn > 0) {
-            as.nchunk = (kn + BWD_COLS - 1) / BWD_COLS;
-            for (int32_t c = 0; c < as.nchunk; ++c)
-              bwd_tasks.push_back(BwdTask{s, c * BWD_COLS, std::min(BWD_COLS, kn - c * BWD_COLS), c});
+          if (K > 0 && kn > 0 && as.nb_end > as.nb_begin) {
+            // backward chunks by readiness: neighbours eliminated before s (final at the
+            // level start), then the later ones latest-eliminated first (they finish first
+            // in the reverse sweep); the last BWD_CRIT later neighbours — the critical path
+            // of the sweep — get a chunk of their own, the rest are packed to BWD_COLS
+            std::stable_sort(AP.bnb.begin() + as.nb_begin, AP.bnb.begin() + as.nb_end,
+                             [&](const BwdNb& x, const BwdNb& y) {
+                               const int32_t kx = x.later ? INT32_MAX - bpos[x.q] : -1;
+                               const int32_t ky = y.later ? INT32_MAX - bpos[y.q] : -1;
+                               return kx < ky;
+                             });
+            int32_t nlater = 0;
+            for (int32_t b = as.nb_begin; b < as.nb_end; ++b) nlater += AP.bnb[b].later;
+            const int32_t crit0 = as.nb_end - std::min<int32_t>(nlater, BWD_CRIT);
+            as.nchunk = 0;
+            for (int32_t b0 = as.nb_begin; b0 < as.nb_end;) {
+              int32_t b1 = b0, cols = 0;
+              while (b1 < as.nb_end && (b1 == b0 || (b1 < crit0 && b0 < crit0 && cols + AP.bnb[b1].len <= BWD_COLS))) {
+                AP.bnb[b1].off = cols;
+                cols += AP.bnb[b1++].len;
+              }
+              bwd_tasks.push_back(BwdTask{s, b0, b1, cols, as.nchunk++, 0});
+              b0 = b1;
+            }
             AP.parts += (int64_t)as.nchunk * K;
           } else {
             as.nchunk = 1;
-            bwd_tasks.push_back(BwdTask{s, 0, 0, 0});
+            bwd_tasks.push_back(BwdTask{s, 0, 0, 0, 0, 0});
           }
           foff[s] = ap.ftotal;
           ap.ftotal += K;

@@ -6,6 +6,8 @@
 //   permute-out.
 // PCG (north_star) keeps every scalar on the device; the only host
 // synchronisation per iteration is the 8-byte read of ||r||^2 for the stopping test.
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -126,6 +128,9 @@ void dot(const double* a, const double* b, int64_t n, double* partial, double* o
   count_launch(2);
 }
 
+long long* g_trace = nullptr;   // HS_APPLY_TRACE (profile_apply only)
+int g_trace_level = -1;
+
 ApplyLevelArgs level_args(hs_factor_s* f, int l) {
   ApplyPlan& ap = f->ap;
   const ApplyLevelPlan& P = ap.lv[l];
@@ -149,6 +154,9 @@ ApplyLevelArgs level_args(hs_factor_s* f, int l) {
   a.ticket = a.cnt + 4 * n;
   a.nftask = (int32_t)P.ftask.size();
   a.nbtask = (int32_t)P.btask.size();
+  static const int flags = std::getenv("HS_APPLY_FLAGS") ? std::atoi(std::getenv("HS_APPLY_FLAGS")) : 0;
+  a.flags = flags;
+  a.trace = l == g_trace_level ? g_trace : nullptr;
   return a;
 }
 
@@ -167,6 +175,8 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   };
   mark();
   if (ap.ctr_total) HS_CUDA(cudaMemsetAsync(ap.d_ctr, 0, sizeof(int32_t) * ap.ctr_total, st));
+  // forward contribution slots start empty (all-ones NaN, polled by the consumers)
+  if (ap.contrib_total) HS_CUDA(cudaMemsetAsync(ap.d_contrib, 0xFF, sizeof(double) * ap.contrib_total, st));
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
     mark();
@@ -204,6 +214,63 @@ void profile_apply(hs_factor_s* f, cudaStream_t st) {
                  f->ap.lv[L - 1 - k].btask.size());
   std::fprintf(stderr, "[hs profile]   permute-out %.3f ms\n", el(2 + 2 * L));
   for (auto e : ev) cudaEventDestroy(e);
+  if (const char* tl = std::getenv("HS_APPLY_TRACE")) {   // per-task phase stamps of one level
+    const int lt = std::atoi(tl);
+    if (lt < 0 || lt >= L) return;
+    const ApplyLevelPlan& P = f->ap.lv[lt];
+    const size_t nt = P.ftask.size() + P.btask.size();
+    HS_CUDA(cudaMalloc(&g_trace, sizeof(long long) * 8 * std::max<size_t>(nt, 1)));
+    HS_CUDA(cudaMemset(g_trace, 0, sizeof(long long) * 8 * std::max<size_t>(nt, 1)));
+    g_trace_level = lt;
+    record_apply(f, st);
+    HS_CUDA(cudaStreamSynchronize(st));
+    std::vector<long long> tr(8 * nt);
+    HS_CUDA(cudaMemcpy(tr.data(), g_trace, sizeof(long long) * 8 * nt, cudaMemcpyDeviceToHost));
+    cudaFree(g_trace);
+    g_trace = nullptr;
+    g_trace_level = -1;
+    const size_t nf = P.ftask.size();
+    // forward T tasks: claim->wait, wait->pull, pull->gemv, gemv->produce, produce->publish
+    double acc[5] = {0, 0, 0, 0, 0};
+    int nT = 0;
+    long long t0 = LLONG_MAX, t1 = 0;
+    for (size_t k = 0; k < nf; ++k) {
+      const long long* x = &tr[8 * k];
+      t0 = std::min(t0, x[0]);
+      t1 = std::max(t1, x[5]);
+      if (!P.ftask[k].first) continue;
+      ++nT;
+      for (int j = 0; j < 5; ++j) acc[j] += (double)(x[j + 1] - x[j]);
+    }
+    std::fprintf(stderr, "[hs trace] fwd level %d: span %.1f us, %d T tasks, mean ns: wait %.0f pull %.0f gemv %.0f "
+                 "produce %.0f publish %.0f\n", lt, (t1 - t0) * 1e-3, nT, acc[0] / nT, acc[1] / nT, acc[2] / nT,
+                 acc[3] / nT, acc[4] / nT);
+    double bacc[3] = {0, 0, 0};
+    int nfin = 0;
+    long long b0 = LLONG_MAX, b1 = 0;
+    for (size_t k = nf; k < nt; ++k) {
+      const long long* x = &tr[8 * k];
+      b0 = std::min(b0, x[0]);
+      b1 = std::max(b1, std::max(x[3], x[2]));
+      if (x[1]) bacc[0] += (double)(x[1] - x[0]);
+      if (x[2]) bacc[1] += (double)(x[2] - x[1]);
+      if (x[3] && x[2]) {
+        bacc[2] += (double)(x[3] - x[2]);
+        ++nfin;
+      }
+    }
+    const double nb = (double)(nt - nf);
+    std::fprintf(stderr, "[hs trace] bwd level %d: span %.1f us, %zu tasks, mean ns: wait %.0f partial %.0f; finish %.0f (%d)\n",
+                 lt, (b1 - b0) * 1e-3, nt - nf, bacc[0] / nb, bacc[1] / nb, nfin ? bacc[2] / nfin : 0.0, nfin);
+    // the forward chain: consecutive T tasks, gap between a T's publish and the next T's wait exit
+    if (std::getenv("HS_APPLY_TRACE_DUMP")) {
+      for (size_t k = 0; k < nf; ++k) {
+        const long long* x = &tr[8 * k];
+        std::fprintf(stderr, "[hs trace] f %zu s %d first %d: %lld %lld %lld %lld %lld %lld\n", k, P.ftask[k].s,
+                     P.ftask[k].first, x[0] - t0, x[1] - t0, x[2] - t0, x[3] - t0, x[4] - t0, x[5] - t0);
+      }
+    }
+  }
 }
 
 void ensure_vectors(hs_factor_s* f) {

@@ -30,10 +30,23 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
 __device__ __forceinline__ void wait_ge(const int32_t* p, int32_t v) {
   while (ld_acquire(p) < v) __nanosleep(32);
 }
+// Forward contribution slots are reset to an all-ones NaN before every apply: no FP64
+// arithmetic result has that bit pattern (results are canonical NaNs), so a slot holding
+// anything else holds its final value, and a consumer can poll the values themselves
+// instead of a counter (no fence or atomic on the producer's path).
+constexpr unsigned long long CONTRIB_EMPTY = 0xFFFFFFFFFFFFFFFFull;
+__device__ __forceinline__ double ld_poll(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  while (v == CONTRIB_EMPTY) {
+    __nanosleep(32);
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  }
+  return __longlong_as_double((long long)v);
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-constexpr int NB_SMEM = 512;   // neighbour tables up to this size are staged in shared memory
 
 // Forward sweep of one level (Algorithm 2 lines 3-6 for every cluster of the level, in the
 // batch order of the factor), produce-then-pull.  Two task kinds, ticketed in elimination
@@ -47,92 +60,193 @@ constexpr int NB_SMEM = 512;   // neighbour tables up to this size are staged in
 // subtracted by k_apply_post after the level.  Every entry is accumulated in the factor's
 // event order, so the sweep is deterministic and equal to the sequential Algorithm 2 loop;
 // no target waits on another target's update.
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define AP_TR(t, k)                                            \
+  do {                                                         \
+    if (a.trace && threadIdx.x == 0) a.trace[(int64_t)(t) * 8 + (k)] = gtime(); \
+  } while (0)
 constexpr int PRE_SMEM = 1024;   // pre-contribution slots staged in shared memory
 
+// contrib(s -> q) = C_s[:, cols(q)]^T y_f for the group's targets (a warp per target); the
+// first nst targets read C from shared memory (sC + soff[j], ld = the target's width)
 __device__ __forceinline__ void produce(const ApplyLevelArgs& a, const ApplySrc& S, int K, const double* zf, int g0,
-                                        int g1) {
+                                        int g1, const double* sC = nullptr, const int* soff = nullptr, int nst = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = APPLY_THREADS / 32;
   for (int g = g0 + warp; g < g1; g += nw) {
     const Contrib c = a.ctb[g];
+    const bool st = g - g0 < nst;
     for (int i = lane; i < c.len; i += 32) {
-      const double* Ci = S.C + c.col + i;
       double acc = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * zf[k];
-      a.contrib[c.slot + i] = acc;
+      if (st) {
+        const double* Ci = sC + soff[g - g0] + i;
+        for (int k = 0; k < K; ++k) acc += Ci[k * c.len] * zf[k];
+      } else {
+        const double* Ci = S.C + c.col + i;
+        int k = 0;
+        for (; k + 8 <= K; k += 8) {   // 8 loads in flight, accumulated in k order
+          double cv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cv[u] = Ci[(int64_t)(k + u) * S.ldC];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += cv[u] * zf[k + u];
+        }
+        for (; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * zf[k];
+      }
+      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.contrib + c.slot + i), "d"(acc) : "memory");
     }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0 && c.pre) atomicAdd(a.arr + c.q, 1);
+    if (a.flags & 4) {   // counter mode (previous protocol, A/B switch)
+      __threadfence();
+      __syncwarp();
+      if (lane == 0 && c.pre) atomicAdd(a.arr + c.q, 1);
+    }
   }
 }
+
+// the L2 lines of a contribution group's columns of C_s (targets in any column order)
+__device__ __forceinline__ void prefetch_group(const ApplyLevelArgs& a, const ApplySrc& S, int K, int g0, int g1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = APPLY_THREADS / 32;
+  for (int g = g0; g < g1; ++g) {
+    const Contrib c = a.ctb[g];
+    for (int k = warp; k < K; k += nw)
+      for (int cc = lane * 16; cc < c.len; cc += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c.col + cc);
+  }
+}
+
+constexpr int PRE_BUF = 1024;   // pre-contribution values staged per round (doubles)
+static_assert(MAX_M < PRE_BUF, "a round holds at least one contribution");
+constexpr int PSUM = 512;       // partial sums of a round (np x m)
+constexpr int FWD_STAGE = 3072; // T_s and the first targets' C columns, loaded while T(s) waits (doubles)
 
 __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
   __shared__ double ys[MAX_M];
   __shared__ double z[MAX_M];
   __shared__ int64_t pslot[PRE_SMEM];
+  __shared__ double pbuf[PRE_BUF];
+  __shared__ double psum[PSUM];
   __shared__ int s_task;
+  __shared__ int soff[16];
+  extern __shared__ double stg[];   // FWD_STAGE doubles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(a.ticket, 1);
     __syncthreads();
     const int t = s_task;
     if (t >= a.nftask) return;
+    AP_TR(t, 0);
     const FwdTask tk = a.ftask[t];
     const int s = tk.s;
     const ApplySrc S = a.src[s];
     const int m = S.m, r = S.r, K = m - r;
     if (tk.first) {   // ---- T(s) and s's first contribution group
-      for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
-      if (tk.t_end > tk.t_begin) {
-        const Contrib c0 = a.ctb[tk.t_begin], c1 = a.ctb[tk.t_end - 1];
-        for (int k = warp; k < K; k += nw)
-          for (int c = c0.col + lane * 16; c < c1.col + c1.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
+      // while the contributions to y_s are outstanding: T_s and the C columns of the first
+      // targets (the next hops of the chain) into shared memory, the rest into L2
+      const bool tst = m * m <= FWD_STAGE;
+      int used = tst ? m * m : 0, nst = 0;
+      for (int g = tk.t_begin; g < tk.t_end && nst < 16; ++g) {
+        const int len = a.ctb[g].len;
+        if (used + K * len > FWD_STAGE) break;
+        if (tid == 0) soff[nst] = used;
+        used += K * len;
+        ++nst;
       }
+      if (tst)
+        for (int e = tid; e < m * m; e += APPLY_THREADS) stg[e] = S.T[e];
+      else
+        for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
+      {
+        int off = tst ? m * m : 0;
+        for (int j = 0; j < nst; ++j) {
+          const Contrib c = a.ctb[tk.t_begin + j];
+          for (int e = tid; e < K * c.len; e += APPLY_THREADS) {
+            const int k = e / c.len, i = e - k * c.len;
+            stg[off + e] = S.C[(int64_t)k * S.ldC + c.col + i];
+          }
+          off += K * c.len;
+        }
+      }
+      prefetch_group(a, S, K, tk.t_begin + nst, tk.t_end);
       const int npre = S.pre_end - S.pre_begin;
       const bool staged = npre <= PRE_SMEM;
       if (staged)
         for (int e = tid; e < npre; e += APPLY_THREADS) pslot[e] = a.pull[S.pre_begin + e].slot;
-      if (tid == 0) wait_ge(a.arr + s, npre);
+      const bool poll = !(a.flags & 4);
+      if (!poll && tid == 0) wait_ge(a.arr + s, npre);
       __syncthreads();
-      for (int i = tid; i < m; i += APPLY_THREADS) {
-        double v = __ldcg(S.y + i);
-        int e = 0;
-        for (; e + 8 <= npre; e += 8) {   // 8 loads in flight, subtracted in order
-          double c[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            c[u] = __ldcg(a.contrib + (staged ? pslot[e + u] : a.pull[S.pre_begin + e + u].slot) + i);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v -= c[u];
+      AP_TR(t, 1);
+      // y_s minus its pre-contributions in elimination order: rounds of up to PRE_BUF values
+      // loaded by the whole CTA at once, then summed per entry from shared memory
+      const int per = PRE_BUF / max(m, 1);   // m <= MAX_M < PRE_BUF
+      // entry i's values of a round are summed by np threads (interleaved subsets, each in
+      // order), then combined in subset order: a fixed order for a given m (deterministic)
+      const int np = (a.flags & 1) ? 1 : max(1, min(APPLY_THREADS / max(m, 1), (int)(PSUM / max(m, 1))));
+      {
+        for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
+        for (int e0 = 0; e0 < npre; e0 += per) {
+          const int ne = min(per, npre - e0);
+          for (int x = tid; x < ne * m; x += APPLY_THREADS) {
+            const int e = e0 + x / m, i = x % m;
+            const double* src = a.contrib + (staged ? pslot[e] : a.pull[S.pre_begin + e].slot) + i;
+            pbuf[x] = poll ? ld_poll(src) : __ldcg(src);
+          }
+          __syncthreads();
+          if (np > 1) {
+            if (tid < np * m) {
+              const int i = tid % m, pp = tid / m;
+              double v = 0.0;
+              for (int e = pp; e < ne; e += np) v += pbuf[e * m + i];
+              psum[pp * m + i] = v;
+            }
+            __syncthreads();
+            for (int i = tid; i < m; i += APPLY_THREADS) {
+              double v = ys[i];
+              for (int pp = 0; pp < np; ++pp) v -= psum[pp * m + i];
+              ys[i] = v;
+            }
+          } else {
+            for (int i = tid; i < m; i += APPLY_THREADS) {
+              double v = ys[i];
+              for (int e = 0; e < ne; ++e) v -= pbuf[e * m + i];
+              ys[i] = v;
+            }
+          }
+          __syncthreads();
         }
-        for (; e < npre; ++e) v -= __ldcg(a.contrib + (staged ? pslot[e] : a.pull[S.pre_begin + e].slot) + i);
-        ys[i] = v;
       }
       __syncthreads();
+      AP_TR(t, 2);
       for (int i = warp; i < m; i += nw) {
-        const double* Ti = S.T + (int64_t)i * m;
+        const double* Ti = tst ? stg + i * m : S.T + (int64_t)i * m;
         double acc = 0.0;
         for (int j = lane; j < m; j += 32) acc += Ti[j] * ys[j];
         acc = wsum(acc);
         if (lane == 0) z[i] = acc;
       }
       __syncthreads();
+      // the first group (the targets eliminated soonest: the next hop of the chain) before
+      // the outputs that only the other groups and the parent level read
+      AP_TR(t, 3);
+      if (!(a.flags & 2)) produce(a, S, K, z + r, tk.t_begin, tk.t_end, stg, soff, nst);
+      AP_TR(t, 4);
       for (int i = tid; i < r; i += APPLY_THREADS) S.yc[i] = z[i];
       for (int k = tid; k < K; k += APPLY_THREADS) S.yf[k] = z[r + k];
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicExch(a.cnt + s, 1);
-      produce(a, S, K, z + r, tk.t_begin, tk.t_end);
+      if (a.flags & 2) produce(a, S, K, z + r, tk.t_begin, tk.t_end, stg, soff, nst);
+      AP_TR(t, 5);
     } else {          // ---- P(s, group)
-      const Contrib c0 = a.ctb[tk.t_begin], c1 = a.ctb[tk.t_end - 1];
-      for (int k = warp; k < K; k += nw)
-        for (int c = c0.col + lane * 16; c < c1.col + c1.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + c);
+      prefetch_group(a, S, K, tk.t_begin, tk.t_end);
       if (tid == 0) wait_ge(a.cnt + s, 1);
       __syncthreads();
+      AP_TR(t, 1);
       for (int k = tid; k < K; k += APPLY_THREADS) z[k] = __ldcg(S.yf + k);
       __syncthreads();
       produce(a, S, K, z, tk.t_begin, tk.t_end);
+      AP_TR(t, 5);
     }
     __syncthreads();   // s_task, ys, z reusable
   }
@@ -151,15 +265,15 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_post(ApplyLevelArgs a) 
 }
 
 // Backward sweep of one level (Algorithm 2 backward substitution, reverse batch order).
-// Task (s, columns [c0, c0+nc) of C_s): wait for the neighbours eliminated after s whose
-// columns overlap the chunk, then partial sums p[k] = sum_c C_s[k][c] x_n[c].  The last
-// chunk of s to arrive finishes s: x_f = y_f - sum of the partials (chunk order),
-// x_s = T_s^T [x_c; x_f], and publishes done[s].
+// Task (s, neighbours bnb[b0, b1) of s): wait for those eliminated after s, then partial
+// sums p[k] = sum over their columns c of C_s[k][c] x_n[c].  The last chunk of s to arrive
+// finishes s: x_f = y_f - sum of the partials (chunk order), x_s = T_s^T [x_c; x_f], and
+// publishes done[s].  Chunks follow the neighbours' readiness (host plan), so the chunk
+// that waits for the last neighbour is small.
 __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
   __shared__ double xn[BWD_COLS];
+  __shared__ int ccol[BWD_COLS];
   __shared__ double u[MAX_M];
-  __shared__ int ncol[NB_SMEM];
-  __shared__ const double* nx[NB_SMEM];
   __shared__ int s_task, s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
   for (;;) {
@@ -167,49 +281,45 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
     __syncthreads();
     const int t = s_task;
     if (t >= a.nbtask) return;
+    const int tt = a.nftask + t;
+    AP_TR(tt, 0);
     const BwdTask tk = a.btask[t];
     const ApplySrc S = a.src[tk.s];
     const int m = S.m, r = S.r, K = m - r;
     if (tk.nc > 0) {
-      const int c1 = tk.c0 + tk.nc;
-      const int nnb = S.nb_end - S.nb_begin;
-      const bool staged = nnb <= NB_SMEM;
-      for (int b = tid; b < nnb; b += APPLY_THREADS) {   // neighbour table -> smem; wait for later ones
-        const BwdNb nb = a.bnb[S.nb_begin + b];
-        if (staged) {
-          ncol[b] = nb.col;
-          nx[b] = nb.x;
-        }
-        if (nb.later && nb.col < c1 && nb.col + nb.len > tk.c0) wait_ge(a.done + nb.q, 1);
+      const int nnb = tk.b1 - tk.b0;
+      // prefetch T_s (for the finish) and the chunk's columns of C_s, then wait
+      for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
+      for (int b = 0; b < nnb; ++b) {
+        const BwdNb nb = a.bnb[tk.b0 + b];
+        for (int k = warp; k < K; k += nw)
+          for (int c = lane * 16; c < nb.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + nb.col + c);
       }
-      // prefetch the chunk's rows of C while the neighbours finish
-      for (int k = warp; k < K; k += nw)
-        for (int c = lane * 16; c < tk.nc; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + tk.c0 + c);
+      for (int b = tid; b < nnb; b += APPLY_THREADS) {
+        const BwdNb nb = a.bnb[tk.b0 + b];
+        if (nb.later) wait_ge(a.done + nb.q, 1);
+      }
       __syncthreads();
-      for (int c = tid; c < tk.nc; c += APPLY_THREADS) {   // gather x_n: owner by binary search
-        const int cc = tk.c0 + c;
-        int lo = 0, hi = nnb - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          const int col = staged ? ncol[mid] : a.bnb[S.nb_begin + mid].col;
-          if (col <= cc) lo = mid;
-          else hi = mid - 1;
+      AP_TR(tt, 1);
+      for (int b = warp; b < nnb; b += nw) {   // gather x_n and the column map
+        const BwdNb nb = a.bnb[tk.b0 + b];
+        for (int i = lane; i < nb.len; i += 32) {
+          xn[nb.off + i] = __ldcg(nb.x + i);
+          ccol[nb.off + i] = nb.col + i;
         }
-        const int col = staged ? ncol[lo] : a.bnb[S.nb_begin + lo].col;
-        const double* x = staged ? nx[lo] : a.bnb[S.nb_begin + lo].x;
-        xn[c] = __ldcg(x + (cc - col));
       }
       __syncthreads();
       double* part = a.parts + S.part + (int64_t)tk.chunk * K;
       for (int k = warp; k < K; k += nw) {
-        const double* Ck = S.C + (int64_t)k * S.ldC + tk.c0;
+        const double* Ck = S.C + (int64_t)k * S.ldC;
         double acc = 0.0;
-        for (int c = lane; c < tk.nc; c += 32) acc += Ck[c] * xn[c];
+        for (int c = lane; c < tk.nc; c += 32) acc += Ck[ccol[c]] * xn[c];
         acc = wsum(acc);
         if (lane == 0) part[k] = acc;
       }
       __threadfence();
       __syncthreads();
+      AP_TR(tt, 2);
       if (tid == 0) s_last = (atomicAdd(a.bcnt + tk.s, 1) == S.nchunk - 1);
       __syncthreads();
       if (!s_last) continue;
@@ -226,12 +336,21 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
     __syncthreads();
     for (int i = tid; i < m; i += APPLY_THREADS) {
       double acc = 0.0;
-      for (int j = 0; j < m; ++j) acc += S.T[(int64_t)j * m + i] * u[j];
+      int j = 0;
+      for (; j + 8 <= m; j += 8) {   // 8 loads in flight, accumulated in j order
+        double tv[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) tv[w] = S.T[(int64_t)(j + w) * m + i];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += tv[w] * u[j + w];
+      }
+      for (; j < m; ++j) acc += S.T[(int64_t)j * m + i] * u[j];
       S.x[i] = acc;
     }
     __threadfence();
     __syncthreads();
     if (tid == 0) atomicExch(a.done + tk.s, 1);
+    AP_TR(tt, 3);
   }
 }
 
@@ -288,7 +407,9 @@ static int apply_grid(const void* fn, int ntask) {
   static int per_sm[2] = {0, 0}, nsm = 0;
   const int k = fn == (const void*)k_apply_fwd ? 0 : 1;
   if (!per_sm[k]) {
-    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], fn, APPLY_THREADS, 0));
+    const size_t dyn = k == 0 ? sizeof(double) * FWD_STAGE : 0;
+    if (dyn) set_smem_attr(fn, dyn);
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], fn, APPLY_THREADS, dyn));
     int dev = 0;
     HS_CUDA(cudaGetDevice(&dev));
     HS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -298,7 +419,7 @@ static int apply_grid(const void* fn, int ntask) {
 }
 void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
   if (a.nftask <= 0) return;
-  k_apply_fwd<<<apply_grid((const void*)k_apply_fwd, a.nftask), APPLY_THREADS, 0, st>>>(a);
+  k_apply_fwd<<<apply_grid((const void*)k_apply_fwd, a.nftask), APPLY_THREADS, sizeof(double) * FWD_STAGE, st>>>(a);
   count_launch(1);
 }
 void launch_apply_post_level(const ApplyLevelArgs& a, cudaStream_t st) {
