@@ -132,7 +132,8 @@ struct ApplySrc {
   const double* y;           // live segment at elimination (level vector), m entries
   double* yc;                // coarse destination (parent level vector), r entries
   double* yf;                // fine buffer, K = m - r entries
-  double* x;                 // backward output (level vector segment, = y)
+  double* x;                 // backward output (the x vector's level segment)
+  const double* xc;          // x_c: s's coarse rows in the parent's x segment (final before this level)
   int32_t m, r, ldC, kn;
   int32_t pre;               // forward events on s before its elimination
   int32_t nchunk;            // backward tasks of s (>= 1)

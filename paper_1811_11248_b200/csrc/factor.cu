@@ -379,7 +379,7 @@ hs_factor_s::~hs_factor_s() {
   for (auto& p : ap.lv) {
     fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb);
   }
-  fr(ap.d_y); fr(ap.d_yf); fr(ap.d_parts); fr(ap.d_ctr); fr(ap.d_contrib);
+  fr(ap.d_y); fr(ap.d_yf); fr(ap.d_xb); fr(ap.d_parts); fr(ap.d_ctr); fr(ap.d_contrib);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
   fr(d_r); fr(d_z); fr(d_p); fr(d_q); fr(d_x); fr(d_b); fr(d_red);
   if (h_red) cudaFreeHost(h_red);
@@ -1659,6 +1659,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   ap.vtotal = vbase;
   ap.d_y = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));
   ap.d_yf = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.ftotal, 1));
+  ap.d_xb = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));
   ap.d_parts = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.max_parts, 1));
   ap.d_contrib = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.contrib_total, 1));
   ap.d_ctr = (int32_t*)dc.alloc(sizeof(int32_t) * std::max<int64_t>(ap.ctr_total, 1));
@@ -1673,12 +1674,13 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (auto& as : AP.src) {
       if (as.m == 0) continue;
       as.y = ap.d_y + (uintptr_t)as.y;
-      as.x = ap.d_y + (uintptr_t)as.x;
+      as.x = ap.d_xb + (uintptr_t)as.x;
+      as.xc = ap.d_xb + (uintptr_t)as.yc;
       as.yc = ap.d_y + (uintptr_t)as.yc;
       as.yf = ap.d_yf + (uintptr_t)as.yf;
     }
     for (auto& t : AP.ftgt) t.y = ap.d_y + (uintptr_t)t.y;
-    for (auto& nbr : AP.bnb) nbr.x = ap.d_y + (uintptr_t)nbr.x;
+    for (auto& nbr : AP.bnb) nbr.x = ap.d_xb + (uintptr_t)nbr.x;
     up(AP.src, AP.d_src);
     up(AP.ftask, AP.d_ftask);
     up(AP.ftgt, AP.d_ftgt);

@@ -136,6 +136,7 @@ struct ApplyPlan {
   int64_t vtotal = 0, ftotal = 0, ctr_total = 0, max_parts = 0;
   double* d_y = nullptr;                 // the apply vector (all levels + top)
   double* d_yf = nullptr;                // fine parts y_f of every cluster (forward -> backward)
+  double* d_xb = nullptr;                // backward result x (d_y's layout), reset to "empty" per apply
   double* d_parts = nullptr;
   double* d_contrib = nullptr;           // forward contributions (pull sweep), all levels
   int64_t contrib_total = 0;

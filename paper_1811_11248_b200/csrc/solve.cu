@@ -177,6 +177,9 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   if (ap.ctr_total) HS_CUDA(cudaMemsetAsync(ap.d_ctr, 0, sizeof(int32_t) * ap.ctr_total, st));
   // forward contribution slots start empty (all-ones NaN, polled by the consumers)
   if (ap.contrib_total) HS_CUDA(cudaMemsetAsync(ap.d_contrib, 0xFF, sizeof(double) * ap.contrib_total, st));
+  // backward results start empty too (polled by the neighbours' backward tasks)
+  const int64_t vtot = ap.vbase.back() + f->ntop;   // levels + top
+  HS_CUDA(cudaMemsetAsync(ap.d_xb, 0xFF, sizeof(double) * std::max<int64_t>(vtot, 1), st));
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
     mark();
@@ -184,13 +187,19 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
     launch_apply_post_level(level_args(f, l), st);
   }
   mark();
-  if (f->ntop > 0) launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);
+  if (f->ntop > 0) {
+    launch_top_solve(ap.d_y + ap.vbase[an->L_top], f->d_top, (int)f->ntop, (int)f->ntop, st);
+    HS_CUDA(cudaMemcpyAsync(ap.d_xb + ap.vbase[an->L_top], ap.d_y + ap.vbase[an->L_top], sizeof(double) * f->ntop,
+                            cudaMemcpyDeviceToDevice, st));
+  }
   for (int l = an->L_top - 1; l >= 0; --l) {
     mark();
+    // the level's backward partial sums start empty (polled by the finishing chunks)
+    if (ap.lv[l].parts) HS_CUDA(cudaMemsetAsync(ap.d_parts, 0xFF, sizeof(double) * ap.lv[l].parts, st));
     launch_apply_bwd_level(level_args(f, l), st);
   }
   mark();
-  launch_permute(ap.d_y + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);
+  launch_permute(ap.d_xb + ap.vbase[0], f->d_x, f->d_perm, n, 1, st);
   mark();
 }
 
@@ -264,6 +273,19 @@ void profile_apply(hs_factor_s* f, cudaStream_t st) {
                  lt, (b1 - b0) * 1e-3, nt - nf, bacc[0] / nb, bacc[1] / nb, nfin ? bacc[2] / nfin : 0.0, nfin);
     // the forward chain: consecutive T tasks, gap between a T's publish and the next T's wait exit
     if (std::getenv("HS_APPLY_TRACE_DUMP")) {
+      for (size_t k = nf; k < nt; ++k) {
+        const long long* x = &tr[8 * k];
+        const BwdTask& bt = P.btask[k - nf];
+        int nl = 0, lq = -1;
+        for (int b = bt.b0; b < bt.b1; ++b)
+          if (P.bnb[b].later) {
+            ++nl;
+            lq = P.bnb[b].q;
+          }
+        std::fprintf(stderr, "[hs trace] b %zu s %d chunk %d nc %d later %d lastq %d: %lld %lld %lld %lld\n", k - nf, bt.s,
+                     bt.chunk, bt.nc, nl, lq, x[0] - b0, x[1] ? x[1] - b0 : -1, x[2] ? x[2] - b0 : -1,
+                     x[3] ? x[3] - b0 : -1);
+      }
       for (size_t k = 0; k < nf; ++k) {
         const long long* x = &tr[8 * k];
         std::fprintf(stderr, "[hs trace] f %zu s %d first %d: %lld %lld %lld %lld %lld %lld\n", k, P.ftask[k].s,

@@ -264,17 +264,24 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_post(ApplyLevelArgs a) 
   }
 }
 
+constexpr int BWD_STAGE = 4096;    // C columns of a chunk, then T_s + partials for the finish (doubles)
+
 // Backward sweep of one level (Algorithm 2 backward substitution, reverse batch order).
-// Task (s, neighbours bnb[b0, b1) of s): wait for those eliminated after s, then partial
-// sums p[k] = sum over their columns c of C_s[k][c] x_n[c].  The last chunk of s to arrive
-// finishes s: x_f = y_f - sum of the partials (chunk order), x_s = T_s^T [x_c; x_f], and
-// publishes done[s].  Chunks follow the neighbours' readiness (host plan), so the chunk
-// that waits for the last neighbour is small.
+// Task (s, neighbours bnb[b0, b1) of s): the chunk's columns of C_s go to shared memory
+// while the later neighbours finish; once their x values appear (polled: x starts empty),
+// partial sums p[k] = sum over the chunk's columns c of C_s[k][c] x_n[c].  The chunks
+// follow the neighbours' readiness (host plan) and the LAST chunk of s — the one waiting
+// for the neighbour that finishes last — finishes s: it polls the other chunks' partials
+// (they start empty too), x_f = y_f - sum of the partials (chunk order),
+// x_s = T_s^T [x_c; x_f].  No fences, counters or flags on the chain: every value a task
+// waits for is polled directly.  A chunk only waits on tasks with smaller tickets.
 __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
   __shared__ double xn[BWD_COLS];
   __shared__ int ccol[BWD_COLS];
   __shared__ double u[MAX_M];
-  __shared__ int s_task, s_last;
+  __shared__ double pown[MAX_M];   // the finisher's own partial
+  __shared__ int s_task;
+  extern __shared__ double bst[];  // BWD_STAGE doubles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
   for (;;) {
     if (tid == 0) s_task = atomicAdd(a.ticket + 1, 1);
@@ -286,71 +293,108 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
     const BwdTask tk = a.btask[t];
     const ApplySrc S = a.src[tk.s];
     const int m = S.m, r = S.r, K = m - r;
+    const bool fin = tk.chunk == S.nchunk - 1;
     if (tk.nc > 0) {
       const int nnb = tk.b1 - tk.b0;
-      // prefetch T_s (for the finish) and the chunk's columns of C_s, then wait
-      for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
-      for (int b = 0; b < nnb; ++b) {
+      const bool cst = K * tk.nc <= BWD_STAGE;
+      for (int b = warp; b < nnb; b += nw) {   // column map (+ the chunk's C columns)
         const BwdNb nb = a.bnb[tk.b0 + b];
-        for (int k = warp; k < K; k += nw)
-          for (int c = lane * 16; c < nb.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + nb.col + c);
+        for (int i = lane; i < nb.len; i += 32) ccol[nb.off + i] = nb.col + i;
       }
-      for (int b = tid; b < nnb; b += APPLY_THREADS) {
+      if (fin)
+        for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
+      __syncthreads();
+      if (cst) {
+        for (int e = tid; e < K * tk.nc; e += APPLY_THREADS) {
+          const int k = e / tk.nc, c = e - k * tk.nc;
+          bst[e] = S.C[(int64_t)k * S.ldC + ccol[c]];
+        }
+      } else {
+        for (int b = 0; b < nnb; ++b) {
+          const BwdNb nb = a.bnb[tk.b0 + b];
+          for (int k = warp; k < K; k += nw)
+            for (int c = lane * 16; c < nb.len; c += 32 * 16) prefetch_l2(S.C + (int64_t)k * S.ldC + nb.col + c);
+        }
+      }
+      for (int b = tid; b < nnb; b += APPLY_THREADS) {   // one waiter per later neighbour
         const BwdNb nb = a.bnb[tk.b0 + b];
-        if (nb.later) wait_ge(a.done + nb.q, 1);
+        if (nb.later) ld_poll(nb.x);
       }
       __syncthreads();
       AP_TR(tt, 1);
-      for (int b = warp; b < nnb; b += nw) {   // gather x_n and the column map
+      for (int b = warp; b < nnb; b += nw) {   // gather x_n (final once not empty)
         const BwdNb nb = a.bnb[tk.b0 + b];
-        for (int i = lane; i < nb.len; i += 32) {
-          xn[nb.off + i] = __ldcg(nb.x + i);
-          ccol[nb.off + i] = nb.col + i;
-        }
+        for (int i = lane; i < nb.len; i += 32) xn[nb.off + i] = ld_poll(nb.x + i);
       }
       __syncthreads();
       double* part = a.parts + S.part + (int64_t)tk.chunk * K;
       for (int k = warp; k < K; k += nw) {
-        const double* Ck = S.C + (int64_t)k * S.ldC;
         double acc = 0.0;
-        for (int c = lane; c < tk.nc; c += 32) acc += Ck[ccol[c]] * xn[c];
+        if (cst) {
+          const double* Ck = bst + k * tk.nc;
+          for (int c = lane; c < tk.nc; c += 32) acc += Ck[c] * xn[c];
+        } else {
+          const double* Ck = S.C + (int64_t)k * S.ldC;
+          int c = lane;
+          for (; c + 32 * 7 < tk.nc; c += 32 * 8) {   // 8 loads in flight, accumulated in c order
+            double cv[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) cv[w] = Ck[ccol[c + 32 * w]];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) acc += cv[w] * xn[c + 32 * w];
+          }
+          for (; c < tk.nc; c += 32) acc += Ck[ccol[c]] * xn[c];
+        }
         acc = wsum(acc);
-        if (lane == 0) part[k] = acc;
+        if (lane == 0) {
+          if (fin) pown[k] = acc;
+          else asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(part + k), "d"(acc) : "memory");
+        }
       }
-      __threadfence();
-      __syncthreads();
       AP_TR(tt, 2);
-      if (tid == 0) s_last = (atomicAdd(a.bcnt + tk.s, 1) == S.nchunk - 1);
-      __syncthreads();
-      if (!s_last) continue;
-      __threadfence();
+      if (!fin) {
+        __syncthreads();   // bst, ccol, xn reusable
+        continue;
+      }
+      __syncthreads();   // bst free for the finish
     }
+    // ---- finish s: x_c, y_f, the other chunks' partials (polled) and T_s in one pass
     const bool has_parts = tk.nc > 0;
-    for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.yc + i);
-    for (int k = tid; k < K; k += APPLY_THREADS) {
-      double s = 0.0;
-      if (has_parts)
-        for (int q = 0; q < S.nchunk; ++q) s += __ldcg(a.parts + S.part + (int64_t)q * K + k);
-      u[r + k] = __ldcg(S.yf + k) - s;
-    }
+    const bool tst = m * m <= BWD_STAGE - (has_parts ? S.nchunk * K : 0);
+    double* pS = bst;                                     // nchunk x K
+    double* tS = bst + (has_parts ? S.nchunk * K : 0);    // m x m
+    const bool pst = !has_parts || S.nchunk * K <= BWD_STAGE;
+    for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.xc + i);
+    for (int k = tid; k < K; k += APPLY_THREADS) u[r + k] = __ldcg(S.yf + k);
+    if (tst)
+      for (int e = tid; e < m * m; e += APPLY_THREADS) tS[e] = S.T[e];
+    if (has_parts && pst)
+      for (int e = tid; e < (S.nchunk - 1) * K; e += APPLY_THREADS) pS[e] = ld_poll(a.parts + S.part + e);
     __syncthreads();
+    if (has_parts)
+      for (int k = tid; k < K; k += APPLY_THREADS) {
+        double s = 0.0;
+        for (int q = 0; q < S.nchunk - 1; ++q) s += pst ? pS[q * K + k] : ld_poll(a.parts + S.part + (int64_t)q * K + k);
+        s += pown[k];
+        u[r + k] -= s;
+      }
+    __syncthreads();
+    const double* Tm = tst ? tS : S.T;
     for (int i = tid; i < m; i += APPLY_THREADS) {
       double acc = 0.0;
       int j = 0;
       for (; j + 8 <= m; j += 8) {   // 8 loads in flight, accumulated in j order
         double tv[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) tv[w] = S.T[(int64_t)(j + w) * m + i];
+        for (int w = 0; w < 8; ++w) tv[w] = Tm[(int64_t)(j + w) * m + i];
 #pragma unroll
         for (int w = 0; w < 8; ++w) acc += tv[w] * u[j + w];
       }
-      for (; j < m; ++j) acc += S.T[(int64_t)j * m + i] * u[j];
-      S.x[i] = acc;
+      for (; j < m; ++j) acc += Tm[(int64_t)j * m + i] * u[j];
+      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(S.x + i), "d"(acc) : "memory");
     }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) atomicExch(a.done + tk.s, 1);
     AP_TR(tt, 3);
+    __syncthreads();   // u, bst reusable
   }
 }
 
@@ -407,7 +451,7 @@ static int apply_grid(const void* fn, int ntask) {
   static int per_sm[2] = {0, 0}, nsm = 0;
   const int k = fn == (const void*)k_apply_fwd ? 0 : 1;
   if (!per_sm[k]) {
-    const size_t dyn = k == 0 ? sizeof(double) * FWD_STAGE : 0;
+    const size_t dyn = sizeof(double) * (k == 0 ? FWD_STAGE : BWD_STAGE);
     if (dyn) set_smem_attr(fn, dyn);
     HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[k], fn, APPLY_THREADS, dyn));
     int dev = 0;
@@ -429,7 +473,8 @@ void launch_apply_post_level(const ApplyLevelArgs& a, cudaStream_t st) {
 }
 void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
   if (a.nbtask <= 0) return;
-  k_apply_bwd<<<apply_grid((const void*)k_apply_bwd, a.nbtask), APPLY_THREADS, 0, st>>>(a);
+  k_apply_bwd<<<apply_grid((const void*)k_apply_bwd, a.nbtask), APPLY_THREADS,
+                sizeof(double) * BWD_STAGE, st>>>(a);
   count_launch(1);
 }
 
