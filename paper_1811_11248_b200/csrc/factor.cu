@@ -218,6 +218,17 @@ struct BlockStore {
 struct PhaseTimer {
   cudaEvent_t a[5], b[3];
   bool b_pending = false;
+  // Each event record costs ~2-3 us of stream time per batch, so phases are timed only on
+  // request: HS_PHASE_EVENTS=all brackets every phase, =cpqr only the CPQR kernel.
+  int level = [] {
+    const char* e = std::getenv("HS_PHASE_EVENTS");
+    if (!e) return std::getenv("HS_PROFILE") ? 2 : 0;
+    return std::strcmp(e, "all") == 0 ? 2 : std::strcmp(e, "cpqr") == 0 ? 1 : 0;
+  }();
+  bool on = level == 2;
+  void rec(cudaEvent_t e, cudaStream_t st) {
+    if (on || (level == 1 && (e == a[3] || e == a[4]))) HS_CUDA(cudaEventRecord(e, st));
+  }
   PhaseTimer() {
     for (auto& e : a) HS_CUDA(cudaEventCreate(&e));
     for (auto& e : b) HS_CUDA(cudaEventCreate(&e));
@@ -232,14 +243,17 @@ struct PhaseTimer {
     return ms * 1e-3;
   }
   void collect_b(hs_factor_stats_t& S) {
-    if (!b_pending) return;
+    if (!b_pending || !on) return;
     HS_CUDA(cudaEventSynchronize(b[2]));
     S.t_phase_s[4] += el(b[0], b[1]);
     S.t_phase_s[5] += el(b[1], b[2]);
     b_pending = false;
   }
   void collect_a(hs_factor_stats_t& S) {
-    for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
+    if (on)
+      for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
+    else if (level == 1)
+      S.t_phase_s[3] += el(a[3], a[4]);
   }
   void collect(hs_factor_stats_t& S) {   // after a synchronising point
     collect_a(S);
@@ -804,21 +818,21 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
         t_plan += now_s() - tp0;
         upA.send(st);
-        HS_CUDA(cudaEventRecord(pt.a[0], st));
+        pt.rec(pt.a[0], st);
         if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
-          HS_CUDA(cudaEventRecord(pt.a[1], st));
+          pt.rec(pt.a[1], st);
           launch_chol(upA.dptr<FusedItem>(iI), (int)fci.size(), max_m, d_status, st);
-          HS_CUDA(cudaEventRecord(pt.a[2], st));
+          pt.rec(pt.a[2], st);
           launch_scale_tiles(upA.dptr<FusedItem>(iF), (int)fz.size(), upA.dptr<FusedSeg>(iS), max_m, st);
         } else {
           launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
-          HS_CUDA(cudaEventRecord(pt.a[1], st));
+          pt.rec(pt.a[1], st);
           if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
-          HS_CUDA(cudaEventRecord(pt.a[2], st));
+          pt.rec(pt.a[2], st);
           if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
           else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), st);   // R-floor
         }
-        HS_CUDA(cudaEventRecord(pt.a[3], st));
+        pt.rec(pt.a[3], st);
         d_clu_batch = upA.dptr<CluItem>(iC);
         if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
         else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
@@ -826,7 +840,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
           launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
         }
-        HS_CUDA(cudaEventRecord(pt.a[4], st));
+        pt.rec(pt.a[4], st);
         HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
         if (dpatch) {
           HS_CUDA(cudaMemcpyAsync(h_stat, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
@@ -1172,16 +1186,16 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         t_plan += now_s() - tp1;
         upB.send(st);
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
-        HS_CUDA(cudaEventRecord(pt.b[0], st));
+        pt.rec(pt.b[0], st);
         launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
         launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
                         upB.dptr<SchurSrc>(jS), upB.dptr<NbCol>(jN), bs.dir(), st);
-        HS_CUDA(cudaEventRecord(pt.b[1], st));
+        pt.rec(pt.b[1], st);
         launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
         launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
-        HS_CUDA(cudaEventRecord(pt.b[2], st));
+        pt.rec(pt.b[2], st);
         pt.b_pending = true;
         // apply operators T_s = U^T G^{-1} of the batch on the side stream (they are only
         // read by the apply): reads the workspace's G, V, tau, so the workspace (and the
@@ -1508,12 +1522,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     t_plan += now_s() - tp2;
     t_trans += now_s() - tp2;
     upA.send(st);
-    HS_CUDA(cudaEventRecord(pt.a[0], st));
+    pt.rec(pt.a[0], st);
     launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
-    HS_CUDA(cudaEventRecord(pt.a[1], st));
+    pt.rec(pt.a[1], st);
     HS_CUDA(cudaStreamSynchronize(st));
     pt.collect_b(S);
-    S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
+    if (pt.on) S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
     const double tr1 = now_s();
     bs.release();
     bs = std::move(nbs);
@@ -1612,11 +1626,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       upA.copy_in(iA, items);
       upA.send(st);
       launch_copy2d(upA.dptr<CopyItem>(iA), (int)items.size(), st);
-      HS_CUDA(cudaEventRecord(pt.a[0], st));
+      pt.rec(pt.a[0], st);
       dense_potrf(f->d_top, (int)N, (int)N, d_status, an->L_top, nullptr, st);
-      HS_CUDA(cudaEventRecord(pt.a[1], st));
+      pt.rec(pt.a[1], st);
       check_status(d_status, &h_status, st);
-      S.t_phase_s[6] += PhaseTimer::el(pt.a[0], pt.a[1]);
+      if (pt.on) S.t_phase_s[6] += PhaseTimer::el(pt.a[0], pt.a[1]);
       S.flops += (double)N * N * N / 3.0;
       S.flops_phase[6] += (double)N * N * N / 3.0;
     }

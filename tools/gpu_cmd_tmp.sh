@@ -1,7 +1,4 @@
 mkdir -p gpurun_out
-HS_APPLY_TRACE=3 HS_APPLY_TRACE_DUMP=1 timeout 300 python tools/apply_profile.py 2>&1 | grep "hs trace\] b " | tail -4125 > gpurun_out/bwd_dump_f0.log
-timeout 300 python tools/apply_profile.py 2>&1 | tail -22 | grep -E "(fwd|bwd) level [0-5]" > gpurun_out/apply_trace.log
-cat gpurun_out/apply_trace.log
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log
 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
-tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/bench.log | cut -c1-900
+tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/bench.log | cut -c1-2500
