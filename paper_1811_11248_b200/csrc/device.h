@@ -114,6 +114,7 @@ struct NbCol {               // neighbour q occupies columns [col, col+len) of t
 };
 struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
   double* blk;
+  int64_t total;             // doubles in the store (bounds checks)
   const int64_t* ptr;
   const int32_t* q;
   const int64_t* off;

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <memory>
 #include <unordered_map>
 
@@ -197,7 +198,7 @@ struct BlockStore {
     HS_CUDA(cudaMemcpyAsync(d_cap, cap.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaStreamSynchronize(st));   // host vectors go out of scope
   }
-  BlockDir dir() const { return BlockDir{d, d_ptr, d_q, d_off, d_cap}; }
+  BlockDir dir() const { return BlockDir{d, (int64_t)total, d_ptr, d_q, d_off, d_cap}; }
   void release() {
     for (void* p : {(void*)d, (void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
       if (p) dc->free(p);
@@ -477,6 +478,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->opt = opt;
   f->keep_records = std::getenv("HS_KEEP_RECORDS") != nullptr;
   double t_plan = 0.0;
+  double t_rank_wait = 0.0;   // host blocked on the previous batch's ranks (HS_PROFILE)
+  double t_apply_plan = 0.0;  // apply planning (host worker)
+  std::future<void> plan_prev;  // the chain of per-level apply-plan tasks (joined before upload)
   double t_sub[4] = {0, 0, 0, 0};
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
   double t_tr[4] = {0, 0, 0, 0};   // level transition: block store build, upload_dir, arena alloc, release
@@ -673,7 +677,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     auto finish_pending = [&]() {
       if (!pend_active) return;
       pend_active = false;
+      const double tw0 = now_s();
       HS_CUDA(cudaEventSynchronize(ev_rank));
+      t_rank_wait += now_s() - tw0;
       if (h_stat->flag) {
         char buf[256];
         std::snprintf(buf, sizeof buf, "NOT_SPD: Cholesky breakdown at level %d cluster %d pivot %d value %.17g (P:283)",
@@ -1345,142 +1351,155 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::vector<int32_t> capn(nP);
     for (int P = 0; P < nP; ++P) capn[P] = L.rank[2 * P] + L.rank[2 * P + 1];
     if (plan_apply) {
-      ApplyLevelPlan& AP = ap.lv[l];
-      AP.src.assign(lev.nclus, ApplySrc{});
-      std::vector<int32_t> fev(lev.nclus, 0), lv2 = cap;
-      std::vector<uint8_t> proc(lev.nclus, 0);
-      std::vector<std::vector<PullSrc>> pre(lev.nclus), post(lev.nclus);
-      int64_t slots = 0;   // contribution slots of the level
-      std::vector<std::vector<BwdTask>> bwd_batches;
-      std::vector<int64_t> foff(lev.nclus, 0);
-      const double ta = now_s();
-      std::vector<int32_t> bpos(lev.nclus, 0);   // batch index of each cluster
-      for (size_t b = 0; b < lev.batches.size(); ++b)
-        for (int32_t c : lev.batches[b]) bpos[c] = (int32_t)b;
-      for (const auto& Bt : lev.batches) {
-        if (level_dofs == 0) break;
-        bwd_batches.emplace_back();
-        std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
-        for (int32_t s : Bt) {
-          const int32_t m = lv2[s], r = L.rank[s], K = m - r, kn = L.kn[s];
-          if (m == 0) continue;
-          const auto& ns = lev.H[s];
-          std::vector<int32_t> noff(ns.size() + 1, 0);
-          for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + lv2[ns[a]];
-          // the cluster's record, its forward target tasks (targets grouped up to FWD_COLS
-          // columns) and its backward column chunks
-          ApplySrc& as = AP.src[s];
-          as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
-          as.pre = fev[s]++;
-          as.nb_begin = (int32_t)AP.bnb.size();
-          // forward (pull form): s contributes to the unprocessed neighbours before their own
-          // elimination (their pre lists) and to the coarse parts of the processed ones
-          // afterwards (post lists); lists grow in elimination order
-          as.tg_begin = (int32_t)AP.ctb.size();
-          for (size_t a = 0; a < ns.size(); ++a) {
-            const int32_t q = ns[a];
-            if (lv2[q] == 0 || K == 0) continue;
-            (proc[q] ? post[q] : pre[q]).push_back(PullSrc{slots, s, 0});
-            AP.ctb.push_back(Contrib{slots, noff[a], lv2[q], q, proc[q] ? 0 : 1});
-            slots += lv2[q];
-            AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1, 0, 0});
-          }
-          as.tg_end = (int32_t)AP.ctb.size();
-          as.nb_end = (int32_t)AP.bnb.size();
-          // produce order: the targets eliminated soonest first (T(s) produces the first
-          // group itself, so the next cluster on the chain waits for one task, not two);
-          // the order in which a target subtracts its contributions is its pre list's
-          std::stable_sort(AP.ctb.begin() + as.tg_begin, AP.ctb.begin() + as.tg_end,
-                           [&](const Contrib& x, const Contrib& y) {
-                             const int32_t bx = x.pre ? bpos[x.q] : INT32_MAX, by = y.pre ? bpos[y.q] : INT32_MAX;
-                             return bx < by;
-                           });
-          // T(s) with s's first contribution group, then the other groups (<= FWD_COLS
-          // columns / 16 targets each) as tasks of their own
-          if (as.tg_begin == as.tg_end) AP.ftask.push_back(FwdTask{s, as.tg_begin, as.tg_end, 1});
-          for (int32_t g0 = as.tg_begin, first = 1; g0 < as.tg_end; first = 0) {
-            int32_t g1 = g0, cols = 0;
-            while (g1 < as.tg_end && (g1 == g0 || (cols + AP.ctb[g1].len <= FWD_COLS && g1 - g0 < 16)))
-              cols += AP.ctb[g1++].len;
-            AP.ftask.push_back(FwdTask{s, g0, g1, first});
-            g0 = g1;
-          }
-          as.part = AP.parts;
-          if (K > 0 && kn > 0 && as.nb_end > as.nb_begin) {
-            // backward chunks by readiness: neighbours eliminated before s (final at the
-            // level start), then the later ones latest-eliminated first (they finish first
-            // in the reverse sweep); the last BWD_CRIT later neighbours — the critical path
-            // of the sweep — get a chunk of their own, the rest are packed to BWD_COLS
-            std::stable_sort(AP.bnb.begin() + as.nb_begin, AP.bnb.begin() + as.nb_end,
-                             [&](const BwdNb& x, const BwdNb& y) {
-                               const int32_t kx = x.later ? INT32_MAX - bpos[x.q] : -1;
-                               const int32_t ky = y.later ? INT32_MAX - bpos[y.q] : -1;
-                               return kx < ky;
-                             });
-            int32_t nlater = 0;
-            for (int32_t b = as.nb_begin; b < as.nb_end; ++b) nlater += AP.bnb[b].later;
-            const int32_t crit0 = as.nb_end - std::min<int32_t>(nlater, BWD_CRIT);
-            as.nchunk = 0;
-            for (int32_t b0 = as.nb_begin; b0 < as.nb_end;) {
-              int32_t b1 = b0, cols = 0;
-              while (b1 < as.nb_end && (b1 == b0 || (b1 < crit0 && b0 < crit0 && cols + AP.bnb[b1].len <= BWD_COLS))) {
-                AP.bnb[b1].off = cols;
-                cols += AP.bnb[b1++].len;
-              }
-              bwd_tasks.push_back(BwdTask{s, b0, b1, cols, as.nchunk++, 0});
-              b0 = b1;
+      // The apply plan of level l only reads this level's records: single GPU, it is built
+      // on a host worker (chained after the previous level's) while the next level factors.
+      auto plan_task = [l, &lev = lev, &L = L, &ap, capc = cap, capn, level_dofs, vb0 = ap.vbase[l], vbn0 = vbase,
+                        nP, &t_apply_plan]() {
+        ApplyLevelPlan& AP = ap.lv[l];
+        AP.src.assign(lev.nclus, ApplySrc{});
+        std::vector<int32_t> fev(lev.nclus, 0), lv2 = capc;
+        std::vector<uint8_t> proc(lev.nclus, 0);
+        std::vector<std::vector<PullSrc>> pre(lev.nclus), post(lev.nclus);
+        int64_t slots = 0;   // contribution slots of the level
+        std::vector<std::vector<BwdTask>> bwd_batches;
+        std::vector<int64_t> foff(lev.nclus, 0);
+        const double ta = now_s();
+        std::vector<int32_t> bpos(lev.nclus, 0);   // batch index of each cluster
+        for (size_t b = 0; b < lev.batches.size(); ++b)
+          for (int32_t c : lev.batches[b]) bpos[c] = (int32_t)b;
+        for (const auto& Bt : lev.batches) {
+          if (level_dofs == 0) break;
+          bwd_batches.emplace_back();
+          std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
+          for (int32_t s : Bt) {
+            const int32_t m = lv2[s], r = L.rank[s], K = m - r, kn = L.kn[s];
+            if (m == 0) continue;
+            const auto& ns = lev.H[s];
+            std::vector<int32_t> noff(ns.size() + 1, 0);
+            for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + lv2[ns[a]];
+            // the cluster's record, its forward target tasks (targets grouped up to FWD_COLS
+            // columns) and its backward column chunks
+            ApplySrc& as = AP.src[s];
+            as.T = L.T[s]; as.C = L.C[s]; as.ldC = kn; as.m = m; as.r = r; as.kn = kn;
+            as.pre = fev[s]++;
+            as.nb_begin = (int32_t)AP.bnb.size();
+            // forward (pull form): s contributes to the unprocessed neighbours before their own
+            // elimination (their pre lists) and to the coarse parts of the processed ones
+            // afterwards (post lists); lists grow in elimination order
+            as.tg_begin = (int32_t)AP.ctb.size();
+            for (size_t a = 0; a < ns.size(); ++a) {
+              const int32_t q = ns[a];
+              if (lv2[q] == 0 || K == 0) continue;
+              (proc[q] ? post[q] : pre[q]).push_back(PullSrc{slots, s, 0});
+              AP.ctb.push_back(Contrib{slots, noff[a], lv2[q], q, proc[q] ? 0 : 1});
+              slots += lv2[q];
+              AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1, 0, 0});
             }
-            AP.parts += (int64_t)as.nchunk * K;
-          } else {
-            as.nchunk = 1;
-            bwd_tasks.push_back(BwdTask{s, 0, 0, 0, 0, 0});
+            as.tg_end = (int32_t)AP.ctb.size();
+            as.nb_end = (int32_t)AP.bnb.size();
+            // produce order: the targets eliminated soonest first (T(s) produces the first
+            // group itself, so the next cluster on the chain waits for one task, not two);
+            // the order in which a target subtracts its contributions is its pre list's
+            std::stable_sort(AP.ctb.begin() + as.tg_begin, AP.ctb.begin() + as.tg_end,
+                             [&](const Contrib& x, const Contrib& y) {
+                               const int32_t bx = x.pre ? bpos[x.q] : INT32_MAX, by = y.pre ? bpos[y.q] : INT32_MAX;
+                               return bx < by;
+                             });
+            // T(s) with s's first contribution group, then the other groups (<= FWD_COLS
+            // columns / 16 targets each) as tasks of their own
+            if (as.tg_begin == as.tg_end) AP.ftask.push_back(FwdTask{s, as.tg_begin, as.tg_end, 1});
+            for (int32_t g0 = as.tg_begin, first = 1; g0 < as.tg_end; first = 0) {
+              int32_t g1 = g0, cols = 0;
+              while (g1 < as.tg_end && (g1 == g0 || (cols + AP.ctb[g1].len <= FWD_COLS && g1 - g0 < 16)))
+                cols += AP.ctb[g1++].len;
+              AP.ftask.push_back(FwdTask{s, g0, g1, first});
+              g0 = g1;
+            }
+            as.part = AP.parts;
+            if (K > 0 && kn > 0 && as.nb_end > as.nb_begin) {
+              // backward chunks by readiness: neighbours eliminated before s (final at the
+              // level start), then the later ones latest-eliminated first (they finish first
+              // in the reverse sweep); the last BWD_CRIT later neighbours — the critical path
+              // of the sweep — get a chunk of their own, the rest are packed to BWD_COLS
+              std::stable_sort(AP.bnb.begin() + as.nb_begin, AP.bnb.begin() + as.nb_end,
+                               [&](const BwdNb& x, const BwdNb& y) {
+                                 const int32_t kx = x.later ? INT32_MAX - bpos[x.q] : -1;
+                                 const int32_t ky = y.later ? INT32_MAX - bpos[y.q] : -1;
+                                 return kx < ky;
+                               });
+              int32_t nlater = 0;
+              for (int32_t b = as.nb_begin; b < as.nb_end; ++b) nlater += AP.bnb[b].later;
+              const int32_t crit0 = as.nb_end - std::min<int32_t>(nlater, BWD_CRIT);
+              as.nchunk = 0;
+              for (int32_t b0 = as.nb_begin; b0 < as.nb_end;) {
+                int32_t b1 = b0, cols = 0;
+                while (b1 < as.nb_end && (b1 == b0 || (b1 < crit0 && b0 < crit0 && cols + AP.bnb[b1].len <= BWD_COLS))) {
+                  AP.bnb[b1].off = cols;
+                  cols += AP.bnb[b1++].len;
+                }
+                bwd_tasks.push_back(BwdTask{s, b0, b1, cols, as.nchunk++, 0});
+                b0 = b1;
+              }
+              AP.parts += (int64_t)as.nchunk * K;
+            } else {
+              as.nchunk = 1;
+              bwd_tasks.push_back(BwdTask{s, 0, 0, 0, 0, 0});
+            }
+            foff[s] = ap.ftotal;
+            ap.ftotal += K;
           }
-          foff[s] = ap.ftotal;
-          ap.ftotal += K;
+          for (int32_t s : Bt) {
+            lv2[s] = L.rank[s];
+            proc[s] = 1;
+          }
         }
-        for (int32_t s : Bt) {
-          lv2[s] = L.rank[s];
-          proc[s] = 1;
+        // vector positions (offsets into d_y / d_yf, made absolute at the end).  A cluster's
+        // live segment is its level segment until it is eliminated, then its coarse rows
+        // inside the parent's segment [coarse(2P); coarse(2P+1)].
+        std::vector<int64_t> voffn(nP + 1, 0);
+        for (int P = 0; P < nP; ++P) voffn[P + 1] = voffn[P] + capn[P];
+        const int64_t vb = vb0, vbn = vbn0;   // this level's and the next level's vector bases
+        auto lpos = [&](int32_t c) { return (double*)(uintptr_t)(vb + L.voff[c]); };
+        auto ppos = [&](int32_t c) {
+          return (double*)(uintptr_t)(vbn + voffn[c >> 1] + ((c & 1) ? L.rank[c - 1] : 0));
+        };
+        for (int32_t c = 0; c < lev.nclus; ++c) {
+          ApplySrc& as = AP.src[c];
+          if (as.m == 0) continue;
+          as.y = lpos(c);
+          as.x = lpos(c);
+          as.yc = ppos(c);
+          as.yf = (double*)(uintptr_t)foff[c];
         }
-      }
-      // vector positions (offsets into d_y / d_yf, made absolute at the end).  A cluster's
-      // live segment is its level segment until it is eliminated, then its coarse rows
-      // inside the parent's segment [coarse(2P); coarse(2P+1)].
-      std::vector<int64_t> voffn(nP + 1, 0);
-      for (int P = 0; P < nP; ++P) voffn[P + 1] = voffn[P] + capn[P];
-      const int64_t vb = ap.vbase[l], vbn = vbase;   // vbase already advanced past this level
-      auto lpos = [&](int32_t c) { return (double*)(uintptr_t)(vb + L.voff[c]); };
-      auto ppos = [&](int32_t c) {
-        return (double*)(uintptr_t)(vbn + voffn[c >> 1] + ((c & 1) ? L.rank[c - 1] : 0));
+        for (auto& t : AP.ftgt) t.y = t.proc ? ppos(t.q) : lpos(t.q);
+        for (auto& nbr : AP.bnb) nbr.x = (double*)(nbr.later ? lpos(nbr.q) : ppos(nbr.q));
+        for (auto it = bwd_batches.rbegin(); it != bwd_batches.rend(); ++it)
+          AP.btask.insert(AP.btask.end(), it->begin(), it->end());
+        AP.contrib_off = ap.contrib_total;
+        ap.contrib_total += slots;
+        for (int32_t c = 0; c < lev.nclus; ++c) {
+          ApplySrc& as = AP.src[c];
+          as.pre_begin = (int32_t)AP.pull.size();
+          AP.pull.insert(AP.pull.end(), pre[c].begin(), pre[c].end());
+          as.pre_end = (int32_t)AP.pull.size();
+          as.post_begin = (int32_t)AP.pull.size();
+          AP.pull.insert(AP.pull.end(), post[c].begin(), post[c].end());
+          as.post_end = (int32_t)AP.pull.size();
+          if (!post[c].empty() && as.m > 0) AP.post_cl.push_back(c);
+        }
+        AP.ctr_off = ap.ctr_total;
+        ap.ctr_total += 4 * (int64_t)lev.nclus + 2;
+        ap.max_parts = std::max(ap.max_parts, AP.parts);
+        t_apply_plan += now_s() - ta;
       };
-      for (int32_t c = 0; c < lev.nclus; ++c) {
-        ApplySrc& as = AP.src[c];
-        if (as.m == 0) continue;
-        as.y = lpos(c);
-        as.x = lpos(c);
-        as.yc = ppos(c);
-        as.yf = (double*)(uintptr_t)foff[c];
+      if (dist) {
+        plan_task();
+      } else {
+        plan_prev = std::async(std::launch::async, [task = std::move(plan_task), prev = std::move(plan_prev)]() mutable {
+          if (prev.valid()) prev.get();
+          task();
+        });
       }
-      for (auto& t : AP.ftgt) t.y = t.proc ? ppos(t.q) : lpos(t.q);
-      for (auto& nbr : AP.bnb) nbr.x = (double*)(nbr.later ? lpos(nbr.q) : ppos(nbr.q));
-      for (auto it = bwd_batches.rbegin(); it != bwd_batches.rend(); ++it)
-        AP.btask.insert(AP.btask.end(), it->begin(), it->end());
-      AP.contrib_off = ap.contrib_total;
-      ap.contrib_total += slots;
-      for (int32_t c = 0; c < lev.nclus; ++c) {
-        ApplySrc& as = AP.src[c];
-        as.pre_begin = (int32_t)AP.pull.size();
-        AP.pull.insert(AP.pull.end(), pre[c].begin(), pre[c].end());
-        as.pre_end = (int32_t)AP.pull.size();
-        as.post_begin = (int32_t)AP.pull.size();
-        AP.pull.insert(AP.pull.end(), post[c].begin(), post[c].end());
-        as.post_end = (int32_t)AP.pull.size();
-        if (!post[c].empty() && as.m > 0) AP.post_cl.push_back(c);
-      }
-      AP.ctr_off = ap.ctr_total;
-      ap.ctr_total += 4 * (int64_t)lev.nclus + 2;
-      ap.max_parts = std::max(ap.max_parts, AP.parts);
-      t_sub[2] += now_s() - ta;
     }
     // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] -----------------
     const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
@@ -1653,6 +1672,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
+  if (std::getenv("HS_PROFILE") || std::getenv("HS_RANK_WAIT"))
+    std::fprintf(stderr, "[hs profile] host blocked on batch ranks: %.1f ms of %.1f ms\n", 1e3 * t_rank_wait, ms);
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] device cache: in use %.2f GB, peak %.2f GB, cached %.2f GB\n", dc.in_use / 1e9,
                  dc.peak / 1e9, dc.cached / 1e9);
@@ -1671,6 +1692,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   S.factor_bytes = fb;
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
+  const double tj0 = now_s();
+  if (plan_prev.valid()) plan_prev.get();   // every level's apply plan (rethrows a failure)
+  if (std::getenv("HS_PROFILE"))
+    std::fprintf(stderr, "[hs profile] apply planning on the host worker %.1f ms (main thread waited %.1f ms)\n",
+                 1e3 * t_apply_plan, 1e3 * (now_s() - tj0));
   ap.d_y = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));
   ap.d_yf = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ap.ftotal, 1));
   ap.d_xb = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(vbase, 1));

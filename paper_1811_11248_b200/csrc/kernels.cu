@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -919,6 +920,158 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
       if (tp[tc][e]) *tp[tc][e] = old[tc][e] - acc[tc][e];
 }
 
+// a5 v3: the same update with a shorter dependency chain per tile.  The C tile loads, the
+// owner loads and the owner dedupe (warp ballots instead of a serial scan) overlap; the
+// target addresses are resolved and the 16 old values per thread are in flight while the
+// DMMA product runs; the subtract-and-store follows.
+__global__ void __launch_bounds__(256, 2) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
+                                                const NbCol* __restrict__ nbc, BlockDir dir) {
+  const SchurTile2 t = tiles[blockIdx.x];
+  const SchurSrc s = srcs[t.src];
+  if (s.K <= 0) return;   // planned before its rank was known and kept everything (uniform)
+  const NbCol* nb = nbc + s.nb_off;
+  __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
+  __shared__ double aq[16][68];
+  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
+  __shared__ int r_slot[64], c_slot[64];
+  __shared__ int r_list[64], c_list[64];
+  __shared__ int nr, nc;
+  __shared__ double* ptab[SCH_MAXO][SCH_MAXO];
+  __shared__ int ldtab[SCH_MAXO];
+  const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const double* Cp = s.C + t.i0;
+  const double* Cq = s.C + t.j0;
+  // (1) owners of the tile's rows (warp 0) and columns (warp 1) + the first K-chunk of C
+  int o0 = -1, o1 = -1;
+  if (w < 2) {
+    const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
+    if (lane < lim) o0 = s.own[base + lane];
+    if (lane + 32 < lim) o1 = s.own[base + lane + 32];
+  }
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      const int kk = e >> 6, ii = e & 63;
+      const bool kin = k0 + kk < s.K;
+      ap[kk][ii] = (kin && ii < rows) ? Cp[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+      aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+    }
+  };
+  load_chunk(0);
+  if (w < 2) {   // (2) distinct owners in order (rows/cols are sorted by owner): ballots
+    const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
+    const int prev0 = __shfl_up_sync(0xffffffffu, o0, 1);
+    const int last0 = __shfl_sync(0xffffffffu, o0, 31);
+    const int prev1 = __shfl_up_sync(0xffffffffu, o1, 1);
+    const bool f0 = lane < lim && (lane == 0 || o0 != prev0);
+    const bool f1 = lane + 32 < lim && (lane == 0 ? o1 != last0 : o1 != prev1);
+    const unsigned m0 = __ballot_sync(0xffffffffu, f0), m1 = __ballot_sync(0xffffffffu, f1);
+    const unsigned le = 0xffffffffu >> (31 - lane);
+    const int s0 = __popc(m0 & le) - 1, s1 = __popc(m0) + __popc(m1 & le) - 1;
+    int* own = w == 0 ? r_own : c_own;
+    int* loc = w == 0 ? r_loc : c_loc;
+    int* slot = w == 0 ? r_slot : c_slot;
+    int* list = w == 0 ? r_list : c_list;
+    if (lane < lim) {
+      own[lane] = o0;
+      loc[lane] = base + lane - nb[o0].col;
+      slot[lane] = s0;
+      if (f0) list[s0] = o0;
+    }
+    if (lane + 32 < lim) {
+      own[lane + 32] = o1;
+      loc[lane + 32] = base + lane + 32 - nb[o1].col;
+      slot[lane + 32] = s1;
+      if (f1) list[s1] = o1;
+    }
+    if (lane == 0) (w == 0 ? nr : nc) = __popc(m0) + __popc(m1);
+  }
+  __syncthreads();
+  // (3) target block pointers of the distinct owner pairs
+  const bool table = nr <= SCH_MAXO && nc <= SCH_MAXO;
+  if (table) {
+    for (int e = tid; e < nr * nc; e += blockDim.x) {
+      const int ra = e / nc, cb = e % nc;
+      const int a = nb[r_list[ra]].idx, b = nb[c_list[cb]].idx;
+      ptab[ra][cb] = a >= b ? s.pairs[(int64_t)a * (a + 1) / 2 + b] : nullptr;
+    }
+    for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
+  }
+  __syncthreads();
+  // (4) target addresses and the old values in flight ...
+  int32_t tp[8][2];   // element offsets into the store (< 2^31 doubles: host-checked), -1 = none
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      tp[tc][e] = -1;
+      const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
+      if (i >= rows || j >= cols) continue;
+      const int oa = r_own[i], ob = c_own[j];
+      if (oa < ob) continue;                               // upper: the transposed block
+      const int li = r_loc[i], lj = c_loc[j];
+      if (oa == ob && li < lj) continue;                   // diagonal block: lower triangle only
+      double* p;
+      int ld;
+      if (table) {
+        p = ptab[r_slot[i]][c_slot[j]];
+        ld = ldtab[c_slot[j]];
+      } else {
+        const int fa = nb[oa].idx, fb = nb[ob].idx;
+        p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
+        ld = dir.cap[nb[ob].q];
+      }
+      if (p) tp[tc][e] = (int32_t)((p - dir.blk) + (int64_t)li * ld + lj);
+    }
+  double old[8][2];
+  if (dir.total < 0)   // debug: HS_SCHUR_CHECK (total passed negated)
+#pragma unroll
+    for (int tc = 0; tc < 8; ++tc)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (tp[tc][e] >= 0 && tp[tc][e] >= -dir.total) {
+          const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
+          printf("schur3 OOB: tile %d src %d i0 %d j0 %d i %d j %d own %d %d loc %d %d slots %d %d nr %d nc %d table %d kn %d K %d off %lld\n",
+                 blockIdx.x, t.src, t.i0, t.j0, i, j, r_own[i], c_own[j], r_loc[i], c_loc[j], r_slot[i], c_slot[j], nr, nc,
+                 (int)table, s.kn, s.K, (long long)tp[tc][e]);
+          tp[tc][e] = -1;
+        }
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] >= 0 ? dir.blk[tp[tc][e]] : 0.0;
+  // (5) ... while the 64 x 64 tile of C^T C forms on the FP64 tensor cores (DMMA m8n8k4):
+  // warp w owns output rows 8w..8w+7; lane l holds rows 8w + l/4, columns 8 tc + 2 (l % 4) + {0, 1}
+  double acc[8][2];
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc) acc[tc][0] = acc[tc][1] = 0.0;
+  for (int k0 = 0; k0 < s.K; k0 += 16) {
+    if (k0 > 0) {
+      __syncthreads();
+      load_chunk(k0);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      const double a = ap[kk + (lane & 3)][8 * w + (lane >> 2)];   // A = C_p^T, row-major 8 x 4
+#pragma unroll
+      for (int tc = 0; tc < 8; ++tc) {
+        const double b = aq[kk + (lane & 3)][8 * tc + (lane >> 2)];   // B = C_q, col-major 4 x 8
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[tc][0]), "+d"(acc[tc][1])
+                     : "d"(a), "d"(b));
+      }
+    }
+  }
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (tp[tc][e] >= 0) dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
+}
+
 __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,
                            int32_t* flag) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
@@ -1173,7 +1326,14 @@ void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* p
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st) {
   if (n <= 0) return;
-  k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
+  static const bool v2 = std::getenv("HS_SCHUR_V2") != nullptr;   // A/B: the previous tile kernel
+  if (v2 || dir.total >= (int64_t)1 << 31) k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
+  else {
+    static const bool chk = std::getenv("HS_SCHUR_CHECK") != nullptr;
+    BlockDir d2 = dir;
+    if (chk) d2.total = -dir.total;
+    k_schur3<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, d2);
+  }
   count_launch(1);
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <utility>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -61,15 +62,22 @@ struct HostStage {
   ~HostStage();
 };
 
-// Uploads a set of host vectors into one device scratch region with one memcpy.
+// Uploads a set of host vectors into one device scratch region with one memcpy.  The
+// pinned staging is double-buffered: the factor plans batch b+1 while batch b's second-half
+// copy may still be queued (it waits for a batch's ranks, not for its second half), so
+// reset() alternates between two buffers.  A buffer is rewritten two resets later, when the
+// host has waited for an event behind its copy (the next batch's ranks): no event of its own.
 struct Upload {
-  HostStage stage;
+  HostStage stage, other;
   DevScratch dev;
   std::vector<std::pair<size_t, size_t>> parts;   // (offset, bytes)
   size_t total = 0;
   void reset() {
     parts.clear();
     total = 0;
+    std::swap(stage.h, other.h);
+    std::swap(stage.cap, other.cap);
+    std::swap(stage.used, other.used);
   }
   template <class T>
   size_t add(const std::vector<T>& v) {
