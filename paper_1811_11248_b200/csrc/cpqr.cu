@@ -66,6 +66,20 @@ __host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, 
   const size_t w = sm ? (((size_t)wchunk * cq_ldm(m, cq_group(m, MR)) + 1) & ~(size_t)1) : 0;
   return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * cq_msg_words(m);
 }
+// direct write-back: the store element (row l of s, column j of B_s), j in the segment list
+__device__ __forceinline__ double* dwb_addr(const FusedSeg* seg, int nseg, int j, int l) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {   // last segment with col <= j
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg[mid].col <= j) lo = mid;
+    else hi = mid - 1;
+  }
+  const FusedSeg g = seg[lo];
+  if (j < g.col || j >= g.col + g.len) return nullptr;   // a column of an empty neighbour: none
+  double* p = const_cast<double*>(g.src);
+  return g.trans ? p + (int64_t)(j - g.col) * g.sld + l : p + (int64_t)l * g.sld + (j - g.col);
+}
+
 template <int G>
 __device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
@@ -466,6 +480,21 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       const int l = e / nw, c = e % nw;
       it.B[(size_t)l * ld + w_lo + c] = W[(size_t)c * ldm + l];
     }
+  if (it.dwb) {   // ... and straight into the store blocks (s, q), q in w(s); I_r on (s, s)
+    for (int c = tid; c < nw; c += CQ_THREADS) {
+      const double* src = SM ? W + (size_t)c * ldm : it.B + w_lo + c;
+      const size_t sst = SM ? 1 : ld;
+      for (int l = 0; l < r; ++l) {
+        double* d = dwb_addr(it.seg, it.nseg, w_lo + c, l);
+        if (d) *d = src[(size_t)l * sst];
+      }
+    }
+    if (crank == 0)
+      for (int e = tid; e < r * r; e += CQ_THREADS) {
+        const int i = e / r, j = e % r;
+        it.Dss[(size_t)i * it.ldss + j] = (i == j) ? 1.0 : 0.0;
+      }
+  }
   cl.sync();   // no CTA leaves while another may still copy into its shared memory
   CQ_TR(251);
   if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[252] = r;
@@ -530,6 +559,20 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
     const int l = t + i * G;
     if (act && l < m) col[(size_t)l * ld] = x[i];
   }
+  if (it.dwb && act) {   // coarse-n rows into the store blocks (s, q), C rows into the slab
+    const int jn = c0 + grp;
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int l = t + i * G;
+      if (l >= m) continue;
+      if (l < r) {
+        double* d = dwb_addr(it.seg, it.nseg, it.kw + jn, l);
+        if (d) *d = x[i];
+      } else {
+        it.Cout[(size_t)(l - r) * it.kn + jn] = x[i];
+      }
+    }
+  }
 }
 
 template <int MR>
@@ -540,7 +583,7 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
   const TrsmItem ti = items[blockIdx.x];
   const CluItem it = clu[ti.ci];
   const int r = rank[ti.ci];
-  if (it.m == 0 || r == 0) return;
+  if (it.m == 0 || (r == 0 && !it.dwb)) return;   // dwb with r = 0: C = B_n still goes to its slab
   // reflectors staged in shared memory when they fit, else read through L1
   const bool staged = (size_t)it.m * r + r <= (size_t)cap_words;
   const double* Vs = it.V;

@@ -27,6 +27,8 @@ struct CopyItem {
   int32_t sld, dld, rows, cols, trans, pad;
 };
 
+struct FusedSeg;
+
 // One cluster of a batch (a1-a4).
 struct CluItem {
   double* G;        // m x m, row-major ld m: holds A_ss on entry, the lower factor G_s on exit
@@ -38,6 +40,14 @@ struct CluItem {
   unsigned long long* nmax;   // max n-column norm of B_n (double bits; zeroed by the upload, set by TRSM)
   int32_t m, kw, kn, ldB;
   int32_t level, cluster, pad0, pad1;
+  // direct write-back (dwb = 1, DC path with device patching): CPQR writes the coarse-w rows
+  // and I_r, k_rotate_n the coarse-n rows, straight into the store blocks of row s (seg:
+  // the cluster's store segments in column order), and C = rows [r, m) of the rotated B_n
+  // into its persistent slab Cout (ld kn)
+  const FusedSeg* seg;
+  double* Dss;      // the diagonal store block (s, s), ld ldss
+  double* Cout;
+  int32_t nseg, ldss, dwb, pad2;
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
@@ -97,7 +107,7 @@ struct SchurSrc {
 };
 // Device-side patch of a batch's pre-planned second half with the kept ranks r_s read from
 // d_rank (no host round trip between CPQR and the Schur update): one thread per item.
-enum PatchKind : int32_t { PK_SRC = 0, PK_ROWS, PK_COLS, PK_I32, PK_FT, PK_CCOPY };
+enum PatchKind : int32_t { PK_SRC = 0, PK_ROWS, PK_COLS, PK_I32, PK_FT, PK_CCOPY, PK_K };
 struct PatchItem {
   void* target;          // SchurSrc* / CopyItem* / int32_t* / FormTItem*
   const double* base;    // B_s

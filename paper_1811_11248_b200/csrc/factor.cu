@@ -553,6 +553,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;
   const bool cpqr_v2 = std::getenv("HS_CPQR_V2") != nullptr;
   const bool no_fused = std::getenv("HS_NO_FUSED_POTRF_TRSM") != nullptr;   // separate gather/POTRF/TRSM
+  const bool no_dwb = std::getenv("HS_NO_DIRECT_WB") != nullptr;            // write-back pass instead
   // ---- multi-GPU (dist.cpp; protocol of oracle/dist.py) ---------------------
   // Rank g eliminates the clusters of its subdomains and stores only the blocks it holds
   // (it owns an endpoint).  Phase-I batches are local; before phase II and at the level end
@@ -740,6 +741,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       int max_m = 1;
       for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bo[bi]]);
       const bool fused = !nodc && max_m <= CI_MAX_M && !no_fused;
+      // direct write-back: CPQR / k_rotate_n write row s's coarse blocks, I_r and C_s
+      // themselves (no write-back pass); needs the device patch and CPQR v3
+      const bool dwb = fused && dpatch && !cpqr_single_cta && !cpqr_v2 && !no_dwb;
+      std::vector<int32_t> seg0v(nb, 0);
       // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
       int64_t wsz = 0;
       std::vector<int64_t> wo(nb);
@@ -792,6 +797,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           int32_t sb = seg0;
           const int32_t se = (int32_t)fseg.size();
           fci.push_back(FusedItem{pss, L.G[s], L.V[s], L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+          if (dwb) {
+            seg0v[bi] = seg0;
+            it.nseg = se - seg0;
+            it.Dss = const_cast<double*>(pss);
+            it.ldss = ldss;
+            it.dwb = 1;
+            if (kn > 0) {
+              L.C[s] = cslab.get((int64_t)m * kn);   // C_s = rows [r, m) of the rotated B_n (K <= m)
+              it.Cout = L.C[s];
+            }
+          }
           for (int32_t c0 = 0; c0 < ldB; c0 += 64) {
             const int32_t nc = std::min(64, ldB - c0);
             while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
@@ -802,7 +818,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         } else {
           for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
         }
-        if (!cpqr_single_cta && !cpqr_v2 && kw > 0) {   // v3 rotates the n-columns in k_rotate_n
+        if (!cpqr_single_cta && !cpqr_v2 && (kw > 0 || (dwb && kn > 0))) {   // v3 rotates the n-columns in k_rotate_n
           const int32_t rw = rot_tile_cols(m, max_m);
           for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
         }
@@ -820,6 +836,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upA.dev.ensure(upA.total);
         for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
         for (auto& f : fz) f.nmax = upA.dptr<unsigned long long>(iM) + f.bi;
+        for (int bi = 0; bi < nb; ++bi)
+          if (clu[bi].dwb) clu[bi].seg = upA.dptr<FusedSeg>(iS) + seg0v[bi];
         upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
         upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
         t_plan += now_s() - tp0;
@@ -908,7 +926,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           while (w < 63 && ((used >> w) & 1ull)) ++w;
           if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
           const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
-          SchurSrc sc{nullptr, ldB, 0, kn, (int32_t)nbc.size(), 0, 0};
+          SchurSrc sc{nullptr, dwb ? kn : ldB, 0, kn, (int32_t)nbc.size(), 0, 0};
           for (size_t a = 0; a < ns.size(); ++a)
             if (live[ns[a]] > 0) {
               nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], (int32_t)a});
@@ -926,7 +944,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         // write-back of row s: [I_r | coarse-w | coarse-n] into the blocks held here (rows r)
         double* p; int32_t ld, tr;
-        if (mine) {
+        if (mine && !dwb) {
           bs.get(s, s, p, ld, tr);
           if (nodc) {
             pd.diag = (int64_t)wb.size();
@@ -940,7 +958,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         int32_t col = 0;
         const auto& ro = row_offs(s);
         size_t kq = 0;
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = 0; pass < (dwb ? 0 : 2); ++pass)
           for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
             const int64_t o = ro[kq++];
             if (live[q] > 0 && o >= 0) {
@@ -1055,9 +1073,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           const int32_t m = live_at[pd.k], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
           PatchItem base{nullptr, Bs, pd.k, PK_SRC, m, ldB, kw, 0, 0, 0};
           if (pd.src >= 0) {
-            srcs[pd.src].C = Bs + kw;
+            srcs[pd.src].C = dwb ? L.C[s] : Bs + kw;
             srcs[pd.src].K = 0;
-            prefs.push_back({base, 0, (size_t)pd.src});
+            PatchItem q = base;
+            if (dwb) q.kind = PK_K;
+            prefs.push_back({q, 0, (size_t)pd.src});
           }
           for (size_t i = pd.wb_begin; i < pd.wb_end; ++i) {
             CopyItem& c = wb[i];
@@ -1076,7 +1096,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             q.kind = PK_FT;
             prefs.push_back({q, 3, (size_t)pd.ft});
           }
-          if (kn > 0) {   // C_s = B_s[r:, kw:] into a slab piece sized for K <= m rows
+          if (kn > 0 && !dwb) {   // C_s = B_s[r:, kw:] into a slab piece sized for K <= m rows
             L.C[s] = cslab.get((int64_t)m * kn);
             const int32_t step = std::max(1, 16384 / kn);
             for (int32_t i0 = 0; i0 < m; i0 += step) {

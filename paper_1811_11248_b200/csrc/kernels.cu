@@ -1133,6 +1133,7 @@ __global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_
       t->K = K;
       break;
     }
+    case PK_K: ((SchurSrc*)p.target)->K = K; break;   // C already in its slab
     case PK_ROWS: ((CopyItem*)p.target)->rows = r; break;
     case PK_COLS: ((CopyItem*)p.target)->cols = r; break;
     case PK_I32: *(int32_t*)p.target = r; break;

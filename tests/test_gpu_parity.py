@@ -268,3 +268,23 @@ def test_no_deferred_compression_eps0_exact(H, handle, name, gen, kw):
     A = p.to_scipy().toarray()
     x_ref = sla.cho_solve(sla.cho_factor(A), p.b)
     assert np.linalg.norm(H.hs_apply(f, p.b) - x_ref) / np.linalg.norm(x_ref) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_repeated_factor_pipeline_is_deterministic(H, handle):
+    """The factor pipelines batches (the host plans batch b+1 while batch b's second half
+    is still queued, the apply plan is built on a host worker): repeated factors of the
+    same system in one process must be bit-identical and never fault.  A larger 3-D case
+    (hundreds of batches, many sequential ones) so that staging reuse is exercised."""
+    p = gen_laplace3d(32, leaf_size=64)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=64)
+    v = np.random.default_rng(7).standard_normal(p.n)
+    ref = None
+    for _ in range(6):
+        f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+        x = H.hs_apply(f, v)
+        if ref is None:
+            ref = x
+        else:
+            assert np.array_equal(x, ref)
+        del f

@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round measurement (run under gpurun): bench line, launch list of the bench command,
-# ncu --set full captures of the top kernels.  Outputs in gpurun_out/ (copied to profiles/).
+# Round measurement (run under gpurun): bench line, launch list of one bench step, ncu --set
+# full captures of the top kernels.  Outputs in gpurun_out/ (copied to profiles/).
 mkdir -p gpurun_out
 R=${1:-r01}
 timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/${R}_bench.log 2>&1
@@ -9,13 +9,17 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 
   --log-file gpurun_out/${R}_launches.csv python tools/one_factor_pcg.py C2 \
   > gpurun_out/${R}_ncu_launches.log 2>&1
 python tools/summarize_launches.py gpurun_out/${R}_launches.csv > gpurun_out/${R}_launches_summary.txt 2>&1
-# full captures: level-0 CPQR batch, a level-3 Schur launch, one forward apply level kernel
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_cpqr3 --launch-skip 5 --launch-count 1 \
-  -o gpurun_out/${R}_ncu_cpqr3 -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_cpqr3.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_schur2 --launch-skip 400 --launch-count 1 \
-  -o gpurun_out/${R}_ncu_schur2 -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_schur2.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_apply_fwd --launch-skip 3 --launch-count 1 \
-  -o gpurun_out/${R}_ncu_apply -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_apply.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_schur2 --launch-skip 30 --launch-count 1 \
-  -o gpurun_out/${R}_ncu_schur2_l0 -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_schur2_l0.log 2>&1
-tail -c 400 gpurun_out/${R}_bench.log; head -12 gpurun_out/${R}_launches_summary.txt
+# full captures: level-0 CPQR batch, a level-3 and a level-0 Schur launch, the level-0 scaling
+# tiles, a forward and a backward apply level kernel
+cap() {   # name regex skip
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$2 --launch-skip $3 --launch-count 1 \
+    -o gpurun_out/${R}_ncu_$1 -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_$1.log 2>&1
+}
+cap cpqr3 k_cpqr3 5
+cap schur3 k_schur3 400
+cap schur3_l0 k_schur3 30
+cap scale k_scale_tile 5
+cap apply_fwd k_apply_fwd 3
+cap apply_bwd k_apply_bwd 5
+for f in gpurun_out/${R}_ncu_*.ncu-rep; do python tools/ncu_summary.py $f; done > gpurun_out/${R}_ncu_summary.jsonl 2>&1
+tail -c 600 gpurun_out/${R}_bench.log; head -16 gpurun_out/${R}_launches_summary.txt; cat gpurun_out/${R}_ncu_summary.jsonl
