@@ -116,6 +116,16 @@ struct PatchItem {
 };
 void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st);
 
+// A batch's kept ranks and the status published to mapped pinned host memory by one small
+// kernel (no D2H copies or events in the stream); the host spins on seq.
+struct RankPub {
+  volatile int32_t seq;
+  int32_t flag, level, cluster, pivot, pad;
+  double value;
+  int32_t rank[1];   // [max batch]
+};
+
+
 struct SchurTile2 {
   int32_t src, i0, j0, pad;
 };
@@ -210,6 +220,8 @@ struct DevStatus {
   int32_t flag, level, cluster, pivot;
   double value;
 };
+void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
+                    cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st);
 
@@ -248,6 +260,7 @@ int rot_tile_cols(int m, int max_m);   // columns per rotation tile (max_m: of t
 void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, const int32_t* d_rank,
                      cudaStream_t st);
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
+bool schur_needs_prep(const BlockDir& dir);
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st);
 // per-source column owners (nb index per n-column), once per batch before the waves

@@ -9,6 +9,7 @@
 // (P:626-628).  The elimination record (G, V, tau, C) stays in device memory for the
 // apply, whose plan (descriptors) is built alongside and replayed as a CUDA graph.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -532,12 +533,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   HS_CUDA(cudaMallocHost(&h_rank, sizeof(int32_t) * max_batch));
   std::unique_ptr<void, void (*)(void*)> rank_guard(d_rank, [](void* p) { cudaFree(p); });
   std::unique_ptr<void, void (*)(void*)> hrank_guard(h_rank, [](void* p) { cudaFreeHost(p); });
-  DevStatus* h_stat = nullptr;   // pinned: read back asynchronously with the ranks
-  HS_CUDA(cudaMallocHost(&h_stat, sizeof(DevStatus)));
-  std::unique_ptr<void, void (*)(void*)> hstat_guard(h_stat, [](void* p) { cudaFreeHost(p); });
-  cudaEvent_t ev_rank = nullptr;
-  HS_CUDA(cudaEventCreateWithFlags(&ev_rank, cudaEventDisableTiming));
-  std::unique_ptr<void, void (*)(void*)> evr_guard((void*)ev_rank, [](void* e) { cudaEventDestroy((cudaEvent_t)e); });
+  // dpatch: ranks + status published by k_publish into mapped pinned memory (host spins on seq)
+  RankPub* pub = nullptr;
+  HS_CUDA(cudaHostAlloc((void**)&pub, sizeof(RankPub) + sizeof(int32_t) * max_batch, cudaHostAllocMapped));
+  std::unique_ptr<void, void (*)(void*)> pub_guard(pub, [](void* p) { cudaFreeHost(p); });
+  RankPub* pub_dev = nullptr;
+  HS_CUDA(cudaHostGetDevicePointer((void**)&pub_dev, pub, 0));
+  pub->seq = 0;
+  int32_t pub_seq = 0;
 
   hs_factor_stats_t& S = f->stats;
   PhaseTimer pt;
@@ -679,18 +682,23 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (!pend_active) return;
       pend_active = false;
       const double tw0 = now_s();
-      HS_CUDA(cudaEventSynchronize(ev_rank));
+      for (uint64_t spin = 0; pub->seq != pub_seq; ++spin)
+        if ((spin & 0xFFFF) == 0xFFFF) {   // the stream faulted: report instead of spinning
+          const cudaError_t e = cudaStreamQuery(st);
+          if (e != cudaSuccess && e != cudaErrorNotReady) HS_CUDA(e);
+        }
+      std::atomic_thread_fence(std::memory_order_acquire);
       t_rank_wait += now_s() - tw0;
-      if (h_stat->flag) {
+      if (pub->flag) {
         char buf[256];
         std::snprintf(buf, sizeof buf, "NOT_SPD: Cholesky breakdown at level %d cluster %d pivot %d value %.17g (P:283)",
-                      h_stat->level, h_stat->cluster, h_stat->pivot, h_stat->value);
+                      pub->level, pub->cluster, pub->pivot, pub->value);
         fail(HS_E_NOT_SPD, buf);
       }
       pt.collect_a(S);
       for (size_t bi = 0; bi < pend_cl.size(); ++bi) {
         const int32_t s = pend_cl[bi].first, m = pend_cl[bi].second;
-        const int32_t r = m == 0 ? 0 : h_rank[bi];
+        const int32_t r = m == 0 ? 0 : pub->rank[bi];
         L.rank[s] = r;
         live[s] = r;
         done[s] = 1;
@@ -865,11 +873,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
         }
         pt.rec(pt.a[4], st);
-        HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
-        if (dpatch) {
-          HS_CUDA(cudaMemcpyAsync(h_stat, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
-          HS_CUDA(cudaEventRecord(ev_rank, st));
-        }
+        if (dpatch) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
+        else HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       } else {
         t_plan += now_s() - tp0;
       }
@@ -1214,7 +1219,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         pt.rec(pt.b[0], st);
         launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
-        launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
+        if (schur_needs_prep(bs.dir()))
+          launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
                         upB.dptr<SchurSrc>(jS), upB.dptr<NbCol>(jN), bs.dir(), st);

@@ -766,6 +766,7 @@ __global__ void __launch_bounds__(256) k_schur(const SchurTile* __restrict__ til
 // block pointers by binary search in the level's block directory (one lookup per distinct
 // owner pair of the tile).  HBM-bound: 16 bytes of read-modify-write per target element.
 constexpr int SCH_MAXO = 32;   // distinct owners per tile side held in the pointer table
+constexpr int SCH_NBS = 512;   // neighbour column starts staged for the owner searches (k_schur3)
 
 __device__ __forceinline__ int64_t dir_find(const BlockDir& d, int p, int q) {   // p >= q; -1 if absent
   int64_t lo = d.ptr[p], hi = d.ptr[p + 1];
@@ -938,17 +939,16 @@ __global__ void __launch_bounds__(256, 2) k_schur3(const SchurTile2* __restrict_
   __shared__ int nr, nc;
   __shared__ double* ptab[SCH_MAXO][SCH_MAXO];
   __shared__ int ldtab[SCH_MAXO];
+  __shared__ int nbcol[SCH_NBS];
   const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double* Cp = s.C + t.i0;
   const double* Cq = s.C + t.j0;
-  // (1) owners of the tile's rows (warp 0) and columns (warp 1) + the first K-chunk of C
-  int o0 = -1, o1 = -1;
-  if (w < 2) {
-    const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
-    if (lane < lim) o0 = s.own[base + lane];
-    if (lane + 32 < lim) o1 = s.own[base + lane + 32];
-  }
+  // (1) the neighbours' column starts into shared memory (the owner searches) + the first
+  // K-chunk of C
+  const bool nst = s.nnb <= SCH_NBS;
+  if (nst)
+    for (int a = tid; a < s.nnb; a += blockDim.x) nbcol[a] = nb[a].col;
   auto load_chunk = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -960,8 +960,21 @@ __global__ void __launch_bounds__(256, 2) k_schur3(const SchurTile2* __restrict_
     }
   };
   load_chunk(0);
-  if (w < 2) {   // (2) distinct owners in order (rows/cols are sorted by owner): ballots
+  __syncthreads();
+  if (w < 2) {   // (2) owners of the tile's rows (warp 0) / columns (warp 1) by binary search,
+                 // distinct owners in order (rows/cols are sorted by owner): ballots
     const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
+    auto owner = [&](int c) {   // last a with col(a) <= c
+      int lo = 0, hi = s.nnb - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((nst ? nbcol[mid] : nb[mid].col) <= c) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    const int o0 = lane < lim ? owner(base + lane) : -1;
+    const int o1 = lane + 32 < lim ? owner(base + lane + 32) : -1;
     const int prev0 = __shfl_up_sync(0xffffffffu, o0, 1);
     const int last0 = __shfl_sync(0xffffffffu, o0, 31);
     const int prev1 = __shfl_up_sync(0xffffffffu, o1, 1);
@@ -1148,6 +1161,32 @@ __global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_
 }
 }  // namespace
 
+namespace {
+__global__ void k_publish(const int32_t* __restrict__ rank, int n, const DevStatus* __restrict__ status, RankPub* pub,
+                          int32_t seq) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pub->rank[i] = rank[i];
+  if (threadIdx.x == 0) {
+    pub->flag = status->flag;
+    pub->level = status->level;
+    pub->cluster = status->cluster;
+    pub->pivot = status->pivot;
+    pub->value = status->value;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    pub->seq = seq;
+  }
+}
+}  // namespace
+
+void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
+                    cudaStream_t st) {
+  k_publish<<<1, 256, 0, st>>>(d_rank, n, d_status, pub, seq);
+  count_launch(1);
+}
+
 void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st) {
   if (n <= 0) return;
   k_patch<<<(n + 127) / 128, 128, 0, st>>>(d_items, n, d_rank);
@@ -1324,11 +1363,16 @@ void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* p
   k_level_pairs<<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(hptr, hq, poff, row_cl, nrows, pairs, dir);
   count_launch(1);
 }
+// k_schur2 (previous order; also when the store exceeds 2^31 doubles) reads the column owners
+// k_schur_prep writes; k_schur3 searches them itself
+bool schur_needs_prep(const BlockDir& dir) {
+  static const bool v2 = std::getenv("HS_SCHUR_V2") != nullptr;   // A/B: the previous tile kernel
+  return v2 || dir.total >= (int64_t)1 << 31;
+}
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st) {
   if (n <= 0) return;
-  static const bool v2 = std::getenv("HS_SCHUR_V2") != nullptr;   // A/B: the previous tile kernel
-  if (v2 || dir.total >= (int64_t)1 << 31) k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
+  if (schur_needs_prep(dir)) k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
   else {
     static const bool chk = std::getenv("HS_SCHUR_CHECK") != nullptr;
     BlockDir d2 = dir;
