@@ -63,7 +63,7 @@ struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operato
 struct FusedItem {
   const double* Ass;          // diagonal block in the store (lower, row-major, ld lda)
   double* G;                  // workspace G_s
-  double* Ginv;               // unused
+  double* Ginv;               // G_s^{-1} (k_chol writes it, k_scale_gemm reads it; the V workspace), or null
   double* B;                  // workspace B_s (m x ldB)
   unsigned long long* nmax;   // R-floor slot
   int32_t m, lda, ldB, kw;
@@ -224,6 +224,7 @@ void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, Ran
                     cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st);
+bool scale_by_inverse();
 
 // ---- launch accounting (every launcher counts its kernels; graphs count their nodes) -----
 void count_launch(int64_t n);

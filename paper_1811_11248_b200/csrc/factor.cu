@@ -804,7 +804,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           // segments are in column order: each tile takes the run of segments overlapping it
           int32_t sb = seg0;
           const int32_t se = (int32_t)fseg.size();
-          fci.push_back(FusedItem{pss, L.G[s], L.V[s], L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+          double* ginv = scale_by_inverse() ? L.V[s] : nullptr;   // G^{-1} in V (CPQR overwrites it later)
+          fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
           if (dwb) {
             seg0v[bi] = seg0;
             it.nseg = se - seg0;
@@ -821,7 +822,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
             int32_t sf = sb;
             while (sf < se && fseg[sf].col < c0 + nc) ++sf;
-            fz.push_back(FusedItem{pss, L.G[s], L.V[s], L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
+            fz.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
           }
         } else {
           for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
