@@ -294,15 +294,27 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
     const ApplySrc S = a.src[tk.s];
     const int m = S.m, r = S.r, K = m - r;
     const bool fin = tk.chunk == S.nchunk - 1;
-    if (tk.nc > 0) {
+    const bool has_parts = tk.nc > 0;
+    const bool cst = has_parts && K * tk.nc <= BWD_STAGE;
+    // shared-memory stage: [the chunk's C columns | T_s | the other chunks' partials]
+    const int coff = cst ? K * tk.nc : 0;
+    const bool tst = coff + m * m <= BWD_STAGE;
+    double* tS = bst + coff;
+    const int np = has_parts ? (S.nchunk - 1) * K : 0;
+    double* pS = bst + coff + (tst ? m * m : 0);
+    const bool pst = coff + (tst ? m * m : 0) + np <= BWD_STAGE;
+    if (fin) {   // the finisher's inputs that are final already: x_c, y_f, T_s (before any wait)
+      for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.xc + i);
+      for (int k = tid; k < K; k += APPLY_THREADS) u[r + k] = __ldcg(S.yf + k);
+      if (tst)
+        for (int e = tid; e < m * m; e += APPLY_THREADS) tS[e] = S.T[e];
+    }
+    if (has_parts) {
       const int nnb = tk.b1 - tk.b0;
-      const bool cst = K * tk.nc <= BWD_STAGE;
       for (int b = warp; b < nnb; b += nw) {   // column map (+ the chunk's C columns)
         const BwdNb nb = a.bnb[tk.b0 + b];
         for (int i = lane; i < nb.len; i += 32) ccol[nb.off + i] = nb.col + i;
       }
-      if (fin)
-        for (int e = tid * 16; e < m * m; e += APPLY_THREADS * 16) prefetch_l2(S.T + e);
       __syncthreads();
       if (cst) {
         for (int e = tid; e < K * tk.nc; e += APPLY_THREADS) {
@@ -356,20 +368,11 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
         __syncthreads();   // bst, ccol, xn reusable
         continue;
       }
-      __syncthreads();   // bst free for the finish
     }
-    // ---- finish s: x_c, y_f, the other chunks' partials (polled) and T_s in one pass
-    const bool has_parts = tk.nc > 0;
-    const bool tst = m * m <= BWD_STAGE - (has_parts ? S.nchunk * K : 0);
-    double* pS = bst;                                     // nchunk x K
-    double* tS = bst + (has_parts ? S.nchunk * K : 0);    // m x m
-    const bool pst = !has_parts || S.nchunk * K <= BWD_STAGE;
-    for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.xc + i);
-    for (int k = tid; k < K; k += APPLY_THREADS) u[r + k] = __ldcg(S.yf + k);
-    if (tst)
-      for (int e = tid; e < m * m; e += APPLY_THREADS) tS[e] = S.T[e];
-    if (has_parts && pst)
-      for (int e = tid; e < (S.nchunk - 1) * K; e += APPLY_THREADS) pS[e] = ld_poll(a.parts + S.part + e);
+    // ---- finish s: the other chunks' partials (polled), x_f = y_f - their sum (chunk
+    // order), x_s = T_s^T [x_c; x_f]
+    if (pst)
+      for (int e = tid; e < np; e += APPLY_THREADS) pS[e] = ld_poll(a.parts + S.part + e);
     __syncthreads();
     if (has_parts)
       for (int k = tid; k < K; k += APPLY_THREADS) {
