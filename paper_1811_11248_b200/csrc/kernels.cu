@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
 // owner loads and the owner dedupe (warp ballots instead of a serial scan) overlap; the
 // target addresses are resolved and the 16 old values per thread are in flight while the
 // DMMA product runs; the subtract-and-store follows.
-__global__ void __launch_bounds__(256, 2) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
+__global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
   const SchurTile2 t = tiles[blockIdx.x];
   const SchurSrc s = srcs[t.src];
