@@ -321,8 +321,12 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     // (2) decision from the CS messages (identical in every thread of every CTA)
     bar_wait(sm_addr(&sh.bar1[buf]), par);
     if (j < 60) CQ_TR(4 + 4 * j);
-    double M = -1.0;
-    for (int k = 0; k < CS; ++k) M = fmax(M, slot[(size_t)k * msgw]);
+    // the CS local maxima: lane k of every warp reads CTA k's (CS <= 16), warp max and a
+    // ballot for the lowest CTA over the window (the same values in every warp)
+    const double sv = lane < CS ? slot[(size_t)lane * msgw] : -1.0;
+    double M = sv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
     if (j == 0) {
       tau_s = relative ? eps * M : eps;
       if (relative && eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(M, Rn));
@@ -332,8 +336,8 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       break;
     }
     const double thr = CQ_WINDOW * M;
-    int k0 = 0;
-    while (!(slot[(size_t)k0 * msgw] >= thr)) ++k0;   // lowest CTA holding a global candidate
+    const unsigned over = __ballot_sync(0xffffffffu, lane < CS && sv >= thr);
+    const int k0 = over ? __ffs(over) - 1 : 0;           // lowest CTA holding a global candidate
     const double* vmsg = slot + (size_t)k0 * msgw;     // its reflector
     int p = (int)vmsg[2];
     if (!(vmsg[1] >= thr)) {
