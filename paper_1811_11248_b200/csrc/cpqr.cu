@@ -479,7 +479,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   CQ_TR(250);
   __syncthreads();
   // ---- coarse-w rows back to global memory (rows [0, r) of the slice) -----------------
-  if (SM)
+  if (SM && (!it.dwb || it.keepB))   // (direct write-back: only the debug records need B)
     for (int e = tid; e < r * nw; e += CQ_THREADS) {
       const int l = e / nw, c = e % nw;
       it.B[(size_t)l * ld + w_lo + c] = W[(size_t)c * ldm + l];
@@ -558,11 +558,12 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
 #pragma unroll
     for (int i = 0; i < MR; ++i) x[i] -= td * vv[i];
   }
+  if (!it.dwb || it.keepB)
 #pragma unroll
-  for (int i = 0; i < MR; ++i) {
-    const int l = t + i * G;
-    if (act && l < m) col[(size_t)l * ld] = x[i];
-  }
+    for (int i = 0; i < MR; ++i) {
+      const int l = t + i * G;
+      if (act && l < m) col[(size_t)l * ld] = x[i];
+    }
   if (it.dwb && act) {   // coarse-n rows into the store blocks (s, q), C rows into the slab
     const int jn = c0 + grp;
 #pragma unroll

@@ -47,7 +47,7 @@ struct CluItem {
   const FusedSeg* seg;
   double* Dss;      // the diagonal store block (s, s), ld ldss
   double* Cout;
-  int32_t nseg, ldss, dwb, pad2;
+  int32_t nseg, ldss, dwb, keepB;   // keepB: also write the coarse rows / rotated B_n back to B (records)
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)

@@ -812,6 +812,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             it.Dss = const_cast<double*>(pss);
             it.ldss = ldss;
             it.dwb = 1;
+            it.keepB = f->keep_records ? 1 : 0;
             if (kn > 0) {
               L.C[s] = cslab.get((int64_t)m * kn);   // C_s = rows [r, m) of the rotated B_n (K <= m)
               it.Cout = L.C[s];

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-HS_CQ_TRACE=200 timeout 120 python tools/one_factor_pcg.py 2>&1 | grep "cq trace" | head -5
-HS_PROFILE=1 python tools/factor_loop.py 2>&1 | grep "level [0-4]:" | tail -5 | sed 's/sum m.*//' | cut -c1-150
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
-for i in 1 2; do timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "EXIT $?"; tail -1 gpurun_out/bench.log | cut -c1-200; done
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "TESTS_EXIT $?" >> gpurun_out/gpu_tests.log; tail -2 gpurun_out/gpu_tests.log
+for i in 1 2; do timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "EXIT $?"; tail -1 gpurun_out/bench.log | cut -c1-200; done
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_cpqr3 --launch-skip 5 --launch-count 1 -o gpurun_out/r01e_ncu_cpqr3 -f python tools/profile_run.py C2 > gpurun_out/r01e_ncu_cpqr3.log 2>&1; python tools/ncu_summary.py gpurun_out/r01e_ncu_cpqr3.ncu-rep

@@ -16,6 +16,7 @@ cap() {   # name regex skip
     -o gpurun_out/${R}_ncu_$1 -f python tools/profile_run.py C2 > gpurun_out/${R}_ncu_$1.log 2>&1
 }
 cap cpqr3 k_cpqr3 5
+cap cpqr3_l2 k_cpqr3 150
 cap schur3 k_schur3 400
 cap schur3_l0 k_schur3 30
 cap scale k_scale_tile 5
