@@ -173,6 +173,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   do {                                                                      \
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[k] = clock64(); \
   } while (0)
+  const bool trace_split = trace && trace[255] != 0;   // HS_CQ_TRACE_SPLIT: stamp 4 at the push
   CQ_TR(0);
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -317,10 +318,11 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       if (lane < CS)
         bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
                   remote(sm_addr(&sh.bar1[buf]), lane));
+      if (trace_split && j < 60) CQ_TR(4 + 4 * j);   // local work done, message sent
     }
     // (2) decision from the CS messages (identical in every thread of every CTA)
     bar_wait(sm_addr(&sh.bar1[buf]), par);
-    if (j < 60) CQ_TR(4 + 4 * j);
+    if (!trace_split && j < 60) CQ_TR(4 + 4 * j);
     // the CS local maxima: lane k of every warp reads CTA k's (CS <= 16), warp max and a
     // ballot for the lowest CTA over the window (the same values in every warp)
     const double sv = lane < CS ? slot[(size_t)lane * msgw] : -1.0;
@@ -690,6 +692,10 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
   if (launches++ == trace_at) {
     HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
     HS_CUDA(cudaMemsetAsync(trace, 0, 256 * sizeof(long long), st));
+    if (std::getenv("HS_CQ_TRACE_SPLIT")) {
+      static const long long one = 1;
+      HS_CUDA(cudaMemcpyAsync(trace + 255, &one, sizeof one, cudaMemcpyHostToDevice, st));
+    }
   }
   if (MR == 8) {
     if (sm) launch_one<8, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
