@@ -123,6 +123,24 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// the same wait with cluster-scope acquire: the messages arrive as remote st.shared::cluster
+// stores ordered by the senders' release arrivals
+__device__ __forceinline__ void bar_wait_cl(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(__double_as_longlong(v)) : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -174,6 +192,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[k] = clock64(); \
   } while (0)
   const bool trace_split = trace && trace[255] != 0;   // HS_CQ_TRACE_SPLIT: stamp 4 at the push
+  // bit 1 of `relative`: step messages by direct remote stores + release arrivals (count-CS
+  // barrier) instead of bulk async copies (HS_CPQR_DIRECT_MSG=1; slower, kept for A/B)
+  const bool direct = (relative & 2) != 0;
+  relative &= 1;
   CQ_TR(0);
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -202,7 +224,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      bar_init(sm_addr(&sh.bar1[b]), 1);   // the local expect_tx arrival; data by complete_tx
+      bar_init(sm_addr(&sh.bar1[b]), direct ? CS : 1);   // CS release arrivals, or the local expect_tx
       bar_init(sm_addr(&sh.bar3[b]), 1);
     }
     bar_init(sm_addr(&sh.bar2), 1);
@@ -264,7 +286,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     // (1) local max, local candidate and its reflector -> every CTA
     lm = wmax(lm);
     if (lane == 0) sh.wred[wid] = lm;
-    if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
+    if (tid == 0 && !direct) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
     __syncthreads();
     if (j < 60) CQ_TR(3 + 4 * j);
     if (wid == 0) {
@@ -315,13 +337,26 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       if (lane == 0) mymsg[0] = Mc;
       fence_proxy_async();
       __syncwarp();
-      if (lane < CS)
+      if (direct) {
+        // the message into every CTA's slot (this CTA's included) by remote stores, then one
+        // release arrival per destination
+        const uint32_t dst0 = sm_addr(slot + (size_t)crank * msgw);
+        for (int e = lane; e < CS * msgw; e += 32) {
+          const int k = e / msgw, w = e - k * msgw;
+          st_cluster(remote(dst0 + 8u * (uint32_t)w, k), mymsg[w]);
+        }
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        __syncwarp();
+        if (lane < CS) arrive_remote(remote(sm_addr(&sh.bar1[buf]), lane));
+      } else if (lane < CS) {
         bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
                   remote(sm_addr(&sh.bar1[buf]), lane));
+      }
       if (trace_split && j < 60) CQ_TR(4 + 4 * j);   // local work done, message sent
     }
     // (2) decision from the CS messages (identical in every thread of every CTA)
-    bar_wait(sm_addr(&sh.bar1[buf]), par);
+    if (direct) bar_wait_cl(sm_addr(&sh.bar1[buf]), par);
+    else bar_wait(sm_addr(&sh.bar1[buf]), par);
     if (!trace_split && j < 60) CQ_TR(4 + 4 * j);
     // the CS local maxima: lane k of every warp reads CTA k's (CS <= 16), warp max and a
     // ballot for the lowest CTA over the window (the same values in every warp)
@@ -633,7 +668,10 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, relative, d_rank, trace));
+  // HS_CPQR_DIRECT_MSG=1: step messages by remote stores + release arrivals instead of bulk
+  // async copies — measured slower on C2 (message phase 3.6k -> 5.0-5.6k cycles per step)
+  static const bool direct = std::getenv("HS_CPQR_DIRECT_MSG") != nullptr;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, (relative ? 1 : 0) | (direct ? 2 : 0), d_rank, trace));
   count_launch(1);
 }
 
