@@ -1170,12 +1170,13 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         prep_words += ((int64_t)sc.kn + 1) / 2;
         max_kn_src = std::max(max_kn_src, sc.kn);
       }
-      char* prep = prep_words ? (char*)dc.alloc(8 * prep_words) : nullptr;
+      const bool need_prep = schur_needs_prep(bs.dir());   // k_schur3 finds the owners itself
+      char* prep = (prep_words && need_prep) ? (char*)dc.alloc(8 * prep_words) : nullptr;
       {
         char* cur = prep;
         for (size_t k = 0; k < srcs.size(); ++k) {
           srcs[k].own = (int32_t*)cur;
-          cur += 8 * (((int64_t)srcs[k].kn + 1) / 2);
+          if (cur) cur += 8 * (((int64_t)srcs[k].kn + 1) / 2);
           srcs[k].pairs = lp.pairs + lp.poff[src_cl[k]];
         }
       }
@@ -1221,7 +1222,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         pt.rec(pt.b[0], st);
         launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
-        if (schur_needs_prep(bs.dir()))
+        if (need_prep)
           launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
