@@ -546,6 +546,8 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 template <int MR, bool SM>
 __global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
                                                           int32_t* __restrict__ rank_out, long long* trace) {
+  pdl_trigger();
+  pdl_wait();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int item = blockIdx.x / (int)cl.num_blocks();
@@ -621,6 +623,8 @@ template <int MR>
 __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restrict__ clu,
                                                          const TrsmItem* __restrict__ items,
                                                          const int32_t* __restrict__ rank, int cap_words) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double rsm[];
   const TrsmItem ti = items[blockIdx.x];
   const CluItem it = clu[ti.ci];
@@ -657,11 +661,13 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
     HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   });
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(n * CS);
   cfg.blockDim = dim3(CQ_THREADS);
   cfg.dynamicSmemBytes = smem;
@@ -773,13 +779,13 @@ void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int m
     std::call_once(once, [] {
       HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
-    k_rotate_n<8><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
+    launch_pdl(k_rotate_n<8>, dim3(n), dim3(CQ_THREADS), smem, st, d_clu, d_items, (const int32_t*)d_rank, (int)words);
   } else {
     static std::once_flag once;
     std::call_once(once, [] {
       HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_n<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
-    k_rotate_n<16><<<n, CQ_THREADS, smem, st>>>(d_clu, d_items, d_rank, (int)words);
+    launch_pdl(k_rotate_n<16>, dim3(n), dim3(CQ_THREADS), smem, st, d_clu, d_items, (const int32_t*)d_rank, (int)words);
   }
   count_launch(1);
 }

@@ -27,6 +27,31 @@ struct CopyItem {
   int32_t sld, dld, rows, cols, trans, pad;
 };
 
+// ---- programmatic dependent launch (sm_90+) ------------------------------------------
+// The per-batch kernels are launched with programmatic stream serialization: a kernel may be
+// scheduled while its stream predecessor drains; it calls pdl_wait() (griddepcontrol.wait:
+// the predecessor grid has completed and its writes are visible) before touching anything
+// the predecessor produced, and pdl_trigger() to let its own successor launch early.
+bool pdl_enabled();   // HS_NO_PDL=1 turns the attribute off (A/B)
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+#endif
+
 struct FusedSeg;
 
 // One cluster of a batch (a1-a4).

@@ -25,6 +25,8 @@ constexpr int ST_TW = 64;   // columns per k_scale_tile CTA
 
 template <int R4>
 __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ items, DevStatus* status) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double sm[];
   const FusedItem it = items[blockIdx.x];
   const int m = it.m;
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ item
 template <int R>
 __global__ void __launch_bounds__(256) k_scale_gemm(const FusedItem* __restrict__ items,
                                                     const FusedSeg* __restrict__ segs) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double sm[];
   const FusedItem it = items[blockIdx.x];
   const int m = it.m;
@@ -223,6 +227,8 @@ __global__ void __launch_bounds__(256) k_scale_gemm(const FusedItem* __restrict_
 template <int R4>
 __global__ void __launch_bounds__(256) k_scale_tile(const FusedItem* __restrict__ items,
                                                     const FusedSeg* __restrict__ segs) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double sm[];
   const FusedItem it = items[blockIdx.x];
   const int m = it.m;
@@ -310,7 +316,7 @@ void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, 
 #define HS_CH(RR)                                               \
   case RR:                                                      \
     set_smem_attr((const void*)k_chol<4 * RR>, sm);             \
-    k_chol<4 * RR><<<n, 256, sm, st>>>(d_items, status);        \
+    launch_pdl(k_chol<4 * RR>, dim3(n), dim3(256), sm, st, d_items, status); \
     break;
   switch (R) {
     HS_CH(1) HS_CH(2) HS_CH(3) HS_CH(4) HS_CH(5) HS_CH(6) HS_CH(7)
@@ -336,7 +342,7 @@ void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs,
 #define HS_SG(RR)                                                     \
   case RR:                                                            \
     set_smem_attr((const void*)k_scale_gemm<RR>, sm);                 \
-    k_scale_gemm<RR><<<n, 256, sm, st>>>(d_items, d_segs);            \
+    launch_pdl(k_scale_gemm<RR>, dim3(n), dim3(256), sm, st, d_items, d_segs); \
     break;
     switch ((max_m + 15) / 16) {
       HS_SG(1) HS_SG(2) HS_SG(3) HS_SG(4) HS_SG(5) HS_SG(6) HS_SG(7)
@@ -351,7 +357,7 @@ void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs,
 #define HS_ST(RR)                                                     \
   case RR:                                                            \
     set_smem_attr((const void*)k_scale_tile<4 * RR>, sm);             \
-    k_scale_tile<4 * RR><<<n, 256, sm, st>>>(d_items, d_segs);        \
+    launch_pdl(k_scale_tile<4 * RR>, dim3(n), dim3(256), sm, st, d_items, d_segs); \
     break;
   switch (R) {
     HS_ST(1) HS_ST(2) HS_ST(3) HS_ST(4) HS_ST(5) HS_ST(6) HS_ST(7)

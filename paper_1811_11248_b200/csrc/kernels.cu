@@ -927,6 +927,8 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
 // DMMA product runs; the subtract-and-store follows.
 __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
+  pdl_trigger();
+  pdl_wait();
   const SchurTile2 t = tiles[blockIdx.x];
   const SchurSrc s = srcs[t.src];
   if (s.K <= 0) return;   // planned before its rank was known and kept everything (uniform)
@@ -1110,6 +1112,11 @@ std::atomic<int64_t> g_launches{0};
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("HS_NO_PDL") == nullptr;
+  return on;
+}
+
 void set_smem_attr(const void* f, size_t bytes) { set_smem(f, bytes); }
 
 namespace {
@@ -1135,6 +1142,8 @@ void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32
 }
 namespace {
 __global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PatchItem p = items[i];
@@ -1164,6 +1173,8 @@ __global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_
 namespace {
 __global__ void k_publish(const int32_t* __restrict__ rank, int n, const DevStatus* __restrict__ status, RankPub* pub,
                           int32_t seq) {
+  pdl_trigger();
+  pdl_wait();
   for (int i = threadIdx.x; i < n; i += blockDim.x) pub->rank[i] = rank[i];
   if (threadIdx.x == 0) {
     pub->flag = status->flag;
@@ -1183,13 +1194,13 @@ __global__ void k_publish(const int32_t* __restrict__ rank, int n, const DevStat
 
 void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
                     cudaStream_t st) {
-  k_publish<<<1, 256, 0, st>>>(d_rank, n, d_status, pub, seq);
+  launch_pdl(k_publish, dim3(1), dim3(256), 0, st, d_rank, n, d_status, pub, seq);
   count_launch(1);
 }
 
 void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st) {
   if (n <= 0) return;
-  k_patch<<<(n + 127) / 128, 128, 0, st>>>(d_items, n, d_rank);
+  launch_pdl(k_patch, dim3((n + 127) / 128), dim3(128), 0, st, d_items, n, d_rank);
   count_launch(1);
 }
 
@@ -1377,7 +1388,7 @@ void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, cons
     static const bool chk = std::getenv("HS_SCHUR_CHECK") != nullptr;
     BlockDir d2 = dir;
     if (chk) d2.total = -dir.total;
-    k_schur3<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, d2);
+    launch_pdl(k_schur3, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
   }
   count_launch(1);
 }
