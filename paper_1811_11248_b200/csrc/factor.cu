@@ -836,6 +836,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
       }
+      // the first half's launches: at once (host patch), or (device patch) deferred until the
+      // second half is planned, so that both uploads precede one uninterrupted kernel chain
+      std::function<void()> first_half_launch;
       if (nb > 0) {
         split_copies(gather);
         upA.reset();
@@ -851,32 +854,40 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
         upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
         t_plan += now_s() - tp0;
-        upA.send(st);
-        pt.rec(pt.a[0], st);
-        if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
-          pt.rec(pt.a[1], st);
-          launch_chol(upA.dptr<FusedItem>(iI), (int)fci.size(), max_m, d_status, st);
-          pt.rec(pt.a[2], st);
-          launch_scale_tiles(upA.dptr<FusedItem>(iF), (int)fz.size(), upA.dptr<FusedSeg>(iS), max_m, st);
-        } else {
-          launch_copy2d(upA.dptr<CopyItem>(iG), (int)gather.size(), st);
-          pt.rec(pt.a[1], st);
-          if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
-          pt.rec(pt.a[2], st);
-          if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), max_m, st);
-          else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)trsm.size(), st);   // R-floor
-        }
-        pt.rec(pt.a[3], st);
         d_clu_batch = upA.dptr<CluItem>(iC);
-        if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
-        else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-        else {
-          launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-          launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)rot.size(), max_m, d_rank, st);
+        const size_t nfz = fz.size(), nfci = fci.size(), ngather = gather.size(), ntrsm = trsm.size(),
+                     nrot = rot.size();
+        first_half_launch = [&, iG, iC, iT, iR, iF, iS, iI, fused, max_m, nb, nfz, nfci, ngather, ntrsm, nrot, clu]() {
+          pt.rec(pt.a[0], st);
+          if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
+            pt.rec(pt.a[1], st);
+            launch_chol(upA.dptr<FusedItem>(iI), (int)nfci, max_m, d_status, st);
+            pt.rec(pt.a[2], st);
+            launch_scale_tiles(upA.dptr<FusedItem>(iF), (int)nfz, upA.dptr<FusedSeg>(iS), max_m, st);
+          } else {
+            launch_copy2d(upA.dptr<CopyItem>(iG), (int)ngather, st);
+            pt.rec(pt.a[1], st);
+            if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
+            pt.rec(pt.a[2], st);
+            if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, max_m, st);
+            else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, st);   // R-floor
+          }
+          pt.rec(pt.a[3], st);
+          if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
+          else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+          else {
+            launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+            launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)nrot, max_m, d_rank, st);
+          }
+          pt.rec(pt.a[4], st);
+          if (dpatch) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
+          else HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+        };
+        if (!dpatch) {
+          upA.send(st);
+          first_half_launch();
+          first_half_launch = nullptr;
         }
-        pt.rec(pt.a[4], st);
-        if (dpatch) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
-        else HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
       } else {
         t_plan += now_s() - tp0;
       }
@@ -1218,7 +1229,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
         upB.copy_in(jX, patch);
         t_plan += now_s() - tp1;
-        upB.send(st);
+        if (first_half_launch) {   // device patch: both uploads, then the whole batch's kernels
+          upA.send(st);
+          upB.send(st);
+          first_half_launch();
+          first_half_launch = nullptr;
+        } else {
+          upB.send(st);
+        }
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         pt.rec(pt.b[0], st);
         launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
@@ -1259,6 +1277,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
       } else {
         t_plan += now_s() - tp1;
+      }
+      if (first_half_launch) {   // no second half (every cluster of the batch empty)
+        upA.send(st);
+        first_half_launch();
+        first_half_launch = nullptr;
       }
       if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)
       for (double* b : rbuf)
