@@ -139,7 +139,7 @@ struct PatchItem {
   int32_t bi, kind, m, ldB;
   int32_t kw, i0, step, pad;
 };
-void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st);
+
 
 // A batch's kept ranks and the status published to mapped pinned host memory by one small
 // kernel (no D2H copies or events in the stream); the host spins on seq.
@@ -245,6 +245,9 @@ struct DevStatus {
   int32_t flag, level, cluster, pivot;
   double value;
 };
+// the patch items; with pub: also publishes the batch's ranks (one extra block)
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st, int nrank = 0,
+                  const DevStatus* d_status = nullptr, RankPub* pub = nullptr, int32_t seq = 0);
 void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
                     cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);

@@ -838,7 +838,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       // the first half's launches: at once (host patch), or (device patch) deferred until the
       // second half is planned, so that both uploads precede one uninterrupted kernel chain
-      std::function<void()> first_half_launch;
+      std::function<void(bool)> first_half_launch;   // argument: publish the ranks here
       if (nb > 0) {
         split_copies(gather);
         upA.reset();
@@ -857,7 +857,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         d_clu_batch = upA.dptr<CluItem>(iC);
         const size_t nfz = fz.size(), nfci = fci.size(), ngather = gather.size(), ntrsm = trsm.size(),
                      nrot = rot.size();
-        first_half_launch = [&, iG, iC, iT, iR, iF, iS, iI, fused, max_m, nb, nfz, nfci, ngather, ntrsm, nrot, clu]() {
+        first_half_launch = [&, iG, iC, iT, iR, iF, iS, iI, fused, max_m, nb, nfz, nfci, ngather, ntrsm, nrot,
+                             clu](bool publish) {
           pt.rec(pt.a[0], st);
           if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
             pt.rec(pt.a[1], st);
@@ -880,12 +881,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)nrot, max_m, d_rank, st);
           }
           pt.rec(pt.a[4], st);
-          if (dpatch) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
-          else HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+          if (dpatch) {
+            if (publish) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
+          } else {
+            HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+          }
         };
         if (!dpatch) {
           upA.send(st);
-          first_half_launch();
+          first_half_launch(true);
           first_half_launch = nullptr;
         }
       } else {
@@ -1229,17 +1233,21 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
         upB.copy_in(jX, patch);
         t_plan += now_s() - tp1;
+        const bool pub_here = (bool)first_half_launch;   // the patch kernel publishes the ranks
         if (first_half_launch) {   // device patch: both uploads, then the whole batch's kernels
           upA.send(st);
           upB.send(st);
-          first_half_launch();
+          first_half_launch(false);
           first_half_launch = nullptr;
         } else {
           upB.send(st);
         }
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         pt.rec(pt.b[0], st);
-        launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
+        if (pub_here)
+          launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st, nb, d_status, pub_dev, ++pub_seq);
+        else
+          launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
         if (need_prep)
           launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
@@ -1280,7 +1288,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       if (first_half_launch) {   // no second half (every cluster of the batch empty)
         upA.send(st);
-        first_half_launch();
+        first_half_launch(true);
         first_half_launch = nullptr;
       }
       if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)

@@ -1141,9 +1141,33 @@ void launch_symcheck(const double* vals, const int64_t* tmap, int64_t nnz, int32
   count_launch(1);
 }
 namespace {
-__global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank) {
+__device__ void publish_body(const int32_t* __restrict__ rank, int n, const DevStatus* __restrict__ status,
+                             RankPub* pub, int32_t seq) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pub->rank[i] = rank[i];
+  if (threadIdx.x == 0) {
+    pub->flag = status->flag;
+    pub->level = status->level;
+    pub->cluster = status->cluster;
+    pub->pivot = status->pivot;
+    pub->value = status->value;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    pub->seq = seq;
+  }
+}
+
+// the patch items, plus (pub != null) one extra block that publishes the batch's ranks
+__global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank, int nrank,
+                        const DevStatus* __restrict__ status, RankPub* pub, int32_t seq) {
   pdl_trigger();
   pdl_wait();
+  if (pub && blockIdx.x == gridDim.x - 1) {
+    publish_body(rank, nrank, status, pub, seq);
+    return;
+  }
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PatchItem p = items[i];
@@ -1171,24 +1195,13 @@ __global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_
 }  // namespace
 
 namespace {
+__device__ void publish_body(const int32_t* __restrict__ rank, int n, const DevStatus* __restrict__ status,
+                             RankPub* pub, int32_t seq);
 __global__ void k_publish(const int32_t* __restrict__ rank, int n, const DevStatus* __restrict__ status, RankPub* pub,
                           int32_t seq) {
   pdl_trigger();
   pdl_wait();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) pub->rank[i] = rank[i];
-  if (threadIdx.x == 0) {
-    pub->flag = status->flag;
-    pub->level = status->level;
-    pub->cluster = status->cluster;
-    pub->pivot = status->pivot;
-    pub->value = status->value;
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    pub->seq = seq;
-  }
+  publish_body(rank, n, status, pub, seq);
 }
 }  // namespace
 
@@ -1198,9 +1211,11 @@ void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, Ran
   count_launch(1);
 }
 
-void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st) {
-  if (n <= 0) return;
-  launch_pdl(k_patch, dim3((n + 127) / 128), dim3(128), 0, st, d_items, n, d_rank);
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st, int nrank,
+                  const DevStatus* d_status, RankPub* pub, int32_t seq) {
+  const int blocks = (n + 127) / 128 + (pub ? 1 : 0);
+  if (blocks <= 0) return;
+  launch_pdl(k_patch, dim3(blocks), dim3(128), 0, st, d_items, n, d_rank, nrank, d_status, pub, seq);
   count_launch(1);
 }
 
