@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(256) k_scale_tile(const FusedItem* __restrict_
     const int i = e / m, k = e % m;
     if (k <= i) g[i * ldg + k] = it.G[e];
   }
+  // 1 / G_ii in the unused last slot of row i: the substitution chain multiplies instead of
+  // dividing (a long FP64 instruction sequence on the critical path of every step)
+  if (tid < m) g[tid * ldg + m] = 1.0 / it.G[(int64_t)tid * m + tid];
   for (int e = tid; e < m * ST_TW; e += blockDim.x) x[e] = 0.0;
   __syncthreads();
   for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {   // the tile's columns from the store
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(256) k_scale_tile(const FusedItem* __restrict_
     for (int gi = 0; gi < 4; ++gi) {
       const int i = 4 * ti + gi;
       if (i < m) {   // uniform over the CTA
-        if (gr == gi) r[ti] = r[ti] / g[i * ldg + i];
+        if (gr == gi) r[ti] = r[ti] * g[i * ldg + m];
         const double xi = __shfl_sync(0xffffffffu, r[ti], (lane & 7) + 8 * gi);
 #pragma unroll
         for (int t = ti; t < R4; ++t) {
