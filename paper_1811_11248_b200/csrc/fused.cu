@@ -23,7 +23,7 @@ namespace {
 
 constexpr int ST_TW = 64;   // columns per k_scale_tile CTA
 
-template <int R4>
+template <int R4, bool INV>
 __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ items, DevStatus* status) {
   pdl_trigger();
   pdl_wait();
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ item
     const int i = e / m, j = e % m;
     it.G[e] = j <= i ? U[j * ldu + i] : 0.0;
   }
-  if (!it.Ginv) return;
+  if (!INV || !it.Ginv) return;
   // G_s^{-1} (lower) by forward substitution on I, warp-synchronously: warp w owns columns
   // cb + 8w + (lane & 7), lane group gr = lane >> 3 owns rows gr + 4t in registers; the
   // pivot of row i is broadcast by shuffle (no CTA barrier in the m-step chain)
@@ -316,10 +316,16 @@ void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, 
   if (n <= 0) return;
   const size_t sm = sizeof(double) * (size_t)max_m * (max_m + 1);
   const int R = (max_m + 15) / 16;   // R4 = 4 R rows per lane group (the inverse)
+  if (!scale_by_inverse()) {   // no inverse: one lean instantiation for every m
+    set_smem_attr((const void*)k_chol<4, false>, sm);
+    launch_pdl(k_chol<4, false>, dim3(n), dim3(256), sm, st, d_items, status);
+    count_launch(1);
+    return;
+  }
 #define HS_CH(RR)                                               \
   case RR:                                                      \
-    set_smem_attr((const void*)k_chol<4 * RR>, sm);             \
-    launch_pdl(k_chol<4 * RR>, dim3(n), dim3(256), sm, st, d_items, status); \
+    set_smem_attr((const void*)k_chol<4 * RR, true>, sm);       \
+    launch_pdl(k_chol<4 * RR, true>, dim3(n), dim3(256), sm, st, d_items, status); \
     break;
   switch (R) {
     HS_CH(1) HS_CH(2) HS_CH(3) HS_CH(4) HS_CH(5) HS_CH(6) HS_CH(7)
