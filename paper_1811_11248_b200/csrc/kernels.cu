@@ -925,6 +925,10 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
 // owner loads and the owner dedupe (warp ballots instead of a serial scan) overlap; the
 // target addresses are resolved and the 16 old values per thread are in flight while the
 // DMMA product runs; the subtract-and-store follows.
+// RED: the subtraction as a fire-and-forget FP64 reduction in L2 (red.global.add.f64; one
+// update per target element per launch, so the result is the same as load-subtract-store)
+// — no old values held across the product, no spills, one more CTA per SM.
+template <bool RED>
 __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
   pdl_trigger();
@@ -1041,22 +1045,11 @@ __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict_
       if (p) tp[tc][e] = (int32_t)((p - dir.blk) + (int64_t)li * ld + lj);
     }
   double old[8][2];
-  if (dir.total < 0)   // debug: HS_SCHUR_CHECK (total passed negated)
+  if (!RED)
 #pragma unroll
     for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (tp[tc][e] >= 0 && tp[tc][e] >= -dir.total) {
-          const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
-          printf("schur3 OOB: tile %d src %d i0 %d j0 %d i %d j %d own %d %d loc %d %d slots %d %d nr %d nc %d table %d kn %d K %d off %lld\n",
-                 blockIdx.x, t.src, t.i0, t.j0, i, j, r_own[i], c_own[j], r_loc[i], c_loc[j], r_slot[i], c_slot[j], nr, nc,
-                 (int)table, s.kn, s.K, (long long)tp[tc][e]);
-          tp[tc][e] = -1;
-        }
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] >= 0 ? dir.blk[tp[tc][e]] : 0.0;
+      for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] >= 0 ? dir.blk[tp[tc][e]] : 0.0;
   // (5) ... while the 64 x 64 tile of C^T C forms on the FP64 tensor cores (DMMA m8n8k4):
   // warp w owns output rows 8w..8w+7; lane l holds rows 8w + l/4, columns 8 tc + 2 (l % 4) + {0, 1}
   double acc[8][2];
@@ -1084,7 +1077,10 @@ __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict_
   for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
     for (int e = 0; e < 2; ++e)
-      if (tp[tc][e] >= 0) dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
+      if (tp[tc][e] >= 0) {
+        if (RED) atomicAdd(dir.blk + tp[tc][e], -acc[tc][e]);
+        else dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
+      }
 }
 
 __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,
@@ -1400,10 +1396,10 @@ void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, cons
   if (n <= 0) return;
   if (schur_needs_prep(dir)) k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
   else {
-    static const bool chk = std::getenv("HS_SCHUR_CHECK") != nullptr;
-    BlockDir d2 = dir;
-    if (chk) d2.total = -dir.total;
-    launch_pdl(k_schur3, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
+    const BlockDir d2 = dir;
+    static const bool red = std::getenv("HS_SCHUR_NO_RED") == nullptr;
+    if (red) launch_pdl(k_schur3<true>, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
+    else launch_pdl(k_schur3<false>, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
   }
   count_launch(1);
 }
