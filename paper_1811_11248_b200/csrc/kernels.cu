@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ t
 // update per target element per launch, so the result is the same as load-subtract-store)
 // — no old values held across the product, no spills, one more CTA per SM.
 template <bool RED>
-__global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
+__global__ void __launch_bounds__(256, RED ? 4 : 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
   pdl_trigger();
   pdl_wait();
@@ -1019,31 +1019,33 @@ __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict_
     for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
   }
   __syncthreads();
-  // (4) target addresses and the old values in flight ...
-  int32_t tp[8][2];   // element offsets into the store (< 2^31 doubles: host-checked), -1 = none
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      tp[tc][e] = -1;
-      const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
-      if (i >= rows || j >= cols) continue;
-      const int oa = r_own[i], ob = c_own[j];
-      if (oa < ob) continue;                               // upper: the transposed block
-      const int li = r_loc[i], lj = c_loc[j];
-      if (oa == ob && li < lj) continue;                   // diagonal block: lower triangle only
-      double* p;
-      int ld;
-      if (table) {
-        p = ptab[r_slot[i]][c_slot[j]];
-        ld = ldtab[c_slot[j]];
-      } else {
-        const int fa = nb[oa].idx, fb = nb[ob].idx;
-        p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
-        ld = dir.cap[nb[ob].q];
-      }
-      if (p) tp[tc][e] = (int32_t)((p - dir.blk) + (int64_t)li * ld + lj);
+  // (4) target addresses (element offsets into the store, < 2^31 doubles: host-checked; -1 = none)
+  auto target = [&](int tc, int e) -> int32_t {
+    const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
+    if (i >= rows || j >= cols) return -1;
+    const int oa = r_own[i], ob = c_own[j];
+    if (oa < ob) return -1;                               // upper: the transposed block
+    const int li = r_loc[i], lj = c_loc[j];
+    if (oa == ob && li < lj) return -1;                   // diagonal block: lower triangle only
+    double* p;
+    int ld;
+    if (table) {
+      p = ptab[r_slot[i]][c_slot[j]];
+      ld = ldtab[c_slot[j]];
+    } else {
+      const int fa = nb[oa].idx, fb = nb[ob].idx;
+      p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
+      ld = dir.cap[nb[ob].q];
     }
+    return p ? (int32_t)((p - dir.blk) + (int64_t)li * ld + lj) : -1;
+  };
+  // ... and (load-subtract-store variant) the old values in flight during the product
+  int32_t tp[8][2];
+  if (!RED)
+#pragma unroll
+    for (int tc = 0; tc < 8; ++tc)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) tp[tc][e] = target(tc, e);
   double old[8][2];
   if (!RED)
 #pragma unroll
@@ -1076,11 +1078,14 @@ __global__ void __launch_bounds__(256, 3) k_schur3(const SchurTile2* __restrict_
 #pragma unroll
   for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
-      if (tp[tc][e] >= 0) {
-        if (RED) atomicAdd(dir.blk + tp[tc][e], -acc[tc][e]);
-        else dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
+    for (int e = 0; e < 2; ++e) {
+      if (RED) {   // addresses resolved after the product: nothing but acc live across it
+        const int32_t o = target(tc, e);
+        if (o >= 0) atomicAdd(dir.blk + o, -acc[tc][e]);
+      } else if (tp[tc][e] >= 0) {
+        dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
       }
+    }
 }
 
 __global__ void k_symcheck(const double* __restrict__ v, const int64_t* __restrict__ tmap, int64_t nnz,
