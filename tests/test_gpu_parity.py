@@ -288,3 +288,35 @@ def test_repeated_factor_pipeline_is_deterministic(H, handle):
         else:
             assert np.array_equal(x, ref)
         del f
+
+
+@pytest.mark.gpu
+def test_pipeline_modes_agree(H, handle, monkeypatch):
+    """The batch pipeline's modes compute the same factor: the device patch with the ranks
+    read one batch late vs the synchronous host patch, and the direct write-back (CPQR /
+    n-rotation write row s and C_s themselves) vs the write-back pass — bit for bit, since
+    they only move the same values; the gather + POTRF + TRSM kernels vs the gather-free
+    Cholesky + column-tile scaling to rounding."""
+    p = gen_laplace3d(24, leaf_size=27)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=27)
+    v = np.random.default_rng(11).standard_normal(p.n)
+
+    def run(**env):
+        for k in ("HS_HOST_PATCH", "HS_NO_DIRECT_WB", "HS_NO_FUSED_POTRF_TRSM"):
+            monkeypatch.delenv(k, raising=False)
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+        x = H.hs_apply(f, v)
+        r = [H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(H.hs_analysis_get_info(a)["L_top"])]
+        del f
+        return x, r
+
+    x0, r0 = run()
+    for env in ({"HS_HOST_PATCH": "1"}, {"HS_NO_DIRECT_WB": "1"}):
+        x1, r1 = run(**env)
+        assert all(np.array_equal(u, w) for u, w in zip(r0, r1)), env
+        assert np.array_equal(x1, x0), env
+    x2, r2 = run(HS_NO_FUSED_POTRF_TRSM="1")
+    assert all(np.array_equal(u, w) for u, w in zip(r0, r2))
+    assert np.linalg.norm(x2 - x0) <= 1e-11 * np.linalg.norm(x0)
