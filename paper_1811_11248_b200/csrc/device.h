@@ -236,7 +236,7 @@ struct ApplyLevelArgs {
   int32_t* arr;              // forward: contributions arrived per target (nclus)
   int32_t* ticket;           // [0] forward, [1] backward
   int32_t nftask, nbtask;
-  int32_t flags, pad;        // experiment switches (HS_APPLY_FLAGS)
+  int32_t spare0, spare1;
   long long* trace;          // HS_APPLY_TRACE: 8 globaltimer stamps per task (profiling only)
 };
 

@@ -154,8 +154,6 @@ ApplyLevelArgs level_args(hs_factor_s* f, int l) {
   a.ticket = a.cnt + 4 * n;
   a.nftask = (int32_t)P.ftask.size();
   a.nbtask = (int32_t)P.btask.size();
-  static const int flags = std::getenv("HS_APPLY_FLAGS") ? std::atoi(std::getenv("HS_APPLY_FLAGS")) : 0;
-  a.flags = flags;
   a.trace = l == g_trace_level ? g_trace : nullptr;
   return a;
 }

@@ -98,11 +98,6 @@ __device__ __forceinline__ void produce(const ApplyLevelArgs& a, const ApplySrc&
       }
       asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.contrib + c.slot + i), "d"(acc) : "memory");
     }
-    if (a.flags & 4) {   // counter mode (previous protocol, A/B switch)
-      __threadfence();
-      __syncwarp();
-      if (lane == 0 && c.pre) atomicAdd(a.arr + c.q, 1);
-    }
   }
 }
 
@@ -173,8 +168,6 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
       const bool staged = npre <= PRE_SMEM;
       if (staged)
         for (int e = tid; e < npre; e += APPLY_THREADS) pslot[e] = a.pull[S.pre_begin + e].slot;
-      const bool poll = !(a.flags & 4);
-      if (!poll && tid == 0) wait_ge(a.arr + s, npre);
       __syncthreads();
       AP_TR(t, 1);
       // y_s minus its pre-contributions in elimination order: rounds of up to PRE_BUF values
@@ -182,7 +175,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
       const int per = PRE_BUF / max(m, 1);   // m <= MAX_M < PRE_BUF
       // entry i's values of a round are summed by np threads (interleaved subsets, each in
       // order), then combined in subset order: a fixed order for a given m (deterministic)
-      const int np = (a.flags & 1) ? 1 : max(1, min(APPLY_THREADS / max(m, 1), (int)(PSUM / max(m, 1))));
+      const int np = max(1, min(APPLY_THREADS / max(m, 1), (int)(PSUM / max(m, 1))));
       {
         for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
         for (int e0 = 0; e0 < npre; e0 += per) {
@@ -190,7 +183,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
           for (int x = tid; x < ne * m; x += APPLY_THREADS) {
             const int e = e0 + x / m, i = x % m;
             const double* src = a.contrib + (staged ? pslot[e] : a.pull[S.pre_begin + e].slot) + i;
-            pbuf[x] = poll ? ld_poll(src) : __ldcg(src);
+            pbuf[x] = ld_poll(src);
           }
           __syncthreads();
           if (np > 1) {
@@ -229,14 +222,13 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd(ApplyLevelArgs a) {
       // the first group (the targets eliminated soonest: the next hop of the chain) before
       // the outputs that only the other groups and the parent level read
       AP_TR(t, 3);
-      if (!(a.flags & 2)) produce(a, S, K, z + r, tk.t_begin, tk.t_end, stg, soff, nst);
+      produce(a, S, K, z + r, tk.t_begin, tk.t_end, stg, soff, nst);
       AP_TR(t, 4);
       for (int i = tid; i < r; i += APPLY_THREADS) S.yc[i] = z[i];
       for (int k = tid; k < K; k += APPLY_THREADS) S.yf[k] = z[r + k];
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicExch(a.cnt + s, 1);
-      if (a.flags & 2) produce(a, S, K, z + r, tk.t_begin, tk.t_end, stg, soff, nst);
       AP_TR(t, 5);
     } else {          // ---- P(s, group)
       prefetch_group(a, S, K, tk.t_begin, tk.t_end);
