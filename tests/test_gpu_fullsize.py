@@ -102,3 +102,22 @@ def test_full_size_config(H, handle, name):
     assert rep["converged"]
     res = np.linalg.norm(p.b - A @ xs) / np.linalg.norm(p.b)
     assert res <= 10 * p.tol and abs(res - rep["relres_true"]) <= 1e-3 * max(res, 1e-300) + 1e-15
+
+
+def test_c2_refactor_is_bitwise_deterministic(H, handle):
+    """At the bench's size, in the bench's launch configuration: two factors of C2 on the
+    same analysis give bit-identical kept ranks and preconditioner applications (every sum
+    in the pipeline has a fixed order: batched kernels, L2 reductions with one update per
+    target element per launch, the apply's polled contributions summed in plan order)."""
+    p = gen_config("C2")
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+    L = H.hs_analysis_get_info(a)["L_top"]
+    v = np.random.default_rng(5).standard_normal(p.n)
+    out = []
+    for _ in range(2):
+        f = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
+        out.append(([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)], H.hs_apply(f, v)))
+        del f
+    assert all(np.array_equal(x, y) for x, y in zip(out[0][0], out[1][0]))
+    assert np.array_equal(out[0][1], out[1][1])
