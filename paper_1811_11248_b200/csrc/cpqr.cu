@@ -161,6 +161,7 @@ struct CqShared {
   unsigned long long bar1[2], bar2, bar3[2];   // step messages / fallback vector / fallback candidates
   CqFb mine3[2], slot3[2][16];
   double wred[CQ_WARPS];
+  int wcand[CQ_WARPS];                          // per-warp lowest local candidate (INT_MAX: none)
   __align__(16) double vstage[MAX_M + 8];      // fallback: owner's (tau, beta, v) staging
   __align__(16) double vbuf[MAX_M + 8];        // fallback: received (tau, beta, v)
 };
@@ -289,17 +290,25 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     if (tid == 0 && !direct) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
     __syncthreads();
     if (j < 60) CQ_TR(3 + 4 * j);
-    if (wid == 0) {
+    {   // every warp: the CTA max, and the lowest column of a strided share over the window
       double Mc = lane < CQ_WARPS ? sh.wred[lane] : -1.0;
       Mc = wmax(Mc);
       const double thr_c = CQ_WINDOW * Mc;
-      int li = INT_MAX;
+      int lw = INT_MAX;
       if (Mc >= 0.0)
-        for (int c = lane; c < nw; c += 32)
+        for (int c = wid * 32 + lane; c < nw; c += CQ_THREADS)
           if (nu[c] >= thr_c) {
-            li = c;
+            lw = c;
             break;
           }
+      lw = wmin_i(lw);
+      if (lane == 0) sh.wcand[wid] = lw;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double Mc = lane < CQ_WARPS ? sh.wred[lane] : -1.0;
+      Mc = wmax(Mc);
+      int li = lane < CQ_WARPS ? sh.wcand[lane] : INT_MAX;   // the lowest over all shares
       li = wmin_i(li);
       if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
         const double* col = W + (size_t)li * sc;
