@@ -46,15 +46,20 @@ def _both(H, handle, p, eps, kw=None, dc=1):
         # eps = 0 keeps every nonzero: decisions on rounding noise are not comparable,
         # and both sides are exact Cholesky factorizations (checked by the caller)
         return an, None, a, f, 0
-    fac, flagged = oracle_with_injection(H, f, an, p, eps, dc=dc)
+    fac, flagged, injected, nelim = oracle_with_injection(H, f, an, p, eps, dc=dc)
+    # decision injection is an exemption for fragile clusters, not a way to pass: report it
+    # and bound it ("make the exemption visible")
+    print(f"[parity] eliminations {nelim} flagged {flagged} injected {injected}")
+    assert injected <= max(2, nelim // 200), f"{injected} of {nelim} clusters needed decision injection"
     assert np.array_equal(H.hs_factor_export(f, H.HS_FEXP_TOP), fac.top_sizes)
-    return an, fac, a, f, flagged
+    return an, fac, a, f, injected
 
 
 def oracle_with_injection(H, f, an, p, eps, max_rounds=200, dc=1):
     """Rank/pivot parity with the margin exemption: walk the clusters in elimination
     order; at the first disagreement, a flagged cluster gets the GPU's decisions
-    injected into the oracle (which is re-run), an unflagged one fails the test."""
+    injected into the oracle (which is re-run), an unflagged one fails the test.
+    Returns (oracle factor, flagged clusters, injected clusters, eliminations)."""
     gpu = []
     for l in range(len(an.levels)):
         gpu.append((H.hs_factor_export(f, H.HS_FEXP_RANKS, l), H.hs_factor_export(f, H.HS_FEXP_PIV_PTR, l),
@@ -63,12 +68,13 @@ def oracle_with_injection(H, f, an, p, eps, max_rounds=200, dc=1):
     for _ in range(max_rounds):
         fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps, inject=inject or None, dc=bool(dc))
         first = None
-        nflag = 0
+        nflag = nelim = 0
         for l, lv in enumerate(fac.elims):
             g_r, g_pp, g_pv = gpu[l]
             for eb in lv:
                 for e in eb:
                     nflag += int(e.flagged)
+                    nelim += 1
                     gpiv = g_pv[g_pp[e.s]:g_pp[e.s + 1]]
                     if (l, e.s) in inject or (g_r[e.s] == e.r and np.array_equal(gpiv, e.piv)):
                         continue
@@ -79,7 +85,7 @@ def oracle_with_injection(H, f, an, p, eps, max_rounds=200, dc=1):
             if first:
                 break
         if first is None:
-            return fac, nflag
+            return fac, nflag, len(inject), nelim
         l, e, gpiv = first
         assert e.flagged, (f"decision mismatch at level {l} cluster {e.s} (unflagged, mu={e.mu:.2e}, "
                            f"pi={e.pi:.2e}): gpu r={gpu[l][0][e.s]} piv={list(gpiv)} oracle r={e.r} "
