@@ -34,8 +34,9 @@ class Level:
     wlist: list        # w(s) = F-adj(s) \ n(s) at the moment s is eliminated, ascending
     batches: list      # list of lists of cluster ids (ascending inside a batch)
     nphase1: int       # number of phase-I (interior) batches
-    interior: np.ndarray   # bool per cluster
+    interior: np.ndarray   # bool per cluster: all of F_start-adj(s) in s's subdomain
     Ffinal: list       # fill graph after the level, sorted lists
+    Fstart: list = None    # block pattern at the level start (= H under coarse_fill=1)
 
 
 @dataclasses.dataclass
@@ -157,7 +158,7 @@ def gbisect(n, rowptr, colind, D):
 
 
 def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_columns=0,
-            top_log2=3, nsub_log2=3) -> Analysis:
+            top_log2=3, nsub_log2=3, coarse_fill=0) -> Analysis:
     rowptr = np.asarray(rowptr, dtype=np.int64)
     colind = np.asarray(colind, dtype=np.int64)
     if coords is None:
@@ -170,7 +171,7 @@ def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_column
         D = 0
         while -(-U // (1 << D)) > leaf_units:
             D += 1
-        return _schedule(n, rowptr, colind, gbisect(n, rowptr, colind, D), D, top_log2, nsub_log2)
+        return _schedule(n, rowptr, colind, gbisect(n, rowptr, colind, D), D, top_log2, nsub_log2, coarse_fill)
     ucoord, unit_of_dof = _units(n, coords, column_id)
     U = ucoord.shape[0]
     leaf_units = leaf_columns if column_id is not None else leaf_size
@@ -182,10 +183,24 @@ def analyze(n, rowptr, colind, coords, column_id=None, leaf_size=64, leaf_column
         D += 1
     uleaf = rcb(ucoord, D)
     dof_leaf = uleaf if unit_of_dof is None else uleaf[unit_of_dof]
-    return _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2)
+    return _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2, coarse_fill)
 
 
-def _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2) -> Analysis:
+def _merge(adj, nclus):
+    """Merge-quotient onto the parents (binary tree, reading Q9): P ~ Q iff some child of P
+    is adjacent to some child of Q, P != Q."""
+    out = [set() for _ in range(nclus // 2)]
+    for c in range(nclus):
+        P = c >> 1
+        for q in adj[c]:
+            if q >> 1 != P:
+                out[P].add(q >> 1)
+    return [sorted(h) for h in out]
+
+
+def _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2, coarse_fill=0) -> Analysis:
+    if coarse_fill not in (0, 1):
+        raise ValueError("coarse_fill must be 0 (structural coarse neighbours) or 1 (fill-closed)")
     # O2.4 permutation: leaves left to right, DOFs ascending inside a leaf
     perm = np.lexsort((np.arange(n), dof_leaf)).astype(np.int64)
     nleaf = 1 << D
@@ -204,14 +219,15 @@ def _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2) -> Analysis:
     for pq in pairs.tolist():
         H[pq // nleaf].append(pq % nleaf)
     H = [sorted(set(h)) for h in H]
+    F0 = H                  # block pattern of the level's input A_l (H_0 at level 0)
     levels = []
     for l in range(L_top):
         nclus = 1 << (D - l)
         d = D - l
         sub = [c >> (d - sd) for c in range(nclus)]
-        F = [set(h) for h in H]
+        F = [set(h) for h in F0]
         nlist = [list(h) for h in H]
-        interior = np.array([all(sub[q] == sub[s] for q in H[s]) for s in range(nclus)], dtype=bool)
+        interior = np.array([all(sub[q] == sub[s] for q in F0[s]) for s in range(nclus)], dtype=bool)
         wlist = [None] * nclus
         processed = np.zeros(nclus, dtype=bool)
         batches = []
@@ -239,21 +255,17 @@ def _schedule(n, rowptr, colind, dof_leaf, D, top_log2, nsub_log2) -> Analysis:
                 if phase == 1:
                     nphase1 += 1
         Ffinal = [sorted(f) for f in F]
-        levels.append(Level(nclus, H, nlist, wlist, batches, nphase1, interior, Ffinal))
-        # O2.9 H_{l+1}: parents adjacent iff some children are F_final-adjacent
-        Hn = [set() for _ in range(nclus // 2)]
-        for c in range(nclus):
-            P = c >> 1
-            for q in F[c]:
-                Q = q >> 1
-                if Q != P:
-                    Hn[P].add(Q)
-        H = [sorted(h) for h in Hn]
+        levels.append(Level(nclus, H, nlist, wlist, batches, nphase1, interior, Ffinal, [list(f) for f in F0]))
+        # the block pattern of A_c: parents adjacent iff some children are F_final-adjacent
+        F0 = _merge(Ffinal, nclus)
+        # H_{l+1}: R-coarse merges the structural neighbours; O2.9 takes the whole pattern
+        H = F0 if coarse_fill else _merge(H, nclus)
+    # the top's block pattern is the whole pattern of A_top under both readings
     return Analysis(n=n, D=D, L_top=L_top, nsub_log2=sd, perm=perm, leaf_off=leaf_off,
-                    levels=levels, H_top=H)
+                    levels=levels, H_top=F0)
 
 
-def analyze_problem(p, top_log2=3, nsub_log2=3) -> Analysis:
+def analyze_problem(p, top_log2=3, nsub_log2=3, coarse_fill=0) -> Analysis:
     return analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id,
                    leaf_size=p.leaf_size, leaf_columns=p.leaf_columns,
-                   top_log2=top_log2, nsub_log2=nsub_log2)
+                   top_log2=top_log2, nsub_log2=nsub_log2, coarse_fill=coarse_fill)

@@ -141,7 +141,7 @@ def factor_dist(an: Analysis, rowptr, colind, vals, comm, rank: int, world: int,
         # end of level: every rank needs every kept rank (ghost parents' sizes)
         _sync_live(st, own, lev.nclus, comm)
         nP = lev.nclus // 2
-        Hn = an.levels[l + 1].H if l + 1 < len(an.levels) else an.H_top
+        Hn = an.levels[l + 1].Fstart if l + 1 < len(an.levels) else an.H_top   # block pattern of A_c
         lv_next = [st.live[2 * P] + st.live[2 * P + 1] for P in range(nP)]
         if l + 1 < len(an.levels):
             own_n = np.array([owner(an, l + 1, c, world) == rank for c in range(nP)], dtype=bool)

@@ -229,13 +229,13 @@ def eliminate_nodc(st: BlockStore, l: int, s: int, nlist, wlist, eps, relative, 
     return e
 
 
-def next_level(st: BlockStore, H_next, nclus_next) -> BlockStore:
+def next_level(st: BlockStore, pattern_next, nclus_next) -> BlockStore:
     """Extract A_c: parent P = [coarse(2P); coarse(2P+1)], blocks are the
     2x2 assemblies of the child blocks (missing child blocks are zero)."""
     live = [st.live[2 * P] + st.live[2 * P + 1] for P in range(nclus_next)]
     nst = BlockStore(live)
     for P in range(nclus_next):
-        for Q in [x for x in H_next[P] if x < P] + [P]:
+        for Q in [x for x in pattern_next[P] if x < P] + [P]:
             M = np.zeros((live[P], live[Q]))
             ro = [0, st.live[2 * P]]
             co = [0, st.live[2 * Q]]
@@ -282,7 +282,7 @@ def factor(an: Analysis, rowptr, colind, vals, eps=1e-2, relative=True, inject=N
         live1.append(list(st.live))
         if max_levels is not None and l + 1 >= max_levels:
             return Factor(an, eps, relative, elims, live0, live1, None, None)
-        Hn = an.levels[l + 1].H if l + 1 < len(an.levels) else an.H_top
+        Hn = an.levels[l + 1].Fstart if l + 1 < len(an.levels) else an.H_top   # block pattern of A_c
         st = next_level(st, Hn, lev.nclus // 2)
     ntop = 1 << (an.D - an.L_top)
     A_top, _ = assemble_top(st, ntop)

@@ -75,7 +75,8 @@ def _resimulate(an):
     independence, maximality, phase order and the recorded w(s)."""
     for l, lev in enumerate(an.levels):
         nclus = lev.nclus
-        F = [set(h) for h in lev.H]
+        F = [set(h) for h in lev.Fstart]
+        assert all(set(h) <= set(f) for h, f in zip(lev.H, lev.Fstart))
         done = np.zeros(nclus, dtype=bool)
         for bi, B in enumerate(lev.batches):
             phase1 = bi < lev.nphase1
@@ -101,20 +102,77 @@ def _resimulate(an):
                 done[s] = True
         assert done.all()
         assert [sorted(f) for f in F] == lev.Ffinal
-        # subdomain locality of phase-I fill
+        # subdomain locality of phase-I fill: an interior cluster's
+        # whole starting pattern (its n and its inherited w) lies in its subdomain
         for s in range(nclus):
             if lev.interior[s]:
-                assert all(an.subdomain(l, q) == an.subdomain(l, s) for q in lev.H[s])
+                assert all(an.subdomain(l, q) == an.subdomain(l, s) for q in lev.Fstart[s])
+        # the next level starts from the block pattern of A_c: the merge of F_final
+        nxt = an.levels[l + 1].Fstart if l + 1 < len(an.levels) else an.H_top
+        merged = [set() for _ in range(nclus // 2)]
+        for c in range(nclus):
+            for q in F[c]:
+                if q >> 1 != c >> 1:
+                    merged[c >> 1].add(q >> 1)
+        assert [sorted(m) for m in merged] == [list(x) for x in nxt]
 
 
 @pytest.mark.parametrize("gen", [lambda: gen_poisson2d(32), lambda: gen_laplace3d(16, leaf_size=16),
                                  lambda: gen_slab(32, 4, leaf_columns=4),
                                  lambda: gen_stokes_q1(12, 12, 3, leaf_columns=2)])
-def test_batches_independent_maximal(gen):
+@pytest.mark.parametrize("coarse_fill", [0, 1])
+def test_batches_independent_maximal(gen, coarse_fill):
     p = gen()
-    an = analyze_problem(p)
+    an = analyze_problem(p, coarse_fill=coarse_fill)
     assert len(an.levels) >= 1
     _resimulate(an)
+    for l, lev in enumerate(an.levels):
+        if coarse_fill:   # O2.9: the neighbours are the whole starting pattern
+            assert [list(h) for h in lev.H] == [list(f) for f in lev.Fstart]
+
+
+def _box_graph(p, an, l, dims):
+    """Closed form of the structural coarse neighbours on a grid with a face-coupling
+    stencil (5-point / 7-point): the level-l clusters are axis-aligned boxes of grid cells
+    (RCB on grid coordinates), and two boxes are neighbours iff they share a face, i.e. their
+    intervals touch (hi + 1 == lo) on one axis and overlap on all others."""
+    nclus = an.levels[l].nclus
+    lo = np.zeros((nclus, dims)); hi = np.zeros((nclus, dims))
+    span = 1 << l
+    for c in range(nclus):
+        d = an.perm[an.leaf_off[c * span]:an.leaf_off[(c + 1) * span]]
+        cc = p.coords[d][:, :dims]
+        lo[c], hi[c] = cc.min(0), cc.max(0)
+    G = [[] for _ in range(nclus)]
+    for s in range(nclus):
+        for q in range(nclus):
+            if q == s:
+                continue
+            touch = overlap = 0
+            for a in range(dims):
+                if hi[s, a] + 1 == lo[q, a] or hi[q, a] + 1 == lo[s, a]:
+                    touch += 1
+                elif lo[s, a] <= hi[q, a] and lo[q, a] <= hi[s, a]:
+                    overlap += 1
+            if touch == 1 and overlap == dims - 1:
+                G[s].append(q)
+    return G
+
+
+@pytest.mark.parametrize("gen,dims", [(lambda: gen_poisson2d(32), 2), (lambda: gen_laplace3d(16, leaf_size=8), 3)])
+def test_rcoarse_neighbours_are_face_adjacent_boxes(gen, dims):
+    """Pin of reading R-coarse: at every level n(s) = the clusters whose box
+    shares a face with s's box (closed form from the coordinates, not from the merge), so the
+    neighbour count stays <= 2*dims at every level (Thm 1 condition 1), while the
+    starting pattern keeps the inherited fill as w."""
+    p = gen()
+    an = analyze_problem(p)
+    for l, lev in enumerate(an.levels):
+        assert [list(h) for h in lev.H] == _box_graph(p, an, l, dims), l
+        assert max(len(h) for h in lev.H) <= 2 * dims
+    # O2.9 instead grows the neighbour sets with the level (fill becomes n)
+    an1 = analyze_problem(p, coarse_fill=1)
+    assert max(len(h) for h in an1.levels[-1].H) > 2 * dims
 
 
 def test_depth_rule_and_empty_children():
