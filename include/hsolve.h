@@ -74,6 +74,16 @@ typedef struct {
   int32_t leaf_columns;  /* columns per leaf when column_id != NULL (C3: 8, C4: 2, C5: 4)      */
   int32_t top_log2;      /* base case at the first level with <= 2^top_log2 clusters (3 -> 8) */
   int32_t nsub_log2;     /* fixed subdomain depth (3 -> 8 subdomains); must be <= top_log2    */
+  int32_t coarse_fill;   /* neighbours n(s) at the coarse levels l >= 1:
+                            0 (default): reading R-coarse -- the merged structural
+                              neighbours (H_{l+1} = merge-quotient of H_l), so that "the number of
+                              neighbor clusters is bounded by a constant" (Thm 1) and the
+                              per-level cost falls proportionally; blocks created by fill
+                              stay well-separated (w) and are compressed again at every level;
+                            1: SURVEY O2.9 literally (P:494 applied to A_c): every nonzero block of
+                              A_c is a neighbour -- the neighbour sets double per level on 2-D/3-D
+                              grids and the coarse levels become a dense block Cholesky.
+                            Both readings start each level from the whole block pattern of A_c. */
 } hs_analyze_opts;
 
 typedef struct {
@@ -102,12 +112,14 @@ enum {
   HS_EXP_W_IDX = 5,
   HS_EXP_BATCH_PTR = 6,  /* level l: batches (independent sets), in elimination order   */
   HS_EXP_BATCH_IDX = 7,
-  HS_EXP_INTERIOR = 8,   /* level l: 1 if all neighbours share the cluster's subdomain  */
+  HS_EXP_INTERIOR = 8,   /* level l: 1 if the cluster's whole starting pattern shares its subdomain */
   HS_EXP_F_PTR = 9,      /* level l: fill graph after the level                          */
   HS_EXP_F_IDX = 10,
   HS_EXP_NPHASE1 = 11,   /* level l: [1] number of phase-I (interior) batches            */
   HS_EXP_HTOP_PTR = 12,  /* block pattern of the top level                               */
-  HS_EXP_HTOP_IDX = 13
+  HS_EXP_HTOP_IDX = 13,
+  HS_EXP_FS_PTR = 14,    /* level l: block pattern at the level start (merge of F_final(l-1)) */
+  HS_EXP_FS_IDX = 15
 };
 
 /* keys for hs_dist_plan_export (multi-GPU decomposition plan) */

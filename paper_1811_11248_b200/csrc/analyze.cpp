@@ -232,17 +232,35 @@ Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const
     std::sort(h.begin(), h.end());
     h.erase(std::unique(h.begin(), h.end()), h.end());
   }
-  // ---- per-level schedule (O2.8, O2.9) -------------------------------------------------
+  // ---- per-level schedule (O2.8, O2.9 / reading R-coarse) --------------------------------
+  // F0 = the block pattern of the level's input A_l (H_0 at level 0, then the merge of the
+  // previous level's final fill graph).  H = n(s): under R-coarse (coarse_fill = 0) the
+  // merged structural neighbours, under O2.9 (coarse_fill = 1) the whole pattern F0.
+  if (opt.coarse_fill != 0 && opt.coarse_fill != 1) fail(HS_E_INVALID_ARG, "analyze: coarse_fill must be 0 or 1");
+  auto merge = [](const Adj& A, int32_t nclus) {
+    Adj M(nclus / 2);
+    for (int32_t c = 0; c < nclus; ++c) {
+      const int32_t P = c >> 1;
+      for (int32_t q : A[c])
+        if ((q >> 1) != P) M[P].push_back(q >> 1);
+    }
+    for (auto& h : M) {
+      std::sort(h.begin(), h.end());
+      h.erase(std::unique(h.begin(), h.end()), h.end());
+    }
+    return M;
+  };
+  Adj F0 = H;
   std::vector<int32_t> tmp;
   for (int l = 0; l < an->L_top; ++l) {
     Level lev;
     const int32_t nclus = (int32_t)(int64_t(1) << (D - l));
     lev.nclus = nclus;
     lev.H = H;
-    Adj F = H;
+    Adj F = F0;
     lev.interior.assign(nclus, 1);
     for (int32_t s = 0; s < nclus; ++s)
-      for (int32_t q : H[s])
+      for (int32_t q : F0[s])
         if (an->subdomain(l, q) != an->subdomain(l, s)) { lev.interior[s] = 0; break; }
     lev.w.assign(nclus, {});
     std::vector<uint8_t> done(nclus, 0), inB(nclus, 0);
@@ -269,22 +287,16 @@ Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const
         if (phase == 1) lev.nphase1++;
       }
     }
-    // H_{l+1}: parents adjacent iff some children are F_final-adjacent
-    Adj Hn(nclus / 2);
-    for (int32_t c = 0; c < nclus; ++c) {
-      const int32_t P = c >> 1;
-      for (int32_t q : F[c])
-        if ((q >> 1) != P) Hn[P].push_back(q >> 1);
-    }
-    for (auto& h : Hn) {
-      std::sort(h.begin(), h.end());
-      h.erase(std::unique(h.begin(), h.end()), h.end());
-    }
+    // A_c's block pattern: parents adjacent iff some children are F_final-adjacent
+    Adj Fn = merge(F, nclus);
+    Adj Hn = opt.coarse_fill ? Fn : merge(H, nclus);
+    lev.Fstart = std::move(F0);
     lev.Ffinal = std::move(F);
     an->levels.push_back(std::move(lev));
-    H.swap(Hn);
+    F0 = std::move(Fn);
+    H = std::move(Hn);
   }
-  an->H_top = std::move(H);
+  an->H_top = std::move(F0);   // the top's whole block pattern (under both readings)
   return an;
 }
 

@@ -248,6 +248,8 @@ hs_status hs_analysis_export(hs_analysis a, int32_t key, int32_t level, int64_t*
       case HS_EXP_NPHASE1: export_vec(std::vector<int64_t>{lev().nphase1}, out, cap, len); break;
       case HS_EXP_HTOP_PTR: export_adj(an.H_top, true, out, cap, len); break;
       case HS_EXP_HTOP_IDX: export_adj(an.H_top, false, out, cap, len); break;
+      case HS_EXP_FS_PTR: export_adj(lev().Fstart, true, out, cap, len); break;
+      case HS_EXP_FS_IDX: export_adj(lev().Fstart, false, out, cap, len); break;
       default: hs::fail(HS_E_INVALID_ARG, "hs_analysis_export: bad key");
     }
   });

@@ -28,7 +28,8 @@ struct Level {
   Adj w;                       // w(s) at elimination time
   std::vector<std::vector<int32_t>> batches;
   int32_t nphase1 = 0;
-  std::vector<uint8_t> interior;
+  std::vector<uint8_t> interior;   // all of Fstart-adj(s) in s's subdomain
+  Adj Fstart;                  // block pattern of the level's input A_l (= H under coarse_fill = 1)
   Adj Ffinal;                  // fill graph after the level
 };
 

@@ -25,7 +25,7 @@ for _i, _s in enumerate(STATUS):
 # hs_analysis_export keys
 (HS_EXP_PERM, HS_EXP_LEAF_OFF, HS_EXP_H_PTR, HS_EXP_H_IDX, HS_EXP_W_PTR, HS_EXP_W_IDX, HS_EXP_BATCH_PTR,
  HS_EXP_BATCH_IDX, HS_EXP_INTERIOR, HS_EXP_F_PTR, HS_EXP_F_IDX, HS_EXP_NPHASE1, HS_EXP_HTOP_PTR,
- HS_EXP_HTOP_IDX) = range(14)
+ HS_EXP_HTOP_IDX, HS_EXP_FS_PTR, HS_EXP_FS_IDX) = range(16)
 # hs_dist_plan_export keys
 HS_DEXP_OWNER, HS_DEXP_RECV_PTR, HS_DEXP_RECV, HS_DEXP_HELD_PTR, HS_DEXP_HELD = range(5)
 # hs_factor_export keys
@@ -48,7 +48,7 @@ class HSError(RuntimeError):
 
 class hs_analyze_opts(C.Structure):
     _fields_ = [("leaf_size", C.c_int32), ("leaf_columns", C.c_int32), ("top_log2", C.c_int32),
-                ("nsub_log2", C.c_int32)]
+                ("nsub_log2", C.c_int32), ("coarse_fill", C.c_int32)]
 
 
 class hs_factor_opts(C.Structure):
@@ -232,7 +232,7 @@ def hs_set_stream(h: Handle, stream_ptr: int | None):
 
 
 def hs_analyze(h: Handle | None, n, rowptr, colind, coords=None, column_id=None, leaf_size=64, leaf_columns=0,
-               top_log2=3, nsub_log2=3) -> Analysis:
+               top_log2=3, nsub_log2=3, coarse_fill=0) -> Analysis:
     rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
     colind = np.ascontiguousarray(colind, dtype=np.int32)
     cd = 0
@@ -241,7 +241,7 @@ def hs_analyze(h: Handle | None, n, rowptr, colind, coords=None, column_id=None,
         cd = coords.shape[1]
     if column_id is not None:
         column_id = np.ascontiguousarray(column_id, dtype=np.int32)
-    opt = hs_analyze_opts(leaf_size, leaf_columns, top_log2, nsub_log2)
+    opt = hs_analyze_opts(leaf_size, leaf_columns, top_log2, nsub_log2, coarse_fill)
     a = C.c_void_p()
     hp = h.ptr if h is not None else None
     _check(lib().hs_analyze(hp, int(n), rowptr.ctypes.data, colind.ctypes.data,

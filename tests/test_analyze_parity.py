@@ -70,15 +70,16 @@ CASES += [
 ]
 
 
+@pytest.mark.parametrize("coarse_fill", [0, 1])
 @pytest.mark.parametrize("name,gen,kw", CASES, ids=[c[0] for c in CASES])
-def test_analyze_bit_exact(name, gen, kw):
+def test_analyze_bit_exact(name, gen, kw, coarse_fill):
     p = gen()
     top_log2 = kw.get("top_log2", 3)
     nsub_log2 = kw.get("nsub_log2", 3)
     orc = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
-                  leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
+                  leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2, coarse_fill=coarse_fill)
     a = H.hs_analyze(None, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
-                     leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2)
+                     leaf_columns=p.leaf_columns, top_log2=top_log2, nsub_log2=nsub_log2, coarse_fill=coarse_fill)
     info = H.hs_analysis_get_info(a)
     assert (info["depth"], info["L_top"]) == (orc.D, orc.L_top)
     assert np.array_equal(H.hs_analysis_export(a, H.HS_EXP_PERM), orc.perm)
@@ -86,7 +87,8 @@ def test_analyze_bit_exact(name, gen, kw):
     for l, lev in enumerate(orc.levels):
         for kp, ki, adj in [(H.HS_EXP_H_PTR, H.HS_EXP_H_IDX, lev.H), (H.HS_EXP_W_PTR, H.HS_EXP_W_IDX, lev.wlist),
                             (H.HS_EXP_BATCH_PTR, H.HS_EXP_BATCH_IDX, lev.batches),
-                            (H.HS_EXP_F_PTR, H.HS_EXP_F_IDX, lev.Ffinal)]:
+                            (H.HS_EXP_F_PTR, H.HS_EXP_F_IDX, lev.Ffinal),
+                            (H.HS_EXP_FS_PTR, H.HS_EXP_FS_IDX, lev.Fstart)]:
             ptr, idx = _csr(adj)
             assert np.array_equal(H.hs_analysis_export(a, kp, l), ptr), (l, kp)
             assert np.array_equal(H.hs_analysis_export(a, ki, l), idx), (l, ki)
