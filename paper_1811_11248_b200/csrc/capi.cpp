@@ -135,6 +135,7 @@ static hs_status create_impl(hs_handle* out, int device, int world_size, int ran
     HS_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     h->upA.dev.dc = &h->cache;
     h->upB.dev.dc = &h->cache;
+    h->upC.dev.dc = &h->cache;
     h->world = world_size;
     h->rank = rank;
     if (world_size > 1 && loopback) {
@@ -182,7 +183,7 @@ void hs_destroy(hs_handle h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   // release the staging buffers while their stream is still alive (stream-ordered frees)
-  for (hs::Upload* u : {&h->upA, &h->upB}) {
+  for (hs::Upload* u : {&h->upA, &h->upB, &h->upC}) {
     if (u->dev.d) h->cache.free(u->dev.d);
     u->dev.d = nullptr;
     u->dev.cap = 0;

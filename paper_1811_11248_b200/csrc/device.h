@@ -127,7 +127,6 @@ struct SchurContrib {
 struct SchurSrc {
   const double* C;           // fine rows of the n-part, ld ldC
   int32_t ldC, K, kn, nb_off, nnb, pad;
-  int32_t* own;              // [kn] neighbour index owning each n-column (k_schur_prep)
   double** pairs;            // [nnb (nnb+1) / 2] target block of neighbour pair (a >= b), or null
 };
 // Device-side patch of a batch's pre-planned second half with the kept ranks r_s read from
@@ -289,11 +288,9 @@ int rot_tile_cols(int m, int max_m);   // columns per rotation tile (max_m: of t
 void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, const int32_t* d_rank,
                      cudaStream_t st);
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st);
-bool schur_needs_prep(const BlockDir& dir);
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st);
 // per-source column owners (nb index per n-column), once per batch before the waves
-void launch_schur_prep(const SchurSrc* d_src, int nsrc, int max_kn, const NbCol* d_nb, cudaStream_t st);
 // per level: target block of every neighbour pair (a >= b) of every cluster's n(s) list
 // (hptr/hq: n(s) as CSR; poff: offsets of each cluster's triangular table in pairs)
 void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* poff, int nclus, int64_t nrows,

@@ -10,6 +10,7 @@
 // apply, whose plan (descriptors) is built alongside and replayed as a CUDA graph.
 #include <algorithm>
 #include <atomic>
+#include <cuda.h>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -60,6 +61,7 @@ void DevCache::free(void* p) {
   live.erase(it);
 }
 void DevCache::trim() {
+  if (vmm) vmm->trim();
   if (!cached) return;
   cudaDeviceSynchronize();
   for (auto& b : bins)
@@ -67,6 +69,102 @@ void DevCache::trim() {
   bins.clear();
   cached = 0;
 }
+
+// ---- CUDA VMM through the driver entry points (no link-time dependency on libcuda) -------
+namespace {
+struct DriverVmm {
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  DriverVmm() {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        *fn = nullptr;
+    };
+    get("cuMemCreate", (void**)&create);
+    get("cuMemRelease", (void**)&release);
+    get("cuMemAddressReserve", (void**)&reserve);
+    get("cuMemAddressFree", (void**)&addr_free);
+    get("cuMemMap", (void**)&map);
+    get("cuMemUnmap", (void**)&unmap);
+    get("cuMemSetAccess", (void**)&set_access);
+    get("cuMemGetAllocationGranularity", (void**)&granularity);
+  }
+  void need() const {
+    if (!create || !release || !reserve || !addr_free || !map || !unmap || !set_access || !granularity)
+      fail(HS_E_CUDA, "CUDA virtual memory management entry points unavailable");
+  }
+};
+const DriverVmm& drv() {
+  static DriverVmm d;
+  d.need();
+  return d;
+}
+void cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return;
+  fail(r == CUDA_ERROR_OUT_OF_MEMORY ? HS_E_OOM : HS_E_CUDA, std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+}
+CUmemAllocationProp chunk_prop(int device) {
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  return prop;
+}
+}  // namespace
+
+void VmmPool::init(int dev) {
+  if (device == dev && chunk) return;
+  device = dev;
+  const CUmemAllocationProp prop = chunk_prop(dev);
+  size_t g = 0;
+  cu_check(drv().granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+  const size_t want = (size_t)256 << 20;   // 256 MB chunks
+  chunk = (want + g - 1) / g * g;
+}
+unsigned long long VmmPool::take() {
+  if (!idle.empty()) {
+    const unsigned long long h = idle.back();
+    idle.pop_back();
+    return h;
+  }
+  const CUmemAllocationProp prop = chunk_prop(device);
+  CUmemGenericAllocationHandle h = 0;
+  CUresult r = drv().create(&h, chunk, &prop, 0);
+  if (r == CUDA_ERROR_OUT_OF_MEMORY && dc) {   // give cached blocks back to the driver and retry once
+    dc->trim();
+    r = drv().create(&h, chunk, &prop, 0);
+  }
+  cu_check(r, "cuMemCreate (block store chunk)");
+  ++created;
+  return (unsigned long long)h;
+}
+void VmmPool::trim() {
+  for (unsigned long long h : idle) drv().release((CUmemGenericAllocationHandle)h);
+  created -= idle.size();
+  idle.clear();
+}
+unsigned long long vmm_reserve(size_t bytes) {
+  CUdeviceptr p = 0;
+  cu_check(drv().reserve(&p, bytes, 0, 0, 0), "cuMemAddressReserve");
+  return (unsigned long long)p;
+}
+void vmm_free_range(unsigned long long base, size_t bytes) { drv().addr_free((CUdeviceptr)base, bytes); }
+void vmm_map(unsigned long long va, unsigned long long handle, size_t bytes, int device) {
+  cu_check(drv().map((CUdeviceptr)va, bytes, 0, (CUmemGenericAllocationHandle)handle, 0), "cuMemMap");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  cu_check(drv().set_access((CUdeviceptr)va, bytes, &acc, 1), "cuMemSetAccess");
+}
+void vmm_unmap(unsigned long long va, size_t bytes) { cu_check(drv().unmap((CUdeviceptr)va, bytes), "cuMemUnmap"); }
 
 void DevScratch::ensure(size_t bytes) {
   if (bytes <= cap) return;
@@ -95,17 +193,84 @@ struct BlockStore {
   double* d = nullptr;
   std::vector<int32_t> cap;
   std::vector<std::vector<std::pair<int32_t, int64_t>>> rows;   // p -> sorted (q <= p, offset)
+  std::vector<int64_t> rowbeg;   // [n + 1] first offset of row p's blocks (rows are contiguous, ascending)
   size_t total = 0;
   cudaStream_t st = nullptr;
   DevCache* dc = nullptr;
+  // VMM backing: one virtual range of nchunk chunks; handle[i] != 0 while chunk i is mapped
+  VmmPool* pool = nullptr;
+  size_t vbytes = 0;
+  std::vector<unsigned long long> handle;
 
   // dp/level (multi-GPU): keep only the blocks this rank holds (it owns p or q)
-  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache,
+  BlockStore() = default;
+  BlockStore(const BlockStore&) = delete;
+  BlockStore& operator=(const BlockStore&) = delete;
+  BlockStore& operator=(BlockStore&&) = default;   // the moved-from store must be forget()-ed
+  ~BlockStore() {   // error paths: wait for the store's users, then give the chunks back
+    if (!d && !d_ptr) return;
+    if (st) cudaStreamSynchronize(st);
+    try {
+      release();
+    } catch (...) {
+    }
+  }
+  void build(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache, VmmPool* vp,
              const DistPlan* dp = nullptr, int level = 0) {
+    reserve(caps, edges, stream, cache, vp, dp, level);
+    map_bytes(0, total * sizeof(double));
+  }
+  // layout + virtual range, nothing mapped yet
+  void reserve(const std::vector<int32_t>& caps, const Adj& edges, cudaStream_t stream, DevCache* cache, VmmPool* vp,
+               const DistPlan* dp = nullptr, int level = 0) {
     st = stream;
     dc = cache;
+    pool = vp;
     layout(caps, edges, dp, level);
-    if (total) d = (double*)dc->alloc(total * sizeof(double));
+    if (!total) return;
+    // map/unmap cost milliseconds per chunk: stores that fit comfortably twice come from the
+    // caching allocator, only the large ones (C4-sized) are VMM-backed
+    static const size_t vmm_min = [] {
+      const char* e = std::getenv("HS_VMM_MIN_GB");
+      return (size_t)(e ? std::atof(e) * 1e9 : 24e9);
+    }();
+    if (total * sizeof(double) < vmm_min) {
+      pool = nullptr;
+      d = (double*)dc->alloc(total * sizeof(double));
+      return;
+    }
+    const size_t cb = pool->chunk;
+    vbytes = (total * sizeof(double) + cb - 1) / cb * cb;
+    d = (double*)(uintptr_t)vmm_reserve(vbytes);
+    handle.assign(vbytes / cb, 0ull);
+  }
+  // map (and zero) every chunk overlapping the byte range [b0, b1) that is not mapped yet
+  void map_bytes(size_t b0, size_t b1) {
+    if (!total || b1 <= b0) return;
+    if (!pool) {   // cache-backed: zero exactly the range
+      b1 = std::min(b1, total * sizeof(double));
+      if (b1 > b0) HS_CUDA(cudaMemsetAsync((char*)d + b0, 0, b1 - b0, st));
+      return;
+    }
+    const size_t cb = pool->chunk;
+    size_t i0 = b0 / cb, i1 = (std::min(b1, vbytes) + cb - 1) / cb;
+    for (size_t i = i0; i < i1; ++i) {
+      if (handle[i]) continue;
+      handle[i] = pool->take();
+      vmm_map((unsigned long long)(uintptr_t)d + i * cb, handle[i], cb, pool->device);
+      HS_CUDA(cudaMemsetAsync((char*)d + i * cb, 0, cb, st));
+    }
+  }
+  // unmap every chunk lying entirely below byte b (its users must have completed)
+  void unmap_below(size_t b) {
+    if (!total || !pool) return;
+    const size_t cb = pool->chunk;
+    for (size_t i = 0; i < handle.size() && (i + 1) * cb <= b; ++i)
+      if (handle[i]) {
+        vmm_unmap((unsigned long long)(uintptr_t)d + i * cb, cb);
+        pool->give(handle[i]);
+        handle[i] = 0;
+      }
   }
   std::vector<std::vector<std::pair<int32_t, int64_t>>> cols;   // q -> sorted (p > q, offset)
   void layout(const std::vector<int32_t>& caps, const Adj& edges, const DistPlan* dp = nullptr, int level = 0) {
@@ -114,7 +279,9 @@ struct BlockStore {
     rows.assign(n, {});
     cols.assign(n, {});
     int64_t off = 0;
+    rowbeg.assign(n + 1, 0);
     for (int p = 0; p < n; ++p) {
+      rowbeg[p] = off;
       for (int32_t q : edges[p])
         if (q < p && (!dp || dp->holds(level, p, q))) {
           rows[p].push_back({q, off});
@@ -126,6 +293,7 @@ struct BlockStore {
         off += (int64_t)caps[p] * caps[p];
       }
     }
+    rowbeg[n] = off;
     total = (size_t)off;
   }
   int64_t off(int32_t p, int32_t q) const {   // p >= q
@@ -200,12 +368,21 @@ struct BlockStore {
     HS_CUDA(cudaStreamSynchronize(st));   // host vectors go out of scope
   }
   BlockDir dir() const { return BlockDir{d, (int64_t)total, d_ptr, d_q, d_off, d_cap}; }
+  // the store's users must have completed (the callers synchronise the stream first)
   void release() {
-    for (void* p : {(void*)d, (void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
+    if (d && pool) {
+      unmap_below(vbytes);
+      vmm_free_range((unsigned long long)(uintptr_t)d, vbytes);
+    } else if (d) {
+      dc->free(d);
+    }
+    for (void* p : {(void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
       if (p) dc->free(p);
     forget();
   }
   void forget() {
+    handle.clear();
+    vbytes = 0;
     d = nullptr;
     d_ptr = nullptr;
     d_q = nullptr;
@@ -493,6 +670,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->d_colind = an->d_colind;
   f->d_perm = an->d_perm;
   DevCache& dc = h->cache;
+  h->vmm.init(h->device);   // physical chunks of the block stores
+  h->vmm.dc = &dc;
+  dc.vmm = &h->vmm;
   f->d_vals = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(nnz, 1));
   HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz,
                           opt.values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -514,9 +694,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   std::vector<int32_t> cap(nleaf0);
   for (int c = 0; c < nleaf0; ++c) cap[c] = (int32_t)(an->leaf_off[c + 1] - an->leaf_off[c]);
   BlockStore bs;
-  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc,
-           h->world > 1 && an->L_top > 0 ? &DP : nullptr, 0);
-  if (bs.total) HS_CUDA(cudaMemsetAsync(bs.d, 0, bs.total * sizeof(double), st));
+  bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc, &h->vmm,
+           h->world > 1 && an->L_top > 0 ? &DP : nullptr, 0);   // mapped and zeroed
   launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
   if (an->L_top > 0) bs.upload_dir();
 
@@ -524,6 +703,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   Upload& upB = h->upB;
   upA.dev.dc = &dc;
   upB.dev.dc = &dc;
+  h->upC.dev.dc = &dc;
   int32_t* d_rank = nullptr;
   int32_t* h_rank = nullptr;
   int max_batch = 1;
@@ -678,6 +858,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     // the batch whose ranks are still on their way to the host (dpatch): (s, m) of its clusters
     std::vector<std::pair<int32_t, int32_t>> pend_cl;
     bool pend_active = false;
+    // dpatch: C_s is written into a per-batch region sized for m rows (the rank is not known
+    // when the batch is planned) and compacted to its K = m - r rows in the persistent slab
+    // once the host reads the ranks (the Schur waves that read it are queued before the copy)
+    double* ctmp = nullptr;          // the planned batch's region
+    double* pend_ctmp = nullptr;     // the pending batch's region
     auto finish_pending = [&]() {
       if (!pend_active) return;
       pend_active = false;
@@ -704,7 +889,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         done[s] = 1;
         if (m == 0) continue;
         const int32_t K = m - r, kn = L.kn[s], kw = L.kw[s];
-        if (K == 0) L.C[s] = nullptr;   // the slab piece (sized for m rows) stays unused
         S.max_m = std::max(S.max_m, m);
         S.max_rank = std::max(S.max_rank, r);
         double fq = 0.0;
@@ -712,6 +896,32 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.flops += fq + (double)K * kn * (kn + 1);
         S.flops_phase[3] += fq;
         S.flops_phase[4] += (double)K * kn * (kn + 1);
+      }
+      if (pend_ctmp) {   // compact the batch's C_s: K x kn each into the persistent slab
+        std::vector<CopyItem> cc;
+        for (size_t bi = 0; bi < pend_cl.size(); ++bi) {
+          const int32_t s = pend_cl[bi].first, m = pend_cl[bi].second;
+          if (!L.C[s]) continue;
+          const int32_t K = m - L.rank[s], kn = L.kn[s];
+          if (K <= 0 || kn <= 0) {
+            L.C[s] = nullptr;
+            continue;
+          }
+          double* dst = cslab.get((int64_t)K * kn);
+          cc.push_back(CopyItem{L.C[s], dst, kn, kn, K, kn, 0, 0});
+          L.C[s] = dst;
+        }
+        split_copies(cc);
+        Upload& upC = h->upC;
+        upC.reset();
+        const size_t iC = upC.add(cc);
+        upC.stage.ensure(upC.total);
+        upC.dev.ensure(upC.total);
+        upC.copy_in(iC, cc);
+        upC.send(st);
+        launch_copy2d(upC.dptr<CopyItem>(iC), (int)cc.size(), st);
+        dc.free(pend_ctmp);   // stream-ordered reuse: later users are queued after the copy
+        pend_ctmp = nullptr;
       }
     };
 
@@ -763,6 +973,18 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         wsz += 2 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
       }
       double* ws = nb ? (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4)) : nullptr;
+      // the batch's C_s region (dpatch: m rows each, compacted once the ranks are known)
+      int64_t csz = 0;
+      std::vector<int64_t> co(nb, -1);
+      if (dpatch)
+        for (int bi = 0; bi < nb; ++bi) {
+          const int64_t m = live[Bo[bi]], kn = L.kn[Bo[bi]];
+          if (m > 0 && kn > 0) {
+            co[bi] = csz;
+            csz += (m * kn + 3) & ~int64_t(3);
+          }
+        }
+      ctmp = csz ? (double*)dc.alloc(sizeof(double) * csz) : nullptr;
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
@@ -814,7 +1036,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             it.dwb = 1;
             it.keepB = f->keep_records ? 1 : 0;
             if (kn > 0) {
-              L.C[s] = cslab.get((int64_t)m * kn);   // C_s = rows [r, m) of the rotated B_n (K <= m)
+              L.C[s] = ctmp + co[bi];   // C_s = rows [r, m) of the rotated B_n (K <= m)
               it.Cout = L.C[s];
             }
           }
@@ -1118,8 +1340,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             q.kind = PK_FT;
             prefs.push_back({q, 3, (size_t)pd.ft});
           }
-          if (kn > 0 && !dwb) {   // C_s = B_s[r:, kw:] into a slab piece sized for K <= m rows
-            L.C[s] = cslab.get((int64_t)m * kn);
+          if (kn > 0 && !dwb) {   // C_s = B_s[r:, kw:] into the batch region (K <= m rows)
+            L.C[s] = ctmp + co[pd.k];
             const int32_t step = std::max(1, 16384 / kn);
             for (int32_t i0 = 0; i0 < m; i0 += step) {
               PatchItem q = base;
@@ -1134,6 +1356,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         pend_cl.clear();
         for (size_t k = 0; k < Bt.size(); ++k) pend_cl.emplace_back(Bt[k], live_at[k]);
         pend_active = nb > 0;
+        pend_ctmp = ctmp;
+        ctmp = nullptr;
       }
       for (auto& pd : pend) {
         if (dpatch) break;
@@ -1178,23 +1402,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       t_sub[1] += now_s() - tp1;
       const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
-      // scratch of k_schur_prep (column owners); the pair tables are the level's
-      int64_t prep_words = 0;
-      int max_kn_src = 0;
-      for (const auto& sc : srcs) {
-        prep_words += ((int64_t)sc.kn + 1) / 2;
-        max_kn_src = std::max(max_kn_src, sc.kn);
-      }
-      const bool need_prep = schur_needs_prep(bs.dir());   // k_schur3 finds the owners itself
-      char* prep = (prep_words && need_prep) ? (char*)dc.alloc(8 * prep_words) : nullptr;
-      {
-        char* cur = prep;
-        for (size_t k = 0; k < srcs.size(); ++k) {
-          srcs[k].own = (int32_t*)cur;
-          if (cur) cur += 8 * (((int64_t)srcs[k].kn + 1) / 2);
-          srcs[k].pairs = lp.pairs + lp.poff[src_cl[k]];
-        }
-      }
+      for (size_t k = 0; k < srcs.size(); ++k) srcs[k].pairs = lp.pairs + lp.poff[src_cl[k]];   // the level's pair tables
       std::vector<SchurTile2> tiles;
       std::vector<int32_t> wave_off(1, 0);
       for (const auto& wv : waves) {
@@ -1248,8 +1456,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st, nb, d_status, pub_dev, ++pub_seq);
         else
           launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
-        if (need_prep)
-          launch_schur_prep(upB.dptr<SchurSrc>(jS), (int)srcs.size(), max_kn_src, upB.dptr<NbCol>(jN), st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
                         upB.dptr<SchurSrc>(jS), upB.dptr<NbCol>(jN), bs.dir(), st);
@@ -1291,7 +1497,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         first_half_launch(true);
         first_half_launch = nullptr;
       }
-      if (prep) dc.free(prep);   // consumed by this batch's Schur waves (same stream)
       for (double* b : rbuf)
         if (b) dc.free(b);
       if (ws) {
@@ -1562,48 +1767,58 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
     }
     // ---- end of level: A_c = parents of [coarse(2P); coarse(2P+1)] -----------------
+    // The parent store is mapped group by group of parent rows while the consumed child rows'
+    // chunks are unmapped: the two stores never coexist in full.
     const Adj& En = (l + 1 < an->L_top) ? an->levels[l + 1].Ffinal : an->H_top;
     BlockStore nbs;
-    nbs.build(capn, En, st, &dc, dist ? &DP : nullptr, l + 1);
-    if (nbs.total) HS_CUDA(cudaMemsetAsync(nbs.d, 0, nbs.total * sizeof(double), st));
+    nbs.reserve(capn, En, st, &dc, &h->vmm, dist ? &DP : nullptr, l + 1);
     t_tr[0] += now_s() - tp2;
     // every stored child block (c >= d) lands in parent block (c/2, d/2) at offset
     // (c odd ? r(2P) : 0, d odd ? r(2Q) : 0); the upper child pair of a parent diagonal
     // block never occurs (c >= d), matching its lower-triangle semantics.  A rank holds
     // every child block of the parent blocks it holds (same owners).
-    std::vector<CopyItem> asmb;
-    for (int32_t c = 0; c < lev.nclus; ++c) {
-      if (L.rank[c] == 0) continue;
-      const int32_t P = c >> 1;
-      const auto& prow = nbs.rows[P];
-      size_t pi = 0;
-      for (const auto& dof : bs.rows[c]) {
-        const int32_t d = dof.first;
-        if (L.rank[d] == 0) continue;
-        const int32_t Q = d >> 1;
-        while (pi < prow.size() && prow[pi].first < Q) ++pi;   // d ascending -> Q ascending
-        if (pi == prow.size() || prow[pi].first != Q) {
-          if (dist) continue;   // a parent block this rank does not hold
-          fail(HS_E_INTERNAL, "assembly: parent block missing");
+    const int64_t group_words = std::max<int64_t>((int64_t)(2ull << 30) / 8, (int64_t)nbs.total / 16);
+    pt.rec(pt.a[0], st);
+    for (int32_t Pa = 0; Pa < nP;) {
+      int32_t Pb = Pa + 1;
+      while (Pb < nP && nbs.rowbeg[Pb + 1] - nbs.rowbeg[Pa] <= group_words) ++Pb;
+      nbs.map_bytes((size_t)nbs.rowbeg[Pa] * sizeof(double), (size_t)nbs.rowbeg[Pb] * sizeof(double));
+      std::vector<CopyItem> asmb;
+      for (int32_t c = 2 * Pa; c < std::min(2 * Pb, lev.nclus); ++c) {
+        if (L.rank[c] == 0) continue;
+        const int32_t P = c >> 1;
+        const auto& prow = nbs.rows[P];
+        size_t pi = 0;
+        for (const auto& dof : bs.rows[c]) {
+          const int32_t d = dof.first;
+          if (L.rank[d] == 0) continue;
+          const int32_t Q = d >> 1;
+          while (pi < prow.size() && prow[pi].first < Q) ++pi;   // d ascending -> Q ascending
+          if (pi == prow.size() || prow[pi].first != Q) {
+            if (dist) continue;   // a parent block this rank does not hold
+            fail(HS_E_INTERNAL, "assembly: parent block missing");
+          }
+          const int32_t dld = capn[Q];
+          const int32_t ro = (c & 1) ? L.rank[2 * P] : 0, co = (d & 1) ? L.rank[2 * Q] : 0;
+          asmb.push_back(CopyItem{bs.d + dof.second, nbs.d + prow[pi].second + (int64_t)ro * dld + co, cap[d], dld,
+                                  L.rank[c], L.rank[d], 0, 0});
         }
-        const int32_t dld = capn[Q];
-        const int32_t ro = (c & 1) ? L.rank[2 * P] : 0, co = (d & 1) ? L.rank[2 * Q] : 0;
-        asmb.push_back(CopyItem{bs.d + dof.second, nbs.d + prow[pi].second + (int64_t)ro * dld + co, cap[d], dld,
-                                L.rank[c], L.rank[d], 0, 0});
       }
+      split_copies(asmb);
+      upA.reset();
+      const size_t iA = upA.add(asmb);
+      upA.stage.ensure(upA.total);
+      upA.dev.ensure(upA.total);
+      upA.copy_in(iA, asmb);
+      upA.send(st);
+      launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
+      HS_CUDA(cudaStreamSynchronize(st));   // the consumed child rows can go
+      bs.unmap_below((size_t)bs.rowbeg[std::min(2 * Pb, lev.nclus)] * sizeof(double));
+      Pa = Pb;
     }
-    split_copies(asmb);
-    upA.reset();
-    const size_t iA = upA.add(asmb);
-    upA.stage.ensure(upA.total);
-    upA.dev.ensure(upA.total);
-    upA.copy_in(iA, asmb);
+    pt.rec(pt.a[1], st);
     t_plan += now_s() - tp2;
     t_trans += now_s() - tp2;
-    upA.send(st);
-    pt.rec(pt.a[0], st);
-    launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
-    pt.rec(pt.a[1], st);
     HS_CUDA(cudaStreamSynchronize(st));
     pt.collect_b(S);
     if (pt.on) S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
@@ -1623,12 +1838,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       std::fprintf(stderr,
                    "[hs profile] level %d: %d clusters %zu batches wall %.1f ms plan %.1f ms | gather %.1f potrf %.1f "
-                   "trsm %.1f cpqr %.1f schur %.1f wb %.1f ms | sum m %lld r %lld kn %lld kw %lld max ldB %lld\n",
+                   "trsm %.1f cpqr %.1f schur %.1f wb %.1f ms | sum m %lld r %lld kn %lld kw %lld max ldB %lld | "
+                   "cache in use %.1f GB (peak %.1f), store chunks %.1f GB\n",
                    l, lev.nclus, lev.batches.size(), 1e3 * (now_s() - lv_t0), 1e3 * (t_plan - lv_plan0),
                    1e3 * (S.t_phase_s[0] - lv_ph0[0]), 1e3 * (S.t_phase_s[1] - lv_ph0[1]),
                    1e3 * (S.t_phase_s[2] - lv_ph0[2]), 1e3 * (S.t_phase_s[3] - lv_ph0[3]),
                    1e3 * (S.t_phase_s[4] - lv_ph0[4]), 1e3 * (S.t_phase_s[5] - lv_ph0[5]), (long long)sm,
-                   (long long)sr, (long long)skn, (long long)skw, (long long)mx);
+                   (long long)sr, (long long)skn, (long long)skw, (long long)mx, dc.in_use / 1e9, dc.peak / 1e9,
+                   h->vmm.created * (double)h->vmm.chunk / 1e9);
     }
   }
   // ---- top: dense Cholesky of all live DOFs, on rank 0 -------------------------

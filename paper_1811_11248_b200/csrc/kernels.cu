@@ -759,12 +759,10 @@ __global__ void __launch_bounds__(256) k_schur(const SchurTile* __restrict__ til
 }
 
 // ---------------------------------------------------------------------------------------
-// a5 v2: Schur update X_nn -= C^T C (Eq. CC:eqn:elim) for one source cluster per tile.
-// The 64 x 64 tile of C^T C is formed with FP64 FMA (K staged through smem 16 rows at a
-// time), then every element is subtracted in place from its target block, found on the
-// device: row/column owners by binary search in the source's neighbour-column table,
-// block pointers by binary search in the level's block directory (one lookup per distinct
-// owner pair of the tile).  HBM-bound: 16 bytes of read-modify-write per target element.
+// a5: Schur update X_nn -= C^T C (Eq. CC:eqn:elim) for one source cluster per 64 x 64 tile
+// of C^T C.  Target blocks are found on the device: row/column owners by binary search in
+// the source's neighbour-column table, block pointers from the level's neighbour-pair
+// tables (k_level_pairs, one directory search per pair per level).
 constexpr int SCH_MAXO = 32;   // distinct owners per tile side held in the pointer table
 constexpr int SCH_NBS = 512;   // neighbour column starts staged for the owner searches (k_schur3)
 
@@ -778,158 +776,12 @@ __device__ __forceinline__ int64_t dir_find(const BlockDir& d, int p, int q) {  
   return (lo < d.ptr[p + 1] && d.q[lo] == q) ? d.off[lo] : -1;
 }
 
-__device__ __forceinline__ int nb_owner(const NbCol* nb, int nnb, int c) {   // last a with nb[a].col <= c
-  int lo = 0, hi = nnb - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (nb[mid].col <= c) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-__global__ void __launch_bounds__(256) k_schur2(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
-                                                const NbCol* __restrict__ nbc, BlockDir dir) {
-  const SchurTile2 t = tiles[blockIdx.x];
-  const SchurSrc s = srcs[t.src];
-  if (s.K <= 0) return;   // planned before its rank was known and kept everything (uniform)
-  const NbCol* nb = nbc + s.nb_off;
-  __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
-  __shared__ double aq[16][68];
-  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
-  __shared__ int r_slot[64], c_slot[64];
-  __shared__ int r_list[SCH_MAXO], c_list[SCH_MAXO];
-  __shared__ int nr, nc;
-  __shared__ double* ptab[SCH_MAXO][SCH_MAXO];
-  __shared__ int ldtab[SCH_MAXO];
-  const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
-  const int tid = threadIdx.x;
-  if (tid < 64) {
-    if (tid < rows) {
-      const int a = s.own[t.i0 + tid];
-      r_own[tid] = a;
-      r_loc[tid] = t.i0 + tid - nb[a].col;
-    }
-  } else if (tid < 128) {
-    const int u = tid - 64;
-    if (u < cols) {
-      const int b = s.own[t.j0 + u];
-      c_own[u] = b;
-      c_loc[u] = t.j0 + u - nb[b].col;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {   // distinct owners (rows/cols are sorted by owner)
-    int k = -1;
-    for (int i = 0; i < rows; ++i) {
-      if (i == 0 || r_own[i] != r_own[i - 1]) {
-        ++k;
-        if (k < SCH_MAXO) r_list[k] = r_own[i];
-      }
-      r_slot[i] = k;
-    }
-    nr = k + 1;
-  } else if (tid == 32) {
-    int k = -1;
-    for (int j = 0; j < cols; ++j) {
-      if (j == 0 || c_own[j] != c_own[j - 1]) {
-        ++k;
-        if (k < SCH_MAXO) c_list[k] = c_own[j];
-      }
-      c_slot[j] = k;
-    }
-    nc = k + 1;
-  }
-  __syncthreads();
-  const bool table = nr <= SCH_MAXO && nc <= SCH_MAXO;
-  if (table) {
-    for (int e = tid; e < nr * nc; e += blockDim.x) {
-      const int ra = e / nc, cb = e % nc;
-      const int a = nb[r_list[ra]].idx, b = nb[c_list[cb]].idx;
-      ptab[ra][cb] = a >= b ? s.pairs[(int64_t)a * (a + 1) / 2 + b] : nullptr;
-    }
-    for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
-  }
-  __syncthreads();
-  // dense 64 x 64 tile of C^T C on the FP64 tensor cores (DMMA, mma.sync m8n8k4): warp w
-  // owns output rows 8w..8w+7 and the eight 8 x 8 column tiles; lane l holds rows
-  // 8w + l/4, columns 8 tc + 2 (l % 4) + {0, 1} (the m8n8k4 accumulator layout).
-  const int lane = tid & 31, w = tid >> 5;
-  double acc[8][2];
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc) acc[tc][0] = acc[tc][1] = 0.0;
-  const double* Cp = s.C + t.i0;
-  const double* Cq = s.C + t.j0;
-  for (int k0 = 0; k0 < s.K; k0 += 16) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + 256 * q;
-      const int kk = e >> 6, ii = e & 63;
-      const bool kin = k0 + kk < s.K;
-      ap[kk][ii] = (kin && ii < rows) ? Cp[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
-      aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; kk += 4) {
-      const double a = ap[kk + (lane & 3)][8 * w + (lane >> 2)];   // A = C_p^T, row-major 8 x 4
-#pragma unroll
-      for (int tc = 0; tc < 8; ++tc) {
-        const double b = aq[kk + (lane & 3)][8 * tc + (lane >> 2)];   // B = C_q, col-major 4 x 8
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                     : "+d"(acc[tc][0]), "+d"(acc[tc][1])
-                     : "d"(a), "d"(b));
-      }
-    }
-    __syncthreads();
-  }
-  // scatter-subtract into the target blocks: all 16 target addresses first, then all 16
-  // loads in flight, then the stores (no load waits behind a possibly aliasing store)
-  double* tp[8][2];
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      tp[tc][e] = nullptr;
-      const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
-      if (i >= rows || j >= cols) continue;
-      const int oa = r_own[i], ob = c_own[j];
-      if (oa < ob) continue;                               // upper: the transposed block
-      const int li = r_loc[i], lj = c_loc[j];
-      if (oa == ob && li < lj) continue;                   // diagonal block: lower triangle only
-      double* p;
-      int ld;
-      if (table) {
-        p = ptab[r_slot[i]][c_slot[j]];
-        ld = ldtab[c_slot[j]];
-      } else {
-        const int fa = nb[oa].idx, fb = nb[ob].idx;
-        p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
-        ld = dir.cap[nb[ob].q];
-      }
-      if (p) tp[tc][e] = p + (int64_t)li * ld + lj;
-    }
-  double old[8][2];
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] ? *tp[tc][e] : 0.0;
-#pragma unroll
-  for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      if (tp[tc][e]) *tp[tc][e] = old[tc][e] - acc[tc][e];
-}
-
-// a5 v3: the same update with a shorter dependency chain per tile.  The C tile loads, the
-// owner loads and the owner dedupe (warp ballots instead of a serial scan) overlap; the
-// target addresses are resolved and the 16 old values per thread are in flight while the
-// DMMA product runs; the subtract-and-store follows.
-// RED: the subtraction as a fire-and-forget FP64 reduction in L2 (red.global.add.f64; one
-// update per target element per launch, so the result is the same as load-subtract-store)
-// — no old values held across the product, no spills, one more CTA per SM.
-template <bool RED>
-__global__ void __launch_bounds__(256, RED ? 4 : 3) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
+// The C tile loads, the owner loads and the owner dedupe (warp ballots) overlap; the 64 x 64
+// tile forms on the FP64 tensor cores (DMMA m8n8k4); the target addresses are resolved after
+// the product and the subtraction is a fire-and-forget FP64 reduction in L2
+// (red.global.add.f64): one update per target element per launch (the waves of a batch
+// never share a target), so the result is the same as load-subtract-store.
+__global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict__ tiles, const SchurSrc* __restrict__ srcs,
                                                 const NbCol* __restrict__ nbc, BlockDir dir) {
   pdl_trigger();
   pdl_wait();
@@ -1019,14 +871,14 @@ __global__ void __launch_bounds__(256, RED ? 4 : 3) k_schur3(const SchurTile2* _
     for (int cb = tid; cb < nc; cb += blockDim.x) ldtab[cb] = dir.cap[nb[c_list[cb]].q];
   }
   __syncthreads();
-  // (4) target addresses (element offsets into the store, < 2^31 doubles: host-checked; -1 = none)
-  auto target = [&](int tc, int e) -> int32_t {
+  // (4) target addresses (nullptr = none)
+  auto target = [&](int tc, int e) -> double* {
     const int i = 8 * w + (lane >> 2), j = 8 * tc + 2 * (lane & 3) + e;
-    if (i >= rows || j >= cols) return -1;
+    if (i >= rows || j >= cols) return nullptr;
     const int oa = r_own[i], ob = c_own[j];
-    if (oa < ob) return -1;                               // upper: the transposed block
+    if (oa < ob) return nullptr;                          // upper: the transposed block
     const int li = r_loc[i], lj = c_loc[j];
-    if (oa == ob && li < lj) return -1;                   // diagonal block: lower triangle only
+    if (oa == ob && li < lj) return nullptr;              // diagonal block: lower triangle only
     double* p;
     int ld;
     if (table) {
@@ -1037,22 +889,9 @@ __global__ void __launch_bounds__(256, RED ? 4 : 3) k_schur3(const SchurTile2* _
       p = s.pairs[(int64_t)fa * (fa + 1) / 2 + fb];
       ld = dir.cap[nb[ob].q];
     }
-    return p ? (int32_t)((p - dir.blk) + (int64_t)li * ld + lj) : -1;
+    return p ? p + (int64_t)li * ld + lj : nullptr;
   };
-  // ... and (load-subtract-store variant) the old values in flight during the product
-  int32_t tp[8][2];
-  if (!RED)
-#pragma unroll
-    for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) tp[tc][e] = target(tc, e);
-  double old[8][2];
-  if (!RED)
-#pragma unroll
-    for (int tc = 0; tc < 8; ++tc)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) old[tc][e] = tp[tc][e] >= 0 ? dir.blk[tp[tc][e]] : 0.0;
-  // (5) ... while the 64 x 64 tile of C^T C forms on the FP64 tensor cores (DMMA m8n8k4):
+  // (5) the 64 x 64 tile of C^T C forms on the FP64 tensor cores (DMMA m8n8k4):
   // warp w owns output rows 8w..8w+7; lane l holds rows 8w + l/4, columns 8 tc + 2 (l % 4) + {0, 1}
   double acc[8][2];
 #pragma unroll
@@ -1078,13 +917,9 @@ __global__ void __launch_bounds__(256, RED ? 4 : 3) k_schur3(const SchurTile2* _
 #pragma unroll
   for (int tc = 0; tc < 8; ++tc)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      if (RED) {   // addresses resolved after the product: nothing but acc live across it
-        const int32_t o = target(tc, e);
-        if (o >= 0) atomicAdd(dir.blk + o, -acc[tc][e]);
-      } else if (tp[tc][e] >= 0) {
-        dir.blk[tp[tc][e]] = old[tc][e] - acc[tc][e];
-      }
+    for (int e = 0; e < 2; ++e) {   // addresses resolved after the product: nothing but acc live across it
+      double* o = target(tc, e);
+      if (o) atomicAdd(o, -acc[tc][e]);
     }
 }
 
@@ -1356,17 +1191,6 @@ int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, do
   }
 }
 
-// Column owners of the batch's sources: grid (source, 256-column chunk).
-__global__ void __launch_bounds__(256) k_schur_prep(const SchurSrc* __restrict__ srcs, const NbCol* __restrict__ nbc) {
-  const SchurSrc s = srcs[blockIdx.y];
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < s.kn) s.own[c] = nb_owner(nbc + s.nb_off, s.nnb, c);
-}
-void launch_schur_prep(const SchurSrc* d_src, int nsrc, int max_kn, const NbCol* d_nb, cudaStream_t st) {
-  if (nsrc <= 0 || max_kn <= 0) return;
-  k_schur_prep<<<dim3((max_kn + 255) / 256, nsrc), 256, 0, st>>>(d_src, d_nb);
-  count_launch(1);
-}
 // Level pair tables: a warp per (cluster s, neighbour a); lanes over b <= a look the block
 // (q_a, q_b) up in the level's directory.  Pattern-only, once per level.
 __global__ void __launch_bounds__(256) k_level_pairs(const int64_t* __restrict__ hptr, const int32_t* __restrict__ hq,
@@ -1390,22 +1214,10 @@ void launch_level_pairs(const int64_t* hptr, const int32_t* hq, const int64_t* p
   k_level_pairs<<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(hptr, hq, poff, row_cl, nrows, pairs, dir);
   count_launch(1);
 }
-// k_schur2 (previous order; also when the store exceeds 2^31 doubles) reads the column owners
-// k_schur_prep writes; k_schur3 searches them itself
-bool schur_needs_prep(const BlockDir& dir) {
-  static const bool v2 = std::getenv("HS_SCHUR_V2") != nullptr;   // A/B: the previous tile kernel
-  return v2 || dir.total >= (int64_t)1 << 31;
-}
 void launch_schur2(const SchurTile2* d_tiles, int n, const SchurSrc* d_src, const NbCol* d_nb, const BlockDir& dir,
                    cudaStream_t st) {
   if (n <= 0) return;
-  if (schur_needs_prep(dir)) k_schur2<<<n, 256, 0, st>>>(d_tiles, d_src, d_nb, dir);
-  else {
-    const BlockDir d2 = dir;
-    static const bool red = std::getenv("HS_SCHUR_NO_RED") == nullptr;
-    if (red) launch_pdl(k_schur3<true>, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
-    else launch_pdl(k_schur3<false>, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, d2);
-  }
+  launch_pdl(k_schur3, dim3(n), dim3(256), 0, st, d_tiles, d_src, d_nb, dir);
   count_launch(1);
 }
 

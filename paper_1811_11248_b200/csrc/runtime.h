@@ -18,6 +18,29 @@ struct hs_analysis_s {
 
 namespace hs {
 
+// Physical memory for the level block stores (CUDA virtual memory management).  A store
+// reserves one contiguous virtual range (its kernels address blocks by offset from the
+// base) and maps fixed-size physical chunks into it; the level transition maps the parent
+// store chunk by chunk while it unmaps the consumed child chunks, so the two stores never
+// coexist in full (C4: the level-0 store alone is ~90 GB).  Unmapped chunks are kept idle
+// for the next store / factor and go back to the driver on OOM and at hs_destroy.
+struct VmmPool {
+  int device = -1;
+  size_t chunk = 0;                      // bytes per physical chunk (granularity multiple)
+  std::vector<unsigned long long> idle;  // CUmemGenericAllocationHandle
+  size_t created = 0;                    // chunks alive (mapped or idle)
+  struct DevCache* dc = nullptr;         // trimmed before retrying an allocation that failed
+  void init(int dev);
+  unsigned long long take();
+  void give(unsigned long long h) { idle.push_back(h); }
+  void trim();                           // release the idle chunks
+  ~VmmPool() { trim(); }
+};
+unsigned long long vmm_reserve(size_t bytes);                          // virtual range
+void vmm_free_range(unsigned long long base, size_t bytes);
+void vmm_map(unsigned long long va, unsigned long long handle, size_t bytes, int device);
+void vmm_unmap(unsigned long long va, size_t bytes);
+
 // Per-handle caching device allocator.  Every factor / apply / PCG buffer comes from here and
 // goes back here: blocks are binned by size class (<= 25% rounding) and reused in host
 // order.  All users of a handle's memory run on the handle's stream (the side stream is
@@ -36,7 +59,8 @@ struct DevCache {
   }
   void* alloc(size_t bytes);
   void free(void* p);
-  void trim();        // return every cached block to the driver (synchronises the device)
+  void trim();        // return every cached block (and idle VMM chunk) to the driver (synchronises the device)
+  VmmPool* vmm = nullptr;
   ~DevCache() {       // the handle is going away: also blocks leaked by a failed call
     trim();
     for (auto& kv : live) cudaFree(kv.first);
@@ -183,8 +207,9 @@ struct hs_handle_s {
   int world = 1, rank = 0;
   hs::Comm* comm = nullptr;     // world > 1: NCCL or loopback transport
   std::string err;
+  hs::VmmPool vmm;              // physical chunks of the block stores (destroyed after the cache)
   hs::DevCache cache;           // declared before the staging buffers (destroyed after them)
-  hs::Upload upA, upB;          // descriptor staging, reused across factors
+  hs::Upload upA, upB, upC;     // descriptor staging, reused across factors
 };
 
 struct hs_factor_s {

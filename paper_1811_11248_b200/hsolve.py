@@ -160,6 +160,42 @@ def _ptr(a):
     return C.c_void_p(a.ctypes.data), 0
 
 
+def _is_cuda(a):
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+def _dev_ready(*tensors):
+    """Device inputs may still be being written by torch's current stream, which is not the
+    library's stream: wait for it before the C call reads them (the C calls synchronise their
+    own stream before returning, so device outputs are complete when they return)."""
+    import torch
+    for t in tensors:
+        if _is_cuda(t):
+            torch.cuda.current_stream(t.device).synchronize()
+            return
+
+
+def _check_dev_vec(t, n, name):
+    import torch
+    if t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != n:
+        raise HSError(HS_E_DIM, f"{name}: need a contiguous float64 CUDA tensor of {n} elements "
+                                f"(got {t.dtype}, {tuple(t.shape)}, contiguous={t.is_contiguous()})")
+
+
+def _host_vec(a, n, name, out=False):
+    """A float64 C-contiguous host vector of n entries: inputs are converted, a caller-given
+    output must already be one (the library writes n doubles into it)."""
+    if out:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.size == n
+                and a.flags.writeable):
+            raise HSError(HS_E_DIM, f"{name}: need a writable C-contiguous float64 array of {n} entries")
+        return a
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size != n:
+        raise HSError(HS_E_DIM, f"{name}: {a.size} entries, the factor has {n}")
+    return a
+
+
 class Handle:
     def __init__(self, ptr):
         self.ptr = ptr
@@ -274,10 +310,13 @@ def hs_analysis_export(a: Analysis, key: int, level: int = 0) -> np.ndarray:
 
 def hs_factor_create(h: Handle, a: Analysis, values, eps=1e-2, eps_relative=1, dc=1) -> Factor:
     """values: numpy (host) or a torch CUDA float64 tensor (device-resident CSR values)."""
-    if hasattr(values, "is_cuda") and values.is_cuda:
+    nnz = int(a._keep[0][-1])
+    if _is_cuda(values):
+        _check_dev_vec(values, nnz, "values")
+        _dev_ready(values)
         vp, on_dev = _ptr(values)
     else:
-        values = np.ascontiguousarray(values, dtype=np.float64)
+        values = _host_vec(values, nnz, "values")
         vp, on_dev = C.c_void_p(values.ctypes.data), 0
     opt = hs_factor_opts(eps, eps_relative, dc, on_dev, 0)
     f = C.c_void_p()
@@ -323,28 +362,39 @@ def cluster_record(f: Factor, level: int, cluster: int) -> dict:
             "B": hs_factor_export_cluster(f, HS_CEXP_B, level, cluster).reshape(m, ldB)}
 
 
+def _dev_io(f, b, x):
+    _check_dev_vec(b, f.n, "b")
+    x = b.new_empty(b.shape) if x is None else x
+    if not _is_cuda(x) or x.device != b.device:
+        raise HSError(HS_E_DIM, "x: need a CUDA tensor on b's device")
+    _check_dev_vec(x, f.n, "x")
+    _dev_ready(b)
+    return x
+
+
+def _host_io(f, b, x):
+    b = _host_vec(b, f.n, "b")
+    x = np.empty_like(b) if x is None else _host_vec(x, f.n, "x", out=True)
+    return b, x
+
+
 def hs_apply(f: Factor, b, x=None):
     """x = M^{-1} b.  numpy in -> numpy out; torch CUDA tensor in -> written into x (a tensor)."""
-    if hasattr(b, "is_cuda") and b.is_cuda:
-        if x is None:
-            x = b.new_empty(b.shape)
-        bp, _ = _ptr(b)
-        xp, _ = _ptr(x)
-        _check(lib().hs_apply(f.ptr, bp, xp, 1), f.handle.ptr)
+    if _is_cuda(b):
+        x = _dev_io(f, b, x)
+        _check(lib().hs_apply(f.ptr, _ptr(b)[0], _ptr(x)[0], 1), f.handle.ptr)
         return x
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x = np.empty_like(b) if x is None else x
+    b, x = _host_io(f, b, x)
     _check(lib().hs_apply(f.ptr, b.ctypes.data, x.ctypes.data, 0), f.handle.ptr)
     return x
 
 
 def hs_spmv(f: Factor, x):
-    if hasattr(x, "is_cuda") and x.is_cuda:
-        y = x.new_empty(x.shape)
+    if _is_cuda(x):
+        y = _dev_io(f, x, None)
         _check(lib().hs_spmv(f.ptr, _ptr(x)[0], _ptr(y)[0], 1), f.handle.ptr)
         return y
-    x = np.ascontiguousarray(x, dtype=np.float64)
-    y = np.empty_like(x)
+    x, y = _host_io(f, x, None)
     _check(lib().hs_spmv(f.ptr, x.ctypes.data, y.ctypes.data, 0), f.handle.ptr)
     return y
 
@@ -352,12 +402,11 @@ def hs_spmv(f: Factor, x):
 def hs_pcg(f: Factor, b, tol=1e-8, maxit=1000, x=None, raise_not_converged=True):
     """PCG with M = the factor.  Returns (x, report dict)."""
     rep = hs_pcg_report()
-    if hasattr(b, "is_cuda") and b.is_cuda:
-        x = b.new_empty(b.shape) if x is None else x
+    if _is_cuda(b):
+        x = _dev_io(f, b, x)
         st = lib().hs_pcg(f.ptr, _ptr(b)[0], _ptr(x)[0], tol, maxit, 1, C.byref(rep))
     else:
-        b = np.ascontiguousarray(b, dtype=np.float64)
-        x = np.empty_like(b) if x is None else x
+        b, x = _host_io(f, b, x)
         st = lib().hs_pcg(f.ptr, b.ctypes.data, x.ctypes.data, tol, maxit, 0, C.byref(rep))
     if st == HS_E_NOT_CONVERGED and not raise_not_converged:
         return x, rep.as_dict()
@@ -368,12 +417,11 @@ def hs_pcg(f: Factor, b, tol=1e-8, maxit=1000, x=None, raise_not_converged=True)
 def hs_gmres(f: Factor, b, tol=1e-12, restart=200, maxit=1000, x=None, raise_not_converged=True):
     """Right-preconditioned GMRES(restart) with M = the factor.  Returns (x, report)."""
     rep = hs_pcg_report()
-    if hasattr(b, "is_cuda") and b.is_cuda:
-        x = b.new_empty(b.shape) if x is None else x
+    if _is_cuda(b):
+        x = _dev_io(f, b, x)
         st = lib().hs_gmres(f.ptr, _ptr(b)[0], _ptr(x)[0], tol, restart, maxit, 1, C.byref(rep))
     else:
-        b = np.ascontiguousarray(b, dtype=np.float64)
-        x = np.empty_like(b) if x is None else x
+        b, x = _host_io(f, b, x)
         st = lib().hs_gmres(f.ptr, b.ctypes.data, x.ctypes.data, tol, restart, maxit, 0, C.byref(rep))
     if st == HS_E_NOT_CONVERGED and not raise_not_converged:
         return x, rep.as_dict()
