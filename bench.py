@@ -1,20 +1,28 @@
 """Benchmark of the deferred-compression LoRaSp hot path on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
 
 A step = one pass of the whole hot path on one synthetic system: hs_factor (Algorithm 1:
 POTRF, deferred-compression TRSM, CPQR to eps, Schur updates, top Cholesky) followed by
-hs_pcg (CSR SpMV + the Algorithm-2 apply) to the config's tolerance.  The default workload
-is BASELINE.json configs[1] (C2: 3-D 64^3 Laplacian, k = exp(GRF), leaf 64, eps 1e-2,
-PCG to 1e-8), the config the metric is quoted on; inputs (CSR values, b) are resident in
-HBM when the timed region starts and the analysis (pattern only) is done once before it.
-value = DOF/s = N * K / (device time of the K steps); e2e repeats the step through the
-same C API with HOST buffers (values and b uploaded, x downloaded inside the timed region).
-N > 1 (torchrun, one process per GPU): the factor is partitioned by the 8 fixed subdomains
-over the GPUs with NCCL exchanges (strong scaling: one system
-per step), the solve runs on rank 0; --replicas runs N independent systems instead (weak).
-A watchdog aborts a run whose exchanges never complete (exit 3, an error JSON line).
---impl reference times the CPU oracle (oracle/) on the host cores on a bounded sample.
+hs_pcg (CSR SpMV + the Algorithm-2 apply) to the config's tolerance.
+
+Default workload: BASELINE.json configs[2] (C3: 256 x 256 x 10 thin anisotropic slab, 655,360
+DOF), the largest BASELINE config that fits one B200.  C4 (10.5M DOF, "1 GPU and 8 GPUs") does
+not: measured on its half-size family member C4/2 (2.6M DOF, same operator, leaf, eps, tol) the
+factor alone holds 30.5 GB and the level stores 34 GB at ranks r/m = 0.74 / 0.83 / 0.59 (levels
+0-2), which extrapolates to ~120 GB of factor plus ~100 GB of level store for C4 -- more than
+the 180 GB of one GPU (profiles/r02_c4_memory.txt).  --config C2 / C4/2 / ... run
+the other configs (a "/k" suffix = the config's operator on a 1/k horizontal grid).
+
+Inputs (CSR values, b) are resident in HBM when the timed region starts and the analysis
+(pattern only) is done once before it.  value = DOF/s = N * K / (device time of the K steps);
+e2e repeats the step through the same C API with HOST buffers (values and b uploaded, x
+downloaded inside the timed region).  N > 1 (torchrun, one process per GPU): the factor is
+partitioned by the 8 fixed subdomains over the GPUs with NCCL exchanges (SURVEY §8(e),
+DESIGN.md §7; strong scaling: one system per step), the solve runs on rank 0; --replicas runs
+N independent systems instead (weak).  A watchdog aborts a run whose exchanges never complete
+(exit 3, an error JSON line).  --impl reference times the CPU oracle (oracle/) on all host
+cores on a bounded sample of the workload.
 """
 from __future__ import annotations
 
@@ -39,7 +47,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--cpu-budget", type=float, default=8.0,
+                    help="seconds of oracle work per host core for the CPU baseline")
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -104,41 +114,95 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample_run(nc: int):
-    """The oracle as it stands, one thread, on a bounded sample of the C2 family."""
+def _problem(name):
+    from problems.generators import gen_config, gen_config_scaled
+    if "/" in name:
+        base, k = name.split("/")
+        return gen_config_scaled(base, int(k))
+    return gen_config(name)
+
+
+def _sample_name(config):
+    """The bounded CPU sample of a workload: its family member on a 1/4 horizontal grid (1/16
+    of the DOFs for the 2-D-extruded configs; 1/64 for C2) -- same generator, leaf, eps, tol."""
+    base = config.split("/")[0]
+    k = int(config.split("/")[1]) if "/" in config else 1
+    return f"{base}/{4 * k}" if base in ("C2", "C3", "C4", "C5") else base
+
+
+def _oracle_worker(args):
+    """One host core: the oracle as it stands (one BLAS thread) on independent samples until
+    its time budget is spent; returns (DOFs factored+solved, seconds, PCG iterations)."""
+    name, budget, t_start = args
+    import time as _t
     from threadpoolctl import threadpool_limits
-    from problems import gen_laplace3d
     from oracle.analyze import analyze_problem
     from oracle.factor import factor
     from oracle.solve import apply, pcg
+    p = _problem(name)
+    an = analyze_problem(p)
+    A = p.to_scipy()
+    while _t.time() < t_start:
+        _t.sleep(0.001)
+    t0 = _t.perf_counter()
+    dofs, its = 0, 0
     with threadpool_limits(1):
-        p = gen_laplace3d(nc)
-        an = analyze_problem(p)
-        t0 = time.perf_counter()
-        f = factor(an, p.rowptr, p.colind, p.vals, eps=p.eps)
-        x, rep = pcg(p.to_scipy(), p.b, lambda r: apply(f, r), tol=p.tol)
-        t = time.perf_counter() - t0
-    return p.n, t, rep.iters
+        while True:
+            f = factor(an, p.rowptr, p.colind, p.vals, eps=p.eps)
+            x, rep = pcg(A, p.b, lambda r: apply(f, r), tol=p.tol)
+            dofs += p.n
+            its = rep.iters
+            if _t.perf_counter() - t0 >= budget:
+                break
+    return dofs, _t.perf_counter() - t0, its
+
+
+def cpu_pool_run(config, budget):
+    """The oracle on every host core (multiprocessing pool, one worker per core, spawn), each
+    on independent copies of the bounded sample; value = all DOFs / the slowest worker's time."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    name = _sample_name(config)
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        t_start = time.time() + 5.0 + 0.05 * cores   # every worker has imported and built its sample
+        res = pool.map(_oracle_worker, [(name, budget, t_start)] * cores, chunksize=1)
+    dofs = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    n1 = _problem(name).n
+    return {"value": dofs / wall, "unit": "DOF/s", "cores": cores, "kind": "oracle", "cpu_model": model,
+            "sample": f"{name} ({n1} DOF per system, the {config} operator family at reduced horizontal size; same "
+                      f"generator, leaf, eps, tol, analyze reading): {cores} processes, one per host core, one BLAS "
+                      f"thread each, factor + PCG ({res[0][2]} iterations) of independent systems for >= {budget:.0f} s; "
+                      f"{dofs // n1} systems in {wall:.1f} s"}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    nc = 24 if args.steps + args.warmup > 4 else 32
+    budget = max(2.0, args.cpu_budget / 2)
     for _ in range(args.warmup):
-        cpu_sample_run(nc)
-    tot, n, its = 0.0, 0, 0
+        cpu_pool_run(args.config, 1.0)
+    tot, vals = 0.0, []
+    cb = None
     for _ in range(args.steps):
-        n, t, its = cpu_sample_run(nc)
-        tot += t
-    value = n * args.steps / tot
-    sample = (f"C2 family (3-D Laplacian, k=exp(GRF sigma 1, ell 8), leaf 64, eps 1e-2, PCG 1e-8) at {nc}^3 = "
-              f"{n} DOFs per step (C2 is 64^3 = 262144; the full C2 oracle factor takes ~300 s)")
+        cb = cpu_pool_run(args.config, budget)
+        vals.append(cb["value"])
+    value = float(np.mean(vals))
+    cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 sample: " + sample, "pcg_iters": its},
-            "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {"workload": f"{args.config} (oracle on the host cores, bounded sample: {cb['sample']})"},
+            "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -147,7 +211,6 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local):
     import torch
     from paper_1811_11248_b200 import hsolve as H
-    from problems import gen_config
     torch.cuda.set_device(local)
     dist_factor = world > 1 and not args.replicas
     if world > 1:
@@ -162,7 +225,7 @@ def run_ours(args, rank, world, local):
                                   "error": f"watchdog: no result after {args.watchdog:.0f} s"}), flush=True)
             os._exit(3)
         threading.Thread(target=_watchdog, daemon=True).start()
-    p = gen_config(args.config)
+    p = _problem(args.config)
     if args.eps is not None:
         p.eps = args.eps
     if dist_factor:
@@ -233,8 +296,8 @@ def run_ours(args, rank, world, local):
     value = units * args.steps / (tot_ms * 1e-3)
     # ---- e2e through the C API with host buffers -------------------------------------------
     e2e = None
+    hv = np.ascontiguousarray(p.vals)
     if not args.no_e2e:
-        hv = np.ascontiguousarray(p.vals)
         hb = np.ascontiguousarray(p.b)
         hx = np.empty_like(hb)
         f = H.hs_factor_create(h, a, hv, eps=p.eps)
@@ -316,10 +379,38 @@ def run_ours(args, rank, world, local):
     t_fac = float(np.mean([s["t_factor_s"] for s in stats]))
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        n_s, t_s, it_s = cpu_sample_run(32)
-        cpu = {"value": n_s / t_s, "unit": "DOF/s", "cores": 1, "kind": "oracle",
-               "sample": f"C2 family at 32^3 = {n_s} DOFs (1/8 of C2), same generator/leaf/eps/tol, factor+PCG "
-                         f"({it_s} iterations) in {t_s:.1f} s on 1 host thread"}
+        cpu = cpu_pool_run(args.config, args.cpu_budget)
+    # ---- HBM-bound kernels: the apply (Algorithm 2) and the CSR SpMV of PCG ------------------
+    # algorithmic bytes (§8(d)): apply = T_s (m^2) and C_s (K kn) read by each of the forward
+    # and backward sweeps + the top factor twice + vector gathers/scatters (8 bytes each way of
+    # every live and neighbour entry per sweep); SpMV = 8 nnz + 4 nnz + 8 (N+1) + 8 N (x) + 8 N (y)
+    hbm = mp.get("hbm_gbs")
+    f_last = H.hs_factor_create(h, a, vals, eps=p.eps)
+    nlev = H.hs_factor_get_stats(f_last)["n_levels"]
+    vec = 0
+    for lv in range(nlev):
+        vec += int(H.hs_factor_export(f_last, H.HS_FEXP_LIVE0, lv).sum() + H.hs_factor_export(f_last, H.HS_FEXP_KN, lv).sum())
+    del f_last
+    apply_bytes = 2.0 * S["factor_bytes"] + 2 * 2 * 8.0 * vec
+    n_apply = sum(r["iters"] for r in reps)   # z = M^{-1} r once before the loop, then every non-final iteration
+    n_spmv = sum(r["iters"] for r in reps)
+    t_spmv = sum(r["t_spmv_s"] for r in reps)
+    spmv_bytes = 12.0 * p.nnz + 8.0 * (p.n + 1) + 16.0 * p.n
+
+    def bw(bytes_, t, n):
+        if not n or not t:
+            return None
+        ach = bytes_ / (t / n) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm if hbm else None,
+                "traffic": None, "bytes_per_launch": bytes_, "us_per_launch": 1e6 * t / n, "launches": n}
+    roof["apply"] = bw(apply_bytes, t_apply, n_apply)
+    roof["spmv"] = bw(spmv_bytes, t_spmv, n_spmv)
+    for key in ("apply", "spmv"):
+        tf = os.path.join(ROOT, "profiles", f"r02_traffic_{key}.json")
+        if roof[key] and os.path.exists(tf):
+            tr = json.load(open(tf))
+            roof[key]["traffic"] = tr.get("dram_bytes_per_launch")
+            roof[key]["traffic_source"] = f"profiles/r02_traffic_{key}.json: {tr.get('note', '')}"
     line = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -328,6 +419,8 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{args.config}: {p.name}, N={p.n}, nnz={p.nnz}, eps={p.eps}, pcg_tol={p.tol}, "
                                f"leaf={p.leaf_size or p.leaf_columns}",
                    "l2": "256 MB buffer written between timed steps (and the factor working set > L2)",
+                   "analyze": "reading R-coarse (coarse_fill=0: structural coarse neighbours, DESIGN.md §2)",
+                   "flops": "dense live column counts k_n, k_w (what the kernels compute; >= the support-restricted count)",
                    "parallelism": (f"subdomains over {world} GPUs (factor), solve on rank 0" if dist_factor
                                    else "replicas" if world > 1 else "single"),
                    "pcg_iters": [r["iters"] for r in reps], "relres_true": reps[-1]["relres_true"],

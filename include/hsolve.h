@@ -89,7 +89,8 @@ typedef struct {
 typedef struct {
   double  eps;           /* truncation tolerance, >= 0                 */
   int32_t eps_relative;  /* 1: tau_s = eps * max column norm of G^{-1}A_sw (reading Q1); 0: absolute */
-  int32_t dc;            /* 1: deferred compression (the paper's method); 0 is not supported yet */
+  int32_t dc;            /* 1: deferred compression (the paper's method); 0: the original
+                            LoRaSp step without it (NEXT f1)                     */
   int32_t values_on_device; /* 1: `values` is a device pointer on the handle's device          */
   int32_t reserved;
 } hs_factor_opts;
@@ -139,7 +140,9 @@ enum {
   HS_FEXP_LIVE0 = 1,     /* level l: int64[nclus] live size at the start of the level    */
   HS_FEXP_PIV_PTR = 2,   /* level l: int64[nclus+1] offsets into PIV                      */
   HS_FEXP_PIV = 3,       /* level l: canonical pivot columns of every cluster, pivot order */
-  HS_FEXP_TOP = 4        /* [ntop] live sizes at the top level                            */
+  HS_FEXP_TOP = 4,       /* [ntop] live sizes at the top level                            */
+  HS_FEXP_KN = 5,        /* level l: int64[nclus] k_n, live columns of n(s) at elimination */
+  HS_FEXP_KW = 6         /* level l: int64[nclus] k_w, live columns of w(s) at elimination        */
 };
 
 typedef struct {
@@ -158,6 +161,9 @@ typedef struct {
                             at factor time — the events cost stream time per batch; they
                             are 0 otherwise                                              */
   double  flops_phase[8];
+  double  t_level_s[32]; /* device time of each level l < n_levels (its batches and the A_c
+                            assembly, CUDA events at the level boundaries)   */
+  double  flops_level[32];
 } hs_factor_stats_t;
 
 typedef struct {
@@ -167,7 +173,10 @@ typedef struct {
   double  relres_true;   /* ||b - A x|| / ||b|| computed on the device at the end        */
   double  t_pcg_s;       /* device time                                                  */
   double  t_apply_s;     /* device time spent in the preconditioner                      */
-  double  t_spmv_s;
+  double  t_spmv_s;      /* device time spent in the CSR SpMV (CUDA events)              */
+  double* history;       /* in: caller buffer for ||r_k|| / ||b||, k = 0..iters (or NULL) */
+  int32_t history_cap;   /* in: its capacity                                             */
+  int32_t history_len;   /* out: entries written (min(iters + 1, history_cap))           */
 } hs_pcg_report;
 
 /* ---- handle --------------------------------------------------------------------- */

@@ -345,6 +345,8 @@ hs_status hs_factor_export(hs_factor f, int32_t key, int32_t level, int64_t* out
     switch (key) {
       case HS_FEXP_RANKS: export_vec(L.rank, out, cap, len); break;
       case HS_FEXP_LIVE0: export_vec(L.cap, out, cap, len); break;
+      case HS_FEXP_KN: export_vec(L.kn, out, cap, len); break;
+      case HS_FEXP_KW: export_vec(L.kw, out, cap, len); break;
       case HS_FEXP_PIV_PTR: {
         std::vector<int64_t> p(L.nclus + 1, 0);
         for (int s = 0; s < L.nclus; ++s) p[s + 1] = p[s] + L.rank[s];

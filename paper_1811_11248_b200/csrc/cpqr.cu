@@ -682,7 +682,7 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;   // programmatic dependent launch (pdl_wait precedes every read)
   // HS_CPQR_DIRECT_MSG=1: step messages by remote stores + release arrivals instead of bulk
   // async copies — measured slower on C2 (message phase 3.6k -> 5.0-5.6k cycles per step)
   static const bool direct = std::getenv("HS_CPQR_DIRECT_MSG") != nullptr;
@@ -699,10 +699,13 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
                  int32_t* d_rank, cudaStream_t st) {
   const int n = (int)h_items.size();
   if (n <= 0) return 0;
-  static const size_t target = [] {
+  // read per launch (tests force the modes): HS_CPQR_SMEM_KB = per-CTA slice target,
+  // HS_CPQR_GLOBAL=1 = the global-memory mode (W streamed through L2) at any size
+  const size_t target = [] {
     const char* e = std::getenv("HS_CPQR_SMEM_KB");
     return (size_t)(e ? std::atoi(e) : 192) * 1024;
   }();
+  const bool force_global = std::getenv("HS_CPQR_GLOBAL") != nullptr;
   int max_m = 0;
   for (const auto& it : h_items) max_m = std::max(max_m, it.m);
   const int MR = max_m <= 256 ? 8 : 16;
@@ -732,7 +735,7 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
       max_kw = std::max(max_kw, it.kw);
     }
   while (widen && CS < 16 && n_act * CS * 4 <= nsm && max_kw / (2 * CS) >= 128) CS *= 2;
-  const bool sm = need(CS, true) <= cap;
+  const bool sm = !force_global && need(CS, true) <= cap;
   const size_t smem = need(CS, sm);
   if (smem > cap) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
   // HS_CQ_TRACE=k: clock64 timeline of the k-th launch (cluster 0, CTA 0) on stderr

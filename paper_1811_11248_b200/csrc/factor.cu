@@ -776,7 +776,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     if (h_ired) cudaFreeHost(h_ired);
   });
 
+  // per-level device time (P:1013-1019 report the per-level factor cost): events at the
+  // level boundaries, read once the factor is done
+  std::vector<cudaEvent_t> lev_ev(an->L_top + 1);
+  for (auto& e : lev_ev) HS_CUDA(cudaEventCreate(&e));
+  std::unique_ptr<void, std::function<void(void*)>> lev_ev_guard((void*)1, [&](void*) {
+    for (auto& e : lev_ev) cudaEventDestroy(e);
+  });
+  std::vector<double> lev_flops(an->L_top + 1, 0.0);
   for (int l = 0; l < an->L_top; ++l) {
+    HS_CUDA(cudaEventRecord(lev_ev[l], st));
+    lev_flops[l] = S.flops;
     const Level& lev = an->levels[l];
     LevelRT& L = f->lv[l];
     const double lv_t0 = now_s(), lv_plan0 = t_plan;
@@ -1848,6 +1858,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                    h->vmm.created * (double)h->vmm.chunk / 1e9);
     }
   }
+  HS_CUDA(cudaEventRecord(lev_ev[an->L_top], st));
+  lev_flops[an->L_top] = S.flops;
   // ---- top: dense Cholesky of all live DOFs, on rank 0 -------------------------
   {
     const int ntc = (int)cap.size();
@@ -1945,6 +1957,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   S.t_factor_s = ms * 1e-3;
+  for (int l = 0; l < an->L_top && l < 32; ++l) {
+    float lms = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&lms, lev_ev[l], lev_ev[l + 1]));
+    S.t_level_s[l] = lms * 1e-3;
+    S.flops_level[l] = lev_flops[l + 1] - lev_flops[l];
+  }
   S.t_phase_s[7] = t_plan;
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",

@@ -353,7 +353,13 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   cudaEvent_t e0, e1, a0, a1;
   HS_CUDA(cudaEventCreate(&e0)); HS_CUDA(cudaEventCreate(&e1));
   HS_CUDA(cudaEventCreate(&a0)); HS_CUDA(cudaEventCreate(&a1));
-  double t_apply = 0.0;
+  double t_apply = 0.0, t_spmv = 0.0;
+  cudaEvent_t s0, s1;
+  HS_CUDA(cudaEventCreate(&s0)); HS_CUDA(cudaEventCreate(&s1));
+  rep->history_len = 0;
+  auto hist = [&](double v) {
+    if (rep->history && rep->history_len < rep->history_cap) rep->history[rep->history_len++] = v;
+  };
   HS_CUDA(cudaEventRecord(e0, st));
   k_copy<<<G, T, 0, st>>>(r, d_bin, n);
   k_zero<<<G, T, 0, st>>>(x, n);
@@ -375,6 +381,7 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   rep->iters = 0;
   rep->converged = 0;
   rep->relres = 1.0;
+  hist(bb == 0.0 ? 0.0 : 1.0);
   hs_status err = HS_OK;
   if (bb == 0.0) {
     rep->converged = 1;
@@ -384,7 +391,9 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   } else {
     const double nb = std::sqrt(bb);
     for (int k = 1; k <= maxit; ++k) {
+      HS_CUDA(cudaEventRecord(s0, st));
       launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, p, q, n, st);   // q = A p
+      HS_CUDA(cudaEventRecord(s1, st));
       dot(p, q, n, part, sc + 1, st);                                  // pq
       k_update_xr<<<G, T, 0, st>>>(x, r, p, q, n, sc, part);           // x, r, ||r||^2
       k_finish<<<1, T, 0, st>>>(part, G, sc + 2);
@@ -394,6 +403,12 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
       rep->iters = k;
       const double rel = std::sqrt(std::max(f->h_red[2], 0.0)) / nb;
       rep->relres = rel;
+      hist(rel);
+      {
+        float sms;
+        HS_CUDA(cudaEventElapsedTime(&sms, s0, s1));
+        t_spmv += sms * 1e-3;
+      }
       if (!(f->h_red[0] > 0.0)) { err = HS_E_PRECOND_NOT_POSITIVE; break; }
       if (rel <= tol) { rep->converged = 1; break; }
       HS_CUDA(cudaEventRecord(a0, st));
@@ -415,7 +430,9 @@ void pcg(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int ma
   HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   rep->t_pcg_s = ms * 1e-3;
   rep->t_apply_s = t_apply;
-  rep->t_spmv_s = 0.0;
+  rep->t_spmv_s = t_spmv;
+  cudaEventDestroy(s0);
+  cudaEventDestroy(s1);
   // true residual ||b - A x|| / ||b|| (outside the timed region)
   launch_spmv(f->d_rowptr, f->d_colind, f->d_vals, x, q, n, st);
   k_sub<<<G, T, 0, st>>>(q, d_bin, q, n);
@@ -472,6 +489,7 @@ void gmres(hs_factor_s* f, const double* d_bin, double* d_xout, double tol, int 
   const double nb = norm2(d_bin);
   int its = 0;
   double rel = 1.0;
+  rep->history_len = 0;
   rep->iters = 0;
   rep->converged = 0;
   if (nb == 0.0) rel = 0.0;

@@ -44,6 +44,10 @@ __device__ __forceinline__ double ld_poll(const double* p) {
   }
   return __longlong_as_double((long long)v);
 }
+// A NaN produced by the arithmetic (or carried in from a NaN input) is stored as the
+// canonical quiet NaN, so no polled value can ever take the all-ones "empty" pattern and a
+// consumer never spins on a produced value.
+__device__ __forceinline__ double canon(double v) { return isnan(v) ? __longlong_as_double(0x7ff8000000000000LL) : v; }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -96,7 +100,7 @@ __device__ __forceinline__ void produce(const ApplyLevelArgs& a, const ApplySrc&
         }
         for (; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * zf[k];
       }
-      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.contrib + c.slot + i), "d"(acc) : "memory");
+      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.contrib + c.slot + i), "d"(canon(acc)) : "memory");
     }
   }
 }
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
         acc = wsum(acc);
         if (lane == 0) {
           if (fin) pown[k] = acc;
-          else asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(part + k), "d"(acc) : "memory");
+          else asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(part + k), "d"(canon(acc)) : "memory");
         }
       }
       AP_TR(tt, 2);
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
         for (int w = 0; w < 8; ++w) acc += tv[w] * u[j + w];
       }
       for (; j < m; ++j) acc += Tm[(int64_t)j * m + i] * u[j];
-      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(S.x + i), "d"(acc) : "memory");
+      asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(S.x + i), "d"(canon(acc)) : "memory");
     }
     AP_TR(tt, 3);
     __syncthreads();   // u, bst reusable

@@ -29,7 +29,7 @@ for _i, _s in enumerate(STATUS):
 # hs_dist_plan_export keys
 HS_DEXP_OWNER, HS_DEXP_RECV_PTR, HS_DEXP_RECV, HS_DEXP_HELD_PTR, HS_DEXP_HELD = range(5)
 # hs_factor_export keys
-HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP = range(5)
+HS_FEXP_RANKS, HS_FEXP_LIVE0, HS_FEXP_PIV_PTR, HS_FEXP_PIV, HS_FEXP_TOP, HS_FEXP_KN, HS_FEXP_KW = range(7)
 
 # every symbol include/hsolve.h declares
 SYMBOLS = ["hs_create", "hs_nccl_unique_id", "hs_loopback_world_create", "hs_loopback_world_destroy",
@@ -64,21 +64,33 @@ class hs_analysis_info(C.Structure):
 class hs_factor_stats_t(C.Structure):
     _fields_ = [("t_factor_s", C.c_double), ("flops", C.c_double), ("factor_bytes", C.c_double),
                 ("n_top", C.c_int64), ("n_levels", C.c_int32), ("n_batches", C.c_int32), ("max_m", C.c_int32),
-                ("max_rank", C.c_int32), ("t_phase_s", C.c_double * 8), ("flops_phase", C.c_double * 8)]
+                ("max_rank", C.c_int32), ("t_phase_s", C.c_double * 8), ("flops_phase", C.c_double * 8),
+                ("t_level_s", C.c_double * 32), ("flops_level", C.c_double * 32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
-        d["t_phase_s"] = list(self.t_phase_s)
-        d["flops_phase"] = list(self.flops_phase)
+        for k in ("t_phase_s", "flops_phase"):
+            d[k] = list(getattr(self, k))
+        for k in ("t_level_s", "flops_level"):
+            d[k] = list(getattr(self, k))[:self.n_levels]
         return d
 
 
 class hs_pcg_report(C.Structure):
     _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("relres", C.c_double), ("relres_true", C.c_double),
-                ("t_pcg_s", C.c_double), ("t_apply_s", C.c_double), ("t_spmv_s", C.c_double)]
+                ("t_pcg_s", C.c_double), ("t_apply_s", C.c_double), ("t_spmv_s", C.c_double),
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int32), ("history_len", C.c_int32)]
+
+    def __init__(self, cap=1024):
+        super().__init__()
+        self._hist = (C.c_double * cap)()
+        self.history = C.cast(self._hist, C.POINTER(C.c_double))
+        self.history_cap = cap
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("history", "history_cap", "history_len")}
+        d["history"] = list(self._hist[:self.history_len])
+        return d
 
 
 _lib = None

@@ -15,6 +15,7 @@ from problems import gen_poisson2d, gen_laplace3d, gen_slab, gen_stokes_q1
 from oracle.analyze import analyze
 from oracle.factor import factor as ofactor
 from oracle.solve import apply as oapply, pcg as opcg
+from parity_helpers import oracle_with_injection, apply_parity as _apply_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -53,57 +54,6 @@ def _both(H, handle, p, eps, kw=None, dc=1):
     assert injected <= max(2, nelim // 200), f"{injected} of {nelim} clusters needed decision injection"
     assert np.array_equal(H.hs_factor_export(f, H.HS_FEXP_TOP), fac.top_sizes)
     return an, fac, a, f, injected
-
-
-def oracle_with_injection(H, f, an, p, eps, max_rounds=200, dc=1):
-    """Rank/pivot parity with the margin exemption: walk the clusters in elimination
-    order; at the first disagreement, a flagged cluster gets the GPU's decisions
-    injected into the oracle (which is re-run), an unflagged one fails the test.
-    Returns (oracle factor, flagged clusters, injected clusters, eliminations)."""
-    gpu = []
-    for l in range(len(an.levels)):
-        gpu.append((H.hs_factor_export(f, H.HS_FEXP_RANKS, l), H.hs_factor_export(f, H.HS_FEXP_PIV_PTR, l),
-                    H.hs_factor_export(f, H.HS_FEXP_PIV, l)))
-    inject = {}
-    for _ in range(max_rounds):
-        fac = ofactor(an, p.rowptr, p.colind, p.vals, eps=eps, inject=inject or None, dc=bool(dc))
-        first = None
-        nflag = nelim = 0
-        for l, lv in enumerate(fac.elims):
-            g_r, g_pp, g_pv = gpu[l]
-            for eb in lv:
-                for e in eb:
-                    nflag += int(e.flagged)
-                    nelim += 1
-                    gpiv = g_pv[g_pp[e.s]:g_pp[e.s + 1]]
-                    if (l, e.s) in inject or (g_r[e.s] == e.r and np.array_equal(gpiv, e.piv)):
-                        continue
-                    first = (l, e, gpiv)
-                    break
-                if first:
-                    break
-            if first:
-                break
-        if first is None:
-            return fac, nflag, len(inject), nelim
-        l, e, gpiv = first
-        assert e.flagged, (f"decision mismatch at level {l} cluster {e.s} (unflagged, mu={e.mu:.2e}, "
-                           f"pi={e.pi:.2e}): gpu r={gpu[l][0][e.s]} piv={list(gpiv)} oracle r={e.r} "
-                           f"piv={list(e.piv)}")
-        inject[(l, e.s)] = (int(gpu[l][0][e.s]), gpiv.tolist())
-    raise AssertionError("decision injection did not converge")
-
-
-def _apply_parity(H, f, fac, n, seeds=(1, 2, 3), tol=1e-9):
-    worst = 0.0
-    for sd in seeds:
-        v = np.random.default_rng(sd).standard_normal(n)
-        xg = H.hs_apply(f, v)
-        xo = oapply(fac, v)
-        err = np.linalg.norm(xg - xo) / np.linalg.norm(xo)
-        worst = max(worst, err)
-        assert err <= tol, f"apply parity {err:.3e}"
-    return worst
 
 
 TINY = [
@@ -326,3 +276,54 @@ def test_pipeline_modes_agree(H, handle, monkeypatch):
     x2, r2 = run(HS_NO_FUSED_POTRF_TRSM="1")
     assert all(np.array_equal(u, w) for u, w in zip(r0, r2))
     assert np.linalg.norm(x2 - x0) <= 1e-11 * np.linalg.norm(x0)
+
+
+def test_apply_nan_input_terminates(H, handle):
+    """The apply polls contribution / x VALUES against an all-ones 'empty' pattern: a NaN
+    carried in from the input (or produced inside) is stored canonically, so the sweeps
+    terminate and the NaN propagates instead of hanging the GPU."""
+    p = gen_laplace3d(16, leaf_size=16)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, None, leaf_size=16)
+    f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    b = p.b.copy()
+    b[[3, p.n // 2]] = np.nan
+    x = H.hs_apply(f, b)
+    assert np.isnan(x).any()
+    b[3] = -np.nan
+    x = H.hs_apply(f, b)
+    assert np.isnan(x).any()
+    assert np.all(np.isfinite(H.hs_apply(f, p.b)))   # the factor is still usable
+
+
+def test_device_inputs_from_torch_stream(H, handle):
+    """Inputs produced by torch on its own stream (torch.randn on the GPU, no host round trip)
+    are read only once they are written (the wrapper waits for torch's stream)."""
+    import torch
+    p = gen_laplace3d(24, leaf_size=27)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, None, leaf_size=27)
+    f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for _ in range(3):
+        big = torch.randn(1 << 26, device="cuda", dtype=torch.float64, generator=g)   # keep torch's stream busy
+        bt = torch.randn(p.n, device="cuda", dtype=torch.float64, generator=g) * 2.0 + big[:p.n] * 0.0
+        xt = H.hs_apply(f, bt)
+        xh = H.hs_apply(f, bt.cpu().numpy())
+        assert np.array_equal(xt.cpu().numpy(), xh)
+    with pytest.raises(H.HSError):
+        H.hs_apply(f, torch.zeros(p.n - 1, device="cuda", dtype=torch.float64))
+    with pytest.raises(H.HSError):
+        H.hs_apply(f, torch.zeros(p.n, device="cuda", dtype=torch.float32))
+    with pytest.raises(H.HSError):
+        H.hs_apply(f, p.b, x=np.zeros(p.n, dtype=np.float32))
+    # the report carries the residual history and the SpMV time
+    x, rep = H.hs_pcg(f, p.b, tol=1e-8)
+    h = rep["history"]
+    assert len(h) == rep["iters"] + 1 and h[0] == 1.0 and h[-1] <= 1e-8 < h[-2]
+    assert rep["t_spmv_s"] > 0
+    st = H.hs_factor_get_stats(f)
+    assert len(st["t_level_s"]) == st["n_levels"] and all(t > 0 for t in st["t_level_s"])
+    assert abs(sum(st["flops_level"]) - st["flops"]) <= 1e-6 * st["flops"] + st["n_top"] ** 3
+    kn0 = H.hs_factor_export(f, H.HS_FEXP_KN, 0)
+    kw0 = H.hs_factor_export(f, H.HS_FEXP_KW, 0)
+    nleaf = H.hs_analysis_export(a, H.HS_EXP_LEAF_OFF).size - 1
+    assert kn0.size == kw0.size == nleaf and kn0.sum() > 0 and kw0.sum() > 0
