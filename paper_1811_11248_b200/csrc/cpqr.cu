@@ -123,24 +123,6 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-// the same wait with cluster-scope acquire: the messages arrive as remote st.shared::cluster
-// stores ordered by the senders' release arrivals
-__device__ __forceinline__ void bar_wait_cl(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(1000000u)
-        : "memory");
-}
-__device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
-  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(__double_as_longlong(v)) : "memory");
-}
-__device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
-}
 __device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -193,10 +175,6 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[k] = clock64(); \
   } while (0)
   const bool trace_split = trace && trace[255] != 0;   // HS_CQ_TRACE_SPLIT: stamp 4 at the push
-  // bit 1 of `relative`: step messages by direct remote stores + release arrivals (count-CS
-  // barrier) instead of bulk async copies (HS_CPQR_DIRECT_MSG=1; slower, kept for A/B)
-  const bool direct = (relative & 2) != 0;
-  relative &= 1;
   CQ_TR(0);
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -212,11 +190,12 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   const int ldm = cq_ldm(m, G);
   const int msgw = cq_msg_words(m);
   const uint32_t msgb = (uint32_t)(msgw * 8);
-  // element (l, c) of the slice: shared memory column-major (SM) or B_s in place (row-major)
-  const int sr = SM ? 1 : ld, sc = SM ? ldm : 1;
+  // element (l, c) of the slice, column-major with column stride ldm: in shared memory (SM)
+  // or in the cluster's global scratch (global mode: coalesced group loads through L2)
+  const int sr = 1, sc = ldm;
   // dynamic shared memory (16-byte aligned regions, the bulk copies require it):
   // [W (SM mode): wchunk x ldm] [nu: wchunk] [mine: 2 x msgw] [slots: 2 x CS x msgw]
-  double* W = SM ? dsm : it.B + w_lo;
+  double* W = SM ? dsm : it.Wt + (size_t)w_lo * ldm;
   double* nu = SM ? dsm + (((size_t)wchunk * ldm + 1) & ~(size_t)1) : dsm;
   double* mine = nu + ((wchunk + 1) & ~1);
   double* slots = mine + 2 * msgw;
@@ -225,14 +204,14 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      bar_init(sm_addr(&sh.bar1[b]), direct ? CS : 1);   // CS release arrivals, or the local expect_tx
+      bar_init(sm_addr(&sh.bar1[b]), 1);   // the local expect_tx; CS bulk copies complete it
       bar_init(sm_addr(&sh.bar3[b]), 1);
     }
     bar_init(sm_addr(&sh.bar2), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // ---- stage the w-slice (transpose to column-major; coalesced global reads) ----------
-  if (SM) {
+  {
     const int tot = m * nw;
     const double* __restrict__ src = it.B + w_lo;
     for (int e0 = tid; e0 < tot; e0 += 4 * CQ_THREADS) {
@@ -287,7 +266,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     // (1) local max, local candidate and its reflector -> every CTA
     lm = wmax(lm);
     if (lane == 0) sh.wred[wid] = lm;
-    if (tid == 0 && !direct) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
+    if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
     __syncthreads();
     if (j < 60) CQ_TR(3 + 4 * j);
     {   // every warp: the CTA max, and the lowest column of a strided share over the window
@@ -346,26 +325,13 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       if (lane == 0) mymsg[0] = Mc;
       fence_proxy_async();
       __syncwarp();
-      if (direct) {
-        // the message into every CTA's slot (this CTA's included) by remote stores, then one
-        // release arrival per destination
-        const uint32_t dst0 = sm_addr(slot + (size_t)crank * msgw);
-        for (int e = lane; e < CS * msgw; e += 32) {
-          const int k = e / msgw, w = e - k * msgw;
-          st_cluster(remote(dst0 + 8u * (uint32_t)w, k), mymsg[w]);
-        }
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-        __syncwarp();
-        if (lane < CS) arrive_remote(remote(sm_addr(&sh.bar1[buf]), lane));
-      } else if (lane < CS) {
+      if (lane < CS)
         bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
                   remote(sm_addr(&sh.bar1[buf]), lane));
-      }
       if (trace_split && j < 60) CQ_TR(4 + 4 * j);   // local work done, message sent
     }
     // (2) decision from the CS messages (identical in every thread of every CTA)
-    if (direct) bar_wait_cl(sm_addr(&sh.bar1[buf]), par);
-    else bar_wait(sm_addr(&sh.bar1[buf]), par);
+    bar_wait(sm_addr(&sh.bar1[buf]), par);
     if (!trace_split && j < 60) CQ_TR(4 + 4 * j);
     // the CS local maxima: lane k of every warp reads CTA k's (CS <= 16), warp max and a
     // ballot for the lowest CTA over the window (the same values in every warp)
@@ -525,15 +491,15 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   CQ_TR(250);
   __syncthreads();
   // ---- coarse-w rows back to global memory (rows [0, r) of the slice) -----------------
-  if (SM && (!it.dwb || it.keepB))   // (direct write-back: only the debug records need B)
+  if (!it.dwb || it.keepB)   // (direct write-back: only the debug records need B)
     for (int e = tid; e < r * nw; e += CQ_THREADS) {
       const int l = e / nw, c = e % nw;
       it.B[(size_t)l * ld + w_lo + c] = W[(size_t)c * ldm + l];
     }
   if (it.dwb) {   // ... and straight into the store blocks (s, q), q in w(s); I_r on (s, s)
     for (int c = tid; c < nw; c += CQ_THREADS) {
-      const double* src = SM ? W + (size_t)c * ldm : it.B + w_lo + c;
-      const size_t sst = SM ? 1 : ld;
+      const double* src = W + (size_t)c * ldm;
+      const size_t sst = 1;
       for (int l = 0; l < r; ++l) {
         double* d = dwb_addr(it.seg, it.nseg, w_lo + c, l);
         if (d) *d = src[(size_t)l * sst];
@@ -561,6 +527,7 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restri
   cg::cluster_group cl = cg::this_cluster();
   const int item = blockIdx.x / (int)cl.num_blocks();
   const CluItem it = items[item];
+  if ((it.Wt == nullptr) != SM) return;   // the other mode's launch eliminates this cluster
   if (it.m == 0 || it.kw == 0) {   // uniform over the cluster: nobody reaches a cluster barrier
     if (cl.block_rank() == 0 && threadIdx.x == 0) rank_out[item] = 0;
     return;
@@ -683,10 +650,7 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;   // programmatic dependent launch (pdl_wait precedes every read)
-  // HS_CPQR_DIRECT_MSG=1: step messages by remote stores + release arrivals instead of bulk
-  // async copies — measured slower on C2 (message phase 3.6k -> 5.0-5.6k cycles per step)
-  static const bool direct = std::getenv("HS_CPQR_DIRECT_MSG") != nullptr;
-  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, (relative ? 1 : 0) | (direct ? 2 : 0), d_rank, trace));
+  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, relative ? 1 : 0, d_rank, trace));
   count_launch(1);
 }
 
@@ -695,86 +659,107 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
 // Host side: pick the cluster size CS (smallest power of two whose per-CTA w-slice fits the
 // shared-memory target; HS_CPQR_SMEM_KB overrides the 192 KB default), the rows-per-lane
 // template (MR = 8 up to m = 256, else 16) and shared vs global mode.
+static int cq_mr(int max_m) { return max_m <= 256 ? 8 : 16; }
+static constexpr size_t CQ_CAP_BYTES = 200 * 1024 - sizeof(CqShared);
+
+size_t cpqr_global_words(int m, int kw, int max_m) {
+  if (m <= 0 || kw <= 0) return 0;
+  if (std::getenv("HS_CPQR_GLOBAL") == nullptr &&
+      cq_smem_words(m, kw, 16, cq_mr(max_m), true) * sizeof(double) <= CQ_CAP_BYTES)
+    return 0;
+  return (size_t)(kw + 16) * (m + 16);
+}
+
+// Host side: two launches per batch, one per mode (a cluster whose w-block does not fit a
+// 16-CTA cluster's shared memory runs from its global scratch; the others keep theirs in
+// shared memory, so one large cluster no longer moves its whole batch to the slow mode).
+// Per launch: the cluster size CS = the smallest power of two whose per-CTA slice fits the
+// shared-memory target (HS_CPQR_SMEM_KB overrides the 192 KB default), widened for batches of
+// few clusters; the rows-per-lane template MR = 8 up to m = 256, else 16.
 int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
                  int32_t* d_rank, cudaStream_t st) {
   const int n = (int)h_items.size();
   if (n <= 0) return 0;
-  // read per launch (tests force the modes): HS_CPQR_SMEM_KB = per-CTA slice target,
-  // HS_CPQR_GLOBAL=1 = the global-memory mode (W streamed through L2) at any size
+  // read per launch (tests force the modes): HS_CPQR_SMEM_KB = per-CTA slice target
   const size_t target = [] {
     const char* e = std::getenv("HS_CPQR_SMEM_KB");
     return (size_t)(e ? std::atoi(e) : 192) * 1024;
   }();
-  const bool force_global = std::getenv("HS_CPQR_GLOBAL") != nullptr;
   int max_m = 0;
   for (const auto& it : h_items) max_m = std::max(max_m, it.m);
-  const int MR = max_m <= 256 ? 8 : 16;
-  auto need = [&](int cs, bool sm) {
-    size_t w = 2;
-    for (const auto& it : h_items)
-      if (it.m > 0 && it.kw > 0) w = std::max(w, cq_smem_words(it.m, it.kw, cs, MR, sm));
-    return w * sizeof(double);
-  };
-  const size_t cap = 200 * 1024 - sizeof(CqShared);
-  int CS = 1;
-  while (CS < 16 && need(CS, true) > std::min(target, cap)) CS *= 2;
-  // a batch of few clusters leaves most SMs idle: split the columns over more CTAs (a
-  // shorter update per step for a costlier exchange) while the clusters still fill at most
-  // half the GPU and every CTA keeps >= 128 columns (C2 level 3: CPQR 38 -> 29 ms)
+  const int MR = cq_mr(max_m);
   static const int nsm = [] {
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  static const bool widen = std::getenv("HS_CPQR_NO_WIDEN") == nullptr;
-  int n_act = 0, max_kw = 0;
-  for (const auto& it : h_items)
-    if (it.m > 0 && it.kw > 0) {
-      ++n_act;
-      max_kw = std::max(max_kw, it.kw);
-    }
-  while (widen && CS < 16 && n_act * CS * 4 <= nsm && max_kw / (2 * CS) >= 128) CS *= 2;
-  const bool sm = !force_global && need(CS, true) <= cap;
-  const size_t smem = need(CS, sm);
-  if (smem > cap) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
   // HS_CQ_TRACE=k: clock64 timeline of the k-th launch (cluster 0, CTA 0) on stderr
   static const int trace_at = [] {
     const char* e = std::getenv("HS_CQ_TRACE");
     return e ? std::atoi(e) : -1;
   }();
   static std::atomic<int> launches{0};
-  long long* trace = nullptr;
-  if (launches++ == trace_at) {
-    HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
-    HS_CUDA(cudaMemsetAsync(trace, 0, 256 * sizeof(long long), st));
-    if (std::getenv("HS_CQ_TRACE_SPLIT")) {
-      static const long long one = 1;
-      HS_CUDA(cudaMemcpyAsync(trace + 255, &one, sizeof one, cudaMemcpyHostToDevice, st));
+  int CS_ret = 0;
+  for (int mode = 0; mode < 2; ++mode) {   // 0: shared-memory clusters, 1: global-scratch clusters
+    const bool sm = mode == 0;
+    auto need = [&](int cs) {
+      size_t w = 2;
+      for (const auto& it : h_items)
+        if (it.m > 0 && it.kw > 0 && (it.Wt == nullptr) == sm) w = std::max(w, cq_smem_words(it.m, it.kw, cs, MR, sm));
+      return w * sizeof(double);
+    };
+    int n_act = 0, max_kw = 0;
+    for (const auto& it : h_items)
+      if (it.m > 0 && it.kw > 0 && (it.Wt == nullptr) == sm) {
+        ++n_act;
+        max_kw = std::max(max_kw, it.kw);
+      }
+    int n_mode = 0;   // the shared-memory launch also writes r = 0 for the empty clusters
+    for (const auto& it : h_items) n_mode += (it.Wt == nullptr) == sm;
+    if (n_mode == 0) continue;
+    int CS = 1;
+    while (CS < 16 && need(CS) > std::min(target, CQ_CAP_BYTES)) CS *= 2;
+    // a batch of few clusters leaves most SMs idle: split the columns over more CTAs (a
+    // shorter update per step for a costlier exchange) while the clusters still fill at most
+    // a quarter of the GPU and every CTA keeps >= 128 columns (C2 level 3: CPQR 38 -> 29 ms)
+    while (CS < 16 && n_act * CS * 4 <= nsm && max_kw / (2 * CS) >= 128) CS *= 2;
+    const size_t smem = need(CS);
+    if (smem > CQ_CAP_BYTES) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
+    long long* trace = nullptr;
+    if (launches++ == trace_at) {
+      HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
+      HS_CUDA(cudaMemsetAsync(trace, 0, 256 * sizeof(long long), st));
+      if (std::getenv("HS_CQ_TRACE_SPLIT")) {
+        static const long long one = 1;
+        HS_CUDA(cudaMemcpyAsync(trace + 255, &one, sizeof one, cudaMemcpyHostToDevice, st));
+      }
+    }
+    if (MR == 8) {
+      if (sm) launch_one<8, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else launch_one<8, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+    } else {
+      if (sm) launch_one<16, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else launch_one<16, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+    }
+    CS_ret = std::max(CS_ret, CS);
+    if (trace) {
+      long long h[256];
+      HS_CUDA(cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      cudaFree(trace);
+      const long long t0 = h[0];
+      std::fprintf(stderr, "[cq trace] launch %d (%s mode): n=%d CS=%d smem=%zu r=%lld | stage %lld norms %lld cyc\n",
+                   trace_at, sm ? "shared" : "global", n, CS, smem, h[252], h[1] - t0, h[2] - h[1]);
+      for (int j = 0; j < 60 && h[3 + 4 * j]; ++j)
+        std::fprintf(stderr, "[cq trace]  step %2d: B1 %6lld  C1 %6lld  B3 %6lld  upd %6lld\n", j,
+                     h[3 + 4 * j] - (j ? h[6 + 4 * (j - 1)] : h[2]), h[4 + 4 * j] - h[3 + 4 * j],
+                     h[5 + 4 * j] - h[4 + 4 * j], h[6 + 4 * j] - h[5 + 4 * j]);
+      std::fprintf(stderr, "[cq trace]  loop end %lld, exit %lld, total %lld cyc\n", h[250] - t0, h[251] - h[250],
+                   h[251] - t0);
     }
   }
-  if (MR == 8) {
-    if (sm) launch_one<8, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-    else launch_one<8, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-  } else {
-    if (sm) launch_one<16, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-    else launch_one<16, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-  }
-  if (trace) {
-    long long h[256];
-    HS_CUDA(cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st));
-    HS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(trace);
-    const long long t0 = h[0];
-    std::fprintf(stderr, "[cq trace] launch %d: n=%d CS=%d smem=%zu m0=%d kw0=%d r=%lld | stage %lld norms %lld cyc\n",
-                 trace_at, n, CS, smem, h_items[0].m, h_items[0].kw, h[252], h[1] - t0, h[2] - h[1]);
-    for (int j = 0; j < 60 && h[3 + 4 * j]; ++j)
-      std::fprintf(stderr, "[cq trace]  step %2d: B1 %6lld  C1 %6lld  B3 %6lld  upd %6lld\n", j,
-                   h[3 + 4 * j] - (j ? h[6 + 4 * (j - 1)] : h[2]), h[4 + 4 * j] - h[3 + 4 * j],
-                   h[5 + 4 * j] - h[4 + 4 * j], h[6 + 4 * j] - h[5 + 4 * j]);
-    std::fprintf(stderr, "[cq trace]  loop end %lld, exit %lld, total %lld cyc\n", h[250] - t0, h[251] - h[250], h[251] - t0);
-  }
-  return CS;
+  return CS_ret;
 }
 
 // rows per lane: 8 up to m = 256 (the kernels' group size G <= 32), else 16

@@ -73,6 +73,10 @@ struct CluItem {
   double* Dss;      // the diagonal store block (s, s), ld ldss
   double* Cout;
   int32_t nseg, ldss, dwb, keepB;   // keepB: also write the coarse rows / rotated B_n back to B (records)
+  // CPQR global-memory mode (a w-block too large for a 16-CTA cluster's shared memory): the
+  // slices live column-major in this scratch ((kw + 16) x (m + 16) doubles, coalesced group
+  // loads) instead of shared memory; null = shared-memory mode
+  double* Wt;
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
@@ -88,7 +92,6 @@ struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operato
 struct FusedItem {
   const double* Ass;          // diagonal block in the store (lower, row-major, ld lda)
   double* G;                  // workspace G_s
-  double* Ginv;               // G_s^{-1} (k_chol writes it, k_scale_gemm reads it; the V workspace), or null
   double* B;                  // workspace B_s (m x ldB)
   unsigned long long* nmax;   // R-floor slot
   int32_t m, lda, ldB, kw;
@@ -251,7 +254,6 @@ void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, Ran
                     cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st);
-bool scale_by_inverse();
 
 // ---- launch accounting (every launcher counts its kernels; graphs count their nodes) -----
 void count_launch(int64_t n);
@@ -274,12 +276,12 @@ void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d
 void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st);
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
-void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st);
 // thread-block-cluster CPQR; picks the cluster size from the batch shape, returns it
-int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
-                 int32_t* d_rank, cudaStream_t st);
 // a3+a4 v3 (cpqr.cu): thread-block cluster per graph cluster, column groups of G lanes,
 // one DSMEM exchange per step, n-columns rotated after the pivoting loop; returns CS
+// words of global scratch a cluster's CPQR needs (0: it runs from shared memory); max_m is
+// the largest cluster of the batch (it fixes the kernels' rows-per-lane)
+size_t cpqr_global_words(int m, int kw, int max_m);
 int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
                  int32_t* d_rank, cudaStream_t st);
 // a4 for the n-columns: B_n <- Q^T B_n with Q = H_0...H_{r-1} from the CPQR (rank from d_rank).

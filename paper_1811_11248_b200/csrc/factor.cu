@@ -642,8 +642,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (opt.eps < 0 || !std::isfinite(opt.eps)) fail(HS_E_INVALID_ARG, "factor: eps must be finite and >= 0");
   if (opt.dc != 0 && opt.dc != 1) fail(HS_E_INVALID_ARG, "factor: dc must be 0 or 1");
   const bool nodc = opt.dc == 0;   // NEXT f1: the original LoRaSp step (nodc.cu)
-  if (nodc && (std::getenv("HS_CPQR_SINGLE_CTA") || std::getenv("HS_CPQR_V2")))
-    fail(HS_E_UNSUPPORTED, "factor: dc = 0 runs with the v3 CPQR only");
   Analysis* an = const_cast<Analysis*>(an_c);   // the device pattern cache lives in the analysis
   const int64_t n = an->n, nnz = an->rowptr[n];
   cudaStream_t st = h->stream;
@@ -733,8 +731,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
 
   const bool prof = std::getenv("HS_PROFILE") != nullptr;
   // A/B switches for the previous CPQR kernels (single CTA / cluster with per-thread columns)
-  const bool cpqr_single_cta = std::getenv("HS_CPQR_SINGLE_CTA") != nullptr;
-  const bool cpqr_v2 = std::getenv("HS_CPQR_V2") != nullptr;
   const bool no_fused = std::getenv("HS_NO_FUSED_POTRF_TRSM") != nullptr;   // separate gather/POTRF/TRSM
   const bool no_dwb = std::getenv("HS_NO_DIRECT_WB") != nullptr;            // write-back pass instead
   // ---- multi-GPU (dist.cpp; protocol of oracle/dist.py) ---------------------
@@ -971,7 +967,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       const bool fused = !nodc && max_m <= CI_MAX_M && !no_fused;
       // direct write-back: CPQR / k_rotate_n write row s's coarse blocks, I_r and C_s
       // themselves (no write-back pass); needs the device patch and CPQR v3
-      const bool dwb = fused && dpatch && !cpqr_single_cta && !cpqr_v2 && !no_dwb;
+      const bool dwb = fused && dpatch && !no_dwb;
       std::vector<int32_t> seg0v(nb, 0);
       // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
       int64_t wsz = 0;
@@ -995,6 +991,18 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           }
         }
       ctmp = csz ? (double*)dc.alloc(sizeof(double) * csz) : nullptr;
+      // CPQR global-memory scratch of the clusters whose w-block exceeds a 16-CTA cluster's
+      // shared memory (freed once the batch's kernels are queued: stream-ordered reuse)
+      int64_t gsz = 0;
+      std::vector<int64_t> go(nb, -1);
+      for (int bi = 0; bi < nb; ++bi) {
+          const int64_t w = (int64_t)cpqr_global_words(live[Bo[bi]], L.kw[Bo[bi]], max_m);
+          if (w) {
+            go[bi] = gsz;
+            gsz += (w + 3) & ~int64_t(3);
+          }
+        }
+      double* wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
         const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
@@ -1007,6 +1015,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
         it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
+        it.Wt = go[bi] >= 0 ? wtmp + go[bi] : nullptr;
         if (m == 0) continue;
         double* p; int32_t ld, tr;
         bs.get(s, s, p, ld, tr);
@@ -1036,8 +1045,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           // segments are in column order: each tile takes the run of segments overlapping it
           int32_t sb = seg0;
           const int32_t se = (int32_t)fseg.size();
-          double* ginv = scale_by_inverse() ? L.V[s] : nullptr;   // G^{-1} in V (CPQR overwrites it later)
-          fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+          fci.push_back(FusedItem{pss, L.G[s], L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
           if (dwb) {
             seg0v[bi] = seg0;
             it.nseg = se - seg0;
@@ -1055,12 +1063,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
             int32_t sf = sb;
             while (sf < se && fseg[sf].col < c0 + nc) ++sf;
-            fz.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
+            fz.push_back(FusedItem{pss, L.G[s], L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
           }
         } else {
           for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
         }
-        if (!cpqr_single_cta && !cpqr_v2 && (kw > 0 || (dwb && kn > 0))) {   // v3 rotates the n-columns in k_rotate_n
+        if (kw > 0 || (dwb && kn > 0)) {   // the n-columns are rotated by k_rotate_n
           const int32_t rw = rot_tile_cols(m, max_m);
           for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
         }
@@ -1106,12 +1114,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, st);   // R-floor
           }
           pt.rec(pt.a[3], st);
-          if (cpqr_single_cta) launch_cpqr(upA.dptr<CluItem>(iC), nb, opt.eps, opt.eps_relative, d_rank, st);
-          else if (cpqr_v2) launch_cpqr2(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-          else {
-            launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
-            launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)nrot, max_m, d_rank, st);
-          }
+          launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+          launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)nrot, max_m, d_rank, st);
           pt.rec(pt.a[4], st);
           if (dpatch) {
             if (publish) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
@@ -1509,6 +1513,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       for (double* b : rbuf)
         if (b) dc.free(b);
+      if (wtmp) dc.free(wtmp);   // the batch's CPQR is queued
       if (ws) {
         if (f->keep_records) L.wchunks.push_back(ws);
         else dc.free(ws);

@@ -23,7 +23,6 @@ namespace {
 
 constexpr int ST_TW = 64;   // columns per k_scale_tile CTA
 
-template <int R4, bool INV>
 __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ items, DevStatus* status) {
   pdl_trigger();
   pdl_wait();
@@ -104,119 +103,6 @@ __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ item
   for (int e = tid; e < m * m; e += blockDim.x) {   // G_s (lower, zeros above)
     const int i = e / m, j = e % m;
     it.G[e] = j <= i ? U[j * ldu + i] : 0.0;
-  }
-  if (!INV || !it.Ginv) return;
-  // G_s^{-1} (lower) by forward substitution on I, warp-synchronously: warp w owns columns
-  // cb + 8w + (lane & 7), lane group gr = lane >> 3 owns rows gr + 4t in registers; the
-  // pivot of row i is broadcast by shuffle (no CTA barrier in the m-step chain)
-  const int gr = lane >> 3;
-  for (int cb = 0; cb < m; cb += 64) {
-    const int col = cb + wid * 8 + (lane & 7);
-    double r[R4];
-#pragma unroll
-    for (int t = 0; t < R4; ++t) r[t] = (gr + 4 * t == col) ? 1.0 : 0.0;
-#pragma unroll
-    for (int ti = 0; ti < R4; ++ti) {
-#pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        const int i = 4 * ti + gi;
-        if (i < m) {   // uniform over the CTA
-          const double* gc = U + i * ldu;   // column i of G: gc[l] = G[l][i], l >= i
-          if (gr == gi) r[ti] = r[ti] / gc[i];
-          const double xi = __shfl_sync(0xffffffffu, r[ti], (lane & 7) + 8 * gi);
-#pragma unroll
-          for (int t = ti; t < R4; ++t) {
-            const int l = gr + 4 * t;
-            if (l > i && l < m) r[t] = fma(-gc[l], xi, r[t]);
-          }
-        }
-      }
-    }
-    if (col < m)
-#pragma unroll
-      for (int t = 0; t < R4; ++t) {
-        const int l = gr + 4 * t;
-        if (l < m) it.Ginv[(int64_t)l * m + col] = r[t];
-      }
-  }
-}
-
-// B[:, c0:c0+nc] = G^{-1} A[:, c0:c0+nc] as a product with the explicit inverse (register-
-// tiled FFMA, lower triangle only): thread (rg, cg) owns rows rg + 16 r, columns cg + 16 j.
-template <int R>
-__global__ void __launch_bounds__(256) k_scale_gemm(const FusedItem* __restrict__ items,
-                                                    const FusedSeg* __restrict__ segs) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ double sm[];
-  const FusedItem it = items[blockIdx.x];
-  const int m = it.m;
-  if (m == 0 || it.nc <= 0) return;
-  double* gi = sm;              // m x m
-  double* x = sm + m * m;       // m x ST_TW
-  const int tid = threadIdx.x;
-  for (int e = tid; e < m * m; e += blockDim.x) gi[e] = it.Ginv[e];
-  for (int e = tid; e < m * ST_TW; e += blockDim.x) x[e] = 0.0;
-  __syncthreads();
-  for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {   // the tile's columns from the store
-    const FusedSeg g = segs[sg];
-    const int j0 = max(it.c0, g.col), j1 = min(it.c0 + it.nc, g.col + g.len);
-    const int w = j1 - j0;
-    if (g.trans) {
-      for (int e = tid; e < m * w; e += blockDim.x) {   // consecutive threads: consecutive rows i
-        const int j = j0 + e / m, i = e % m;
-        x[i * ST_TW + (j - it.c0)] = g.src[(int64_t)(j - g.col) * g.sld + i];
-      }
-    } else {
-      for (int e = tid; e < m * w; e += blockDim.x) {
-        const int i = e / w, j = j0 + e % w;
-        x[i * ST_TW + (j - it.c0)] = g.src[(int64_t)i * g.sld + (j - g.col)];
-      }
-    }
-  }
-  __syncthreads();
-  const int cg = tid & 15, rg = tid >> 4;
-  double acc[R][4];
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[r][j] = 0.0;
-  const int kend = min(m, rg + 16 * (R - 1) + 1);   // G^{-1} is lower triangular
-  for (int k = 0; k < kend; ++k) {
-    double b[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = x[k * ST_TW + cg + 16 * j];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = rg + 16 * r;
-      const double a = (i < m) ? gi[i * m + k] : 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[r][j] = fma(a, b[j], acc[r][j]);
-    }
-  }
-  __syncthreads();   // x is reused for the result
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = rg + 16 * r;
-    if (i < m)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int cc = cg + 16 * j;
-        x[i * ST_TW + cc] = acc[r][j];
-        if (cc < it.nc) it.B[(int64_t)i * it.ldB + it.c0 + cc] = acc[r][j];
-      }
-  }
-  if (it.nmax && it.c0 + it.nc > it.kw) {   // largest n-column norm (R-floor of tau_s)
-    __syncthreads();
-    double s = -1.0;
-    const int n0 = max(0, it.kw - it.c0);
-    if (tid < ST_TW && tid >= n0 && tid < it.nc) {
-      s = 0.0;
-      for (int i = 0; i < m; ++i) s += x[i * ST_TW + tid] * x[i * ST_TW + tid];
-      s = sqrt(s);
-    }
-    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
-    if ((tid & 31) == 0 && s >= 0.0) atomicMax(it.nmax, (unsigned long long)__double_as_longlong(s));
   }
 }
 
@@ -315,52 +201,13 @@ __global__ void __launch_bounds__(256) k_scale_tile(const FusedItem* __restrict_
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st) {
   if (n <= 0) return;
   const size_t sm = sizeof(double) * (size_t)max_m * (max_m + 1);
-  const int R = (max_m + 15) / 16;   // R4 = 4 R rows per lane group (the inverse)
-  if (!scale_by_inverse()) {   // no inverse: one lean instantiation for every m
-    set_smem_attr((const void*)k_chol<4, false>, sm);
-    launch_pdl(k_chol<4, false>, dim3(n), dim3(256), sm, st, d_items, status);
-    count_launch(1);
-    return;
-  }
-#define HS_CH(RR)                                               \
-  case RR:                                                      \
-    set_smem_attr((const void*)k_chol<4 * RR, true>, sm);       \
-    launch_pdl(k_chol<4 * RR, true>, dim3(n), dim3(256), sm, st, d_items, status); \
-    break;
-  switch (R) {
-    HS_CH(1) HS_CH(2) HS_CH(3) HS_CH(4) HS_CH(5) HS_CH(6) HS_CH(7)
-    default: fail(HS_E_INTERNAL, "launch_chol: m above CI_MAX_M");
-  }
-#undef HS_CH
+  set_smem_attr((const void*)k_chol, sm);
+  launch_pdl(k_chol, dim3(n), dim3(256), sm, st, d_items, status);
   count_launch(1);
-}
-
-// HS_SCALE_INVERSE=1: k_chol also forms G^{-1} and the tiles multiply by it (k_scale_gemm)
-// instead of the warp-synchronous forward substitution.  Measured on C2: the same total —
-// the inverse's m-step chain moves into k_chol (which then needs up to 255 registers, one
-// CTA per SM) and the tiles get cheaper by as much; the substitution is the default.
-bool scale_by_inverse() {
-  static const bool v = std::getenv("HS_SCALE_INVERSE") != nullptr;
-  return v;
 }
 
 void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st) {
   if (n <= 0) return;
-  if (scale_by_inverse()) {
-    const size_t sm = sizeof(double) * ((size_t)max_m * max_m + (size_t)max_m * ST_TW);
-#define HS_SG(RR)                                                     \
-  case RR:                                                            \
-    set_smem_attr((const void*)k_scale_gemm<RR>, sm);                 \
-    launch_pdl(k_scale_gemm<RR>, dim3(n), dim3(256), sm, st, d_items, d_segs); \
-    break;
-    switch ((max_m + 15) / 16) {
-      HS_SG(1) HS_SG(2) HS_SG(3) HS_SG(4) HS_SG(5) HS_SG(6) HS_SG(7)
-      default: fail(HS_E_INTERNAL, "launch_scale_tiles: m above CI_MAX_M");
-    }
-#undef HS_SG
-    count_launch(1);
-    return;
-  }
   const size_t sm = sizeof(double) * ((size_t)max_m * (max_m + 1) + (size_t)max_m * ST_TW);
   const int R = (max_m + 15) / 16;   // R4 = 4 R rows per lane group
 #define HS_ST(RR)                                                     \

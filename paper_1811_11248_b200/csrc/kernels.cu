@@ -377,333 +377,6 @@ __global__ void __launch_bounds__(256) k_form_T(const FormTItem* __restrict__ it
 }
 
 // ---------------------------------------------------------------------------------------
-// a3 + a4: column-pivoted Householder QR of the scaled block W = G^{-1}A_sw (columns
-// [0, kw) of B_s) truncated at the first step with max_i nu_i <= tau_s, tau_s = eps *
-// nu_max(0) (relative) or eps; pivot = lowest column index among nu_i >= (1-1e-10) nu_max.
-// The reflectors are applied to every column, so the n-columns [kw, kw+kn) receive U^T
-// (the sparsification E_s) in the same pass.  Columns are never swapped: on exit rows
-// [0, r) of B_s are [coarse-w | coarse-n] in canonical order and rows [r, m) of the
-// n-part are C = U_2^T G^{-1} A_sn.  Norms are recomputed exactly every step.
-// One CTA per cluster, a thread per column (coalesced along the row-major rows).
-constexpr int CPQR_THREADS = 512;
-
-__global__ void __launch_bounds__(CPQR_THREADS) k_cpqr(const CluItem* __restrict__ items, double eps, int relative,
-                                                       int32_t* __restrict__ rank_out) {
-  const CluItem it = items[blockIdx.x];
-  const int m = it.m, kw = it.kw, ncol = it.kw + it.kn, ld = it.ldB;
-  double* B = it.B;
-  double* nu = it.nu;
-  __shared__ double red[32];
-  __shared__ int redi[32];
-  __shared__ double v[MAX_M];
-  __shared__ double s_tau, s_beta;
-  if (m == 0 || kw == 0) {
-    if (threadIdx.x == 0) rank_out[blockIdx.x] = 0;
-    return;
-  }
-  // initial exact column norms
-  for (int i = threadIdx.x; i < kw; i += blockDim.x) {
-    double s = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double b = B[(int64_t)l * ld + i];
-      s += b * b;
-    }
-    nu[i] = sqrt(s);
-  }
-  // scale of the n part (noise floor of tau_s, reading R-floor)
-  double lmax_n = 0.0;
-  for (int i = kw + threadIdx.x; i < ncol; i += blockDim.x) {
-    double s = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double b = B[(int64_t)l * ld + i];
-      s += b * b;
-    }
-    lmax_n = fmax(lmax_n, sqrt(s));
-  }
-  const double row_n = block_max(lmax_n, red);
-  __syncthreads();
-  const int kmax = min(m, kw);
-  double tau_s = 0.0;
-  int r = kmax;
-  for (int j = 0; j < kmax; ++j) {
-    double lmax = -1.0;
-    for (int i = threadIdx.x; i < kw; i += blockDim.x) lmax = fmax(lmax, nu[i]);
-    const double numax = block_max(lmax, red);
-    if (j == 0) {
-      tau_s = relative ? eps * numax : eps;
-      if (relative && eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(numax, row_n));   // noise floor
-    }
-    if (!(numax > tau_s)) { r = j; break; }        // strict keep rule
-    const double thr = (1.0 - 1e-10) * numax;
-    int lmin = INT_MAX;
-    for (int i = threadIdx.x; i < kw; i += blockDim.x)
-      if (nu[i] >= thr && i < lmin) lmin = i;
-    const int p = block_min_int(lmin, redi);
-    // Householder vector from column p, rows j..m-1 (LAPACK dlarfg convention)
-    if (threadIdx.x < 32) {
-      double xs = 0.0;
-      for (int l = j + 1 + threadIdx.x; l < m; l += 32) {
-        const double b = B[(int64_t)l * ld + p];
-        xs += b * b;
-      }
-      xs = warp_sum(xs);
-      const double alpha = B[(int64_t)j * ld + p];
-      const double xnorm = sqrt(xs);
-      double tau, beta, den;
-      if (xnorm == 0.0) {
-        tau = 0.0; beta = alpha; den = 1.0;
-      } else {
-        const double h = sqrt(alpha * alpha + xnorm * xnorm);
-        beta = alpha >= 0.0 ? -h : h;
-        tau = (beta - alpha) / beta;
-        den = alpha - beta;
-      }
-      for (int l = j + 1 + threadIdx.x; l < m; l += 32) v[l] = (tau == 0.0) ? 0.0 : B[(int64_t)l * ld + p] / den;
-      if (threadIdx.x == 0) {
-        v[j] = 1.0;
-        s_tau = tau;
-        s_beta = beta;
-        it.tau[j] = tau;
-        it.piv[j] = p;
-      }
-    }
-    __syncthreads();
-    const double tau = s_tau;
-    // store v_j (column j of V, zeros above the diagonal)
-    for (int l = threadIdx.x; l < m; l += blockDim.x) it.V[(int64_t)j * m + l] = l < j ? 0.0 : v[l];
-    // apply H_j to every live column but the pivot, recompute the trailing norms
-    for (int i = threadIdx.x; i < ncol; i += blockDim.x) {
-      if (i == p) continue;
-      if (i < kw && nu[i] < 0.0) continue;          // already pivoted
-      double d = 0.0;
-      if (tau != 0.0)
-        for (int l = j; l < m; ++l) d += v[l] * B[(int64_t)l * ld + i];
-      const double td = tau * d;
-      double s = 0.0;
-      for (int l = j; l < m; ++l) {
-        double b = B[(int64_t)l * ld + i];
-        if (tau != 0.0) {
-          b -= td * v[l];
-          B[(int64_t)l * ld + i] = b;
-        }
-        if (l > j) s += b * b;
-      }
-      if (i < kw) nu[i] = sqrt(s);
-    }
-    if (threadIdx.x == 0) {
-      B[(int64_t)j * ld + p] = s_beta;
-      nu[p] = -1.0;
-    }
-    for (int l = j + 1 + threadIdx.x; l < m; l += blockDim.x) B[(int64_t)l * ld + p] = 0.0;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) rank_out[blockIdx.x] = r;
-}
-
-// ---------------------------------------------------------------------------------------
-// a3 + a4 on a thread-block cluster: the same CPQR (same decisions, same arithmetic per
-// column) with the columns of B_s split over CS CTAs.  Each CTA stages its column slice in
-// shared memory when it fits (else works on it in place in global memory).  Per step the
-// cluster exchanges only two scalars per CTA through distributed shared memory (the local
-// max norm, then the local lowest candidate index) and every CTA reads the pivot column
-// (m - j values) from its owner's shared memory, so all CTAs form the identical Householder
-// vector.  The owner finalises its pivot column one step later, after the next cluster
-// barrier guarantees nobody is still reading it.
-constexpr int CPQR2_THREADS = 256;
-constexpr size_t CPQR2_SMEM_BUDGET = 200 * 1024;
-
-__host__ __device__ __forceinline__ bool cpqr2_smem_mode(int m, int chunk) {
-  return ((size_t)m * chunk + chunk) * sizeof(double) <= CPQR2_SMEM_BUDGET;
-}
-
-__global__ void __launch_bounds__(CPQR2_THREADS) k_cpqr2(const CluItem* __restrict__ items, double eps, int relative,
-                                                         int32_t* __restrict__ rank_out) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  const int CS = (int)cl.num_blocks();
-  const int crank = (int)cl.block_rank();
-  const int item = blockIdx.x / CS;
-  const CluItem it = items[item];
-  const int m = it.m, kw = it.kw, ncol = it.kw + it.kn, ld = it.ldB;
-  extern __shared__ double dsm[];
-  __shared__ double s_val[2];
-  __shared__ int s_idx[2];
-  __shared__ double s_rown;
-  __shared__ double vloc[MAX_M];
-  __shared__ double red[32];
-  __shared__ int redi[32];
-  __shared__ double bc_d, bc_rown, bc_beta;
-  __shared__ int bc_i;
-  if (m == 0 || kw == 0) {   // uniform over the cluster: nobody reaches a cluster barrier
-    if (crank == 0 && threadIdx.x == 0) rank_out[item] = 0;
-    return;
-  }
-  const int chunk = (ncol + CS - 1) / CS;
-  const int c_lo = crank * chunk;
-  const int nloc = max(0, min(ncol, c_lo + chunk) - c_lo);
-  const bool sm = cpqr2_smem_mode(m, chunk);
-  double* nu = dsm;                                   // chunk entries
-  double* W = sm ? dsm + chunk : it.B + c_lo;         // local columns
-  const int ldw = sm ? chunk : ld;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (sm)
-    for (int l = 0; l < m; ++l)
-      for (int c = tid; c < nloc; c += blockDim.x) W[l * ldw + c] = it.B[(int64_t)l * ld + c_lo + c];
-  __syncthreads();
-  double lrow = 0.0;
-  for (int c = tid; c < nloc; c += blockDim.x) {
-    double s = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double b = W[(int64_t)l * ldw + c];
-      s += b * b;
-    }
-    if (c_lo + c < kw) nu[c] = sqrt(s);
-    else lrow = fmax(lrow, sqrt(s));
-  }
-  lrow = block_max(lrow, red);
-  if (tid == 0) s_rown = lrow;
-  __syncthreads();
-  const int kmax = min(m, kw);
-  double tau_s = 0.0;
-  int r = kmax;
-  int fix_p = -1, fix_j = 0;       // deferred finalisation of this CTA's last pivot column
-  double fix_beta = 0.0;
-  for (int j = 0; j < kmax; ++j) {
-    const int buf = j & 1;
-    double lmax = -1.0;
-    for (int c = tid; c < nloc; c += blockDim.x)
-      if (c_lo + c < kw) lmax = fmax(lmax, nu[c]);
-    lmax = block_max(lmax, red);
-    if (tid == 0) s_val[buf] = lmax;
-    cl.sync();
-    if (wid == 0) {
-      double v = -1.0, rn = 0.0;
-      if (lane < CS) {
-        v = *cl.map_shared_rank(&s_val[buf], lane);
-        if (j == 0) rn = *cl.map_shared_rank(&s_rown, lane);
-      }
-      v = warp_max(v);
-      rn = warp_max(rn);
-      if (lane == 0) {
-        bc_d = v;
-        if (j == 0) bc_rown = rn;
-      }
-    }
-    // the previous pivot column is no longer read by anyone: finalise it
-    if (fix_p >= 0) {
-      for (int l = fix_j + tid; l < m; l += blockDim.x) W[(int64_t)l * ldw + fix_p] = (l == fix_j) ? fix_beta : 0.0;
-      fix_p = -1;
-    }
-    __syncthreads();
-    const double numax = bc_d;
-    if (j == 0) {
-      tau_s = relative ? eps * numax : eps;
-      if (relative && eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(numax, bc_rown));
-    }
-    if (!(numax > tau_s)) {
-      r = j;
-      break;
-    }
-    const double thr = (1.0 - 1e-10) * numax;
-    int lmin = INT_MAX;
-    for (int c = tid; c < nloc; c += blockDim.x)
-      if (c_lo + c < kw && nu[c] >= thr && c_lo + c < lmin) lmin = c_lo + c;
-    lmin = block_min_int(lmin, redi);
-    if (tid == 0) s_idx[buf] = lmin;
-    cl.sync();
-    if (wid == 0) {
-      int v = INT_MAX;
-      if (lane < CS) v = *cl.map_shared_rank(&s_idx[buf], lane);
-      v = warp_min_int(v);
-      if (lane == 0) bc_i = v;
-    }
-    __syncthreads();
-    const int p = bc_i;
-    const int owner = p / chunk, ploc = p - owner * chunk;
-    // Householder vector from the pivot column (rows j..m-1), identical in every CTA
-    if (wid == 0) {
-      const double* col;
-      int64_t cld;
-      if (sm) {
-        col = cl.map_shared_rank(dsm + chunk, owner) + ploc;
-        cld = chunk;
-      } else {
-        col = it.B + p;
-        cld = ld;
-      }
-      double xs = 0.0;
-      for (int l = j + 1 + lane; l < m; l += 32) {
-        const double b = col[(int64_t)l * cld];
-        vloc[l] = b;
-        xs += b * b;
-      }
-      xs = warp_sum(xs);
-      const double alpha = col[(int64_t)j * cld];
-      const double xnorm = sqrt(xs);
-      double tau, beta, den;
-      if (xnorm == 0.0) {
-        tau = 0.0; beta = alpha; den = 1.0;
-      } else {
-        const double h = sqrt(alpha * alpha + xnorm * xnorm);
-        beta = alpha >= 0.0 ? -h : h;
-        tau = (beta - alpha) / beta;
-        den = alpha - beta;
-      }
-      for (int l = j + 1 + lane; l < m; l += 32) vloc[l] = (tau == 0.0) ? 0.0 : vloc[l] / den;
-      if (lane == 0) {
-        vloc[j] = 1.0;
-        bc_d = tau;
-        bc_beta = beta;
-        if (crank == 0) {
-          it.tau[j] = tau;
-          it.piv[j] = p;
-        }
-      }
-    }
-    __syncthreads();
-    const double tau = bc_d;
-    const double beta = bc_beta;
-    if (crank == 0)
-      for (int l = tid; l < m; l += blockDim.x) it.V[(int64_t)j * m + l] = l < j ? 0.0 : vloc[l];
-    if (crank == owner) {
-      if (tid == 0) nu[ploc] = -1.0;
-      fix_p = ploc;
-      fix_j = j;
-      fix_beta = beta;
-    }
-    __syncthreads();
-    for (int c = tid; c < nloc; c += blockDim.x) {
-      if (crank == owner && c == ploc) continue;
-      if (c_lo + c < kw && nu[c] < 0.0) continue;
-      double* Wc = W + c;
-      double d = 0.0;
-      if (tau != 0.0)
-#pragma unroll 8
-        for (int l = j; l < m; ++l) d += vloc[l] * Wc[(int64_t)l * ldw];
-      const double td = tau * d;
-      double s = 0.0;
-#pragma unroll 8
-      for (int l = j; l < m; ++l) {
-        double b = Wc[(int64_t)l * ldw];
-        if (tau != 0.0) {
-          b -= td * vloc[l];
-          Wc[(int64_t)l * ldw] = b;
-        }
-        if (l > j) s += b * b;
-      }
-      if (c_lo + c < kw) nu[c] = sqrt(s);
-    }
-    __syncthreads();
-  }
-  cl.sync();   // every CTA is done reading the last pivot column
-  if (fix_p >= 0)
-    for (int l = fix_j + tid; l < m; l += blockDim.x) W[(int64_t)l * ldw + fix_p] = (l == fix_j) ? fix_beta : 0.0;
-  __syncthreads();
-  if (sm)
-    for (int l = 0; l < m; ++l)
-      for (int c = tid; c < nloc; c += blockDim.x) it.B[(int64_t)l * ld + c_lo + c] = W[l * ldw + c];
-  if (crank == 0 && tid == 0) rank_out[item] = r;
-}
 
 // ---------------------------------------------------------------------------------------
 // a5: Schur update tiles, FP64 FMA (64 x 64 tile, 256 threads, 4 x 4 per thread),
@@ -1129,68 +802,11 @@ void launch_form_T(const FormTItem* d_items, int n, int max_m, cudaStream_t st) 
   k_form_T<<<n * tiles, 256, sm, st>>>(d_items, tiles);
   count_launch(1);
 }
-void launch_cpqr(const CluItem* d_items, int n, double eps, int relative, int32_t* d_rank, cudaStream_t st) {
-  if (n <= 0) return;
-  k_cpqr<<<n, CPQR_THREADS, 0, st>>>(d_items, eps, relative, d_rank);
-  count_launch(1);
-}
 void launch_schur(const SchurTile* d_tiles, const SchurContrib* d_con, int n, cudaStream_t st) {
   if (n <= 0) return;
   k_schur<<<n, 256, 0, st>>>(d_tiles, d_con);
   count_launch(1);
 }
-int launch_cpqr2(const CluItem* d_items, const std::vector<CluItem>& h_items, double eps, int relative,
-                 int32_t* d_rank, cudaStream_t st) {
-  const int n = (int)h_items.size();
-  if (n <= 0) return 0;
-  int maxcol = 0;
-  for (const auto& it : h_items) maxcol = std::max(maxcol, it.kw + it.kn);
-  static std::once_flag once;
-  std::call_once(once, [] {
-    HS_CUDA(cudaFuncSetAttribute((const void*)k_cpqr2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    HS_CUDA(cudaFuncSetAttribute((const void*)k_cpqr2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)CPQR2_SMEM_BUDGET + 8192));
-  });
-  auto smem_for = [&](int cs) {
-    size_t smem = 8;
-    for (const auto& it : h_items) {
-      if (it.m == 0 || it.kw == 0) continue;
-      const int chunk = (it.kw + it.kn + cs - 1) / cs;
-      const size_t need = (cpqr2_smem_mode(it.m, chunk) ? ((size_t)it.m * chunk + chunk) : (size_t)chunk) * sizeof(double);
-      smem = std::max(smem, need);
-    }
-    return smem;
-  };
-  // The per-step critical path is each CTA's column loop, so split the columns as far
-  // as the barrier/DSMEM overhead allows (>= 64 columns per CTA), up to 16 CTAs.
-  int CS = 1;
-  while (CS < 16 && maxcol / (2 * CS) >= 64) CS *= 2;
-  for (;;) {
-    const size_t smem = smem_for(CS);
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(n * CS);
-    cfg.blockDim = dim3(CPQR2_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (CS > 1 && (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_cpqr2, &cfg) != cudaSuccess || nclusters == 0)) {
-      cudaGetLastError();
-      CS /= 2;
-      continue;
-    }
-    HS_CUDA(cudaLaunchKernelEx(&cfg, k_cpqr2, d_items, eps, relative, d_rank));
-    count_launch(1);
-    return CS;
-  }
-}
-
 // Level pair tables: a warp per (cluster s, neighbour a); lanes over b <= a look the block
 // (q_a, q_b) up in the level's directory.  Pattern-only, once per level.
 __global__ void __launch_bounds__(256) k_level_pairs(const int64_t* __restrict__ hptr, const int32_t* __restrict__ hq,
