@@ -177,24 +177,38 @@ def test_gmres_parity(H, handle, name, gen, kw):
 
 def test_analyze_once_factor_many(H, handle):
     """NEXT f2 / P:763 (Newton and continuation produce a sequence of systems with one
-    pattern): re-factoring new values on the same analysis (cached pattern and scatter map)
+    pattern) on the weak-scaling family (gen_family: the C4 operator at 6 element layers, the
+    paper's Table `ilu` family shape): re-factoring new values on the same analysis (cached
+    pattern and scatter map) matches the ORACLE on those values (ranks, pivots, apply, PCG),
     equals a fresh analysis bit for bit, and re-factoring the same values is deterministic.
     (Scaling A by alpha is NOT a symmetry of the method: the coarse DOFs live in the
     G-scaled space with diagonal I_r, so their couplings scale by sqrt(alpha) while
     unprocessed blocks scale by alpha; the oracle shows the same.)"""
-    p = gen_stokes_q1(12, 10, 5, leaf_columns=2)
-    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=2)
-    f1 = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    import copy
+    from problems import gen_family
+    p = gen_family(6, 0)
+    an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size, leaf_columns=p.leaf_columns)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=p.leaf_columns)
+    f1 = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
     # a symmetric perturbation: scale row i and column i by d_i (D A D stays SPD)
     d = 1.0 + 0.2 * np.sin(np.arange(p.n))
     rows = np.repeat(np.arange(p.n), np.diff(p.rowptr))
-    vals2 = p.vals * d[rows] * d[p.colind]
-    f2 = H.hs_factor_create(handle, a, vals2, eps=1e-2)
-    a_new = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=2)
-    f3 = H.hs_factor_create(handle, a_new, vals2, eps=1e-2)
+    p2 = copy.copy(p)
+    p2.vals = p.vals * d[rows] * d[p.colind]
+    f2 = H.hs_factor_create(handle, a, p2.vals, eps=p.eps)
+    for q, f in ((p, f1), (p2, f2)):   # both factors of the sequence against the oracle
+        fac, flagged, injected, nelim = oracle_with_injection(H, f, an, q, q.eps)
+        assert injected <= max(2, nelim // 200)
+        _apply_parity(H, f, fac, q.n)
+        xo, ro = opcg(q.to_scipy(), q.b, lambda r: oapply(fac, r), tol=q.tol)
+        xg, rg = H.hs_pcg(f, q.b, tol=q.tol)
+        assert abs(rg["iters"] - ro.iters) <= 1
+        assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-8
+    a_new = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=p.leaf_columns)
+    f3 = H.hs_factor_create(handle, a_new, p2.vals, eps=p.eps)
     v = np.random.default_rng(4).standard_normal(p.n)
     assert np.array_equal(H.hs_apply(f2, v), H.hs_apply(f3, v))
-    f4 = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+    f4 = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
     assert np.array_equal(H.hs_apply(f4, v), H.hs_apply(f1, v))
 
 
