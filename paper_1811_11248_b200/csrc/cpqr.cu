@@ -55,7 +55,9 @@ __host__ __device__ __forceinline__ int cq_group(int m, int MR) {
 // offsets i G from its column base.
 __host__ __device__ __forceinline__ int cq_ldm(int m, int G) {
   int l = m < 1 ? 1 : m;
-  if (G >= 16) return (l + 1) & ~1;
+  // G >= 16: a half-warp reads 16 consecutive rows of one column (conflict-free for any
+  // stride); an odd stride also keeps the staging transpose's column-strided stores apart
+  if (G >= 16) return l | 1;
   const int rem = ((l - G) % 16 + 16) % 16;
   return l + (rem ? 16 - rem : 0);
 }
@@ -211,22 +213,25 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // ---- stage the w-slice (transpose to column-major; coalesced global reads) ----------
-  {
-    const int tot = m * nw;
+  if (nw > 0) {   // thread (row rr + k rpp, column cc): coalesced row segments, no division per element
     const double* __restrict__ src = it.B + w_lo;
-    for (int e0 = tid; e0 < tot; e0 += 4 * CQ_THREADS) {
-      double v[4];
+    const int rpp = nw <= CQ_THREADS ? CQ_THREADS / nw : 1;   // rows per pass
+    const int cc0 = nw <= CQ_THREADS ? tid % nw : tid, rr = nw <= CQ_THREADS ? tid / nw : 0;
+    if (rr < rpp)
+      for (int cc = cc0; cc < nw; cc += CQ_THREADS)
+        for (int l0 = rr; l0 < m; l0 += 4 * rpp) {
+          double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * CQ_THREADS;
-        v[u] = e < tot ? src[(size_t)(e / nw) * ld + (e % nw)] : 0.0;
-      }
+          for (int u = 0; u < 4; ++u) {
+            const int l = l0 + u * rpp;
+            v[u] = l < m ? src[(size_t)l * ld + cc] : 0.0;
+          }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * CQ_THREADS;
-        if (e < tot) W[(e % nw) * ldm + e / nw] = v[u];
-      }
-    }
+          for (int u = 0; u < 4; ++u) {
+            const int l = l0 + u * rpp;
+            if (l < m) W[(size_t)cc * ldm + l] = v[u];
+          }
+        }
   }
   __syncthreads();
   CQ_TR(1);

@@ -81,6 +81,7 @@ struct CluItem {
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
   const double* G;
+  const double* Ginv;  // G^{-1} when k_chol formed it (then no substitution here), else null
   const double* V;
   const double* tau;
   double* T;
@@ -92,6 +93,8 @@ struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operato
 struct FusedItem {
   const double* Ass;          // diagonal block in the store (lower, row-major, ld lda)
   double* G;                  // workspace G_s
+  double* Ginv;               // workspace G_s^{-1} (lower, row-major ld m): k_chol writes it, the
+                              // scaling (DMMA product) and the apply operator T_s read it
   double* B;                  // workspace B_s (m x ldB)
   unsigned long long* nmax;   // R-floor slot
   int32_t m, lda, ldB, kw;

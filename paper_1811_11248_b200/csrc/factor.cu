@@ -976,7 +976,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         const int32_t s = Bo[bi];
         const int64_t m = live[s], kn = L.kn[s], kw = L.kw[s];
         wo[bi] = wsz;
-        wsz += 2 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
+        wsz += 3 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
       }
       double* ws = nb ? (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4)) : nullptr;
       // the batch's C_s region (dpatch: m rows each, compacted once the ranks are known)
@@ -1012,6 +1012,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         L.tau[s] = w0 + 2 * (int64_t)m * m;
         L.nu[s] = L.tau[s] + ((m + 3) & ~3);
         L.B[s] = L.nu[s] + ((kw + 3) & ~3);   // 32-byte aligned
+        double* ginv = L.B[s] + (((int64_t)m * (kn + kw) + 3) & ~int64_t(3));   // G^{-1} (fused path)
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
         it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
@@ -1045,7 +1046,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           // segments are in column order: each tile takes the run of segments overlapping it
           int32_t sb = seg0;
           const int32_t se = (int32_t)fseg.size();
-          fci.push_back(FusedItem{pss, L.G[s], L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+          fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
           if (dwb) {
             seg0v[bi] = seg0;
             it.nseg = se - seg0;
@@ -1063,7 +1064,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
             int32_t sf = sb;
             while (sf < se && fseg[sf].col < c0 + nc) ++sf;
-            fz.push_back(FusedItem{pss, L.G[s], L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
+            fz.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
           }
         } else {
           for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
@@ -1168,7 +1169,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         Pend pd{s, (int32_t)k, mine, -1, -1, -1, -1, wb.size(), wb.size()};
         if (mine) {
           pd.ft = (int64_t)ft.size();
-          ft.push_back(FormTItem{L.G[s], L.V[s], L.tau[s], L.T[s], m, 0});
+          const double* gi = fused ? L.B[s] + (((int64_t)m * ldB + 3) & ~int64_t(3)) : nullptr;   // k_chol's G^{-1}
+          ft.push_back(FormTItem{L.G[s], gi, L.V[s], L.tau[s], L.T[s], m, 0});
           ft_max_m = std::max(ft_max_m, m);
         }
         // neighbour column offsets inside the n-part

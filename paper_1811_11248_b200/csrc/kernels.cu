@@ -342,14 +342,22 @@ __global__ void __launch_bounds__(256) k_form_T(const FormTItem* __restrict__ it
     x = sm;
   }
   __shared__ double red[8][64];
-  for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
-    const int i = e / TW, c = e % TW;
-    x[e] = (c < nc && i == c0 + c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
   const int c = threadIdx.x % TW, grp = threadIdx.x / TW, ngrp = blockDim.x / TW;
+  if (it.Ginv) {   // G^{-1} formed by k_chol: X = its columns [c0, c0 + nc)
+    for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+      const int i = e / TW, cc = e % TW;
+      x[e] = cc < nc ? it.Ginv[(int64_t)i * m + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+  } else {
+    for (int e = threadIdx.x; e < m * TW; e += blockDim.x) {
+      const int i = e / TW, cc = e % TW;
+      x[e] = (cc < nc && i == c0 + cc) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+  }
   // X <- G^{-1} X  (rows above c0 stay zero: start the substitution at row c0)
-  for (int i = c0; i < m; ++i) {
+  for (int i = it.Ginv ? m : c0; i < m; ++i) {
     if (grp == 0) x[i * TW + c] /= g[(int64_t)i * ldg + i];
     __syncthreads();
     const double xi = x[i * TW + c];
