@@ -195,3 +195,173 @@ def assemble_factor(an: Analysis, parts, top, eps=1e-2, relative=True) -> Factor
         live1.append([allm[s].r for s in range(lev.nclus)])
     top_sizes, L = top
     return Factor(an, eps, relative, elims, live0, live1, top_sizes, L)
+
+
+# ---- distributed Algorithm 2 and PCG (SURVEY §8(e) "Apply", "PCG") ---------------------------
+# Owner computes: every rank applies the elimination records of the clusters it eliminated
+# (no gather of the factor); the vector lives in per-cluster segments at their owners.
+#   forward, per batch: owners form y_s <- U^T G^{-1} y_s and the contributions C_s[:, q]^T y_f;
+#     interior (phase-I) contributions stay local (O2.8); after each phase-II batch the
+#     contributions are exchanged and every owner subtracts the ones for its clusters in
+#     source order (no batch member is another's target, so this IS the sequential order);
+#   top: rank 0 gathers the top segments, solves with L L^T and scatters the result;
+#   backward, per batch in reverse: owners of a phase-II batch first receive the current x
+#     segments of their remote neighbours, then x_f = y_f - sum_q C[:, q] x_q and
+#     x_s = G^{-T} U [x_c; x_f] (Alg. 2).
+# PCG: the iterate, residual and search direction are distributed the same way (the DOFs
+# of owned leaves); the SpMV of an owned row needs the x entries of its ghost columns (halo
+# exchange), each dot product is a sum of per-rank partial sums (all-reduce).
+
+def owned_leaves(an: Analysis, rank: int, world: int):
+    nleaf = an.leaf_off.shape[0] - 1
+    lvl = 0 if an.levels else an.L_top
+    return [c for c in range(nleaf) if owner(an, lvl, c, world) == rank]
+
+
+def _own_rows(an, rank, world):
+    return np.concatenate([np.arange(an.leaf_off[c], an.leaf_off[c + 1]) for c in owned_leaves(an, rank, world)]
+                          or [np.zeros(0, dtype=np.int64)]).astype(np.int64)
+
+
+def apply_dist(an: Analysis, mine, top, y0, comm, rank: int, world: int):
+    """x = M^{-1} b for the distributed factor.  y0: {leaf: b segment (permuted order)} for
+    the leaves this rank owns; returns {leaf: x segment} for the same leaves."""
+    import scipy.linalg as sla
+    from .dense import apply_Qt, apply_Q
+    y = {c: np.array(v, dtype=np.float64) for c, v in y0.items()}
+    fine = {}
+    for l, lev in enumerate(an.levels):
+        for bi, B in enumerate(lev.batches):
+            out = []
+            for s in B:
+                e = mine[l].get(s)
+                if e is None:
+                    continue
+                t = sla.solve_triangular(e.G, y[s], lower=True) if e.m else y[s].copy()
+                t = apply_Qt(e.V, e.tau, t)
+                yf = t[e.r:]
+                fine[(l, s)] = yf
+                y[s] = t[:e.r]
+                o = 0
+                for q, k in zip(e.nlist, e.nsz):
+                    out.append((s, q, e.C[:, o:o + k].T @ yf))
+                    o += k
+            if bi >= lev.nphase1:   # phase II: contributions travel to their targets' owners
+                out = [m for part in comm.all_gather(out) for m in part]
+            for s, q, v in sorted(out, key=lambda m: m[0]):
+                if owner(an, l, q, world) == rank:
+                    y[q] = y[q] - v
+        nP = lev.nclus // 2
+        y = {P: np.concatenate([y[2 * P], y[2 * P + 1]]) for P in range(nP) if owner(an, l + 1, P, world) == rank}
+    # top (rank 0)
+    parts = comm.all_gather(y)
+    ntop = 1 << (an.D - an.L_top)
+    xtop = None
+    if rank == 0:
+        segs = {}
+        for pt in parts:
+            segs.update(pt)
+        yt = np.concatenate([segs[c] for c in range(ntop)]) if ntop else np.zeros(0)
+        top_sizes, L = top
+        if yt.shape[0]:
+            z = sla.solve_triangular(L, yt, lower=True)
+            xt = sla.solve_triangular(L, z, lower=True, trans="T")
+        else:
+            xt = yt
+        o = np.concatenate([[0], np.cumsum([segs[c].shape[0] for c in range(ntop)])]).astype(int)
+        xtop = {c: xt[o[c]:o[c + 1]] for c in range(ntop)}
+    xtop = comm.all_gather(xtop)[0]
+    x = {c: v for c, v in xtop.items() if owner(an, an.L_top, c, world) == rank}
+    for l in reversed(range(len(an.levels))):
+        lev = an.levels[l]
+        xs = {}
+        for P, v in x.items():   # children of an owned parent are owned (same subdomain)
+            r0 = mine[l][2 * P].r if 2 * P in mine[l] else 0
+            xs[2 * P] = v[:r0]
+            xs[2 * P + 1] = v[r0:]
+        x = xs
+        for bi in reversed(range(len(lev.batches))):
+            B = lev.batches[bi]
+            view = x
+            if bi >= lev.nphase1:   # the remote neighbours' current segments (halo of the sweep)
+                view = {}
+                for pt in comm.all_gather(x):
+                    view.update(pt)
+            for s in reversed(B):
+                e = mine[l].get(s)
+                if e is None:
+                    continue
+                xf = fine[(l, s)].copy()
+                o = 0
+                for q, k in zip(e.nlist, e.nsz):
+                    assert view[q].shape[0] == k
+                    xf = xf - e.C[:, o:o + k] @ view[q]
+                    o += k
+                t = apply_Q(e.V, e.tau, np.concatenate([x[s], xf]))
+                x[s] = sla.solve_triangular(e.G, t, lower=True, trans="T") if e.m else t
+    return x
+
+
+def pcg_dist(an: Analysis, mine, top, rowptr, colind, vals, b, comm, rank: int, world: int, tol=1e-8, maxit=1000):
+    """O5 PCG on the distributed factor.  b: the full right-hand side (original order; each
+    rank reads its own rows).  Returns (x full vector assembled on every rank, iterations,
+    relative residual history)."""
+    import scipy.sparse as sp
+    n = an.n
+    A = sp.csr_matrix((vals, colind, rowptr), shape=(n, n))
+    Ap = A[an.perm][:, an.perm].tocsr()                  # permuted: owned leaves are row ranges
+    rows = _own_rows(an, rank, world)
+    A_loc = Ap[rows]
+    ghost = np.setdiff1d(np.unique(A_loc.indices), rows)  # halo: columns owned elsewhere
+    leaves = owned_leaves(an, rank, world)
+
+    def spmv(v_loc):   # halo exchange: every rank publishes its owned entries, keeps only its ghosts
+        pub = np.zeros(n)
+        for rr, vv in comm.all_gather((rows, v_loc)):
+            pub[rr] = vv
+        full = np.zeros(n)          # owned + ghost entries only: the halo suffices for the owned rows
+        full[rows] = v_loc
+        full[ghost] = pub[ghost]
+        return A_loc @ full
+
+    def dot(u, v):     # all-reduce of per-rank partial sums, summed in rank order
+        return float(sum(comm.all_gather(float(u @ v))))
+
+    def prec(r_loc):
+        segs, o = {}, 0
+        for c in leaves:
+            k = an.leaf_off[c + 1] - an.leaf_off[c]
+            segs[c] = r_loc[o:o + k]
+            o += k
+        xs = apply_dist(an, mine, top, segs, comm, rank, world)
+        return np.concatenate([xs[c] for c in leaves]) if leaves else np.zeros(0)
+
+    bp = np.asarray(b, dtype=np.float64)[an.perm][rows]
+    x = np.zeros_like(bp)
+    r = bp.copy()
+    nb = np.sqrt(dot(bp, bp))
+    hist = [1.0]
+    z = prec(r)
+    p = z.copy()
+    rho = dot(r, z)
+    k = 0
+    while k < maxit:
+        k += 1
+        q = spmv(p)
+        alpha = rho / dot(p, q)
+        x += alpha * p
+        r -= alpha * q
+        rel = np.sqrt(dot(r, r)) / nb
+        hist.append(rel)
+        if rel <= tol:
+            break
+        z = prec(r)
+        rho2 = dot(r, z)
+        p = z + (rho2 / rho) * p
+        rho = rho2
+    full = np.zeros(n)
+    for rr, vv in comm.all_gather((rows, x)):
+        full[rr] = vv
+    out = np.empty(n)
+    out[an.perm] = full
+    return out, k, hist

@@ -152,3 +152,61 @@ def test_library_plan_matches_decomposition(name, world):
         path = os.path.join(td, "ok.npy")
         mp.spawn(_plan_worker, args=(world, _free_port(), name, path), nprocs=world, join=True)
         assert os.path.exists(path)
+
+
+def _pcg_worker(rank, world, port, name, eps, path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.dist import apply_dist, pcg_dist, owned_leaves
+        p = CASES[name]()
+        an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+        comm = _Gloo(world)
+        mine, top = factor_dist(an, p.rowptr, p.colind, p.vals, comm, rank, world, eps=eps)
+        # distributed apply of a random vector, segments at their owners
+        v = np.random.default_rng(1).standard_normal(p.n)[an.perm]
+        segs = {c: v[an.leaf_off[c]:an.leaf_off[c + 1]] for c in owned_leaves(an, rank, world)}
+        xs = apply_dist(an, mine, top, segs, comm, rank, world)
+        got = comm.all_gather(xs)
+        x, its, hist = pcg_dist(an, mine, top, p.rowptr, p.colind, p.vals, p.b, comm, rank, world, tol=p.tol)
+        if rank == 0:
+            full = np.zeros(p.n)
+            for part in got:
+                for c, seg in part.items():
+                    full[an.leaf_off[c]:an.leaf_off[c + 1]] = seg
+            out = np.empty(p.n)
+            out[an.perm] = full
+            np.save(path, out)
+            np.save(path + ".pcg.npy", x)
+            np.save(path + ".its.npy", np.array([its] + hist))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["C1", "3d-16"])
+def test_distributed_oracle_apply_and_pcg(name, world):
+    """The distributed solve of SURVEY §8(e) (owner-computes Algorithm 2 with phase-II
+    contribution exchanges and the top on rank 0; PCG with a halo SpMV and all-reduced dots)
+    reproduces the sequential oracle: apply to 1e-13, PCG solution to 1e-12 with the same
+    iteration count and residual history."""
+    from oracle.solve import pcg as opcg
+    eps = 1e-2
+    p = CASES[name]()
+    an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                 leaf_columns=p.leaf_columns)
+    seq = factor(an, p.rowptr, p.colind, p.vals, eps=eps)
+    ref = oapply(seq, np.random.default_rng(1).standard_normal(p.n))
+    xo, ro = opcg(p.to_scipy(), p.b, lambda r: oapply(seq, r), tol=p.tol)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "x.npy")
+        mp.spawn(_pcg_worker, args=(world, _free_port(), name, eps, path), nprocs=world, join=True)
+        got = np.load(path)
+        xg = np.load(path + ".pcg.npy")
+        its = np.load(path + ".its.npy")
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    assert int(its[0]) == ro.iters
+    assert np.allclose(its[1:], ro.history, rtol=1e-9, atol=1e-14)
+    assert np.linalg.norm(xg - xo) <= 1e-12 * np.linalg.norm(xo)
