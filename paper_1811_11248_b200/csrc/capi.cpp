@@ -419,15 +419,14 @@ static void io_in(hs_factor f, const double* v, double* dtmp, int32_t on_device,
 hs_status hs_apply(hs_factor f, const double* b, double* x, int32_t on_device) {
   return guarded(f ? f->h : nullptr, [&] {
     if (!f || !b || !x) hs::fail(HS_E_INVALID_ARG, "hs_apply: NULL argument");
-    if (f->h->world > 1 && f->h->rank != 0)
-      hs::fail(HS_E_UNSUPPORTED, "hs_apply: the multi-GPU factor is applied on rank 0 (records gathered there)");
     require_device(f->h);
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
     double* din = nullptr;
     din = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, b, din, on_device, st);
-    hs::apply(f, din, din);
+    if (f->ds) hs::dist_apply(f, din, din);   // world > 1: collective, every rank passes b and gets x
+    else hs::apply(f, din, din);
     HS_CUDA(cudaMemcpyAsync(x, din, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     f->h->cache.free(din);
     HS_CUDA(cudaStreamSynchronize(st));
@@ -444,7 +443,8 @@ hs_status hs_spmv(hs_factor f, const double* x, double* y, int32_t on_device) {
     dx = (double*)f->h->cache.alloc(sizeof(double) * n);
     dy = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, x, dx, on_device, st);
-    hs::spmv(f, dx, dy);
+    if (f->ds) hs::dist_spmv_global(f, dx, dy);
+    else hs::spmv(f, dx, dy);
     HS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     f->h->cache.free(dx);
     f->h->cache.free(dy);
@@ -460,8 +460,6 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
   const hs_status s = guarded(f ? f->h : nullptr, [&] {
     if (!f || !b || !x || !rep) hs::fail(HS_E_INVALID_ARG, "hs_pcg: NULL argument");
     if (!(tol >= 0) || maxit < 0) hs::fail(HS_E_INVALID_ARG, "hs_pcg: bad tol/maxit");
-    if (f->h->world > 1 && f->h->rank != 0)
-      hs::fail(HS_E_UNSUPPORTED, "hs_pcg: the multi-GPU factor is solved on rank 0 (records gathered there)");
     require_device(f->h);
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;
@@ -470,7 +468,8 @@ hs_status hs_pcg(hs_factor f, const double* b, double* x, double tol, int32_t ma
     dx = (double*)f->h->cache.alloc(sizeof(double) * n);
     io_in(f, b, db, on_device, st);
     try {
-      hs::pcg(f, db, dx, tol, maxit, rep);
+      if (f->ds) hs::dist_pcg(f, db, dx, tol, maxit, rep);   // world > 1: collective
+      else hs::pcg(f, db, dx, tol, maxit, rep);
     } catch (const hs::Error& e) {
       s_inner = e.status;
       if (e.status != HS_E_NOT_CONVERGED) {
@@ -494,8 +493,7 @@ hs_status hs_gmres(hs_factor f, const double* b, double* x, double tol, int32_t 
   const hs_status s = guarded(f ? f->h : nullptr, [&] {
     if (!f || !b || !x || !rep) hs::fail(HS_E_INVALID_ARG, "hs_gmres: NULL argument");
     if (!(tol >= 0) || maxit < 0 || restart < 1) hs::fail(HS_E_INVALID_ARG, "hs_gmres: bad tol/restart/maxit");
-    if (f->h->world > 1 && f->h->rank != 0)
-      hs::fail(HS_E_UNSUPPORTED, "hs_gmres: the multi-GPU factor is solved on rank 0 (records gathered there)");
+    if (f->ds) hs::fail(HS_E_UNSUPPORTED, "hs_gmres: the distributed solve runs PCG (hs_pcg)");
     require_device(f->h);
     cudaStream_t st = f->h->stream;
     const int64_t n = f->an->n;

@@ -80,6 +80,7 @@ struct Comm {
   int world = 1, rank = 0;
   virtual ~Comm() {}
   virtual void allreduce_sum_i32(int32_t* d_buf, size_t n, cudaStream_t st) = 0;
+  virtual void allreduce_sum_f64(double* d_buf, size_t n, cudaStream_t st) = 0;
   virtual void group_start() = 0;
   virtual void group_end(cudaStream_t st) = 0;
   virtual void send(const double* d, size_t n, int peer, cudaStream_t st) = 0;
@@ -95,6 +96,9 @@ struct NcclComm : Comm {
   }
   void allreduce_sum_i32(int32_t* d_buf, size_t n, cudaStream_t st) override {
     if (n) check(nccl().AllReduce(d_buf, d_buf, n, ncclInt32, ncclSum, c, st), "ncclAllReduce");
+  }
+  void allreduce_sum_f64(double* d_buf, size_t n, cudaStream_t st) override {
+    if (n) check(nccl().AllReduce(d_buf, d_buf, n, ncclFloat64, ncclSum, c, st), "ncclAllReduce");
   }
   void group_start() override { check(nccl().GroupStart(), "ncclGroupStart"); }
   void group_end(cudaStream_t) override { check(nccl().GroupEnd(), "ncclGroupEnd"); }
@@ -128,7 +132,8 @@ struct LoopWorld {
   std::vector<std::vector<Msg>> sends, recvs;   // per rank, posted in the current group
   std::vector<cudaEvent_t> ev_send, ev_done;    // per rank
   std::vector<std::vector<int32_t>> red;        // per rank all-reduce contributions
-  explicit LoopWorld(int w) : world(w), sends(w), recvs(w), ev_send(w, nullptr), ev_done(w, nullptr), red(w) {
+  std::vector<std::vector<double>> redf;
+  explicit LoopWorld(int w) : world(w), sends(w), recvs(w), ev_send(w, nullptr), ev_done(w, nullptr), red(w), redf(w) {
     for (int r = 0; r < w; ++r) {
       HS_CUDA(cudaEventCreateWithFlags(&ev_send[r], cudaEventDisableTiming));
       HS_CUDA(cudaEventCreateWithFlags(&ev_done[r], cudaEventDisableTiming));
@@ -167,6 +172,19 @@ struct LoopComm : Comm {
       for (size_t i = 0; i < n; ++i) sum[i] += w->red[r][i];
     w->barrier();   // everybody has read the contributions
     HS_CUDA(cudaMemcpyAsync(d_buf, sum.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+  }
+  void allreduce_sum_f64(double* d_buf, size_t n, cudaStream_t st) override {   // sum in rank order
+    std::vector<double> v(n);
+    HS_CUDA(cudaMemcpyAsync(v.data(), d_buf, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    w->redf[rank] = v;
+    w->barrier();
+    std::vector<double> sum(n, 0.0);
+    for (int r = 0; r < world; ++r)
+      for (size_t i = 0; i < n; ++i) sum[i] += w->redf[r][i];
+    w->barrier();
+    HS_CUDA(cudaMemcpyAsync(d_buf, sum.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     HS_CUDA(cudaStreamSynchronize(st));
   }
   void group_start() override {
@@ -242,6 +260,9 @@ void comm_destroy(Comm* c) { delete c; }
 
 void comm_allreduce_sum_i32(Comm* c, int32_t* d_buf, size_t n, cudaStream_t st) {
   if (n) c->allreduce_sum_i32(d_buf, n, st);
+}
+void comm_allreduce_sum_f64(Comm* c, double* d_buf, size_t n, cudaStream_t st) {
+  if (n) c->allreduce_sum_f64(d_buf, n, st);
 }
 void comm_group_start(Comm* c) { c->group_start(); }
 void comm_group_end(Comm* c, cudaStream_t st) { c->group_end(st); }

@@ -742,7 +742,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   // C_s) and the top blocks are gathered to rank 0, which builds the apply (v1: the apply and
   // PCG run on rank 0).
   const bool dist = h->world > 1;
-  const bool plan_apply = !dist || h->rank == 0;
+  const bool plan_apply = !dist;   // world > 1: the distributed solve's plan instead (dsolve.cu)
   auto own = [&](int lv, int c) { return !dist || DP.own(lv, c); };
   // Single GPU, DC: the second half of a batch is patched with the kept ranks on the device
   // (k_patch) and launched right behind the first half; the host reads the ranks back one
@@ -1561,72 +1561,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         for (int32_t s : Bt) lv2[s] = L.rank[s];
       }
-      // T_s is formed on the side stream: join it before the records travel
-      HS_CUDA(cudaEventRecord(h->ev_join, h->side));
-      HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
-      // record sizes of rank g's clusters (ascending id): T (m^2, 4-aligned), C (K kn)
-      auto sizes = [&](int g, int64_t& tw, int64_t& cw) {
-        tw = cw = 0;
-        for (int s = 0; s < lev.nclus; ++s)
-          if (DP.owner[l][s] == g) {
-            tw += ((int64_t)cap[s] * cap[s] + 3) & ~int64_t(3);
-            const int64_t K = cap[s] - L.rank[s];
-            if (K > 0 && L.kn[s] > 0) cw += K * L.kn[s];
-          }
-      };
-      if (h->rank != 0) {
-        int64_t tw, cw;
-        sizes(h->rank, tw, cw);
-        double* cpack = cw ? (double*)dc.alloc(sizeof(double) * cw) : nullptr;
-        std::vector<CopyItem> pk;
-        int64_t co = 0;
-        for (int s = 0; s < lev.nclus; ++s)
-          if (own(l, s) && L.C[s]) {
-            const int32_t K = cap[s] - L.rank[s];
-            pk.push_back(CopyItem{L.C[s], cpack + co, L.kn[s], L.kn[s], K, L.kn[s], 0, 0});
-            co += (int64_t)K * L.kn[s];
-          }
-        split_copies(pk);
-        upA.reset();
-        const size_t iK = upA.add(pk);
-        upA.stage.ensure(upA.total);
-        upA.dev.ensure(upA.total);
-        upA.copy_in(iK, pk);
-        upA.send(st);
-        launch_copy2d(upA.dptr<CopyItem>(iK), (int)pk.size(), st);
-        comm_group_start(h->comm);
-        comm_send_f64(h->comm, L.arena, (size_t)tw, 0, st);
-        comm_send_f64(h->comm, cpack, (size_t)cw, 0, st);
-        comm_group_end(h->comm, st);
-        HS_CUDA(cudaStreamSynchronize(st));
-        if (cpack) dc.free(cpack);
-      } else {
-        std::vector<double*> tb(h->world, nullptr), cb(h->world, nullptr);
-        comm_group_start(h->comm);
-        for (int g = 1; g < h->world; ++g) {
-          int64_t tw, cw;
-          sizes(g, tw, cw);
-          if (tw) tb[g] = (double*)dc.alloc(sizeof(double) * tw);
-          if (cw) cb[g] = (double*)dc.alloc(sizeof(double) * cw);
-          if (tb[g]) L.cchunks.push_back(tb[g]);
-          if (cb[g]) L.cchunks.push_back(cb[g]);
-          comm_recv_f64(h->comm, tb[g], (size_t)tw, g, st);
-          comm_recv_f64(h->comm, cb[g], (size_t)cw, g, st);
-        }
-        comm_group_end(h->comm, st);
-        std::vector<int64_t> to(h->world, 0), co(h->world, 0);
-        for (int s = 0; s < lev.nclus; ++s) {
-          const int g = DP.owner[l][s];
-          if (g == 0) continue;
-          L.T[s] = tb[g] + to[g];
-          to[g] += ((int64_t)cap[s] * cap[s] + 3) & ~int64_t(3);
-          const int64_t K = cap[s] - L.rank[s];
-          if (K > 0 && L.kn[s] > 0) {
-            L.C[s] = cb[g] + co[g];
-            co[g] += K * L.kn[s];
-          }
-        }
-      }
+      // the records (T_s, C_s) stay at their owners: the distributed solve (dsolve.cu)
+      // applies them there; T_s is formed on the side stream, joined below
     }
     // ---- apply plan of the level (Algorithm 2), replayed in elimination order ---------------
     const int nP = lev.nclus / 2;
@@ -1917,7 +1853,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         comm_group_end(h->comm, st);
       }
     }
-    if (N > 0 && plan_apply) {
+    if (N > 0 && (!dist || h->rank == 0)) {   // the top is factored on rank 0
       f->d_top = (double*)dc.alloc(sizeof(double) * N * N);
       HS_CUDA(cudaMemsetAsync(f->d_top, 0, sizeof(double) * N * N, st));
       for (int P = 0; P < ntc; ++P)
@@ -2033,6 +1969,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     up(AP.post_cl, AP.d_post_cl);
   }
   HS_CUDA(cudaStreamSynchronize(st));
+  if (dist) dist_solve_build(f, DP);
   return guard.release();
 }
 

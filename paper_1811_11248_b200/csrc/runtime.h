@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <memory>
 #include <utility>
 #include <string>
 #include <unordered_map>
@@ -192,10 +193,81 @@ void loop_world_destroy(LoopWorld* w);
 int loop_world_size(LoopWorld* w);
 void comm_destroy(Comm* c);
 void comm_allreduce_sum_i32(Comm* c, int32_t* d_buf, size_t n, cudaStream_t st);
+void comm_allreduce_sum_f64(Comm* c, double* d_buf, size_t n, cudaStream_t st);
 void comm_group_start(Comm* c);
 void comm_group_end(Comm* c, cudaStream_t st);
 void comm_send_f64(Comm* c, const double* d, size_t n, int peer, cudaStream_t st);
 void comm_recv_f64(Comm* c, double* d, size_t n, int peer, cudaStream_t st);
+}  // namespace hs
+
+namespace hs {
+// Distributed solve (dsolve.cu): per-rank plan of the owner-computes Algorithm 2 and PCG.
+struct DFwdItem {            // one owned cluster of a batch, forward
+  const double* T;           // T_s (m x m, row-major)
+  const double* C;           // C_s (K x kn, row-major)
+  const double* y;           // y_s (level segment)
+  double* yc;                // coarse part -> the parent's segment
+  double* yf;                // fine part (kept for the backward sweep)
+  double* slot;              // contributions C_s^T y_f (kn), or null
+  int32_t m, r, kn, pad;
+};
+struct DAccItem {            // one owned target of a batch: y -= its contributions in source order
+  double* y;
+  int32_t len, s0, ns, pad;
+};
+struct DBwdItem {            // one owned cluster of a batch, backward
+  const double* T;
+  const double* C;
+  const double* xc;          // coarse part (the parent's segment)
+  const double* yf;
+  double* x;                 // x_s (level segment)
+  int32_t m, r, kn, nb0, nnb, pad;
+};
+struct DNb {                 // a neighbour's current x segment
+  const double* x;
+  int32_t len, pad;
+};
+struct DMsg {                // one message of a group: (device pointer, doubles, peer)
+  double* ptr;
+  int32_t len, peer;
+};
+struct DistBatch {
+  int32_t level = 0, phase2 = 0;
+  int32_t fwd0 = 0, nfwd = 0, acc0 = 0, nacc = 0, bwd0 = 0, nbwd = 0;
+  std::vector<DMsg> fsend, frecv, bsend, brecv;
+};
+struct DevCache;
+struct DistSolve {
+  DevCache* dc = nullptr;
+  std::vector<void*> owned;
+  int rank = 0, world = 1;
+  std::vector<int64_t> vbase;
+  int64_t vtotal = 0;
+  double *d_y = nullptr, *d_x = nullptr, *d_f = nullptr, *d_slot = nullptr;
+  DFwdItem* d_fwd = nullptr;
+  DAccItem* d_acc = nullptr;
+  const double** d_accsrc = nullptr;
+  DBwdItem* d_bwd = nullptr;
+  DNb* d_nb = nullptr;
+  int max_m = 0, max_kn = 0;
+  std::vector<DistBatch> batches;
+  std::vector<DMsg> top;              // per top cluster: (unused, size, owner)
+  std::vector<int64_t> top_off;
+  // PCG
+  int64_t r0 = 0, r1 = 0, nloc = 0, nghost = 0, nnz_loc = 0;
+  std::vector<int64_t> range_lo, range_hi;   // every rank's owned permuted range
+  std::vector<DMsg> hsend, hrecv;
+  std::vector<int64_t> hsend_off, hrecv_off;
+  int64_t* d_lrow = nullptr;
+  int32_t* d_lcol = nullptr;
+  int64_t* d_vidx = nullptr;
+  int32_t* d_sidx = nullptr;
+  double *d_lval = nullptr, *d_xext = nullptr, *d_sbuf = nullptr;
+  double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_xs = nullptr, *d_part = nullptr;
+  double *d_full = nullptr, *d_full2 = nullptr;
+  double* h_scal = nullptr;
+  ~DistSolve();
+};
 }  // namespace hs
 
 struct hs_handle_s {
@@ -226,6 +298,7 @@ struct hs_factor_s {
   int64_t ntop = 0;
   std::vector<int32_t> top_sizes;
   hs::ApplyPlan ap;
+  std::unique_ptr<hs::DistSolve> ds;     // world > 1: the distributed solve (records stay at their owners)
   bool keep_records = false;             // HS_KEEP_RECORDS: per-cluster G, V, tau, B stay exportable
   hs_factor_stats_t stats{};
   // PCG work vectors
@@ -241,4 +314,9 @@ void apply(hs_factor_s* f, const double* d_b, double* d_x);         // device po
 void pcg(hs_factor_s* f, const double* d_b, double* d_x, double tol, int maxit, hs_pcg_report* rep);
 void gmres(hs_factor_s* f, const double* d_b, double* d_x, double tol, int restart, int maxit, hs_pcg_report* rep);
 void spmv(hs_factor_s* f, const double* d_x, double* d_y);
+struct DistPlan;
+void dist_solve_build(hs_factor_s* f, const DistPlan& DP);
+void dist_apply(hs_factor_s* f, const double* d_b, double* d_x);         // collective, global vectors
+void dist_pcg(hs_factor_s* f, const double* d_b, double* d_x, double tol, int maxit, hs_pcg_report* rep);
+void dist_spmv_global(hs_factor_s* f, const double* d_x, double* d_y);
 }  // namespace hs
