@@ -19,8 +19,9 @@ Inputs (CSR values, b) are resident in HBM when the timed region starts and the 
 e2e repeats the step through the same C API with HOST buffers (values and b uploaded, x
 downloaded inside the timed region).  N > 1 (torchrun, one process per GPU): the factor is
 partitioned by the 8 fixed subdomains over the GPUs with NCCL exchanges (SURVEY §8(e),
-DESIGN.md §7; strong scaling: one system per step), the solve runs on rank 0; --replicas runs
-N independent systems instead (weak).  A watchdog aborts a run whose exchanges never complete
+DESIGN.md §7; strong scaling: one system per step), and so is the solve (owner-computes
+Algorithm 2 and PCG with a halo SpMV and all-reduced dots, every rank keeping only its own
+elimination records); --replicas runs N independent systems instead (weak).  A watchdog aborts a run whose exchanges never complete
 (exit 3, an error JSON line).  --impl reference times the CPU oracle (oracle/) on all host
 cores on a bounded sample of the workload.
 """
@@ -230,7 +231,7 @@ def run_ours(args, rank, world, local):
         p.eps = args.eps
     if dist_factor:
         # the factor is partitioned by the 8 fixed subdomains over the ranks
-        # (NCCL exchanges inside hs_factor_create); the solve runs on rank 0 (v1)
+        # (NCCL exchanges inside hs_factor_create), and the solve with it (dsolve.cu)
         uid = [H.hs_nccl_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(uid, src=0)
         h = H.hs_create(local, world, rank, uid[0])
@@ -252,7 +253,7 @@ def run_ours(args, rank, world, local):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    solver = not dist_factor or rank == 0
+    solver = True   # the distributed solve is collective: every rank runs hs_pcg (owner-computes)
 
     def step():
         f = H.hs_factor_create(h, a, vals, eps=p.eps)
@@ -421,7 +422,7 @@ def run_ours(args, rank, world, local):
                    "l2": "256 MB buffer written between timed steps (and the factor working set > L2)",
                    "analyze": "reading R-coarse (coarse_fill=0: structural coarse neighbours, DESIGN.md §2)",
                    "flops": "dense live column counts k_n, k_w (what the kernels compute; >= the support-restricted count)",
-                   "parallelism": (f"subdomains over {world} GPUs (factor), solve on rank 0" if dist_factor
+                   "parallelism": (f"subdomains over {world} GPUs (factor and solve)" if dist_factor
                                    else "replicas" if world > 1 else "single"),
                    "pcg_iters": [r["iters"] for r in reps], "relres_true": reps[-1]["relres_true"],
                    "t_analyze_s": t_analyze, "t_factor_s": t_fac, "t_pcg_s": t_pcg / args.steps,
