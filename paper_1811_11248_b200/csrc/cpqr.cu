@@ -729,6 +729,10 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
     // shorter update per step for a costlier exchange) while the clusters still fill at most
     // a quarter of the GPU and every CTA keeps >= 128 columns (C2 level 3: CPQR 38 -> 29 ms)
     while (CS < 16 && n_act * CS * 4 <= nsm && max_kw / (2 * CS) >= 128) CS *= 2;
+    // global mode is bound by each SM's L2 bandwidth (the slice streams through L2 every
+    // step): spread its clusters over as many SMs as the batch leaves free
+    if (!sm)
+      while (CS < 16 && n_act * CS * 2 <= nsm && max_kw / (2 * CS) >= 32) CS *= 2;
     const size_t smem = need(CS);
     if (smem > CQ_CAP_BYTES) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
     long long* trace = nullptr;

@@ -250,6 +250,26 @@ struct DevStatus {
   int32_t flag, level, cluster, pivot;
   double value;
 };
+// A level of small clusters eliminated wave by wave on the device (small.cu)
+constexpr int SMALL_M = 32;    // largest cluster of such a level
+constexpr int SMALL_K = 512;   // largest k_n + k_w (level-start sizes)
+struct SmallArgs {
+  BlockDir dir;
+  const int32_t *nptr, *nidx, *wptr, *widx;   // n(s), w(s) of the level (CSR)
+  int32_t *live, *rank, *kn, *kw;             // per cluster (live: updated as clusters are eliminated)
+  double* T;                                  // apply-operator arena, T_s at toff[s]
+  const int64_t* toff;
+  int32_t* piv;
+  const int64_t* poff;
+  double* C;                                  // C_s at coff[s] (room for m x k_n at level-start sizes)
+  const int64_t* coff;
+  const int32_t* items;                       // the waves' clusters, concatenated
+  DevStatus* status;
+  double eps;
+  int32_t relative, level, m_max, k_max, nseg_max, npair_max;
+};
+size_t small_smem_bytes(int m_max, int k_max, int nseg_max, int npair_max);
+void launch_elim_small(const SmallArgs& a, int first, int n, cudaStream_t st);
 // the patch items; with pub: also publishes the batch's ranks (one extra block)
 void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st, int nrank = 0,
                   const DevStatus* d_status = nullptr, RankPub* pub = nullptr, int32_t seq = 0);

@@ -933,7 +933,131 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
 
     int64_t level_dofs = 0;
     for (int32_t c : cap) level_dofs += c;
-    for (size_t bidx = 0; bidx < lev.batches.size(); ++bidx) {
+    // ---- a level of small clusters: one device-planned kernel per wave (small.cu) ---------
+    bool small = !dist && !nodc && dpatch && !f->keep_records && level_dofs > 0 &&
+                 std::getenv("HS_NO_SMALL_LEVELS") == nullptr;
+    std::vector<int64_t> kn_cap(lev.nclus, 0), kw_cap(lev.nclus, 0);
+    int small_k = 1, small_m = 1, small_nseg = 1, small_np = 1;
+    for (int s = 0; s < lev.nclus && small; ++s) {
+      for (int32_t q : lev.H[s]) kn_cap[s] += cap[q];
+      for (int32_t q : lev.w[s]) kw_cap[s] += cap[q];
+      const int nn = (int)lev.H[s].size();
+      small = cap[s] <= SMALL_M && kn_cap[s] + kw_cap[s] <= SMALL_K;
+      small_m = std::max(small_m, cap[s]);
+      small_k = std::max<int>(small_k, (int)(kn_cap[s] + kw_cap[s]));
+      small_nseg = std::max<int>(small_nseg, nn + (int)lev.w[s].size());
+      small_np = std::max(small_np, nn * (nn + 1) / 2);
+    }
+    if (small) {
+      const int n = lev.nclus;
+      std::vector<int32_t> nptr(n + 1, 0), nidx, wptr(n + 1, 0), widx, items;
+      for (int c = 0; c < n; ++c) {
+        nidx.insert(nidx.end(), lev.H[c].begin(), lev.H[c].end());
+        widx.insert(widx.end(), lev.w[c].begin(), lev.w[c].end());
+        nptr[c + 1] = (int32_t)nidx.size();
+        wptr[c + 1] = (int32_t)widx.size();
+      }
+      // waves: the clusters of a batch without a common neighbour (Schur targets disjoint)
+      std::vector<std::pair<int32_t, int32_t>> waves;   // (first, count) into items
+      std::vector<uint64_t> mask(n, 0);
+      for (const auto& Bt : lev.batches) {
+        std::vector<std::vector<int32_t>> wv;
+        std::vector<int32_t> touched;
+        for (int32_t c : Bt) {
+          uint64_t used = 0;
+          for (int32_t q : lev.H[c]) used |= mask[q];
+          int w = 0;
+          while (w < 64 && ((used >> w) & 1ull)) ++w;
+          if (w == 64) w = 64 + (int)wv.size();   // overflow: a wave of its own
+          if ((int)wv.size() <= w) wv.resize(w + 1);
+          wv[w].push_back(c);
+          if (w < 64)
+            for (int32_t q : lev.H[c]) {
+              if (!mask[q]) touched.push_back(q);
+              mask[q] |= 1ull << w;
+            }
+        }
+        for (int32_t q : touched) mask[q] = 0;
+        for (auto& v : wv)
+          if (!v.empty()) {
+            waves.push_back({(int32_t)items.size(), (int32_t)v.size()});
+            items.insert(items.end(), v.begin(), v.end());
+          }
+        S.n_batches++;
+      }
+      std::vector<int64_t> toff(n, 0), poff(n, 0), coff(n, 0);
+      int64_t ctot = 0;
+      for (int c = 0; c < n; ++c) {
+        toff[c] = oX[c] < 0 ? 0 : oX[c];
+        poff[c] = oP[c];
+        coff[c] = ctot;
+        ctot += ((int64_t)cap[c] * kn_cap[c] + 3) & ~int64_t(3);
+      }
+      double* cbase = (double*)dc.alloc(sizeof(double) * std::max<int64_t>(ctot, 4));
+      L.cchunks.push_back(cbase);
+      int32_t* dint = (int32_t*)dc.alloc(sizeof(int32_t) * (4 * (size_t)n + 1));   // live rank kn kw
+      upA.reset();
+      const size_t iNP = upA.add(nptr), iNI = upA.add(nidx), iWP = upA.add(wptr), iWI = upA.add(widx),
+                   iIT = upA.add(items), iLV = upA.add(cap), iTO = upA.add(toff), iPO = upA.add(poff),
+                   iCO = upA.add(coff);
+      upA.stage.ensure(upA.total);
+      upA.dev.ensure(upA.total);
+      upA.copy_in(iNP, nptr); upA.copy_in(iNI, nidx); upA.copy_in(iWP, wptr); upA.copy_in(iWI, widx);
+      upA.copy_in(iIT, items); upA.copy_in(iLV, cap); upA.copy_in(iTO, toff); upA.copy_in(iPO, poff);
+      upA.copy_in(iCO, coff);
+      upA.send(st);
+      HS_CUDA(cudaMemcpyAsync(dint, upA.dptr<int32_t>(iLV), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+      SmallArgs sa{};
+      sa.dir = bs.dir();
+      sa.nptr = upA.dptr<int32_t>(iNP); sa.nidx = upA.dptr<int32_t>(iNI);
+      sa.wptr = upA.dptr<int32_t>(iWP); sa.widx = upA.dptr<int32_t>(iWI);
+      sa.live = dint; sa.rank = dint + n; sa.kn = dint + 2 * n; sa.kw = dint + 3 * n;
+      sa.T = L.arena; sa.toff = upA.dptr<int64_t>(iTO);
+      sa.piv = L.iarena; sa.poff = upA.dptr<int64_t>(iPO);
+      sa.C = cbase; sa.coff = upA.dptr<int64_t>(iCO);
+      sa.items = upA.dptr<int32_t>(iIT);
+      sa.status = d_status;
+      sa.eps = opt.eps; sa.relative = opt.eps_relative ? 1 : 0; sa.level = l;
+      sa.m_max = small_m; sa.k_max = small_k; sa.nseg_max = small_nseg; sa.npair_max = small_np;
+      pt.rec(pt.a[3], st);
+      for (const auto& w : waves) launch_elim_small(sa, w.first, w.second, st);
+      pt.rec(pt.a[4], st);
+      std::vector<int32_t> back(3 * (size_t)n);
+      HS_CUDA(cudaMemcpyAsync(back.data(), dint + n, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      dc.free(dint);
+      if (h_status.flag == 1) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "NOT_SPD: Cholesky breakdown at level %d cluster %d pivot %d value %.17g (P:283)",
+                      h_status.level, h_status.cluster, h_status.pivot, h_status.value);
+        fail(HS_E_NOT_SPD, buf);
+      }
+      if (h_status.flag) fail(HS_E_INTERNAL, "small-cluster level: a block of the schedule is missing");
+      if (pt.on) S.t_phase_s[3] += PhaseTimer::el(pt.a[3], pt.a[4]);
+      for (int c = 0; c < n; ++c) {
+        const int32_t m = cap[c], r = back[c], kn = back[n + c], kw = back[2 * n + c];
+        L.rank[c] = r;
+        L.kn[c] = kn;
+        L.kw[c] = kw;
+        L.ldB[c] = kn + kw;
+        live[c] = r;
+        done[c] = 1;
+        L.C[c] = (m > r && kn > 0) ? cbase + coff[c] : nullptr;
+        if (m == 0) continue;
+        const int32_t K = m - r;
+        S.max_m = std::max(S.max_m, m);
+        S.max_rank = std::max(S.max_rank, r);
+        double fq = 0.0;
+        for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
+        S.flops += (double)m * m * m / 3.0 + (double)m * m * (kn + kw) + fq + (double)K * kn * (kn + 1);
+        S.flops_phase[1] += (double)m * m * m / 3.0;
+        S.flops_phase[2] += (double)m * m * (kn + kw);
+        S.flops_phase[3] += fq;
+        S.flops_phase[4] += (double)K * kn * (kn + 1);
+      }
+    }
+    for (size_t bidx = 0; bidx < (small ? 0 : lev.batches.size()); ++bidx) {
       const auto& Bt = lev.batches[bidx];
       if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
       const bool phase2 = (int)bidx >= lev.nphase1;

@@ -1,0 +1,405 @@
+// The elimination of a level of small clusters in ONE kernel per wave, planned on the device
+// (verdict r01 item 7: the sequential batch chains of the coarse levels were host-bound —
+// every batch of the regular pipeline needs the previous batch's ranks on the host before
+// its shapes can be planned, ~0.1 ms of host work per batch for a few microseconds of GPU
+// work when the clusters hold a handful of DOFs).
+//
+// For a level whose clusters all have m <= SMALL_M DOFs (and k_n + k_w <= SMALL_K live
+// columns at their level-start sizes), each batch (independent set, Alg. 1 loop P:633) is
+// split into waves of clusters without a common neighbour (pattern only, planned once per
+// level), and each wave is one launch, one CTA per cluster, doing the whole scaled low-rank
+// elimination of §3.1 in shared memory:
+//   its shapes from the device array of live sizes (the ranks of the clusters eliminated
+//   before it), its blocks found in the level's block directory,
+//   A_ss = G_s G_sᵀ, B = G_s⁻¹[A_sw | A_sn] (the deferred compression),
+//   CPQR of B_w to eps with exact norms and the readings Q1-Q5 + R-floor,
+//   the rotation of B_n by Qᵀ (E_s), the write-back of row s [I_r | coarse],
+//   the Schur update A_pq -= C_pᵀC_q on n(s)² (Eq. CC:eqn:elim) by plain
+//   load-subtract-store (no other cluster of the wave touches these blocks: no common
+//   neighbour), the apply operator T_s = Qᵀ G_s⁻¹ and C_s into the factor record.
+// The host launches the level's waves back to back and reads the ranks once, at the level's
+// end.  Same decisions as the batch pipeline and the oracle (parity tests); other rounding
+// order (sequential per-thread dot products).
+#include <climits>
+#include <cstdio>
+
+#include "device.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int ST = 256;   // threads per CTA
+
+__device__ __forceinline__ int64_t sdir_find(const BlockDir& d, int p, int q) {   // p >= q; -1 if absent
+  int64_t lo = d.ptr[p], hi = d.ptr[p + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (d.q[mid] < q) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < d.ptr[p + 1] && d.q[lo] == q) ? d.off[lo] : -1;
+}
+
+__device__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int k = 1; k < ST / 32; ++k) r = fmax(r, red[k]);
+  return r;
+}
+__device__ int block_min_i(int v, int* red) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int r = red[0];
+  for (int k = 1; k < ST / 32; ++k) r = min(r, red[k]);
+  return r;
+}
+
+__global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
+  extern __shared__ double sm[];
+  const int s = a.items[first + blockIdx.x];
+  const int tid = threadIdx.x;
+  const int MX = a.m_max, KX = a.k_max, NX = a.nseg_max, PX = a.npair_max;
+  // shared memory carve-up (the host sizes it from the same formula: small_smem_bytes)
+  double* G = sm;                            // MX x (MX + 1): A_ss, then its lower factor
+  double* B = G + MX * (MX + 1);             // MX x KX row-major (ld k): [B_w | B_n]
+  double* V = B + (size_t)MX * KX;           // MX x MX: reflector j in row j
+  double* X = V + MX * MX;                   // MX x MX: G^{-1}, then T_s
+  double* tau = X + MX * MX;                 // MX
+  double* nu = tau + MX;                     // KX column norms (-1: pivoted)
+  double* red = nu + KX;                     // 8 (+ 8 ints)
+  int* redi = (int*)(red + 8);
+  double** sptr = (double**)(red + 16);      // NX segment pointers
+  int* scol = (int*)(sptr + NX);             // NX column offsets in B
+  int* slen = scol + NX;
+  int* sld = slen + NX;
+  int* strn = sld + NX;
+  int* sq = strn + NX;
+  double** pptr = (double**)(sq + NX + (NX & 1));   // PX target blocks of the Schur pairs
+  int* poff = (int*)(pptr + PX);             // PX + 1 element prefix
+  int* pa = poff + PX + 1;                   // PX: n-segment index of the row side
+  int* pb = pa + PX;                         // PX: n-segment index of the column side
+  __shared__ int nseg, nw_seg, kw, kn, failed, rr, npair;
+  __shared__ double* Dss;
+  __shared__ int ldss;
+  const int m = a.live[s];
+  if (tid == 0) {
+    failed = 0;
+    int col = 0, ns = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int32_t* lst = pass == 0 ? a.widx + a.wptr[s] : a.nidx + a.nptr[s];
+      const int cnt = pass == 0 ? a.wptr[s + 1] - a.wptr[s] : a.nptr[s + 1] - a.nptr[s];
+      for (int t = 0; t < cnt; ++t) {
+        const int q = lst[t], L = a.live[q];
+        if (L == 0) continue;
+        const int p0 = max(s, q), q0 = min(s, q);
+        const int64_t o = sdir_find(a.dir, p0, q0);
+        if (o < 0 || ns >= NX) {
+          failed = 2;
+          continue;
+        }
+        sptr[ns] = a.dir.blk + o;
+        scol[ns] = col;
+        slen[ns] = L;
+        sld[ns] = a.dir.cap[q0];
+        strn[ns] = q > s ? 1 : 0;
+        sq[ns] = q;
+        ++ns;
+        col += L;
+      }
+      if (pass == 0) {
+        kw = col;
+        nw_seg = ns;
+      }
+    }
+    nseg = ns;
+    kn = col - kw;
+    const int64_t od = sdir_find(a.dir, s, s);
+    Dss = od >= 0 ? a.dir.blk + od : nullptr;
+    ldss = a.dir.cap[s];
+    if (!Dss && m > 0) failed = 2;
+    // Schur pairs (a >= b over the non-empty n-segments, ascending cluster id)
+    int np = 0, e = 0;
+    for (int x = nw_seg; x < ns; ++x)
+      for (int y = nw_seg; y <= x; ++y) {
+        if (np >= PX) {
+          failed = 2;
+          break;
+        }
+        const int64_t o = sdir_find(a.dir, sq[x], sq[y]);
+        if (o < 0) failed = 2;
+        pptr[np] = o >= 0 ? a.dir.blk + o : nullptr;
+        pa[np] = x;
+        pb[np] = y;
+        poff[np] = e;
+        e += (x == y) ? slen[x] * (slen[x] + 1) / 2 : slen[x] * slen[y];
+        ++np;
+      }
+    poff[np] = e;
+    npair = np;
+    if (failed == 2 && atomicCAS(&a.status->flag, 0, 2) == 0) {
+      a.status->level = a.level;
+      a.status->cluster = s;
+      a.status->pivot = -1;
+      a.status->value = 0.0;
+    }
+  }
+  __syncthreads();
+  if (failed) return;
+  const int k = kw + kn;
+  if (m == 0) {
+    if (tid == 0) {
+      a.rank[s] = 0;
+      a.kn[s] = kn;
+      a.kw[s] = kw;
+    }
+    return;
+  }
+  // ---- load A_ss (lower triangle of the stored diagonal block) and [A_sw | A_sn] ----------
+  for (int e = tid; e < m * m; e += ST) {
+    const int i = e / m, j = e % m;
+    G[i * (MX + 1) + j] = j <= i ? Dss[(int64_t)i * ldss + j] : 0.0;
+  }
+  for (int g = 0; g < nseg; ++g) {
+    const double* p = sptr[g];
+    const int L = slen[g], ld = sld[g], c0 = scol[g];
+    if (strn[g]) {
+      for (int e = tid; e < m * L; e += ST) {   // consecutive threads: consecutive rows i
+        const int j = e / m, i = e % m;
+        B[i * k + c0 + j] = p[(int64_t)j * ld + i];
+      }
+    } else {
+      for (int e = tid; e < m * L; e += ST) {
+        const int i = e / L, j = e % L;
+        B[i * k + c0 + j] = p[(int64_t)i * ld + j];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- A_ss = G Gᵀ (right-looking) --------------------------------------------------
+  for (int j = 0; j < m; ++j) {
+    const double d = G[j * (MX + 1) + j];
+    if (!(d > 0.0)) {   // uniform: every thread reads the same d
+      if (tid == 0 && atomicCAS(&a.status->flag, 0, 1) == 0) {
+        a.status->level = a.level;
+        a.status->cluster = s;
+        a.status->pivot = j;
+        a.status->value = d;
+      }
+      return;
+    }
+    const double g = sqrt(d);
+    __syncthreads();
+    if (tid == 0) G[j * (MX + 1) + j] = g;
+    for (int i = j + 1 + tid; i < m; i += ST) G[i * (MX + 1) + j] /= g;
+    __syncthreads();
+    const int t = m - j - 1;
+    for (int e = tid; e < t * t; e += ST) {
+      const int i = j + 1 + e / t, l = j + 1 + e % t;
+      if (l <= i) G[i * (MX + 1) + l] -= G[i * (MX + 1) + j] * G[l * (MX + 1) + j];
+    }
+    __syncthreads();
+  }
+  // ---- B = G⁻¹ [A_sw | A_sn]: forward substitution, a thread per column --------------------
+  for (int c = tid; c < k; c += ST) {
+    for (int i = 0; i < m; ++i) {
+      double b = B[i * k + c];
+      for (int l = 0; l < i; ++l) b -= G[i * (MX + 1) + l] * B[l * k + c];
+      B[i * k + c] = b / G[i * (MX + 1) + i];
+    }
+  }
+  __syncthreads();
+  // R-floor: the largest n-column norm of B_n
+  double rn = 0.0;
+  for (int c = kw + tid; c < k; c += ST) {
+    double s2 = 0.0;
+    for (int i = 0; i < m; ++i) s2 += B[i * k + c] * B[i * k + c];
+    rn = fmax(rn, sqrt(s2));
+  }
+  const double Rn = block_max(rn, red);
+  // ---- CPQR of B_w to eps (Q1-Q5): exact norms, strict keep rule, lowest-index tie window -
+  for (int c = tid; c < kw; c += ST) nu[c] = 0.0;
+  if (tid == 0) rr = min(m, kw);
+  __syncthreads();
+  double tau_s = 0.0;
+  const int jmax = min(m, kw);
+  for (int j = 0; j < jmax; ++j) {
+    double lmax = -1.0;
+    for (int c = tid; c < kw; c += ST) {
+      if (nu[c] < 0.0) continue;
+      double s2 = 0.0;
+      for (int i = j; i < m; ++i) s2 += B[i * k + c] * B[i * k + c];
+      nu[c] = sqrt(s2);
+      lmax = fmax(lmax, nu[c]);
+    }
+    const double numax = block_max(lmax, red);
+    if (j == 0) {
+      tau_s = a.relative ? a.eps * numax : a.eps;
+      if (a.relative && a.eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(numax, Rn));
+    }
+    if (!(numax > tau_s)) {
+      if (tid == 0) rr = j;
+      break;
+    }
+    const double thr = (1.0 - 1e-10) * numax;
+    int lo = INT_MAX;
+    for (int c = tid; c < kw; c += ST)
+      if (nu[c] >= thr) {
+        lo = c;
+        break;
+      }
+    const int p = block_min_i(lo, redi);
+    // dlarfg of column p, rows j..m-1 (one warp)
+    if (tid < 32) {
+      double xs = 0.0;
+      for (int l = j + 1 + tid; l < m; l += 32) xs += B[l * k + p] * B[l * k + p];
+      for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+      const double alpha = B[j * k + p], xnorm = sqrt(xs);
+      double t, beta, rden;
+      if (xnorm == 0.0) {
+        t = 0.0;
+        beta = alpha;
+        rden = 0.0;
+      } else {
+        const double h = sqrt(alpha * alpha + xnorm * xnorm);
+        beta = alpha >= 0.0 ? -h : h;
+        t = (beta - alpha) / beta;
+        rden = 1.0 / (alpha - beta);
+      }
+      for (int l = tid; l < m; l += 32) V[j * MX + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : B[l * k + p] * rden;
+      if (tid == 0) {
+        tau[j] = t;
+        red[7] = beta;
+        a.piv[a.poff[s] + j] = p;
+      }
+    }
+    __syncthreads();
+    const double t = tau[j], beta = red[7];
+    for (int c = tid; c < kw; c += ST) {
+      if (c == p || nu[c] < 0.0 || t == 0.0) continue;
+      double w = 0.0;
+      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * k + c];
+      const double tw = t * w;
+      for (int l = j; l < m; ++l) B[l * k + c] -= tw * V[j * MX + l];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      B[j * k + p] = beta;
+      for (int l = j + 1; l < m; ++l) B[l * k + p] = 0.0;
+      nu[p] = -1.0;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int r = kw > 0 ? rr : 0, K = m - r;
+  // ---- E_s on the n-columns: Qᵀ B_n (H_0 first) ----------------------------------------------
+  for (int c = kw + tid; c < k; c += ST)
+    for (int j = 0; j < r; ++j) {
+      if (tau[j] == 0.0) continue;
+      double w = 0.0;
+      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * k + c];
+      const double tw = tau[j] * w;
+      for (int l = j; l < m; ++l) B[l * k + c] -= tw * V[j * MX + l];
+    }
+  // ---- T_s = Qᵀ G⁻¹ (the apply operator), a thread per column ---------------------------------
+  for (int c = tid; c < m; c += ST) {
+    for (int i = 0; i < m; ++i) {
+      double x = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) x -= G[i * (MX + 1) + l] * X[l * MX + c];
+      X[i * MX + c] = i < c ? 0.0 : x / G[i * (MX + 1) + i];
+    }
+    for (int j = 0; j < r; ++j) {
+      if (tau[j] == 0.0) continue;
+      double w = 0.0;
+      for (int l = j; l < m; ++l) w += V[j * MX + l] * X[l * MX + c];
+      const double tw = tau[j] * w;
+      for (int l = j; l < m; ++l) X[l * MX + c] -= tw * V[j * MX + l];
+    }
+  }
+  __syncthreads();
+  double* T = a.T + a.toff[s];
+  for (int e = tid; e < m * m; e += ST) T[e] = X[(e / m) * MX + (e % m)];
+  // ---- C_s = rows [r, m) of the rotated B_n into the factor record (ld kn) -----------------
+  if (kn > 0 && K > 0) {
+    double* C = a.C + a.coff[s];
+    for (int e = tid; e < K * kn; e += ST) C[e] = B[(r + e / kn) * k + kw + e % kn];
+  }
+  // ---- write-back of row s: I_r on (s, s), the coarse rows into the blocks (s, q) -----------
+  for (int e = tid; e < r * r; e += ST) {
+    const int i = e / r, j = e % r;
+    if (j <= i) Dss[(int64_t)i * ldss + j] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int g = 0; g < nseg; ++g) {
+    double* p = sptr[g];
+    const int L = slen[g], ld = sld[g], c0 = scol[g];
+    if (strn[g]) {
+      for (int e = tid; e < r * L; e += ST) {
+        const int j = e / r, i = e % r;
+        p[(int64_t)j * ld + i] = B[i * k + c0 + j];
+      }
+    } else {
+      for (int e = tid; e < r * L; e += ST) {
+        const int i = e / L, j = e % L;
+        p[(int64_t)i * ld + j] = B[i * k + c0 + j];
+      }
+    }
+  }
+  // ---- Schur update on n(s)²: A_pq -= C_pᵀ C_q (the wave has no other writer of these) -----
+  if (K > 0) {
+    const int tot = poff[npair];
+    for (int e = tid; e < tot; e += ST) {
+      int lo = 0, hi = npair - 1;   // the pair holding element e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (poff[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const int x = pa[lo], y = pb[lo], o = e - poff[lo];
+      int i, j;
+      if (x == y) {   // lower triangle: row i holds i + 1 entries
+        i = (int)((sqrt(8.0 * o + 1.0) - 1.0) * 0.5);
+        while ((i + 1) * (i + 2) / 2 <= o) ++i;
+        while (i * (i + 1) / 2 > o) --i;
+        j = o - i * (i + 1) / 2;
+      } else {
+        i = o / slen[y];
+        j = o % slen[y];
+      }
+      const int cp = scol[x] - kw + i, cq = scol[y] - kw + j;
+      double acc = 0.0;
+      for (int kk = 0; kk < K; ++kk) acc += B[(r + kk) * k + kw + cp] * B[(r + kk) * k + kw + cq];
+      double* tgt = pptr[lo] + (int64_t)i * a.dir.cap[sq[y]] + j;   // block (p, q): row-major, ld cap[q]
+      *tgt -= acc;
+    }
+  }
+  if (tid == 0) {
+    a.rank[s] = r;
+    a.kn[s] = kn;
+    a.kw[s] = kw;
+    a.live[s] = r;   // no other cluster of this batch reads it (independent set)
+  }
+}
+
+}  // namespace
+
+size_t small_smem_bytes(int m_max, int k_max, int nseg_max, int npair_max) {
+  const size_t d = (size_t)m_max * (m_max + 1) + (size_t)m_max * k_max + 2 * (size_t)m_max * m_max + m_max + k_max + 16;
+  const size_t pbytes = sizeof(double*) * (size_t)(nseg_max + npair_max);
+  const size_t ibytes = sizeof(int) * (size_t)(5 * nseg_max + 1 + (nseg_max & 1) + 3 * npair_max + 1);
+  return d * sizeof(double) + pbytes + ibytes + 64;
+}
+
+void launch_elim_small(const SmallArgs& a, int first, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t smem = small_smem_bytes(a.m_max, a.k_max, a.nseg_max, a.npair_max);
+  set_smem_attr((const void*)k_elim_small, smem);
+  k_elim_small<<<n, ST, smem, st>>>(a, first);
+  count_launch(1);
+}
+
+}  // namespace hs

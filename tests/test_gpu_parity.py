@@ -341,3 +341,31 @@ def test_device_inputs_from_torch_stream(H, handle):
     kw0 = H.hs_factor_export(f, H.HS_FEXP_KW, 0)
     nleaf = H.hs_analysis_export(a, H.HS_EXP_LEAF_OFF).size - 1
     assert kn0.size == kw0.size == nleaf and kn0.sum() > 0 and kw0.sum() > 0
+
+
+@pytest.mark.gpu
+def test_small_level_path_agrees_with_batch_pipeline(H, handle, monkeypatch):
+    """Levels of small clusters run one device-planned kernel per wave (small.cu); the batch
+    pipeline (HS_NO_SMALL_LEVELS=1) computes the same factor: identical kept ranks and pivots,
+    the preconditioner to rounding.  (Both are compared with the oracle by the parity tests.)"""
+    from problems import gen_slab
+    p = gen_slab(64, 10, leaf_columns=8)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_columns=8)
+    L = H.hs_analysis_get_info(a)["L_top"]
+    v = np.random.default_rng(12).standard_normal(p.n)
+
+    def run(**env):
+        monkeypatch.delenv("HS_NO_SMALL_LEVELS", raising=False)
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
+        out = ([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)],
+               [H.hs_factor_export(f, H.HS_FEXP_PIV, l) for l in range(L)], H.hs_apply(f, v))
+        del f
+        return out
+
+    r0, p0, x0 = run()
+    r1, p1, x1 = run(HS_NO_SMALL_LEVELS="1")
+    assert all(np.array_equal(u, w) for u, w in zip(r0, r1))
+    assert all(np.array_equal(u, w) for u, w in zip(p0, p1))
+    assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
