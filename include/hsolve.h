@@ -155,7 +155,9 @@ typedef struct {
   int32_t max_m;         /* largest cluster size eliminated                             */
   int32_t max_rank;
   double  t_phase_s[8];  /* per-kernel-class device time: 0 gather 1 potrf 2 trsm 3 cpqr
-                            4 schur 5 writeback/assemble 6 top 7 host planning (wall).
+                            (and the fused elimination of small-cluster levels, all of whose
+                            flops are counted in flops_phase[3]) 4 schur 5 writeback/assemble
+                            6 top 7 host planning (wall).
                             Entries 0-6 are measured with CUDA events between the kernels
                             only when HS_PHASE_EVENTS=all (or =cpqr: entry 3 only) is set
                             at factor time — the events cost stream time per batch; they

@@ -945,7 +945,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       small = cap[s] <= SMALL_M && kn_cap[s] + kw_cap[s] <= SMALL_K;
       small_m = std::max(small_m, cap[s]);
       small_k = std::max<int>(small_k, (int)(kn_cap[s] + kw_cap[s]));
-      small_nseg = std::max<int>(small_nseg, nn + (int)lev.w[s].size());
+      small_nseg = std::max<int>(small_nseg, nn + (int)lev.w[s].size());   // raw entries (empty ones included)
       small_np = std::max(small_np, nn * (nn + 1) / 2);
     }
     if (small) {
@@ -1050,11 +1050,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.max_rank = std::max(S.max_rank, r);
         double fq = 0.0;
         for (int j = 0; j < r; ++j) fq += 4.0 * (m - j) * (double)(kw - j) + 4.0 * (m - j) * (double)kn;
-        S.flops += (double)m * m * m / 3.0 + (double)m * m * (kn + kw) + fq + (double)K * kn * (kn + 1);
-        S.flops_phase[1] += (double)m * m * m / 3.0;
-        S.flops_phase[2] += (double)m * m * (kn + kw);
-        S.flops_phase[3] += fq;
-        S.flops_phase[4] += (double)K * kn * (kn + 1);
+        const double all = (double)m * m * m / 3.0 + (double)m * m * (kn + kw) + fq + (double)K * kn * (kn + 1);
+        S.flops += all;
+        S.flops_phase[3] += all;   // the fused small-cluster kernel is timed as one phase (entry 3)
       }
     }
     for (size_t bidx = 0; bidx < (small ? 0 : lev.batches.size()); ++bidx) {

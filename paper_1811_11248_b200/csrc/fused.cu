@@ -164,26 +164,47 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
   double* gi = sm;                  // mp x ldg, G^{-1} (zeros above the diagonal and below m)
   double* x = sm + (size_t)mp * ldg;   // mp x SM_LDX
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int e = tid; e < mp * ldg; e += blockDim.x) {
-    const int i = e / ldg, k = e % ldg;
-    gi[e] = (i < m && k <= i) ? it.Ginv[(int64_t)i * m + k] : 0.0;
+  // staging: every thread issues 4 independent global loads before its shared stores (the
+  // kernel is bound by the latency of these loads at a few CTAs per SM)
+  for (int e0 = tid; e0 < mp * ldg; e0 += 4 * 256) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + 256 * u, i = e / ldg, k = e % ldg;
+      v[u] = (e < mp * ldg && i < m && k <= i) ? it.Ginv[(int64_t)i * m + k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + 256 * u < mp * ldg) gi[e0 + 256 * u] = v[u];
   }
   for (int e = tid; e < mp * SM_LDX; e += blockDim.x) x[e] = 0.0;
   __syncthreads();
   for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {   // the tile's columns from the store
     const FusedSeg sgm = segs[sg];
     const int j0 = max(it.c0, sgm.col), j1 = min(it.c0 + it.nc, sgm.col + sgm.len);
-    const int wd = j1 - j0;
-    if (sgm.trans) {
-      for (int e = tid; e < m * wd; e += blockDim.x) {   // consecutive threads: consecutive rows i
-        const int j = j0 + e / m, i = e % m;
-        x[i * SM_LDX + (j - it.c0)] = sgm.src[(int64_t)(j - sgm.col) * sgm.sld + i];
+    const int wd = j1 - j0, tot = m * wd;
+    for (int e0 = tid; e0 < tot; e0 += 4 * 256) {
+      double v[4];
+      int dst[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + 256 * u;
+        int i, j;
+        if (sgm.trans) {   // consecutive threads: consecutive rows i
+          j = j0 + e / m;
+          i = e % m;
+        } else {
+          i = e / wd;
+          j = j0 + e % wd;
+        }
+        dst[u] = e < tot ? i * SM_LDX + (j - it.c0) : -1;
+        v[u] = e < tot ? (sgm.trans ? sgm.src[(int64_t)(j - sgm.col) * sgm.sld + i]
+                                    : sgm.src[(int64_t)i * sgm.sld + (j - sgm.col)])
+                       : 0.0;
       }
-    } else {
-      for (int e = tid; e < m * wd; e += blockDim.x) {
-        const int i = e / wd, j = j0 + e % wd;
-        x[i * SM_LDX + (j - it.c0)] = sgm.src[(int64_t)i * sgm.sld + (j - sgm.col)];
-      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dst[u] >= 0) x[dst[u]] = v[u];
     }
   }
   __syncthreads();

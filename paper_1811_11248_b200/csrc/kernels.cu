@@ -329,10 +329,11 @@ __global__ void __launch_bounds__(256) k_form_T(const FormTItem* __restrict__ it
   double* x;
   if (gs) {
     double* gg = sm;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int i = e / m, k = e % m;
-      gg[e] = (k <= i) ? it.G[(int64_t)i * m + k] : 0.0;
-    }
+    if (!it.Ginv)   // G^{-1} given: no substitution, G is not needed
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int i = e / m, k = e % m;
+        gg[e] = (k <= i) ? it.G[(int64_t)i * m + k] : 0.0;
+      }
     g = gg;
     ldg = m;
     x = sm + m * m;

@@ -88,52 +88,62 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
   __shared__ double* Dss;
   __shared__ int ldss;
   const int m = a.live[s];
-  if (tid == 0) {
-    failed = 0;
+  // segment table: the directory lookups and live-size reads run in parallel (a serial chain
+  // of dependent global loads in one thread would dominate a cluster of a few DOFs)
+  const int nw0 = a.wptr[s + 1] - a.wptr[s], nn0 = a.nptr[s + 1] - a.nptr[s], nall = nw0 + nn0;
+  if (tid == 0) failed = (nall > NX) ? 2 : 0;
+  __syncthreads();
+  if (!failed) {
+    for (int t = tid; t < nall; t += ST) {   // raw (uncompacted) entries in slots [0, nall)
+      const int q = t < nw0 ? a.widx[a.wptr[s] + t] : a.nidx[a.nptr[s] + t - nw0];
+      const int L = a.live[q];
+      slen[t] = L;
+      sq[t] = q;
+      const int p0 = max(s, q), q0 = min(s, q);
+      const int64_t o = L > 0 ? sdir_find(a.dir, p0, q0) : 0;
+      if (o < 0) failed = 2;
+      sptr[t] = L > 0 ? a.dir.blk + o : nullptr;
+      sld[t] = a.dir.cap[q0];
+      strn[t] = q > s ? 1 : 0;
+    }
+    if (tid == 32) {
+      const int64_t od = sdir_find(a.dir, s, s);
+      Dss = od >= 0 ? a.dir.blk + od : nullptr;
+      ldss = a.dir.cap[s];
+      if (!Dss && m > 0) failed = 2;
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && !failed) {   // compact the empty neighbours away, column offsets (shared memory only)
     int col = 0, ns = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      const int32_t* lst = pass == 0 ? a.widx + a.wptr[s] : a.nidx + a.nptr[s];
-      const int cnt = pass == 0 ? a.wptr[s + 1] - a.wptr[s] : a.nptr[s + 1] - a.nptr[s];
-      for (int t = 0; t < cnt; ++t) {
-        const int q = lst[t], L = a.live[q];
-        if (L == 0) continue;
-        const int p0 = max(s, q), q0 = min(s, q);
-        const int64_t o = sdir_find(a.dir, p0, q0);
-        if (o < 0 || ns >= NX) {
-          failed = 2;
-          continue;
-        }
-        sptr[ns] = a.dir.blk + o;
-        scol[ns] = col;
-        slen[ns] = L;
-        sld[ns] = a.dir.cap[q0];
-        strn[ns] = q > s ? 1 : 0;
-        sq[ns] = q;
-        ++ns;
-        col += L;
-      }
-      if (pass == 0) {
+    for (int t = 0; t < nall; ++t) {
+      if (t == nw0) {
         kw = col;
         nw_seg = ns;
       }
+      if (slen[t] == 0) continue;
+      sptr[ns] = sptr[t];
+      slen[ns] = slen[t];
+      sld[ns] = sld[t];
+      strn[ns] = strn[t];
+      sq[ns] = sq[t];
+      scol[ns] = col;
+      col += slen[ns];
+      ++ns;
+    }
+    if (nw0 == nall) {
+      kw = col;
+      nw_seg = ns;
     }
     nseg = ns;
     kn = col - kw;
-    const int64_t od = sdir_find(a.dir, s, s);
-    Dss = od >= 0 ? a.dir.blk + od : nullptr;
-    ldss = a.dir.cap[s];
-    if (!Dss && m > 0) failed = 2;
-    // Schur pairs (a >= b over the non-empty n-segments, ascending cluster id)
-    int np = 0, e = 0;
+    int np = 0, e = 0;   // Schur pairs (x >= y over the non-empty n-segments, ascending cluster id)
     for (int x = nw_seg; x < ns; ++x)
       for (int y = nw_seg; y <= x; ++y) {
         if (np >= PX) {
           failed = 2;
           break;
         }
-        const int64_t o = sdir_find(a.dir, sq[x], sq[y]);
-        if (o < 0) failed = 2;
-        pptr[np] = o >= 0 ? a.dir.blk + o : nullptr;
         pa[np] = x;
         pb[np] = y;
         poff[np] = e;
@@ -142,12 +152,20 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
       }
     poff[np] = e;
     npair = np;
-    if (failed == 2 && atomicCAS(&a.status->flag, 0, 2) == 0) {
-      a.status->level = a.level;
-      a.status->cluster = s;
-      a.status->pivot = -1;
-      a.status->value = 0.0;
+  }
+  __syncthreads();
+  if (!failed)
+    for (int t = tid; t < npair; t += ST) {   // the target blocks of the pairs, in parallel
+      const int64_t o = sdir_find(a.dir, sq[pa[t]], sq[pb[t]]);
+      if (o < 0) failed = 2;
+      pptr[t] = o >= 0 ? a.dir.blk + o : nullptr;
     }
+  __syncthreads();
+  if (tid == 0 && failed == 2 && atomicCAS(&a.status->flag, 0, 2) == 0) {
+    a.status->level = a.level;
+    a.status->cluster = s;
+    a.status->pivot = -1;
+    a.status->value = 0.0;
   }
   __syncthreads();
   if (failed) return;
