@@ -67,10 +67,9 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
   const int MX = a.m_max, KX = a.k_max, NX = a.nseg_max, PX = a.npair_max;
   // shared memory carve-up (the host sizes it from the same formula: small_smem_bytes)
   double* G = sm;                            // MX x (MX + 1): A_ss, then its lower factor
-  double* B = G + MX * (MX + 1);             // MX x KX row-major (ld k): [B_w | B_n]
-  double* V = B + (size_t)MX * KX;           // MX x MX: reflector j in row j
-  double* X = V + MX * MX;                   // MX x MX: G^{-1}, then T_s
-  double* tau = X + MX * MX;                 // MX
+  double* B = G + MX * (MX + 1);             // MX x (KX + MX) row-major (ld kb): [B_w | B_n | G^{-1}]
+  double* V = B + (size_t)MX * (KX + MX);    // MX x MX: reflector j in row j
+  double* tau = V + MX * MX;                 // MX
   double* nu = tau + MX;                     // KX column norms (-1: pivoted)
   double* red = nu + KX;                     // 8 (+ 8 ints)
   int* redi = (int*)(red + 8);
@@ -170,6 +169,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
   __syncthreads();
   if (failed) return;
   const int k = kw + kn;
+  const int kb = k + m;   // B = [A_sw | A_sn | I_m]: the substitution also forms G^{-1}, the rotation Qᵀ G^{-1} = T_s
   if (m == 0) {
     if (tid == 0) {
       a.rank[s] = 0;
@@ -178,23 +178,36 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     }
     return;
   }
-  // ---- load A_ss (lower triangle of the stored diagonal block) and [A_sw | A_sn] ----------
+  // ---- load A_ss (lower triangle of the stored diagonal block) and [A_sw | A_sn | I] --------
   for (int e = tid; e < m * m; e += ST) {
     const int i = e / m, j = e % m;
     G[i * (MX + 1) + j] = j <= i ? Dss[(int64_t)i * ldss + j] : 0.0;
+    B[i * kb + k + j] = (i == j) ? 1.0 : 0.0;
   }
-  for (int g = 0; g < nseg; ++g) {
-    const double* p = sptr[g];
-    const int L = slen[g], ld = sld[g], c0 = scol[g];
-    if (strn[g]) {
-      for (int e = tid; e < m * L; e += ST) {   // consecutive threads: consecutive rows i
-        const int j = e / m, i = e % m;
-        B[i * k + c0 + j] = p[(int64_t)j * ld + i];
+  {   // every element of [A_sw | A_sn]: 4 independent global loads in flight per thread
+    const int tot = m * k;
+    for (int e0 = tid; e0 < tot; e0 += 4 * ST) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * ST;
+        v[u] = 0.0;
+        if (e < tot) {
+          const int i = e / k, c = e % k;
+          int lo = 0, hi = nseg - 1;   // the segment holding column c
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (scol[mid] <= c) lo = mid;
+            else hi = mid - 1;
+          }
+          const int j = c - scol[lo];
+          v[u] = strn[lo] ? sptr[lo][(int64_t)j * sld[lo] + i] : sptr[lo][(int64_t)i * sld[lo] + j];
+        }
       }
-    } else {
-      for (int e = tid; e < m * L; e += ST) {
-        const int i = e / L, j = e % L;
-        B[i * k + c0 + j] = p[(int64_t)i * ld + j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * ST;
+        if (e < tot) B[(e / k) * kb + (e % k)] = v[u];
       }
     }
   }
@@ -223,12 +236,12 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     }
     __syncthreads();
   }
-  // ---- B = G⁻¹ [A_sw | A_sn]: forward substitution, a thread per column --------------------
-  for (int c = tid; c < k; c += ST) {
+  // ---- B = G⁻¹ [A_sw | A_sn | I]: forward substitution, a thread per column ------------------
+  for (int c = tid; c < kb; c += ST) {
     for (int i = 0; i < m; ++i) {
-      double b = B[i * k + c];
-      for (int l = 0; l < i; ++l) b -= G[i * (MX + 1) + l] * B[l * k + c];
-      B[i * k + c] = b / G[i * (MX + 1) + i];
+      double b = B[i * kb + c];
+      for (int l = 0; l < i; ++l) b -= G[i * (MX + 1) + l] * B[l * kb + c];
+      B[i * kb + c] = b / G[i * (MX + 1) + i];
     }
   }
   __syncthreads();
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
   double rn = 0.0;
   for (int c = kw + tid; c < k; c += ST) {
     double s2 = 0.0;
-    for (int i = 0; i < m; ++i) s2 += B[i * k + c] * B[i * k + c];
+    for (int i = 0; i < m; ++i) s2 += B[i * kb + c] * B[i * kb + c];
     rn = fmax(rn, sqrt(s2));
   }
   const double Rn = block_max(rn, red);
@@ -251,7 +264,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     for (int c = tid; c < kw; c += ST) {
       if (nu[c] < 0.0) continue;
       double s2 = 0.0;
-      for (int i = j; i < m; ++i) s2 += B[i * k + c] * B[i * k + c];
+      for (int i = j; i < m; ++i) s2 += B[i * kb + c] * B[i * kb + c];
       nu[c] = sqrt(s2);
       lmax = fmax(lmax, nu[c]);
     }
@@ -275,9 +288,9 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     // dlarfg of column p, rows j..m-1 (one warp)
     if (tid < 32) {
       double xs = 0.0;
-      for (int l = j + 1 + tid; l < m; l += 32) xs += B[l * k + p] * B[l * k + p];
+      for (int l = j + 1 + tid; l < m; l += 32) xs += B[l * kb + p] * B[l * kb + p];
       for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-      const double alpha = B[j * k + p], xnorm = sqrt(xs);
+      const double alpha = B[j * kb + p], xnorm = sqrt(xs);
       double t, beta, rden;
       if (xnorm == 0.0) {
         t = 0.0;
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
         t = (beta - alpha) / beta;
         rden = 1.0 / (alpha - beta);
       }
-      for (int l = tid; l < m; l += 32) V[j * MX + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : B[l * k + p] * rden;
+      for (int l = tid; l < m; l += 32) V[j * MX + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : B[l * kb + p] * rden;
       if (tid == 0) {
         tau[j] = t;
         red[7] = beta;
@@ -301,51 +314,36 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     for (int c = tid; c < kw; c += ST) {
       if (c == p || nu[c] < 0.0 || t == 0.0) continue;
       double w = 0.0;
-      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * k + c];
+      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * kb + c];
       const double tw = t * w;
-      for (int l = j; l < m; ++l) B[l * k + c] -= tw * V[j * MX + l];
+      for (int l = j; l < m; ++l) B[l * kb + c] -= tw * V[j * MX + l];
     }
     __syncthreads();
     if (tid == 0) {
-      B[j * k + p] = beta;
-      for (int l = j + 1; l < m; ++l) B[l * k + p] = 0.0;
+      B[j * kb + p] = beta;
+      for (int l = j + 1; l < m; ++l) B[l * kb + p] = 0.0;
       nu[p] = -1.0;
     }
     __syncthreads();
   }
   __syncthreads();
   const int r = kw > 0 ? rr : 0, K = m - r;
-  // ---- E_s on the n-columns: Qᵀ B_n (H_0 first) ----------------------------------------------
-  for (int c = kw + tid; c < k; c += ST)
+  // ---- E_s on the n-columns and on G⁻¹: Qᵀ B_n and T_s = Qᵀ G⁻¹ (H_0 first) ---------------------
+  for (int c = kw + tid; c < kb; c += ST)
     for (int j = 0; j < r; ++j) {
       if (tau[j] == 0.0) continue;
       double w = 0.0;
-      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * k + c];
+      for (int l = j; l < m; ++l) w += V[j * MX + l] * B[l * kb + c];
       const double tw = tau[j] * w;
-      for (int l = j; l < m; ++l) B[l * k + c] -= tw * V[j * MX + l];
+      for (int l = j; l < m; ++l) B[l * kb + c] -= tw * V[j * MX + l];
     }
-  // ---- T_s = Qᵀ G⁻¹ (the apply operator), a thread per column ---------------------------------
-  for (int c = tid; c < m; c += ST) {
-    for (int i = 0; i < m; ++i) {
-      double x = (i == c) ? 1.0 : 0.0;
-      for (int l = c; l < i; ++l) x -= G[i * (MX + 1) + l] * X[l * MX + c];
-      X[i * MX + c] = i < c ? 0.0 : x / G[i * (MX + 1) + i];
-    }
-    for (int j = 0; j < r; ++j) {
-      if (tau[j] == 0.0) continue;
-      double w = 0.0;
-      for (int l = j; l < m; ++l) w += V[j * MX + l] * X[l * MX + c];
-      const double tw = tau[j] * w;
-      for (int l = j; l < m; ++l) X[l * MX + c] -= tw * V[j * MX + l];
-    }
-  }
   __syncthreads();
   double* T = a.T + a.toff[s];
-  for (int e = tid; e < m * m; e += ST) T[e] = X[(e / m) * MX + (e % m)];
+  for (int e = tid; e < m * m; e += ST) T[e] = B[(e / m) * kb + k + (e % m)];   // T_s row-major
   // ---- C_s = rows [r, m) of the rotated B_n into the factor record (ld kn) -----------------
   if (kn > 0 && K > 0) {
     double* C = a.C + a.coff[s];
-    for (int e = tid; e < K * kn; e += ST) C[e] = B[(r + e / kn) * k + kw + e % kn];
+    for (int e = tid; e < K * kn; e += ST) C[e] = B[(r + e / kn) * kb + kw + e % kn];
   }
   // ---- write-back of row s: I_r on (s, s), the coarse rows into the blocks (s, q) -----------
   for (int e = tid; e < r * r; e += ST) {
@@ -358,12 +356,12 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     if (strn[g]) {
       for (int e = tid; e < r * L; e += ST) {
         const int j = e / r, i = e % r;
-        p[(int64_t)j * ld + i] = B[i * k + c0 + j];
+        p[(int64_t)j * ld + i] = B[i * kb + c0 + j];
       }
     } else {
       for (int e = tid; e < r * L; e += ST) {
         const int i = e / L, j = e % L;
-        p[(int64_t)i * ld + j] = B[i * k + c0 + j];
+        p[(int64_t)i * ld + j] = B[i * kb + c0 + j];
       }
     }
   }
@@ -390,7 +388,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
       }
       const int cp = scol[x] - kw + i, cq = scol[y] - kw + j;
       double acc = 0.0;
-      for (int kk = 0; kk < K; ++kk) acc += B[(r + kk) * k + kw + cp] * B[(r + kk) * k + kw + cq];
+      for (int kk = 0; kk < K; ++kk) acc += B[(r + kk) * kb + kw + cp] * B[(r + kk) * kb + kw + cq];
       double* tgt = pptr[lo] + (int64_t)i * a.dir.cap[sq[y]] + j;   // block (p, q): row-major, ld cap[q]
       *tgt -= acc;
     }
@@ -406,7 +404,8 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
 }  // namespace
 
 size_t small_smem_bytes(int m_max, int k_max, int nseg_max, int npair_max) {
-  const size_t d = (size_t)m_max * (m_max + 1) + (size_t)m_max * k_max + 2 * (size_t)m_max * m_max + m_max + k_max + 16;
+  const size_t d = (size_t)m_max * (m_max + 1) + (size_t)m_max * (k_max + m_max) + (size_t)m_max * m_max + m_max +
+                   k_max + 16;
   const size_t pbytes = sizeof(double*) * (size_t)(nseg_max + npair_max);
   const size_t ibytes = sizeof(int) * (size_t)(5 * nseg_max + 1 + (nseg_max & 1) + 3 * npair_max + 1);
   return d * sizeof(double) + pbytes + ibytes + 64;
