@@ -552,11 +552,11 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restri
 // a4 on the n-columns: one CTA per tile of NGRP = CQ_THREADS / G columns of one cluster.
 template <int MR, int G>
 __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, int r, const double* Vs,
-                                            const double* ts) {
-  const int m = it.m, ld = it.ldB;
+                                            const double* ts, bool tcols) {
+  const int m = it.m, ld = tcols ? m : it.ldB;
   const int tid = threadIdx.x, t = tid % G, grp = tid / G;
   const bool act = grp < nc;
-  double* col = it.B + it.kw + c0 + grp;
+  const double* col = tcols ? it.Ginv + c0 + grp : it.B + it.kw + c0 + grp;
   double x[MR];
 #pragma unroll
   for (int i = 0; i < MR; ++i) {
@@ -578,11 +578,20 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
 #pragma unroll
     for (int i = 0; i < MR; ++i) x[i] -= td * vv[i];
   }
+  if (tcols) {   // T_s[:, c0 + grp] (row-major m x m)
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int l = t + i * G;
+      if (act && l < m) it.Tout[(size_t)l * m + c0 + grp] = x[i];
+    }
+    return;
+  }
+  double* colw = const_cast<double*>(col);
   if (!it.dwb || it.keepB)
 #pragma unroll
     for (int i = 0; i < MR; ++i) {
       const int l = t + i * G;
-      if (act && l < m) col[(size_t)l * ld] = x[i];
+      if (act && l < m) colw[(size_t)l * ld] = x[i];
     }
   if (it.dwb && act) {   // coarse-n rows into the store blocks (s, q), C rows into the slab
     const int jn = c0 + grp;
@@ -610,7 +619,8 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
   const TrsmItem ti = items[blockIdx.x];
   const CluItem it = clu[ti.ci];
   const int r = rank[ti.ci];
-  if (it.m == 0 || (r == 0 && !it.dwb)) return;   // dwb with r = 0: C = B_n still goes to its slab
+  const bool tcols = ti.pad == 1;   // a tile of T_s = Qᵀ G^{-1}
+  if (it.m == 0 || (r == 0 && !it.dwb && !tcols)) return;   // dwb with r = 0: C = B_n still goes to its slab
   // reflectors staged in shared memory when they fit, else read through L1
   const bool staged = (size_t)it.m * r + r <= (size_t)cap_words;
   const double* Vs = it.V;
@@ -623,12 +633,12 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
     ts = rsm + (size_t)it.m * r;
   }
   switch (cq_group(it.m, MR)) {
-    case 1: rotate_body<MR, 1>(it, ti.c0, ti.nc, r, Vs, ts); break;
-    case 2: rotate_body<MR, 2>(it, ti.c0, ti.nc, r, Vs, ts); break;
-    case 4: rotate_body<MR, 4>(it, ti.c0, ti.nc, r, Vs, ts); break;
-    case 8: rotate_body<MR, 8>(it, ti.c0, ti.nc, r, Vs, ts); break;
-    case 16: rotate_body<MR, 16>(it, ti.c0, ti.nc, r, Vs, ts); break;
-    default: rotate_body<MR, 32>(it, ti.c0, ti.nc, r, Vs, ts); break;
+    case 1: rotate_body<MR, 1>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
+    case 2: rotate_body<MR, 2>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
+    case 4: rotate_body<MR, 4>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
+    case 8: rotate_body<MR, 8>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
+    case 16: rotate_body<MR, 16>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
+    default: rotate_body<MR, 32>(it, ti.c0, ti.nc, r, Vs, ts, tcols); break;
   }
 }
 

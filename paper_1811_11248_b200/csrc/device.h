@@ -77,6 +77,9 @@ struct CluItem {
   // slices live column-major in this scratch ((kw + 16) x (m + 16) doubles, coalesced group
   // loads) instead of shared memory; null = shared-memory mode
   double* Wt;
+  // the apply operator formed by k_rotate_n: T_s = Qᵀ G_s^{-1} from k_chol's G^{-1} (fused path)
+  const double* Ginv;
+  double* Tout;
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
@@ -108,7 +111,7 @@ struct FusedSeg {             // block (s, q) of the store: B_s columns [col, co
 constexpr int CI_MAX_M = 112;   // k_scale_tile: G (ld m + 1) and a 64-column tile in shared memory, <= 28 rows per lane
 
 struct TrsmItem {   // one column tile of one cluster's B_s
-  int32_t ci, c0, nc, pad;
+  int32_t ci, c0, nc, pad;   // k_rotate_n: pad = 1 for a tile of T_s = Qᵀ G_s^{-1} (columns of Ginv)
 };
 
 // Schur target tile (a5):

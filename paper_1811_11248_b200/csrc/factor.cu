@@ -1195,6 +1195,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           const int32_t rw = rot_tile_cols(m, max_m);
           for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
         }
+        if (fused) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
+          it.Ginv = ginv;
+          it.Tout = L.T[s];
+          const int32_t rw = rot_tile_cols(m, max_m);
+          for (int32_t c0 = 0; c0 < m; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, m - c0), 1});
+        }
         S.flops += (double)m * m * m / 3.0 + (double)m * m * ldB;
         S.flops_phase[1] += (double)m * m * m / 3.0;
         S.flops_phase[2] += (double)m * m * ldB;
@@ -1289,10 +1295,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         const int32_t m = live[s], kn = L.kn[s], ldB = L.ldB[s];
         if (m == 0) continue;
         Pend pd{s, (int32_t)k, mine, -1, -1, -1, -1, wb.size(), wb.size()};
-        if (mine) {
+        if (mine && !fused) {   // (fused: k_rotate_n forms T_s from k_chol's G^{-1})
           pd.ft = (int64_t)ft.size();
-          const double* gi = fused ? L.B[s] + (((int64_t)m * ldB + 3) & ~int64_t(3)) : nullptr;   // k_chol's G^{-1}
-          ft.push_back(FormTItem{L.G[s], gi, L.V[s], L.tau[s], L.T[s], m, 0});
+          ft.push_back(FormTItem{L.G[s], nullptr, L.V[s], L.tau[s], L.T[s], m, 0});
           ft_max_m = std::max(ft_max_m, m);
         }
         // neighbour column offsets inside the n-part
