@@ -359,7 +359,11 @@ def run_ours(args, rank, world, local):
     if names[dom] in ("potrf", "trsm", "cpqr", "schur", "top"):
         achieved = fl_ph[dom] / t_ph[dom] / 1e12
         peak = alu_peak if alu_peak else None
-        roof = {"bound": "alu", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        roof = {"bound": "alu", "kernel": names[dom],
+                "kernels": {"cpqr": "k_cpqr3 (+ k_elim_small: the fused elimination of small-cluster levels)",
+                            "potrf": "k_chol (+ G^-1)", "trsm": "k_scale_mma (DMMA)", "schur": "k_schur3 (DMMA)",
+                            "top": "dense_potrf"}.get(names[dom], names[dom]),
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if peak else None, "traffic": None,
                 "peak_source": "profiles/fp64_peaks.json dfma_tflops (FFMA.F64 chain, measured on this pool's B200)"
                 if peak else "FP64 peak not measured yet"}
@@ -370,7 +374,7 @@ def run_ours(args, rank, world, local):
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (tools/profile_round.sh -> profiles/*_traffic.json; one representative launch)
     tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
-    if tp:
+    if tp and args.config == "C3":   # the committed capture is of the default workload
         tr = json.load(open(os.path.join(ROOT, "profiles", tp[-1])))
         if tr.get("class") == roof["kernel"]:
             roof["traffic"] = tr["dram_bytes_per_launch"]
@@ -408,7 +412,7 @@ def run_ours(args, rank, world, local):
     roof["spmv"] = bw(spmv_bytes, t_spmv, n_spmv)
     for key in ("apply", "spmv"):
         tf = os.path.join(ROOT, "profiles", f"r02_traffic_{key}.json")
-        if roof[key] and os.path.exists(tf):
+        if roof[key] and os.path.exists(tf) and args.config == "C3":
             tr = json.load(open(tf))
             roof[key]["traffic"] = tr.get("dram_bytes_per_launch")
             roof[key]["traffic_source"] = f"profiles/r02_traffic_{key}.json: {tr.get('note', '')}"
