@@ -190,6 +190,8 @@ void hs_destroy(hs_handle h) {
   }
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->side) cudaStreamSynchronize(h->side);
+  if (h->h_rank) cudaFreeHost(h->h_rank);
+  if (h->pub) cudaFreeHost(h->pub);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);

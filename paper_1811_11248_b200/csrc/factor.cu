@@ -655,6 +655,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   f->keep_records = std::getenv("HS_KEEP_RECORDS") != nullptr;
   double t_plan = 0.0;
   double t_rank_wait = 0.0;   // host blocked on the previous batch's ranks (HS_PROFILE)
+  double t_launch = 0.0;      // host time issuing a batch's uploads and kernels (HS_PROFILE)
   double t_apply_plan = 0.0;  // apply planning (host worker)
   std::future<void> plan_prev;  // the chain of per-level apply-plan tasks (joined before upload)
   double t_sub[4] = {0, 0, 0, 0};
@@ -664,6 +665,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   HS_CUDA(cudaEventCreate(&ev0));
   HS_CUDA(cudaEventCreate(&ev1));
   HS_CUDA(cudaEventRecord(ev0, st));
+  std::vector<std::pair<const char*, double>> tl{{"start", now_s()}};   // host timeline (HS_PROFILE)
   f->d_rowptr = an->d_rowptr;      // borrowed from the analysis
   f->d_colind = an->d_colind;
   f->d_perm = an->d_perm;
@@ -675,10 +677,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   HS_CUDA(cudaMemcpyAsync(f->d_vals, values, sizeof(double) * nnz,
                           opt.values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
 
-  DevStatus* d_status = nullptr;
   DevStatus h_status{};
-  HS_CUDA(cudaMalloc(&d_status, sizeof(DevStatus)));
-  std::unique_ptr<void, void (*)(void*)> status_guard(d_status, [](void* p) { cudaFree(p); });
+  DevStatus* d_status = (DevStatus*)dc.alloc(sizeof(DevStatus));
+  std::unique_ptr<void, std::function<void(void*)>> status_guard(d_status, [&dc](void* p) { dc.free(p); });
   HS_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), st));
   // numerical symmetry of the values (A SPD, A_ns = A_sn^T), checked on the device
   launch_symcheck(f->d_vals, an->d_tmap, nnz, &d_status->pivot, st);
@@ -687,6 +688,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (h_status.pivot) fail(HS_E_NOT_SYMMETRIC, "factor: values are not symmetric");
   HS_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), st));
 
+  tl.push_back({"values + symmetry check", now_s()});
   // ---- level-0 blocks from the permuted CSR ------------------------------------------------
   const int nleaf0 = (int)(an->leaf_off.size() - 1);
   std::vector<int32_t> cap(nleaf0);
@@ -707,14 +709,22 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   int max_batch = 1;
   for (const auto& lev : an->levels)
     for (const auto& B : lev.batches) max_batch = std::max(max_batch, (int)B.size());
-  HS_CUDA(cudaMalloc(&d_rank, sizeof(int32_t) * max_batch));
-  HS_CUDA(cudaMallocHost(&h_rank, sizeof(int32_t) * max_batch));
-  std::unique_ptr<void, void (*)(void*)> rank_guard(d_rank, [](void* p) { cudaFree(p); });
-  std::unique_ptr<void, void (*)(void*)> hrank_guard(h_rank, [](void* p) { cudaFreeHost(p); });
-  // dpatch: ranks + status published by k_publish into mapped pinned memory (host spins on seq)
-  RankPub* pub = nullptr;
-  HS_CUDA(cudaHostAlloc((void**)&pub, sizeof(RankPub) + sizeof(int32_t) * max_batch, cudaHostAllocMapped));
-  std::unique_ptr<void, void (*)(void*)> pub_guard(pub, [](void* p) { cudaFreeHost(p); });
+  d_rank = (int32_t*)dc.alloc(sizeof(int32_t) * max_batch);
+  std::unique_ptr<void, std::function<void(void*)>> rank_guard(d_rank, [&dc](void* p) { dc.free(p); });
+  // dpatch: ranks + status published by k_publish into mapped pinned memory (host spins on seq);
+  // the pinned buffers live in the handle (allocating them costs milliseconds per factor)
+  if (h->pub_cap < max_batch) {
+    if (h->h_rank) cudaFreeHost(h->h_rank);
+    if (h->pub) cudaFreeHost(h->pub);
+    h->h_rank = nullptr;
+    h->pub = nullptr;
+    h->pub_cap = 0;
+    HS_CUDA(cudaMallocHost(&h->h_rank, sizeof(int32_t) * max_batch));
+    HS_CUDA(cudaHostAlloc(&h->pub, sizeof(RankPub) + sizeof(int32_t) * max_batch, cudaHostAllocMapped));
+    h->pub_cap = max_batch;
+  }
+  h_rank = h->h_rank;
+  RankPub* pub = (RankPub*)h->pub;
   RankPub* pub_dev = nullptr;
   HS_CUDA(cudaHostGetDevicePointer((void**)&pub_dev, pub, 0));
   pub->seq = 0;
@@ -780,6 +790,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (auto& e : lev_ev) cudaEventDestroy(e);
   });
   std::vector<double> lev_flops(an->L_top + 1, 0.0);
+  tl.push_back({"level-0 store + setup", now_s()});
   for (int l = 0; l < an->L_top; ++l) {
     HS_CUDA(cudaEventRecord(lev_ev[l], st));
     lev_flops[l] = S.flops;
@@ -1584,6 +1595,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upB.copy_in(jP, id_ptr); upB.copy_in(jL, id_ld); upB.copy_in(jR, id_r); upB.copy_in(jF, ft);
         upB.copy_in(jX, patch);
         t_plan += now_s() - tp1;
+        const double tl0 = now_s();
         const bool pub_here = (bool)first_half_launch;   // the patch kernel publishes the ranks
         if (first_half_launch) {   // device patch: both uploads, then the whole batch's kernels
           upA.send(st);
@@ -1606,6 +1618,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         launch_copy2d(upB.dptr<CopyItem>(jW), (int)wb.size(), st);
         launch_identity(upB.dptr<double*>(jP), upB.dptr<int32_t>(jL), upB.dptr<int32_t>(jR), (int)id_ptr.size(), st);
         pt.rec(pt.b[2], st);
+        t_launch += now_s() - tl0;
         pt.b_pending = true;
         // apply operators T_s = U^T G^{-1} of the batch on the side stream (they are only
         // read by the apply): reads the workspace's G, V, tau, so the workspace (and the
@@ -1930,6 +1943,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   }
   HS_CUDA(cudaEventRecord(lev_ev[an->L_top], st));
   lev_flops[an->L_top] = S.flops;
+  tl.push_back({"levels", now_s()});
   // ---- top: dense Cholesky of all live DOFs, on rank 0 -------------------------
   {
     const int ntc = (int)cap.size();
@@ -2038,7 +2052,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
   if (std::getenv("HS_PROFILE") || std::getenv("HS_RANK_WAIT"))
-    std::fprintf(stderr, "[hs profile] host blocked on batch ranks: %.1f ms of %.1f ms\n", 1e3 * t_rank_wait, ms);
+    std::fprintf(stderr, "[hs profile] host blocked on batch ranks: %.1f ms of %.1f ms; issuing uploads + kernels %.1f ms\n",
+                 1e3 * t_rank_wait, ms, 1e3 * t_launch);
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] device cache: in use %.2f GB, peak %.2f GB, cached %.2f GB\n", dc.in_use / 1e9,
                  dc.peak / 1e9, dc.cached / 1e9);
@@ -2055,6 +2070,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     }
   fb += 8.0 * (double)f->ntop * (f->ntop + 1) / 2;
   S.factor_bytes = fb;
+  tl.push_back({"top + join", now_s()});
   // ---- device apply plan ----------------------------------------------------------------
   ap.vtotal = vbase;
   const double tj0 = now_s();
@@ -2097,6 +2113,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   }
   HS_CUDA(cudaStreamSynchronize(st));
   if (dist) dist_solve_build(f, DP);
+  tl.push_back({"apply plan upload", now_s()});
+  if (prof) {
+    std::fprintf(stderr, "[hs profile] host timeline:");
+    for (size_t i = 1; i < tl.size(); ++i) std::fprintf(stderr, " %s %.1f ms |", tl[i].first, 1e3 * (tl[i].second - tl[i - 1].second));
+    std::fprintf(stderr, "\n");
+  }
   return guard.release();
 }
 

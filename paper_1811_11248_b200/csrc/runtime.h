@@ -282,6 +282,10 @@ struct hs_handle_s {
   hs::VmmPool vmm;              // physical chunks of the block stores (destroyed after the cache)
   hs::DevCache cache;           // declared before the staging buffers (destroyed after them)
   hs::Upload upA, upB, upC;     // descriptor staging, reused across factors
+  // per-factor host buffers kept across factors (pinned / mapped allocations cost milliseconds)
+  int32_t* h_rank = nullptr;    // pinned, pub_cap entries
+  void* pub = nullptr;          // mapped RankPub + pub_cap ranks
+  int pub_cap = 0;
 };
 
 struct hs_factor_s {

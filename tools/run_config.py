@@ -33,6 +33,7 @@ for rep in range(int(os.environ.get("REPS", "2"))):
     print(f"factor wall {time.time()-t:.2f}s dev {st['t_factor_s']:.3f}s batches {st['n_batches']} levels {st['n_levels']} "
           f"max_m {st['max_m']} max_r {st['max_rank']} n_top {st['n_top']} GF {st['flops']/1e9:.1f} GB {st['factor_bytes']/1e9:.2f}",
           flush=True)
+    print("  level device times (ms):", [round(1e3 * t, 2) for t in st["t_level_s"]], flush=True)
     x, rep_ = H.hs_pcg(f, p.b, tol=p.tol, raise_not_converged=False)
     print("pcg", {k: rep_[k] for k in ("iters", "converged", "relres_true", "t_pcg_s")}, flush=True)
     if rep == 0:
