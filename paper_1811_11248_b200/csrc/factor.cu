@@ -346,26 +346,36 @@ struct BlockStore {
   int32_t* d_q = nullptr;
   int64_t* d_off = nullptr;
   int32_t* d_cap = nullptr;
-  void upload_dir() {
+  // the directory through one pinned staging buffer, no host synchronisation: the staging is
+  // rewritten only at the next level transition, after the stream has drained
+  void upload_dir(HostStage& hst) {
     const int n = (int)cap.size();
-    std::vector<int64_t> ptr(n + 1, 0), off;
-    std::vector<int32_t> qq;
+    size_t nq = 0;
+    for (int p = 0; p < n; ++p) nq += rows[p].size();
+    const size_t o_ptr = 0, o_off = o_ptr + 8 * (size_t)(n + 1), o_q = o_off + 8 * std::max<size_t>(nq, 1),
+                 o_cap = o_q + ((4 * std::max<size_t>(nq, 1) + 7) & ~size_t(7)), tot = o_cap + 4 * (size_t)std::max(n, 1);
+    hst.ensure(tot);
+    int64_t* ptr = (int64_t*)(hst.h + o_ptr);
+    int64_t* off = (int64_t*)(hst.h + o_off);
+    int32_t* qq = (int32_t*)(hst.h + o_q);
+    int32_t* cp = (int32_t*)(hst.h + o_cap);
+    size_t k = 0;
+    ptr[0] = 0;
     for (int p = 0; p < n; ++p) {
       for (const auto& e : rows[p]) {
-        qq.push_back(e.first);
-        off.push_back(e.second);
+        qq[k] = e.first;
+        off[k] = e.second;
+        ++k;
       }
-      ptr[p + 1] = (int64_t)qq.size();
+      ptr[p + 1] = (int64_t)k;
     }
-    d_ptr = (int64_t*)dc->alloc(sizeof(int64_t) * (n + 1));
-    d_q = (int32_t*)dc->alloc(sizeof(int32_t) * std::max<size_t>(qq.size(), 1));
-    d_off = (int64_t*)dc->alloc(sizeof(int64_t) * std::max<size_t>(off.size(), 1));
-    d_cap = (int32_t*)dc->alloc(sizeof(int32_t) * std::max(n, 1));
-    HS_CUDA(cudaMemcpyAsync(d_ptr, ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-    HS_CUDA(cudaMemcpyAsync(d_q, qq.data(), sizeof(int32_t) * qq.size(), cudaMemcpyHostToDevice, st));
-    HS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
-    HS_CUDA(cudaMemcpyAsync(d_cap, cap.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-    HS_CUDA(cudaStreamSynchronize(st));   // host vectors go out of scope
+    for (int p = 0; p < n; ++p) cp[p] = cap[p];
+    char* dev = (char*)dc->alloc(tot);
+    HS_CUDA(cudaMemcpyAsync(dev, hst.h, tot, cudaMemcpyHostToDevice, st));
+    d_ptr = (int64_t*)(dev + o_ptr);
+    d_off = (int64_t*)(dev + o_off);
+    d_q = (int32_t*)(dev + o_q);
+    d_cap = (int32_t*)(dev + o_cap);
   }
   BlockDir dir() const { return BlockDir{d, (int64_t)total, d_ptr, d_q, d_off, d_cap}; }
   // the store's users must have completed (the callers synchronise the stream first)
@@ -376,8 +386,7 @@ struct BlockStore {
     } else if (d) {
       dc->free(d);
     }
-    for (void* p : {(void*)d_ptr, (void*)d_q, (void*)d_off, (void*)d_cap})
-      if (p) dc->free(p);
+    if (d_ptr) dc->free(d_ptr);   // one allocation holds the whole directory
     forget();
   }
   void forget() {
@@ -697,7 +706,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc, &h->vmm,
            h->world > 1 && an->L_top > 0 ? &DP : nullptr, 0);   // mapped and zeroed
   launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
-  if (an->L_top > 0) bs.upload_dir();
+  if (an->L_top > 0) bs.upload_dir(h->dirstage);
 
   Upload& upA = h->upA;   // persistent per handle: pinned staging is allocated once
   Upload& upB = h->upB;
@@ -842,8 +851,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         L.T[s] = L.arena + oX[s];
       }
     // neighbour-pair target tables of the level (pattern-only; k_level_pairs)
-    LevelPairs lp;
-    lp.build(lev, bs, dc, upA, st);
+    LevelPairs lp;   // built below for the levels that run the batch pipeline
     std::vector<int32_t> live = cap;
     std::vector<uint8_t> done(lev.nclus, 0);   // eliminated (rank known here)
     // store offsets of row s's blocks, [w(s) ..., n(s) ...] (computed once per cluster)
@@ -1066,6 +1074,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         S.flops_phase[3] += all;   // the fused small-cluster kernel is timed as one phase (entry 3)
       }
     }
+    if (!small) lp.build(lev, bs, dc, upA, st);   // n(s)-pair target tables of the Schur tiles
     for (size_t bidx = 0; bidx < (small ? 0 : lev.batches.size()); ++bidx) {
       const auto& Bt = lev.batches[bidx];
       if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
@@ -1905,14 +1914,18 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       upA.copy_in(iA, asmb);
       upA.send(st);
       launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
-      HS_CUDA(cudaStreamSynchronize(st));   // the consumed child rows can go
-      bs.unmap_below((size_t)bs.rowbeg[std::min(2 * Pb, lev.nclus)] * sizeof(double));
+      if (bs.pool || Pb < nP) {   // VMM-backed: the consumed child rows can go (a group's staging is reused)
+        HS_CUDA(cudaStreamSynchronize(st));
+        bs.unmap_below((size_t)bs.rowbeg[std::min(2 * Pb, lev.nclus)] * sizeof(double));
+      }
       Pa = Pb;
     }
     pt.rec(pt.a[1], st);
     t_plan += now_s() - tp2;
     t_trans += now_s() - tp2;
-    HS_CUDA(cudaStreamSynchronize(st));
+    // the child store goes back to the stream-ordered cache without a host sync (cache-backed);
+    // a VMM-backed one is unmapped after the stream has drained
+    if (pt.on || bs.pool) HS_CUDA(cudaStreamSynchronize(st));
     pt.collect_b(S);
     if (pt.on) S.t_phase_s[5] += PhaseTimer::el(pt.a[0], pt.a[1]);
     const double tr1 = now_s();
@@ -1920,7 +1933,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     bs = std::move(nbs);
     nbs.forget();
     t_tr[3] += now_s() - tr1;
-    if (l + 1 < an->L_top) bs.upload_dir();
+    if (l + 1 < an->L_top) bs.upload_dir(h->dirstage);
     t_tr[1] += now_s() - tr1;
     cap = capn;
     if (prof) {

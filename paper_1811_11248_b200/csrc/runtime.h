@@ -282,6 +282,7 @@ struct hs_handle_s {
   hs::VmmPool vmm;              // physical chunks of the block stores (destroyed after the cache)
   hs::DevCache cache;           // declared before the staging buffers (destroyed after them)
   hs::Upload upA, upB, upC;     // descriptor staging, reused across factors
+  hs::HostStage dirstage;       // pinned staging of the level directories (one upload per level)
   // per-factor host buffers kept across factors (pinned / mapped allocations cost milliseconds)
   int32_t* h_rank = nullptr;    // pinned, pub_cap entries
   void* pub = nullptr;          // mapped RankPub + pub_cap ranks
