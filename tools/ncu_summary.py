@@ -8,6 +8,9 @@ hdr, units, data = rows[0], rows[1], rows[2:]
 want = {"Kernel Name": "kernel", "gpu__time_duration.sum": "duration",
         "dram__bytes_read.sum": "dram_read", "dram__bytes_write.sum": "dram_write",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_active_pct",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
         "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
         "launch__grid_size": "grid", "launch__cluster_dim_x": "cluster_x"}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9, "usecond": 1e-6,
