@@ -11,10 +11,11 @@ Modules
   dense    — Cholesky, triangular solve, Householder (dlarfg), column-pivoted QR
   analyze  — O2: units, RCB cluster tree, permutation, H_0, per-level schedule
   factor   — O3: Algorithm 1 with the scaled low-rank elimination
-  solve    — O4: Algorithm 2; O5: PCG
-  work     — algorithmic flop / byte formulas
+  solve    — O4: Algorithm 2; O5: PCG; GMRES(200)
+  dist     — the subdomain-distributed factor, apply and PCG, gloo-tested
 
-Parity status: every function is pinned by tests/test_oracle_*.py (P1-P9);
+Parity status: every function is pinned by tests/test_oracle_*.py (P1-P9, the R-floor, the
+decision-flag window, PCG beyond iteration 1, the R-coarse neighbour closed form);
 the ranks/iterations on C2-C5 are "parity unpinned" beyond oracle-vs-GPU
 (no published values exist for these synthetic inputs).
 """
