@@ -209,6 +209,66 @@ def run_reference(args, rank, world):
     return 0
 
 
+def khat_level0_flops(H, a, f, p):
+    """Level-0 factor flops with the SUPPORT-RESTRICTED column counts of SURVEY §8(d) (k̂_n, k̂_w:
+    only the structurally nonzero columns of a block count), next to the dense live counts the
+    kernels compute.  Symbolic, host-side: the column support of block (s, q) starts as the CSR
+    coupling of the two leaves, grows by the fill of every eliminated t with s, q in n(t)
+    (supp(t, q)), and is dense (r_q columns) once q is eliminated (its coarse DOFs)."""
+    perm = H.hs_analysis_export(a, H.HS_EXP_PERM)
+    loff = H.hs_analysis_export(a, H.HS_EXP_LEAF_OFF)
+    nleaf = loff.size - 1
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(perm.size)
+    leaf = np.searchsorted(loff, iperm, side="right") - 1          # leaf of every original DOF
+    rows = np.repeat(np.arange(p.n), np.diff(p.rowptr))
+    lp, lq = leaf[rows], leaf[p.colind]
+    sel = lp != lq
+    loc = iperm[p.colind[sel]] - loff[lq[sel]]
+    supp = {}
+    for x, y, c in zip(lp[sel].tolist(), lq[sel].tolist(), loc.tolist()):
+        supp.setdefault((x, y), set()).add(c)
+    hp, hi = H.hs_analysis_export(a, H.HS_EXP_H_PTR, 0), H.hs_analysis_export(a, H.HS_EXP_H_IDX, 0)
+    wp, wi = H.hs_analysis_export(a, H.HS_EXP_W_PTR, 0), H.hs_analysis_export(a, H.HS_EXP_W_IDX, 0)
+    bp, bi = H.hs_analysis_export(a, H.HS_EXP_BATCH_PTR, 0), H.hs_analysis_export(a, H.HS_EXP_BATCH_IDX, 0)
+    rk = H.hs_factor_export(f, H.HS_FEXP_RANKS, 0)
+    done = np.zeros(nleaf, dtype=bool)
+    fl_hat = fl_dense = 0.0
+    for b in range(bp.size - 1):
+        batch = bi[bp[b]:bp[b + 1]].tolist()
+        fills = []
+        for s_ in batch:
+            m = int(loff[s_ + 1] - loff[s_])
+            if m == 0:
+                continue
+            ns, ws = hi[hp[s_]:hp[s_ + 1]].tolist(), wi[wp[s_]:wp[s_ + 1]].tolist()
+            def cnt(q, hat):
+                if done[q]:
+                    return int(rk[q])
+                return len(supp.get((s_, q), ())) if hat else int(loff[q + 1] - loff[q])
+            r = int(rk[s_])
+            for hat in (True, False):
+                kn = sum(cnt(q, hat) for q in ns)
+                kw = sum(cnt(q, hat) for q in ws)
+                K = m - r
+                fq = sum(4.0 * (m - j) * (kw - j) + 4.0 * (m - j) * kn for j in range(r))
+                v = m ** 3 / 3.0 + m * m * (kn + kw) + fq + K * kn * (kn + 1)
+                if hat:
+                    fl_hat += v
+                else:
+                    fl_dense += v
+            if r < m:   # fill of the fine DOFs' elimination on n(s) x n(s)
+                fills.append([(q, frozenset(supp.get((s_, q), ()))) for q in ns if not done[q]])
+        for s_ in batch:
+            done[s_] = True
+        for nb in fills:
+            for x, _ in nb:
+                for y, sy in nb:
+                    if x != y and sy:
+                        supp.setdefault((x, y), set()).update(sy)
+    return fl_hat, fl_dense
+
+
 def run_ours(args, rank, world, local):
     import torch
     from paper_1811_11248_b200 import hsolve as H
@@ -397,6 +457,10 @@ def run_ours(args, rank, world, local):
         vec += int(H.hs_factor_export(f_last, H.HS_FEXP_LIVE0, lv).sum() + H.hs_factor_export(f_last, H.HS_FEXP_KN, lv).sum())
     del f_last
     apply_bytes = 2.0 * S["factor_bytes"] + 2 * 2 * 8.0 * vec
+    f_k = H.hs_factor_create(h, a, vals, eps=p.eps)
+    fl0_hat, fl0_dense = khat_level0_flops(H, a, f_k, p)
+    del f_k
+    flops_khat = factor_flops - fl0_dense + fl0_hat
     n_apply = sum(r["iters"] for r in reps)   # z = M^{-1} r once before the loop, then every non-final iteration
     n_spmv = sum(r["iters"] for r in reps)
     t_spmv = sum(r["t_spmv_s"] for r in reps)
@@ -433,6 +497,9 @@ def run_ours(args, rank, world, local):
                    "t_apply_s_per_step": t_apply / args.steps,
                    "factor_tflops": factor_flops / t_fac / 1e12,
                    "factor_gflop": factor_flops / 1e9, "factor_gb": S["factor_bytes"] / 1e9,
+                   "factor_gflop_khat": flops_khat / 1e9, "factor_tflops_khat": flops_khat / t_fac / 1e12,
+                   "flops_note": "factor_gflop counts the dense live columns the kernels compute; *_khat counts "
+                                 "level 0 with the support-restricted k̂_n, k̂_w of SURVEY §8(d) (levels >= 1 are dense)",
                    "phase_s_per_step": {nm: float(t_ph[i] / args.steps) for i, nm in enumerate(names)},
                    "phase_events": f"phases and roofline from {args.steps} profiled factor steps (every phase "
                                    f"bracketed with CUDA events, {prof_ms / args.steps:.1f} ms/factor); the timed "
