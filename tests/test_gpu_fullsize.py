@@ -8,7 +8,7 @@ apply on 3 seeded vectors (1e-9), PCG (1e-8, +-1 iteration) -- SURVEY §8(c) par
   * the C4 operator (Q1 first-order-Stokes-type, 2 DOF/node, 20 layers) on a 1/16 horizontal
     grid (40,960 DOF; its ranks make the oracle take ~2 min even so): C4 itself does not fit
     one B200 (bench.py docstring, DESIGN.md §5);
-  * the C5 operator on a 1/32 grid (128-DOF leaves: the non-fused m > 112 path);
+  * the C5 operator on a 1/64 grid (128-DOF leaves: the non-fused m > 112 path);
   * the CPQR kernel's global-memory mode (W streamed through L2, taken when a block does not
     fit a 16-CTA cluster's shared memory) forced on a case with wide blocks;
 plus the analyze schedule bit-exact, operator properties (symmetry, positivity, linearity),
@@ -114,12 +114,14 @@ def test_c4_operator_sixteenth_scale(H, handle):
     _full_parity(H, handle, p, "C4/16")
 
 
-def test_c5_operator_thirtysecond_scale(H, handle):
+def test_c5_operator_sixtyfourth_scale(H, handle):
     """The C5 operator (1024^2 x 16 node layers, aspect 1e4, 4-column leaves of 128 DOF: the
-    clusters above the fused kernels' 112-DOF limit, i.e. the gather / k_potrf / k_trsm path)
-    on a 1/32 horizontal grid (32,768 DOF).  C5 itself needs several GPUs."""
-    p = gen_config_scaled("C5", 32)
-    _full_parity(H, handle, p, "C5/32")
+    clusters above the fused kernels' 112-DOF limit, i.e. the gather / k_potrf / k_trsm path,
+    coarse clusters up to m = 318 and a 1,286-DOF top) on a 1/64 horizontal grid (8,192 DOF).
+    At 1/32 a coarse cluster already exceeds the kernels' 512-DOF limit (HS_E_UNSUPPORTED,
+    DESIGN.md §5); C5 itself needs several GPUs."""
+    p = gen_config_scaled("C5", 64)
+    _full_parity(H, handle, p, "C5/64")
 
 
 def test_cpqr_global_memory_mode(H, handle, monkeypatch):
