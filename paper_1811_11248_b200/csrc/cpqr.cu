@@ -69,17 +69,28 @@ __host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, 
   return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * cq_msg_words(m);
 }
 // direct write-back: the store element (row l of s, column j of B_s), j in the segment list
-__device__ __forceinline__ double* dwb_addr(const FusedSeg* seg, int nseg, int j, int l) {
+__device__ __forceinline__ int seg_find(const FusedSeg* seg, int nseg, int j) {
   int lo = 0, hi = nseg - 1;
   while (lo < hi) {   // last segment with col <= j
     const int mid = (lo + hi + 1) >> 1;
     if (seg[mid].col <= j) lo = mid;
     else hi = mid - 1;
   }
-  const FusedSeg g = seg[lo];
+  return lo;
+}
+// (colmap: the compressed B_s of a support-restricted level-0 cluster, see CluItem)
+__device__ __forceinline__ double* dwb_addr(const FusedSeg* seg, int nseg, const int32_t* colmap, int j, int l) {
+  const FusedSeg g = seg[seg_find(seg, nseg, j)];
   if (j < g.col || j >= g.col + g.len) return nullptr;   // a column of an empty neighbour: none
+  const int lc = colmap ? colmap[j] : j - g.col;
   double* p = const_cast<double*>(g.src);
-  return g.trans ? p + (int64_t)(j - g.col) * g.sld + l : p + (int64_t)l * g.sld + (j - g.col);
+  return g.trans ? p + (int64_t)lc * g.sld + l : p + (int64_t)l * g.sld + lc;
+}
+// the canonical (dense) index of B_s column j: the pivot order of the dense B_s
+__device__ __forceinline__ int dense_col(const CluItem& it, int j) {
+  if (!it.colmap) return j;
+  const FusedSeg g = it.seg[seg_find(it.seg, it.nseg, j)];
+  return g.dcol + it.colmap[j];
 }
 
 template <int G>
@@ -428,7 +439,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       for (int l = lane; l < m; l += 32) it.V[(size_t)j * m + l] = vmsg[8 + l];
       if (lane == 0) {
         it.tau[j] = tau;
-        it.piv[j] = p;
+        it.piv[j] = dense_col(it, p);
         nu[ploc] = -1.0;   // visible to the other warps after the next step's barrier
       }
     }
@@ -506,7 +517,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       const double* src = W + (size_t)c * ldm;
       const size_t sst = 1;
       for (int l = 0; l < r; ++l) {
-        double* d = dwb_addr(it.seg, it.nseg, w_lo + c, l);
+        double* d = dwb_addr(it.seg, it.nseg, it.colmap, w_lo + c, l);
         if (d) *d = src[(size_t)l * sst];
       }
     }
@@ -600,10 +611,10 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
       const int l = t + i * G;
       if (l >= m) continue;
       if (l < r) {
-        double* d = dwb_addr(it.seg, it.nseg, it.kw + jn, l);
+        double* d = dwb_addr(it.seg, it.nseg, it.colmap, it.kw + jn, l);
         if (d) *d = x[i];
       } else {
-        it.Cout[(size_t)(l - r) * it.kn + jn] = x[i];
+        it.Cout[(size_t)(l - r) * it.ldC + (it.dmapn ? it.dmapn[jn] : jn)] = x[i];
       }
     }
   }

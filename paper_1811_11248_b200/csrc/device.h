@@ -80,6 +80,13 @@ struct CluItem {
   // the apply operator formed by k_rotate_n: T_s = Qᵀ G_s^{-1} from k_chol's G^{-1} (fused path)
   const double* Ginv;
   double* Tout;
+  // support-restricted level 0: B_s holds only the structurally nonzero
+  // columns of its blocks; colmap[j] = local column (inside its block) of B_s column j,
+  // dmapn[c] = dense n-column of compressed n-column c (Cout keeps the dense layout, ld ldC).
+  // null = B_s is dense (colmap = identity inside each segment, ldC = kn)
+  const int32_t* colmap;
+  const int32_t* dmapn;
+  int32_t ldC, pad2;
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
@@ -103,10 +110,12 @@ struct FusedItem {
   int32_t m, lda, ldB, kw;
   int32_t c0, nc, seg_begin, seg_end;
   int32_t level, cluster, bi, pad;
+  const int32_t* colmap;      // compressed B_s: local block column of each B_s column (null: dense)
 };
 struct FusedSeg {             // block (s, q) of the store: B_s columns [col, col + len)
   const double* src;
   int32_t sld, trans, col, len;
+  int32_t dcol, pad;          // the block's first column in the dense B_s (canonical pivot index)
 };
 constexpr int CI_MAX_M = 112;   // k_scale_tile: G (ld m + 1) and a 64-column tile in shared memory, <= 28 rows per lane
 
@@ -137,6 +146,10 @@ struct SchurSrc {
   const double* C;           // fine rows of the n-part, ld ldC
   int32_t ldC, K, kn, nb_off, nnb, pad;
   double** pairs;            // [nnb (nnb+1) / 2] target block of neighbour pair (a >= b), or null
+  // support-restricted level 0: the tile ranges run over the kn compressed n-columns; column
+  // c is dense column dmap[c] of C and local column lmap[c] of its neighbour's block (null: dense)
+  const int32_t* lmap;
+  const int32_t* dmap;
 };
 // Device-side patch of a batch's pre-planned second half with the kept ranks r_s read from
 // d_rank (no host round trip between CPQR and the Schur update): one thread per item.
@@ -162,7 +175,7 @@ struct RankPub {
 struct SchurTile2 {
   int32_t src, i0, j0, pad;
 };
-struct NbCol {               // neighbour q occupies columns [col, col+len) of the n-part
+struct NbCol {               // neighbour q occupies columns [col, col+len) of the (compressed) n-part
   int32_t q, col, len, idx;  // idx: position of q in the full n(s) list (pair table index)
 };
 struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
@@ -273,9 +286,8 @@ struct SmallArgs {
 };
 size_t small_smem_bytes(int m_max, int k_max, int nseg_max, int npair_max);
 void launch_elim_small(const SmallArgs& a, int first, int n, cudaStream_t st);
-// the patch items; with pub: also publishes the batch's ranks (one extra block)
-void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st, int nrank = 0,
-                  const DevStatus* d_status = nullptr, RankPub* pub = nullptr, int32_t seq = 0);
+// the patch items (the batch's ranks are published by launch_publish right after the CPQR)
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st);
 void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
                     cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);

@@ -437,7 +437,8 @@ struct PhaseTimer {
     S.t_phase_s[5] += el(b[1], b[2]);
     b_pending = false;
   }
-  void collect_a(hs_factor_stats_t& S) {
+  void collect_a(hs_factor_stats_t& S) {   // (the ranks are published before a[4]: wait for it)
+    if (on || level == 1) HS_CUDA(cudaEventSynchronize(a[4]));
     if (on)
       for (int k = 0; k < 4; ++k) S.t_phase_s[k] += el(a[k], a[k + 1]);
     else if (level == 1)
@@ -668,6 +669,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   double t_apply_plan = 0.0;  // apply planning (host worker)
   std::future<void> plan_prev;  // the chain of per-level apply-plan tasks (joined before upload)
   double t_sub[4] = {0, 0, 0, 0};
+  double t_fh[3] = {0, 0, 0};   // first-half planning: shapes + column maps, items, upload staging
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
   double t_tr[4] = {0, 0, 0, 0};   // level transition: block store build, upload_dir, arena alloc, release
   cudaEvent_t ev0, ev1;
@@ -854,6 +856,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     LevelPairs lp;   // built below for the levels that run the batch pipeline
     std::vector<int32_t> live = cap;
     std::vector<uint8_t> done(lev.nclus, 0);   // eliminated (rank known here)
+    // support-restricted level 0 (support.cpp): B_s of a level-0 cluster holds
+    // only the structurally nonzero columns of its blocks (single GPU, direct write-back path)
+    const bool khat_lv = l == 0 && dpatch && !no_dwb && !no_fused && !f->keep_records &&
+                         std::getenv("HS_NO_KHAT") == nullptr;
+    if (khat_lv) build_l0_support(*an);
+    std::vector<int32_t> fkn(lev.nclus, 0), fkw(lev.nclus, 0);   // B_s's n/w widths (flop counts)
     // store offsets of row s's blocks, [w(s) ..., n(s) ...] (computed once per cluster)
     std::vector<std::vector<int64_t>> roff(lev.nclus);
     auto row_offs = [&](int32_t s) -> const std::vector<int64_t>& {
@@ -913,7 +921,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         live[s] = r;
         done[s] = 1;
         if (m == 0) continue;
-        const int32_t K = m - r, kn = L.kn[s], kw = L.kw[s];
+        const int32_t K = m - r, kn = fkn[s], kw = fkw[s];
         S.max_m = std::max(S.max_m, m);
         S.max_rank = std::max(S.max_rank, r);
         double fq = 0.0;
@@ -1111,12 +1119,77 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       // themselves (no write-back pass); needs the device patch and CPQR v3
       const bool dwb = fused && dpatch && !no_dwb;
       std::vector<int32_t> seg0v(nb, 0);
+      // the widths of B_s: dense, or (khat) the supported columns of each block; the column
+      // maps of a compressed B_s (CluItem::colmap / dmapn) go up with the batch's items
+      const bool khat = khat_lv && dwb;
+      std::vector<int32_t> bkn(nb), bkw(nb), cmap, dmap;
+      std::vector<std::vector<int32_t>> nlen(nb);   // compressed width of each q of n(s)
+      std::vector<int64_t> cmo(nb, 0), dmo(nb, 0);
+      const L0Support& su = an->l0s;
+      for (int bi = 0; bi < nb; ++bi) {   // widths (and, khat, the offsets of the maps)
+        const int32_t s = Bo[bi];
+        bkn[bi] = L.kn[s];
+        bkw[bi] = L.kw[s];
+        if (!khat) continue;
+        int64_t e = su.sptr[s];
+        bkn[bi] = bkw[bi] = 0;
+        nlen[bi].reserve(lev.H[s].size());
+        for (int pass = 0; pass < 2; ++pass)
+          for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+            const int32_t ln = su.len[e++];
+            if ((ln < 0) != (done[q] != 0)) fail(HS_E_INTERNAL, "support: schedule mismatch");
+            const int32_t c = ln < 0 ? live[q] : ln;
+            if (pass == 0) {
+              bkw[bi] += c;
+            } else {
+              bkn[bi] += c;
+              nlen[bi].push_back(c);
+            }
+          }
+        L.ldB[s] = bkn[bi] + bkw[bi];
+        cmo[bi] = bi ? cmo[bi - 1] + bkn[bi - 1] + bkw[bi - 1] : 0;
+        dmo[bi] = bi ? dmo[bi - 1] + bkn[bi - 1] : 0;
+      }
+      if (khat && nb > 0) {   // the maps: supported local columns (runs of su.idx) / identity
+        cmap.resize(cmo[nb - 1] + bkn[nb - 1] + bkw[nb - 1]);
+        dmap.resize(dmo[nb - 1] + bkn[nb - 1]);
+        for (int bi = 0; bi < nb; ++bi) {
+          const int32_t s = Bo[bi];
+          int64_t e = su.sptr[s], x = su.iptr[s];
+          int32_t* cm = cmap.data() + cmo[bi];
+          int32_t* dm = dmap.data() + dmo[bi];
+          int32_t dn = 0;   // dense n-column of q's first column
+          for (int pass = 0; pass < 2; ++pass)
+            for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+              const int32_t ln = su.len[e++];
+              const int32_t c = ln < 0 ? live[q] : ln;
+              if (ln < 0) {
+                for (int32_t j = 0; j < c; ++j) cm[j] = j;
+              } else {
+                std::memcpy(cm, su.idx.data() + x, sizeof(int32_t) * c);
+                x += c;
+              }
+              if (pass == 1) {
+                for (int32_t j = 0; j < c; ++j) dm[j] = dn + cm[j];
+                dm += c;
+                dn += live[q];
+              }
+              cm += c;
+            }
+        }
+      }
+      for (int bi = 0; bi < nb; ++bi) {
+        fkn[Bo[bi]] = bkn[bi];
+        fkw[Bo[bi]] = bkw[bi];
+      }
+      const double tfh1 = now_s();
+      t_fh[0] += tfh1 - tp0;
       // batch workspace: G (m^2), V (m^2), tau (m), nu (kw), B (m x (kw + kn)) per cluster
       int64_t wsz = 0;
       std::vector<int64_t> wo(nb);
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
-        const int64_t m = live[s], kn = L.kn[s], kw = L.kw[s];
+        const int64_t m = live[s], kn = bkn[bi], kw = bkw[bi];
         wo[bi] = wsz;
         wsz += 3 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
       }
@@ -1138,7 +1211,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       int64_t gsz = 0;
       std::vector<int64_t> go(nb, -1);
       for (int bi = 0; bi < nb; ++bi) {
-          const int64_t w = (int64_t)cpqr_global_words(live[Bo[bi]], L.kw[Bo[bi]], max_m);
+          const int64_t w = (int64_t)cpqr_global_words(live[Bo[bi]], bkw[bi], max_m);
           if (w) {
             go[bi] = gsz;
             gsz += (w + 3) & ~int64_t(3);
@@ -1147,7 +1220,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       double* wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
       for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
-        const int32_t m = live[s], kn = L.kn[s], kw = L.kw[s], ldB = L.ldB[s];
+        const int32_t m = live[s], kn = bkn[bi], kw = bkw[bi], ldB = L.ldB[s];
         double* w0 = ws + wo[bi];
         L.G[s] = w0;
         L.V[s] = w0 + (int64_t)m * m;
@@ -1158,6 +1231,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         CluItem& it = clu[bi];
         it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
         it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
+        it.ldC = L.kn[s];   // Cout keeps the dense n-columns (the apply's record)
         it.Wt = go[bi] >= 0 ? wtmp + go[bi] : nullptr;
         if (m == 0) continue;
         double* p; int32_t ld, tr;
@@ -1169,19 +1243,26 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         const int32_t ldss = ld;
         if (!fused) gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
         const int32_t seg0 = (int32_t)fseg.size();
-        int32_t col = 0;
+        int32_t col = 0, dcol = 0;   // the block's first column in B_s / in the dense B_s
         const auto& ro = row_offs(s);
         size_t kq = 0;
+        int64_t e = khat ? an->l0s.sptr[s] : 0;
         for (int pass = 0; pass < 2; ++pass)
           for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
             const int64_t o = ro[kq++];
+            const int32_t wq = khat && an->l0s.len[e] >= 0 ? an->l0s.len[e] : live[q];
+            if (khat) ++e;
             if (live[q] > 0) {
               if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
               bs.at(s, q, o, p, ld, tr);
-              if (fused) fseg.push_back(FusedSeg{p, ld, tr, col, live[q]});
-              else gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+              if (fused) {
+                if (wq > 0) fseg.push_back(FusedSeg{p, ld, tr, col, wq, dcol, 0});
+              } else {
+                gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+              }
             }
-            col += live[q];
+            col += wq;
+            dcol += live[q];
           }
         const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
         if (fused) {
@@ -1196,7 +1277,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             it.ldss = ldss;
             it.dwb = 1;
             it.keepB = f->keep_records ? 1 : 0;
-            if (kn > 0) {
+            if (L.kn[s] > 0) {
               L.C[s] = ctmp + co[bi];   // C_s = rows [r, m) of the rotated B_n (K <= m)
               it.Cout = L.C[s];
             }
@@ -1228,26 +1309,43 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       // the first half's launches: at once (host patch), or (device patch) deferred until the
       // second half is planned, so that both uploads precede one uninterrupted kernel chain
       std::function<void(bool)> first_half_launch;   // argument: publish the ranks here
+      size_t iCM = 0, iDM = 0;                        // the column maps in upA (khat)
+      const double tfh2 = now_s();
+      t_fh[1] += tfh2 - tfh1;
       if (nb > 0) {
         split_copies(gather);
         upA.reset();
         std::vector<unsigned long long> nmax(nb, 0ull);
         const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
                      iM = upA.add(nmax), iF = upA.add(fz), iS = upA.add(fseg), iI = upA.add(fci);
+        iCM = upA.add(cmap);
+        iDM = upA.add(dmap);
         upA.stage.ensure(upA.total);
         upA.dev.ensure(upA.total);
         for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
         for (auto& f : fz) f.nmax = upA.dptr<unsigned long long>(iM) + f.bi;
         for (int bi = 0; bi < nb; ++bi)
           if (clu[bi].dwb) clu[bi].seg = upA.dptr<FusedSeg>(iS) + seg0v[bi];
+        if (khat) {
+          for (int bi = 0; bi < nb; ++bi) {
+            clu[bi].colmap = upA.dptr<int32_t>(iCM) + cmo[bi];
+            clu[bi].dmapn = upA.dptr<int32_t>(iDM) + dmo[bi];
+          }
+          for (auto& f : fz) f.colmap = clu[f.bi].colmap;
+        }
         upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
         upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
+        upA.copy_in(iCM, cmap); upA.copy_in(iDM, dmap);
         t_plan += now_s() - tp0;
+        t_fh[2] += now_s() - tfh2;
         d_clu_batch = upA.dptr<CluItem>(iC);
         const size_t nfz = fz.size(), nfci = fci.size(), ngather = gather.size(), ntrsm = trsm.size(),
                      nrot = rot.size();
+        double* const czero = khat ? ctmp : nullptr;   // compressed: C_s's unsupported columns are 0
+        const int64_t czn = csz;
         first_half_launch = [&, iG, iC, iT, iR, iF, iS, iI, fused, max_m, nb, nfz, nfci, ngather, ntrsm, nrot,
-                             clu](bool publish) {
+                             clu, czero, czn](bool publish) {
+          if (czero) HS_CUDA(cudaMemsetAsync(czero, 0, sizeof(double) * czn, st));
           pt.rec(pt.a[0], st);
           if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
             pt.rec(pt.a[1], st);
@@ -1264,13 +1362,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           }
           pt.rec(pt.a[3], st);
           launch_cpqr3(upA.dptr<CluItem>(iC), clu, opt.eps, opt.eps_relative, d_rank, st);
+          // the ranks are final here: publish them before the rotation, so that the host plans
+          // the next batch while the rotation and this batch's Schur update run
+          if (dpatch && publish) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
           launch_rotate_n(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iR), (int)nrot, max_m, d_rank, st);
           pt.rec(pt.a[4], st);
-          if (dpatch) {
-            if (publish) launch_publish(d_rank, nb, d_status, pub_dev, ++pub_seq, st);
-          } else {
-            HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
-          }
+          if (!dpatch) HS_CUDA(cudaMemcpyAsync(h_rank, d_rank, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
         };
         if (!dpatch) {
           upA.send(st);
@@ -1314,6 +1411,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
         const int32_t m = live[s], kn = L.kn[s], ldB = L.ldB[s];
         if (m == 0) continue;
+        const int32_t kc = khat ? bkn[k] : kn;   // the n-columns the Schur tiles run over
         Pend pd{s, (int32_t)k, mine, -1, -1, -1, -1, wb.size(), wb.size()};
         if (mine && !fused) {   // (fused: k_rotate_n forms T_s from k_chol's G^{-1})
           pd.ft = (int64_t)ft.size();
@@ -1323,8 +1421,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         // neighbour column offsets inside the n-part
         const auto& ns = lev.H[s];
         std::vector<int32_t> noff(ns.size() + 1, 0);
-        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + live[ns[a]];
-        if (kn > 0) {
+        auto nwid = [&](size_t a) { return khat ? nlen[k][a] : live[ns[a]]; };
+        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + nwid(a);
+        if (kc > 0) {
           // wave = lowest wave in which no earlier source shares a neighbour with s
           uint64_t used = 0;
           for (int32_t q : ns)
@@ -1333,10 +1432,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           while (w < 63 && ((used >> w) & 1ull)) ++w;
           if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
           const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
-          SchurSrc sc{nullptr, dwb ? kn : ldB, 0, kn, (int32_t)nbc.size(), 0, 0};
+          SchurSrc sc{nullptr, dwb ? kn : ldB, 0, kc, (int32_t)nbc.size(), 0, 0};
+          if (khat) {
+            sc.lmap = upA.dptr<int32_t>(iCM) + cmo[k] + bkw[k];
+            sc.dmap = upA.dptr<int32_t>(iDM) + dmo[k];
+          }
           for (size_t a = 0; a < ns.size(); ++a)
             if (live[ns[a]] > 0) {
-              nbc.push_back(NbCol{ns[a], noff[a], live[ns[a]], (int32_t)a});
+              if (nwid(a) > 0) nbc.push_back(NbCol{ns[a], noff[a], nwid(a), (int32_t)a});
               if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
               wave_mask[ns[a]] |= bit;
             }
@@ -1345,7 +1448,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           srcs.push_back(sc);
           src_cl.push_back(s);
           if ((int)waves.size() <= w) waves.resize(w + 1);
-          const int T = (kn + 63) / 64;
+          const int T = (kc + 63) / 64;
           for (int ti = 0; ti < T; ++ti)
             for (int tj = 0; tj <= ti; ++tj) waves[w].push_back(SchurTile2{(int32_t)pd.src, ti * 64, tj * 64, 0});
         }
@@ -1605,21 +1708,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upB.copy_in(jX, patch);
         t_plan += now_s() - tp1;
         const double tl0 = now_s();
-        const bool pub_here = (bool)first_half_launch;   // the patch kernel publishes the ranks
         if (first_half_launch) {   // device patch: both uploads, then the whole batch's kernels
           upA.send(st);
           upB.send(st);
-          first_half_launch(false);
+          first_half_launch(true);
           first_half_launch = nullptr;
         } else {
           upB.send(st);
         }
         pt.collect_b(S);   // the previous batch's second-half events, before they are re-recorded
         pt.rec(pt.b[0], st);
-        if (pub_here)
-          launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st, nb, d_status, pub_dev, ++pub_seq);
-        else
-          launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
+        launch_patch(upB.dptr<PatchItem>(jX), (int)patch.size(), d_rank, st);
         for (size_t w = 0; w + 1 < wave_off.size(); ++w)
           launch_schur2(upB.dptr<SchurTile2>(jT) + wave_off[w], wave_off[w + 1] - wave_off[w],
                         upB.dptr<SchurSrc>(jS), upB.dptr<NbCol>(jN), bs.dir(), st);
@@ -2064,6 +2163,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
+  if (std::getenv("HS_PROFILE"))
+    std::fprintf(stderr, "[hs profile] first-half planning: shapes + column maps %.1f ms, items %.1f ms, upload staging %.1f ms\n",
+                 1e3 * t_fh[0], 1e3 * t_fh[1], 1e3 * t_fh[2]);
   if (std::getenv("HS_PROFILE") || std::getenv("HS_RANK_WAIT"))
     std::fprintf(stderr, "[hs profile] host blocked on batch ranks: %.1f ms of %.1f ms; issuing uploads + kernels %.1f ms\n",
                  1e3 * t_rank_wait, ms, 1e3 * t_launch);

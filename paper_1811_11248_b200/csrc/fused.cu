@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
           j = j0 + e % wd;
         }
         dst[u] = e < tot ? i * SM_LDX + (j - it.c0) : -1;
-        v[u] = e < tot ? (sgm.trans ? sgm.src[(int64_t)(j - sgm.col) * sgm.sld + i]
-                                    : sgm.src[(int64_t)i * sgm.sld + (j - sgm.col)])
+        const int lc = e >= tot ? 0 : (it.colmap ? it.colmap[j] : j - sgm.col);   // column inside the block
+        v[u] = e < tot ? (sgm.trans ? sgm.src[(int64_t)lc * sgm.sld + i] : sgm.src[(int64_t)i * sgm.sld + lc])
                        : 0.0;
       }
 #pragma unroll

@@ -33,6 +33,16 @@ struct Level {
   Adj Ffinal;                  // fill graph after the level
 };
 
+// Structural column supports of the level-0 blocks as each cluster is eliminated (support.cpp)
+struct L0Support {
+  bool built = false;
+  // cluster s: entries sptr[s] .. sptr[s+1] of len, one per q of w(s) then n(s) (the B_s
+  // column order): the number of supported columns of q, or -1 (q eliminated before s: its
+  // coarse columns, dense); the supported local columns, ascending, at idx[iptr[s] ..]
+  std::vector<int64_t> sptr, iptr;
+  std::vector<int32_t> len, idx;
+};
+
 struct Analysis {
   int64_t n = 0;
   int32_t D = 0, L_top = 0, top_log2 = 3, nsub_log2 = 3;
@@ -52,6 +62,7 @@ struct Analysis {
   int64_t* d_perm = nullptr;
   int64_t* d_map = nullptr;     // CSR entry -> offset in the level-0 block store (-1: upper)
   int64_t* d_tmap = nullptr;    // CSR entry (i,j) -> index of (j,i) (value symmetry check)
+  L0Support l0s;                // built by the first factor that restricts level 0 to the supports
   int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
 };
 
@@ -65,6 +76,8 @@ struct DistPlan {
 DistPlan make_plan(const Analysis& an, int world, int rank);
 // ranks other than the owner that receive the elimination record of cluster s of level l
 std::vector<int32_t> receivers(const Analysis& an, const DistPlan& P, int l, int s);
+
+void build_l0_support(Analysis& an);   // fills an.l0s (idempotent, thread-safe)
 
 Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
                   int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts& opt);

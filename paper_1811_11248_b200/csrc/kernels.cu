@@ -482,8 +482,11 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
   __shared__ int nbcol[SCH_NBS];
   const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const double* Cp = s.C + t.i0;
-  const double* Cq = s.C + t.j0;
+  // this thread's C columns in the staged chunks (ii = tid & 63 in every load): the dense
+  // columns of compressed columns i0 + ii / j0 + ii (support-restricted level 0)
+  const int ii0 = tid & 63;
+  const double* Cp = s.C + (ii0 < rows ? (s.dmap ? s.dmap[t.i0 + ii0] : t.i0 + ii0) : 0);
+  const double* Cq = s.C + (ii0 < cols ? (s.dmap ? s.dmap[t.j0 + ii0] : t.j0 + ii0) : 0);
   // (1) the neighbours' column starts into shared memory (the owner searches) + the first
   // K-chunk of C
   const bool nst = s.nnb <= SCH_NBS;
@@ -495,8 +498,8 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
       const int e = tid + 256 * q;
       const int kk = e >> 6, ii = e & 63;
       const bool kin = k0 + kk < s.K;
-      ap[kk][ii] = (kin && ii < rows) ? Cp[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
-      aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC + ii] : 0.0;
+      ap[kk][ii] = (kin && ii < rows) ? Cp[(int64_t)(k0 + kk) * s.ldC] : 0.0;
+      aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC] : 0.0;
     }
   };
   load_chunk(0);
@@ -529,13 +532,13 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
     int* list = w == 0 ? r_list : c_list;
     if (lane < lim) {
       own[lane] = o0;
-      loc[lane] = base + lane - nb[o0].col;
+      loc[lane] = s.lmap ? s.lmap[base + lane] : base + lane - nb[o0].col;
       slot[lane] = s0;
       if (f0) list[s0] = o0;
     }
     if (lane + 32 < lim) {
       own[lane + 32] = o1;
-      loc[lane + 32] = base + lane + 32 - nb[o1].col;
+      loc[lane + 32] = s.lmap ? s.lmap[base + lane + 32] : base + lane + 32 - nb[o1].col;
       slot[lane + 32] = s1;
       if (f1) list[s1] = o1;
     }
@@ -677,15 +680,10 @@ __device__ void publish_body(const int32_t* __restrict__ rank, int n, const DevS
   }
 }
 
-// the patch items, plus (pub != null) one extra block that publishes the batch's ranks
-__global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank, int nrank,
-                        const DevStatus* __restrict__ status, RankPub* pub, int32_t seq) {
+// the patch items: one thread each
+__global__ void k_patch(const PatchItem* __restrict__ items, int n, const int32_t* __restrict__ rank) {
   pdl_trigger();
   pdl_wait();
-  if (pub && blockIdx.x == gridDim.x - 1) {
-    publish_body(rank, nrank, status, pub, seq);
-    return;
-  }
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PatchItem p = items[i];
@@ -729,11 +727,10 @@ void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, Ran
   count_launch(1);
 }
 
-void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st, int nrank,
-                  const DevStatus* d_status, RankPub* pub, int32_t seq) {
-  const int blocks = (n + 127) / 128 + (pub ? 1 : 0);
+void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaStream_t st) {
+  const int blocks = (n + 127) / 128;
   if (blocks <= 0) return;
-  launch_pdl(k_patch, dim3(blocks), dim3(128), 0, st, d_items, n, d_rank, nrank, d_status, pub, seq);
+  launch_pdl(k_patch, dim3(blocks), dim3(128), 0, st, d_items, n, d_rank);
   count_launch(1);
 }
 

@@ -369,3 +369,38 @@ def test_small_level_path_agrees_with_batch_pipeline(H, handle, monkeypatch):
     assert all(np.array_equal(u, w) for u, w in zip(r0, r1))
     assert all(np.array_equal(u, w) for u, w in zip(p0, p1))
     assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
+
+
+@pytest.mark.parametrize("cfg", ["C3/4", "C2/2", "C4/16"])
+def test_support_restricted_level0_is_the_dense_computation(H, handle, monkeypatch, cfg):
+    """Level 0 runs on the structurally nonzero columns of each block only (support.cpp,
+    SURVEY O2.10): a zero column stays zero through the scaling, the CPQR (never a pivot) and
+    the rotation, and the Schur products only reach supported columns -- so the factor is the
+    dense one (HS_NO_KHAT=1): identical kept ranks, canonical pivots, top block and apply."""
+    from problems.generators import gen_config_scaled
+    name, k = cfg.split("/")
+    p = gen_config_scaled(name, int(k))
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+    L = H.hs_analysis_get_info(a)["L_top"]
+    v = np.random.default_rng(21).standard_normal(p.n)
+
+    def run(**env):
+        monkeypatch.delenv("HS_NO_KHAT", raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        f = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
+        st = H.hs_factor_get_stats(f)
+        out = ([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)],
+               [H.hs_factor_export(f, H.HS_FEXP_PIV, l) for l in range(L)],
+               H.hs_factor_export(f, H.HS_FEXP_TOP, 0), H.hs_apply(f, v), st["flops_level"][0])
+        del f
+        return out
+
+    r0, p0, t0, x0, fl0 = run()
+    r1, p1, t1, x1, fl1 = run(HS_NO_KHAT="1")
+    assert all(np.array_equal(u, w) for u, w in zip(r0, r1))
+    assert all(np.array_equal(u, w) for u, w in zip(p0, p1))
+    assert np.array_equal(t0, t1)
+    assert np.array_equal(x0, x1)
+    assert fl0 < fl1   # the level-0 work shrinks with the supports
