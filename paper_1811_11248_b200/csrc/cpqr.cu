@@ -78,19 +78,19 @@ __device__ __forceinline__ int seg_find(const FusedSeg* seg, int nseg, int j) {
   }
   return lo;
 }
-// (colmap: the compressed B_s of a support-restricted level-0 cluster, see CluItem)
-__device__ __forceinline__ double* dwb_addr(const FusedSeg* seg, int nseg, const int32_t* colmap, int j, int l) {
+// (g.idx: the supported columns of a support-restricted level-0 block, see FusedSeg)
+__device__ __forceinline__ double* dwb_addr(const FusedSeg* seg, int nseg, int j, int l) {
   const FusedSeg g = seg[seg_find(seg, nseg, j)];
   if (j < g.col || j >= g.col + g.len) return nullptr;   // a column of an empty neighbour: none
-  const int lc = colmap ? colmap[j] : j - g.col;
+  const int lc = g.idx ? g.idx[j - g.col] : j - g.col;
   double* p = const_cast<double*>(g.src);
   return g.trans ? p + (int64_t)lc * g.sld + l : p + (int64_t)l * g.sld + lc;
 }
 // the canonical (dense) index of B_s column j: the pivot order of the dense B_s
 __device__ __forceinline__ int dense_col(const CluItem& it, int j) {
-  if (!it.colmap) return j;
+  if (it.kwd < 0) return j;
   const FusedSeg g = it.seg[seg_find(it.seg, it.nseg, j)];
-  return g.dcol + it.colmap[j];
+  return g.dcol + (g.idx ? g.idx[j - g.col] : j - g.col);
 }
 
 template <int G>
@@ -517,7 +517,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       const double* src = W + (size_t)c * ldm;
       const size_t sst = 1;
       for (int l = 0; l < r; ++l) {
-        double* d = dwb_addr(it.seg, it.nseg, it.colmap, w_lo + c, l);
+        double* d = dwb_addr(it.seg, it.nseg, w_lo + c, l);
         if (d) *d = src[(size_t)l * sst];
       }
     }
@@ -606,15 +606,16 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
     }
   if (it.dwb && act) {   // coarse-n rows into the store blocks (s, q), C rows into the slab
     const int jn = c0 + grp;
+    const int dn = it.kwd < 0 ? jn : dense_col(it, it.kw + jn) - it.kwd;   // C_s keeps the dense columns
 #pragma unroll
     for (int i = 0; i < MR; ++i) {
       const int l = t + i * G;
       if (l >= m) continue;
       if (l < r) {
-        double* d = dwb_addr(it.seg, it.nseg, it.colmap, it.kw + jn, l);
+        double* d = dwb_addr(it.seg, it.nseg, it.kw + jn, l);
         if (d) *d = x[i];
       } else {
-        it.Cout[(size_t)(l - r) * it.ldC + (it.dmapn ? it.dmapn[jn] : jn)] = x[i];
+        it.Cout[(size_t)(l - r) * it.ldC + dn] = x[i];
       }
     }
   }

@@ -80,13 +80,10 @@ struct CluItem {
   // the apply operator formed by k_rotate_n: T_s = Qᵀ G_s^{-1} from k_chol's G^{-1} (fused path)
   const double* Ginv;
   double* Tout;
-  // support-restricted level 0: B_s holds only the structurally nonzero
-  // columns of its blocks; colmap[j] = local column (inside its block) of B_s column j,
-  // dmapn[c] = dense n-column of compressed n-column c (Cout keeps the dense layout, ld ldC).
-  // null = B_s is dense (colmap = identity inside each segment, ldC = kn)
-  const int32_t* colmap;
-  const int32_t* dmapn;
-  int32_t ldC, pad2;
+  // support-restricted level 0 (support.cpp): B_s holds only the structurally
+  // nonzero columns of its blocks (the segments' idx lists); kwd = the dense w-width (-1: B_s
+  // is dense).  Cout keeps the dense n-columns (ld ldC = the dense kn): the apply's record.
+  int32_t ldC, kwd;
 };
 
 struct FormTItem {  // T_s = U^T G^{-1} of one eliminated cluster (apply operator, m x m row-major)
@@ -110,12 +107,15 @@ struct FusedItem {
   int32_t m, lda, ldB, kw;
   int32_t c0, nc, seg_begin, seg_end;
   int32_t level, cluster, bi, pad;
-  const int32_t* colmap;      // compressed B_s: local block column of each B_s column (null: dense)
 };
 struct FusedSeg {             // block (s, q) of the store: B_s columns [col, col + len)
   const double* src;
+  const int32_t* idx;         // column col + c of B_s = local column idx[c] of the block (null: c)
   int32_t sld, trans, col, len;
   int32_t dcol, pad;          // the block's first column in the dense B_s (canonical pivot index)
+};
+struct ScaleTile {            // k_scale_mma: columns [c0, c0 + nc) of cluster item ci's B_s
+  int32_t ci, c0, nc, seg_begin, seg_end, pad;   // the segments overlapping the tile
 };
 constexpr int CI_MAX_M = 112;   // k_scale_tile: G (ld m + 1) and a 64-column tile in shared memory, <= 28 rows per lane
 
@@ -146,10 +146,6 @@ struct SchurSrc {
   const double* C;           // fine rows of the n-part, ld ldC
   int32_t ldC, K, kn, nb_off, nnb, pad;
   double** pairs;            // [nnb (nnb+1) / 2] target block of neighbour pair (a >= b), or null
-  // support-restricted level 0: the tile ranges run over the kn compressed n-columns; column
-  // c is dense column dmap[c] of C and local column lmap[c] of its neighbour's block (null: dense)
-  const int32_t* lmap;
-  const int32_t* dmap;
 };
 // Device-side patch of a batch's pre-planned second half with the kept ranks r_s read from
 // d_rank (no host round trip between CPQR and the Schur update): one thread per item.
@@ -177,6 +173,8 @@ struct SchurTile2 {
 };
 struct NbCol {               // neighbour q occupies columns [col, col+len) of the (compressed) n-part
   int32_t q, col, len, idx;  // idx: position of q in the full n(s) list (pair table index)
+  int32_t dcol, pad;         // q's first column in the dense n-part (the columns of C_s)
+  const int32_t* sup;        // column col + c = local column sup[c] of q (null: c; support.cpp)
 };
 struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
   double* blk;
@@ -291,7 +289,8 @@ void launch_patch(const PatchItem* d_items, int n, const int32_t* d_rank, cudaSt
 void launch_publish(const int32_t* d_rank, int n, const DevStatus* d_status, RankPub* pub, int32_t seq,
                     cudaStream_t st);
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
-void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st);
+void launch_scale_tiles(const FusedItem* d_clus, const ScaleTile* d_tiles, int n, const FusedSeg* d_segs, int max_m,
+                        cudaStream_t st);
 
 // ---- launch accounting (every launcher counts its kernels; graphs count their nodes) -----
 void count_launch(int64_t n);

@@ -16,9 +16,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <future>
 #include <memory>
+#include <thread>
 #include <unordered_map>
 
 #include "runtime.h"
@@ -450,6 +452,70 @@ struct PhaseTimer {
   }
 };
 
+// [chunk_lo(n, T, t), chunk_lo(n, T, t + 1)): the t-th of T contiguous chunks of [0, n)
+inline int chunk_lo(int n, int T, int t) { return (int)((int64_t)n * t / T); }
+// Host threads for planning n clusters of a batch (HS_PLAN_THREADS overrides; 1 = sequential)
+int plan_threads(int n) {
+  static const int hw = [] {
+    const char* e = std::getenv("HS_PLAN_THREADS");
+    if (e) return std::max(1, std::atoi(e));
+    return std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+  }();
+  return std::max(1, std::min(hw, n / 128));
+}
+// fn(b0, b1, t) over the T chunks of [0, n): T - 1 helper threads and the caller; the first
+// exception is rethrown on the caller once every chunk is done
+template <class F>
+void par_chunks(int n, int T, F&& fn) {
+  if (T <= 1) {
+    fn(0, n, 0);
+    return;
+  }
+  std::vector<std::exception_ptr> ex(T);
+  auto run = [&](int t) {
+    try {
+      fn(chunk_lo(n, T, t), chunk_lo(n, T, t + 1), t);
+    } catch (...) {
+      ex[t] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  for (int t = 1; t < T; ++t) th.emplace_back(run, t);
+  run(0);
+  for (auto& x : th) x.join();
+  for (auto& e : ex)
+    if (e) std::rethrow_exception(e);
+}
+
+// one planning thread's share of a batch's items (PlanPart) and the batch vectors, kept across
+// batches so that their storage is reused (no allocation, no first-touch page faults per batch)
+struct PlanPart {
+  std::vector<CopyItem> gather;
+  std::vector<TrsmItem> trsm, rot;
+  std::vector<FusedItem> fci;
+  std::vector<ScaleTile> fz;
+  std::vector<FusedSeg> fseg;
+  double fl1 = 0.0, fl2 = 0.0;
+  void clear() {
+    gather.clear(); trsm.clear(); rot.clear(); fci.clear(); fz.clear(); fseg.clear();
+    fl1 = fl2 = 0.0;
+  }
+};
+struct BatchVecs {
+  std::vector<PlanPart> parts;
+  std::vector<CopyItem> gather, wb;
+  std::vector<CluItem> clu;
+  std::vector<TrsmItem> trsm, rot;
+  std::vector<FusedItem> fci;
+  std::vector<ScaleTile> fz;
+  std::vector<FusedSeg> fseg;
+  std::vector<SchurSrc> srcs;
+  std::vector<NbCol> nbc;
+  std::vector<SchurTile2> tiles;
+  std::vector<PatchItem> patch;
+};
+
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -669,7 +735,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   double t_apply_plan = 0.0;  // apply planning (host worker)
   std::future<void> plan_prev;  // the chain of per-level apply-plan tasks (joined before upload)
   double t_sub[4] = {0, 0, 0, 0};
-  double t_fh[3] = {0, 0, 0};   // first-half planning: shapes + column maps, items, upload staging
+  double t_fh[6] = {0, 0, 0, 0, 0, 0};   // first-half planning: shapes + column maps, items, upload staging
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
   double t_tr[4] = {0, 0, 0, 0};   // level transition: block store build, upload_dir, arena alloc, release
   cudaEvent_t ev0, ev1;
@@ -801,6 +867,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (auto& e : lev_ev) cudaEventDestroy(e);
   });
   std::vector<double> lev_flops(an->L_top + 1, 0.0);
+  BatchVecs rc;   // the batch vectors, reused batch after batch
   tl.push_back({"level-0 store + setup", now_s()});
   for (int l = 0; l < an->L_top; ++l) {
     HS_CUDA(cudaEventRecord(lev_ev[l], st));
@@ -860,7 +927,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     // only the structurally nonzero columns of its blocks (single GPU, direct write-back path)
     const bool khat_lv = l == 0 && dpatch && !no_dwb && !no_fused && !f->keep_records &&
                          std::getenv("HS_NO_KHAT") == nullptr;
-    if (khat_lv) build_l0_support(*an);
+    const int32_t* d_sup = nullptr;   // the supports on the device
+    if (khat_lv) {
+      build_l0_support(*an);
+      d_sup = l0_support_device(*an, h->device);
+    }
     std::vector<int32_t> fkn(lev.nclus, 0), fkw(lev.nclus, 0);   // B_s's n/w widths (flop counts)
     // store offsets of row s's blocks, [w(s) ..., n(s) ...] (computed once per cluster)
     std::vector<std::vector<int64_t>> roff(lev.nclus);
@@ -1107,11 +1178,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       for (int32_t s : Bt)
         if (own(l, s)) Bo.push_back(s);
       const int nb = (int)Bo.size();
-      std::vector<CopyItem> gather;
-      std::vector<CluItem> clu(nb);
-      std::vector<TrsmItem> trsm, rot;
-      std::vector<FusedItem> fci, fz;   // gather-free Cholesky+inverse per cluster, scaling per tile
-      std::vector<FusedSeg> fseg;
+      auto& gather = rc.gather;
+      auto& clu = rc.clu;
+      auto& trsm = rc.trsm;
+      auto& rot = rc.rot;
+      auto& fci = rc.fci;   // gather-free Cholesky + inverse per cluster
+      auto& fz = rc.fz;     // the scaling per 64-column tile of a cluster (fci index)
+      auto& fseg = rc.fseg;
+      gather.clear(); trsm.clear(); rot.clear(); fci.clear(); fz.clear(); fseg.clear();
+      clu.assign(nb, CluItem{});
       int max_m = 1;
       for (int bi = 0; bi < nb; ++bi) max_m = std::max(max_m, live[Bo[bi]]);
       const bool fused = !nodc && max_m <= CI_MAX_M && !no_fused;
@@ -1119,21 +1194,22 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       // themselves (no write-back pass); needs the device patch and CPQR v3
       const bool dwb = fused && dpatch && !no_dwb;
       std::vector<int32_t> seg0v(nb, 0);
-      // the widths of B_s: dense, or (khat) the supported columns of each block; the column
-      // maps of a compressed B_s (CluItem::colmap / dmapn) go up with the batch's items
+      // the widths of B_s: dense, or (khat) the supported columns of each block (the segments
+      // point into the analysis's device copy of the supports, d_sup)
       const bool khat = khat_lv && dwb;
-      std::vector<int32_t> bkn(nb), bkw(nb), cmap, dmap;
+      std::vector<int32_t> bkn(nb), bkw(nb);
       std::vector<std::vector<int32_t>> nlen(nb);   // compressed width of each q of n(s)
-      std::vector<int64_t> cmo(nb, 0), dmo(nb, 0);
+      std::vector<std::vector<int64_t>> nsup(nb);   // its supported columns in su.idx (-1: dense)
       const L0Support& su = an->l0s;
-      for (int bi = 0; bi < nb; ++bi) {   // widths (and, khat, the offsets of the maps)
+      for (int bi = 0; bi < nb; ++bi) {
         const int32_t s = Bo[bi];
         bkn[bi] = L.kn[s];
         bkw[bi] = L.kw[s];
         if (!khat) continue;
-        int64_t e = su.sptr[s];
+        int64_t e = su.sptr[s], x = su.iptr[s];
         bkn[bi] = bkw[bi] = 0;
         nlen[bi].reserve(lev.H[s].size());
+        nsup[bi].reserve(lev.H[s].size());
         for (int pass = 0; pass < 2; ++pass)
           for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
             const int32_t ln = su.len[e++];
@@ -1144,39 +1220,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             } else {
               bkn[bi] += c;
               nlen[bi].push_back(c);
+              nsup[bi].push_back(ln < 0 ? -1 : x);
             }
+            if (ln > 0) x += ln;
           }
         L.ldB[s] = bkn[bi] + bkw[bi];
-        cmo[bi] = bi ? cmo[bi - 1] + bkn[bi - 1] + bkw[bi - 1] : 0;
-        dmo[bi] = bi ? dmo[bi - 1] + bkn[bi - 1] : 0;
-      }
-      if (khat && nb > 0) {   // the maps: supported local columns (runs of su.idx) / identity
-        cmap.resize(cmo[nb - 1] + bkn[nb - 1] + bkw[nb - 1]);
-        dmap.resize(dmo[nb - 1] + bkn[nb - 1]);
-        for (int bi = 0; bi < nb; ++bi) {
-          const int32_t s = Bo[bi];
-          int64_t e = su.sptr[s], x = su.iptr[s];
-          int32_t* cm = cmap.data() + cmo[bi];
-          int32_t* dm = dmap.data() + dmo[bi];
-          int32_t dn = 0;   // dense n-column of q's first column
-          for (int pass = 0; pass < 2; ++pass)
-            for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
-              const int32_t ln = su.len[e++];
-              const int32_t c = ln < 0 ? live[q] : ln;
-              if (ln < 0) {
-                for (int32_t j = 0; j < c; ++j) cm[j] = j;
-              } else {
-                std::memcpy(cm, su.idx.data() + x, sizeof(int32_t) * c);
-                x += c;
-              }
-              if (pass == 1) {
-                for (int32_t j = 0; j < c; ++j) dm[j] = dn + cm[j];
-                dm += c;
-                dn += live[q];
-              }
-              cm += c;
-            }
-        }
       }
       for (int bi = 0; bi < nb; ++bi) {
         fkn[Bo[bi]] = bkn[bi];
@@ -1218,98 +1266,133 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           }
         }
       double* wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
-      for (int bi = 0; bi < nb; ++bi) {
-        const int32_t s = Bo[bi];
-        const int32_t m = live[s], kn = bkn[bi], kw = bkw[bi], ldB = L.ldB[s];
-        double* w0 = ws + wo[bi];
-        L.G[s] = w0;
-        L.V[s] = w0 + (int64_t)m * m;
-        L.tau[s] = w0 + 2 * (int64_t)m * m;
-        L.nu[s] = L.tau[s] + ((m + 3) & ~3);
-        L.B[s] = L.nu[s] + ((kw + 3) & ~3);   // 32-byte aligned
-        double* ginv = L.B[s] + (((int64_t)m * (kn + kw) + 3) & ~int64_t(3));   // G^{-1} (fused path)
-        CluItem& it = clu[bi];
-        it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
-        it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
-        it.ldC = L.kn[s];   // Cout keeps the dense n-columns (the apply's record)
-        it.Wt = go[bi] >= 0 ? wtmp + go[bi] : nullptr;
-        if (m == 0) continue;
-        double* p; int32_t ld, tr;
-        bs.get(s, s, p, ld, tr);
-        // the store keeps the lower triangle of a diagonal block; dc = 0 rotates both sides
-        // of A_ss, so it is gathered as the full symmetric block (copy mode 2)
-        if (fused && tr) fail(HS_E_INTERNAL, "diagonal block stored transposed");
-        const double* pss = p;
-        const int32_t ldss = ld;
-        if (!fused) gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
-        const int32_t seg0 = (int32_t)fseg.size();
-        int32_t col = 0, dcol = 0;   // the block's first column in B_s / in the dense B_s
-        const auto& ro = row_offs(s);
-        size_t kq = 0;
-        int64_t e = khat ? an->l0s.sptr[s] : 0;
-        for (int pass = 0; pass < 2; ++pass)
-          for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
-            const int64_t o = ro[kq++];
-            const int32_t wq = khat && an->l0s.len[e] >= 0 ? an->l0s.len[e] : live[q];
-            if (khat) ++e;
-            if (live[q] > 0) {
-              if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
-              bs.at(s, q, o, p, ld, tr);
-              if (fused) {
-                if (wq > 0) fseg.push_back(FusedSeg{p, ld, tr, col, wq, dcol, 0});
-              } else {
-                gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+      // the batch's items, planned in contiguous chunks of clusters on PT host threads (segment
+      // indices chunk-local, rebased when the chunks are joined in order: the same item lists
+      // as a sequential pass)
+      const int PT = plan_threads(nb);
+      auto& parts = rc.parts;
+      if ((int)parts.size() < PT) parts.resize(PT);
+      for (int t = 0; t < PT; ++t) parts[t].clear();
+      const double tfa = now_s();
+      t_fh[3] += tfa - tfh1;
+      par_chunks(nb, PT, [&](int b0, int b1, int t) {
+        PlanPart& P = parts[t];
+        for (int bi = b0; bi < b1; ++bi) {
+          const int32_t s = Bo[bi];
+          const int32_t m = live[s], kn = bkn[bi], kw = bkw[bi], ldB = L.ldB[s];
+          double* w0 = ws + wo[bi];
+          L.G[s] = w0;
+          L.V[s] = w0 + (int64_t)m * m;
+          L.tau[s] = w0 + 2 * (int64_t)m * m;
+          L.nu[s] = L.tau[s] + ((m + 3) & ~3);
+          L.B[s] = L.nu[s] + ((kw + 3) & ~3);   // 32-byte aligned
+          double* ginv = L.B[s] + (((int64_t)m * (kn + kw) + 3) & ~int64_t(3));   // G^{-1} (fused path)
+          CluItem& it = clu[bi];
+          it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
+          it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
+          it.ldC = L.kn[s];   // Cout keeps the dense n-columns (the apply's record)
+          it.kwd = khat ? L.kw[s] : -1;
+          it.Wt = go[bi] >= 0 ? wtmp + go[bi] : nullptr;
+          if (m == 0) continue;
+          double* p; int32_t ld, tr;
+          bs.get(s, s, p, ld, tr);
+          // the store keeps the lower triangle of a diagonal block; dc = 0 rotates both sides
+          // of A_ss, so it is gathered as the full symmetric block (copy mode 2)
+          if (fused && tr) fail(HS_E_INTERNAL, "diagonal block stored transposed");
+          const double* pss = p;
+          const int32_t ldss = ld;
+          if (!fused) P.gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
+          const int32_t seg0 = (int32_t)P.fseg.size();
+          int32_t col = 0, dcol = 0;   // the block's first column in B_s / in the dense B_s
+          const auto& ro = row_offs(s);
+          size_t kq = 0;
+          int64_t e = khat ? su.sptr[s] : 0, x = khat ? su.iptr[s] : 0;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+              const int64_t o = ro[kq++];
+              const int32_t ln = khat ? su.len[e++] : -1;   // >= 0: the supported columns at su.idx[x]
+              const int32_t wq = ln >= 0 ? ln : live[q];
+              const int32_t* sidx = ln >= 0 ? d_sup + x : nullptr;
+              if (ln > 0) x += ln;
+              if (live[q] > 0) {
+                if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
+                bs.at(s, q, o, p, ld, tr);
+                if (fused) {
+                  if (wq > 0) P.fseg.push_back(FusedSeg{p, sidx, ld, tr, col, wq, dcol, 0});
+                } else {
+                  P.gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+                }
+              }
+              col += wq;
+              dcol += live[q];
+            }
+          const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
+          if (fused) {
+            // segments are in column order: each tile takes the run of segments overlapping it
+            int32_t sb = seg0;
+            const int32_t se = (int32_t)P.fseg.size();
+            const int32_t ci = (int32_t)P.fci.size();   // chunk-local, rebased at the join
+            P.fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+            if (dwb) {
+              seg0v[bi] = seg0;
+              it.nseg = se - seg0;
+              it.Dss = const_cast<double*>(pss);
+              it.ldss = ldss;
+              it.dwb = 1;
+              it.keepB = f->keep_records ? 1 : 0;
+              if (L.kn[s] > 0) {
+                L.C[s] = ctmp + co[bi];   // C_s = rows [r, m) of the rotated B_n (K <= m)
+                it.Cout = L.C[s];
               }
             }
-            col += wq;
-            dcol += live[q];
-          }
-        const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
-        if (fused) {
-          // segments are in column order: each tile takes the run of segments overlapping it
-          int32_t sb = seg0;
-          const int32_t se = (int32_t)fseg.size();
-          fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
-          if (dwb) {
-            seg0v[bi] = seg0;
-            it.nseg = se - seg0;
-            it.Dss = const_cast<double*>(pss);
-            it.ldss = ldss;
-            it.dwb = 1;
-            it.keepB = f->keep_records ? 1 : 0;
-            if (L.kn[s] > 0) {
-              L.C[s] = ctmp + co[bi];   // C_s = rows [r, m) of the rotated B_n (K <= m)
-              it.Cout = L.C[s];
+            for (int32_t c0 = 0; c0 < ldB; c0 += 64) {
+              const int32_t nc = std::min(64, ldB - c0);
+              while (sb < se && P.fseg[sb].col + P.fseg[sb].len <= c0) ++sb;
+              int32_t sf = sb;
+              while (sf < se && P.fseg[sf].col < c0 + nc) ++sf;
+              P.fz.push_back(ScaleTile{ci, c0, nc, sb, sf, 0});
             }
+          } else {
+            for (int32_t c0 = 0; c0 < ldB; c0 += tw) P.trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
           }
-          for (int32_t c0 = 0; c0 < ldB; c0 += 64) {
-            const int32_t nc = std::min(64, ldB - c0);
-            while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
-            int32_t sf = sb;
-            while (sf < se && fseg[sf].col < c0 + nc) ++sf;
-            fz.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, c0, nc, sb, sf, l, s, bi, 0});
+          if (kw > 0 || (dwb && kn > 0)) {   // the n-columns are rotated by k_rotate_n
+            const int32_t rw = rot_tile_cols(m, max_m);
+            for (int32_t c0 = 0; c0 < kn; c0 += rw) P.rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
           }
-        } else {
-          for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
+          if (fused) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
+            it.Ginv = ginv;
+            it.Tout = L.T[s];
+            const int32_t rw = rot_tile_cols(m, max_m);
+            for (int32_t c0 = 0; c0 < m; c0 += rw) P.rot.push_back(TrsmItem{bi, c0, std::min(rw, m - c0), 1});
+          }
+          P.fl1 += (double)m * m * m / 3.0;
+          P.fl2 += (double)m * m * ldB;
         }
-        if (kw > 0 || (dwb && kn > 0)) {   // the n-columns are rotated by k_rotate_n
-          const int32_t rw = rot_tile_cols(m, max_m);
-          for (int32_t c0 = 0; c0 < kn; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
+      });
+      const double tfb = now_s();
+      t_fh[4] += tfb - tfa;
+      for (int t = 0; t < PT; ++t) {
+        PlanPart& P = parts[t];
+        const int32_t sbase = (int32_t)fseg.size(), cbase = (int32_t)fci.size();
+        fseg.insert(fseg.end(), P.fseg.begin(), P.fseg.end());
+        for (ScaleTile x : P.fz) {
+          x.ci += cbase;
+          x.seg_begin += sbase;
+          x.seg_end += sbase;
+          fz.push_back(x);
         }
-        if (fused) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
-          it.Ginv = ginv;
-          it.Tout = L.T[s];
-          const int32_t rw = rot_tile_cols(m, max_m);
-          for (int32_t c0 = 0; c0 < m; c0 += rw) rot.push_back(TrsmItem{bi, c0, std::min(rw, m - c0), 1});
-        }
-        S.flops += (double)m * m * m / 3.0 + (double)m * m * ldB;
-        S.flops_phase[1] += (double)m * m * m / 3.0;
-        S.flops_phase[2] += (double)m * m * ldB;
+        for (int bi = chunk_lo(nb, PT, t); bi < chunk_lo(nb, PT, t + 1); ++bi) seg0v[bi] += sbase;
+        gather.insert(gather.end(), P.gather.begin(), P.gather.end());
+        trsm.insert(trsm.end(), P.trsm.begin(), P.trsm.end());
+        rot.insert(rot.end(), P.rot.begin(), P.rot.end());
+        fci.insert(fci.end(), P.fci.begin(), P.fci.end());
+        S.flops += P.fl1 + P.fl2;
+        S.flops_phase[1] += P.fl1;
+        S.flops_phase[2] += P.fl2;
       }
       // the first half's launches: at once (host patch), or (device patch) deferred until the
       // second half is planned, so that both uploads precede one uninterrupted kernel chain
       std::function<void(bool)> first_half_launch;   // argument: publish the ranks here
-      size_t iCM = 0, iDM = 0;                        // the column maps in upA (khat)
       const double tfh2 = now_s();
       t_fh[1] += tfh2 - tfh1;
       if (nb > 0) {
@@ -1318,24 +1401,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         std::vector<unsigned long long> nmax(nb, 0ull);
         const size_t iG = upA.add(gather), iC = upA.add(clu), iT = upA.add(trsm), iR = upA.add(rot),
                      iM = upA.add(nmax), iF = upA.add(fz), iS = upA.add(fseg), iI = upA.add(fci);
-        iCM = upA.add(cmap);
-        iDM = upA.add(dmap);
         upA.stage.ensure(upA.total);
         upA.dev.ensure(upA.total);
         for (int bi = 0; bi < nb; ++bi) clu[bi].nmax = upA.dptr<unsigned long long>(iM) + bi;
-        for (auto& f : fz) f.nmax = upA.dptr<unsigned long long>(iM) + f.bi;
+        for (auto& f : fci) f.nmax = upA.dptr<unsigned long long>(iM) + f.bi;   // R-floor slot
         for (int bi = 0; bi < nb; ++bi)
           if (clu[bi].dwb) clu[bi].seg = upA.dptr<FusedSeg>(iS) + seg0v[bi];
-        if (khat) {
-          for (int bi = 0; bi < nb; ++bi) {
-            clu[bi].colmap = upA.dptr<int32_t>(iCM) + cmo[bi];
-            clu[bi].dmapn = upA.dptr<int32_t>(iDM) + dmo[bi];
-          }
-          for (auto& f : fz) f.colmap = clu[f.bi].colmap;
-        }
         upA.copy_in(iG, gather); upA.copy_in(iC, clu); upA.copy_in(iT, trsm); upA.copy_in(iR, rot);
         upA.copy_in(iM, nmax); upA.copy_in(iF, fz); upA.copy_in(iS, fseg); upA.copy_in(iI, fci);
-        upA.copy_in(iCM, cmap); upA.copy_in(iDM, dmap);
         t_plan += now_s() - tp0;
         t_fh[2] += now_s() - tfh2;
         d_clu_batch = upA.dptr<CluItem>(iC);
@@ -1351,7 +1424,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             pt.rec(pt.a[1], st);
             launch_chol(upA.dptr<FusedItem>(iI), (int)nfci, max_m, d_status, st);
             pt.rec(pt.a[2], st);
-            launch_scale_tiles(upA.dptr<FusedItem>(iF), (int)nfz, upA.dptr<FusedSeg>(iS), max_m, st);
+            launch_scale_tiles(upA.dptr<FusedItem>(iI), upA.dptr<ScaleTile>(iF), (int)nfz, upA.dptr<FusedSeg>(iS),
+                               max_m, st);
           } else {
             launch_copy2d(upA.dptr<CopyItem>(iG), (int)ngather, st);
             pt.rec(pt.a[1], st);
@@ -1382,12 +1456,15 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       // phantom whose tiles exit at once).  Remote clusters of a phase-II batch are planned if
       // this rank will receive their record.
       const double tpp = now_s();
-      std::vector<SchurSrc> srcs;
+      auto& srcs = rc.srcs;
       std::vector<int32_t> src_cl;
-      std::vector<NbCol> nbc;
+      auto& nbc = rc.nbc;
+      srcs.clear();
+      nbc.clear();
       std::vector<std::vector<SchurTile2>> waves;
       std::vector<int32_t> touched;
-      std::vector<CopyItem> wb;
+      auto& wb = rc.wb;
+      wb.clear();
       std::vector<double*> id_ptr;
       std::vector<int32_t> id_ld, id_r;
       std::vector<FormTItem> ft;
@@ -1422,7 +1499,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         const auto& ns = lev.H[s];
         std::vector<int32_t> noff(ns.size() + 1, 0);
         auto nwid = [&](size_t a) { return khat ? nlen[k][a] : live[ns[a]]; };
-        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + nwid(a);
+        std::vector<int32_t> dnoff(ns.size() + 1, 0);   // ... and in the dense n-part (C_s's columns)
+        for (size_t a = 0; a < ns.size(); ++a) {
+          noff[a + 1] = noff[a] + nwid(a);
+          dnoff[a + 1] = dnoff[a] + live[ns[a]];
+        }
         if (kc > 0) {
           // wave = lowest wave in which no earlier source shares a neighbour with s
           uint64_t used = 0;
@@ -1433,13 +1514,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
           const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
           SchurSrc sc{nullptr, dwb ? kn : ldB, 0, kc, (int32_t)nbc.size(), 0, 0};
-          if (khat) {
-            sc.lmap = upA.dptr<int32_t>(iCM) + cmo[k] + bkw[k];
-            sc.dmap = upA.dptr<int32_t>(iDM) + dmo[k];
-          }
           for (size_t a = 0; a < ns.size(); ++a)
             if (live[ns[a]] > 0) {
-              if (nwid(a) > 0) nbc.push_back(NbCol{ns[a], noff[a], nwid(a), (int32_t)a});
+              if (nwid(a) > 0)
+                nbc.push_back(NbCol{ns[a], noff[a], nwid(a), (int32_t)a, dnoff[a], 0,
+                                    khat && nsup[k][a] >= 0 ? d_sup + nsup[k][a] : nullptr});
               if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
               wave_mask[ns[a]] |= bit;
             }
@@ -1669,7 +1748,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       const double tq3 = now_s();
       for (int32_t q : touched) wave_mask[q] = 0;
       for (size_t k = 0; k < srcs.size(); ++k) srcs[k].pairs = lp.pairs + lp.poff[src_cl[k]];   // the level's pair tables
-      std::vector<SchurTile2> tiles;
+      auto& tiles = rc.tiles;
+      tiles.clear();
       std::vector<int32_t> wave_off(1, 0);
       for (const auto& wv : waves) {
         tiles.insert(tiles.end(), wv.begin(), wv.end());
@@ -1686,7 +1766,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       if (second) {
         if (!dpatch) split_copies(wb);   // dpatch: item indices are patch targets (C copies pre-split)
         upB.reset();
-        std::vector<PatchItem> patch(prefs.size());
+        auto& patch = rc.patch;
+        patch.assign(prefs.size(), PatchItem{});
         const size_t jT = upB.add(tiles), jS = upB.add(srcs), jN = upB.add(nbc), jW = upB.add(wb),
                      jP = upB.add(id_ptr), jL = upB.add(id_ld), jR = upB.add(id_r), jF = upB.add(ft),
                      jX = upB.add(patch);
@@ -2164,8 +2245,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     std::fprintf(stderr, "[hs profile] host planning %.1f ms: schur+gather-side %.1f, write-back %.1f, apply %.1f, batch tail %.1f, level transitions %.1f\n",
                  1e3 * t_plan, 1e3 * t_sub[0], 1e3 * t_sub[1], 1e3 * t_sub[2], 1e3 * t_sub[3], 1e3 * t_trans);
   if (std::getenv("HS_PROFILE"))
-    std::fprintf(stderr, "[hs profile] first-half planning: shapes + column maps %.1f ms, items %.1f ms, upload staging %.1f ms\n",
-                 1e3 * t_fh[0], 1e3 * t_fh[1], 1e3 * t_fh[2]);
+    std::fprintf(stderr, "[hs profile] first-half planning: shapes + column maps %.1f ms, items %.1f ms (workspace %.1f, "
+                 "%d threads %.1f), upload staging %.1f ms\n", 1e3 * t_fh[0], 1e3 * t_fh[1], 1e3 * t_fh[3],
+                 plan_threads(1 << 20), 1e3 * t_fh[4], 1e3 * t_fh[2]);
   if (std::getenv("HS_PROFILE") || std::getenv("HS_RANK_WAIT"))
     std::fprintf(stderr, "[hs profile] host blocked on batch ranks: %.1f ms of %.1f ms; issuing uploads + kernels %.1f ms\n",
                  1e3 * t_rank_wait, ms, 1e3 * t_launch);

@@ -1,11 +1,10 @@
 // a0 + a1 + a2 for the DC path (clusters up to CI_MAX_M): the deferred-compression scaling
 // B_s = G_s^{-1} [A_sw | A_sn] with A_ss = G_s G_s^T (Eq. CC:eqn:scaling)
 // as two kernels, no gather pass and no CTA-wide barrier inside the triangular solve:
-//   k_chol       one CTA per cluster: A_ss read straight from the level's block store into
-//                shared memory (as its upper triangle), right-looking Cholesky with one
-//                barrier per pivot (the trailing update uses the unscaled row, the scaling
-//                by sqrt(d_j) happens once at the end), G_s stored to the workspace;
-//                It also forms G_s^{-1} (warp-synchronous forward substitution on I);
+//   k_chol_mma   one CTA per cluster: A_ss read straight from the level's block store into
+//                shared memory, blocked (8 x 8 tiles) Cholesky and G_s^{-1} with the panel,
+//                trailing and inverse products on the FP64 tensor cores; G_s and G_s^{-1}
+//                stored to the workspace;
 //   k_scale_mma  one CTA per (cluster, 64-column tile): the tile of [A_sw | A_sn] gathered
 //                from the store segments, B = G_s^{-1} A as an m x m by m x 64 product on the
 //                FP64 tensor cores (DMMA), B stored and the largest n-column norm (R-floor)
@@ -23,125 +22,6 @@ namespace {
 
 constexpr int ST_TW = 64;   // columns per k_scale_mma CTA
 
-template <int R4>
-__global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ items, DevStatus* status) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ double sm[];
-  const FusedItem it = items[blockIdx.x];
-  const int m = it.m;
-  if (m == 0) return;
-  const int ldu = m + 1;
-  double* U = sm;   // U = the upper triangle (A_ss^T), ld m + 1
-  __shared__ double rd[CI_MAX_M];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  for (int e = tid; e < m * m; e += blockDim.x) {
-    const int i = e / m, k = e % m;   // A[i][k], k <= i  ->  U[k][i]
-    if (k <= i) U[k * ldu + i] = it.Ass[(int64_t)i * it.lda + k];
-  }
-  __syncthreads();
-  // step j subtracts U[j][i] U[j][k] / d_j from the trailing U[i][k] (j < i <= k); row j is
-  // final after step j and never written again
-  for (int j = 0; j < m; ++j) {
-    const double* uj = U + j * ldu;
-    const double d = uj[j];
-    if (!(d > 0.0)) {   // every thread reads the same d: uniform exit
-      if (tid == 0 && atomicCAS(&status->flag, 0, 1) == 0) {
-        status->level = it.level;
-        status->cluster = it.cluster;
-        status->pivot = j;
-        status->value = d;
-      }
-      return;
-    }
-    const double inv = 1.0 / d;
-    double ujr[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int k = lane + 32 * t;
-      ujr[t] = (k > j && k < m) ? uj[k] : 0.0;
-    }
-    int i = j + 1 + wid;
-    for (; i + nw < m; i += 2 * nw) {   // two rows at a time: independent loads before stores
-      const int i2 = i + nw;
-      const double f1 = uj[i] * inv, f2 = uj[i2] * inv;
-      double* u1 = U + i * ldu;
-      double* u2 = U + i2 * ldu;
-      double a1[4], a2[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int k = lane + 32 * t;
-        a1[t] = (k >= i && k < m) ? u1[k] : 0.0;
-        a2[t] = (k >= i2 && k < m) ? u2[k] : 0.0;
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int k = lane + 32 * t;
-        if (k >= i && k < m) u1[k] = a1[t] - f1 * ujr[t];
-        if (k >= i2 && k < m) u2[k] = a2[t] - f2 * ujr[t];
-      }
-    }
-    if (i < m) {
-      const double f1 = uj[i] * inv;
-      double* u1 = U + i * ldu;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int k = lane + 32 * t;
-        if (k >= i && k < m) u1[k] -= f1 * ujr[t];
-      }
-    }
-    __syncthreads();
-  }
-  if (tid < m) rd[tid] = 1.0 / sqrt(U[tid * ldu + tid]);
-  __syncthreads();
-  // U <- G^T in place: G[i][j] = U[j][i] / sqrt(d_j) (i > j), G[j][j] = sqrt(d_j)
-  for (int e = tid; e < m * m; e += blockDim.x) {
-    const int j = e / m, i = e % m;
-    if (i > j) U[j * ldu + i] *= rd[j];
-    else if (i == j) U[j * ldu + j] = sqrt(U[j * ldu + j]);
-  }
-  __syncthreads();
-  for (int e = tid; e < m * m; e += blockDim.x) {   // G_s (lower, zeros above)
-    const int i = e / m, j = e % m;
-    it.G[e] = j <= i ? U[j * ldu + i] : 0.0;
-  }
-  // G_s^{-1} (lower) by forward substitution on I, warp-synchronously: warp w owns columns
-  // cb + 8w + (lane & 7), lane group gr = lane >> 3 owns rows gr + 4t in registers; the
-  // pivot of row i is broadcast by shuffle (no CTA barrier in the m-step chain).  Both the
-  // deferred-compression scaling (a DMMA product, k_scale_mma) and the apply operator
-  // T_s = U^T G_s^{-1} (k_form_T) consume it.
-  const int gr = lane >> 3;
-  for (int cb = 0; cb < m; cb += 64) {
-    const int col = cb + wid * 8 + (lane & 7);
-    double r[R4];
-#pragma unroll
-    for (int t = 0; t < R4; ++t) r[t] = (gr + 4 * t == col) ? 1.0 : 0.0;
-#pragma unroll
-    for (int ti = 0; ti < R4; ++ti) {
-#pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        const int i = 4 * ti + gi;
-        if (i < m && i >= cb) {   // uniform over the CTA; rows above the block stay zero
-          const double* gc = U + i * ldu;   // column i of G: gc[l] = G[l][i], l >= i
-          if (gr == gi) r[ti] = r[ti] * rd[i];   // 1 / G_ii (rd holds 1/sqrt(d_i) = 1/G_ii)
-          const double xi = __shfl_sync(0xffffffffu, r[ti], (lane & 7) + 8 * gi);
-#pragma unroll
-          for (int t = ti; t < R4; ++t) {
-            const int l = gr + 4 * t;
-            if (l > i && l < m) r[t] = fma(-gc[l], xi, r[t]);
-          }
-        }
-      }
-    }
-    if (col < m)
-#pragma unroll
-      for (int t = 0; t < R4; ++t) {
-        const int l = gr + 4 * t;
-        if (l < m) it.Ginv[(int64_t)l * m + col] = r[t];
-      }
-  }
-}
-
 // B[:, c0:c0+nc] = G^{-1} A[:, c0:c0+nc] on the FP64 tensor cores: the tile of [A_sw | A_sn]
 // is gathered from the store segments into shared memory, G_s^{-1} (lower) staged beside it,
 // and the m x 64 product formed with DMMA (mma.sync.m8n8k4.f64): warp w owns output columns
@@ -151,15 +31,192 @@ __global__ void __launch_bounds__(256) k_chol(const FusedItem* __restrict__ item
 // reduced from it.
 constexpr int SM_LDX = 68;   // tile row stride (doubles)
 __host__ __device__ __forceinline__ int mma_ldg(int m) { return ((m + 11) / 16) * 16 + 4; }   // >= m, == 4 mod 16
+// A_ss = G_s G_s^T and G_s^{-1}, blocked by 8 x 8 tiles on the FP64 tensor cores
+// (DMMA m8n8k4).  One CTA per cluster, the matrix in shared memory (rows padded to 8 NB8
+// with an identity tail, row stride == 4 mod 16: conflict-free fragments).  Per diagonal
+// tile kb: warp 0 factors the 8 x 8 tile and inverts it (8 warp-synchronous steps each);
+// the panel L[ib][kb] = A[ib][kb] L_kk^{-T} and the trailing update A[ib][jb] -= L[ib][kb]
+// L[jb][kb]^T are 8 x 8 x 8 DMMA products spread over the warps (3 barriers per tile
+// column instead of one per pivot).  G^{-1} follows by blocked forward substitution,
+// X[ib][jb] = -X[ib][ib] sum_{jb <= t < ib} L[ib][t] X[t][jb], one tile row at a time.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+// One warp: the 8 x 8 lower tile T = G_kk G_kk^T factored in place (G_kk) and its inverse
+// written to Y, in registers: lane c (and its copies c + 8, c + 16, c + 24) holds column c of
+// T and of Y; step j broadcasts column j (shuffles), every lane updates its column (the
+// loop over j is unrolled, so every register index is static).  false: pivot j not positive.
+__device__ __forceinline__ bool diag8(double* T, double* Y, int ld, int lane, double& dbad, int& jbad) {
+  const int c = lane & 7;
+  double t[8], y[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    t[r] = T[r * ld + c];
+    y[r] = r == c ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double d = __shfl_sync(0xffffffffu, t[j], j);
+    if (!(d > 0.0)) {   // the same d on every lane
+      dbad = d;
+      jbad = j;
+      return false;
+    }
+    const double g = sqrt(d), rg = 1.0 / g;
+    if (c == j) {
+      t[j] = g;
+#pragma unroll
+      for (int r = j + 1; r < 8; ++r) t[r] *= rg;
+    }
+    double v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = __shfl_sync(0xffffffffu, t[r], j);   // column j of G
+    double vc = v[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) vc = c == q ? v[q] : vc;   // G[c][j]
+#pragma unroll
+    for (int r = j + 1; r < 8; ++r)
+      if (c > j && r >= c) t[r] = fma(-v[r], vc, t[r]);   // T[r][c] -= G[r][j] G[c][j]
+    y[j] *= rg;                                             // Y[j][c] final
+#pragma unroll
+    for (int r = j + 1; r < 8; ++r) y[r] = fma(-v[r], y[j], y[r]);
+  }
+  if (lane < 8)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r >= c) T[r * ld + c] = t[r];
+      Y[r * ld + c] = r >= c ? y[r] : 0.0;
+    }
+  __syncwarp();
+  return true;
+}
+template <int NB8>
+__global__ void __launch_bounds__(256) k_chol_mma(const FusedItem* __restrict__ items, DevStatus* status) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ double sm[];
+  constexpr int MP = 8 * NB8;
+  const int ld = mma_ldg(MP);
+  double* L = sm;              // MP x ld: A (lower), overwritten by G
+  double* X = sm + MP * ld;    // MP x ld: G^{-1} (lower)
+  __shared__ int bad;
+  const FusedItem it = items[blockIdx.x];
+  const int m = it.m;
+  if (m == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int e0 = tid; e0 < MP * MP; e0 += 8 * 256) {   // 8 loads in flight per thread
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + 256 * u, i = e / MP, k = e % MP;
+      v[u] = (e < MP * MP && i < m && k <= i) ? it.Ass[(int64_t)i * it.lda + k] : (i == k ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + 256 * u, i = e / MP, k = e % MP;
+      if (e < MP * MP) {
+        L[i * ld + k] = v[u];
+        X[i * ld + k] = 0.0;
+      }
+    }
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int kb = 0; kb < NB8; ++kb) {
+    const int o = 8 * kb;
+    if (w == 0) {   // factor the diagonal tile T = L[o:o+8, o:o+8] and invert it into X
+      double d;
+      int jbad;
+      if (!diag8(L + o * ld + o, X + o * ld + o, ld, lane, d, jbad) && lane == 0) {
+        bad = 1;
+        if (atomicCAS(&status->flag, 0, 1) == 0) {
+          status->level = it.level;
+          status->cluster = it.cluster;
+          status->pivot = o + jbad;
+          status->value = d;
+        }
+      }
+    }
+    __syncthreads();
+    if (bad) return;
+    // panel: L[ib][kb] = A[ib][kb] Y^T (Y = L_kk^{-1}), a tile per warp
+    for (int ib = kb + 1 + w; ib < NB8; ib += 8) {
+      double* P = L + 8 * ib * ld + o;
+      const double* Y = X + o * ld + o;
+      double c[2] = {0.0, 0.0};
+      const double a0 = P[fr * ld + fc], a1 = P[fr * ld + 4 + fc];
+      const double b0 = Y[fr * ld + fc], b1 = Y[fr * ld + 4 + fc];   // B[k][n] = Y[n][k]
+      dmma(c, a0, b0);
+      dmma(c, a1, b1);
+      P[fr * ld + 2 * fc] = c[0];
+      P[fr * ld + 2 * fc + 1] = c[1];
+    }
+    __syncthreads();
+    // trailing: A[ib][jb] -= L[ib][kb] L[jb][kb]^T, kb < jb <= ib
+    const int Tn = NB8 - kb - 1;
+    for (int t = w; t < Tn * (Tn + 1) / 2; t += 8) {
+      int ib = 0;
+      while ((ib + 1) * (ib + 2) / 2 <= t) ++ib;
+      const int jb = t - ib * (ib + 1) / 2;
+      const int I = 8 * (kb + 1 + ib), J = 8 * (kb + 1 + jb);
+      double* C = L + I * ld + J;
+      double c[2] = {C[fr * ld + 2 * fc], C[fr * ld + 2 * fc + 1]};
+      const double* Pi = L + I * ld + o;
+      const double* Pj = L + J * ld + o;
+      dmma(c, -Pi[fr * ld + fc], Pj[fr * ld + fc]);
+      dmma(c, -Pi[fr * ld + 4 + fc], Pj[fr * ld + 4 + fc]);
+      C[fr * ld + 2 * fc] = c[0];
+      C[fr * ld + 2 * fc + 1] = c[1];
+    }
+    __syncthreads();
+  }
+  // G^{-1}: tile row ib, every jb < ib on its own warp
+  for (int ib = 1; ib < NB8; ++ib) {
+    for (int jb = w; jb < ib; jb += 8) {
+      double s[2] = {0.0, 0.0};
+      for (int t = jb; t < ib; ++t) {   // S = sum_t L[ib][t] X[t][jb]
+        const double* Lt = L + 8 * ib * ld + 8 * t;
+        const double* Xt = X + 8 * t * ld + 8 * jb;
+        dmma(s, Lt[fr * ld + fc], Xt[fc * ld + fr]);
+        dmma(s, Lt[fr * ld + 4 + fc], Xt[(4 + fc) * ld + fr]);
+      }
+      double* D = X + 8 * ib * ld + 8 * jb;   // S staged in its destination, then X = -Y_ib S
+      D[fr * ld + 2 * fc] = s[0];
+      D[fr * ld + 2 * fc + 1] = s[1];
+      __syncwarp();
+      const double* Y = X + 8 * ib * ld + 8 * ib;
+      const double a0 = -Y[fr * ld + fc], a1 = -Y[fr * ld + 4 + fc];
+      const double b0 = D[fc * ld + fr], b1 = D[(4 + fc) * ld + fr];
+      double x[2] = {0.0, 0.0};
+      dmma(x, a0, b0);
+      dmma(x, a1, b1);
+      __syncwarp();
+      D[fr * ld + 2 * fc] = x[0];
+      D[fr * ld + 2 * fc + 1] = x[1];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * m; e += 256) {   // G and G^{-1}: lower, zeros above
+    const int i = e / m, k = e % m;
+    it.G[e] = k <= i ? L[i * ld + k] : 0.0;
+    it.Ginv[e] = k <= i ? X[i * ld + k] : 0.0;
+  }
+}
+
 template <int NRB>
-__global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__ items,
+__global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__ clus,
+                                                   const ScaleTile* __restrict__ tiles,
                                                    const FusedSeg* __restrict__ segs) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ double sm[];
-  const FusedItem it = items[blockIdx.x];
+  const ScaleTile tl = tiles[blockIdx.x];
+  const FusedItem it = clus[tl.ci];
   const int m = it.m;
-  if (m == 0 || it.nc <= 0) return;
+  if (m == 0 || tl.nc <= 0) return;
   const int ldg = mma_ldg(m), mp = 8 * NRB;   // rows padded to the 8-row blocks
   double* gi = sm;                  // mp x ldg, G^{-1} (zeros above the diagonal and below m)
   double* x = sm + (size_t)mp * ldg;   // mp x SM_LDX
@@ -179,9 +236,9 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
   }
   for (int e = tid; e < mp * SM_LDX; e += blockDim.x) x[e] = 0.0;
   __syncthreads();
-  for (int sg = it.seg_begin; sg < it.seg_end; ++sg) {   // the tile's columns from the store
+  for (int sg = tl.seg_begin; sg < tl.seg_end; ++sg) {   // the tile's columns from the store
     const FusedSeg sgm = segs[sg];
-    const int j0 = max(it.c0, sgm.col), j1 = min(it.c0 + it.nc, sgm.col + sgm.len);
+    const int j0 = max(tl.c0, sgm.col), j1 = min(tl.c0 + tl.nc, sgm.col + sgm.len);
     const int wd = j1 - j0, tot = m * wd;
     for (int e0 = tid; e0 < tot; e0 += 4 * 256) {
       double v[4];
@@ -197,8 +254,8 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
           i = e / wd;
           j = j0 + e % wd;
         }
-        dst[u] = e < tot ? i * SM_LDX + (j - it.c0) : -1;
-        const int lc = e >= tot ? 0 : (it.colmap ? it.colmap[j] : j - sgm.col);   // column inside the block
+        dst[u] = e < tot ? i * SM_LDX + (j - tl.c0) : -1;
+        const int lc = e >= tot ? 0 : (sgm.idx ? sgm.idx[j - sgm.col] : j - sgm.col);   // column inside the block
         v[u] = e < tot ? (sgm.trans ? sgm.src[(int64_t)lc * sgm.sld + i] : sgm.src[(int64_t)i * sgm.sld + lc])
                        : 0.0;
       }
@@ -235,12 +292,12 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
   __syncthreads();
   for (int e = tid; e < m * ST_TW; e += blockDim.x) {
     const int i = e / ST_TW, cc = e % ST_TW;
-    if (cc < it.nc) it.B[(int64_t)i * it.ldB + it.c0 + cc] = x[i * SM_LDX + cc];
+    if (cc < tl.nc) it.B[(int64_t)i * it.ldB + tl.c0 + cc] = x[i * SM_LDX + cc];
   }
-  if (it.nmax && it.c0 + it.nc > it.kw) {   // largest n-column norm (R-floor of tau_s)
+  if (it.nmax && tl.c0 + tl.nc > it.kw) {   // largest n-column norm (R-floor of tau_s)
     double s = -1.0;
-    const int n0 = max(0, it.kw - it.c0);
-    if (tid < ST_TW && tid >= n0 && tid < it.nc) {
+    const int n0 = max(0, it.kw - tl.c0);
+    if (tid < ST_TW && tid >= n0 && tid < tl.nc) {
       s = 0.0;
       for (int i = 0; i < m; ++i) s += x[i * SM_LDX + tid] * x[i * SM_LDX + tid];
       s = sqrt(s);
@@ -254,29 +311,32 @@ __global__ void __launch_bounds__(256) k_scale_mma(const FusedItem* __restrict__
 
 void launch_chol(const FusedItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st) {
   if (n <= 0) return;
-  const size_t sm = sizeof(double) * (size_t)max_m * (max_m + 1);
-  const int R = (max_m + 15) / 16;   // R4 = 4 R rows per lane group (the inverse)
-#define HS_CH(RR)                                               \
-  case RR:                                                      \
-    set_smem_attr((const void*)k_chol<4 * RR>, sm);             \
-    launch_pdl(k_chol<4 * RR>, dim3(n), dim3(256), sm, st, d_items, status); \
-    break;
-  switch (R) {
+  const int NB8 = (max_m + 7) / 8;
+#define HS_CH(B)                                                                   \
+  case B: {                                                                        \
+    const size_t sm = sizeof(double) * 2 * (size_t)(8 * B) * mma_ldg(8 * B);        \
+    set_smem_attr((const void*)k_chol_mma<B>, sm);                                 \
+    launch_pdl(k_chol_mma<B>, dim3(n), dim3(256), sm, st, d_items, status);        \
+    break;                                                                         \
+  }
+  switch (NB8) {
     HS_CH(1) HS_CH(2) HS_CH(3) HS_CH(4) HS_CH(5) HS_CH(6) HS_CH(7)
+    HS_CH(8) HS_CH(9) HS_CH(10) HS_CH(11) HS_CH(12) HS_CH(13) HS_CH(14)
     default: fail(HS_E_INTERNAL, "launch_chol: m above CI_MAX_M");
   }
 #undef HS_CH
   count_launch(1);
 }
 
-void launch_scale_tiles(const FusedItem* d_items, int n, const FusedSeg* d_segs, int max_m, cudaStream_t st) {
+void launch_scale_tiles(const FusedItem* d_clus, const ScaleTile* d_tiles, int n, const FusedSeg* d_segs, int max_m,
+                        cudaStream_t st) {
   if (n <= 0) return;
   const int nrb = (max_m + 7) / 8;
   const size_t sm = sizeof(double) * ((size_t)8 * nrb * mma_ldg(max_m) + (size_t)8 * nrb * SM_LDX);
 #define HS_SM(NB)                                                     \
   case NB:                                                            \
     set_smem_attr((const void*)k_scale_mma<NB>, sm);                  \
-    launch_pdl(k_scale_mma<NB>, dim3(n), dim3(256), sm, st, d_items, d_segs); \
+    launch_pdl(k_scale_mma<NB>, dim3(n), dim3(256), sm, st, d_clus, d_tiles, d_segs); \
     break;
   switch (nrb) {
     HS_SM(1) HS_SM(2) HS_SM(3) HS_SM(4) HS_SM(5) HS_SM(6) HS_SM(7)

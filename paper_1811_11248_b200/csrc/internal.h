@@ -41,6 +41,8 @@ struct L0Support {
   // coarse columns, dense); the supported local columns, ascending, at idx[iptr[s] ..]
   std::vector<int64_t> sptr, iptr;
   std::vector<int32_t> len, idx;
+  int32_t* d_idx = nullptr;   // idx on device dev (l0_support_device; freed with the analysis)
+  int dev = -1;
 };
 
 struct Analysis {
@@ -78,6 +80,8 @@ DistPlan make_plan(const Analysis& an, int world, int rank);
 std::vector<int32_t> receivers(const Analysis& an, const DistPlan& P, int l, int s);
 
 void build_l0_support(Analysis& an);   // fills an.l0s (idempotent, thread-safe)
+// an.l0s.idx on the device (uploaded once per analysis and device; thread-safe)
+const int32_t* l0_support_device(Analysis& an, int device);
 
 Analysis* analyze(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* coords,
                   int32_t coord_dim, const int32_t* column_id, const hs_analyze_opts& opt);

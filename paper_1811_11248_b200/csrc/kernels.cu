@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
   const NbCol* nb = nbc + s.nb_off;
   __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
   __shared__ double aq[16][68];
-  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
+  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64], r_dc[64], c_dc[64];
   __shared__ int r_slot[64], c_slot[64];
   __shared__ int r_list[64], c_list[64];
   __shared__ int nr, nc;
@@ -482,16 +482,13 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
   __shared__ int nbcol[SCH_NBS];
   const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  // this thread's C columns in the staged chunks (ii = tid & 63 in every load): the dense
-  // columns of compressed columns i0 + ii / j0 + ii (support-restricted level 0)
-  const int ii0 = tid & 63;
-  const double* Cp = s.C + (ii0 < rows ? (s.dmap ? s.dmap[t.i0 + ii0] : t.i0 + ii0) : 0);
-  const double* Cq = s.C + (ii0 < cols ? (s.dmap ? s.dmap[t.j0 + ii0] : t.j0 + ii0) : 0);
-  // (1) the neighbours' column starts into shared memory (the owner searches) + the first
-  // K-chunk of C
+  // (1) the neighbours' column starts into shared memory (the owner searches)
   const bool nst = s.nnb <= SCH_NBS;
   if (nst)
     for (int a = tid; a < s.nnb; a += blockDim.x) nbcol[a] = nb[a].col;
+  __syncthreads();
+  const double* Cp;
+  const double* Cq;
   auto load_chunk = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -502,8 +499,6 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
       aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC] : 0.0;
     }
   };
-  load_chunk(0);
-  __syncthreads();
   if (w < 2) {   // (2) owners of the tile's rows (warp 0) / columns (warp 1) by binary search,
                  // distinct owners in order (rows/cols are sorted by owner): ballots
     const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
@@ -528,23 +523,36 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
     const int s0 = __popc(m0 & le) - 1, s1 = __popc(m0) + __popc(m1 & le) - 1;
     int* own = w == 0 ? r_own : c_own;
     int* loc = w == 0 ? r_loc : c_loc;
+    int* dc = w == 0 ? r_dc : c_dc;   // the column of C (dense n-part)
     int* slot = w == 0 ? r_slot : c_slot;
     int* list = w == 0 ? r_list : c_list;
     if (lane < lim) {
       own[lane] = o0;
-      loc[lane] = s.lmap ? s.lmap[base + lane] : base + lane - nb[o0].col;
+      const NbCol g = nb[o0];
+      const int c = base + lane - g.col;
+      loc[lane] = g.sup ? g.sup[c] : c;
+      dc[lane] = g.dcol + loc[lane];
       slot[lane] = s0;
       if (f0) list[s0] = o0;
     }
     if (lane + 32 < lim) {
       own[lane + 32] = o1;
-      loc[lane + 32] = s.lmap ? s.lmap[base + lane + 32] : base + lane + 32 - nb[o1].col;
+      const NbCol g = nb[o1];
+      const int c = base + lane + 32 - g.col;
+      loc[lane + 32] = g.sup ? g.sup[c] : c;
+      dc[lane + 32] = g.dcol + loc[lane + 32];
       slot[lane + 32] = s1;
       if (f1) list[s1] = o1;
     }
     if (lane == 0) (w == 0 ? nr : nc) = __popc(m0) + __popc(m1);
   }
   __syncthreads();
+  // this thread's C columns in every staged chunk (ii = tid & 63): the first K-chunk loads
+  // while the pair table below is filled
+  const int ii0 = tid & 63;
+  Cp = s.C + (ii0 < rows ? r_dc[ii0] : 0);
+  Cq = s.C + (ii0 < cols ? c_dc[ii0] : 0);
+  load_chunk(0);
   // (3) target block pointers of the distinct owner pairs
   const bool table = nr <= SCH_MAXO && nc <= SCH_MAXO;
   if (table) {

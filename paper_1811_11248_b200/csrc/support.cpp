@@ -18,6 +18,8 @@
 //   supp(p, q) |= supp(s, q).
 // A block whose column cluster q was eliminated earlier on the level has q's r_q coarse
 // columns, all of them potentially nonzero (dense).
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -25,9 +27,34 @@
 
 namespace hs {
 
+namespace {
+std::mutex g_mu;
+}
+
+const int32_t* l0_support_device(Analysis& an, int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  L0Support& o = an.l0s;
+  if (!o.built) fail(HS_E_INTERNAL, "support: not built");
+  if (o.d_idx && o.dev == device) return o.d_idx;
+  if (o.d_idx) {   // cached on another device
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(o.dev);
+    cudaFree(o.d_idx);
+    cudaSetDevice(cur);
+    o.d_idx = nullptr;
+  }
+  const size_t bytes = sizeof(int32_t) * std::max<size_t>(o.idx.size(), 1);
+  if (cudaMalloc(&o.d_idx, bytes) != cudaSuccess) fail(HS_E_OOM, "support: device copy");
+  if (!o.idx.empty() &&
+      cudaMemcpy(o.d_idx, o.idx.data(), sizeof(int32_t) * o.idx.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    fail(HS_E_CUDA, "support: device copy");
+  o.dev = device;
+  return o.d_idx;
+}
+
 void build_l0_support(Analysis& an) {
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(g_mu);
   if (an.l0s.built) return;
   const Level& lev = an.levels.at(0);
   const int32_t nc = lev.nclus;
