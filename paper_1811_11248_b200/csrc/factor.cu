@@ -20,6 +20,8 @@
 #include <functional>
 #include <future>
 #include <memory>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <unordered_map>
 
@@ -463,47 +465,102 @@ int plan_threads(int n) {
   }();
   return std::max(1, std::min(hw, n / 128));
 }
-// fn(b0, b1, t) over the T chunks of [0, n): T - 1 helper threads and the caller; the first
-// exception is rethrown on the caller once every chunk is done
+// Persistent host worker threads for the batch planning (spawning threads per batch costs
+// more than the planning they would share).  run(T, fn) calls fn(t) for t = 1 .. T-1 on the
+// workers and fn(0) on the caller, and returns when all are done; the first exception is
+// rethrown on the caller.  Calls from several host threads are serialised.
+class PlanPool {
+ public:
+  static PlanPool& get() {
+    static PlanPool pool;
+    return pool;
+  }
+  void run(int T, const std::function<void(int)>& fn) {
+    if (T <= 1) {
+      fn(0);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      while ((int)th_.size() < T - 1) th_.emplace_back([this] { loop(); });
+      job_ = &fn;
+      next_ = 1;
+      ntask_ = T;
+      pending_ = T - 1;
+      err_ = nullptr;
+      ++gen_;
+    }
+    cv_.notify_all();
+    std::exception_ptr e0;
+    try {
+      fn(0);
+    } catch (...) {
+      e0 = std::current_exception();
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+    if (e0) std::rethrow_exception(e0);
+    if (err_) std::rethrow_exception(err_);
+  }
+  ~PlanPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < ntask_); });
+      if (stop_) return;
+      seen = gen_;
+      while (next_ < ntask_) {
+        const int t = next_++;
+        const std::function<void(int)>* job = job_;
+        lk.unlock();
+        std::exception_ptr e;
+        try {
+          (*job)(t);
+        } catch (...) {
+          e = std::current_exception();
+        }
+        lk.lock();
+        if (e && !err_) err_ = e;
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* job_ = nullptr;
+  int next_ = 0, ntask_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::exception_ptr err_;
+};
+
+// fn(b0, b1, t) over the T contiguous chunks of [0, n) on the planning pool
 template <class F>
 void par_chunks(int n, int T, F&& fn) {
   if (T <= 1) {
     fn(0, n, 0);
     return;
   }
-  std::vector<std::exception_ptr> ex(T);
-  auto run = [&](int t) {
-    try {
-      fn(chunk_lo(n, T, t), chunk_lo(n, T, t + 1), t);
-    } catch (...) {
-      ex[t] = std::current_exception();
-    }
-  };
-  std::vector<std::thread> th;
-  th.reserve(T - 1);
-  for (int t = 1; t < T; ++t) th.emplace_back(run, t);
-  run(0);
-  for (auto& x : th) x.join();
-  for (auto& e : ex)
-    if (e) std::rethrow_exception(e);
+  PlanPool::get().run(T, [&](int t) { fn(chunk_lo(n, T, t), chunk_lo(n, T, t + 1), t); });
 }
 
-// one planning thread's share of a batch's items (PlanPart) and the batch vectors, kept across
-// batches so that their storage is reused (no allocation, no first-touch page faults per batch)
-struct PlanPart {
-  std::vector<CopyItem> gather;
-  std::vector<TrsmItem> trsm, rot;
-  std::vector<FusedItem> fci;
-  std::vector<ScaleTile> fz;
-  std::vector<FusedSeg> fseg;
-  double fl1 = 0.0, fl2 = 0.0;
-  void clear() {
-    gather.clear(); trsm.clear(); rot.clear(); fci.clear(); fz.clear(); fseg.clear();
-    fl1 = fl2 = 0.0;
-  }
-};
+// the batch vectors, kept across batches so that their storage is reused (no allocation, no
+// first-touch page faults per batch)
 struct BatchVecs {
-  std::vector<PlanPart> parts;
+  std::vector<int32_t> cnt[6];
   std::vector<CopyItem> gather, wb;
   std::vector<CluItem> clu;
   std::vector<TrsmItem> trsm, rot;
@@ -1266,20 +1323,50 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           }
         }
       double* wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
-      // the batch's items, planned in contiguous chunks of clusters on PT host threads (segment
-      // indices chunk-local, rebased when the chunks are joined in order: the same item lists
-      // as a sequential pass)
+      // the batch's items: the counts per cluster (sequential, cheap), then every cluster fills
+      // its own ranges of the item lists on PT pooled host threads (the same lists as a
+      // sequential pass)
+      auto& cnt = rc.cnt;   // [6][nb + 1] prefix counts: segments, scale tiles, rotation tiles, fci, gathers, trsm
+      for (auto& v : cnt) v.assign(nb + 1, 0);
+      for (int bi = 0; bi < nb; ++bi) {
+        const int32_t s = Bo[bi], m = live[s], kn = bkn[bi], kw = bkw[bi], ldB = L.ldB[s];
+        int32_t c[6] = {0, 0, 0, 0, 0, 0};
+        if (m > 0) {
+          int64_t e = khat ? su.sptr[s] : 0;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int32_t q : (pass == 0 ? lev.w[s] : lev.H[s])) {
+              const int32_t ln = khat ? su.len[e++] : -1;
+              const int32_t wq = ln >= 0 ? ln : live[q];
+              if (live[q] > 0) {
+                if (fused) c[0] += wq > 0;
+                else ++c[4];
+              }
+            }
+          const int32_t rw = rot_tile_cols(m, max_m), tw = m <= SMEM_M ? 64 : 32;
+          if (fused) {
+            c[1] = (ldB + 63) / 64;
+            c[2] = (m + rw - 1) / rw;
+            c[3] = 1;
+          } else {
+            c[4] += 1;
+            c[5] = (ldB + tw - 1) / tw;
+          }
+          if (kw > 0 || (dwb && kn > 0)) c[2] += (kn + rw - 1) / rw;
+        }
+        for (int k = 0; k < 6; ++k) cnt[k][bi + 1] = cnt[k][bi] + c[k];
+      }
+      fseg.resize(cnt[0][nb]); fz.resize(cnt[1][nb]); rot.resize(cnt[2][nb]); fci.resize(cnt[3][nb]);
+      gather.resize(cnt[4][nb]); trsm.resize(cnt[5][nb]);
       const int PT = plan_threads(nb);
-      auto& parts = rc.parts;
-      if ((int)parts.size() < PT) parts.resize(PT);
-      for (int t = 0; t < PT; ++t) parts[t].clear();
+      std::vector<double> pfl(2 * PT, 0.0);
       const double tfa = now_s();
       t_fh[3] += tfa - tfh1;
       par_chunks(nb, PT, [&](int b0, int b1, int t) {
-        PlanPart& P = parts[t];
         for (int bi = b0; bi < b1; ++bi) {
           const int32_t s = Bo[bi];
           const int32_t m = live[s], kn = bkn[bi], kw = bkw[bi], ldB = L.ldB[s];
+          int32_t isg = cnt[0][bi], itl = cnt[1][bi], irt = cnt[2][bi], igt = cnt[4][bi], itr = cnt[5][bi];
+          const int32_t ci = cnt[3][bi];
           double* w0 = ws + wo[bi];
           L.G[s] = w0;
           L.V[s] = w0 + (int64_t)m * m;
@@ -1301,8 +1388,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           if (fused && tr) fail(HS_E_INTERNAL, "diagonal block stored transposed");
           const double* pss = p;
           const int32_t ldss = ld;
-          if (!fused) P.gather.push_back(CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0});
-          const int32_t seg0 = (int32_t)P.fseg.size();
+          if (!fused) gather[igt++] = CopyItem{p, L.G[s], ld, m, m, m, nodc ? 2 : tr, 0};
+          const int32_t seg0 = isg;
           int32_t col = 0, dcol = 0;   // the block's first column in B_s / in the dense B_s
           const auto& ro = row_offs(s);
           size_t kq = 0;
@@ -1318,9 +1405,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                 if (o < 0) fail(HS_E_INTERNAL, "gather: block of an owned row missing");
                 bs.at(s, q, o, p, ld, tr);
                 if (fused) {
-                  if (wq > 0) P.fseg.push_back(FusedSeg{p, sidx, ld, tr, col, wq, dcol, 0});
+                  if (wq > 0) fseg[isg++] = FusedSeg{p, sidx, ld, tr, col, wq, dcol, 0};
                 } else {
-                  P.gather.push_back(CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0});
+                  gather[igt++] = CopyItem{p, L.B[s] + col, ld, ldB, m, live[q], tr, 0};
                 }
               }
               col += wq;
@@ -1330,9 +1417,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           if (fused) {
             // segments are in column order: each tile takes the run of segments overlapping it
             int32_t sb = seg0;
-            const int32_t se = (int32_t)P.fseg.size();
-            const int32_t ci = (int32_t)P.fci.size();   // chunk-local, rebased at the join
-            P.fci.push_back(FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0});
+            const int32_t se = isg;
+            fci[ci] = FusedItem{pss, L.G[s], ginv, L.B[s], nullptr, m, ldss, ldB, kw, 0, 0, 0, 0, l, s, bi, 0};
             if (dwb) {
               seg0v[bi] = seg0;
               it.nseg = se - seg0;
@@ -1347,48 +1433,37 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             }
             for (int32_t c0 = 0; c0 < ldB; c0 += 64) {
               const int32_t nc = std::min(64, ldB - c0);
-              while (sb < se && P.fseg[sb].col + P.fseg[sb].len <= c0) ++sb;
+              while (sb < se && fseg[sb].col + fseg[sb].len <= c0) ++sb;
               int32_t sf = sb;
-              while (sf < se && P.fseg[sf].col < c0 + nc) ++sf;
-              P.fz.push_back(ScaleTile{ci, c0, nc, sb, sf, 0});
+              while (sf < se && fseg[sf].col < c0 + nc) ++sf;
+              fz[itl++] = ScaleTile{ci, c0, nc, sb, sf, 0};
             }
           } else {
-            for (int32_t c0 = 0; c0 < ldB; c0 += tw) P.trsm.push_back(TrsmItem{bi, c0, std::min(tw, ldB - c0), 0});
+            for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm[itr++] = TrsmItem{bi, c0, std::min(tw, ldB - c0), 0};
           }
           if (kw > 0 || (dwb && kn > 0)) {   // the n-columns are rotated by k_rotate_n
             const int32_t rw = rot_tile_cols(m, max_m);
-            for (int32_t c0 = 0; c0 < kn; c0 += rw) P.rot.push_back(TrsmItem{bi, c0, std::min(rw, kn - c0), 0});
+            for (int32_t c0 = 0; c0 < kn; c0 += rw) rot[irt++] = TrsmItem{bi, c0, std::min(rw, kn - c0), 0};
           }
           if (fused) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
             it.Ginv = ginv;
             it.Tout = L.T[s];
             const int32_t rw = rot_tile_cols(m, max_m);
-            for (int32_t c0 = 0; c0 < m; c0 += rw) P.rot.push_back(TrsmItem{bi, c0, std::min(rw, m - c0), 1});
+            for (int32_t c0 = 0; c0 < m; c0 += rw) rot[irt++] = TrsmItem{bi, c0, std::min(rw, m - c0), 1};
           }
-          P.fl1 += (double)m * m * m / 3.0;
-          P.fl2 += (double)m * m * ldB;
+          if (isg != cnt[0][bi + 1] || itl != cnt[1][bi + 1] || irt != cnt[2][bi + 1] || igt != cnt[4][bi + 1] ||
+              itr != cnt[5][bi + 1])
+            fail(HS_E_INTERNAL, "batch plan: item counts");
+          pfl[2 * t] += (double)m * m * m / 3.0;
+          pfl[2 * t + 1] += (double)m * m * ldB;
         }
       });
       const double tfb = now_s();
       t_fh[4] += tfb - tfa;
       for (int t = 0; t < PT; ++t) {
-        PlanPart& P = parts[t];
-        const int32_t sbase = (int32_t)fseg.size(), cbase = (int32_t)fci.size();
-        fseg.insert(fseg.end(), P.fseg.begin(), P.fseg.end());
-        for (ScaleTile x : P.fz) {
-          x.ci += cbase;
-          x.seg_begin += sbase;
-          x.seg_end += sbase;
-          fz.push_back(x);
-        }
-        for (int bi = chunk_lo(nb, PT, t); bi < chunk_lo(nb, PT, t + 1); ++bi) seg0v[bi] += sbase;
-        gather.insert(gather.end(), P.gather.begin(), P.gather.end());
-        trsm.insert(trsm.end(), P.trsm.begin(), P.trsm.end());
-        rot.insert(rot.end(), P.rot.begin(), P.rot.end());
-        fci.insert(fci.end(), P.fci.begin(), P.fci.end());
-        S.flops += P.fl1 + P.fl2;
-        S.flops_phase[1] += P.fl1;
-        S.flops_phase[2] += P.fl2;
+        S.flops += pfl[2 * t] + pfl[2 * t + 1];
+        S.flops_phase[1] += pfl[2 * t];
+        S.flops_phase[2] += pfl[2 * t + 1];
       }
       // the first half's launches: at once (host patch), or (device patch) deferred until the
       // second half is planned, so that both uploads precede one uninterrupted kernel chain
