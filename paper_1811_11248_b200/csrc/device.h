@@ -346,6 +346,11 @@ void launch_form_T(const FormTItem* d_items, int n, int max_m, cudaStream_t st);
 void launch_apply_fwd_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_apply_post_level(const ApplyLevelArgs& a, cudaStream_t st);
 void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st);
+// batch-synchronous sweeps: the clusters d_cl[0, n) of one batch (levels of large batches)
+constexpr int BS_MAXG = 128;       // contributions per source
+constexpr int BS_MAXCOLS = 4096;   // k_n per source
+void launch_apply_fwd_batch(const ApplyLevelArgs& a, const int32_t* d_cl, int n, cudaStream_t st);
+void launch_apply_bwd_batch(const ApplyLevelArgs& a, const int32_t* d_cl, int n, cudaStream_t st);
 void launch_top_solve(double* y, const double* A, int N, int ld, cudaStream_t st);
 void launch_permute(const double* src, double* dst, const int64_t* idx, int64_t n, int scatter, cudaStream_t st);
 void launch_spmv(const int64_t* rowptr, const int32_t* colind, const double* vals, const double* x, double* y,

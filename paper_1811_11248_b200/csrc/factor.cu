@@ -703,7 +703,7 @@ hs_factor_s::~hs_factor_s() {
     for (double* p : l.cchunks) fr(p);
   }
   for (auto& p : ap.lv) {
-    fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb);
+    fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb); fr(p.d_bcl);
   }
   fr(ap.d_y); fr(ap.d_yf); fr(ap.d_xb); fr(ap.d_parts); fr(ap.d_ctr); fr(ap.d_contrib);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
@@ -2112,6 +2112,27 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         AP.ctr_off = ap.ctr_total;
         ap.ctr_total += 4 * (int64_t)lev.nclus + 2;
         ap.max_parts = std::max(ap.max_parts, AP.parts);
+        // batch-synchronous sweeps (one launch per batch) where the batches are large: the
+        // clusters of every batch, in order
+        {
+          int64_t nonempty = 0;
+          bool fits = !lev.batches.empty();
+          for (int32_t c = 0; c < lev.nclus; ++c) {
+            const ApplySrc& as = AP.src[c];
+            if (as.m == 0) continue;
+            ++nonempty;
+            fits = fits && as.tg_end - as.tg_begin <= BS_MAXG && as.kn <= BS_MAXCOLS;
+          }
+          AP.bsync = fits && nonempty >= 128 * (int64_t)lev.batches.size() && std::getenv("HS_APPLY_DEP") == nullptr;
+          AP.bcl.clear();
+          AP.boff.assign(1, 0);
+          if (AP.bsync)
+            for (const auto& Bt : lev.batches) {
+              for (int32_t c : Bt)
+                if (AP.src[c].m > 0) AP.bcl.push_back(c);
+              AP.boff.push_back((int32_t)AP.bcl.size());
+            }
+        }
         t_apply_plan += now_s() - ta;
       };
       if (dist) {
@@ -2382,6 +2403,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     up(AP.pull, AP.d_pull);
     up(AP.ctb, AP.d_ctb);
     up(AP.post_cl, AP.d_post_cl);
+    up(AP.bcl, AP.d_bcl);
   }
   HS_CUDA(cudaStreamSynchronize(st));
   if (dist) dist_solve_build(f, DP);

@@ -161,6 +161,11 @@ struct ApplyLevelPlan {
   PullSrc* d_pull = nullptr;
   Contrib* d_ctb = nullptr;
   int32_t* d_post_cl = nullptr;
+  // batch-synchronous sweeps (levels of large batches): the clusters of batch b are
+  // bcl[boff[b], boff[b+1])
+  bool bsync = false;
+  std::vector<int32_t> bcl, boff;
+  int32_t* d_bcl = nullptr;
 };
 
 struct ApplyPlan {

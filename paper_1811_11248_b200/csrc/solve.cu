@@ -181,7 +181,14 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   launch_permute(f->d_b, ap.d_y + ap.vbase[0], f->d_perm, n, 0, st);
   for (int l = 0; l < an->L_top; ++l) {
     mark();
-    launch_apply_fwd_level(level_args(f, l), st);
+    const ApplyLevelPlan& P = ap.lv[l];
+    if (P.bsync) {
+      const ApplyLevelArgs a = level_args(f, l);
+      for (size_t b = 0; b + 1 < P.boff.size(); ++b)
+        launch_apply_fwd_batch(a, P.d_bcl + P.boff[b], P.boff[b + 1] - P.boff[b], st);
+    } else {
+      launch_apply_fwd_level(level_args(f, l), st);
+    }
     launch_apply_post_level(level_args(f, l), st);
   }
   mark();
@@ -193,6 +200,13 @@ void record_apply(hs_factor_s* f, cudaStream_t st, std::vector<cudaEvent_t>* ev 
   for (int l = an->L_top - 1; l >= 0; --l) {
     mark();
     // the level's backward partial sums start empty (polled by the finishing chunks)
+    const ApplyLevelPlan& P = ap.lv[l];
+    if (P.bsync) {
+      const ApplyLevelArgs a = level_args(f, l);
+      for (size_t b = P.boff.size() - 1; b-- > 0;)
+        launch_apply_bwd_batch(a, P.d_bcl + P.boff[b], P.boff[b + 1] - P.boff[b], st);
+      continue;
+    }
     if (ap.lv[l].parts) HS_CUDA(cudaMemsetAsync(ap.d_parts, 0xFF, sizeof(double) * ap.lv[l].parts, st));
     launch_apply_bwd_level(level_args(f, l), st);
   }

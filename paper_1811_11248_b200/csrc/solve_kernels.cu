@@ -444,6 +444,149 @@ __global__ void k_spmv(const int64_t* __restrict__ rowptr, const int32_t* __rest
   if (row < n && sub == 0) y[row] = acc;
 }
 
+// ---- batch-synchronous sweeps (levels of large batches) -----------------------------------
+// One launch per batch of the factor's schedule, a CTA per cluster of the batch, no waiting:
+// every value a cluster reads (its pre-contributions forward, its neighbours' x backward) was
+// written by an earlier launch.  The factor records stream from HBM with the loads of the
+// whole CTA in flight: T_s row by row (a warp per 4 rows, coalesced), C_s column-parallel
+// (a thread per contribution entry, the K rows unrolled by 8) forward and row-parallel (a warp
+// per 4 rows) backward.  Same sums in a fixed order (deterministic).
+constexpr int BSF_PRE = 4096;   // pre-contribution values staged per round (doubles)
+
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd_b(ApplyLevelArgs a, const int32_t* __restrict__ cl) {
+  __shared__ double ys[MAX_M], yf[MAX_M];
+  __shared__ double pv[BSF_PRE];
+  __shared__ int gpre[BS_MAXG + 1];
+  const int s = cl[blockIdx.x];
+  const ApplySrc S = a.src[s];
+  const int m = S.m, r = S.r, K = m - r;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (m == 0) return;
+  for (int i = tid; i < m; i += APPLY_THREADS) ys[i] = __ldcg(S.y + i);
+  // y_s minus its pre-contributions in elimination order (staged round by round)
+  const int npre = S.pre_end - S.pre_begin, per = max(1, BSF_PRE / m);
+  for (int e0 = 0; e0 < npre; e0 += per) {
+    const int ne = min(per, npre - e0);
+    __syncthreads();
+    for (int x = tid; x < ne * m; x += APPLY_THREADS) {
+      const int e = e0 + x / m, i = x % m;
+      pv[x] = __ldcg(a.contrib + a.pull[S.pre_begin + e].slot + i);
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += APPLY_THREADS) {
+      double v = ys[i];
+      for (int e = 0; e < ne; ++e) v -= pv[e * m + i];
+      ys[i] = v;
+    }
+  }
+  const int ng = S.tg_end - S.tg_begin;
+  if (tid == 0) {   // flattened (contribution, entry) index of the producing phase
+    int acc = 0;
+    for (int g = 0; g < ng; ++g) {
+      gpre[g] = acc;
+      acc += a.ctb[S.tg_begin + g].len;
+    }
+    gpre[ng] = acc;
+  }
+  __syncthreads();
+  // z = T_s y_s: a warp per 4 rows
+  for (int i0 = 4 * warp; i0 < m; i0 += 4 * (APPLY_THREADS / 32)) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = lane; j < m; j += 32) {
+      const double yj = ys[j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u < m) acc[u] += S.T[(int64_t)(i0 + u) * m + j] * yj;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = wsum(acc[u]);
+      const int i = i0 + u;
+      if (lane == 0 && i < m) {
+        if (i < r) S.yc[i] = v;
+        else {
+          yf[i - r] = v;
+          S.yf[i - r] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // contributions C_s[:, cols(q)]ᵀ y_f: a thread per entry
+  const int tot = gpre[ng];
+  for (int t = tid; t < tot; t += APPLY_THREADS) {
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (gpre[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const Contrib c = a.ctb[S.tg_begin + lo];
+    const int i = t - gpre[lo];
+    const double* Ci = S.C + c.col + i;
+    double acc = 0.0;
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+      double cv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cv[u] = Ci[(int64_t)(k + u) * S.ldC];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += cv[u] * yf[k + u];
+    }
+    for (; k < K; ++k) acc += Ci[(int64_t)k * S.ldC] * yf[k];
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.contrib + c.slot + i), "d"(canon(acc)) : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd_b(ApplyLevelArgs a, const int32_t* __restrict__ cl) {
+  __shared__ double u[MAX_M];
+  __shared__ double xn[BS_MAXCOLS];
+  const int s = cl[blockIdx.x];
+  const ApplySrc S = a.src[s];
+  const int m = S.m, r = S.r, K = m - r;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = APPLY_THREADS / 32;
+  if (m == 0) return;
+  for (int i = tid; i < r; i += APPLY_THREADS) u[i] = __ldcg(S.xc + i);
+  for (int k = tid; k < K; k += APPLY_THREADS) u[r + k] = __ldcg(S.yf + k);
+  int kn = 0;
+  for (int b = S.nb_begin; b < S.nb_end; ++b) kn = max(kn, a.bnb[b].col + a.bnb[b].len);
+  for (int b = S.nb_begin + warp; b < S.nb_end; b += nw) {   // x of the neighbours' columns
+    const BwdNb nb = a.bnb[b];
+    for (int i = lane; i < nb.len; i += 32) xn[nb.col + i] = __ldcg(nb.x + i);
+  }
+  __syncthreads();
+  // x_f = y_f - C_s x_n: a warp per 4 rows of C_s
+  for (int k0 = 4 * warp; k0 < K && kn > 0; k0 += 4 * nw) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = lane; c < kn; c += 32) {
+      const double xc = xn[c];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (k0 + v < K) acc[v] += S.C[(int64_t)(k0 + v) * S.ldC + c] * xc;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double w = wsum(acc[v]);
+      if (lane == 0 && k0 + v < K) u[r + k0 + v] -= w;
+    }
+  }
+  __syncthreads();
+  // x_s = T_sᵀ [x_c; x_f]: a thread per entry, T_s rows coalesced
+  for (int i = tid; i < m; i += APPLY_THREADS) {
+    double acc = 0.0;
+    int j = 0;
+    for (; j + 8 <= m; j += 8) {
+      double tv[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) tv[w] = S.T[(int64_t)(j + w) * m + i];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) acc += tv[w] * u[j + w];
+    }
+    for (; j < m; ++j) acc += S.T[(int64_t)j * m + i] * u[j];
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(S.x + i), "d"(canon(acc)) : "memory");
+  }
+}
+
 }  // namespace
 
 static int apply_grid(const void* fn, int ntask) {
@@ -474,6 +617,17 @@ void launch_apply_bwd_level(const ApplyLevelArgs& a, cudaStream_t st) {
   if (a.nbtask <= 0) return;
   k_apply_bwd<<<apply_grid((const void*)k_apply_bwd, a.nbtask), APPLY_THREADS,
                 sizeof(double) * BWD_STAGE, st>>>(a);
+  count_launch(1);
+}
+
+void launch_apply_fwd_batch(const ApplyLevelArgs& a, const int32_t* d_cl, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_apply_fwd_b<<<n, APPLY_THREADS, 0, st>>>(a, d_cl);
+  count_launch(1);
+}
+void launch_apply_bwd_batch(const ApplyLevelArgs& a, const int32_t* d_cl, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_apply_bwd_b<<<n, APPLY_THREADS, 0, st>>>(a, d_cl);
   count_launch(1);
 }
 
