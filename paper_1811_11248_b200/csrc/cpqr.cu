@@ -606,7 +606,6 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
     }
   if (it.dwb && act) {   // coarse-n rows into the store blocks (s, q), C rows into the slab
     const int jn = c0 + grp;
-    const int dn = it.kwd < 0 ? jn : dense_col(it, it.kw + jn) - it.kwd;   // C_s keeps the dense columns
 #pragma unroll
     for (int i = 0; i < MR; ++i) {
       const int l = t + i * G;
@@ -615,7 +614,7 @@ __device__ __forceinline__ void rotate_body(const CluItem& it, int c0, int nc, i
         double* d = dwb_addr(it.seg, it.nseg, it.kw + jn, l);
         if (d) *d = x[i];
       } else {
-        it.Cout[(size_t)(l - r) * it.ldC + dn] = x[i];
+        it.Cout[(size_t)(l - r) * it.ldC + jn] = x[i];
       }
     }
   }

@@ -82,7 +82,7 @@ struct CluItem {
   double* Tout;
   // support-restricted level 0 (support.cpp): B_s holds only the structurally
   // nonzero columns of its blocks (the segments' idx lists); kwd = the dense w-width (-1: B_s
-  // is dense).  Cout keeps the dense n-columns (ld ldC = the dense kn): the apply's record.
+  // is dense).  Cout = C_s on the same (compressed) n-columns, ld ldC = kn: the apply's record.
   int32_t ldC, kwd;
 };
 
@@ -173,7 +173,6 @@ struct SchurTile2 {
 };
 struct NbCol {               // neighbour q occupies columns [col, col+len) of the (compressed) n-part
   int32_t q, col, len, idx;  // idx: position of q in the full n(s) list (pair table index)
-  int32_t dcol, pad;         // q's first column in the dense n-part (the columns of C_s)
   const int32_t* sup;        // column col + c = local column sup[c] of q (null: c; support.cpp)
 };
 struct BlockDir {            // the level's block store: row p has blocks (p, q<=p) sorted by q
@@ -212,10 +211,14 @@ struct PullSrc {             // y[0:len] -= contrib[slot : slot+len], produced b
   int64_t slot;
   int32_t t, pad;
 };
-struct Contrib {             // contrib[slot : slot+len] = C_s[:, col:col+len]^T y_f,s (source s)
+struct Contrib {             // contrib[slot : slot+dlen] = C_s[:, cols(q)]^T y_f,s (source s)
   int64_t slot;
-  int32_t col, len;
+  int32_t col, len;          // q's columns [col, col+len) of C_s
   int32_t q, pre;            // target; pre: q is eliminated later (counts toward arr[q])
+  int32_t dlen, pad;         // entries of the contribution (q's live size)
+  // a support-restricted record (level 0): entry i is C_s column col + inv[i], or 0 when
+  // inv[i] < 0; null: entry i is column col + i (dlen == len)
+  const int32_t* inv;
 };
 struct FwdTgt {              // y_q[0:len] -= C_s[:, col:col+len]^T y_f,s
   double* y;                 // q's live segment (level or parent vector)
@@ -229,6 +232,7 @@ struct BwdNb {               // neighbour q: columns [col, col+len) of C_s read 
   const double* x;
   int32_t q, col, len, later;   // later: q eliminated after s at this level (wait for it)
   int32_t off, pad;             // position of q's columns inside its backward chunk
+  const int32_t* sup;           // support-restricted record: column col + i reads x[sup[i]] (null: x[i])
 };
 struct BwdTask {             // neighbours bnb[b0, b1) of s (nc columns in all) -> partial sums
   int32_t s, b0, b1, nc, chunk, pad;

@@ -703,7 +703,7 @@ hs_factor_s::~hs_factor_s() {
     for (double* p : l.cchunks) fr(p);
   }
   for (auto& p : ap.lv) {
-    fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb); fr(p.d_bcl);
+    fr(p.d_src); fr(p.d_ftask); fr(p.d_ftgt); fr(p.d_btask); fr(p.d_bnb); fr(p.d_pull); fr(p.d_post_cl); fr(p.d_ctb); fr(p.d_bcl); fr(p.d_cinv);
   }
   fr(ap.d_y); fr(ap.d_yf); fr(ap.d_xb); fr(ap.d_parts); fr(ap.d_ctr); fr(ap.d_contrib);
   if (ap.graph) cudaGraphExecDestroy(ap.graph);
@@ -940,6 +940,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     L.kn.assign(lev.nclus, 0);
     L.kw.assign(lev.nclus, 0);
     L.ldB.assign(lev.nclus, 0);
+    L.ldc.assign(lev.nclus, 0);
     L.voff.assign(lev.nclus + 1, 0);
     for (int c = 0; c < lev.nclus; ++c) L.voff[c + 1] = L.voff[c] + cap[c];
     L.vlen = L.voff[lev.nclus];
@@ -989,6 +990,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       build_l0_support(*an);
       d_sup = l0_support_device(*an, h->device);
     }
+    L.khat = khat_lv;
     std::vector<int32_t> fkn(lev.nclus, 0), fkw(lev.nclus, 0);   // B_s's n/w widths (flop counts)
     // store offsets of row s's blocks, [w(s) ..., n(s) ...] (computed once per cluster)
     std::vector<std::vector<int64_t>> roff(lev.nclus);
@@ -1063,7 +1065,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         for (size_t bi = 0; bi < pend_cl.size(); ++bi) {
           const int32_t s = pend_cl[bi].first, m = pend_cl[bi].second;
           if (!L.C[s]) continue;
-          const int32_t K = m - L.rank[s], kn = L.kn[s];
+          const int32_t K = m - L.rank[s], kn = L.ldc[s];
           if (K <= 0 || kn <= 0) {
             L.C[s] = nullptr;
             continue;
@@ -1196,6 +1198,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         L.kn[c] = kn;
         L.kw[c] = kw;
         L.ldB[c] = kn + kw;
+        L.ldc[c] = kn;
         live[c] = r;
         done[c] = 1;
         L.C[c] = (m > r && kn > 0) ? cbase + coff[c] : nullptr;
@@ -1228,7 +1231,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         int32_t kn = 0, kw = 0;
         for (int32_t q : lev.H[s]) kn += live[q];
         for (int32_t q : lev.w[s]) kw += live[q];
-        L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw;
+        L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw; L.ldc[s] = kn;
       }
       CluItem* d_clu_batch = nullptr;   // this batch's cluster items on the device (upA)
       std::vector<int32_t> Bo;   // the batch's clusters eliminated here
@@ -1282,6 +1285,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             if (ln > 0) x += ln;
           }
         L.ldB[s] = bkn[bi] + bkw[bi];
+        L.ldc[s] = bkn[bi];   // C_s on the supported n-columns
       }
       for (int bi = 0; bi < nb; ++bi) {
         fkn[Bo[bi]] = bkn[bi];
@@ -1304,7 +1308,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       std::vector<int64_t> co(nb, -1);
       if (dpatch)
         for (int bi = 0; bi < nb; ++bi) {
-          const int64_t m = live[Bo[bi]], kn = L.kn[Bo[bi]];
+          const int64_t m = live[Bo[bi]], kn = L.ldc[Bo[bi]];
           if (m > 0 && kn > 0) {
             co[bi] = csz;
             csz += (m * kn + 3) & ~int64_t(3);
@@ -1377,7 +1381,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           CluItem& it = clu[bi];
           it.G = L.G[s]; it.V = L.V[s]; it.tau = L.tau[s]; it.B = L.B[s]; it.piv = L.piv[s]; it.nu = L.nu[s];
           it.m = m; it.kw = kw; it.kn = kn; it.ldB = ldB; it.level = l; it.cluster = s;
-          it.ldC = L.kn[s];   // Cout keeps the dense n-columns (the apply's record)
+          it.ldC = L.ldc[s];   // C_s: the record on B_s's n-columns
           it.kwd = khat ? L.kw[s] : -1;
           it.Wt = go[bi] >= 0 ? wtmp + go[bi] : nullptr;
           if (m == 0) continue;
@@ -1426,7 +1430,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               it.ldss = ldss;
               it.dwb = 1;
               it.keepB = f->keep_records ? 1 : 0;
-              if (L.kn[s] > 0) {
+              if (L.ldc[s] > 0) {
                 L.C[s] = ctmp + co[bi];   // C_s = rows [r, m) of the rotated B_n (K <= m)
                 it.Cout = L.C[s];
               }
@@ -1489,11 +1493,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         d_clu_batch = upA.dptr<CluItem>(iC);
         const size_t nfz = fz.size(), nfci = fci.size(), ngather = gather.size(), ntrsm = trsm.size(),
                      nrot = rot.size();
-        double* const czero = khat ? ctmp : nullptr;   // compressed: C_s's unsupported columns are 0
-        const int64_t czn = csz;
         first_half_launch = [&, iG, iC, iT, iR, iF, iS, iI, fused, max_m, nb, nfz, nfci, ngather, ntrsm, nrot,
-                             clu, czero, czn](bool publish) {
-          if (czero) HS_CUDA(cudaMemsetAsync(czero, 0, sizeof(double) * czn, st));
+                             clu](bool publish) {
           pt.rec(pt.a[0], st);
           if (fused) {   // Cholesky per cluster ("potrf"), scaling per tile ("trsm")
             pt.rec(pt.a[1], st);
@@ -1574,11 +1575,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         const auto& ns = lev.H[s];
         std::vector<int32_t> noff(ns.size() + 1, 0);
         auto nwid = [&](size_t a) { return khat ? nlen[k][a] : live[ns[a]]; };
-        std::vector<int32_t> dnoff(ns.size() + 1, 0);   // ... and in the dense n-part (C_s's columns)
-        for (size_t a = 0; a < ns.size(); ++a) {
-          noff[a + 1] = noff[a] + nwid(a);
-          dnoff[a + 1] = dnoff[a] + live[ns[a]];
-        }
+        for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + nwid(a);
         if (kc > 0) {
           // wave = lowest wave in which no earlier source shares a neighbour with s
           uint64_t used = 0;
@@ -1588,11 +1585,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           while (w < 63 && ((used >> w) & 1ull)) ++w;
           if ((used >> w) & 1ull) w = 63 + (int)waves.size();   // overflow: a wave of its own
           const uint64_t bit = w < 64 ? (1ull << w) : 0ull;
-          SchurSrc sc{nullptr, dwb ? kn : ldB, 0, kc, (int32_t)nbc.size(), 0, 0};
+          SchurSrc sc{nullptr, dwb ? L.ldc[s] : ldB, 0, kc, (int32_t)nbc.size(), 0, 0};
           for (size_t a = 0; a < ns.size(); ++a)
             if (live[ns[a]] > 0) {
               if (nwid(a) > 0)
-                nbc.push_back(NbCol{ns[a], noff[a], nwid(a), (int32_t)a, dnoff[a], 0,
+                nbc.push_back(NbCol{ns[a], noff[a], nwid(a), (int32_t)a,
                                     khat && nsup[k][a] >= 0 ? d_sup + nsup[k][a] : nullptr});
               if (!wave_mask[ns[a]]) touched.push_back(ns[a]);
               wave_mask[ns[a]] |= bit;
@@ -1961,7 +1958,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           int32_t kn = 0, kw = 0;
           for (int32_t q : lev.H[s]) kn += lv2[q];
           for (int32_t q : lev.w[s]) kw += lv2[q];
-          L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw;
+          L.kn[s] = kn; L.kw[s] = kw; L.ldB[s] = kn + kw; L.ldc[s] = kn;
         }
         for (int32_t s : Bt) lv2[s] = L.rank[s];
       }
@@ -1976,8 +1973,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       // The apply plan of level l only reads this level's records: single GPU, it is built
       // on a host worker (chained after the previous level's) while the next level factors.
       auto plan_task = [l, &lev = lev, &L = L, &ap, capc = cap, capn, level_dofs, vb0 = ap.vbase[l], vbn0 = vbase,
-                        nP, &t_apply_plan]() {
+                        nP, &t_apply_plan, su = &an->l0s, dsup = d_sup]() {
         ApplyLevelPlan& AP = ap.lv[l];
+        AP.cinv.clear();
         AP.src.assign(lev.nclus, ApplySrc{});
         std::vector<int32_t> fev(lev.nclus, 0), lv2 = capc;
         std::vector<uint8_t> proc(lev.nclus, 0);
@@ -1994,11 +1992,29 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           bwd_batches.emplace_back();
           std::vector<BwdTask>& bwd_tasks = bwd_batches.back();
           for (int32_t s : Bt) {
-            const int32_t m = lv2[s], r = L.rank[s], K = m - r, kn = L.kn[s];
+            const int32_t m = lv2[s], r = L.rank[s], K = m - r, kn = L.ldc[s];
             if (m == 0) continue;
             const auto& ns = lev.H[s];
-            std::vector<int32_t> noff(ns.size() + 1, 0);
-            for (size_t a = 0; a < ns.size(); ++a) noff[a + 1] = noff[a] + lv2[ns[a]];
+            // q's columns of C_s: its live width, or (support-restricted level) the supported
+            // columns of a neighbour not yet eliminated (su.idx: host inverse maps / device gathers)
+            std::vector<int32_t> cw(ns.size()), noff(ns.size() + 1, 0);
+            std::vector<int64_t> sx(ns.size(), -1);
+            // (a cluster of a batch too large for the fused path keeps a dense record)
+            const bool kh = L.khat && kn != L.kn[s];
+            int64_t e = kh ? su->sptr[s] : 0, x = kh ? su->iptr[s] : 0;
+            if (kh)
+              for (size_t b = 0; b < lev.w[s].size(); ++b) {
+                const int32_t ln = su->len[e++];
+                if (ln > 0) x += ln;
+              }
+            for (size_t a = 0; a < ns.size(); ++a) {
+              const int32_t ln = kh ? su->len[e++] : -1;
+              cw[a] = ln >= 0 ? ln : lv2[ns[a]];
+              if (ln >= 0) sx[a] = x;
+              if (ln > 0) x += ln;
+              noff[a + 1] = noff[a] + cw[a];
+            }
+            if (noff[ns.size()] != kn) fail(HS_E_INTERNAL, "apply plan: record width");
             // the cluster's record, its forward target tasks (targets grouped up to FWD_COLS
             // columns) and its backward column chunks
             ApplySrc& as = AP.src[s];
@@ -2013,9 +2029,17 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               const int32_t q = ns[a];
               if (lv2[q] == 0 || K == 0) continue;
               (proc[q] ? post[q] : pre[q]).push_back(PullSrc{slots, s, 0});
-              AP.ctb.push_back(Contrib{slots, noff[a], lv2[q], q, proc[q] ? 0 : 1});
+              const int32_t* inv = nullptr;   // (offset + 1 into AP.cinv until the upload)
+              if (sx[a] >= 0) {
+                const size_t base = AP.cinv.size();
+                AP.cinv.resize(base + lv2[q], -1);
+                for (int32_t j = 0; j < cw[a]; ++j) AP.cinv[base + su->idx[sx[a] + j]] = j;
+                inv = (const int32_t*)(uintptr_t)(base + 1);
+              }
+              AP.ctb.push_back(Contrib{slots, noff[a], cw[a], q, proc[q] ? 0 : 1, lv2[q], 0, inv});
               slots += lv2[q];
-              AP.bnb.push_back(BwdNb{nullptr, q, noff[a], lv2[q], proc[q] ? 0 : 1, 0, 0});
+              AP.bnb.push_back(BwdNb{nullptr, q, noff[a], cw[a], proc[q] ? 0 : 1, 0, 0,
+                                     sx[a] >= 0 ? dsup + sx[a] : nullptr});
             }
             as.tg_end = (int32_t)AP.ctb.size();
             as.nb_end = (int32_t)AP.bnb.size();
@@ -2359,7 +2383,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   for (const auto& L : f->lv)
     for (int s = 0; s < L.nclus; ++s) {
       const double m = L.cap[s], r = L.rank[s];
-      fb += 8.0 * (m * m + (m - r) * L.kn[s]);
+      fb += 8.0 * (m * m + (m - r) * L.ldc[s]);
     }
   fb += 8.0 * (double)f->ntop * (f->ntop + 1) / 2;
   S.factor_bytes = fb;
@@ -2395,6 +2419,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     }
     for (auto& t : AP.ftgt) t.y = ap.d_y + (uintptr_t)t.y;
     for (auto& nbr : AP.bnb) nbr.x = ap.d_xb + (uintptr_t)nbr.x;
+    up(AP.cinv, AP.d_cinv);
+    for (auto& c : AP.ctb)
+      if (c.inv) c.inv = AP.d_cinv + ((uintptr_t)c.inv - 1);
     up(AP.src, AP.d_src);
     up(AP.ftask, AP.d_ftask);
     up(AP.ftgt, AP.d_ftgt);

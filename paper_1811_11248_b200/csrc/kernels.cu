@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
   const NbCol* nb = nbc + s.nb_off;
   __shared__ double ap[16][68];   // row stride == 4 (mod 16): conflict-free m8n8k4 fragments
   __shared__ double aq[16][68];
-  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64], r_dc[64], c_dc[64];
+  __shared__ int r_own[64], r_loc[64], c_own[64], c_loc[64];
   __shared__ int r_slot[64], c_slot[64];
   __shared__ int r_list[64], c_list[64];
   __shared__ int nr, nc;
@@ -482,13 +482,14 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
   __shared__ int nbcol[SCH_NBS];
   const int rows = min(64, s.kn - t.i0), cols = min(64, s.kn - t.j0);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  // (1) the neighbours' column starts into shared memory (the owner searches)
+  // (1) the neighbours' column starts into shared memory (the owner searches) + the first
+  // K-chunk of C (this thread's columns i0 + ii / j0 + ii, ii = tid & 63 in every chunk)
   const bool nst = s.nnb <= SCH_NBS;
   if (nst)
     for (int a = tid; a < s.nnb; a += blockDim.x) nbcol[a] = nb[a].col;
-  __syncthreads();
-  const double* Cp;
-  const double* Cq;
+  const int ii0 = tid & 63;
+  const double* Cp = s.C + t.i0 + (ii0 < rows ? ii0 : 0);
+  const double* Cq = s.C + t.j0 + (ii0 < cols ? ii0 : 0);
   auto load_chunk = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -499,6 +500,8 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
       aq[kk][ii] = (kin && ii < cols) ? Cq[(int64_t)(k0 + kk) * s.ldC] : 0.0;
     }
   };
+  load_chunk(0);
+  __syncthreads();
   if (w < 2) {   // (2) owners of the tile's rows (warp 0) / columns (warp 1) by binary search,
                  // distinct owners in order (rows/cols are sorted by owner): ballots
     const int lim = w == 0 ? rows : cols, base = w == 0 ? t.i0 : t.j0;
@@ -523,7 +526,6 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
     const int s0 = __popc(m0 & le) - 1, s1 = __popc(m0) + __popc(m1 & le) - 1;
     int* own = w == 0 ? r_own : c_own;
     int* loc = w == 0 ? r_loc : c_loc;
-    int* dc = w == 0 ? r_dc : c_dc;   // the column of C (dense n-part)
     int* slot = w == 0 ? r_slot : c_slot;
     int* list = w == 0 ? r_list : c_list;
     if (lane < lim) {
@@ -531,7 +533,6 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
       const NbCol g = nb[o0];
       const int c = base + lane - g.col;
       loc[lane] = g.sup ? g.sup[c] : c;
-      dc[lane] = g.dcol + loc[lane];
       slot[lane] = s0;
       if (f0) list[s0] = o0;
     }
@@ -540,19 +541,12 @@ __global__ void __launch_bounds__(256, 4) k_schur3(const SchurTile2* __restrict_
       const NbCol g = nb[o1];
       const int c = base + lane + 32 - g.col;
       loc[lane + 32] = g.sup ? g.sup[c] : c;
-      dc[lane + 32] = g.dcol + loc[lane + 32];
       slot[lane + 32] = s1;
       if (f1) list[s1] = o1;
     }
     if (lane == 0) (w == 0 ? nr : nc) = __popc(m0) + __popc(m1);
   }
   __syncthreads();
-  // this thread's C columns in every staged chunk (ii = tid & 63): the first K-chunk loads
-  // while the pair table below is filled
-  const int ii0 = tid & 63;
-  Cp = s.C + (ii0 < rows ? r_dc[ii0] : 0);
-  Cq = s.C + (ii0 < cols ? c_dc[ii0] : 0);
-  load_chunk(0);
   // (3) target block pointers of the distinct owner pairs
   const bool table = nr <= SCH_MAXO && nc <= SCH_MAXO;
   if (table) {

@@ -127,6 +127,8 @@ struct Upload {
 struct LevelRT {
   int32_t nclus = 0;
   std::vector<int32_t> cap, rank, kn, kw, ldB;
+  std::vector<int32_t> ldc;             // C_s's columns (= kn, or the supported ones on a support-restricted level)
+  bool khat = false;                    // level 0 restricted to the supports (support.cpp)
   std::vector<int64_t> voff;            // apply-vector offsets (prefix sums of cap)
   int64_t vlen = 0;
   double* arena = nullptr;              // T_s of every cluster (persistent: the apply operators)
@@ -161,6 +163,8 @@ struct ApplyLevelPlan {
   PullSrc* d_pull = nullptr;
   Contrib* d_ctb = nullptr;
   int32_t* d_post_cl = nullptr;
+  std::vector<int32_t> cinv;            // support-restricted records: Contrib::inv maps
+  int32_t* d_cinv = nullptr;
   // batch-synchronous sweeps (levels of large batches): the clusters of batch b are
   // bcl[boff[b], boff[b+1])
   bool bsync = false;

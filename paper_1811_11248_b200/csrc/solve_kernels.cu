@@ -83,13 +83,15 @@ __device__ __forceinline__ void produce(const ApplyLevelArgs& a, const ApplySrc&
   for (int g = g0 + warp; g < g1; g += nw) {
     const Contrib c = a.ctb[g];
     const bool st = g - g0 < nst;
-    for (int i = lane; i < c.len; i += 32) {
+    for (int i = lane; i < c.dlen; i += 32) {
       double acc = 0.0;
-      if (st) {
-        const double* Ci = sC + soff[g - g0] + i;
+      const int cc = c.inv ? c.inv[i] : i;   // the entry's column among q's columns of C_s (< 0: zero)
+      if (cc < 0) {
+      } else if (st) {
+        const double* Ci = sC + soff[g - g0] + cc;
         for (int k = 0; k < K; ++k) acc += Ci[k * c.len] * zf[k];
       } else {
-        const double* Ci = S.C + c.col + i;
+        const double* Ci = S.C + c.col + cc;
         int k = 0;
         for (; k + 8 <= K; k += 8) {   // 8 loads in flight, accumulated in k order
           double cv[8];
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd(ApplyLevelArgs a) {
       AP_TR(tt, 1);
       for (int b = warp; b < nnb; b += nw) {   // gather x_n (final once not empty)
         const BwdNb nb = a.bnb[tk.b0 + b];
-        for (int i = lane; i < nb.len; i += 32) xn[nb.off + i] = ld_poll(nb.x + i);
+        for (int i = lane; i < nb.len; i += 32) xn[nb.off + i] = ld_poll(nb.x + (nb.sup ? nb.sup[i] : i));
       }
       __syncthreads();
       double* part = a.parts + S.part + (int64_t)tk.chunk * K;
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd_b(ApplyLevelArgs a,
     int acc = 0;
     for (int g = 0; g < ng; ++g) {
       gpre[g] = acc;
-      acc += a.ctb[S.tg_begin + g].len;
+      acc += a.ctb[S.tg_begin + g].dlen;
     }
     gpre[ng] = acc;
   }
@@ -523,9 +525,10 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fwd_b(ApplyLevelArgs a,
     }
     const Contrib c = a.ctb[S.tg_begin + lo];
     const int i = t - gpre[lo];
-    const double* Ci = S.C + c.col + i;
+    const int cc = c.inv ? c.inv[i] : i;   // (< 0: an unsupported entry, zero)
+    const double* Ci = S.C + c.col + max(cc, 0);
     double acc = 0.0;
-    int k = 0;
+    int k = cc < 0 ? K : 0;
     for (; k + 8 <= K; k += 8) {
       double cv[8];
 #pragma unroll
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_bwd_b(ApplyLevelArgs a,
   for (int b = S.nb_begin; b < S.nb_end; ++b) kn = max(kn, a.bnb[b].col + a.bnb[b].len);
   for (int b = S.nb_begin + warp; b < S.nb_end; b += nw) {   // x of the neighbours' columns
     const BwdNb nb = a.bnb[b];
-    for (int i = lane; i < nb.len; i += 32) xn[nb.col + i] = __ldcg(nb.x + i);
+    for (int i = lane; i < nb.len; i += 32) xn[nb.col + i] = __ldcg(nb.x + (nb.sup ? nb.sup[i] : i));
   }
   __syncthreads();
   // x_f = y_f - C_s x_n: a warp per 4 rows of C_s

@@ -266,7 +266,9 @@ def test_pipeline_modes_agree(H, handle, monkeypatch):
     read one batch late vs the synchronous host patch, and the direct write-back (CPQR /
     n-rotation write row s and C_s themselves) vs the write-back pass — bit for bit, since
     they only move the same values; the gather + POTRF + TRSM kernels vs the gather-free
-    Cholesky + column-tile scaling to rounding."""
+    Cholesky + column-tile scaling to rounding.  (All with dense level-0 blocks: the modes
+    without the direct write-back keep them dense; test_support_restricted_level0_* compares
+    the support-restricted level 0 with it.)"""
     p = gen_laplace3d(24, leaf_size=27)
     a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=27)
     v = np.random.default_rng(11).standard_normal(p.n)
@@ -274,6 +276,7 @@ def test_pipeline_modes_agree(H, handle, monkeypatch):
     def run(**env):
         for k in ("HS_HOST_PATCH", "HS_NO_DIRECT_WB", "HS_NO_FUSED_POTRF_TRSM"):
             monkeypatch.delenv(k, raising=False)
+        monkeypatch.setenv("HS_NO_KHAT", "1")
         for k, val in env.items():
             monkeypatch.setenv(k, val)
         f = H.hs_factor_create(handle, a, p.vals, eps=1e-2)
@@ -376,7 +379,8 @@ def test_support_restricted_level0_is_the_dense_computation(H, handle, monkeypat
     """Level 0 runs on the structurally nonzero columns of each block only (support.cpp,
     SURVEY O2.10): a zero column stays zero through the scaling, the CPQR (never a pivot) and
     the rotation, and the Schur products only reach supported columns -- so the factor is the
-    dense one (HS_NO_KHAT=1): identical kept ranks, canonical pivots, top block and apply."""
+    dense one (HS_NO_KHAT=1): identical kept ranks, canonical pivots and top block, the same
+    preconditioner to rounding."""
     from problems.generators import gen_config_scaled
     name, k = cfg.split("/")
     p = gen_config_scaled(name, int(k))
@@ -402,7 +406,9 @@ def test_support_restricted_level0_is_the_dense_computation(H, handle, monkeypat
     assert all(np.array_equal(u, w) for u, w in zip(r0, r1))
     assert all(np.array_equal(u, w) for u, w in zip(p0, p1))
     assert np.array_equal(t0, t1)
-    assert np.array_equal(x0, x1)
+    # the records hold the supported columns only: the apply sums fewer (zero) terms per
+    # lane, so it agrees to rounding
+    assert np.linalg.norm(x1 - x0) <= 1e-13 * np.linalg.norm(x1)
     assert fl0 < fl1   # the level-0 work shrinks with the supports
 
 
