@@ -317,6 +317,9 @@ void launch_identity(double* const* d_ptr, const int32_t* d_ld, const int32_t* d
 void launch_scatter(const double* vals, const int64_t* map, int64_t nnz, double* blk, cudaStream_t st);
 void launch_potrf(const CluItem* d_items, int n, int max_m, DevStatus* status, cudaStream_t st);
 void launch_trsm(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
+// a2 on the FP64 tensor cores for the non-fused DC path (trsm_mma.cu): strips of trsm_mma_tile_cols()
+void launch_trsm_mma(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, cudaStream_t st);
+int trsm_mma_tile_cols();
 // thread-block-cluster CPQR; picks the cluster size from the batch shape, returns it
 // a3+a4 v3 (cpqr.cu): thread-block cluster per graph cluster, column groups of G lanes,
 // one DSMEM exchange per step, n-columns rotated after the pivoting loop; returns CS

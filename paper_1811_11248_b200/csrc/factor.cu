@@ -1346,7 +1346,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                 else ++c[4];
               }
             }
-          const int32_t rw = rot_tile_cols(m, max_m), tw = m <= SMEM_M ? 64 : 32;
+          const int32_t rw = rot_tile_cols(m, max_m), tw = nodc ? (m <= SMEM_M ? 64 : 32) : trsm_mma_tile_cols();
           if (fused) {
             c[1] = (ldB + 63) / 64;
             c[2] = (m + rw - 1) / rw;
@@ -1417,7 +1417,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               col += wq;
               dcol += live[q];
             }
-          const int32_t tw = m <= SMEM_M ? 64 : 32;   // trsm_core's tile width for this m
+          const int32_t tw = nodc ? (m <= SMEM_M ? 64 : 32) : trsm_mma_tile_cols();   // the scaling kernel's strip width
           if (fused) {
             // segments are in column order: each tile takes the run of segments overlapping it
             int32_t sb = seg0;
@@ -1507,7 +1507,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             pt.rec(pt.a[1], st);
             if (!nodc) launch_potrf(upA.dptr<CluItem>(iC), nb, max_m, d_status, st);
             pt.rec(pt.a[2], st);
-            if (!nodc) launch_trsm(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, max_m, st);
+            if (!nodc) launch_trsm_mma(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, max_m, st);
             else launch_nmax(upA.dptr<CluItem>(iC), upA.dptr<TrsmItem>(iT), (int)ntrsm, st);   // R-floor
           }
           pt.rec(pt.a[3], st);

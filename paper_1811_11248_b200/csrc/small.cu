@@ -22,6 +22,7 @@
 // order (sequential per-thread dot products).
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.h"
 
@@ -29,7 +30,6 @@ namespace hs {
 
 namespace {
 
-constexpr int ST = 256;   // threads per CTA
 
 __device__ __forceinline__ int64_t sdir_find(const BlockDir& d, int p, int q) {   // p >= q; -1 if absent
   int64_t lo = d.ptr[p], hi = d.ptr[p + 1];
@@ -41,6 +41,7 @@ __device__ __forceinline__ int64_t sdir_find(const BlockDir& d, int p, int q) { 
   return (lo < d.ptr[p + 1] && d.q[lo] == q) ? d.off[lo] : -1;
 }
 
+template <int ST>
 __device__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
@@ -50,6 +51,7 @@ __device__ double block_max(double v, double* red) {
   for (int k = 1; k < ST / 32; ++k) r = fmax(r, red[k]);
   return r;
 }
+template <int ST>
 __device__ int block_min_i(int v, int* red) {
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
@@ -60,6 +62,7 @@ __device__ int block_min_i(int v, int* red) {
   return r;
 }
 
+template <int ST>
 __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
   extern __shared__ double sm[];
   const int s = a.items[first + blockIdx.x];
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
     for (int i = 0; i < m; ++i) s2 += B[i * kb + c] * B[i * kb + c];
     rn = fmax(rn, sqrt(s2));
   }
-  const double Rn = block_max(rn, red);
+  const double Rn = block_max<ST>(rn, red);
   // ---- CPQR of B_w to eps (Q1-Q5): exact norms, strict keep rule, lowest-index tie window -
   for (int c = tid; c < kw; c += ST) nu[c] = 0.0;
   if (tid == 0) rr = min(m, kw);
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
       nu[c] = sqrt(s2);
       lmax = fmax(lmax, nu[c]);
     }
-    const double numax = block_max(lmax, red);
+    const double numax = block_max<ST>(lmax, red);
     if (j == 0) {
       tau_s = a.relative ? a.eps * numax : a.eps;
       if (a.relative && a.eps > 0.0) tau_s = fmax(tau_s, 1e-12 * fmax(numax, Rn));
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(ST) k_elim_small(SmallArgs a, int first) {
         lo = c;
         break;
       }
-    const int p = block_min_i(lo, redi);
+    const int p = block_min_i<ST>(lo, redi);
     // dlarfg of column p, rows j..m-1 (one warp)
     if (tid < 32) {
       double xs = 0.0;
@@ -414,8 +417,23 @@ size_t small_smem_bytes(int m_max, int k_max, int nseg_max, int npair_max) {
 void launch_elim_small(const SmallArgs& a, int first, int n, cudaStream_t st) {
   if (n <= 0) return;
   const size_t smem = small_smem_bytes(a.m_max, a.k_max, a.nseg_max, a.npair_max);
-  set_smem_attr((const void*)k_elim_small, smem);
-  k_elim_small<<<n, ST, smem, st>>>(a, first);
+  // threads per CTA (HS_SMALL_THREADS: 64 / 128 / 256): the column loops use at most
+  // k_w threads, so fewer threads mostly shorten the CTA barriers of the step chains
+  static const int nt = [] {
+    const char* e = std::getenv("HS_SMALL_THREADS");
+    const int v = e ? std::atoi(e) : 128;
+    return (v == 64 || v == 256) ? v : 128;
+  }();
+  if (nt == 64) {
+    set_smem_attr((const void*)k_elim_small<64>, smem);
+    k_elim_small<64><<<n, 64, smem, st>>>(a, first);
+  } else if (nt == 256) {
+    set_smem_attr((const void*)k_elim_small<256>, smem);
+    k_elim_small<256><<<n, 256, smem, st>>>(a, first);
+  } else {
+    set_smem_attr((const void*)k_elim_small<128>, smem);
+    k_elim_small<128><<<n, 128, smem, st>>>(a, first);
+  }
   count_launch(1);
 }
 
