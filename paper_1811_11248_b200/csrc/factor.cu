@@ -44,10 +44,24 @@ void* DevCache::alloc(size_t bytes) {
       trim();
       e = cudaMalloc(&p, c);
     }
+    if (e == cudaErrorMemoryAllocation && vmm && vmm->rec) {   // then spill completed factor records
+      cudaGetLastError();
+      while (e == cudaErrorMemoryAllocation && vmm->rec->spill(c + ((size_t)1 << 30))) {
+        cudaGetLastError();
+        vmm->trim();
+        e = cudaMalloc(&p, c);
+      }
+    }
     if (e != cudaSuccess) {
       cudaGetLastError();
+      size_t fb = 0, tb = 0;
+      cudaMemGetInfo(&fb, &tb);
+      cudaGetLastError();
       fail(e == cudaErrorMemoryAllocation ? HS_E_OOM : HS_E_CUDA,
-           std::string("device allocation of ") + std::to_string(c) + " bytes: " + cudaGetErrorString(e));
+           std::string("device allocation of ") + std::to_string(c) + " bytes: " + cudaGetErrorString(e) +
+               " (cache in use " + std::to_string(in_use >> 20) + " MB, VMM chunks " +
+               std::to_string(vmm ? (vmm->created * vmm->chunk) >> 20 : 0) + " MB, device free " +
+               std::to_string(fb >> 20) + " MB)");
     }
   }
   live[p] = c;
@@ -145,6 +159,14 @@ unsigned long long VmmPool::take() {
     dc->trim();
     r = drv().create(&h, chunk, &prop, 0);
   }
+  if (r == CUDA_ERROR_OUT_OF_MEMORY && rec && rec->spill(chunk)) {   // a spilled record chunk's memory
+    if (!idle.empty()) {
+      const unsigned long long hh = idle.back();
+      idle.pop_back();
+      return hh;
+    }
+    r = drv().create(&h, chunk, &prop, 0);
+  }
   cu_check(r, "cuMemCreate (block store chunk)");
   ++created;
   return (unsigned long long)h;
@@ -153,6 +175,127 @@ void VmmPool::trim() {
   for (unsigned long long h : idle) drv().release((CUmemGenericAllocationHandle)h);
   created -= idle.size();
   idle.clear();
+}
+char* VmmPool::take_host() {
+  if (!host_idle.empty()) {
+    char* p = host_idle.back();
+    host_idle.pop_back();
+    return p;
+  }
+  char* p = nullptr;
+  HS_CUDA(cudaHostAlloc((void**)&p, chunk, cudaHostAllocDefault));
+  return p;
+}
+VmmPool::~VmmPool() {
+  trim();
+  for (char* p : host_idle) cudaFreeHost(p);
+  host_idle.clear();
+}
+
+// ---- factor records in a spillable virtual range (runtime.h) --------------------------------
+void RecSpace::init(VmmPool* p, size_t reserve_bytes, cudaStream_t stream) {
+  release();
+  pool = p;
+  st = stream;
+  const size_t cb = pool->chunk;
+  vbytes = (reserve_bytes + cb - 1) / cb * cb;
+  base = vmm_reserve(vbytes);
+  handle.assign(vbytes / cb, 0ull);
+  host.assign(vbytes / cb, nullptr);
+  top = frontier = pin_lo = pin_hi = 0;
+  n_spilled = bytes_spilled = bytes_restored = 0;
+  t_spill = t_restore = 0.0;
+}
+void* RecSpace::alloc(size_t bytes) {
+  const size_t cb = pool->chunk;
+  const size_t off = (top + 255) & ~size_t(255), end = off + std::max<size_t>(bytes, 8);
+  if (end > vbytes) fail(HS_E_OOM, "factor records exceed the device memory (record space of " + std::to_string(vbytes) + " bytes)");
+  for (size_t i = off / cb; i < (end + cb - 1) / cb; ++i) {
+    if (handle[i]) continue;
+    const unsigned long long hd = pool->take();   // may spill chunks below the frontier (not this one)
+    vmm_map(base + i * cb, hd, cb, pool->device);
+    handle[i] = hd;
+  }
+  top = end;
+  return (void*)(uintptr_t)(base + off);
+}
+void RecSpace::level_start() {
+  const size_t cb = pool->chunk;
+  top = (top + cb - 1) / cb * cb;
+  frontier = top;
+}
+size_t RecSpace::spill(size_t bytes) {
+  const size_t cb = pool->chunk;
+  std::vector<size_t> pick;
+  size_t got = 0;
+  for (size_t i = 0; i < handle.size() && (i + 1) * cb <= frontier && got < bytes; ++i)
+    if (handle[i] && !((i + 1) * cb > pin_lo && i * cb < pin_hi)) {
+      pick.push_back(i);
+      got += cb;
+    }
+  if (pick.empty()) return 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  HS_CUDA(cudaDeviceSynchronize());   // every writer of a completed record has finished
+  for (size_t i : pick) {
+    host[i] = pool->take_host();
+    HS_CUDA(cudaMemcpyAsync(host[i], (const void*)(uintptr_t)(base + i * cb), cb, cudaMemcpyDeviceToHost, st));
+  }
+  HS_CUDA(cudaStreamSynchronize(st));
+  for (size_t i : pick) {
+    vmm_unmap(base + i * cb, cb);
+    pool->give(handle[i]);
+    handle[i] = 0;
+  }
+  n_spilled += pick.size();
+  bytes_spilled += got;
+  t_spill += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return got;
+}
+void RecSpace::restore() {
+  if (!active()) return;
+  const size_t cb = pool->chunk;
+  const auto t0 = std::chrono::steady_clock::now();
+  bool any = false;
+  for (size_t i = 0; i < host.size(); ++i)
+    if (host[i]) {
+      const unsigned long long hd = pool->take();
+      vmm_map(base + i * cb, hd, cb, pool->device);
+      handle[i] = hd;
+      HS_CUDA(cudaMemcpyAsync((void*)(uintptr_t)(base + i * cb), host[i], cb, cudaMemcpyHostToDevice, st));
+      bytes_restored += cb;
+      any = true;
+    }
+  if (!any) return;
+  HS_CUDA(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < host.size(); ++i)
+    if (host[i]) {
+      pool->give_host(host[i]);
+      host[i] = nullptr;
+    }
+  t_restore += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+void RecSpace::release() {
+  if (!base) return;
+  cudaDeviceSynchronize();   // the apply / a failed factor's kernels may still read the records
+  const size_t cb = pool->chunk;
+  try {
+    for (size_t i = 0; i < handle.size(); ++i) {
+      if (handle[i]) {
+        vmm_unmap(base + i * cb, cb);
+        pool->give(handle[i]);
+        handle[i] = 0;
+      }
+      if (host[i]) {
+        pool->give_host(host[i]);
+        host[i] = nullptr;
+      }
+    }
+    vmm_free_range(base, vbytes);
+  } catch (...) {
+  }
+  if (pool && pool->rec == this) pool->rec = nullptr;
+  base = 0;
+  vbytes = top = frontier = pin_lo = pin_hi = 0;
 }
 unsigned long long vmm_reserve(size_t bytes) {
   CUdeviceptr p = 0;
@@ -617,6 +760,7 @@ struct DeferredFree {
 // Bump allocator for the persistent C_s records of a factor: slabs from the cache.
 struct Slab {
   DevCache* dc = nullptr;
+  RecSpace* rec = nullptr;   // active: slabs from the factor's record space
   std::vector<double*>* owned = nullptr;
   double* cur = nullptr;
   int64_t left = 0;
@@ -624,8 +768,12 @@ struct Slab {
     words = (words + 3) & ~int64_t(3);
     if (words > left) {
       const int64_t sz = std::max<int64_t>(words, (int64_t)8 << 20);   // >= 64 MB
-      cur = (double*)dc->alloc(sizeof(double) * sz);
-      owned->push_back(cur);
+      if (rec && rec->active()) {   // exact: a record is complete once its writer is queued
+        return (double*)rec->alloc(sizeof(double) * words);
+      } else {
+        cur = (double*)dc->alloc(sizeof(double) * sz);
+        owned->push_back(cur);
+      }
       left = sz;
     }
     double* p = cur;
@@ -717,9 +865,20 @@ namespace hs {
 // the permutation, the map of every CSR entry into the level-0 block store and the
 // transpose map used by the on-device symmetry check.
 static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, const DistPlan& dp) {
-  if (an->dev == device && an->d_map && an->map_world == dp.world && an->map_rank == dp.rank) return;
+  if (an->dev == device && an->d_rowptr && an->map_world == dp.world && an->map_rank == dp.rank) {
+    if (an->d_map) return;
+    if (!an->h_map.empty()) {   // dropped by the previous (record-space) factor: upload again
+      const int64_t nnz = an->rowptr[an->n];
+      HS_CUDA(cudaMalloc(&an->d_map, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+      HS_CUDA(cudaMalloc(&an->d_tmap, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+      HS_CUDA(cudaMemcpyAsync(an->d_map, an->h_map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+      HS_CUDA(cudaMemcpyAsync(an->d_tmap, an->h_tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+  }
   if (an->dev >= 0 && an->dev != device) fail(HS_E_INVALID_ARG, "factor: analysis already bound to another device");
-  if (an->d_map) {   // cached for another (world, rank): rebuild
+  if (an->d_rowptr) {   // cached for another (world, rank): rebuild
     HS_CUDA(cudaStreamSynchronize(st));
     for (void* p : {(void*)an->d_rowptr, (void*)an->d_colind, (void*)an->d_perm, (void*)an->d_map, (void*)an->d_tmap})
       if (p) cudaFree(p);
@@ -766,6 +925,10 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, con
   HS_CUDA(cudaMemcpyAsync(an->d_map, map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
   HS_CUDA(cudaMemcpyAsync(an->d_tmap, tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
   HS_CUDA(cudaStreamSynchronize(st));
+  if (!dist && nnz * 16 >= ((int64_t)2 << 30)) {
+    an->h_map = std::move(map);
+    an->h_tmap = std::move(tmap);
+  }
   an->dev = device;
   an->map_world = dp.world;
   an->map_rank = dp.rank;
@@ -925,6 +1088,24 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   });
   std::vector<double> lev_flops(an->L_top + 1, 0.0);
   BatchVecs rc;   // the batch vectors, reused batch after batch
+  // Large factors (the level-0 store is VMM-backed, C4-sized) keep their records in a record
+  // space whose completed chunks spill to pinned host memory when a later level's store does
+  // not fit beside them (RecSpace, runtime.h).  HS_RECSPACE=0/1 forces it off/on; "force"
+  // also spills every completed level at its end (tests the spill/restore path on small cases).
+  const char* rs_env = std::getenv("HS_RECSPACE");
+  const bool rec_force = rs_env && std::strcmp(rs_env, "force") == 0;
+  if (!dist && !nodc && an->L_top > 0 && (rs_env ? std::strcmp(rs_env, "0") != 0 : bs.pool != nullptr)) {
+    size_t fr_b = 0, tot_b = 0;
+    HS_CUDA(cudaMemGetInfo(&fr_b, &tot_b));
+    f->rec.init(&h->vmm, tot_b, st);
+    h->vmm.rec = &f->rec;
+    if (!an->h_map.empty()) {   // the level-0 scatter and the symmetry check are done with them
+      HS_CUDA(cudaStreamSynchronize(st));
+      cudaFree(an->d_map);
+      cudaFree(an->d_tmap);
+      an->d_map = an->d_tmap = nullptr;
+    }
+  }
   tl.push_back({"level-0 store + setup", now_s()});
   for (int l = 0; l < an->L_top; ++l) {
     HS_CUDA(cudaEventRecord(lev_ev[l], st));
@@ -963,15 +1144,32 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     }
     L.arena_bytes = (size_t)off * sizeof(double);
     const double ta0 = now_s();
-    L.arena = (double*)dc.alloc(std::max<size_t>(L.arena_bytes, 8));
+    if (f->rec.active()) {   // written batch after batch: not spillable before the level ends
+      f->rec.level_start();
+      L.arena = (double*)f->rec.alloc(L.arena_bytes);
+      f->rec.pin_lo = (uintptr_t)L.arena - f->rec.base;
+      f->rec.level_start();
+      f->rec.pin_hi = f->rec.top;
+    } else {
+      L.arena = (double*)dc.alloc(std::max<size_t>(L.arena_bytes, 8));
+    }
     L.iarena = (int32_t*)dc.alloc(std::max<size_t>(sizeof(int32_t) * ioff, 4));
     t_tr[2] += now_s() - ta0;
+    if (prof) {
+      size_t fb = 0, tb = 0;
+      HS_CUDA(cudaMemGetInfo(&fb, &tb));
+      std::fprintf(stderr, "[hs profile] level %d start: store %.1f GB, T_s arena %.1f GB, cache in use %.1f GB, "
+                   "VMM chunks %.1f GB, records %.1f GB (%.1f GB spilled), device free %.1f GB\n", l,
+                   bs.total * 8.0 / 1e9, L.arena_bytes / 1e9, dc.in_use / 1e9, h->vmm.created * (double)h->vmm.chunk / 1e9,
+                   f->rec.top / 1e9, f->rec.bytes_spilled / 1e9, fb / 1e9);
+    }
     L.G.assign(lev.nclus, nullptr); L.V.assign(lev.nclus, nullptr); L.tau.assign(lev.nclus, nullptr);
     L.B.assign(lev.nclus, nullptr); L.nu.assign(lev.nclus, nullptr); L.C.assign(lev.nclus, nullptr);
     L.piv.assign(lev.nclus, nullptr); L.T.assign(lev.nclus, nullptr);
     Slab cslab;
     cslab.dc = &dc;
     cslab.owned = &L.cchunks;
+    cslab.rec = &f->rec;
     for (int s = 0; s < lev.nclus; ++s)
       if (oX[s] >= 0) {
         L.piv[s] = L.iarena + oP[s];
@@ -1085,6 +1283,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         launch_copy2d(upC.dptr<CopyItem>(iC), (int)cc.size(), st);
         dc.free(pend_ctmp);   // stream-ordered reuse: later users are queued after the copy
         pend_ctmp = nullptr;
+        if (f->rec.active()) f->rec.frontier = f->rec.top;   // these C_s are complete (spillable)
       }
     };
 
@@ -1214,8 +1413,52 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
     }
     if (!small) lp.build(lev, bs, dc, upA, st);   // n(s)-pair target tables of the Schur tiles
-    for (size_t bidx = 0; bidx < (small ? 0 : lev.batches.size()); ++bidx) {
-      const auto& Bt = lev.batches[bidx];
+    // Batches whose workspace (G, G^-1, V, B_s, the C_s region; bounded with the level-start
+    // sizes) exceeds the budget run as consecutive sub-batches: a batch is an independent set,
+    // so its clusters' eliminations commute and each Schur target still receives its updates
+    // in source order (C4 on one GPU: a level-2 batch would need ~30 GB of workspace next to
+    // a ~130 GB block store).  HS_BATCH_WS_GB sets the budget (default 12 GB).
+    struct SubBatch { size_t bidx; size_t b0, b1; };
+    std::vector<SubBatch> subs;
+    {
+      static const double ws_cap = [] {
+        const char* e = std::getenv("HS_BATCH_WS_GB");
+        return (e ? std::atof(e) : 12.0) * 1e9;
+      }();
+      double ws_budget = ws_cap;
+      if (f->rec.active()) {   // a quarter of what the store, the arena and the resident data leave
+        size_t fb = 0, tb = 0;
+        HS_CUDA(cudaMemGetInfo(&fb, &tb));
+        const double resident = 12.0 * nnz + 24.0 * n + (an->d_map ? 16.0 * nnz : 0.0);
+        const double left = (double)tb - 8.0 * bs.total - (double)L.arena_bytes - (double)dc.in_use - resident;
+        ws_budget = std::min(ws_cap, std::max(1e9, 0.25 * left));
+      }
+      for (size_t bidx = 0; bidx < (small ? 0 : lev.batches.size()); ++bidx) {
+        const auto& Bt = lev.batches[bidx];
+        size_t b0 = 0;
+        double acc = 0.0;
+        for (size_t i = 0; i < Bt.size(); ++i) {
+          const int32_t c = Bt[i];
+          const double m = cap[c];
+          double kk = 0.0;
+          for (int32_t q : lev.H[c]) kk += cap[q];
+          for (int32_t q : lev.w[c]) kk += cap[q];
+          const double w = 8.0 * (3 * m * m + 2 * m + kk + 2 * m * kk);
+          if (!dist && i > b0 && acc + w > ws_budget) {
+            subs.push_back({bidx, b0, i});
+            b0 = i;
+            acc = 0.0;
+          }
+          acc += w;
+        }
+        subs.push_back({bidx, b0, Bt.size()});
+      }
+    }
+    std::vector<int32_t> sub_cl;
+    for (size_t ib = 0; ib < subs.size(); ++ib) {
+      const size_t bidx = subs[ib].bidx;
+      sub_cl.assign(lev.batches[bidx].begin() + subs[ib].b0, lev.batches[bidx].begin() + subs[ib].b1);
+      const auto& Bt = sub_cl;
       if (level_dofs == 0) break;   // every cluster is empty: nothing to eliminate on this level
       const bool phase2 = (int)bidx >= lev.nphase1;
       if (dist && phase2 && (int)bidx == lev.nphase1) {   // the phase-I ranks of every owner
@@ -1945,6 +2188,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
     }
     finish_pending();
+    if (f->rec.active()) {   // the level's records are complete (spillable)
+      f->rec.pin_lo = f->rec.pin_hi = 0;
+      f->rec.level_start();
+      if (rec_force) f->rec.spill(~size_t(0));
+    }
     // ---- every rank learns every kept rank; the records go to rank 0 (dist) -----------------
     const double tp2 = now_s();
     if (dist) {
@@ -2343,6 +2591,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (double* b : tbufs)
       if (b) dc.free(b);
     bs.release();
+  }
+  if (f->rec.active()) {   // the spilled records come back to the device (same addresses)
+    f->rec.restore();
+    h->vmm.rec = nullptr;
+    if (prof || f->rec.n_spilled)
+      std::fprintf(stderr, "[hs profile] record space: %.2f GB of records, %.2f GB spilled to the host in %.2f s, "
+                   "%.2f GB restored in %.2f s\n", f->rec.top / 1e9, f->rec.bytes_spilled / 1e9, f->rec.t_spill,
+                   f->rec.bytes_restored / 1e9, f->rec.t_restore);
   }
   HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // join the side stream (apply operators)
   HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));

@@ -64,6 +64,10 @@ struct Analysis {
   int64_t* d_perm = nullptr;
   int64_t* d_map = nullptr;     // CSR entry -> offset in the level-0 block store (-1: upper)
   int64_t* d_tmap = nullptr;    // CSR entry (i,j) -> index of (j,i) (value symmetry check)
+  // large patterns: host copies of the two maps, so that a factor that needs the device memory
+  // (record space active) can drop d_map / d_tmap after its level-0 scatter and the next
+  // factor uploads them again instead of recomputing them
+  std::vector<int64_t> h_map, h_tmap;
   L0Support l0s;                // built by the first factor that restricts level 0 to the supports
   int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
 };

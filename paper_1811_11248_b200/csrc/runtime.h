@@ -31,11 +31,44 @@ struct VmmPool {
   std::vector<unsigned long long> idle;  // CUmemGenericAllocationHandle
   size_t created = 0;                    // chunks alive (mapped or idle)
   struct DevCache* dc = nullptr;         // trimmed before retrying an allocation that failed
+  struct RecSpace* rec = nullptr;        // the running factor's records: spilled to the host on OOM
+  std::vector<char*> host_idle;          // pinned host chunks (spilled records), kept for the next factor
   void init(int dev);
   unsigned long long take();
   void give(unsigned long long h) { idle.push_back(h); }
+  char* take_host();
+  void give_host(char* p) { host_idle.push_back(p); }
   void trim();                           // release the idle chunks
-  ~VmmPool() { trim(); }
+  ~VmmPool();
+};
+
+// Persistent factor records (the T_s arenas and the C_s slabs of every level) of a large
+// factor, in one virtual range backed by VmmPool chunks.  The records of completed levels
+// are read only by the apply, after the factorization; when a block store or workspace does
+// not fit beside them (C4 on one GPU: ~100 GB of records next to a ~100 GB level store), the
+// oldest completed chunks are copied to pinned host memory and their physical memory goes to
+// the pool.  After the last store is released every spilled chunk is mapped again at the
+// SAME virtual address and copied back, so every record pointer (apply plan, exports) stays
+// valid and the apply reads device memory only.
+struct RecSpace {
+  VmmPool* pool = nullptr;
+  unsigned long long base = 0;
+  size_t vbytes = 0, top = 0;
+  size_t frontier = 0;                    // records below this byte offset are complete
+  size_t pin_lo = 0, pin_hi = 0;          // except this range (the running level's T_s arena)
+  std::vector<unsigned long long> handle; // physical chunk mapped at chunk i (0: none)
+  std::vector<char*> host;                // pinned copy of a spilled chunk
+  cudaStream_t st = nullptr;
+  size_t n_spilled = 0, bytes_spilled = 0, bytes_restored = 0;
+  double t_spill = 0.0, t_restore = 0.0;
+  void init(VmmPool* p, size_t reserve_bytes, cudaStream_t stream);
+  void* alloc(size_t bytes);
+  void level_start();                     // a level begins: everything allocated so far is complete
+  size_t spill(size_t bytes);             // >= bytes of completed records to the host (syncs the device)
+  void restore();                         // map and copy back every spilled chunk (stream-ordered)
+  void release();
+  bool active() const { return base != 0; }
+  ~RecSpace() { release(); }
 };
 unsigned long long vmm_reserve(size_t bytes);                          // virtual range
 void vmm_free_range(unsigned long long base, size_t bytes);
@@ -314,6 +347,7 @@ struct hs_factor_s {
   hs::ApplyPlan ap;
   std::unique_ptr<hs::DistSolve> ds;     // world > 1: the distributed solve (records stay at their owners)
   bool keep_records = false;             // HS_KEEP_RECORDS: per-cluster G, V, tau, B stay exportable
+  hs::RecSpace rec;                      // large factors: T_s / C_s records, spillable during the factorization
   hs_factor_stats_t stats{};
   // PCG work vectors
   double *d_r = nullptr, *d_z = nullptr, *d_p = nullptr, *d_q = nullptr, *d_x = nullptr, *d_b = nullptr;

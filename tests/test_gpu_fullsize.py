@@ -151,3 +151,31 @@ def test_refactor_is_bitwise_deterministic(H, handle, name):
         del f
     assert all(np.array_equal(x, y) for x, y in zip(out[0][0], out[1][0]))
     assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("name", ["C4/16", "C2"])
+def test_record_space_spill_restore_bitwise(H, handle, monkeypatch, name):
+    """Large factors keep their T_s / C_s records in a virtual range whose completed chunks
+    spill to pinned host memory while a later level's block store needs the device memory,
+    and come back at the same addresses before the apply (RecSpace; C4 on one B200).  Forced
+    here on every level end: the kept ranks and the preconditioner application are bitwise
+    those of the factor whose records never left the device."""
+    base, _, k = name.partition("/")
+    p = gen_config_scaled(base, int(k)) if k else gen_config(base)
+    a = H.hs_analyze(handle, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
+                     leaf_columns=p.leaf_columns)
+    L = H.hs_analysis_get_info(a)["L_top"]
+    v = np.random.default_rng(7).standard_normal(p.n)
+    out = {}
+    for mode in ("0", "1", "force"):
+        monkeypatch.setenv("HS_RECSPACE", mode)
+        f = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
+        x, rep = H.hs_pcg(f, v, tol=p.tol)
+        out[mode] = ([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)], H.hs_apply(f, v), x,
+                     rep["iters"])
+        del f
+    for mode in ("1", "force"):
+        assert all(np.array_equal(x, y) for x, y in zip(out["0"][0], out[mode][0])), mode
+        assert np.array_equal(out["0"][1], out[mode][1]), mode
+        assert np.array_equal(out["0"][2], out[mode][2]), mode
+        assert out["0"][3] == out[mode][3]
