@@ -1,18 +1,19 @@
 """Benchmark of the deferred-compression LoRaSp hot path on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
 
 A step = one pass of the whole hot path on one synthetic system: hs_factor (Algorithm 1:
 POTRF, deferred-compression TRSM, CPQR to eps, Schur updates, top Cholesky) followed by
 hs_pcg (CSR SpMV + the Algorithm-2 apply) to the config's tolerance.
 
-Default workload: BASELINE.json configs[2] (C3: 256 x 256 x 10 thin anisotropic slab, 655,360
-DOF), the largest BASELINE config that fits one B200.  C4 (10.5M DOF, "1 GPU and 8 GPUs") does
-not: measured on its half-size family member C4/2 (2.6M DOF, same operator, leaf, eps, tol) the
-factor alone holds 30.5 GB and the level stores 34 GB at ranks r/m = 0.74 / 0.83 / 0.59 (levels
-0-2), which extrapolates to ~120 GB of factor plus ~100 GB of level store for C4 -- more than
-the 180 GB of one GPU (profiles/r02_c4_memory.txt).  --config C2 / C4/2 / ... run
-the other configs (a "/k" suffix = the config's operator on a 1/k horizontal grid).
+Default workload: BASELINE.json configs[3] (C4: Q1 first-order-Stokes-type operator, 512 x 512
+x 20 hexahedra, 2 DOF/node, 10,485,760 DOF, eps 1e-2, PCG to 1e-8; "1 GPU and 8 GPUs"), the
+largest BASELINE config and the one north_star's FP64 target is defined on.  It fits one B200
+because the factor records of completed levels spill to pinned host memory while a later
+level's block store needs the HBM (level 2: a 131 GB store) and are mapped back at the same
+addresses before the apply (RecSpace).  Default K = 2 steps for C4 (a step is
+~40 s), 5 otherwise.  --config C3 / C2 / C4/2 / ... run the other configs (a "/k" suffix = the
+config's operator on a 1/k horizontal grid).
 
 Inputs (CSR values, b) are resident in HBM when the timed region starts and the analysis
 (pattern only) is done once before it.  value = DOF/s = N * K / (device time of the K steps);
@@ -45,10 +46,10 @@ METRIC = "factor+PCG DOF/s at 1/2/4/8 B200; FP64 TFLOP/s frac of peak; PCG iters
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None, help="default: 2 for C4, 5 otherwise")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--cpu-budget", type=float, default=8.0,
                     help="seconds of oracle work per host core for the CPU baseline")
     ap.add_argument("--eps", type=float, default=None)
@@ -58,7 +59,10 @@ def parse():
                     help="N>1: N independent single-GPU factorizations instead of the subdomain-distributed one")
     ap.add_argument("--watchdog", type=float, default=900.0,
                     help="N>1: abort (exit 3) if the run has not finished after this many seconds")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 2 if args.config == "C4" else 5
+    return args
 
 
 def dist_env():
@@ -125,10 +129,16 @@ def _problem(name):
 
 def _sample_name(config):
     """The bounded CPU sample of a workload: its family member on a 1/4 horizontal grid (1/16
-    of the DOFs for the 2-D-extruded configs; 1/64 for C2) -- same generator, leaf, eps, tol."""
+    of the DOFs for the 2-D-extruded configs; 1/64 for C2) -- same generator, leaf, eps, tol.
+    The C4/C5 operators keep high ranks (r/m ~ 0.6-0.8): their oracle samples are the 1/32
+    (C4: 10,240 DOF, ~13 s per oracle factor + PCG on one core) and 1/64 grids."""
     base = config.split("/")[0]
     k = int(config.split("/")[1]) if "/" in config else 1
-    return f"{base}/{4 * k}" if base in ("C2", "C3", "C4", "C5") else base
+    if base == "C4":
+        return f"C4/{max(32, k)}"
+    if base == "C5":
+        return f"C5/{max(64, k)}"
+    return f"{base}/{4 * k}" if base in ("C2", "C3") else base
 
 
 def _oracle_worker(args):
@@ -361,11 +371,7 @@ def run_ours(args, rank, world, local):
     if not args.no_e2e:
         hb = np.ascontiguousarray(p.b)
         hx = np.empty_like(hb)
-        f = H.hs_factor_create(h, a, hv, eps=p.eps)
-        if solver:
-            H.hs_pcg(f, hb, tol=p.tol, x=hx)
-        del f
-        e2e_ms = 0.0
+        e2e_ms = 0.0   # (the warm-up steps ran the same kernels; the host-buffer path adds copies)
         for _ in range(args.steps):
             flush.zero_()
             barrier()
@@ -387,9 +393,14 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(p.vals.nbytes + p.b.nbytes), "d2h_bytes_per_step": int(hx.nbytes)}
     # profiled steps: the same factor, every phase bracketed with CUDA events on the
     # library stream (HS_PHASE_EVENTS=all); the roofline's achieved rate is measured here
+    # (one profiled factor for the large configs: a C4 factor is ~40 s); the last one also
+    # gives the exports the apply roofline and the k-hat flop count need (a second factor
+    # cannot coexist with it at C4's size)
     os.environ["HS_PHASE_EVENTS"] = "all"
     pstats, prof_ms = [], 0.0
-    for _ in range(args.steps):
+    n_prof = 1 if p.n > 4_000_000 else args.steps
+    vec, fl0_hat, fl0_dense = 0, None, None
+    for i in range(n_prof):
         flush.zero_()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -400,6 +411,11 @@ def run_ours(args, rank, world, local):
         e1.synchronize()
         prof_ms += e0.elapsed_time(e1)
         pstats.append(H.hs_factor_get_stats(fp))
+        if i == n_prof - 1 and rank == 0:
+            for lv in range(pstats[-1]["n_levels"]):
+                vec += int(H.hs_factor_export(fp, H.HS_FEXP_LIVE0, lv).sum() + H.hs_factor_export(fp, H.HS_FEXP_KN, lv).sum())
+            if p.n <= 4_000_000:   # (a host-side Python pass over every CSR entry: minutes at C4)
+                fl0_hat, fl0_dense = khat_level0_flops(H, a, fp, p)
         del fp
     os.environ.pop("HS_PHASE_EVENTS")
     if rank != 0:
@@ -450,21 +466,12 @@ def run_ours(args, rank, world, local):
     # and backward sweeps + the top factor twice + vector gathers/scatters (8 bytes each way of
     # every live and neighbour entry per sweep); SpMV = 8 nnz + 4 nnz + 8 (N+1) + 8 N (x) + 8 N (y)
     hbm = mp.get("hbm_gbs")
-    f_last = H.hs_factor_create(h, a, vals, eps=p.eps)
-    nlev = H.hs_factor_get_stats(f_last)["n_levels"]
-    vec = 0
-    for lv in range(nlev):
-        vec += int(H.hs_factor_export(f_last, H.HS_FEXP_LIVE0, lv).sum() + H.hs_factor_export(f_last, H.HS_FEXP_KN, lv).sum())
-    del f_last
     apply_bytes = 2.0 * S["factor_bytes"] + 2 * 2 * 8.0 * vec
-    f_k = H.hs_factor_create(h, a, vals, eps=p.eps)
-    fl0_hat, fl0_dense = khat_level0_flops(H, a, f_k, p)
-    del f_k
     # the library counts every level with the column widths its kernels compute: at a
     # support-restricted level 0 those are B_s's supported columns (>= k-hat), dense above
     lib_l0 = float(np.mean([s["flops_level"][0] for s in stats]))
-    flops_khat = factor_flops - lib_l0 + fl0_hat
-    flops_dense = factor_flops - lib_l0 + fl0_dense
+    flops_khat = factor_flops - lib_l0 + fl0_hat if fl0_hat is not None else None
+    flops_dense = factor_flops - lib_l0 + fl0_dense if fl0_dense is not None else None
     n_apply = sum(r["iters"] for r in reps)   # z = M^{-1} r once before the loop, then every non-final iteration
     n_spmv = sum(r["iters"] for r in reps)
     t_spmv = sum(r["t_spmv_s"] for r in reps)
@@ -501,14 +508,15 @@ def run_ours(args, rank, world, local):
                    "t_apply_s_per_step": t_apply / args.steps,
                    "factor_tflops": factor_flops / t_fac / 1e12,
                    "factor_gflop": factor_flops / 1e9, "factor_gb": S["factor_bytes"] / 1e9,
-                   "factor_gflop_khat": flops_khat / 1e9, "factor_tflops_khat": flops_khat / t_fac / 1e12,
-                   "factor_gflop_dense": flops_dense / 1e9,
+                   "factor_gflop_khat": flops_khat / 1e9 if flops_khat else None,
+                   "factor_tflops_khat": flops_khat / t_fac / 1e12 if flops_khat else None,
+                   "factor_gflop_dense": flops_dense / 1e9 if flops_dense else None,
                    "flops_note": "factor_gflop counts the columns the kernels compute; *_khat counts level 0 with "
                                  "the support-restricted k̂_n, k̂_w of SURVEY §8(d), *_dense with the dense live "
                                  "widths (levels >= 1 are dense in all three)",
-                   "phase_s_per_step": {nm: float(t_ph[i] / args.steps) for i, nm in enumerate(names)},
-                   "phase_events": f"phases and roofline from {args.steps} profiled factor steps (every phase "
-                                   f"bracketed with CUDA events, {prof_ms / args.steps:.1f} ms/factor); the timed "
+                   "phase_s_per_step": {nm: float(t_ph[i] / n_prof) for i, nm in enumerate(names)},
+                   "phase_events": f"phases and roofline from {n_prof} profiled factor step(s) (every phase "
+                                   f"bracketed with CUDA events, {prof_ms / n_prof:.1f} ms/factor); the timed "
                                    f"steps run without per-batch events",
                    "host_planning_s_per_step": float(np.mean([s["t_phase_s"][7] for s in stats])),
                    "batches": S["n_batches"], "levels": S["n_levels"], "n_top": S["n_top"],

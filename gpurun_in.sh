@@ -1,3 +1,2 @@
-HS_PROFILE=1 timeout 1500 python bench.py --config C4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/s6_bench_c4.json 2> gpurun_out/s6_bench_c4.err; grep "hs profile\|Error" gpurun_out/s6_bench_c4.err | cut -c1-600
-tail -c 2500 gpurun_out/s6_bench_c4.json
-free -g | head -2
+( time python bench.py ) > gpurun_out/s7_bench_c4.json 2> gpurun_out/s7_bench_c4.err; tail -c 3000 gpurun_out/s7_bench_c4.json; tail -5 gpurun_out/s7_bench_c4.err
+( time python bench.py --impl reference --steps 1 --warmup 0 ) > gpurun_out/s7_ref.json 2> gpurun_out/s7_ref.err; tail -c 1000 gpurun_out/s7_ref.json; tail -4 gpurun_out/s7_ref.err
