@@ -185,7 +185,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   // HS_CQ_TRACE debug aid: clock64 timeline of cluster 0 / CTA 0 / thread 0
 #define CQ_TR(k)                                                            \
   do {                                                                      \
-    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[k] = clock64(); \
+    if (trace && (long long)blockIdx.x == trace[254] && threadIdx.x == 0) trace[k] = clock64(); \
   } while (0)
   const bool trace_split = trace && trace[255] != 0;   // HS_CQ_TRACE_SPLIT: stamp 4 at the push
   CQ_TR(0);
@@ -205,13 +205,25 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   const uint32_t msgb = (uint32_t)(msgw * 8);
   // element (l, c) of the slice, column-major with column stride ldm: in shared memory (SM)
   // or in the cluster's global scratch (global mode: coalesced group loads through L2)
-  const int sr = 1, sc = ldm;
+  const int sr = 1;
   // dynamic shared memory (16-byte aligned regions, the bulk copies require it):
   // [W (SM mode): wchunk x ldm] [nu: wchunk] [mine: 2 x msgw] [slots: 2 x CS x msgw]
-  double* W = SM ? dsm : it.Wt + (size_t)w_lo * ldm;
+  // global mode (hybrid): [nu] [mine] [slots] [the first nsmc columns of the slice]; columns
+  // [nsmc, nw) live in the global scratch (same column-major layout), so only the part of
+  // the slice that exceeds the CTA's shared memory streams through L2 every step
   double* nu = SM ? dsm + (((size_t)wchunk * ldm + 1) & ~(size_t)1) : dsm;
   double* mine = nu + ((wchunk + 1) & ~1);
   double* slots = mine + 2 * msgw;
+  double* const Wsm = SM ? dsm : slots + (((size_t)2 * CS * msgw + 1) & ~(size_t)1);
+  double* const Wg = SM ? dsm : it.Wt + (size_t)w_lo * ldm;
+  int nsmc = nw;
+  if (!SM) {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const long long room = (long long)(dyn / 8) - (long long)(Wsm - dsm);
+    nsmc = (int)max(0LL, min((long long)nw, room / ldm));
+  }
+  auto Wc = [&](int c) -> double* { return (SM || c < nsmc ? Wsm : Wg) + (size_t)c * ldm; };
   const int kiters = (nw + NGRP - 1) / NGRP;
   const int nr = (m - t + G - 1) / G;   // rows l = t + i G < m of this lane: i < nr
 
@@ -240,7 +252,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int l = l0 + u * rpp;
-            if (l < m) W[(size_t)cc * ldm + l] = v[u];
+            if (l < m) Wc(cc)[l] = v[u];
           }
         }
   }
@@ -250,7 +262,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   double lm = -1.0;
   for (int k = 0; k < kiters; ++k) {
     const int c = grp + k * NGRP;
-    const double* colp = W + (size_t)(c < nw ? c : 0) * sc + (size_t)t * sr;
+    const double* colp = Wc(c < nw ? c : 0) + (size_t)t * sr;
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < MR; ++i)
@@ -306,7 +318,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       int li = lane < CQ_WARPS ? sh.wcand[lane] : INT_MAX;   // the lowest over all shares
       li = wmin_i(li);
       if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
-        const double* col = W + (size_t)li * sc;
+        const double* col = Wc(li);
         double xs = 0.0;
         for (int l = j + 1 + lane; l < m; l += 32) {
           const double b = col[(size_t)l * sr];
@@ -398,7 +410,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       const uint32_t par2 = (uint32_t)(use2++ & 1);
       if (tid == 0) bar_expect(sm_addr(&sh.bar2), vbytes);
       if (crank == ow && wid == 0) {
-        const double* col = W + (size_t)(p - ow * wchunk) * sc;
+        const double* col = Wc(p - ow * wchunk);
         double xs = 0.0;
         for (int l = j + 1 + lane; l < m; l += 32) {
           const double b = col[(size_t)l * sr];
@@ -463,7 +475,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
         const bool in = (k + u) < kiters && c < nw;
         const int cx = in ? c : 0;
         cxs[u] = cx;
-        cp[u] = W + (size_t)cx * sc + (size_t)t * sr;
+        cp[u] = Wc(cx) + (size_t)t * sr;
         piv[u] = in && crank == owner && c == ploc;
         act[u] = in && !piv[u] && nu[cx] >= 0.0;
         d[u] = 0.0;
@@ -510,11 +522,11 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   if (!it.dwb || it.keepB)   // (direct write-back: only the debug records need B)
     for (int e = tid; e < r * nw; e += CQ_THREADS) {
       const int l = e / nw, c = e % nw;
-      it.B[(size_t)l * ld + w_lo + c] = W[(size_t)c * ldm + l];
+      it.B[(size_t)l * ld + w_lo + c] = Wc(c)[l];
     }
   if (it.dwb) {   // ... and straight into the store blocks (s, q), q in w(s); I_r on (s, s)
     for (int c = tid; c < nw; c += CQ_THREADS) {
-      const double* src = W + (size_t)c * ldm;
+      const double* src = Wc(c);
       const size_t sst = 1;
       for (int l = 0; l < r; ++l) {
         double* d = dwb_addr(it.seg, it.nseg, w_lo + c, l);
@@ -529,7 +541,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   }
   cl.sync();   // no CTA leaves while another may still copy into its shared memory
   CQ_TR(251);
-  if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[252] = r;
+  if (trace && (long long)blockIdx.x == trace[254] && threadIdx.x == 0) trace[252] = r;
 #undef CQ_TR
   if (crank == 0 && tid == 0) *rank_slot = r;
 }
@@ -752,14 +764,44 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
     while (CS < 16 && n_act * CS * 4 <= nsm && max_kw / (2 * CS) >= 128) CS *= 2;
     // global mode is bound by each SM's L2 bandwidth (the slice streams through L2 every
     // step): spread its clusters over as many SMs as the batch leaves free
+    // global mode keeps as many columns of each slice in shared memory as fit (hybrid): the
+    // widest cluster and all the shared memory, the rest streams through L2 every step
+    if (!sm && std::getenv("HS_CPQR_GLOBAL") == nullptr) CS = 16;
     if (!sm)
       while (CS < 16 && n_act * CS * 2 <= nsm && max_kw / (2 * CS) >= 32) CS *= 2;
-    const size_t smem = need(CS);
+    size_t smem = sm ? need(CS) : std::max(need(CS), std::min(target, CQ_CAP_BYTES));
+    if (!sm && std::getenv("HS_CPQR_GLOBAL")) {   // forced (tests): about half of each slice in shared memory
+      size_t half = 0;
+      for (const auto& it : h_items)
+        if (it.m > 0 && it.kw > 0)
+          half = std::max(half, (size_t)cq_ldm(it.m, cq_group(it.m, MR)) * (((it.kw + CS - 1) / CS + 1) / 2));
+      smem = std::min(CQ_CAP_BYTES, need(CS) + 8 * half + 16);
+    }
     if (smem > CQ_CAP_BYTES) fail(HS_E_UNSUPPORTED, "cpqr: cluster block too large for the shared-memory messages");
+    static const bool cq_log = std::getenv("HS_CQ_LOG") != nullptr;
+    if (cq_log) {
+      int mm = 0;
+      double work = 0.0;
+      for (const auto& it : h_items)
+        if (it.m > 0 && it.kw > 0 && (it.Wt == nullptr) == sm) {
+          mm = std::max(mm, it.m);
+          work += (double)it.m * it.kw;
+        }
+      std::fprintf(stderr, "[cq log] launch %d %s: items %d active %d CS %d smem %zu max m %d max kw %d sum m*kw %.3g\n",
+                   launches.load(), sm ? "shared" : "global", n, n_act, CS, smem, mm, max_kw, work);
+    }
     long long* trace = nullptr;
     if (launches++ == trace_at) {
       HS_CUDA(cudaMalloc(&trace, 256 * sizeof(long long)));
       HS_CUDA(cudaMemsetAsync(trace, 0, 256 * sizeof(long long), st));
+      long long tb = 0;   // the first CTA of the first cluster of this launch's mode
+      for (int i = 0; i < n; ++i)
+        if (h_items[i].m > 0 && h_items[i].kw > 0 && (h_items[i].Wt == nullptr) == sm) {
+          tb = (long long)i * CS;
+          break;
+        }
+      HS_CUDA(cudaMemcpyAsync(trace + 254, &tb, sizeof tb, cudaMemcpyHostToDevice, st));
+      HS_CUDA(cudaStreamSynchronize(st));
       if (std::getenv("HS_CQ_TRACE_SPLIT")) {
         static const long long one = 1;
         HS_CUDA(cudaMemcpyAsync(trace + 255, &one, sizeof one, cudaMemcpyHostToDevice, st));
@@ -779,8 +821,8 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
       HS_CUDA(cudaStreamSynchronize(st));
       cudaFree(trace);
       const long long t0 = h[0];
-      std::fprintf(stderr, "[cq trace] launch %d (%s mode): n=%d CS=%d smem=%zu r=%lld | stage %lld norms %lld cyc\n",
-                   trace_at, sm ? "shared" : "global", n, CS, smem, h[252], h[1] - t0, h[2] - h[1]);
+      std::fprintf(stderr, "[cq trace] launch %d (%s mode): n=%d active=%d CS=%d smem=%zu max kw %d r=%lld | stage %lld norms %lld cyc\n",
+                   trace_at, sm ? "shared" : "global", n, n_act, CS, smem, max_kw, h[252], h[1] - t0, h[2] - h[1]);
       for (int j = 0; j < 60 && h[3 + 4 * j]; ++j)
         std::fprintf(stderr, "[cq trace]  step %2d: B1 %6lld  C1 %6lld  B3 %6lld  upd %6lld\n", j,
                      h[3 + 4 * j] - (j ? h[6 + 4 * (j - 1)] : h[2]), h[4 + 4 * j] - h[3 + 4 * j],

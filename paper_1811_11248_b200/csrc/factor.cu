@@ -1224,6 +1224,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     // once the host reads the ranks (the Schur waves that read it are queued before the copy)
     double* ctmp = nullptr;          // the planned batch's region
     double* pend_ctmp = nullptr;     // the pending batch's region
+    bool pend_in_arena = false;      // ... carved from the level's workspace arena
     auto finish_pending = [&]() {
       if (!pend_active) return;
       pend_active = false;
@@ -1281,7 +1282,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         upC.copy_in(iC, cc);
         upC.send(st);
         launch_copy2d(upC.dptr<CopyItem>(iC), (int)cc.size(), st);
-        dc.free(pend_ctmp);   // stream-ordered reuse: later users are queued after the copy
+        if (!pend_in_arena) dc.free(pend_ctmp);   // stream-ordered reuse: later users are queued after the copy
         pend_ctmp = nullptr;
         if (f->rec.active()) f->rec.frontier = f->rec.top;   // these C_s are complete (spillable)
       }
@@ -1454,6 +1455,30 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         subs.push_back({bidx, b0, Bt.size()});
       }
     }
+    // Record-space factors (C4-sized, device memory nearly full): one workspace arena per level,
+    // sized by the largest sub-batch's bound (level-start sizes), from which every batch carves
+    // its G / G^-1 / V / B_s, C_s region and CPQR scratch -- per-batch allocations of changing
+    // sizes would miss the cache and trim it (a device synchronisation) batch after batch
+    double* lvl_ws = nullptr;
+    int64_t lvl_ws_words = 0;
+    if (f->rec.active() && !dist && !subs.empty()) {
+      for (const auto& sb : subs) {
+        int64_t w = 0;
+        for (size_t i = sb.b0; i < sb.b1; ++i) {
+          const int32_t c = lev.batches[sb.bidx][i];
+          const int64_t m = cap[c];
+          int64_t kn = 0, kw = 0;
+          for (int32_t q : lev.H[c]) kn += cap[q];
+          for (int32_t q : lev.w[c]) kw += cap[q];
+          w += 3 * m * m + m + kw + m * (kn + kw) + 12 + m * kn + 4;
+          const int64_t g = (int64_t)std::max(cpqr_global_words((int)m, (int)kw, (int)m),
+                                              cpqr_global_words((int)m, (int)kw, MAX_M));
+          if (g) w += g + 4;
+        }
+        lvl_ws_words = std::max(lvl_ws_words, w + 16);
+      }
+      lvl_ws = (double*)dc.alloc(sizeof(double) * lvl_ws_words);
+    }
     std::vector<int32_t> sub_cl;
     for (size_t ib = 0; ib < subs.size(); ++ib) {
       const size_t bidx = subs[ib].bidx;
@@ -1545,7 +1570,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         wo[bi] = wsz;
         wsz += 3 * m * m + ((m + 3) & ~int64_t(3)) + ((kw + 3) & ~int64_t(3)) + ((m * (kn + kw) + 3) & ~int64_t(3));
       }
-      double* ws = nb ? (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4)) : nullptr;
       // the batch's C_s region (dpatch: m rows each, compacted once the ranks are known)
       int64_t csz = 0;
       std::vector<int64_t> co(nb, -1);
@@ -1557,7 +1581,6 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             csz += (m * kn + 3) & ~int64_t(3);
           }
         }
-      ctmp = csz ? (double*)dc.alloc(sizeof(double) * csz) : nullptr;
       // CPQR global-memory scratch of the clusters whose w-block exceeds a 16-CTA cluster's
       // shared memory (freed once the batch's kernels are queued: stream-ordered reuse)
       int64_t gsz = 0;
@@ -1569,7 +1592,18 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             gsz += (w + 3) & ~int64_t(3);
           }
         }
-      double* wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
+      double *ws = nullptr, *wtmp = nullptr;
+      const int64_t wsz4 = (std::max<int64_t>(wsz, 4) + 3) & ~int64_t(3), csz4 = (csz + 3) & ~int64_t(3);
+      const bool in_arena = nb && lvl_ws && wsz4 + csz4 + gsz <= lvl_ws_words;
+      if (in_arena) {   // carved from the level's workspace arena (stream-ordered reuse)
+        ws = lvl_ws;
+        ctmp = csz ? lvl_ws + wsz4 : nullptr;
+        wtmp = gsz ? lvl_ws + wsz4 + csz4 : nullptr;
+      } else {
+        ws = nb ? (double*)dc.alloc(sizeof(double) * std::max<int64_t>(wsz, 4)) : nullptr;
+        ctmp = csz ? (double*)dc.alloc(sizeof(double) * csz) : nullptr;
+        wtmp = gsz ? (double*)dc.alloc(sizeof(double) * gsz) : nullptr;
+      }
       // the batch's items: the counts per cluster (sequential, cheap), then every cluster fills
       // its own ranges of the item lists on PT pooled host threads (the same lists as a
       // sequential pass)
@@ -1597,6 +1631,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
           } else {
             c[4] += 1;
             c[5] = (ldB + tw - 1) / tw;
+            if (!nodc) {   // G_s^{-1} as identity strips of the TRSM, T_s by the rotation
+              c[5] += (m + tw - 1) / tw;
+              c[2] = (m + rw - 1) / rw;
+            }
           }
           if (kw > 0 || (dwb && kn > 0)) c[2] += (kn + rw - 1) / rw;
         }
@@ -1687,12 +1725,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
             }
           } else {
             for (int32_t c0 = 0; c0 < ldB; c0 += tw) trsm[itr++] = TrsmItem{bi, c0, std::min(tw, ldB - c0), 0};
+            if (!nodc)   // G_s^{-1} = the TRSM of the identity (k_trsm_mma strips, pad = 2)
+              for (int32_t c0 = 0; c0 < m; c0 += tw) trsm[itr++] = TrsmItem{bi, c0, std::min(tw, m - c0), 2};
           }
           if (kw > 0 || (dwb && kn > 0)) {   // the n-columns are rotated by k_rotate_n
             const int32_t rw = rot_tile_cols(m, max_m);
             for (int32_t c0 = 0; c0 < kn; c0 += rw) rot[irt++] = TrsmItem{bi, c0, std::min(rw, kn - c0), 0};
           }
-          if (fused) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
+          if (fused || !nodc) {   // ... and so is G^{-1}: the apply operator T_s = Qᵀ G_s^{-1} (no k_form_T)
             it.Ginv = ginv;
             it.Tout = L.T[s];
             const int32_t rw = rot_tile_cols(m, max_m);
@@ -1702,7 +1742,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
               itr != cnt[5][bi + 1])
             fail(HS_E_INTERNAL, "batch plan: item counts");
           pfl[2 * t] += (double)m * m * m / 3.0;
-          pfl[2 * t + 1] += (double)m * m * ldB;
+          pfl[2 * t + 1] += (double)m * m * ldB + (!fused && !nodc ? (double)m * m * m / 3.0 : 0.0);
         }
       });
       const double tfb = now_s();
@@ -1809,7 +1849,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         if (m == 0) continue;
         const int32_t kc = khat ? bkn[k] : kn;   // the n-columns the Schur tiles run over
         Pend pd{s, (int32_t)k, mine, -1, -1, -1, -1, wb.size(), wb.size()};
-        if (mine && !fused) {   // (fused: k_rotate_n forms T_s from k_chol's G^{-1})
+        if (mine && !fused && nodc) {   // (dc: k_rotate_n forms T_s from G^{-1} of k_chol / k_trsm_mma)
           pd.ft = (int64_t)ft.size();
           ft.push_back(FormTItem{L.G[s], nullptr, L.V[s], L.tau[s], L.T[s], m, 0});
           ft_max_m = std::max(ft_max_m, m);
@@ -2017,6 +2057,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         for (size_t k = 0; k < Bt.size(); ++k) pend_cl.emplace_back(Bt[k], live_at[k]);
         pend_active = nb > 0;
         pend_ctmp = ctmp;
+        pend_in_arena = in_arena;
         ctmp = nullptr;
       }
       for (auto& pd : pend) {
@@ -2159,8 +2200,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
       for (double* b : rbuf)
         if (b) dc.free(b);
-      if (wtmp) dc.free(wtmp);   // the batch's CPQR is queued
-      if (ws) {
+      if (wtmp && !in_arena) dc.free(wtmp);   // the batch's CPQR is queued
+      if (ws && !in_arena) {
         if (f->keep_records) L.wchunks.push_back(ws);
         else dc.free(ws);
       }
@@ -2188,6 +2229,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       }
     }
     finish_pending();
+    if (lvl_ws) dc.free(lvl_ws);   // stream-ordered: the level's kernels are queued
     if (f->rec.active()) {   // the level's records are complete (spillable)
       f->rec.pin_lo = f->rec.pin_hi = 0;
       f->rec.level_start();

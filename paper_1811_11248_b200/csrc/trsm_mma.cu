@@ -70,8 +70,13 @@ __global__ void __launch_bounds__(NWARP * 32) k_trsm_mma(const CluItem* __restri
   }
 
   // ---- the strip in registers: acc[j][cb] = rows 8 (j NWARP + w) + fr, cols 8 cb + 2 fc + {0,1}
+  // t.pad == 2: the strip is columns [c0, c0 + nc) of the identity and the result goes to
+  // G_s^{-1} (m x m row-major, it.Ginv) -- the input of T_s = Qᵀ G_s^{-1} (k_rotate_n);
+  // its rows above c0 stay zero, so the substitution starts at block c0 / 8
   double acc[NW][4][2];
   const int c0 = t.c0, nc = t.nc;
+  const bool ident = t.pad == 2;
+  const int bstart = ident ? (c0 >> 3) : 0;
 #pragma unroll
   for (int j = 0; j < NW; ++j) {
     const int row = 8 * (j * NWARP + w) + fr;
@@ -80,7 +85,9 @@ __global__ void __launch_bounds__(NWARP * 32) k_trsm_mma(const CluItem* __restri
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = 8 * cb + 2 * fc + h;
-        acc[j][cb][h] = (row < m && col < nc) ? it.B[(int64_t)row * it.ldB + c0 + col] : 0.0;
+        acc[j][cb][h] = (row < m && col < nc) ? (ident ? (row == c0 + col ? 1.0 : 0.0)
+                                                       : it.B[(int64_t)row * it.ldB + c0 + col])
+                                              : 0.0;
       }
   }
   // G_ib fragments of the coming step (negated: the DMMA accumulates X_i += (-G_ib) X_b)
@@ -97,13 +104,14 @@ __global__ void __launch_bounds__(NWARP * 32) k_trsm_mma(const CluItem* __restri
     }
   };
   __syncthreads();   // Yd
-  if (nb > 1) load_g(0);
+  if (bstart + 1 < nb) load_g(bstart);
 
 #pragma unroll
   for (int bb = 0; bb < NW; ++bb) {
     for (int wo = 0; wo < NWARP; ++wo) {
       const int b = bb * NWARP + wo;
       if (b >= nb) break;   // uniform across the CTA
+      if (b < bstart) continue;
       double* hb = buf + (b & 1) * 8 * TM_LDS;
       if (w == wo) {   // owner: X_b <- Y_b X_b, published in the hand-over tile
 #pragma unroll
@@ -171,12 +179,15 @@ __global__ void __launch_bounds__(NWARP * 32) k_trsm_mma(const CluItem* __restri
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = 8 * cb + 2 * fc + h;
-          if (col < nc) it.B[(int64_t)row * it.ldB + c0 + col] = acc[j][cb][h];
+          if (col < nc) {
+            if (ident) const_cast<double*>(it.Ginv)[(int64_t)row * m + c0 + col] = acc[j][cb][h];
+            else it.B[(int64_t)row * it.ldB + c0 + col] = acc[j][cb][h];
+          }
           cs[cb][h] = fma(acc[j][cb][h], acc[j][cb][h], cs[cb][h]);
         }
     }
   }
-  if (it.nmax && c0 + nc > it.kw) {
+  if (it.nmax && c0 + nc > it.kw && !ident) {
 #pragma unroll
     for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
