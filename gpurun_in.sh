@@ -1,2 +1,1 @@
-python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_c4.py -m gpu -x -q -s -k "record_space or global or c4" > gpurun_out/s12_tests.txt 2>&1; grep -v "^\[hs" gpurun_out/s12_tests.txt | tail -12
-HS_PROFILE=1 python bench.py --no-cpu-baseline > gpurun_out/s12_bench_c4.json 2> gpurun_out/s12_bench_c4.err; tail -c 1500 gpurun_out/s12_bench_c4.json; grep "first-half\|host blocked\|record space" gpurun_out/s12_bench_c4.err | tail -3
+HS_CQ_TRACE_FINE=1 HS_CQ_TRACE_SPLIT=1 HS_CQ_TRACE=23 timeout 600 python tools/one_factor_pcg.py C4/2 > gpurun_out/s14_a.log 2>&1; grep "cq " gpurun_out/s14_a.log | head -30

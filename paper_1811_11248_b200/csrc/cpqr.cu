@@ -179,7 +179,7 @@ __host__ __device__ __forceinline__ int cq_msg_words(int m) { return (8 + m + 1)
 //   (3) apply H_j to the local active columns and recompute their norms; the owner writes
 //       the pivot column as (beta, 0, ..., 0) and the reflector to V / tau / piv.
 // One mbarrier wait per step, no cluster-wide barrier inside the loop.
-template <int MR, int G, bool SM>
+template <int MR, int G, bool SM, int NT>
 __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int relative, int32_t* rank_slot,
                                           double* dsm, CqShared& sh, long long* trace) {
   // HS_CQ_TRACE debug aid: clock64 timeline of cluster 0 / CTA 0 / thread 0
@@ -188,6 +188,11 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     if (trace && (long long)blockIdx.x == trace[254] && threadIdx.x == 0) trace[k] = clock64(); \
   } while (0)
   const bool trace_split = trace && trace[255] != 0;   // HS_CQ_TRACE_SPLIT: stamp 4 at the push
+  const bool trace_fine = trace && trace[253] != 0;    // HS_CQ_TRACE_FINE: warp 0's dlarfg / push sub-steps
+#define CQ_TF(j, k)                                 \
+  do {                                              \
+    if (trace_fine && (j) < 12) CQ_TR(100 + 8 * (j) + (k)); \
+  } while (0)
   CQ_TR(0);
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -196,7 +201,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   const int m = it.m, kw = it.kw, ld = it.ldB;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int t = tid % G, grp = tid / G;
-  constexpr int NGRP = CQ_THREADS / G;
+  constexpr int NGRP = NT / G;
   const int wchunk = (kw + CS - 1) / CS;
   const int w_lo = crank * wchunk;
   const int nw = max(0, min(kw - w_lo, wchunk));
@@ -238,10 +243,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   // ---- stage the w-slice (transpose to column-major; coalesced global reads) ----------
   if (nw > 0) {   // thread (row rr + k rpp, column cc): coalesced row segments, no division per element
     const double* __restrict__ src = it.B + w_lo;
-    const int rpp = nw <= CQ_THREADS ? CQ_THREADS / nw : 1;   // rows per pass
-    const int cc0 = nw <= CQ_THREADS ? tid % nw : tid, rr = nw <= CQ_THREADS ? tid / nw : 0;
+    const int rpp = nw <= NT ? NT / nw : 1;   // rows per pass
+    const int cc0 = nw <= NT ? tid % nw : tid, rr = nw <= NT ? tid / nw : 0;
     if (rr < rpp)
-      for (int cc = cc0; cc < nw; cc += CQ_THREADS)
+      for (int cc = cc0; cc < nw; cc += NT)
         for (int l0 = rr; l0 < m; l0 += 4 * rpp) {
           double v[4];
 #pragma unroll
@@ -296,14 +301,14 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     if (lane == 0) sh.wred[wid] = lm;
     if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
     __syncthreads();
-    if (j < 60) CQ_TR(3 + 4 * j);
+    if (j < (trace_fine ? 24 : 60)) CQ_TR(3 + 4 * j);
     {   // every warp: the CTA max, and the lowest column of a strided share over the window
-      double Mc = lane < CQ_WARPS ? sh.wred[lane] : -1.0;
+      double Mc = lane < (NT / 32) ? sh.wred[lane] : -1.0;
       Mc = wmax(Mc);
       const double thr_c = CQ_WINDOW * Mc;
       int lw = INT_MAX;
       if (Mc >= 0.0)
-        for (int c = wid * 32 + lane; c < nw; c += CQ_THREADS)
+        for (int c = wid * 32 + lane; c < nw; c += NT)
           if (nu[c] >= thr_c) {
             lw = c;
             break;
@@ -313,9 +318,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     }
     __syncthreads();
     if (wid == 0) {
-      double Mc = lane < CQ_WARPS ? sh.wred[lane] : -1.0;
+      CQ_TF(j, 0);
+      double Mc = lane < (NT / 32) ? sh.wred[lane] : -1.0;
       Mc = wmax(Mc);
-      int li = lane < CQ_WARPS ? sh.wcand[lane] : INT_MAX;   // the lowest over all shares
+      int li = lane < (NT / 32) ? sh.wcand[lane] : INT_MAX;   // the lowest over all shares
       li = wmin_i(li);
       if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
         const double* col = Wc(li);
@@ -325,6 +331,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
           xs += b * b;
         }
         xs = wsum(xs);
+        CQ_TF(j, 1);
         const double alpha = col[(size_t)j * sr];
         const double xnorm = sqrt(xs);
         double tau, beta, rden;
@@ -338,8 +345,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
           tau = (beta - alpha) / beta;
           rden = 1.0 / (alpha - beta);   // dlarfg scales x by 1/(alpha - beta)
         }
+        CQ_TF(j, 2);
         for (int l = lane; l < m; l += 32)
           mymsg[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : col[(size_t)l * sr] * rden;
+        CQ_TF(j, 3);
         if (lane == 0) {
           mymsg[1] = nu[li];
           mymsg[2] = (double)(w_lo + li);
@@ -352,15 +361,17 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       }
       if (lane == 0) mymsg[0] = Mc;
       fence_proxy_async();
+      CQ_TF(j, 4);
       __syncwarp();
       if (lane < CS)
         bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
                   remote(sm_addr(&sh.bar1[buf]), lane));
-      if (trace_split && j < 60) CQ_TR(4 + 4 * j);   // local work done, message sent
+      CQ_TF(j, 5);
+      if (trace_split && j < (trace_fine ? 24 : 60)) CQ_TR(4 + 4 * j);   // local work done, message sent
     }
     // (2) decision from the CS messages (identical in every thread of every CTA)
     bar_wait(sm_addr(&sh.bar1[buf]), par);
-    if (!trace_split && j < 60) CQ_TR(4 + 4 * j);
+    if (!trace_split && j < (trace_fine ? 24 : 60)) CQ_TR(4 + 4 * j);
     // the CS local maxima: lane k of every warp reads CTA k's (CS <= 16), warp max and a
     // ballot for the lowest CTA over the window (the same values in every warp)
     const double sv = lane < CS ? slot[(size_t)lane * msgw] : -1.0;
@@ -455,7 +466,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
         nu[ploc] = -1.0;   // visible to the other warps after the next step's barrier
       }
     }
-    if (j < 60) CQ_TR(5 + 4 * j);
+    if (j < (trace_fine ? 24 : 60)) CQ_TR(5 + 4 * j);
     // (3) apply H_j to the active columns (two per group in flight), norms over rows > j.
     // v is zero above row j, so rows < j pass through unchanged: every row of the lane is
     // loaded, updated and stored without a row predicate; only the norm is masked (l > j).
@@ -514,18 +525,18 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
           lm = fmax(lm, v);
         }
     }
-    if (j < 60) CQ_TR(6 + 4 * j);
+    if (j < (trace_fine ? 24 : 60)) CQ_TR(6 + 4 * j);
   }
   CQ_TR(250);
   __syncthreads();
   // ---- coarse-w rows back to global memory (rows [0, r) of the slice) -----------------
   if (!it.dwb || it.keepB)   // (direct write-back: only the debug records need B)
-    for (int e = tid; e < r * nw; e += CQ_THREADS) {
+    for (int e = tid; e < r * nw; e += NT) {
       const int l = e / nw, c = e % nw;
       it.B[(size_t)l * ld + w_lo + c] = Wc(c)[l];
     }
   if (it.dwb) {   // ... and straight into the store blocks (s, q), q in w(s); I_r on (s, s)
-    for (int c = tid; c < nw; c += CQ_THREADS) {
+    for (int c = tid; c < nw; c += NT) {
       const double* src = Wc(c);
       const size_t sst = 1;
       for (int l = 0; l < r; ++l) {
@@ -534,7 +545,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       }
     }
     if (crank == 0)
-      for (int e = tid; e < r * r; e += CQ_THREADS) {
+      for (int e = tid; e < r * r; e += NT) {
         const int i = e / r, j = e % r;
         it.Dss[(size_t)i * it.ldss + j] = (i == j) ? 1.0 : 0.0;
       }
@@ -546,8 +557,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   if (crank == 0 && tid == 0) *rank_slot = r;
 }
 
-template <int MR, bool SM>
-__global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
+// NT threads per CTA, 512 / NT CTAs per SM (<= 128 registers a thread either way): smaller CTAs
+// let several clusters' latency-bound step chains share an SM when their slices fit
+template <int MR, bool SM, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
                                                           int32_t* __restrict__ rank_out, long long* trace) {
   pdl_trigger();
   pdl_wait();
@@ -563,12 +576,12 @@ __global__ void __launch_bounds__(CQ_THREADS, 1) k_cpqr3(const CluItem* __restri
   extern __shared__ double dsm[];
   __shared__ CqShared sh;
   switch (cq_group(it.m, MR)) {
-    case 1: cpqr_body<MR, 1, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 2: cpqr_body<MR, 2, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 4: cpqr_body<MR, 4, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 8: cpqr_body<MR, 8, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 16: cpqr_body<MR, 16, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    default: cpqr_body<MR, 32, SM>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 1: cpqr_body<MR, 1, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 2: cpqr_body<MR, 2, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 4: cpqr_body<MR, 4, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 8: cpqr_body<MR, 8, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 16: cpqr_body<MR, 16, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    default: cpqr_body<MR, 32, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
   }
 }
 
@@ -665,10 +678,10 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
   }
 }
 
-template <int MR, bool SM>
+template <int MR, bool SM, int NT>
 void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
                 cudaStream_t st, long long* trace) {
-  auto kern = k_cpqr3<MR, SM>;
+  auto kern = k_cpqr3<MR, SM, NT>;
   static std::once_flag once;
   std::call_once(once, [&] {
     HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -683,7 +696,7 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(n * CS);
-  cfg.blockDim = dim3(CQ_THREADS);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = at;
@@ -758,6 +771,28 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
     if (n_mode == 0) continue;
     int CS = 1;
     while (CS < 16 && need(CS) > std::min(target, CQ_CAP_BYTES)) CS *= 2;
+    // shared mode: smaller CTAs (NT = 256 / 128 threads, 2 / 4 CTAs per SM) when every slice
+    // still fits their share of the SM's shared memory at CS <= 16 and the batch fills the
+    // GPU: several clusters' step chains then interleave on an SM (HS_CQ_NT forces 128/256/512)
+    static const int nt_env = [] {
+      const char* e = std::getenv("HS_CQ_NT");
+      return e ? std::atoi(e) : 0;
+    }();
+    int NT = 512;
+    if (sm && nt_env != 512) {
+      for (int nt : {128, 256}) {
+        if (nt_env && nt != nt_env) continue;
+        const int B = 512 / nt;
+        const size_t lim = (228 * 1024) / B - sizeof(CqShared) - 1024;
+        int cs = 1;
+        while (cs < 16 && need(cs) > lim) cs *= 2;
+        if (need(cs) > lim) continue;
+        if (!nt_env && (size_t)n_act * std::max(cs, CS) < (size_t)nsm * B) continue;   // a partial wave: keep 512
+        NT = nt;
+        CS = std::max(CS, cs);
+        break;
+      }
+    }
     // a batch of few clusters leaves most SMs idle: split the columns over more CTAs (a
     // shorter update per step for a costlier exchange) while the clusters still fill at most
     // a quarter of the GPU and every CTA keeps >= 128 columns (C2 level 3: CPQR 38 -> 29 ms)
@@ -787,8 +822,8 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
           mm = std::max(mm, it.m);
           work += (double)it.m * it.kw;
         }
-      std::fprintf(stderr, "[cq log] launch %d %s: items %d active %d CS %d smem %zu max m %d max kw %d sum m*kw %.3g\n",
-                   launches.load(), sm ? "shared" : "global", n, n_act, CS, smem, mm, max_kw, work);
+      std::fprintf(stderr, "[cq log] launch %d %s: items %d active %d CS %d NT %d smem %zu max m %d max kw %d sum m*kw %.3g\n",
+                   launches.load(), sm ? "shared" : "global", n, n_act, CS, NT, smem, mm, max_kw, work);
     }
     long long* trace = nullptr;
     if (launches++ == trace_at) {
@@ -802,17 +837,25 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
         }
       HS_CUDA(cudaMemcpyAsync(trace + 254, &tb, sizeof tb, cudaMemcpyHostToDevice, st));
       HS_CUDA(cudaStreamSynchronize(st));
+      if (std::getenv("HS_CQ_TRACE_FINE")) {
+        static const long long one = 1;
+        HS_CUDA(cudaMemcpyAsync(trace + 253, &one, sizeof one, cudaMemcpyHostToDevice, st));
+      }
       if (std::getenv("HS_CQ_TRACE_SPLIT")) {
         static const long long one = 1;
         HS_CUDA(cudaMemcpyAsync(trace + 255, &one, sizeof one, cudaMemcpyHostToDevice, st));
       }
     }
     if (MR == 8) {
-      if (sm) launch_one<8, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else launch_one<8, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      if (!sm) launch_one<8, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else if (NT == 128) launch_one<8, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else if (NT == 256) launch_one<8, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else launch_one<8, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
     } else {
-      if (sm) launch_one<16, true>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else launch_one<16, false>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      if (!sm) launch_one<16, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else if (NT == 128) launch_one<16, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else if (NT == 256) launch_one<16, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      else launch_one<16, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
     }
     CS_ret = std::max(CS_ret, CS);
     if (trace) {
@@ -829,6 +872,11 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
                      h[5 + 4 * j] - h[4 + 4 * j], h[6 + 4 * j] - h[5 + 4 * j]);
       std::fprintf(stderr, "[cq trace]  loop end %lld, exit %lld, total %lld cyc\n", h[250] - t0, h[251] - h[250],
                    h[251] - t0);
+      if (std::getenv("HS_CQ_TRACE_FINE"))
+        for (int j = 0; j < 12 && h[100 + 8 * j]; ++j)
+          std::fprintf(stderr, "[cq fine]  step %2d: sync->w0 %6lld  xnorm %6lld  scalars %6lld  msg %6lld  fence %6lld  push %6lld\n",
+                       j, h[100 + 8 * j] - h[3 + 4 * j], h[101 + 8 * j] - h[100 + 8 * j], h[102 + 8 * j] - h[101 + 8 * j],
+                       h[103 + 8 * j] - h[102 + 8 * j], h[104 + 8 * j] - h[103 + 8 * j], h[105 + 8 * j] - h[104 + 8 * j]);
     }
   }
   return CS_ret;
