@@ -63,10 +63,10 @@ __host__ __device__ __forceinline__ int cq_ldm(int m, int G) {
 }
 __host__ __device__ __forceinline__ int cq_msg_words(int m);
 // dynamic shared memory words: W slice (SM mode) + norms + message staging and slots
-__host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, int MR, bool sm) {
+__host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, int MR, bool sm, bool light = false) {
   const int wchunk = (kw + CS - 1) / CS;
   const size_t w = sm ? (((size_t)wchunk * cq_ldm(m, cq_group(m, MR)) + 1) & ~(size_t)1) : 0;
-  return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * cq_msg_words(m);
+  return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * (light ? 8 : cq_msg_words(m));
 }
 // direct write-back: the store element (row l of s, column j of B_s), j in the segment list
 __device__ __forceinline__ int seg_find(const FusedSeg* seg, int nseg, int j) {
@@ -155,7 +155,8 @@ struct __align__(16) CqFb {     // fallback message: exact lowest candidate w.r.
 struct CqShared {
   unsigned long long bar1[2], bar2, bar3[2];   // step messages / fallback vector / fallback candidates
   CqFb mine3[2], slot3[2][16];
-  double wred[CQ_WARPS];
+  double wred[CQ_WARPS];                        // per-warp max norm
+  double wcnu[CQ_WARPS];                        // nu of the warp's candidate
   int wcand[CQ_WARPS];                          // per-warp lowest local candidate (INT_MAX: none)
   __align__(16) double vstage[MAX_M + 8];      // fallback: owner's (tau, beta, v) staging
   __align__(16) double vbuf[MAX_M + 8];        // fallback: received (tau, beta, v)
@@ -163,6 +164,43 @@ struct CqShared {
 // Step message of one CTA (doubles): [0] M_c, [1] nu(i_c), [2] i_c (canonical, -1: none),
 // [3] tau, [4] beta of the Householder reflector of column i_c, [5..8) pad, [8, 8+m) v
 __host__ __device__ __forceinline__ int cq_msg_words(int m) { return (8 + m + 1) & ~1; }
+
+// dlarfg (LAPACK convention) of column col, rows j..m-1, by one warp: the column in registers
+// once (m <= 32 MR), x_norm from them, dst[8 + l] = v_l (zero above j, one at j, x_l / (alpha -
+// beta) below); tau and beta in every lane.
+template <int MR>
+__device__ __forceinline__ void form_reflector(const double* col, int j, int m, int lane, double* dst, double& tau,
+                                               double& beta) {
+  double xr[MR];
+  double xs = 0.0;
+  const double alpha = col[j];
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    const int l = lane + 32 * i;
+    xr[i] = l < m ? col[l] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < MR; ++i)
+    if (lane + 32 * i > j) xs += xr[i] * xr[i];
+  xs = wsum(xs);
+  const double xnorm = sqrt(xs);
+  double rden;
+  if (xnorm == 0.0) {
+    tau = 0.0;
+    beta = alpha;
+    rden = 0.0;
+  } else {
+    const double h = sqrt(alpha * alpha + xnorm * xnorm);
+    beta = alpha >= 0.0 ? -h : h;
+    tau = (beta - alpha) / beta;
+    rden = 1.0 / (alpha - beta);   // dlarfg scales x by 1/(alpha - beta)
+  }
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    const int l = lane + 32 * i;
+    if (l < m) dst[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : xr[i] * rden;
+  }
+}
 
 // The pivoting loop for a fixed group size G (lanes per column).
 //
@@ -181,7 +219,7 @@ __host__ __device__ __forceinline__ int cq_msg_words(int m) { return (8 + m + 1)
 // One mbarrier wait per step, no cluster-wide barrier inside the loop.
 template <int MR, int G, bool SM, int NT>
 __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int relative, int32_t* rank_slot,
-                                          double* dsm, CqShared& sh, long long* trace) {
+                                          double* dsm, CqShared& sh, long long* trace, bool light) {
   // HS_CQ_TRACE debug aid: clock64 timeline of cluster 0 / CTA 0 / thread 0
 #define CQ_TR(k)                                                            \
   do {                                                                      \
@@ -206,7 +244,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   const int w_lo = crank * wchunk;
   const int nw = max(0, min(kw - w_lo, wchunk));
   const int ldm = cq_ldm(m, G);
-  const int msgw = cq_msg_words(m);
+  // light messages (header only; the owner of the chosen pivot pushes its reflector after the
+  // decision): the slots shrink from (2 + 2 CS)(8 + m) to (2 + 2 CS) 8 words, so wide blocks
+  // keep their whole slice in shared memory
+  const int msgw = light ? 8 : cq_msg_words(m);
   const uint32_t msgb = (uint32_t)(msgw * 8);
   // element (l, c) of the slice, column-major with column stride ldm: in shared memory (SM)
   // or in the cluster's global scratch (global mode: coalesced group loads through L2)
@@ -298,56 +339,58 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     double* slot = slots + (size_t)buf * CS * msgw;
     // (1) local max, local candidate and its reflector -> every CTA
     lm = wmax(lm);
-    if (lane == 0) sh.wred[wid] = lm;
-    if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
-    __syncthreads();
-    if (j < (trace_fine ? 24 : 60)) CQ_TR(3 + 4 * j);
-    {   // every warp: the CTA max, and the lowest column of a strided share over the window
-      double Mc = lane < (NT / 32) ? sh.wred[lane] : -1.0;
-      Mc = wmax(Mc);
-      const double thr_c = CQ_WINDOW * Mc;
+    {   // every warp, over the columns its own groups updated (their norms are the warp's own
+        // writes): its max M_w and its lowest column with nu >= (1 - 1e-10) M_w
+      __syncwarp();
+      const double thr_w = CQ_WINDOW * lm;
       int lw = INT_MAX;
-      if (Mc >= 0.0)
-        for (int c = wid * 32 + lane; c < nw; c += NT)
-          if (nu[c] >= thr_c) {
+      if (lm >= 0.0)
+        for (int k = t; k < kiters; k += G) {
+          const int c = grp + k * NGRP;
+          if (c < nw && nu[c] >= thr_w) {
             lw = c;
             break;
           }
+        }
       lw = wmin_i(lw);
-      if (lane == 0) sh.wcand[wid] = lw;
+      if (lane == 0) {
+        sh.wred[wid] = lm;
+        sh.wcand[wid] = lw;
+        sh.wcnu[wid] = lw != INT_MAX ? nu[lw] : -1.0;
+      }
     }
+    if (tid == 0) bar_expect(sm_addr(&sh.bar1[buf]), (uint32_t)CS * msgb);
     __syncthreads();
+    if (j < (trace_fine ? 24 : 60)) CQ_TR(3 + 4 * j);
     if (wid == 0) {
       CQ_TF(j, 0);
       double Mc = lane < (NT / 32) ? sh.wred[lane] : -1.0;
       Mc = wmax(Mc);
-      int li = lane < (NT / 32) ? sh.wcand[lane] : INT_MAX;   // the lowest over all shares
+      // the CTA's lowest column over the CTA window: the lowest warp candidate inside it; a warp
+      // that reaches the window with its own candidate below it (a near-tie straddling the warp
+      // and CTA windows) makes warp 0 rescan every column
+      const double thr_c = CQ_WINDOW * Mc;
+      const bool reach = Mc >= 0.0 && lane < (NT / 32) && sh.wred[lane] >= thr_c;
+      const bool okc = reach && sh.wcnu[lane] >= thr_c;
+      int li = okc ? sh.wcand[lane] : INT_MAX;
       li = wmin_i(li);
-      if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
-        const double* col = Wc(li);
-        double xs = 0.0;
-        for (int l = j + 1 + lane; l < m; l += 32) {
-          const double b = col[(size_t)l * sr];
-          xs += b * b;
+      if (__any_sync(0xffffffffu, reach && !okc)) {
+        li = INT_MAX;
+        for (int c = lane; c < nw; c += 32)
+          if (nu[c] >= thr_c) {
+            li = c;
+            break;
+          }
+        li = wmin_i(li);
+      }
+      if (li != INT_MAX && light) {
+        if (lane == 0) {
+          mymsg[1] = nu[li];
+          mymsg[2] = (double)(w_lo + li);
         }
-        xs = wsum(xs);
-        CQ_TF(j, 1);
-        const double alpha = col[(size_t)j * sr];
-        const double xnorm = sqrt(xs);
-        double tau, beta, rden;
-        if (xnorm == 0.0) {
-          tau = 0.0;
-          beta = alpha;
-          rden = 0.0;
-        } else {
-          const double h = sqrt(alpha * alpha + xnorm * xnorm);
-          beta = alpha >= 0.0 ? -h : h;
-          tau = (beta - alpha) / beta;
-          rden = 1.0 / (alpha - beta);   // dlarfg scales x by 1/(alpha - beta)
-        }
-        CQ_TF(j, 2);
-        for (int l = lane; l < m; l += 32)
-          mymsg[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : col[(size_t)l * sr] * rden;
+      } else if (li != INT_MAX) {   // dlarfg of column li, rows j..m-1
+        double tau, beta;
+        form_reflector<MR>(Wc(li), j, m, lane, mymsg, tau, beta);
         CQ_TF(j, 3);
         if (lane == 0) {
           mymsg[1] = nu[li];
@@ -391,9 +434,11 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     const int k0 = over ? __ffs(over) - 1 : 0;           // lowest CTA holding a global candidate
     const double* vmsg = slot + (size_t)k0 * msgw;     // its reflector
     int p = (int)vmsg[2];
+    bool push = light;   // light: the owner forms and pushes the reflector of p
     if (!(vmsg[1] >= thr)) {
       // near-tie straddling the local and global windows: exchange the exact candidates,
       // then the owner forms and pushes the reflector of the true pivot
+      push = true;
       const uint32_t par3 = (uint32_t)(use3[buf]++ & 1);
       if (tid == 0) bar_expect(sm_addr(&sh.bar3[buf]), (uint32_t)(CS * sizeof(CqFb)));
       if (wid == 0) {
@@ -416,33 +461,15 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       bar_wait(sm_addr(&sh.bar3[buf]), par3);
       p = INT_MAX;
       for (int k = 0; k < CS; ++k) p = min(p, sh.slot3[buf][k].F);
+    }
+    if (push) {
       const int ow = p / wchunk;
       const uint32_t vbytes = (uint32_t)(((8 + m) * 8 + 15) & ~15);
       const uint32_t par2 = (uint32_t)(use2++ & 1);
       if (tid == 0) bar_expect(sm_addr(&sh.bar2), vbytes);
       if (crank == ow && wid == 0) {
-        const double* col = Wc(p - ow * wchunk);
-        double xs = 0.0;
-        for (int l = j + 1 + lane; l < m; l += 32) {
-          const double b = col[(size_t)l * sr];
-          xs += b * b;
-        }
-        xs = wsum(xs);
-        const double alpha = col[(size_t)j * sr];
-        const double xnorm = sqrt(xs);
-        double tau, beta, rden;
-        if (xnorm == 0.0) {
-          tau = 0.0;
-          beta = alpha;
-          rden = 0.0;
-        } else {
-          const double h = sqrt(alpha * alpha + xnorm * xnorm);
-          beta = alpha >= 0.0 ? -h : h;
-          tau = (beta - alpha) / beta;
-          rden = 1.0 / (alpha - beta);
-        }
-        for (int l = lane; l < m; l += 32)
-          sh.vstage[8 + l] = (l < j) ? 0.0 : (l == j) ? 1.0 : col[(size_t)l * sr] * rden;
+        double tau, beta;
+        form_reflector<MR>(Wc(p - ow * wchunk), j, m, lane, sh.vstage, tau, beta);
         if (lane == 0) {
           sh.vstage[2] = (double)p;
           sh.vstage[3] = tau;
@@ -509,7 +536,8 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
             if (i < nr) cp[u][(size_t)i * G * sr] = y;
             if (i >= gi) ss[u] += y * y;
           }
-        } else if (piv[u]) {   // the pivot column: (beta, 0, ..., 0) from row j
+        } else if (piv[u]) {   // the pivot column: (beta, 0, ..., 0) from row j; out of the search
+          if (t == 0) nu[cxs[u]] = -1.0;
 #pragma unroll
           for (int i = 0; i < MR; ++i)
             if (i < nr && t + i * G >= j) cp[u][(size_t)i * G * sr] = (t + i * G == j) ? beta : 0.0;
@@ -561,7 +589,8 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 // let several clusters' latency-bound step chains share an SM when their slices fit
 template <int MR, bool SM, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
-                                                          int32_t* __restrict__ rank_out, long long* trace) {
+                                                          int32_t* __restrict__ rank_out, long long* trace,
+                                                          int light) {
   pdl_trigger();
   pdl_wait();
   namespace cg = cooperative_groups;
@@ -576,12 +605,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_cpqr3(const CluItem* __restric
   extern __shared__ double dsm[];
   __shared__ CqShared sh;
   switch (cq_group(it.m, MR)) {
-    case 1: cpqr_body<MR, 1, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 2: cpqr_body<MR, 2, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 4: cpqr_body<MR, 4, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 8: cpqr_body<MR, 8, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    case 16: cpqr_body<MR, 16, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
-    default: cpqr_body<MR, 32, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace); break;
+    case 1: cpqr_body<MR, 1, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 2: cpqr_body<MR, 2, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 4: cpqr_body<MR, 4, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 8: cpqr_body<MR, 8, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 16: cpqr_body<MR, 16, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    default: cpqr_body<MR, 32, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
   }
 }
 
@@ -680,7 +709,7 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
 
 template <int MR, bool SM, int NT>
 void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
-                cudaStream_t st, long long* trace) {
+                cudaStream_t st, long long* trace, bool light) {
   auto kern = k_cpqr3<MR, SM, NT>;
   static std::once_flag once;
   std::call_once(once, [&] {
@@ -701,7 +730,15 @@ void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, 
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;   // programmatic dependent launch (pdl_wait precedes every read)
-  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, relative ? 1 : 0, d_rank, trace));
+  static const bool cq_log = std::getenv("HS_CQ_LOG") != nullptr;
+  if (cq_log) {   // co-resident clusters of this shape (GPC packing)
+    int ncl = -1;
+    cudaLaunchConfig_t oc = cfg;
+    oc.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)kern, &oc) != cudaSuccess) cudaGetLastError();
+    std::fprintf(stderr, "[cq log]   max active clusters %d (CS %d, NT %d, smem %zu)\n", ncl, CS, NT, smem);
+  }
+  HS_CUDA(cudaLaunchKernelEx(&cfg, kern, d_items, eps, relative ? 1 : 0, d_rank, trace, light ? 1 : 0));
   count_launch(1);
 }
 
@@ -716,7 +753,9 @@ static constexpr size_t CQ_CAP_BYTES = 200 * 1024 - sizeof(CqShared);
 size_t cpqr_global_words(int m, int kw, int max_m) {
   if (m <= 0 || kw <= 0) return 0;
   if (std::getenv("HS_CPQR_GLOBAL") == nullptr &&
-      cq_smem_words(m, kw, 16, cq_mr(max_m), true) * sizeof(double) <= CQ_CAP_BYTES)
+      cq_smem_words(m, kw, 16, cq_mr(max_m), true, std::getenv("HS_CPQR_LIGHT") == nullptr ||
+                                                      std::atoi(std::getenv("HS_CPQR_LIGHT")) != 0) *
+              sizeof(double) <= CQ_CAP_BYTES)
     return 0;
   return (size_t)(kw + 16) * (m + 16);
 }
@@ -754,10 +793,19 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
   int CS_ret = 0;
   for (int mode = 0; mode < 2; ++mode) {   // 0: shared-memory clusters, 1: global-scratch clusters
     const bool sm = mode == 0;
+    // light messages (HS_CPQR_LIGHT=1 forces them, =0 forbids them): the global-mode launch
+    // always (its slices keep more columns in shared memory), the shared-mode launch when its
+    // widest slice does not fit a 16-CTA cluster with the speculative reflector messages
+    static const int light_env = [] {
+      const char* e = std::getenv("HS_CPQR_LIGHT");
+      return e ? std::atoi(e) : -1;
+    }();
+    bool light = light_env == 1 || (!sm && light_env != 0);
     auto need = [&](int cs) {
       size_t w = 2;
       for (const auto& it : h_items)
-        if (it.m > 0 && it.kw > 0 && (it.Wt == nullptr) == sm) w = std::max(w, cq_smem_words(it.m, it.kw, cs, MR, sm));
+        if (it.m > 0 && it.kw > 0 && (it.Wt == nullptr) == sm)
+          w = std::max(w, cq_smem_words(it.m, it.kw, cs, MR, sm, light));
       return w * sizeof(double);
     };
     int n_act = 0, max_kw = 0;
@@ -771,6 +819,11 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
     if (n_mode == 0) continue;
     int CS = 1;
     while (CS < 16 && need(CS) > std::min(target, CQ_CAP_BYTES)) CS *= 2;
+    if (sm && !light && light_env != 0 && need(CS) > std::min(target, CQ_CAP_BYTES)) {
+      light = true;
+      CS = 1;
+      while (CS < 16 && need(CS) > std::min(target, CQ_CAP_BYTES)) CS *= 2;
+    }
     // shared mode: smaller CTAs (NT = 256 / 128 threads, 2 / 4 CTAs per SM) when every slice
     // still fits their share of the SM's shared memory at CS <= 16 and the batch fills the
     // GPU: several clusters' step chains then interleave on an SM (HS_CQ_NT forces 128/256/512)
@@ -822,8 +875,8 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
           mm = std::max(mm, it.m);
           work += (double)it.m * it.kw;
         }
-      std::fprintf(stderr, "[cq log] launch %d %s: items %d active %d CS %d NT %d smem %zu max m %d max kw %d sum m*kw %.3g\n",
-                   launches.load(), sm ? "shared" : "global", n, n_act, CS, NT, smem, mm, max_kw, work);
+      std::fprintf(stderr, "[cq log] launch %d %s%s: items %d active %d CS %d NT %d smem %zu max m %d max kw %d sum m*kw %.3g\n",
+                   launches.load(), sm ? "shared" : "global", light ? " light" : "", n, n_act, CS, NT, smem, mm, max_kw, work);
     }
     long long* trace = nullptr;
     if (launches++ == trace_at) {
@@ -847,15 +900,15 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
       }
     }
     if (MR == 8) {
-      if (!sm) launch_one<8, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else if (NT == 128) launch_one<8, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else if (NT == 256) launch_one<8, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else launch_one<8, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      if (!sm) launch_one<8, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 128) launch_one<8, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 256) launch_one<8, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else launch_one<8, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
     } else {
-      if (!sm) launch_one<16, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else if (NT == 128) launch_one<16, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else if (NT == 256) launch_one<16, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
-      else launch_one<16, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace);
+      if (!sm) launch_one<16, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 128) launch_one<16, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 256) launch_one<16, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else launch_one<16, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
     }
     CS_ret = std::max(CS_ret, CS);
     if (trace) {
