@@ -231,7 +231,13 @@ hs_status hs_dist_plan_export(hs_analysis a, int32_t world, int32_t rank, int32_
  * first factor caches the pattern and its level-0 scatter map on the device inside the
  * analysis, so re-factoring new values on the same pattern (Newton / continuation
  * sequences) uploads only the values.  On HS_E_NOT_SPD no factor is created and
- * hs_last_error names (level, cluster, pivot, value). */
+ * hs_last_error names (level, cluster, pivot, value).
+ * Memory: the handle owns a caching allocator; large factors (a level-0 block store of
+ * >= 24 GB, e.g. C4) keep their records in a virtual range whose completed levels are
+ * copied to pinned HOST memory when a later level's block store needs the device memory,
+ * and mapped back at the same addresses before the call returns (the apply reads device
+ * memory only).  HS_E_OOM if the store of one level plus the running level's records do
+ * not fit the device, or the records of the whole factor exceed it. */
 hs_status hs_factor_create(hs_handle h, hs_analysis a, const double* values,
                            const hs_factor_opts* opt, hs_factor* out);
 hs_status hs_factor_get_stats(hs_factor f, hs_factor_stats_t* st);

@@ -313,6 +313,10 @@ void hs_analysis_destroy(hs_analysis a) {
                     (void*)a->an->d_tmap})
       if (p) cudaFree(p);
   }
+  if (a->an && a->an->maps_pinned) {
+    cudaHostUnregister(a->an->h_map.data());
+    cudaHostUnregister(a->an->h_tmap.data());
+  }
   if (a->an && a->an->l0s.d_idx) {
     cudaSetDevice(a->an->l0s.dev);
     cudaFree(a->an->l0s.d_idx);

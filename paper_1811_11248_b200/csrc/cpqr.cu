@@ -66,7 +66,8 @@ __host__ __device__ __forceinline__ int cq_msg_words(int m);
 __host__ __device__ __forceinline__ size_t cq_smem_words(int m, int kw, int CS, int MR, bool sm, bool light = false) {
   const int wchunk = (kw + CS - 1) / CS;
   const size_t w = sm ? (((size_t)wchunk * cq_ldm(m, cq_group(m, MR)) + 1) & ~(size_t)1) : 0;
-  return w + (size_t)((wchunk + 1) & ~1) + (size_t)(2 + 2 * CS) * (light ? 8 : cq_msg_words(m));
+  return w + (size_t)((wchunk + 1) & ~1) + (light ? (size_t)2 * cq_msg_words(m) + (size_t)2 * CS * 8
+                                                  : (size_t)(2 + 2 * CS) * cq_msg_words(m));
 }
 // direct write-back: the store element (row l of s, column j of B_s), j in the segment list
 __device__ __forceinline__ int seg_find(const FusedSeg* seg, int nseg, int j) {
@@ -247,7 +248,10 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   // light messages (header only; the owner of the chosen pivot pushes its reflector after the
   // decision): the slots shrink from (2 + 2 CS)(8 + m) to (2 + 2 CS) 8 words, so wide blocks
   // keep their whole slice in shared memory
-  const int msgw = light ? 8 : cq_msg_words(m);
+  // light: the own message buffers hold the header AND the speculatively formed reflector of
+  // the local candidate (formed while the headers travel; pushed only if it wins)
+  const int msgw = light ? 8 : cq_msg_words(m);             // slot stride
+  const int msgo = light ? cq_msg_words(m) : msgw;          // own buffer stride
   const uint32_t msgb = (uint32_t)(msgw * 8);
   // element (l, c) of the slice, column-major with column stride ldm: in shared memory (SM)
   // or in the cluster's global scratch (global mode: coalesced group loads through L2)
@@ -259,7 +263,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   // the slice that exceeds the CTA's shared memory streams through L2 every step
   double* nu = SM ? dsm + (((size_t)wchunk * ldm + 1) & ~(size_t)1) : dsm;
   double* mine = nu + ((wchunk + 1) & ~1);
-  double* slots = mine + 2 * msgw;
+  double* slots = mine + 2 * msgo;
   double* const Wsm = SM ? dsm : slots + (((size_t)2 * CS * msgw + 1) & ~(size_t)1);
   double* const Wg = SM ? dsm : it.Wt + (size_t)w_lo * ldm;
   int nsmc = nw;
@@ -329,13 +333,15 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
   CQ_TR(2);
 
   const int kmax = min(m, kw);
+  int spec_li = INT_MAX;               // light: warp 0's local candidate of this step
+  double spec_tau = 0.0, spec_beta = 0.0;
   double tau_s = 0.0;
   int r = kmax;
   int use3[2] = {0, 0}, use2 = 0;
   for (int j = 0; j < kmax; ++j) {
     const int buf = j & 1;
     const uint32_t par = (uint32_t)((j >> 1) & 1);
-    double* mymsg = mine + buf * msgw;
+    double* mymsg = mine + buf * msgo;
     double* slot = slots + (size_t)buf * CS * msgw;
     // (1) local max, local candidate and its reflector -> every CTA
     lm = wmax(lm);
@@ -383,6 +389,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
           }
         li = wmin_i(li);
       }
+      spec_li = light ? li : INT_MAX;
       if (li != INT_MAX && light) {
         if (lane == 0) {
           mymsg[1] = nu[li];
@@ -410,6 +417,8 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
         bulk_push(remote(sm_addr(slot + (size_t)crank * msgw), lane), sm_addr(mymsg), msgb,
                   remote(sm_addr(&sh.bar1[buf]), lane));
       CQ_TF(j, 5);
+      if (spec_li != INT_MAX)   // light: the candidate's reflector while the headers travel
+        form_reflector<MR>(Wc(spec_li), j, m, lane, mymsg, spec_tau, spec_beta);
       if (trace_split && j < (trace_fine ? 24 : 60)) CQ_TR(4 + 4 * j);   // local work done, message sent
     }
     // (2) decision from the CS messages (identical in every thread of every CTA)
@@ -468,17 +477,26 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
       const uint32_t par2 = (uint32_t)(use2++ & 1);
       if (tid == 0) bar_expect(sm_addr(&sh.bar2), vbytes);
       if (crank == ow && wid == 0) {
-        double tau, beta;
-        form_reflector<MR>(Wc(p - ow * wchunk), j, m, lane, sh.vstage, tau, beta);
-        if (lane == 0) {
-          sh.vstage[2] = (double)p;
-          sh.vstage[3] = tau;
-          sh.vstage[4] = beta;
+        double* src = sh.vstage;
+        if (spec_li != INT_MAX && p == w_lo + spec_li) {   // the speculative reflector won
+          src = mymsg;
+          if (lane == 0) {
+            src[3] = spec_tau;
+            src[4] = spec_beta;
+          }
+        } else {
+          double tau, beta;
+          form_reflector<MR>(Wc(p - ow * wchunk), j, m, lane, sh.vstage, tau, beta);
+          if (lane == 0) {
+            sh.vstage[2] = (double)p;
+            sh.vstage[3] = tau;
+            sh.vstage[4] = beta;
+          }
         }
         fence_proxy_async();
         __syncwarp();
         if (lane < CS)
-          bulk_push(remote(sm_addr(sh.vbuf), lane), sm_addr(sh.vstage), vbytes, remote(sm_addr(&sh.bar2), lane));
+          bulk_push(remote(sm_addr(sh.vbuf), lane), sm_addr(src), vbytes, remote(sm_addr(&sh.bar2), lane));
       }
       bar_wait(sm_addr(&sh.bar2), par2);
       vmsg = sh.vbuf;
@@ -707,6 +725,153 @@ __global__ void __launch_bounds__(CQ_THREADS) k_rotate_n(const CluItem* __restri
   }
 }
 
+// a4 (and T_s = Qᵀ G_s^{-1}) on the FP64 tensor cores: Qᵀ X = H_{r-1} ... H_0 X in panels of
+// RW_B reflectors in compact-WY form, H_{j0+b-1} ... H_{j0} = I - V_p T_pᵀ V_pᵀ (T_p upper
+// triangular, LAPACK dlarft forward/columnwise), per panel
+//     Y = V_pᵀ X (b x NC, K = m: DMMA),   Z = T_pᵀ Y,   X <- X - V_p Z (m x NC, K = b: DMMA).
+// One CTA of 8 warps per (cluster, 32-column tile); X stays in shared memory for all panels,
+// T_p is formed per tile from the panel's Gram matrix (the panel's reflectors are read once
+// per tile from L2).  Same quantity as the reflector-by-reflector rotation, other rounding
+// order (DESIGN.md §2 "Rounding order").  m <= 256.
+constexpr int RW_NC = 32;        // tile columns
+constexpr int RW_B = 16;         // reflectors per panel
+constexpr int RW_LDX = RW_NC + 4;   // X row stride (== 4 mod 16 doubles: conflict-free fragments)
+constexpr int RW_LDV = RW_B + 4;    // V_p row stride
+
+__device__ __forceinline__ void rw_dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_rotate_wy(const CluItem* __restrict__ clu, const TrsmItem* __restrict__ items,
+                                                    const int32_t* __restrict__ rank) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ double rws[];
+  const TrsmItem ti = items[blockIdx.x];
+  const CluItem it = clu[ti.ci];
+  const int r = rank[ti.ci];
+  const bool tcols = ti.pad == 1;   // a tile of T_s = Qᵀ G_s^{-1}
+  const int m = it.m;
+  if (m == 0 || (r == 0 && !it.dwb && !tcols)) return;
+  const int c0 = ti.c0, nc = ti.nc;
+  const int mp = (m + 7) & ~7;                    // rows padded to the 8-row DMMA tiles
+  double* X = rws;                                // mp x RW_LDX
+  double* Vp = X + (size_t)mp * RW_LDX;           // mp x RW_LDV  (V_p, row l, column i)
+  double* Tp = Vp + (size_t)mp * RW_LDV;          // RW_B x RW_B  (T_p, upper)
+  double* Gm = Tp + RW_B * RW_B;                  // RW_B x RW_B  (Gram V_pᵀ V_p)
+  double* Y = Gm + RW_B * RW_B;                   // RW_B x RW_LDX (Y, then Z)
+  double* tauv = Y + RW_B * RW_LDX;               // RW_B
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const double* src = tcols ? it.Ginv + c0 : it.B + it.kw + c0;
+  const int lds = tcols ? m : it.ldB;
+  for (int e = tid; e < mp * RW_NC; e += 256) {   // X <- the tile (zero-padded)
+    const int l = e / RW_NC, c = e % RW_NC;
+    X[l * RW_LDX + c] = (l < m && c < nc) ? src[(size_t)l * lds + c] : 0.0;
+  }
+  for (int j0 = 0; j0 < r; j0 += RW_B) {
+    const int b = min(RW_B, r - j0);
+    __syncthreads();   // the previous panel's users of Vp / Y are done
+    for (int e = tid; e < mp * RW_B; e += 256) {   // V_p: column i = v_{j0+i} (zeros beyond b / m)
+      const int i = e / mp, l = e % mp;
+      Vp[l * RW_LDV + i] = (i < b && l < m) ? it.V[(size_t)(j0 + i) * m + l] : 0.0;
+    }
+    if (tid < RW_B) tauv[tid] = tid < b ? it.tau[j0 + tid] : 0.0;
+    __syncthreads();
+    if (w < 4) {   // Gram matrix V_pᵀ V_p: 2 x 2 tiles of 8 x 8 on warps 0-3 (K = mp, from row j0)
+      const int ti8 = w >> 1, tj8 = w & 1;
+      double c[2] = {0.0, 0.0};
+      for (int k = j0 & ~3; k < mp; k += 4) {
+        const double a = Vp[(k + fc) * RW_LDV + 8 * ti8 + fr];
+        const double bb = Vp[(k + fc) * RW_LDV + 8 * tj8 + fr];
+        rw_dmma(c, a, bb);
+      }
+      Gm[(8 * ti8 + fr) * RW_B + 8 * tj8 + 2 * fc] = c[0];
+      Gm[(8 * ti8 + fr) * RW_B + 8 * tj8 + 2 * fc + 1] = c[1];
+    }
+    __syncthreads();
+    if (w == 0) {   // dlarft: T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] (V_pᵀ v_i)[0:i]
+      for (int i = 0; i < RW_B; ++i) {
+        double t = 0.0;
+        if (lane < i) {
+          for (int q = lane; q < i; ++q) t = fma(Tp[lane * RW_B + q], Gm[q * RW_B + i], t);
+          t *= -tauv[i];
+        }
+        if (lane < RW_B) {
+          if (lane < i) Tp[lane * RW_B + i] = t;
+          else if (lane == i) Tp[i * RW_B + i] = tauv[i];
+          else Tp[lane * RW_B + i] = 0.0;
+        }
+        __syncwarp();
+      }
+    }
+    // Y = V_pᵀ X: 2 x 4 output tiles of 8 x 8, one per warp, K = mp
+    {
+      const int ti8 = w >> 2, tn = w & 3;
+      double c[2] = {0.0, 0.0};
+      for (int k = 0; k < mp; k += 4) {
+        const double a = Vp[(k + fc) * RW_LDV + 8 * ti8 + fr];   // A = V_pᵀ: (row i, col k)
+        const double bb = X[(k + fc) * RW_LDX + 8 * tn + fr];    // B = X: (k, n)
+        rw_dmma(c, a, bb);
+      }
+      Y[(8 * ti8 + fr) * RW_LDX + 8 * tn + 2 * fc] = c[0];
+      Y[(8 * ti8 + fr) * RW_LDX + 8 * tn + 2 * fc + 1] = c[1];
+    }
+    __syncthreads();
+    {   // Z = T_pᵀ Y (in place, by column): Z[i][n] = sum_{k <= i} T[k][i] Y[k][n]
+      const int n = tid % RW_NC, i0 = tid / RW_NC;   // 8 row pairs x 32 columns
+      double z[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * i0 + h;
+        double acc = 0.0;
+        for (int k = 0; k <= i; ++k) acc = fma(Tp[k * RW_B + i], Y[k * RW_LDX + n], acc);
+        z[h] = acc;
+      }
+      __syncthreads();
+      Y[(2 * i0) * RW_LDX + n] = z[0];
+      Y[(2 * i0 + 1) * RW_LDX + n] = z[1];
+    }
+    __syncthreads();
+    // X <- X - V_p Z: (mp / 8) x 4 tiles over the warps, K = RW_B
+    for (int t8 = w; t8 < (mp >> 3) * 4; t8 += 8) {
+      const int tr = t8 >> 2, tn = t8 & 3;
+      double* xp = X + (8 * tr + fr) * RW_LDX + 8 * tn + 2 * fc;
+      double c[2] = {xp[0], xp[1]};
+#pragma unroll
+      for (int k = 0; k < RW_B; k += 4) {
+        const double a = -Vp[(8 * tr + fr) * RW_LDV + k + fc];
+        const double bb = Y[(k + fc) * RW_LDX + 8 * tn + fr];
+        rw_dmma(c, a, bb);
+      }
+      xp[0] = c[0];
+      xp[1] = c[1];
+    }
+  }
+  __syncthreads();
+  // epilogue (as rotate_body): T_s tile, or B_n write-back / coarse-n rows to the store / C_s
+  for (int e = tid; e < m * nc; e += 256) {
+    const int l = e / nc, c = e % nc;
+    const double x = X[l * RW_LDX + c];
+    if (tcols) {
+      it.Tout[(size_t)l * m + c0 + c] = x;
+      continue;
+    }
+    if (!it.dwb || it.keepB) const_cast<double*>(src)[(size_t)l * lds + c] = x;
+    if (it.dwb) {
+      const int jn = c0 + c;
+      if (l < r) {
+        double* d = dwb_addr(it.seg, it.nseg, it.kw + jn, l);
+        if (d) *d = x;
+      } else {
+        it.Cout[(size_t)(l - r) * it.ldC + jn] = x;
+      }
+    }
+  }
+}
+
 template <int MR, bool SM, int NT>
 void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
                 cudaStream_t st, long long* trace, bool light) {
@@ -837,10 +1002,18 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
         if (nt_env && nt != nt_env) continue;
         const int B = 512 / nt;
         const size_t lim = (228 * 1024) / B - sizeof(CqShared) - 1024;
+        const bool light0 = light;
         int cs = 1;
         while (cs < 16 && need(cs) > lim) cs *= 2;
-        if (need(cs) > lim) continue;
-        if (!nt_env && (size_t)n_act * std::max(cs, CS) < (size_t)nsm * B) continue;   // a partial wave: keep 512
+        if (need(cs) > lim && !light && light_env != 0) {   // light messages may make it fit
+          light = true;
+          cs = 1;
+          while (cs < 16 && need(cs) > lim) cs *= 2;
+        }
+        if (need(cs) > lim || (!nt_env && (size_t)n_act * std::max(cs, CS) < (size_t)nsm * B)) {
+          light = light0;   // does not fit, or a partial wave: keep 512
+          continue;
+        }
         NT = nt;
         CS = std::max(CS, cs);
         break;
@@ -937,11 +1110,28 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
 
 // rows per lane: 8 up to m = 256 (the kernels' group size G <= 32), else 16
 static int rot_mr(int max_m) { return max_m <= 256 ? 8 : 16; }
-int rot_tile_cols(int m, int max_m) { return CQ_THREADS / cq_group(std::max(m, 1), rot_mr(max_m)); }
+static bool rot_wy(int max_m) {   // the compact-WY DMMA rotation (HS_ROTATE_LEGACY=1: reflector by reflector)
+  static const bool legacy = std::getenv("HS_ROTATE_LEGACY") != nullptr;
+  return !legacy && max_m <= 256;
+}
+int rot_tile_cols(int m, int max_m) {
+  return rot_wy(max_m) ? RW_NC : CQ_THREADS / cq_group(std::max(m, 1), rot_mr(max_m));
+}
 
 void launch_rotate_n(const CluItem* d_clu, const TrsmItem* d_items, int n, int max_m, const int32_t* d_rank,
                      cudaStream_t st) {
   if (n <= 0) return;
+  if (rot_wy(max_m)) {
+    const int mp = (max_m + 7) & ~7;
+    const size_t smem = sizeof(double) * ((size_t)mp * (RW_LDX + RW_LDV) + 2 * RW_B * RW_B + RW_B * RW_LDX + RW_B);
+    static std::once_flag once;
+    std::call_once(once, [] {
+      HS_CUDA(cudaFuncSetAttribute((const void*)k_rotate_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    });
+    launch_pdl(k_rotate_wy, dim3(n), dim3(256), smem, st, d_clu, d_items, (const int32_t*)d_rank);
+    count_launch(1);
+    return;
+  }
   const size_t words = std::min<size_t>((size_t)max_m * max_m + max_m, 24 * 1024);
   const size_t smem = sizeof(double) * words;
   if (max_m <= 256) {

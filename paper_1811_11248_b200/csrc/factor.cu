@@ -864,18 +864,10 @@ namespace hs {
 // Pattern-only device data, computed once per analysis and cached in it: the CSR pattern,
 // the permutation, the map of every CSR entry into the level-0 block store and the
 // transpose map used by the on-device symmetry check.
-static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, const DistPlan& dp) {
+static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, const DistPlan& dp, DevCache* dc) {
   if (an->dev == device && an->d_rowptr && an->map_world == dp.world && an->map_rank == dp.rank) {
     if (an->d_map) return;
-    if (!an->h_map.empty()) {   // dropped by the previous (record-space) factor: upload again
-      const int64_t nnz = an->rowptr[an->n];
-      HS_CUDA(cudaMalloc(&an->d_map, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
-      HS_CUDA(cudaMalloc(&an->d_tmap, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
-      HS_CUDA(cudaMemcpyAsync(an->d_map, an->h_map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-      HS_CUDA(cudaMemcpyAsync(an->d_tmap, an->h_tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
-      HS_CUDA(cudaStreamSynchronize(st));
-      return;
-    }
+    if (!an->h_map.empty()) return;   // large pattern: each factor stages the maps itself (factor_create)
   }
   if (an->dev >= 0 && an->dev != device) fail(HS_E_INVALID_ARG, "factor: analysis already bound to another device");
   if (an->d_rowptr) {   // cached for another (world, rank): rebuild
@@ -883,6 +875,13 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, con
     for (void* p : {(void*)an->d_rowptr, (void*)an->d_colind, (void*)an->d_perm, (void*)an->d_map, (void*)an->d_tmap})
       if (p) cudaFree(p);
     an->d_rowptr = nullptr; an->d_colind = nullptr; an->d_perm = nullptr; an->d_map = nullptr; an->d_tmap = nullptr;
+    if (an->maps_pinned) {
+      cudaHostUnregister(an->h_map.data());
+      cudaHostUnregister(an->h_tmap.data());
+      an->maps_pinned = false;
+    }
+    an->h_map.clear();
+    an->h_tmap.clear();
   }
   const bool dist = dp.world > 1;
   const int64_t n = an->n, nnz = an->rowptr[n];
@@ -928,6 +927,10 @@ static void ensure_device_pattern(Analysis* an, int device, cudaStream_t st, con
   if (!dist && nnz * 16 >= ((int64_t)2 << 30)) {
     an->h_map = std::move(map);
     an->h_tmap = std::move(tmap);
+    // pinned: a factor that stages them copies at full PCIe speed (unregistered by hs_analysis_destroy)
+    an->maps_pinned = cudaHostRegister(an->h_map.data(), sizeof(int64_t) * nnz, cudaHostRegisterDefault) == cudaSuccess &&
+                      cudaHostRegister(an->h_tmap.data(), sizeof(int64_t) * nnz, cudaHostRegisterDefault) == cudaSuccess;
+    cudaGetLastError();
   }
   an->dev = device;
   an->map_world = dp.world;
@@ -942,7 +945,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   const int64_t n = an->n, nnz = an->rowptr[n];
   cudaStream_t st = h->stream;
   const DistPlan DP = make_plan(*an, h->world, h->rank);
-  ensure_device_pattern(an, h->device, st, DP);
+  ensure_device_pattern(an, h->device, st, DP, &h->cache);
   auto* f = new hs_factor_s();
   std::unique_ptr<hs_factor_s> guard(f);
   f->h = h;
@@ -979,7 +982,22 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   std::unique_ptr<void, std::function<void(void*)>> status_guard(d_status, [&dc](void* p) { dc.free(p); });
   HS_CUDA(cudaMemsetAsync(d_status, 0, sizeof(DevStatus), st));
   // numerical symmetry of the values (A SPD, A_ns = A_sn^T), checked on the device
-  launch_symcheck(f->d_vals, an->d_tmap, nnz, &d_status->pivot, st);
+  // the level-0 scatter map and the transpose map: the analysis's device copies, or (large
+  // patterns whose maps a record-space factor dropped) staged from the host copies into the
+  // handle's cache for this factor's symmetry check and scatter only
+  const int64_t* d_map = an->d_map;
+  const int64_t* d_tmap = an->d_tmap;
+  int64_t *stage_map = nullptr, *stage_tmap = nullptr;
+  if (!d_map) {
+    if (an->h_map.empty()) fail(HS_E_INTERNAL, "factor: level-0 scatter map missing");
+    stage_map = (int64_t*)dc.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    stage_tmap = (int64_t*)dc.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    HS_CUDA(cudaMemcpyAsync(stage_map, an->h_map.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(stage_tmap, an->h_tmap.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+    d_map = stage_map;
+    d_tmap = stage_tmap;
+  }
+  launch_symcheck(f->d_vals, d_tmap, nnz, &d_status->pivot, st);
   HS_CUDA(cudaMemcpyAsync(&h_status, d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   HS_CUDA(cudaStreamSynchronize(st));
   if (h_status.pivot) fail(HS_E_NOT_SYMMETRIC, "factor: values are not symmetric");
@@ -993,7 +1011,11 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   BlockStore bs;
   bs.build(cap, an->L_top > 0 ? an->levels[0].Ffinal : an->H_top, st, &dc, &h->vmm,
            h->world > 1 && an->L_top > 0 ? &DP : nullptr, 0);   // mapped and zeroed
-  launch_scatter(f->d_vals, an->d_map, nnz, bs.d, st);
+  launch_scatter(f->d_vals, d_map, nnz, bs.d, st);
+  if (stage_map) {   // stream-ordered reuse by the factor's later allocations
+    dc.free(stage_map);
+    dc.free(stage_tmap);
+  }
   if (an->L_top > 0) bs.upload_dir(h->dirstage);
 
   Upload& upA = h->upA;   // persistent per handle: pinned staging is allocated once

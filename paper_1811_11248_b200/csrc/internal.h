@@ -68,6 +68,7 @@ struct Analysis {
   // (record space active) can drop d_map / d_tmap after its level-0 scatter and the next
   // factor uploads them again instead of recomputing them
   std::vector<int64_t> h_map, h_tmap;
+  bool maps_pinned = false;     // h_map / h_tmap registered with cudaHostRegister
   L0Support l0s;                // built by the first factor that restricts level 0 to the supports
   int32_t subdomain(int32_t level, int32_t c) const { return c >> ((D - level) - nsub_log2); }
 };

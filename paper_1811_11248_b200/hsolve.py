@@ -10,6 +10,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import weakref
+
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -211,11 +213,18 @@ def _host_vec(a, n, name, out=False):
 class Handle:
     def __init__(self, ptr):
         self.ptr = ptr
+        self._factors = weakref.WeakSet()   # a factor must go before its handle (its memory is the handle's)
+
+    def close(self):
+        """Destroy the handle now (its factors first): its cached device memory goes back to the driver."""
+        if self.ptr and _lib is not None and not _exiting:
+            for f in list(self._factors):   # garbage-collected cycles finalize in any order
+                f._destroy()
+            _lib.hs_destroy(self.ptr)
+        self.ptr = None
 
     def __del__(self):
-        if self.ptr and _lib is not None and not _exiting:
-            _lib.hs_destroy(self.ptr)
-            self.ptr = None
+        self.close()
 
 
 class Analysis:
@@ -235,11 +244,15 @@ class Factor:
         self.handle = handle       # keep alive
         self.analysis = analysis
         self.n = n
+        handle._factors.add(self)
+
+    def _destroy(self):
+        if self.ptr and _lib is not None and not _exiting and self.handle.ptr:
+            _lib.hs_factor_destroy(self.ptr)
+        self.ptr = None
 
     def __del__(self):
-        if self.ptr and _lib is not None and not _exiting:
-            _lib.hs_factor_destroy(self.ptr)
-            self.ptr = None
+        self._destroy()
 
 
 def hs_nccl_unique_id() -> bytes:

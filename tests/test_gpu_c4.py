@@ -36,9 +36,18 @@ def H():
 
 
 def test_c4_full_size(H):
+    import gc
     p = gen_config("C4")
     assert p.n == 10_485_760
     h = H.hs_create(0)
+    try:
+        _c4_checks(H, h, p)
+    finally:   # the handle's ~170 GB of cached device memory must not outlive the test
+        h.close()
+        gc.collect()
+
+
+def _c4_checks(H, h, p):
     a = H.hs_analyze(h, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
                      leaf_columns=p.leaf_columns)
     an = analyze(p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size,
@@ -57,7 +66,7 @@ def test_c4_full_size(H):
         f = H.hs_factor_create(h, a, p.vals, eps=p.eps)
         runs.append(([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)], H.hs_apply(f, v)))
         if len(runs) == 1:
-            del f
+            del f   # two C4 factors cannot coexist on one GPU
     assert all(np.array_equal(x, y) for x, y in zip(runs[0][0], runs[1][0]))
     assert np.array_equal(runs[0][1], runs[1][1])
 
