@@ -5,23 +5,32 @@ runs with the record space active (completed levels' T_s / C_s spilled to pinned
 while the 131 GB level-2 store is resident) and with oversized batches split into sub-batches
 by the workspace budget -- the two paths only C4 takes.
 
-The whole oracle factor of C4 is out of reach (hours of Python), and no cluster's input can be
-reproduced on the host without replaying the elimination before it (the first batch of level 0,
-whose blocks are A's own, has w(s) empty: no compression decision at all).  So this leg checks
-what holds at any size (SURVEY §8(c) parity protocol, full-size leg):
+The whole oracle factor of C4 is out of reach (hours of Python), so this leg checks what the
+oracle can compute one by one at this size, and what holds at any size (SURVEY §8(c) parity
+protocol, full-size leg):
   * the analysis (partition, cluster tree, every level's batches) bit-exact with oracle/analyze;
+  * the kept rank and pivot sequence of a seeded sample of 200 clusters of level 0's SECOND
+    batch (the first with compression decisions: batch 0 has w(s) = ∅), each eliminated by the
+    oracle (oracle.factor.eliminate) after exactly the batch-0 clusters that touch its blocks
+    (its batch-0 neighbours, in batch order; a batch is an independent set and a phase-I batch
+    stays inside its subdomain, so no other elimination reaches them), on level-0 blocks built
+    from the permuted CSR on first access; a disagreement is allowed only where the oracle's
+    margins flag the cluster;
   * operator properties of the factor apply (symmetry, positivity, linearity);
   * PCG to the config's tolerance with the true residual recomputed against A on the host;
   * bitwise determinism across two factors (every level's kept ranks, the apply), i.e. the
     sub-batch split and the spill / restore of the records change nothing between runs.
-The C4 operator itself is compared with the oracle on every cluster at 1/16 scale
-(test_gpu_fullsize.py), and the spill / restore path bitwise against resident records there.
+The C4 operator is compared with the oracle on every cluster at 1/16 scale (test_gpu_fullsize.py),
+and the spill / restore path bitwise against resident records there.
 """
 import numpy as np
 import pytest
 
+import scipy.sparse as sp
+
 from problems import gen_config
 from oracle.analyze import analyze
+from oracle.factor import BlockStore, eliminate
 
 pytestmark = pytest.mark.gpu
 
@@ -33,6 +42,59 @@ def H():
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
     hsolve.lib()
     return hsolve
+
+
+class _LazyLevel0(BlockStore):
+    """The oracle's block store on level 0 of the permuted A, each block built from the CSR on
+    first access (an untouched block of an eliminated cluster is structurally zero)."""
+
+    def __init__(self, p, an):
+        super().__init__(np.diff(an.leaf_off).tolist())
+        self.size0 = list(self.live)
+        self.A = sp.csr_matrix((p.vals, p.colind, p.rowptr), shape=(p.n, p.n))
+        self.off, self.perm = an.leaf_off, an.perm
+        self.iperm = np.empty_like(an.perm)
+        self.iperm[an.perm] = np.arange(an.perm.size)
+        self.rows = {}
+
+    def _row(self, q):
+        if q not in self.rows:
+            R = self.A[self.perm[self.off[q]:self.off[q + 1]]].tocoo()
+            cn = self.iperm[R.col]
+            self.rows[q] = (R.row, cn, R.data, np.searchsorted(self.off, cn, side="right") - 1)
+        return self.rows[q]
+
+    def get(self, p, q):
+        key = (p, q) if p >= q else (q, p)
+        if key not in self.blocks and all(self.live[c] == self.size0[c] for c in key):
+            rr, cn, dv, lf = self._row(key[0])
+            sel = lf == key[1]
+            M = np.zeros((self.size0[key[0]], self.size0[key[1]]))
+            np.add.at(M, (rr[sel], cn[sel] - self.off[key[1]]), dv[sel])
+            self.blocks[key] = M
+        return super().get(p, q)
+
+
+def _level0_batch1_sample(p, an, ranks, pp, pv, nsample=200):
+    lev = an.levels[0]
+    assert lev.nphase1 >= 2
+    b0 = set(lev.batches[0])
+    S1 = sorted(np.random.default_rng(0).choice(lev.batches[1], nsample, replace=False).tolist())
+    T = sorted({t for s in S1 for t in list(lev.nlist[s]) + list(lev.wlist[s]) if t in b0})
+    st = _LazyLevel0(p, an)
+    for t in T:   # batch 0 in batch order (ascending)
+        eliminate(st, 0, t, lev.nlist[t], lev.wlist[t], p.eps, True)
+    flagged_diff = ncpqr = 0
+    for s in S1:
+        e = eliminate(st, 0, s, lev.nlist[s], lev.wlist[s], p.eps, True)
+        ncpqr += len(lev.wlist[s]) > 0
+        g = pv[pp[s]:pp[s + 1]]
+        if not (ranks[s] == e.r and np.array_equal(g, e.piv)):
+            assert e.flagged, f"level-0 cluster {s}: gpu r={ranks[s]} oracle r={e.r} (unflagged)"
+            flagged_diff += 1
+    print(f"[C4] level-0 batch-1 sample: {len(S1)} clusters ({ncpqr} with compression) after {len(T)} "
+          f"batch-0 eliminations, {flagged_diff} flagged differences")
+    assert ncpqr > 0 and flagged_diff <= 2
 
 
 def test_c4_full_size(H):
@@ -67,6 +129,8 @@ def _c4_checks(H, h, p):
         runs.append(([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)], H.hs_apply(f, v)))
         if len(runs) == 1:
             del f   # two C4 factors cannot coexist on one GPU
+    _level0_batch1_sample(p, an, runs[1][0][0], H.hs_factor_export(f, H.HS_FEXP_PIV_PTR, 0),
+                          H.hs_factor_export(f, H.HS_FEXP_PIV, 0))
     assert all(np.array_equal(x, y) for x, y in zip(runs[0][0], runs[1][0]))
     assert np.array_equal(runs[0][1], runs[1][1])
 
