@@ -6,8 +6,10 @@ import numpy as np
 import torch
 from paper_1811_11248_b200 import hsolve as H
 from problems import gen_config
+from problems.generators import gen_config_scaled
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-p = gen_config(name)
+base, _, k = name.partition("/")
+p = gen_config_scaled(base, int(k)) if k else gen_config(base)
 h = H.hs_create(0)
 a = H.hs_analyze(h, p.n, p.rowptr, p.colind, p.coords, p.column_id, leaf_size=p.leaf_size, leaf_columns=p.leaf_columns)
 for rep in range(2):
