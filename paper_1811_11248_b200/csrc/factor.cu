@@ -202,9 +202,52 @@ void RecSpace::init(VmmPool* p, size_t reserve_bytes, cudaStream_t stream) {
   base = vmm_reserve(vbytes);
   handle.assign(vbytes / cb, 0ull);
   host.assign(vbytes / cb, nullptr);
+  pre.assign(vbytes / cb, nullptr);
+  pre_ev.assign(vbytes / cb, nullptr);
   top = frontier = pin_lo = pin_hi = 0;
   n_spilled = bytes_spilled = bytes_restored = 0;
   t_spill = t_restore = 0.0;
+  pre_bytes = pre_used = 0;
+  pre_budget = 0;
+  const char* e = std::getenv("HS_REC_PRECOPY");   // 0: off; else the previous factor's spill + 1 GB
+  if (!(e && std::atoi(e) == 0) && pool->last_spilled > 0) pre_budget = pool->last_spilled + ((size_t)1 << 30);
+}
+void RecSpace::precopy(cudaStream_t side) {
+  if (!active() || pre_budget == 0) return;
+  const size_t cb = pool->chunk;
+  bool started = false;
+  for (size_t i = 0; i < handle.size() && (i + 1) * cb <= frontier && pre_bytes < pre_budget; ++i) {
+    if (!handle[i] || host[i] || pre[i] || ((i + 1) * cb > pin_lo && i * cb < pin_hi)) continue;
+    if (!started) {   // the copies start after every writer queued so far (main and side stream)
+      if (!cst) HS_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+      cudaEvent_t ev;
+      HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      HS_CUDA(cudaEventRecord(ev, st));
+      HS_CUDA(cudaStreamWaitEvent(cst, ev, 0));
+      if (side) {
+        HS_CUDA(cudaEventRecord(ev, side));
+        HS_CUDA(cudaStreamWaitEvent(cst, ev, 0));
+      }
+      HS_CUDA(cudaEventDestroy(ev));
+      started = true;
+    }
+    pre[i] = pool->take_host();
+    HS_CUDA(cudaMemcpyAsync(pre[i], (const void*)(uintptr_t)(base + i * cb), cb, cudaMemcpyDeviceToHost, cst));
+    HS_CUDA(cudaEventCreateWithFlags(&pre_ev[i], cudaEventDisableTiming));
+    HS_CUDA(cudaEventRecord(pre_ev[i], cst));
+    pre_bytes += cb;
+  }
+}
+static void drop_precopy(RecSpace& R, size_t i) {   // the chunk's pre-copy is not needed (any more)
+  if (R.pre_ev[i]) {
+    cudaEventSynchronize(R.pre_ev[i]);
+    cudaEventDestroy(R.pre_ev[i]);
+    R.pre_ev[i] = nullptr;
+  }
+  if (R.pre[i]) {
+    R.pool->give_host(R.pre[i]);
+    R.pre[i] = nullptr;
+  }
 }
 void* RecSpace::alloc(size_t bytes) {
   const size_t cb = pool->chunk;
@@ -235,12 +278,23 @@ size_t RecSpace::spill(size_t bytes) {
     }
   if (pick.empty()) return 0;
   const auto t0 = std::chrono::steady_clock::now();
-  HS_CUDA(cudaDeviceSynchronize());   // every writer of a completed record has finished
+  bool copy = false;
+  for (size_t i : pick) copy |= pre[i] == nullptr;
+  if (copy) HS_CUDA(cudaDeviceSynchronize());   // every writer of a completed record has finished
   for (size_t i : pick) {
+    if (pre[i]) {   // pre-copied on the copy stream: wait for that copy only
+      HS_CUDA(cudaEventSynchronize(pre_ev[i]));
+      HS_CUDA(cudaEventDestroy(pre_ev[i]));
+      pre_ev[i] = nullptr;
+      host[i] = pre[i];
+      pre[i] = nullptr;
+      pre_used += cb;
+      continue;
+    }
     host[i] = pool->take_host();
     HS_CUDA(cudaMemcpyAsync(host[i], (const void*)(uintptr_t)(base + i * cb), cb, cudaMemcpyDeviceToHost, st));
   }
-  HS_CUDA(cudaStreamSynchronize(st));
+  if (copy) HS_CUDA(cudaStreamSynchronize(st));
   for (size_t i : pick) {
     vmm_unmap(base + i * cb, cb);
     pool->give(handle[i]);
@@ -254,6 +308,8 @@ size_t RecSpace::spill(size_t bytes) {
 void RecSpace::restore() {
   if (!active()) return;
   const size_t cb = pool->chunk;
+  for (size_t i = 0; i < pre.size(); ++i) drop_precopy(*this, i);   // pre-copies never spilled
+  pool->last_spilled = bytes_spilled;
   const auto t0 = std::chrono::steady_clock::now();
   bool any = false;
   for (size_t i = 0; i < host.size(); ++i)
@@ -279,6 +335,11 @@ void RecSpace::release() {
   cudaDeviceSynchronize();   // the apply / a failed factor's kernels may still read the records
   const size_t cb = pool->chunk;
   try {
+    for (size_t i = 0; i < pre.size(); ++i) drop_precopy(*this, i);
+    if (cst) {
+      cudaStreamDestroy(cst);
+      cst = nullptr;
+    }
     for (size_t i = 0; i < handle.size(); ++i) {
       if (handle[i]) {
         vmm_unmap(base + i * cb, cb);
@@ -310,6 +371,16 @@ void vmm_map(unsigned long long va, unsigned long long handle, size_t bytes, int
   acc.location.id = device;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   cu_check(drv().set_access((CUdeviceptr)va, bytes, &acc, 1), "cuMemSetAccess");
+}
+// one cuMemMap per chunk, then one cuMemSetAccess over each contiguous run of new mappings
+static void vmm_map_run(unsigned long long va0, const unsigned long long* handles, size_t n, size_t cb, int device) {
+  for (size_t i = 0; i < n; ++i)
+    cu_check(drv().map((CUdeviceptr)(va0 + i * cb), cb, 0, (CUmemGenericAllocationHandle)handles[i], 0), "cuMemMap");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  cu_check(drv().set_access((CUdeviceptr)va0, n * cb, &acc, 1), "cuMemSetAccess");
 }
 void vmm_unmap(unsigned long long va, size_t bytes) { cu_check(drv().unmap((CUdeviceptr)va, bytes), "cuMemUnmap"); }
 
@@ -401,11 +472,16 @@ struct BlockStore {
     }
     const size_t cb = pool->chunk;
     size_t i0 = b0 / cb, i1 = (std::min(b1, vbytes) + cb - 1) / cb;
-    for (size_t i = i0; i < i1; ++i) {
-      if (handle[i]) continue;
-      handle[i] = pool->take();
-      vmm_map((unsigned long long)(uintptr_t)d + i * cb, handle[i], cb, pool->device);
-      HS_CUDA(cudaMemsetAsync((char*)d + i * cb, 0, cb, st));
+    for (size_t i = i0; i < i1;) {
+      if (handle[i]) {
+        ++i;
+        continue;
+      }
+      size_t j = i;
+      for (; j < i1 && !handle[j]; ++j) handle[j] = pool->take();
+      vmm_map_run((unsigned long long)(uintptr_t)d + i * cb, &handle[i], j - i, cb, pool->device);
+      HS_CUDA(cudaMemsetAsync((char*)d + i * cb, 0, (j - i) * cb, st));
+      i = j;
     }
   }
   // unmap every chunk lying entirely below byte b (its users must have completed)
@@ -961,6 +1037,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
   double t_fh[6] = {0, 0, 0, 0, 0, 0};   // first-half planning: shapes + column maps, items, upload staging
   double t_trans = 0.0;   // host planning breakdown (HS_PROFILE): schur, write-back, apply, tail
   double t_tr[4] = {0, 0, 0, 0};   // level transition: block store build, upload_dir, arena alloc, release
+  double t_as[5] = {0, 0, 0, 0, 0};   // assembly loop: map, items, upload + launch, sync, unmap
   cudaEvent_t ev0, ev1;
   HS_CUDA(cudaEventCreate(&ev0));
   HS_CUDA(cudaEventCreate(&ev1));
@@ -2255,6 +2332,7 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     if (f->rec.active()) {   // the level's records are complete (spillable)
       f->rec.pin_lo = f->rec.pin_hi = 0;
       f->rec.level_start();
+      f->rec.precopy(h->side);
       if (rec_force) f->rec.spill(~size_t(0));
     }
     // ---- every rank learns every kept rank; the records go to rank 0 (dist) -----------------
@@ -2496,7 +2574,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     for (int32_t Pa = 0; Pa < nP;) {
       int32_t Pb = Pa + 1;
       while (Pb < nP && nbs.rowbeg[Pb + 1] - nbs.rowbeg[Pa] <= group_words) ++Pb;
+      double ta = now_s();
       nbs.map_bytes((size_t)nbs.rowbeg[Pa] * sizeof(double), (size_t)nbs.rowbeg[Pb] * sizeof(double));
+      t_as[0] += now_s() - ta;
+      ta = now_s();
       std::vector<CopyItem> asmb;
       for (int32_t c = 2 * Pa; c < std::min(2 * Pb, lev.nclus); ++c) {
         if (L.rank[c] == 0) continue;
@@ -2519,6 +2600,8 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
         }
       }
       split_copies(asmb);
+      t_as[1] += now_s() - ta;
+      ta = now_s();
       upA.reset();
       const size_t iA = upA.add(asmb);
       upA.stage.ensure(upA.total);
@@ -2526,9 +2609,14 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
       upA.copy_in(iA, asmb);
       upA.send(st);
       launch_copy2d(upA.dptr<CopyItem>(iA), (int)asmb.size(), st);
+      t_as[2] += now_s() - ta;
       if (bs.pool || Pb < nP) {   // VMM-backed: the consumed child rows can go (a group's staging is reused)
+        ta = now_s();
         HS_CUDA(cudaStreamSynchronize(st));
+        t_as[3] += now_s() - ta;
+        ta = now_s();
         bs.unmap_below((size_t)bs.rowbeg[std::min(2 * Pb, lev.nclus)] * sizeof(double));
+        t_as[4] += now_s() - ta;
       }
       Pa = Pb;
     }
@@ -2660,9 +2748,10 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
     f->rec.restore();
     h->vmm.rec = nullptr;
     if (prof || f->rec.n_spilled)
-      std::fprintf(stderr, "[hs profile] record space: %.2f GB of records, %.2f GB spilled to the host in %.2f s, "
-                   "%.2f GB restored in %.2f s\n", f->rec.top / 1e9, f->rec.bytes_spilled / 1e9, f->rec.t_spill,
-                   f->rec.bytes_restored / 1e9, f->rec.t_restore);
+      std::fprintf(stderr, "[hs profile] record space: %.2f GB of records, %.2f GB spilled to the host in %.2f s "
+                   "(%.2f GB of them pre-copied during earlier levels; %.2f GB pre-copied), %.2f GB restored in %.2f s\n",
+                   f->rec.top / 1e9, f->rec.bytes_spilled / 1e9, f->rec.t_spill, f->rec.pre_used / 1e9,
+                   f->rec.pre_bytes / 1e9, f->rec.bytes_restored / 1e9, f->rec.t_restore);
   }
   HS_CUDA(cudaEventRecord(h->ev_join, h->side));   // join the side stream (apply operators)
   HS_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
@@ -2696,7 +2785,9 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                  dc.peak / 1e9, dc.cached / 1e9);
   if (std::getenv("HS_PROFILE"))
     std::fprintf(stderr, "[hs profile] level transitions: block store build %.1f ms, release+upload_dir (sync) %.1f ms "
-                 "(release %.1f), arena alloc %.1f ms\n", 1e3 * t_tr[0], 1e3 * t_tr[1], 1e3 * t_tr[3], 1e3 * t_tr[2]);
+                 "(release %.1f), arena alloc %.1f ms; assembly: map %.1f, items %.1f, upload+launch %.1f, "
+                 "sync %.1f, unmap %.1f ms\n", 1e3 * t_tr[0], 1e3 * t_tr[1], 1e3 * t_tr[3], 1e3 * t_tr[2],
+                 1e3 * t_as[0], 1e3 * t_as[1], 1e3 * t_as[2], 1e3 * t_as[3], 1e3 * t_as[4]);
   S.n_levels = an->L_top;
   // factor bytes read by the apply: T_s (m^2) and C_s ((m - r) kn) per cluster + top (N^2/2)
   double fb = 0.0;

@@ -33,6 +33,7 @@ struct VmmPool {
   struct DevCache* dc = nullptr;         // trimmed before retrying an allocation that failed
   struct RecSpace* rec = nullptr;        // the running factor's records: spilled to the host on OOM
   std::vector<char*> host_idle;          // pinned host chunks (spilled records), kept for the next factor
+  size_t last_spilled = 0;               // bytes the previous factor on this handle spilled (pre-copy budget)
   void init(int dev);
   unsigned long long take();
   void give(unsigned long long h) { idle.push_back(h); }
@@ -58,6 +59,13 @@ struct RecSpace {
   size_t pin_lo = 0, pin_hi = 0;          // except this range (the running level's T_s arena)
   std::vector<unsigned long long> handle; // physical chunk mapped at chunk i (0: none)
   std::vector<char*> host;                // pinned copy of a spilled chunk
+  // pre-copies: completed chunks copied to pinned host memory on a copy stream while later
+  // levels compute, so a spill of a pre-copied chunk is an event wait and an unmap (no device
+  // synchronisation, no copy on the critical path); budget = what the previous factor spilled
+  std::vector<char*> pre;                 // pinned copy in flight / done (valid once pre_ev[i] completed)
+  std::vector<cudaEvent_t> pre_ev;
+  cudaStream_t cst = nullptr;             // copy stream of the pre-copies
+  size_t pre_bytes = 0, pre_used = 0, pre_budget = 0;
   cudaStream_t st = nullptr;
   size_t n_spilled = 0, bytes_spilled = 0, bytes_restored = 0;
   double t_spill = 0.0, t_restore = 0.0;
@@ -66,6 +74,7 @@ struct RecSpace {
   void level_start();                     // a level begins: everything allocated so far is complete
   size_t spill(size_t bytes);             // >= bytes of completed records to the host (syncs the device)
   void restore();                         // map and copy back every spilled chunk (stream-ordered)
+  void precopy(cudaStream_t side);        // level end: pre-copy completed chunks up to the budget
   void release();
   bool active() const { return base != 0; }
   ~RecSpace() { release(); }

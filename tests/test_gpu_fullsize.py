@@ -167,14 +167,17 @@ def test_record_space_spill_restore_bitwise(H, handle, monkeypatch, name):
     L = H.hs_analysis_get_info(a)["L_top"]
     v = np.random.default_rng(7).standard_normal(p.n)
     out = {}
-    for mode in ("0", "1", "force"):
-        monkeypatch.setenv("HS_RECSPACE", mode)
+    # "force" twice on the same handle: the second factor pre-copies its completed chunks on the
+    # copy stream during later levels (budget = the first one's spill), so its spills are event
+    # waits on those copies
+    for mode in ("0", "1", "force", "force-precopied"):
+        monkeypatch.setenv("HS_RECSPACE", mode.partition("-")[0])
         f = H.hs_factor_create(handle, a, p.vals, eps=p.eps)
         x, rep = H.hs_pcg(f, v, tol=p.tol)
         out[mode] = ([H.hs_factor_export(f, H.HS_FEXP_RANKS, l) for l in range(L)], H.hs_apply(f, v), x,
                      rep["iters"])
         del f
-    for mode in ("1", "force"):
+    for mode in ("1", "force", "force-precopied"):
         assert all(np.array_equal(x, y) for x, y in zip(out["0"][0], out[mode][0])), mode
         assert np.array_equal(out["0"][1], out[mode][1]), mode
         assert np.array_equal(out["0"][2], out[mode][2]), mode
