@@ -449,12 +449,14 @@ def run_ours(args, rank, world, local):
                 "frac": None, "traffic": None}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (tools/profile_round.sh -> profiles/*_traffic.json; one representative launch)
+    # (one per workload: the file's "workload" key, C3 when absent)
     tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
-    if tp and args.config == "C3":   # the committed capture is of the default workload
-        tr = json.load(open(os.path.join(ROOT, "profiles", tp[-1])))
-        if tr.get("class") == roof["kernel"]:
+    for f in reversed(tp):
+        tr = json.load(open(os.path.join(ROOT, "profiles", f)))
+        if tr.get("workload", "C3") == args.config and tr.get("class") == roof["kernel"]:
             roof["traffic"] = tr["dram_bytes_per_launch"]
-            roof["traffic_source"] = f"profiles/{tp[-1]}: {tr['note']}"
+            roof["traffic_source"] = f"profiles/{f}: {tr['note']}"
+            break
     S = stats[-1]
     factor_flops = float(np.mean([s["flops"] for s in stats]))
     t_fac = float(np.mean([s["t_factor_s"] for s in stats]))

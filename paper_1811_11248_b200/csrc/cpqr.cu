@@ -218,7 +218,7 @@ __device__ __forceinline__ void form_reflector(const double* col, int j, int m, 
 //   (3) apply H_j to the local active columns and recompute their norms; the owner writes
 //       the pivot column as (beta, 0, ..., 0) and the reflector to V / tau / piv.
 // One mbarrier wait per step, no cluster-wide barrier inside the loop.
-template <int MR, int G, bool SM, int NT>
+template <int MR, int G, bool SM, int NT, int U>
 __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int relative, int32_t* rank_slot,
                                           double* dsm, CqShared& sh, long long* trace, bool light) {
   // HS_CQ_TRACE debug aid: clock64 timeline of cluster 0 / CTA 0 / thread 0
@@ -520,13 +520,15 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
     for (int i = 0; i < MR; ++i) vr[i] = (i < nr) ? vmsg[8 + t + i * G] : 0.0;
     const int gi = (j >= t) ? (j - t) / G + 1 : 0;   // rows l > j of this lane: i >= gi
     lm = -1.0;
-    for (int k = 0; k < kiters; k += 2) {
-      double* cp[2];
-      int cxs[2];
-      bool act[2], piv[2];
-      double x[2][MR], d[2], ss[2];
+    // U columns in flight per group: two up to 8 rows a lane; one at MR = 16 (two need 64
+    // registers of column values and spill ~1 KB a thread under the 128-register bound)
+    for (int k = 0; k < kiters; k += U) {
+      double* cp[U];
+      int cxs[U];
+      bool act[U], piv[U];
+      double x[U][MR], d[U], ss[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int c = grp + (k + u) * NGRP;
         const bool in = (k + u) < kiters && c < nw;
         const int cx = in ? c : 0;
@@ -542,9 +544,9 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) d[u] = group_sum<G>(d[u]);
+      for (int u = 0; u < U; ++u) d[u] = group_sum<G>(d[u]);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const double td = tau * d[u];
         ss[u] = 0.0;
         if (act[u]) {
@@ -562,9 +564,9 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) ss[u] = group_sum<G>(ss[u]);
+      for (int u = 0; u < U; ++u) ss[u] = group_sum<G>(ss[u]);
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < U; ++u)
         if (act[u]) {
           const double v = sqrt(ss[u]);
           if (t == 0) nu[cxs[u]] = v;
@@ -605,7 +607,7 @@ __device__ __forceinline__ void cpqr_body(const CluItem& it, double eps, int rel
 
 // NT threads per CTA, 512 / NT CTAs per SM (<= 128 registers a thread either way): smaller CTAs
 // let several clusters' latency-bound step chains share an SM when their slices fit
-template <int MR, bool SM, int NT>
+template <int MR, bool SM, int NT, int U>
 __global__ void __launch_bounds__(NT, 512 / NT) k_cpqr3(const CluItem* __restrict__ items, double eps, int relative,
                                                           int32_t* __restrict__ rank_out, long long* trace,
                                                           int light) {
@@ -623,12 +625,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_cpqr3(const CluItem* __restric
   extern __shared__ double dsm[];
   __shared__ CqShared sh;
   switch (cq_group(it.m, MR)) {
-    case 1: cpqr_body<MR, 1, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
-    case 2: cpqr_body<MR, 2, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
-    case 4: cpqr_body<MR, 4, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
-    case 8: cpqr_body<MR, 8, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
-    case 16: cpqr_body<MR, 16, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
-    default: cpqr_body<MR, 32, SM, NT>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 1: cpqr_body<MR, 1, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 2: cpqr_body<MR, 2, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 4: cpqr_body<MR, 4, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 8: cpqr_body<MR, 8, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    case 16: cpqr_body<MR, 16, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
+    default: cpqr_body<MR, 32, SM, NT, U>(it, eps, relative, rank_out + item, dsm, sh, trace, light != 0); break;
   }
 }
 
@@ -872,10 +874,10 @@ __global__ void __launch_bounds__(256) k_rotate_wy(const CluItem* __restrict__ c
   }
 }
 
-template <int MR, bool SM, int NT>
+template <int MR, bool SM, int NT, int U = (MR >= 16 ? 1 : 2)>
 void launch_one(const CluItem* d_items, int n, int CS, size_t smem, double eps, int relative, int32_t* d_rank,
                 cudaStream_t st, long long* trace, bool light) {
-  auto kern = k_cpqr3<MR, SM, NT>;
+  auto kern = k_cpqr3<MR, SM, NT, U>;
   static std::once_flag once;
   std::call_once(once, [&] {
     HS_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1077,6 +1079,11 @@ int launch_cpqr3(const CluItem* d_items, const std::vector<CluItem>& h_items, do
       else if (NT == 128) launch_one<8, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
       else if (NT == 256) launch_one<8, true, 256>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
       else launch_one<8, true, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+    } else if (std::getenv("HS_CQ_U2")) {   // A/B: two columns in flight at MR = 16 (spills)
+      if (!sm) launch_one<16, false, 512, 2>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 128) launch_one<16, true, 128, 2>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else if (NT == 256) launch_one<16, true, 256, 2>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
+      else launch_one<16, true, 512, 2>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
     } else {
       if (!sm) launch_one<16, false, 512>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);
       else if (NT == 128) launch_one<16, true, 128>(d_items, n, CS, smem, eps, relative, d_rank, st, trace, light);

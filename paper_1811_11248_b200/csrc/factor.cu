@@ -137,16 +137,31 @@ CUmemAllocationProp chunk_prop(int device) {
 }
 }  // namespace
 
+// HS_PROFILE: host time in the VMM calls (take = reuse / cuMemCreate incl. spills, map, access, unmap)
+double g_vmm_t[4] = {0, 0, 0, 0};
+long long g_vmm_n[4] = {0, 0, 0, 0};
+static inline double vmm_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 void VmmPool::init(int dev) {
   if (device == dev && chunk) return;
   device = dev;
   const CUmemAllocationProp prop = chunk_prop(dev);
   size_t g = 0;
   cu_check(drv().granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
-  const size_t want = (size_t)256 << 20;   // 256 MB chunks
+  const char* ce = std::getenv("HS_VMM_CHUNK_MB");   // 256 MB chunks (A/B: other sizes)
+  const size_t want = (size_t)(ce ? std::max(2, std::atoi(ce)) : 256) << 20;
   chunk = (want + g - 1) / g * g;
 }
 unsigned long long VmmPool::take() {
+  const double t0 = vmm_now();
+  struct Acc {
+    double t0;
+    ~Acc() {
+      g_vmm_t[0] += vmm_now() - t0;
+      ++g_vmm_n[0];
+    }
+  } acc{t0};
   if (!idle.empty()) {
     const unsigned long long h = idle.back();
     idle.pop_back();
@@ -374,15 +389,26 @@ void vmm_map(unsigned long long va, unsigned long long handle, size_t bytes, int
 }
 // one cuMemMap per chunk, then one cuMemSetAccess over each contiguous run of new mappings
 static void vmm_map_run(unsigned long long va0, const unsigned long long* handles, size_t n, size_t cb, int device) {
+  double t0 = vmm_now();
   for (size_t i = 0; i < n; ++i)
     cu_check(drv().map((CUdeviceptr)(va0 + i * cb), cb, 0, (CUmemGenericAllocationHandle)handles[i], 0), "cuMemMap");
+  g_vmm_t[1] += vmm_now() - t0;
+  g_vmm_n[1] += (long long)n;
+  t0 = vmm_now();
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = device;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   cu_check(drv().set_access((CUdeviceptr)va0, n * cb, &acc, 1), "cuMemSetAccess");
+  g_vmm_t[2] += vmm_now() - t0;
+  ++g_vmm_n[2];
 }
-void vmm_unmap(unsigned long long va, size_t bytes) { cu_check(drv().unmap((CUdeviceptr)va, bytes), "cuMemUnmap"); }
+void vmm_unmap(unsigned long long va, size_t bytes) {
+  const double t0 = vmm_now();
+  cu_check(drv().unmap((CUdeviceptr)va, bytes), "cuMemUnmap");
+  g_vmm_t[3] += vmm_now() - t0;
+  ++g_vmm_n[3];
+}
 
 void DevScratch::ensure(size_t bytes) {
   if (bytes <= cap) return;
@@ -2788,6 +2814,12 @@ hs_factor_s* factor_create(hs_handle_s* h, const Analysis* an_c, const double* v
                  "(release %.1f), arena alloc %.1f ms; assembly: map %.1f, items %.1f, upload+launch %.1f, "
                  "sync %.1f, unmap %.1f ms\n", 1e3 * t_tr[0], 1e3 * t_tr[1], 1e3 * t_tr[3], 1e3 * t_tr[2],
                  1e3 * t_as[0], 1e3 * t_as[1], 1e3 * t_as[2], 1e3 * t_as[3], 1e3 * t_as[4]);
+  if (std::getenv("HS_PROFILE")) {
+    std::fprintf(stderr, "[hs profile] VMM calls so far (chunk %.0f MB): take %.1f ms (%lld), map %.1f ms (%lld), "
+                 "access %.1f ms (%lld runs), unmap %.1f ms (%lld)\n", h->vmm.chunk / 1048576.0, 1e3 * g_vmm_t[0],
+                 g_vmm_n[0], 1e3 * g_vmm_t[1], g_vmm_n[1], 1e3 * g_vmm_t[2], g_vmm_n[2], 1e3 * g_vmm_t[3], g_vmm_n[3]);
+    for (int i = 0; i < 4; ++i) g_vmm_t[i] = 0, g_vmm_n[i] = 0;
+  }
   S.n_levels = an->L_top;
   // factor bytes read by the apply: T_s (m^2) and C_s ((m - r) kn) per cluster + top (N^2/2)
   double fb = 0.0;
