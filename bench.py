@@ -450,7 +450,7 @@ def run_ours(args, rank, world, local):
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (tools/profile_round.sh -> profiles/*_traffic.json; one representative launch)
     # (one per workload: the file's "workload" key, C3 when absent)
-    tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
+    tp = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if "_traffic" in f and f.endswith(".json"))
     for f in reversed(tp):
         tr = json.load(open(os.path.join(ROOT, "profiles", f)))
         if tr.get("workload", "C3") == args.config and tr.get("class") == roof["kernel"]:
