@@ -149,8 +149,8 @@ void VmmPool::init(int dev) {
   const CUmemAllocationProp prop = chunk_prop(dev);
   size_t g = 0;
   cu_check(drv().granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
-  const char* ce = std::getenv("HS_VMM_CHUNK_MB");   // 256 MB chunks (A/B: other sizes)
-  const size_t want = (size_t)(ce ? std::max(2, std::atoi(ce)) : 256) << 20;
+  const char* ce = std::getenv("HS_VMM_CHUNK_MB");   // 1 GB chunks (A/B vs 256 MB: profiles/r02fin_c4_chunk*.json)
+  const size_t want = (size_t)(ce ? std::max(2, std::atoi(ce)) : 1024) << 20;
   chunk = (want + g - 1) / g * g;
 }
 unsigned long long VmmPool::take() {
